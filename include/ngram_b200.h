@@ -1,0 +1,195 @@
+/*
+ * ngram_b200.h -- C-ABI of the B200-native N-gram Embedding hot path (libngram_b200.so).
+ *
+ * The reference (arXiv 2601.21204, /root/reference/proj) exposes only a C++ header API
+ * (proj/include/ngram/*.hpp) and no FFI.  These entry points are what that API's hot
+ * path binds to when it is backed by the GPU: include/ngram/*.hpp (the drop-in C++
+ * headers) and the Python mirror (paper_2601_21204_b200/ngram.py) both call exactly
+ * this surface.  Each entry cites the reference interface it replaces.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  "dev" pointers are CUDA device pointers on the
+ *     bank's device; "host" pointers are host memory (pinned or pageable).
+ *   - Every call returns an ngram_status.  On failure ngram_last_error() (thread-local)
+ *     holds the message.  Status codes map 1:1 onto the reference's exceptions
+ *     (include/ngram/errors.hpp): EINVAL -> std::invalid_argument, ERANGE ->
+ *     std::out_of_range, EIO -> io_error, EPARSE -> parse_error, ECONFIG ->
+ *     config_error, ENUMERIC -> numeric_error.
+ *   - Device calls are stream-ordered (stream = cudaStream_t or NULL for the legacy
+ *     stream) and never allocate on the hot path once ngram_bank_reserve() has sized
+ *     the workspace.  Token-range errors detected on the device (token >= V0) are
+ *     recorded in a device error word: every later kernel of the same call skips its
+ *     writes (no output is produced, as the reference raises before writing) and the
+ *     error surfaces as NGRAM_ERANGE from ngram_sync_errors() / any host-buffer call.
+ *   - There is no CPU fallback: every compute entry point runs CUDA kernels.
+ */
+#ifndef NGRAM_B200_H
+#define NGRAM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum ngram_status {
+    NGRAM_OK = 0,
+    NGRAM_EINVAL = 1,   /* std::invalid_argument  */
+    NGRAM_ERANGE = 2,   /* std::out_of_range      */
+    NGRAM_EIO = 3,      /* ngram::io_error        */
+    NGRAM_EPARSE = 4,   /* ngram::parse_error     */
+    NGRAM_ECONFIG = 5,  /* ngram::config_error    */
+    NGRAM_ENUMERIC = 6, /* ngram::numeric_error   */
+    NGRAM_ECUDA = 7,    /* CUDA runtime / driver failure   */
+    NGRAM_ENCCL = 8,    /* collective failure              */
+    NGRAM_ENOMEM = 9    /* device allocation failure       */
+} ngram_status;
+
+typedef enum ngram_dtype { NGRAM_F32 = 0, NGRAM_BF16 = 1 } ngram_dtype;
+
+typedef struct ngram_bank ngram_bank;     /* device-resident embedding_bank */
+typedef struct ngram_decode ngram_decode; /* device-resident batch of sequence_cache */
+
+/* ------------------------------------------------------------------ misc */
+const char* ngram_last_error(void);
+const char* ngram_version(void);
+/* Number of kernels this process has launched through the library (bench evidence). */
+uint64_t ngram_kernel_launches(void);
+
+/* ------------------------------------------------------------------ config (host) */
+/* Replaces ngram_config_from_json + validate (config.cpp:124-139, :32-77). */
+int ngram_config_validate(const char* config_json);
+/* Replaces make_default_config + to_json_string (config.cpp:163-183, :109-122). */
+int ngram_make_default_config(uint32_t base_vocab, int dim, int max_order, int sub_tables, char* json_out,
+                              size_t cap);
+
+/* ------------------------------------------------------------------ banks */
+/* Device bank for `config_json` (embedding_bank_t, embedding.hpp:31-70) on `device`.
+ * Layout in HBM: sub-tables bf16, concatenated by branch, row pitch d;
+ * E0 bf16 V0 x D; W_cat bf16 D x D with W_cat[i][b*d+j] = W_b[i*d+j] (K-major);
+ * LayerNorm gain/bias f32.  shard_count > 1 keeps only rank shard_rank's contiguous
+ * row block of every sub-table (owner(b,h) = floor(h * shard_count / V_b)). */
+int ngram_bank_create(const char* config_json, int device, int shard_rank, int shard_count, ngram_bank** out);
+int ngram_bank_destroy(ngram_bank* bank);
+/* Upload a reference-layout float bank (make_bank / load_bank output) from HOST memory,
+ * converting to bf16 (round-to-nearest-even).  sub[b] / proj[b] indexed by branch_index;
+ * proj ignored for averaged_v1; gain/bias only for layer_norm.  Replaces the implicit
+ * "bank lives in host vectors" of embedding.hpp:31-38. */
+int ngram_bank_upload_f32(ngram_bank* bank, const float* base, const float* const* sub, const float* const* proj,
+                          const float* ln_gain, const float* ln_bias);
+/* Fill the bank on device with the counter-based synthetic generator:
+ * used for LongCat-scale tables that cannot exist on the host. */
+int ngram_bank_generate(ngram_bank* bank, uint64_t seed, void* stream);
+/* Stream a reference bank file (save_bank format, embedding.cpp:77-98 / SPEC.md:285)
+ * straight into the device bank (f32 -> bf16 on device, chunked, no host bank). */
+int ngram_bank_load_file(ngram_bank* bank, const char* path);
+/* Size the per-bank workspace for calls of up to max_tokens tokens (no hot-path allocation). */
+int ngram_bank_reserve(ngram_bank* bank, int64_t max_tokens);
+
+typedef struct ngram_bank_info {
+    int max_order, sub_tables, dim, branch_count, branch_dim, variant, amplification, merge_denominator;
+    uint32_t base_vocab;
+    int shard_rank, shard_count;
+    int tensor_core_path; /* 1 if forward runs the tcgen05 projection GEMM */
+    uint64_t device_bytes;
+    uint64_t sub_vocab[64];   /* V_b in branch order */
+    int64_t row_lo[64];       /* this shard's first row of table b */
+    int64_t row_hi[64];       /* one past this shard's last row of table b */
+    const void* sub_ptr;      /* dev: concatenated local sub-table rows (bf16) */
+    const void* e0_ptr;       /* dev: E0 (bf16) */
+    const void* wcat_ptr;     /* dev: W_cat (bf16), NULL for v1 */
+} ngram_bank_info;
+int ngram_bank_get_info(const ngram_bank* bank, ngram_bank_info* info);
+
+/* ------------------------------------------------------------------ hashing */
+/* rolling_hash over `count` windows (hashing.cpp:33-59).  windows: dev, count x stride
+ * u32, window i = windows[i*stride .. i*stride+lengths[i]) oldest first; lengths (NULL =
+ * orders), orders, bases, moduli: dev per-window hash_spec; out: dev u64.  status: dev
+ * i32 per window: 0, NGRAM_EINVAL (hash_spec::validate or length != order) or
+ * NGRAM_ERANGE (token >= base) -- the per-call exception of the reference. */
+int ngram_rolling_hash_batch(const uint32_t* windows, int64_t stride, const int32_t* lengths, const int32_t* orders,
+                             const uint64_t* bases, const uint64_t* moduli, int64_t count, uint64_t* out,
+                             int32_t* status, void* stream);
+/* hash_all_orders at every position of a batch of sequences (hashing.cpp:61-81 with the
+ * windows of embed_sequence, embedding.hpp:391-405).
+ *   tokens:      dev u32, total_tokens, sequences concatenated
+ *   seq_offsets: dev i64, nseq+1 prefix offsets (seq s = tokens[off[s], off[s+1]))
+ *   prior:       dev u32 nseq x (N-1), the N-1 tokens preceding each sequence
+ *                (prior_context, right-aligned, 0 = pad), or NULL for none
+ *   ids_out:     dev, total_tokens x branch_count, u64 if ids_u64 else u32, entry
+ *                [t][branch_index(n,k)] exactly as hash_all_orders' vector. */
+int ngram_hash_ids(ngram_bank* bank, const uint32_t* tokens, const int64_t* seq_offsets, int64_t nseq,
+                   int64_t total_tokens, const uint32_t* prior, void* ids_out, int ids_u64, void* stream);
+
+/* ------------------------------------------------------------------ forward */
+/* embed_sequence_cached over a batch (embedding.hpp:409-429): rows_out = amplify(merged),
+ * merged_out = merged (either may be NULL), each total_tokens x D of out_dtype, dev. */
+int ngram_embed_forward(ngram_bank* bank, const uint32_t* tokens, const int64_t* seq_offsets, int64_t nseq,
+                        int64_t total_tokens, const uint32_t* prior, void* rows_out, void* merged_out,
+                        int out_dtype, void* stream);
+/* embed_from_ids (embedding.hpp:163-201) for T tokens: ids dev u64 T x branch_count
+ * (global bucket ids), merged_out dev T x D (pre-amplification, as the reference). */
+int ngram_embed_from_ids(ngram_bank* bank, const uint32_t* tokens, const uint64_t* ids, int64_t T, void* merged_out,
+                         int out_dtype, void* stream);
+/* Synchronise `stream` and report (then clear) the bank's device error word:
+ * NGRAM_ERANGE with the offending token when a token >= V0 was seen. */
+int ngram_sync_errors(ngram_bank* bank, void* stream);
+/* Host-buffer entry (the drop-in embed_sequence path): copies tokens/prior from host,
+ * runs the forward, copies rows/merged back to host (NULL to skip), overlapping the
+ * copies with compute in chunks.  Synchronous; raises ERANGE before returning output. */
+int ngram_embed_sequence_host(ngram_bank* bank, const uint32_t* tokens, const int64_t* seq_offsets, int64_t nseq,
+                              const uint32_t* prior, void* rows_out, void* merged_out, int out_dtype);
+
+/* ------------------------------------------------------------------ decode / verify */
+/* A batch of `batch` decode streams (sequence_cache, cache.hpp:38-80): per-stream ring
+ * of the trailing N-1 confirmed tokens (zero-initialised), length and last token,
+ * resident on the device.  max_draft bounds verify blocks. */
+int ngram_decode_create(ngram_bank* bank, int64_t batch, int max_draft, ngram_decode** out);
+int ngram_decode_destroy(ngram_decode* st);
+/* Reset every stream; prior (dev u32 batch x (N-1), may be NULL = zeros) seeds the ring
+ * as if those tokens had been appended (prefill hand-off); lengths (dev u64 or NULL). */
+int ngram_decode_reset(ngram_decode* st, const uint32_t* prior, const uint64_t* lengths, void* stream);
+/* One decode step for every stream: sequence_cache::append(tokens[s]) (cache.cpp:37-57)
+ * followed by embed_from_ids (cache.cpp:136): ids_out (dev u64 batch x branch_count, may
+ * be NULL), merged_out (dev batch x D, pre-amplification, may be NULL). */
+int ngram_decode_step(ngram_decode* st, const uint32_t* tokens, uint64_t* ids_out, void* merged_out, int out_dtype,
+                      void* stream);
+/* Speculative verification block (draft_verify, cache.cpp:152-195): for every stream s
+ * and draft position i < L, the merged embedding of draft[s][i] given ring ++
+ * draft[s][0..i) -- WITHOUT changing the state (the snapshot/rollback of the reference).
+ * draft: dev u32 batch x L; merged_out: dev batch x L x D. */
+int ngram_verify_block(ngram_decode* st, const uint32_t* draft, int L, void* merged_out, int out_dtype,
+                       void* stream);
+/* Accept the first accept[s] (0..L) draft tokens of every stream: the state afterwards
+ * equals accept[s] sequential appends (cache.cpp:185-193); accept > L -> EINVAL. */
+int ngram_commit(ngram_decode* st, const uint32_t* draft, int L, const int32_t* accept, void* stream);
+/* Read back the state (host buffers): ring batch x (N-1), length, last token. */
+int ngram_decode_get_state(ngram_decode* st, uint32_t* ring, uint64_t* length, uint32_t* last);
+
+/* ------------------------------------------------------------------ multi-GPU (row shards) */
+/* Peer-memory exchange for row-sharded banks.  A process group of
+ * shard_count ranks, one GPU each, shares one exchange buffer per rank (X rows of the
+ * home rank's tokens).  ngram_shard_export/open exchange CUDA IPC handles (the caller
+ * moves the 64-byte handles between ranks, e.g. with torch.distributed). */
+typedef struct ngram_shard_group ngram_shard_group;
+int ngram_shard_group_create(ngram_bank* bank, int64_t max_home_tokens, ngram_shard_group** out);
+int ngram_shard_group_destroy(ngram_shard_group* g);
+int ngram_shard_export(ngram_shard_group* g, void* handle64_out);
+int ngram_shard_open(ngram_shard_group* g, int peer_rank, const void* handle64);
+/* Fused gather + NVLink peer store: for the ALL-GATHERED token batch (every rank's
+ * tokens, rank r's sequences at all_seq_offsets[r .. r+1] sequences), write every row
+ * this rank owns straight into its home rank's X buffer.  Stream-ordered; the caller
+ * places a cross-rank barrier (e.g. an NCCL all-reduce on `stream`) before the
+ * projection reads X. */
+int ngram_shard_scatter_rows(ngram_shard_group* g, const uint32_t* all_tokens, const int64_t* all_seq_offsets,
+                             int64_t all_nseq, int64_t all_tokens_n, const int64_t* rank_token_offsets,
+                             const uint32_t* all_prior, void* stream);
+/* Projection + epilogue for this rank's home tokens from its (now complete) X buffer. */
+int ngram_shard_project(ngram_shard_group* g, const uint32_t* home_tokens, int64_t home_T, void* rows_out,
+                        void* merged_out, int out_dtype, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NGRAM_B200_H */

@@ -1,0 +1,337 @@
+// ref_shim.cpp -- extern "C" handle onto the UNMODIFIED reference library.
+//
+// TEST INFRASTRUCTURE ONLY.  oracle/Makefile compiles this file together with the
+// reference's own sources, where they lie under /root/reference/proj/src, into
+// oracle/_ref/libngram_ref.so.  Nothing here re-implements reference arithmetic: every
+// entry point calls the reference function named in its comment.  Used to
+//   * generate tests/golden/ (tests/golden/make_golden.py),
+//   * pin oracle/ngram_oracle.c against the reference (tests/test_oracle_golden.py),
+//   * time the reference CPU path for bench.py --impl reference / cpu_baseline.
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "ngram/cache.hpp"
+#include "ngram/config.hpp"
+#include "ngram/embedding.hpp"
+#include "ngram/errors.hpp"
+#include "ngram/hashing.hpp"
+
+using namespace ngram;
+
+namespace {
+
+thread_local std::string g_err;
+
+int map_exc() {
+    try {
+        throw;
+    } catch (const std::out_of_range& e) {
+        g_err = e.what();
+        return -2;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return -1;
+    } catch (const parse_error& e) {
+        g_err = e.what();
+        return -4;
+    } catch (const io_error& e) {
+        g_err = e.what();
+        return -3;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -9;
+    }
+}
+
+struct ref_bank {
+    embedding_bank bank;
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+// config.cpp:163-183 make_default_config -> JSON (config.cpp:109-122)
+int ref_make_default_config_json(uint32_t v0, int dim, int max_order, int sub_tables, char* buf, int64_t cap) {
+    try {
+        const auto s = to_json_string(make_default_config(v0, dim, max_order, sub_tables));
+        if ((int64_t)s.size() + 1 > cap) return -1;
+        std::memcpy(buf, s.c_str(), s.size() + 1);
+        return 0;
+    } catch (...) {
+        return map_exc();
+    }
+}
+
+// config.cpp:124-139 ngram_config_from_json (validates)
+int ref_config_validate_json(const char* json) {
+    try {
+        ngram_config_from_json(json);
+        return 0;
+    } catch (...) {
+        return map_exc();
+    }
+}
+
+// hashing.cpp:33-59
+int ref_rolling_hash(const uint32_t* window, int64_t len, int order, uint64_t base, uint64_t modulus, uint64_t* out) {
+    try {
+        *out = rolling_hash(std::span<const token_id>(window, std::size_t(len)), hash_spec{order, base, modulus});
+        return 0;
+    } catch (...) {
+        return map_exc();
+    }
+}
+
+// Reproduces tests/test_hashing.cpp:40-57's sample stream (rng64(seed), n in 2..8,
+// base < 2^17, log-uniform modulus < 2^48) and evaluates reference rolling_hash on it.
+// windows: count x 8 (unused tail zero).
+int ref_rolling_hash_cases(uint64_t seed, int count, int32_t* n_out, uint64_t* base_out, uint64_t* mod_out,
+                           uint32_t* windows, uint64_t* hash_out) {
+    try {
+        rng64 rng(seed);
+        for (int trial = 0; trial < count; ++trial) {
+            const int n = 2 + int(uniform_below(rng, 7));
+            const std::uint64_t base = 2 + uniform_below(rng, (1u << 17) - 1);
+            const int bits = 1 + int(uniform_below(rng, 48));
+            const std::uint64_t modulus = 1 + uniform_below(rng, (std::uint64_t(1) << bits));
+            std::vector<token_id> w(static_cast<std::size_t>(n));
+            for (auto& t : w) t = token_id(uniform_below(rng, base));
+            n_out[trial] = n;
+            base_out[trial] = base;
+            mod_out[trial] = modulus;
+            for (int j = 0; j < 8; ++j) windows[trial * 8 + j] = j < n ? w[std::size_t(j)] : 0u;
+            hash_out[trial] = rolling_hash(w, hash_spec{n, base, modulus});
+        }
+        return 0;
+    } catch (...) {
+        return map_exc();
+    }
+}
+
+// hashing.cpp:61-81 over every position of a sequence; windows built by the
+// reference's own detail::fill_context (embedding.hpp:391-405). ids: len x B.
+int ref_hash_sequence(const char* cfg_json, const uint32_t* tokens, int64_t len, const uint32_t* prior,
+                      int64_t prior_len, uint64_t* ids) {
+    try {
+        const auto cfg = ngram_config_from_json(cfg_json);
+        const std::size_t B = std::size_t(cfg.branch_count());
+        std::vector<token_id> ctx;
+        std::span<const token_id> toks(tokens, std::size_t(len));
+        std::span<const token_id> pr(prior, std::size_t(prior_len));
+        for (int64_t pos = 0; pos < len; ++pos) {
+            detail::fill_context(toks, std::size_t(pos), cfg.max_order, pr, ctx);
+            const auto v = hash_all_orders(ctx, cfg);
+            std::memcpy(ids + pos * int64_t(B), v.data(), B * sizeof(uint64_t));
+        }
+        return 0;
+    } catch (...) {
+        return map_exc();
+    }
+}
+
+// embedding.hpp:76-110 make_bank<float>; optionally bf16-round every value (RNE)
+// so the bf16 device bank and this float bank hold identical numbers.
+void* ref_bank_create(const char* cfg_json, uint64_t seed, int round_bf16) {
+    try {
+        auto cfg = ngram_config_from_json(cfg_json);
+        auto rb = std::make_unique<ref_bank>();
+        rb->bank = make_bank<float>(cfg, seed);
+        if (round_bf16) {
+            auto rnd = [](std::vector<float>& v) {
+                for (auto& x : v) {
+                    uint32_t u;
+                    std::memcpy(&u, &x, 4);
+                    u = (u + 0x7fffu + ((u >> 16) & 1u)) & 0xffff0000u;
+                    std::memcpy(&x, &u, 4);
+                }
+            };
+            rnd(rb->bank.base);
+            for (auto& t : rb->bank.sub_tables) rnd(t);
+            for (auto& p : rb->bank.projections) rnd(p);
+            rnd(rb->bank.ln_gain);
+            rnd(rb->bank.ln_bias);
+        }
+        return rb.release();
+    } catch (...) {
+        map_exc();
+        return nullptr;
+    }
+}
+
+// embedding.cpp:100-140 load_bank
+void* ref_bank_load(const char* path) {
+    try {
+        auto rb = std::make_unique<ref_bank>();
+        rb->bank = load_bank(path);
+        return rb.release();
+    } catch (...) {
+        map_exc();
+        return nullptr;
+    }
+}
+
+// embedding.cpp:77-98 save_bank
+int ref_bank_save(void* h, const char* path) {
+    try {
+        save_bank(static_cast<ref_bank*>(h)->bank, path);
+        return 0;
+    } catch (...) {
+        return map_exc();
+    }
+}
+
+void ref_bank_destroy(void* h) { delete static_cast<ref_bank*>(h); }
+
+// Raw tensor views (row-major, embedding.hpp:31-38). which: 0 base, 1 sub[b], 2 proj[b], 3 gain, 4 bias.
+const float* ref_bank_tensor(void* h, int which, int b, int64_t* numel) {
+    auto& bk = static_cast<ref_bank*>(h)->bank;
+    const std::vector<float>* v = nullptr;
+    switch (which) {
+        case 0: v = &bk.base; break;
+        case 1: v = &bk.sub_tables.at(std::size_t(b)); break;
+        case 2: v = &bk.projections.at(std::size_t(b)); break;
+        case 3: v = &bk.ln_gain; break;
+        case 4: v = &bk.ln_bias; break;
+        default: return nullptr;
+    }
+    *numel = int64_t(v->size());
+    return v->data();
+}
+
+// Overwrite the LN gain/bias (the reference tests draw them non-trivially, test_embedding.cpp:211-214).
+int ref_bank_set_ln(void* h, const float* gain, const float* bias) {
+    auto& bk = static_cast<ref_bank*>(h)->bank;
+    if (bk.ln_gain.empty()) return -1;
+    std::memcpy(bk.ln_gain.data(), gain, bk.ln_gain.size() * 4);
+    std::memcpy(bk.ln_bias.data(), bias, bk.ln_bias.size() * 4);
+    return 0;
+}
+
+// embedding.hpp:409-429 embed_sequence_cached<float>: rows (amplified) and merged.
+int ref_embed_sequence_f32(void* h, const uint32_t* tokens, int64_t len, const uint32_t* prior, int64_t prior_len,
+                           float* rows, float* merged) {
+    try {
+        auto& bk = static_cast<ref_bank*>(h)->bank;
+        auto r = embed_sequence_cached<float>(std::span<const token_id>(tokens, std::size_t(len)), bk,
+                                              std::span<const token_id>(prior, std::size_t(prior_len)));
+        if (rows) std::memcpy(rows, r.rows.data(), r.rows.size() * 4);
+        if (merged) std::memcpy(merged, r.merged.data(), r.merged.size() * 4);
+        return 0;
+    } catch (...) {
+        return map_exc();
+    }
+}
+
+// Same in double on bank_cast<float,double> (embedding.hpp:140-156): the tolerance reference.
+int ref_embed_sequence_f64(void* h, const uint32_t* tokens, int64_t len, const uint32_t* prior, int64_t prior_len,
+                           double* rows, double* merged) {
+    try {
+        auto& bk = static_cast<ref_bank*>(h)->bank;
+        const auto bd = bank_cast<float, double>(bk);
+        auto r = embed_sequence_cached<double>(std::span<const token_id>(tokens, std::size_t(len)), bd,
+                                               std::span<const token_id>(prior, std::size_t(prior_len)));
+        if (rows) std::memcpy(rows, r.rows.data(), r.rows.size() * 8);
+        if (merged) std::memcpy(merged, r.merged.data(), r.merged.size() * 8);
+        return 0;
+    } catch (...) {
+        return map_exc();
+    }
+}
+
+// The reference CPU path run over a batch of sequences, one sequence per std::thread
+// (embed_sequence is pure and the bank read-only). Used as the
+// timed CPU baseline. seq_offsets: nseq+1 prefix offsets into tokens; rows: total x D.
+int ref_embed_batch_mt(void* h, const uint32_t* tokens, const int64_t* seq_offsets, int nseq, int nthreads,
+                       float* rows) {
+    auto& bk = static_cast<ref_bank*>(h)->bank;
+    const int64_t D = bk.config.dim;
+    std::vector<std::thread> pool;
+    std::vector<int> rc(std::size_t(nseq), 0);
+    std::atomic<int> next{0};
+    if (nthreads < 1) nthreads = 1;
+    for (int w = 0; w < nthreads; ++w) {
+        pool.emplace_back([&]() {
+            for (;;) {
+                const int s = next.fetch_add(1);
+                if (s >= nseq) return;
+                try {
+                    const int64_t a = seq_offsets[s], b = seq_offsets[s + 1];
+                    const auto r = embed_sequence<float>(std::span<const token_id>(tokens + a, std::size_t(b - a)), bk);
+                    std::memcpy(rows + a * D, r.data(), r.size() * 4);
+                } catch (...) {
+                    rc[std::size_t(s)] = -1;
+                }
+            }
+        });
+    }
+    for (auto& t : pool) t.join();
+    for (int x : rc)
+        if (x) return x;
+    return 0;
+}
+
+// --- cache.cpp ---------------------------------------------------------------
+void* ref_cache_create(const char* cfg_json) {
+    try {
+        return new sequence_cache(ngram_config_from_json(cfg_json));
+    } catch (...) {
+        map_exc();
+        return nullptr;
+    }
+}
+void ref_cache_destroy(void* h) { delete static_cast<sequence_cache*>(h); }
+
+// cache.cpp:37-57
+int ref_cache_append(void* h, uint32_t token, uint64_t* ids) {
+    try {
+        const auto v = static_cast<sequence_cache*>(h)->append(token);
+        std::memcpy(ids, v.data(), v.size() * 8);
+        return 0;
+    } catch (...) {
+        return map_exc();
+    }
+}
+
+int ref_cache_ring(void* h, uint32_t* ring, uint64_t* length, uint32_t* last) {
+    auto* c = static_cast<sequence_cache*>(h);
+    const auto r = c->ring();
+    std::memcpy(ring, r.data(), r.size() * 4);
+    *length = c->length();
+    *last = c->last_token();
+    return int(r.size());
+}
+
+// cache.cpp:152-195 draft_verify with a fresh memo of `memo_capacity`: accepted merged
+// vectors (accept x D) and counters (8 x u64, cache.hpp:17-26 order).
+int ref_draft_verify(void* cache, void* bank, const uint32_t* draft, int64_t len, int64_t accept, int64_t memo_capacity,
+                     int conventional, float* accepted, uint64_t* counters) {
+    try {
+        auto& bk = static_cast<ref_bank*>(bank)->bank;
+        embedding_memo memo{static_cast<std::size_t>(memo_capacity)};
+        cache_counters c;
+        draft_options opts;
+        opts.conventional_draft_embedding = conventional != 0;
+        const auto r = draft_verify(*static_cast<sequence_cache*>(cache), memo, bk,
+                                    std::span<const token_id>(draft, std::size_t(len)), std::size_t(accept), &c, opts);
+        const std::size_t D = std::size_t(bk.config.dim);
+        for (std::size_t i = 0; i < r.accepted.size(); ++i) std::memcpy(accepted + i * D, r.accepted[i].data(), D * 4);
+        const uint64_t cv[8] = {c.appends,          c.rollbacks,        c.memo_hits,           c.memo_misses,
+                                c.table_gathers,    c.projection_madds, c.draft_table_gathers, c.verify_table_gathers};
+        std::memcpy(counters, cv, sizeof(cv));
+        return 0;
+    } catch (...) {
+        return map_exc();
+    }
+}
+
+}  // extern "C"

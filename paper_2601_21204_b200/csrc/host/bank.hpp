@@ -1,0 +1,118 @@
+// bank.hpp -- the device-resident bank (ngram_bank) and decode state (ngram_decode)
+// behind the C-ABI.  Host C++: allocation, layout, tensor maps, workspaces; every
+// computation is a kernel in csrc/kernels.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../kernels/kernels.h"
+#include "config.hpp"
+
+namespace ngh {
+
+void check_cuda(cudaError_t e, const char* what);
+#define NGH_CUDA(x) ::ngh::check_cuda((x), #x)
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev);
+    ~DeviceGuard();
+};
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void alloc(size_t count) {
+        release();
+        if (count == 0) return;
+        cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            p = nullptr;
+            throw Error(NGRAM_ENOMEM, "cudaMalloc of " + std::to_string(count * sizeof(T)) + " bytes failed: " +
+                                          cudaGetErrorString(e));
+        }
+        n = count;
+    }
+    void ensure(size_t count) {
+        if (count > n) alloc(count);
+    }
+};
+
+struct Workspace {
+    int64_t tokens_cap = 0;
+    DevBuf<int32_t> grow;           // [B][Tpad]
+    DevBuf<float> merged_f32;       // [T][D] (LayerNorm staging)
+    DevBuf<uint32_t> tokens;        // host-API staging / decode tokens
+    DevBuf<int64_t> offsets;
+    DevBuf<uint32_t> prior;
+};
+
+}  // namespace ngh
+
+struct ngram_bank {
+    ngh::Config cfg;
+    ngk::Shape shape{};
+    int device = 0;
+    int num_sms = 148;
+    int shard_rank = 0, shard_count = 1;
+    std::vector<int64_t> row_lo, row_hi, row_base;
+    int64_t local_rows = 0;
+    bool tc_path = false;
+
+    ngh::DevBuf<__nv_bfloat16> sub, e0, wcat;
+    ngh::DevBuf<float> ln_gain, ln_bias;
+    ngh::DevBuf<ngk::HashTables> ht;
+    ngh::DevBuf<unsigned long long> err;
+
+    CUtensorMap tmap_sub{}, tmap_w{};
+    ngh::Workspace ws;
+
+    // host-buffer pipeline (ngram_embed_sequence_host)
+    cudaStream_t host_streams[2] = {nullptr, nullptr};
+    ngh::DevBuf<uint8_t> host_out[2];
+    ngh::DevBuf<uint8_t> host_merged[2];
+    ngh::DevBuf<int64_t> host_off[2];
+    ngh::DevBuf<uint32_t> host_prior[2];
+    void* pinned[2] = {nullptr, nullptr};
+    size_t pinned_bytes = 0;
+
+    uint64_t device_bytes() const;
+    ~ngram_bank();
+};
+
+struct ngram_decode {
+    ngram_bank* bank = nullptr;
+    int64_t batch = 0;
+    int max_draft = 0;
+    ngh::DevBuf<uint32_t> ring;             // [batch][N-1] trailing confirmed tokens, oldest first
+    ngh::DevBuf<uint64_t> length;           // [batch]
+    ngh::DevBuf<uint32_t> last;             // [batch]
+    ngh::DevBuf<int64_t> seq_off;           // [max_draft][batch+1] = s * L
+    ngh::DevBuf<int32_t> grow;              // [B][round_up(batch*max_draft, 128)]
+    ngh::DevBuf<unsigned long long> derr;   // decode error word
+};
+
+namespace ngh {
+// Build the TMA descriptors of a bank (driver entry point, no libcuda link).
+void make_tensor_map_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t rows, uint64_t row_pitch_bytes,
+                        uint32_t box_inner, uint32_t box_rows);
+void ensure_workspace(ngram_bank* b, int64_t T);
+inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+}  // namespace ngh

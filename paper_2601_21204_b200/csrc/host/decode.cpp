@@ -1,0 +1,145 @@
+// decode.cpp -- C-ABI of the incremental decode / speculative-verify path
+// (sequence_cache, draft_verify: cache.hpp:38-136, cache.cpp:31-195) over a batch of
+// device-resident streams.  No host round trip on the hot calls.
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <vector>
+
+#include "api_util.hpp"
+#include "bank.hpp"
+
+namespace ngh {
+void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, int64_t gstride, int64_t T,
+                    void* rows, void* merged, int out_bf16, float* ln_scratch, const CUtensorMap* tmap_x,
+                    cudaStream_t st, int amp);
+void reset_error_word(ngram_bank* b, cudaStream_t st);
+}  // namespace ngh
+
+using namespace ngh;
+
+namespace {
+
+// Hash + project T = batch * L block positions whose windows are ring ++ draft.
+void decode_block(ngram_decode* d, const uint32_t* draft, int L, uint64_t* ids_out, void* merged_out, int out_dtype,
+                  cudaStream_t st) {
+    ngram_bank* b = d->bank;
+    const int64_t T = d->batch * L;
+    const int64_t Tpad = round_up(T, 128);
+    reset_error_word(b, st);
+    const int R = b->cfg.max_order - 1;
+    ngk::launch_hash_ids(b->shape, b->ht.p, draft, d->seq_off.p + size_t(L - 1) * size_t(d->batch + 1), d->batch, T,
+                         R > 0 ? d->ring.p : nullptr, ids_out, 1, d->grow.p, Tpad, b->err.p, st);
+    if (merged_out)
+        run_projection(b, draft, d->grow.p, Tpad, T, nullptr, merged_out, out_dtype == NGRAM_BF16, nullptr, nullptr,
+                       st, 0);
+}
+
+}  // namespace
+
+extern "C" {
+
+int ngram_decode_create(ngram_bank* b, int64_t batch, int max_draft, ngram_decode** out) {
+    NGRAM_API_BEGIN
+    if (!b || !out || batch < 1 || max_draft < 1) throw Error(NGRAM_EINVAL, "ngram_decode_create: bad argument");
+    if (b->shard_count != 1) throw Error(NGRAM_EINVAL, "decode state needs a full (unsharded) bank");
+    *out = nullptr;
+    DeviceGuard g(b->device);
+    auto d = std::make_unique<ngram_decode>();
+    d->bank = b;
+    d->batch = batch;
+    d->max_draft = max_draft;
+    const int R = std::max(b->cfg.max_order - 1, 1);
+    d->ring.alloc(size_t(batch) * size_t(R));
+    d->length.alloc(size_t(batch));
+    d->last.alloc(size_t(batch));
+    const int64_t Tmax = batch * max_draft;
+    d->grow.alloc(size_t(std::max(b->shape.B, 1)) * size_t(round_up(Tmax, 128)));
+    d->derr.alloc(1);
+    // per-L sequence offsets {0, L, 2L, ..., batch*L} for L = 1..max_draft
+    std::vector<int64_t> off(size_t(max_draft) * size_t(batch + 1));
+    for (int L = 1; L <= max_draft; ++L)
+        for (int64_t s = 0; s <= batch; ++s) off[size_t(L - 1) * size_t(batch + 1) + size_t(s)] = s * L;
+    d->seq_off.alloc(off.size());
+    NGH_CUDA(cudaMemcpy(d->seq_off.p, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
+    NGH_CUDA(cudaMemset(d->derr.p, 0xff, 8));
+    ngk::launch_decode_reset(b->shape, d->ring.p, d->length.p, d->last.p, nullptr, nullptr, batch, nullptr);
+    NGH_CUDA(cudaDeviceSynchronize());
+    ensure_workspace(b, Tmax);
+    *out = d.release();
+    NGRAM_API_END
+}
+
+int ngram_decode_destroy(ngram_decode* d) {
+    NGRAM_API_BEGIN
+    if (d) {
+        DeviceGuard g(d->bank->device);
+        delete d;
+    }
+    NGRAM_API_END
+}
+
+int ngram_decode_reset(ngram_decode* d, const uint32_t* prior, const uint64_t* lengths, void* stream) {
+    NGRAM_API_BEGIN
+    if (!d) throw Error(NGRAM_EINVAL, "null decode state");
+    DeviceGuard g(d->bank->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    ngk::launch_decode_reset(d->bank->shape, d->ring.p, d->length.p, d->last.p, prior, lengths, d->batch, st);
+    NGH_CUDA(cudaMemsetAsync(d->derr.p, 0xff, 8, st));
+    NGH_CUDA(cudaGetLastError());
+    NGRAM_API_END
+}
+
+int ngram_decode_step(ngram_decode* d, const uint32_t* tokens, uint64_t* ids_out, void* merged_out, int out_dtype,
+                      void* stream) {
+    NGRAM_API_BEGIN
+    if (!d || !tokens) throw Error(NGRAM_EINVAL, "ngram_decode_step: bad argument");
+    if (out_dtype != NGRAM_F32 && out_dtype != NGRAM_BF16) throw Error(NGRAM_EINVAL, "bad out_dtype");
+    DeviceGuard g(d->bank->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    decode_block(d, tokens, 1, ids_out, merged_out, out_dtype, st);
+    ngk::launch_decode_commit(d->bank->shape, d->ring.p, d->length.p, d->last.p, tokens, 1, nullptr, d->batch,
+                              d->bank->err.p, d->derr.p, st);
+    NGH_CUDA(cudaGetLastError());
+    NGRAM_API_END
+}
+
+int ngram_verify_block(ngram_decode* d, const uint32_t* draft, int L, void* merged_out, int out_dtype, void* stream) {
+    NGRAM_API_BEGIN
+    if (!d || !draft || L < 1 || L > d->max_draft) throw Error(NGRAM_EINVAL, "ngram_verify_block: bad argument");
+    if (out_dtype != NGRAM_F32 && out_dtype != NGRAM_BF16) throw Error(NGRAM_EINVAL, "bad out_dtype");
+    DeviceGuard g(d->bank->device);
+    decode_block(d, draft, L, nullptr, merged_out, out_dtype, static_cast<cudaStream_t>(stream));
+    NGH_CUDA(cudaGetLastError());
+    NGRAM_API_END
+}
+
+int ngram_commit(ngram_decode* d, const uint32_t* draft, int L, const int32_t* accept, void* stream) {
+    NGRAM_API_BEGIN
+    if (!d || !draft || !accept || L < 1 || L > d->max_draft) throw Error(NGRAM_EINVAL, "ngram_commit: bad argument");
+    DeviceGuard g(d->bank->device);
+    ngk::launch_decode_commit(d->bank->shape, d->ring.p, d->length.p, d->last.p, draft, L, accept, d->batch,
+                              d->bank->err.p, d->derr.p, static_cast<cudaStream_t>(stream));
+    NGH_CUDA(cudaGetLastError());
+    NGRAM_API_END
+}
+
+int ngram_decode_get_state(ngram_decode* d, uint32_t* ring, uint64_t* length, uint32_t* last) {
+    NGRAM_API_BEGIN
+    if (!d) throw Error(NGRAM_EINVAL, "null decode state");
+    DeviceGuard g(d->bank->device);
+    NGH_CUDA(cudaDeviceSynchronize());
+    unsigned long long e = 0;
+    NGH_CUDA(cudaMemcpy(&e, d->derr.p, 8, cudaMemcpyDeviceToHost));
+    const int R = d->bank->cfg.max_order - 1;
+    if (ring && R > 0) NGH_CUDA(cudaMemcpy(ring, d->ring.p, size_t(d->batch) * size_t(R) * 4, cudaMemcpyDeviceToHost));
+    if (length) NGH_CUDA(cudaMemcpy(length, d->length.p, size_t(d->batch) * 8, cudaMemcpyDeviceToHost));
+    if (last) NGH_CUDA(cudaMemcpy(last, d->last.p, size_t(d->batch) * 4, cudaMemcpyDeviceToHost));
+    if (e != ~0ull) {
+        NGH_CUDA(cudaMemset(d->derr.p, 0xff, 8));
+        throw Error(int(e >> 32), "draft_verify: accept count exceeds draft length");
+    }
+    NGRAM_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,301 @@
+// forward.cpp -- C-ABI entry points of the prefill hot path: misc / config, hashing,
+// embed forward (device buffers), embed_from_ids, and the host-buffer pipeline.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "api_util.hpp"
+#include "bank.hpp"
+
+namespace ngh {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+int set_error(int status, const char* msg) {
+    g_last_error = msg ? msg : "";
+    return status;
+}
+
+// Validate the per-sequence offsets on the host side of the boundary (cheap, nseq+1).
+static void check_offsets(const int64_t* off, int64_t nseq, int64_t T) {
+    if (off[0] != 0 || off[nseq] != T) throw Error(NGRAM_EINVAL, "seq_offsets must start at 0 and end at total_tokens");
+    for (int64_t i = 0; i < nseq; ++i)
+        if (off[i + 1] < off[i]) throw Error(NGRAM_EINVAL, "seq_offsets must be non-decreasing");
+}
+
+// One forward over T rows whose storage rows are already in `grow` (stride gstride).
+// Writes merged/rows per the bank's amplification; LayerNorm via a second kernel.
+void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, int64_t gstride, int64_t T,
+                    void* rows, void* merged, int out_bf16, float* ln_scratch, const CUtensorMap* tmap_x,
+                    cudaStream_t st, int amp) {
+    if (T <= 0) return;
+    ngk::FwdArgs a{};
+    a.s = b->shape;
+    if (amp >= 0) a.s.amp = amp;
+    a.ht = b->ht.p;
+    a.tokens = tokens;
+    a.grow = grow;
+    a.sub = b->sub.p;
+    a.e0 = b->e0.p;
+    a.wcat = b->wcat.p;
+    a.ln_gain = b->ln_gain.p;
+    a.ln_bias = b->ln_bias.p;
+    a.T = T;
+    a.Tpad = gstride;
+    a.err = b->err.p;
+    a.tmap_sub = &b->tmap_sub;
+    a.tmap_w = &b->tmap_w;
+    a.tmap_x = tmap_x;
+    const bool ln = a.s.amp == 2;
+    float* ln_merged = nullptr;
+    if (ln) {
+        ln_merged = (merged && !out_bf16) ? static_cast<float*>(merged) : ln_scratch;
+        a.merged_out = ln_merged;
+        a.rows_out = nullptr;
+        a.out_bf16 = 0;
+    } else {
+        a.merged_out = merged;
+        a.rows_out = rows;
+        a.out_bf16 = out_bf16;
+    }
+    if (b->tc_path) ngk::launch_forward_tc(a, b->num_sms, st);
+    else ngk::launch_forward_simt(a, st);
+    if (ln)
+        ngk::launch_layernorm_rows(a.s, ln_merged, b->ln_gain.p, b->ln_bias.p, rows,
+                                   (merged && ln_merged != merged) ? merged : nullptr, out_bf16, T, b->err.p, st);
+    NGH_CUDA(cudaGetLastError());
+}
+
+void reset_error_word(ngram_bank* b, cudaStream_t st) {
+    NGH_CUDA(cudaMemsetAsync(b->err.p, 0xff, sizeof(unsigned long long), st));
+}
+
+}  // namespace ngh
+
+using namespace ngh;
+
+extern "C" {
+
+const char* ngram_last_error(void) { return g_last_error.c_str(); }
+const char* ngram_version(void) { return "ngram_b200 0.1 (sm_100a)"; }
+uint64_t ngram_kernel_launches(void) { return ngk::launches(); }
+
+int ngram_config_validate(const char* config_json) {
+    NGRAM_API_BEGIN
+    if (!config_json) throw Error(NGRAM_EINVAL, "null config");
+    parse_config(config_json);
+    NGRAM_API_END
+}
+
+int ngram_make_default_config(uint32_t base_vocab, int dim, int max_order, int sub_tables, char* json_out,
+                              size_t cap) {
+    NGRAM_API_BEGIN
+    const std::string s = to_json(default_config(base_vocab, dim, max_order, sub_tables));
+    if (!json_out || cap < s.size() + 1) throw Error(NGRAM_EINVAL, "output buffer too small");
+    std::memcpy(json_out, s.c_str(), s.size() + 1);
+    NGRAM_API_END
+}
+
+int ngram_rolling_hash_batch(const uint32_t* windows, int64_t stride, const int32_t* lengths, const int32_t* orders,
+                             const uint64_t* bases, const uint64_t* moduli, int64_t count, uint64_t* out,
+                             int32_t* status, void* stream) {
+    NGRAM_API_BEGIN
+    if (count < 0 || (count > 0 && (!windows || !orders || !bases || !moduli || !out || !status)))
+        throw Error(NGRAM_EINVAL, "ngram_rolling_hash_batch: bad argument");
+    ngk::launch_rolling_hash_batch(windows, stride, lengths, orders, bases, moduli, count, out, status,
+                                   static_cast<cudaStream_t>(stream));
+    NGH_CUDA(cudaGetLastError());
+    NGRAM_API_END
+}
+
+int ngram_hash_ids(ngram_bank* b, const uint32_t* tokens, const int64_t* seq_offsets, int64_t nseq,
+                   int64_t total_tokens, const uint32_t* prior, void* ids_out, int ids_u64, void* stream) {
+    NGRAM_API_BEGIN
+    if (!b || nseq < 1 || total_tokens < 0 || !seq_offsets || (total_tokens > 0 && (!tokens || !ids_out)))
+        throw Error(NGRAM_EINVAL, "ngram_hash_ids: bad argument");
+    DeviceGuard g(b->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    reset_error_word(b, st);
+    ngk::launch_hash_ids(b->shape, b->ht.p, tokens, seq_offsets, nseq, total_tokens, prior, ids_out, ids_u64, nullptr,
+                         0, b->err.p, st);
+    NGH_CUDA(cudaGetLastError());
+    NGRAM_API_END
+}
+
+int ngram_embed_forward(ngram_bank* b, const uint32_t* tokens, const int64_t* seq_offsets, int64_t nseq,
+                        int64_t total_tokens, const uint32_t* prior, void* rows_out, void* merged_out, int out_dtype,
+                        void* stream) {
+    NGRAM_API_BEGIN
+    if (!b || nseq < 1 || total_tokens < 0 || !seq_offsets || (total_tokens > 0 && !tokens))
+        throw Error(NGRAM_EINVAL, "ngram_embed_forward: bad argument");
+    if (out_dtype != NGRAM_F32 && out_dtype != NGRAM_BF16) throw Error(NGRAM_EINVAL, "bad out_dtype");
+    DeviceGuard g(b->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    ensure_workspace(b, total_tokens);
+    const int64_t Tpad = round_up(std::max<int64_t>(total_tokens, 1), 128);
+    reset_error_word(b, st);
+    if (total_tokens == 0) return NGRAM_OK;
+    ngk::launch_hash_ids(b->shape, b->ht.p, tokens, seq_offsets, nseq, total_tokens, prior, nullptr, 0, b->ws.grow.p,
+                         Tpad, b->err.p, st);
+    run_projection(b, tokens, b->ws.grow.p, Tpad, total_tokens, rows_out, merged_out, out_dtype == NGRAM_BF16,
+                   b->ws.merged_f32.p, nullptr, st, -1);
+    NGRAM_API_END
+}
+
+int ngram_embed_from_ids(ngram_bank* b, const uint32_t* tokens, const uint64_t* ids, int64_t T, void* merged_out,
+                         int out_dtype, void* stream) {
+    NGRAM_API_BEGIN
+    if (!b || T < 0 || (T > 0 && (!tokens || !ids || !merged_out)))
+        throw Error(NGRAM_EINVAL, "ngram_embed_from_ids: bad argument");
+    DeviceGuard g(b->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    ensure_workspace(b, T);
+    const int64_t Tpad = round_up(std::max<int64_t>(T, 1), 128);
+    reset_error_word(b, st);
+    if (T == 0) return NGRAM_OK;
+    ngk::launch_ids_to_rows(b->shape, b->ht.p, ids, tokens, T, b->ws.grow.p, Tpad, b->err.p, st);
+    // embed_from_ids returns the merged (pre-amplification) vector: run with amp = none.
+    run_projection(b, tokens, b->ws.grow.p, Tpad, T, nullptr, merged_out, out_dtype == NGRAM_BF16, nullptr, nullptr,
+                   st, 0);
+    NGRAM_API_END
+}
+
+int ngram_sync_errors(ngram_bank* b, void* stream) {
+    NGRAM_API_BEGIN
+    if (!b) throw Error(NGRAM_EINVAL, "null bank");
+    DeviceGuard g(b->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    unsigned long long e = 0;
+    NGH_CUDA(cudaMemcpyAsync(&e, b->err.p, sizeof(e), cudaMemcpyDeviceToHost, st));
+    NGH_CUDA(cudaStreamSynchronize(st));
+    if (e != ~0ull) {
+        NGH_CUDA(cudaMemsetAsync(b->err.p, 0xff, sizeof(e), st));
+        NGH_CUDA(cudaStreamSynchronize(st));
+        throw Error(NGRAM_ERANGE, "embedding: token out of range for base vocabulary " +
+                                      std::to_string(b->cfg.base_vocab) + " (first bad window at position " +
+                                      std::to_string(e) + ")");
+    }
+    NGRAM_API_END
+}
+
+int ngram_embed_sequence_host(ngram_bank* b, const uint32_t* tokens, const int64_t* seq_offsets, int64_t nseq,
+                              const uint32_t* prior, void* rows_out, void* merged_out, int out_dtype) {
+    NGRAM_API_BEGIN
+    if (!b || nseq < 1 || !seq_offsets) throw Error(NGRAM_EINVAL, "ngram_embed_sequence_host: bad argument");
+    if (out_dtype != NGRAM_F32 && out_dtype != NGRAM_BF16) throw Error(NGRAM_EINVAL, "bad out_dtype");
+    const int64_t T = seq_offsets[nseq];
+    check_offsets(seq_offsets, nseq, T);
+    DeviceGuard g(b->device);
+    for (int i = 0; i < 2; ++i)
+        if (!b->host_streams[i]) NGH_CUDA(cudaStreamCreateWithFlags(&b->host_streams[i], cudaStreamNonBlocking));
+    cudaStream_t s0 = b->host_streams[0], s1 = b->host_streams[1];
+    const int N1 = std::max(b->cfg.max_order - 1, 0);
+    ensure_workspace(b, T);
+    const int64_t Tpad = round_up(std::max<int64_t>(T, 1), 128);
+    b->ws.tokens.ensure(size_t(std::max<int64_t>(T, 1)));
+    b->ws.offsets.ensure(size_t(nseq + 1));
+    if (prior && N1 > 0) b->ws.prior.ensure(size_t(nseq) * size_t(N1));
+    if (T > 0) NGH_CUDA(cudaMemcpyAsync(b->ws.tokens.p, tokens, size_t(T) * 4, cudaMemcpyHostToDevice, s0));
+    NGH_CUDA(cudaMemcpyAsync(b->ws.offsets.p, seq_offsets, size_t(nseq + 1) * 8, cudaMemcpyHostToDevice, s0));
+    if (prior && N1 > 0)
+        NGH_CUDA(cudaMemcpyAsync(b->ws.prior.p, prior, size_t(nseq) * size_t(N1) * 4, cudaMemcpyHostToDevice, s0));
+    reset_error_word(b, s0);
+    if (T == 0) {
+        NGH_CUDA(cudaStreamSynchronize(s0));
+        return NGRAM_OK;
+    }
+    // K1 over the whole batch first: the reference raises before producing any output.
+    ngk::launch_hash_ids(b->shape, b->ht.p, b->ws.tokens.p, b->ws.offsets.p, nseq, T,
+                         (prior && N1 > 0) ? b->ws.prior.p : nullptr, nullptr, 0, b->ws.grow.p, Tpad, b->err.p, s0);
+    unsigned long long e = 0;
+    NGH_CUDA(cudaMemcpyAsync(&e, b->err.p, sizeof(e), cudaMemcpyDeviceToHost, s0));
+    NGH_CUDA(cudaStreamSynchronize(s0));
+    if (e != ~0ull)
+        throw Error(NGRAM_ERANGE, "embedding: token out of range for base vocabulary " +
+                                      std::to_string(b->cfg.base_vocab) + " (first bad window at position " +
+                                      std::to_string(e) + ")");
+    // Chunked projection on two streams: chunk i's D2H overlaps chunk i+1's kernels.
+    const size_t esz = out_dtype == NGRAM_BF16 ? 2 : 4;
+    const int64_t D = b->cfg.dim;
+    const int64_t chunk = std::min<int64_t>(Tpad, 8192);
+    const size_t cbytes = size_t(chunk) * size_t(D) * esz;
+    cudaPointerAttributes pa{};
+    auto is_pinned = [&](const void* p) {
+        if (!p) return true;
+        if (cudaPointerGetAttributes(&pa, p) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        return pa.type == cudaMemoryTypeHost;
+    };
+    const bool direct = is_pinned(rows_out) && is_pinned(merged_out);
+    for (int i = 0; i < 2; ++i) {
+        if (rows_out) b->host_out[i].ensure(cbytes);
+        if (merged_out) b->host_merged[i].ensure(cbytes);
+    }
+    if (!direct && b->pinned_bytes < cbytes * 2) {
+        for (int i = 0; i < 2; ++i) {
+            if (b->pinned[i]) cudaFreeHost(b->pinned[i]);
+            b->pinned[i] = nullptr;
+            NGH_CUDA(cudaMallocHost(&b->pinned[i], cbytes * 2));
+        }
+        b->pinned_bytes = cbytes * 2;
+    }
+    cudaEvent_t hashed;
+    NGH_CUDA(cudaEventCreateWithFlags(&hashed, cudaEventDisableTiming));
+    NGH_CUDA(cudaEventRecord(hashed, s0));
+    NGH_CUDA(cudaStreamWaitEvent(s1, hashed, 0));
+    int64_t nchunks = (T + chunk - 1) / chunk;
+    std::vector<int64_t> pending(2, -1);  // chunk index whose staged copy awaits a host memcpy
+    auto drain = [&](int slot) {
+        const int64_t c = pending[size_t(slot)];
+        if (c < 0) return;
+        NGH_CUDA(cudaStreamSynchronize(b->host_streams[slot]));
+        const int64_t c0 = c * chunk, n = std::min(chunk, T - c0);
+        const size_t bytes = size_t(n) * size_t(D) * esz;
+        uint8_t* pin = static_cast<uint8_t*>(b->pinned[slot]);
+        if (rows_out) std::memcpy(static_cast<uint8_t*>(rows_out) + size_t(c0) * size_t(D) * esz, pin, bytes);
+        if (merged_out)
+            std::memcpy(static_cast<uint8_t*>(merged_out) + size_t(c0) * size_t(D) * esz, pin + cbytes, bytes);
+        pending[size_t(slot)] = -1;
+    };
+    for (int64_t c = 0; c < nchunks; ++c) {
+        const int slot = int(c & 1);
+        cudaStream_t st = b->host_streams[slot];
+        const int64_t c0 = c * chunk, n = std::min(chunk, T - c0);
+        if (!direct) drain(slot);
+        void* drows = rows_out ? b->host_out[slot].p : nullptr;
+        void* dmerged = merged_out ? b->host_merged[slot].p : nullptr;
+        run_projection(b, b->ws.tokens.p + c0, b->ws.grow.p + c0, Tpad, n, drows, dmerged, out_dtype == NGRAM_BF16,
+                       b->ws.merged_f32.p ? b->ws.merged_f32.p + size_t(c0) * size_t(D) : nullptr, nullptr, st, -1);
+        const size_t bytes = size_t(n) * size_t(D) * esz;
+        if (direct) {
+            if (rows_out)
+                NGH_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(rows_out) + size_t(c0) * size_t(D) * esz, drows, bytes,
+                                         cudaMemcpyDeviceToHost, st));
+            if (merged_out)
+                NGH_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(merged_out) + size_t(c0) * size_t(D) * esz, dmerged,
+                                         bytes, cudaMemcpyDeviceToHost, st));
+        } else {
+            uint8_t* pin = static_cast<uint8_t*>(b->pinned[slot]);
+            if (rows_out) NGH_CUDA(cudaMemcpyAsync(pin, drows, bytes, cudaMemcpyDeviceToHost, st));
+            if (merged_out) NGH_CUDA(cudaMemcpyAsync(pin + cbytes, dmerged, bytes, cudaMemcpyDeviceToHost, st));
+            pending[size_t(slot)] = c;
+        }
+    }
+    if (!direct) {
+        drain(0);
+        drain(1);
+    }
+    NGH_CUDA(cudaStreamSynchronize(s0));
+    NGH_CUDA(cudaStreamSynchronize(s1));
+    cudaEventDestroy(hashed);
+    NGRAM_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,82 @@
+// decode.cu -- device-resident sequence_cache state for a batch of decode streams
+// (cache.hpp:38-80, cache.cpp:31-96).  The hashing of a decode step / verify block is
+// K1 itself (the ring plays the role of prior_context), the projection is K3; these
+// kernels only move the ring:
+//   * commit: ring <- last N-1 tokens of (ring ++ draft[0..accept)), length += accept,
+//     last <- draft[accept-1] -- exactly `accept` sequential appends (cache.cpp:49-55),
+//     i.e. the state draft_verify leaves behind (cache.cpp:182-193).  The whole batch is
+//     validated first (accept <= L for every stream, no out-of-range token recorded by
+//     K1): on any violation no stream changes, as the reference raises before mutating.
+//   * reset: seed every ring from a prior context (prefill hand-off) or zeros.
+#include <cstdint>
+
+#include "kernels.h"
+
+namespace ngk {
+
+namespace {
+
+__global__ void __launch_bounds__(1024) commit_kernel(int R, uint32_t* __restrict__ ring, uint64_t* __restrict__ length,
+                                                      uint32_t* __restrict__ last, const uint32_t* __restrict__ draft,
+                                                      int L, const int32_t* __restrict__ accept, int64_t batch,
+                                                      unsigned long long* err, unsigned long long* derr) {
+    // phase 1: validate the whole batch (single CTA)
+    int bad = 0;
+    for (int64_t s = threadIdx.x; s < batch; s += blockDim.x) {
+        const int a = accept ? accept[s] : L;
+        if (a < 0 || a > L) bad = 1;
+    }
+    bad = __syncthreads_or(bad);
+    if (bad) {
+        if (threadIdx.x == 0) atomicMin(derr, (1ull << 32) | 1ull);  // NGRAM_EINVAL
+        return;
+    }
+    if (*err != ~0ull) return;  // a token of this block was out of range: state unchanged
+    // phase 2: commit
+    for (int64_t s = threadIdx.x; s < batch; s += blockDim.x) {
+        const int a = accept ? accept[s] : L;
+        if (a == 0) continue;
+        uint32_t* rg = ring + s * R;
+        const uint32_t* dr = draft + s * L;
+        uint32_t nr[kMaxOrder];
+        for (int j = 0; j < R; ++j) {  // position j of the new ring = element (a + j) of ring ++ draft
+            const int k = a + j;
+            nr[j] = k < R ? rg[k] : dr[k - R];
+        }
+        for (int j = 0; j < R; ++j) rg[j] = nr[j];
+        length[s] += (uint64_t)a;
+        last[s] = dr[a - 1];
+    }
+}
+
+__global__ void reset_kernel(int R, uint32_t* __restrict__ ring, uint64_t* __restrict__ length,
+                             uint32_t* __restrict__ last, const uint32_t* __restrict__ prior,
+                             const uint64_t* __restrict__ lengths, int64_t batch) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= batch) return;
+    for (int j = 0; j < R; ++j) ring[s * R + j] = prior ? prior[s * R + j] : 0u;
+    length[s] = lengths ? lengths[s] : 0ull;
+    last[s] = (prior && R > 0) ? prior[s * R + R - 1] : 0u;
+}
+
+}  // namespace
+
+void launch_decode_commit(const Shape& s, uint32_t* ring, uint64_t* length, uint32_t* last, const uint32_t* draft,
+                          int L, const int32_t* accept, int64_t batch, unsigned long long* err,
+                          unsigned long long* derr, cudaStream_t st) {
+    if (batch <= 0) return;
+    const int R = s.N > 1 ? s.N - 1 : 0;
+    const int threads = batch >= 1024 ? 1024 : (int)((batch + 31) / 32 * 32);
+    commit_kernel<<<1, threads, 0, st>>>(R, ring, length, last, draft, L, accept, batch, err, derr);
+    count_launch();
+}
+
+void launch_decode_reset(const Shape& s, uint32_t* ring, uint64_t* length, uint32_t* last, const uint32_t* prior,
+                         const uint64_t* lengths, int64_t batch, cudaStream_t st) {
+    if (batch <= 0) return;
+    const int R = s.N > 1 ? s.N - 1 : 0;
+    reset_kernel<<<(unsigned)((batch + 255) / 256), 256, 0, st>>>(R, ring, length, last, prior, lengths, batch);
+    count_launch();
+}
+
+}  // namespace ngk

@@ -1,0 +1,218 @@
+// hash.cu -- K1, the n-gram hash-index kernel (bit-exact restatement of the reference's
+// polynomial rolling hash, hashing.cpp:33-81, over the windows of embed_sequence,
+// embedding.hpp:391-405).
+//
+// One thread per position.  For branch b=(n-2)K+(k-1) the bucket is
+//     h_b = ( sum_{j<n} (w[N-1-j] mod V_b) * (V0^j mod V_b) ) mod V_b
+// -- the same residue the reference accumulates step by step (exact integer arithmetic,
+// so the result is identical).  Fast path (every V_b <= 2^32): all products fit in
+// 64 bits and every reduction is a Barrett step with mu = floor(2^64 / V_b) (quotient
+// estimate low by at most 2, so two conditional subtractions are exact).  General path
+// (any V_b < 2^64): 128-bit products, as the reference's mulmod (hashing.cpp:11-15).
+//
+// HBM: reads N tokens (L1/L2 hits, 4 B/token from DRAM), writes B ids (u32) and B
+// storage rows (i32): 4 + 8B bytes/token -- purely bandwidth/latency bound.
+#include <cstdint>
+
+#include "kernels.h"
+
+namespace ngk {
+
+namespace {
+
+__device__ __forceinline__ uint64_t barrett_mod(uint64_t x, uint64_t m, uint64_t mu) {
+    const uint64_t q = __umul64hi(x, mu);
+    uint64_t r = x - q * m;
+    if (r >= m) r -= m;
+    if (r >= m) r -= m;
+    return r;
+}
+
+__device__ __forceinline__ uint64_t mulmod128(uint64_t a, uint64_t b, uint64_t m) {
+    return static_cast<uint64_t>((static_cast<unsigned __int128>(a) * b) % m);
+}
+
+// Position t of the concatenated batch -> sequence index (largest s with off[s] <= t).
+__device__ __forceinline__ int64_t find_seq(const int64_t* __restrict__ off, int64_t nseq, int64_t t) {
+    int64_t lo = 0, hi = nseq - 1;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (__ldg(off + mid) <= t) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+template <int MAXN>
+__global__ void __launch_bounds__(256) hash_ids_kernel(Shape s, const HashTables* __restrict__ ht,
+                                                        const uint32_t* __restrict__ tokens,
+                                                        const int64_t* __restrict__ seq_off, int64_t nseq, int64_t T,
+                                                        const uint32_t* __restrict__ prior, void* __restrict__ ids_tok,
+                                                        int ids_u64, int32_t* __restrict__ grow, int64_t Tpad,
+                                                        unsigned long long* err) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= Tpad) return;
+    const int N = s.N, K = s.K, B = s.B;
+    if (t >= T) {  // padding rows of the GEMM's last m-tile: a valid (row 0) address, never stored
+        if (grow)
+            for (int b = 0; b < B; ++b) grow[(int64_t)b * Tpad + t] = 0;
+        return;
+    }
+    const int64_t sq = find_seq(seq_off, nseq, t);
+    const int64_t p = t - __ldg(seq_off + sq);
+    const int64_t base = __ldg(seq_off + sq);
+
+    uint32_t w[MAXN];
+    bool bad = false;
+#pragma unroll
+    for (int j = 0; j < MAXN; ++j) {
+        if (j < N) {
+            const int64_t idx = p - (N - 1) + j;
+            uint32_t v;
+            if (idx >= 0) v = __ldg(tokens + base + idx);
+            else v = prior ? __ldg(prior + sq * (N - 1) + (N - 1) + idx) : 0u;
+            w[j] = v;
+            bad |= (v >= s.V0);
+        }
+    }
+    if (bad) {  // the reference throws out_of_range at the first window holding the token
+        atomicMin(err, (unsigned long long)t);
+        return;
+    }
+    for (int b = 0; b < B; ++b) {
+        const int n = 2 + b / K;
+        const uint64_t m = __ldg(&ht->modulus[b]);
+        uint64_t h = 0;
+        if (m > 1) {
+            if (s.fast_hash) {
+                const uint64_t mu = __ldg(&ht->barrett[b]);
+                uint64_t acc = 0;
+#pragma unroll
+                for (int j = 0; j < MAXN; ++j) {
+                    if (j < n) {
+                        const uint64_t tm = barrett_mod((uint64_t)w[N - 1 - j], m, mu);
+                        acc += barrett_mod(tm * __ldg(&ht->pow[b][j]), m, mu);
+                    }
+                }
+                h = barrett_mod(acc, m, mu);  // acc < n * 2^32
+            } else {
+                uint64_t acc = 0;
+#pragma unroll
+                for (int j = 0; j < MAXN; ++j) {
+                    if (j < n) {
+                        const uint64_t tm = (uint64_t)w[N - 1 - j] % m;
+                        acc = (acc + mulmod128(tm, __ldg(&ht->pow[b][j]), m)) % m;
+                    }
+                }
+                h = acc;
+            }
+        }
+        if (ids_tok) {
+            if (ids_u64) static_cast<uint64_t*>(ids_tok)[t * B + b] = h;
+            else static_cast<uint32_t*>(ids_tok)[t * B + b] = (uint32_t)h;
+        }
+        if (grow) {
+            const int64_t lo = __ldg(&ht->row_lo[b]), hi = __ldg(&ht->row_hi[b]);
+            const int64_t hh = (int64_t)h;
+            grow[(int64_t)b * Tpad + t] = (hh >= lo && hh < hi) ? (int32_t)(__ldg(&ht->row_base[b]) + (hh - lo)) : -1;
+        }
+    }
+}
+
+// Reference rolling_hash, one window per thread, with its validation order
+// (hash_spec::validate, then length check, then per-token range check while hashing).
+__global__ void rolling_hash_kernel(const uint32_t* __restrict__ windows, int64_t stride,
+                                    const int32_t* __restrict__ lengths, const int32_t* __restrict__ orders,
+                                    const uint64_t* __restrict__ bases, const uint64_t* __restrict__ moduli,
+                                    int64_t count, uint64_t* __restrict__ out, int32_t* __restrict__ status) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const int order = orders[i];
+    const uint64_t base = bases[i], m = moduli[i];
+    const int len = lengths ? lengths[i] : order;
+    if (order < 2 || base < 2 || m < 1 || len != order) {
+        status[i] = 1;  // NGRAM_EINVAL
+        out[i] = 0;
+        return;
+    }
+    const uint32_t* w = windows + i * stride;
+    const uint64_t base_mod = base % m;
+    uint64_t acc = 0, power = 1 % m;
+    for (int j = 0; j < order; ++j) {
+        const uint32_t t = w[len - 1 - j];
+        if ((uint64_t)t >= base) {
+            status[i] = 2;  // NGRAM_ERANGE
+            out[i] = 0;
+            return;
+        }
+        acc = (acc + mulmod128((uint64_t)t % m, power, m)) % m;
+        power = mulmod128(power, base_mod, m);
+    }
+    out[i] = acc;
+    status[i] = 0;
+}
+
+// User-supplied global bucket ids -> storage rows, with embedding_bank_t::sub_row /
+// base_row range checks (embedding.hpp:41-44, 58-62).
+__global__ void ids_to_rows_kernel(Shape s, const HashTables* __restrict__ ht, const uint64_t* __restrict__ ids,
+                                   const uint32_t* __restrict__ tokens, int64_t T, int32_t* __restrict__ grow,
+                                   int64_t Tpad, unsigned long long* err) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= Tpad) return;
+    const int B = s.B;
+    if (t >= T) {
+        for (int b = 0; b < B; ++b) grow[(int64_t)b * Tpad + t] = 0;
+        return;
+    }
+    bool bad = tokens[t] >= s.V0;
+    for (int b = 0; b < B; ++b) {
+        const uint64_t h = ids[t * B + b];
+        bad |= h >= __ldg(&ht->modulus[b]);
+        const int64_t lo = __ldg(&ht->row_lo[b]), hi = __ldg(&ht->row_hi[b]);
+        const int64_t hh = (int64_t)h;
+        grow[(int64_t)b * Tpad + t] = (hh >= lo && hh < hi) ? (int32_t)(__ldg(&ht->row_base[b]) + (hh - lo)) : -1;
+    }
+    if (bad) atomicMin(err, (unsigned long long)t);
+}
+
+}  // namespace
+
+void launch_hash_ids(const Shape& s, const HashTables* ht, const uint32_t* tokens, const int64_t* seq_off,
+                     int64_t nseq, int64_t T, const uint32_t* prior, void* ids_tok, int ids_u64, int32_t* grow,
+                     int64_t Tpad, unsigned long long* err, cudaStream_t st) {
+    const int64_t n = grow ? Tpad : T;
+    if (n <= 0) return;
+    const int threads = 256;
+    const unsigned blocks = (unsigned)((n + threads - 1) / threads);
+    if (s.N <= 4)
+        hash_ids_kernel<4><<<blocks, threads, 0, st>>>(s, ht, tokens, seq_off, nseq, T, prior, ids_tok, ids_u64, grow,
+                                                       grow ? Tpad : T, err);
+    else if (s.N <= 8)
+        hash_ids_kernel<8><<<blocks, threads, 0, st>>>(s, ht, tokens, seq_off, nseq, T, prior, ids_tok, ids_u64, grow,
+                                                       grow ? Tpad : T, err);
+    else
+        hash_ids_kernel<16><<<blocks, threads, 0, st>>>(s, ht, tokens, seq_off, nseq, T, prior, ids_tok, ids_u64,
+                                                        grow, grow ? Tpad : T, err);
+    count_launch();
+}
+
+void launch_rolling_hash_batch(const uint32_t* windows, int64_t stride, const int32_t* lengths, const int32_t* orders,
+                               const uint64_t* bases, const uint64_t* moduli, int64_t count, uint64_t* out,
+                               int32_t* status, cudaStream_t st) {
+    if (count <= 0) return;
+    const int threads = 256;
+    rolling_hash_kernel<<<(unsigned)((count + threads - 1) / threads), threads, 0, st>>>(
+        windows, stride, lengths, orders, bases, moduli, count, out, status);
+    count_launch();
+}
+
+void launch_ids_to_rows(const Shape& s, const HashTables* ht, const uint64_t* ids, const uint32_t* tokens, int64_t T,
+                        int32_t* grow, int64_t Tpad, unsigned long long* err, cudaStream_t st) {
+    if (Tpad <= 0) return;
+    const int threads = 256;
+    ids_to_rows_kernel<<<(unsigned)((Tpad + threads - 1) / threads), threads, 0, st>>>(s, ht, ids, tokens, T, grow,
+                                                                                        Tpad, err);
+    count_launch();
+}
+
+}  // namespace ngk

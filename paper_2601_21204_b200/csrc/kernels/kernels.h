@@ -1,0 +1,110 @@
+// kernels.h -- host-side launchers for the sm_100a kernels (implemented in *.cu).
+// Used only by the C++ host layer (csrc/host/*.cpp); no torch types anywhere.
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+namespace ngk {
+
+constexpr int kMaxBranches = 64;
+constexpr int kMaxOrder = 16;
+
+// Immutable shape + hashing constants of a bank, resident in device memory.
+struct HashTables {
+    uint64_t modulus[kMaxBranches];            // V_b
+    uint64_t barrett[kMaxBranches];            // floor(2^64 / V_b) (fast path, V_b >= 2)
+    uint64_t pow[kMaxBranches][kMaxOrder];     // V0^j mod V_b
+    int64_t row_base[kMaxBranches];            // storage row of (local) bucket row_lo[b]
+    int64_t row_lo[kMaxBranches];              // first bucket stored on this shard
+    int64_t row_hi[kMaxBranches];              // one past the last bucket stored here
+};
+
+struct Shape {
+    int N, K, B, D, d, variant, amp, denom;
+    uint32_t V0;
+    int fast_hash;  // all V_b <= 2^32
+};
+
+enum AmpMode { kAmpNone = 0, kAmpSqrt = 1, kAmpLN = 2 };
+
+// Global launch counter (bench evidence: kernels launched by this library).
+void count_launch(int n = 1);
+uint64_t launches();
+
+// ---- hashing (hash.cu)
+// ids_tok: [T][B] (u32 or u64) or null; grow: [B][Tpad] int32 storage rows (or -1 when the
+// row is not local to this shard) or null.  err: device u64, min bad token index.
+void launch_hash_ids(const Shape& s, const HashTables* ht, const uint32_t* tokens, const int64_t* seq_off,
+                     int64_t nseq, int64_t T, const uint32_t* prior, void* ids_tok, int ids_u64, int32_t* grow,
+                     int64_t Tpad, unsigned long long* err, cudaStream_t st);
+void launch_rolling_hash_batch(const uint32_t* windows, int64_t stride, const int32_t* lengths, const int32_t* orders,
+                               const uint64_t* bases,
+                               const uint64_t* moduli, int64_t count, uint64_t* out, int32_t* status,
+                               cudaStream_t st);
+// ids (u64 [T][B], global bucket ids) -> grow (branch-major storage rows); validates range.
+void launch_ids_to_rows(const Shape& s, const HashTables* ht, const uint64_t* ids, const uint32_t* tokens, int64_t T,
+                        int32_t* grow, int64_t Tpad, unsigned long long* err, cudaStream_t st);
+
+// ---- bank (bank.cu)
+void launch_synth_fill_bf16(__nv_bfloat16* dst, uint64_t seed, uint32_t table, int64_t row0, int64_t nrows, int ncols,
+                            int64_t pitch, float scale, cudaStream_t st);
+// W_cat[i][b*d + j] = synth(100+b, i, j)
+void launch_synth_wcat(__nv_bfloat16* wcat, uint64_t seed, int D, int d, int B, float scale, cudaStream_t st);
+void launch_f32_to_bf16(const float* src, __nv_bfloat16* dst, int64_t n, cudaStream_t st);
+// proj_b (D x d f32, dev) -> W_cat columns [b*d, (b+1)*d)
+void launch_pack_wcat(const float* proj_b, __nv_bfloat16* wcat, int D, int d, int b, cudaStream_t st);
+void launch_fill_f32(float* dst, float v, int64_t n, cudaStream_t st);
+
+// ---- forward
+struct FwdArgs {
+    Shape s;
+    const HashTables* ht;
+    const uint32_t* tokens;  // [T] base token per row (E0 row)
+    const int32_t* grow;     // [B][Tpad] storage rows
+    const __nv_bfloat16* sub;
+    const __nv_bfloat16* e0;
+    const __nv_bfloat16* wcat;
+    const float* ln_gain;
+    const float* ln_bias;
+    int64_t T, Tpad;     // rows of this call; grow row stride (>= round_up(T, 128))
+    void* rows_out;    // amplified, may be null
+    void* merged_out;  // pre-amplification, may be null
+    int out_bf16;
+    const unsigned long long* err;
+    // tensor maps (tensor-core path)
+    const CUtensorMap* tmap_sub;
+    const CUtensorMap* tmap_w;
+    // X (materialised gathered rows, T x D bf16) instead of sub-table gather, or null
+    const CUtensorMap* tmap_x;
+};
+// tcgen05 projection GEMM with fused gather + base add + scale + amplify (gemm_tc.cu).
+void launch_forward_tc(const FwdArgs& a, int num_sms, cudaStream_t st);
+// generic CUDA-core path: any shape, v1 and v2, reference float op order (simt.cu).
+void launch_forward_simt(const FwdArgs& a, cudaStream_t st);
+// LayerNorm amplification over merged rows (f32 merged -> rows) (simt.cu).
+// merged_copy (may be null): also write the merged rows in the output dtype.
+void launch_layernorm_rows(const Shape& s, const float* merged, const float* gain, const float* bias, void* rows,
+                           void* merged_copy, int out_bf16, int64_t T, const unsigned long long* err,
+                           cudaStream_t st);
+
+// ---- decode (decode.cu)
+// The hashing of a decode step / verify block is launch_hash_ids with prior = ring and
+// seq_off = {0, L, 2L, ...}; these kernels move the ring.  derr: decode error word
+// ((status << 32) | detail), ~0 when clear.
+void launch_decode_commit(const Shape& s, uint32_t* ring, uint64_t* length, uint32_t* last, const uint32_t* draft,
+                          int L, const int32_t* accept, int64_t batch, unsigned long long* err,
+                          unsigned long long* derr, cudaStream_t st);
+void launch_decode_reset(const Shape& s, uint32_t* ring, uint64_t* length, uint32_t* last, const uint32_t* prior,
+                         const uint64_t* lengths, int64_t batch, cudaStream_t st);
+
+// ---- multi-GPU (shard.cu)
+// For every (token, branch) of the all-gathered batch whose bucket row is local, copy
+// the row into X of the token's home rank (peer pointer) at [t_home][b*d .. b*d+d).
+void launch_shard_scatter(const Shape& s, const HashTables* ht, const int32_t* grow_all, int64_t Tpad_all,
+                          const int64_t* rank_token_offsets, int nranks, const __nv_bfloat16* sub,
+                          __nv_bfloat16* const* peer_x, int64_t T_all, const unsigned long long* err,
+                          cudaStream_t st);
+
+}  // namespace ngk

@@ -1,0 +1,399 @@
+"""Python mirror of the reference's hot-path API, backed by the C-ABI.
+
+Names and argument meaning follow proj/include/ngram/*.hpp so the parity tests read
+like the reference's own doctest suites:
+
+    reference (C++)                          here
+    ---------------------------------------  ------------------------------------------
+    make_default_config (config.cpp:163)     make_default_config
+    ngram_config::validate (config.cpp:32)   validate_config
+    rolling_hash (hashing.cpp:33)            rolling_hash / rolling_hash_batch
+    hash_all_orders (hashing.cpp:61)         hash_all_orders / hash_ids (batched)
+    embedding_bank_t (embedding.hpp:31)      DeviceBank (device-resident, bf16)
+    embed_from_ids (embedding.hpp:163)       embed_from_ids
+    embed_sequence(_cached) (:409-436)       embed_sequence / embed_sequence_cached (host
+                                             buffers) and embed_forward (device buffers)
+    sequence_cache (cache.hpp:38)            SequenceCache (one stream) / DecodeState (batch)
+    draft_verify (cache.cpp:152)             draft_verify / DecodeState.verify + commit
+
+Exceptions: InvalidArgument (std::invalid_argument), OutOfRange (std::out_of_range),
+IoError, ParseError, ConfigError -- see abi.py.  torch is used only to own device
+memory and streams; every computation is a CUDA kernel behind the C-ABI.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import abi
+from .abi import InvalidArgument, OutOfRange, check
+
+VARIANTS = {"averaged_v1": 0, "subtable_v2": 1}
+AMPS = {"none": 0, "scale_sqrt_d": 1, "layer_norm": 2}
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+# ----------------------------------------------------------------------------- config
+def make_default_config(base_vocab: int, dim: int, max_order: int = 4, sub_tables: int = 2) -> dict:
+    buf = C.create_string_buffer(1 << 16)
+    check(abi.lib().ngram_make_default_config(base_vocab, dim, max_order, sub_tables, buf, len(buf)))
+    return json.loads(buf.value)
+
+
+def validate_config(cfg: dict) -> None:
+    check(abi.lib().ngram_config_validate(json.dumps(cfg).encode()))
+
+
+def branch_count(cfg) -> int:
+    return 0 if cfg["max_order"] < 2 else (cfg["max_order"] - 1) * cfg["sub_tables"]
+
+
+def branch_dim(cfg) -> int:
+    B = branch_count(cfg)
+    return cfg["dim"] if (cfg["variant"] == "averaged_v1" or B == 0) else cfg["dim"] // B
+
+
+# ----------------------------------------------------------------------------- bank
+class DeviceBank:
+    """Device-resident embedding bank (bf16 tables, W_cat, E0)."""
+
+    def __init__(self, cfg: dict, device: int = 0, shard_rank: int = 0, shard_count: int = 1):
+        self.cfg = cfg
+        self.device = device
+        h = C.c_void_p()
+        check(abi.lib().ngram_bank_create(json.dumps(cfg).encode(), device, shard_rank, shard_count, C.byref(h)))
+        self.handle = h
+        self.info = abi.BankInfo()
+        check(abi.lib().ngram_bank_get_info(self.handle, C.byref(self.info)))
+        self.D = self.info.dim
+        self.B = self.info.branch_count
+        self.N = self.info.max_order
+
+    def close(self):
+        if self.handle:
+            abi.lib().ngram_bank_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def tensor_core_path(self) -> bool:
+        return bool(self.info.tensor_core_path)
+
+    def upload(self, base: np.ndarray, sub: Sequence[np.ndarray], proj: Sequence[np.ndarray] = (),
+               ln_gain: Optional[np.ndarray] = None, ln_bias: Optional[np.ndarray] = None) -> "DeviceBank":
+        """Upload a reference-layout float bank (make_bank / load_bank) from host memory."""
+        keep = [np.ascontiguousarray(a, np.float32) for a in [base] + list(sub) + list(proj)]
+        base_a, sub_a, proj_a = keep[0], keep[1:1 + len(sub)], keep[1 + len(sub):]
+        sp = (C.c_void_p * max(len(sub_a), 1))(*[a.ctypes.data for a in sub_a])
+        pp = (C.c_void_p * max(len(proj_a), 1))(*[a.ctypes.data for a in proj_a])
+        g = None if ln_gain is None else np.ascontiguousarray(ln_gain, np.float32)
+        b = None if ln_bias is None else np.ascontiguousarray(ln_bias, np.float32)
+        check(abi.lib().ngram_bank_upload_f32(self.handle, base_a.ctypes.data, sp, pp if proj_a else None,
+                                              None if g is None else g.ctypes.data,
+                                              None if b is None else b.ctypes.data))
+        return self
+
+    def generate(self, seed: int, stream=None) -> "DeviceBank":
+        """Synthetic counter-based bank, generated on the device (LongCat-scale)."""
+        check(abi.lib().ngram_bank_generate(self.handle, seed, _stream(stream)))
+        return self
+
+    def load_file(self, path: str) -> "DeviceBank":
+        check(abi.lib().ngram_bank_load_file(self.handle, path.encode()))
+        return self
+
+    def reserve(self, max_tokens: int) -> None:
+        check(abi.lib().ngram_bank_reserve(self.handle, max_tokens))
+
+    def sync_errors(self, stream=None) -> None:
+        check(abi.lib().ngram_sync_errors(self.handle, _stream(stream)))
+
+
+# ----------------------------------------------------------------------------- hashing
+def rolling_hash_batch(windows: torch.Tensor, orders: torch.Tensor, bases: torch.Tensor, moduli: torch.Tensor,
+                       lengths: Optional[torch.Tensor] = None, stream=None):
+    """Batched rolling_hash on device. windows: [count, stride] uint32 (int32 storage)."""
+    count, stride = windows.shape
+    out = torch.empty(count, dtype=torch.int64, device=windows.device)
+    status = torch.empty(count, dtype=torch.int32, device=windows.device)
+    check(abi.lib().ngram_rolling_hash_batch(_ptr(windows), stride, _ptr(lengths), _ptr(orders), _ptr(bases),
+                                             _ptr(moduli), count, _ptr(out), _ptr(status), _stream(stream)))
+    return out, status
+
+
+def rolling_hash(window: Sequence[int], spec: tuple, device: int = 0) -> int:
+    """rolling_hash(window, hash_spec{order, base, modulus}) with the reference's exceptions."""
+    order, base, modulus = spec
+    w = list(window)
+    dev = torch.device("cuda", device)
+    wt = torch.tensor([w + [0] * (max(len(w), 1) - len(w))], dtype=torch.int64).to(torch.int32).to(dev)
+    if len(w) == 0:
+        wt = torch.zeros((1, 1), dtype=torch.int32, device=dev)
+    lens = torch.tensor([len(w)], dtype=torch.int32, device=dev)
+    orders = torch.tensor([order], dtype=torch.int32, device=dev)
+    bases = torch.tensor([np.uint64(base).astype(np.int64)], dtype=torch.int64, device=dev)
+    mods = torch.tensor([np.uint64(modulus).astype(np.int64)], dtype=torch.int64, device=dev)
+    out, status = rolling_hash_batch(wt, orders, bases, mods, lens)
+    st = int(status.item())
+    if st == abi.NGRAM_EINVAL:
+        raise InvalidArgument("rolling_hash: invalid hash_spec or window length")
+    if st == abi.NGRAM_ERANGE:
+        raise OutOfRange("rolling_hash: token out of range for base vocabulary")
+    return int(np.int64(out.item()).astype(np.uint64))
+
+
+def hash_ids(bank: DeviceBank, tokens: torch.Tensor, seq_offsets: torch.Tensor, prior: Optional[torch.Tensor] = None,
+             u64: bool = True, stream=None) -> torch.Tensor:
+    """hash_all_orders at every position of a batch (device tensors). -> [T, B] ids."""
+    T = tokens.numel()
+    nseq = seq_offsets.numel() - 1
+    out = torch.empty((T, bank.B), dtype=torch.int64 if u64 else torch.int32, device=tokens.device)
+    check(abi.lib().ngram_hash_ids(bank.handle, _ptr(tokens), _ptr(seq_offsets), nseq, T, _ptr(prior), _ptr(out),
+                                   1 if u64 else 0, _stream(stream)))
+    return out
+
+
+def hash_all_orders(context: Sequence[int], bank: DeviceBank) -> list:
+    """hash_all_orders(context, cfg) for one N-token context (reference signature)."""
+    N = bank.N
+    if len(context) != N:
+        raise InvalidArgument(f"hash_all_orders: context length {len(context)} does not match max order {N}")
+    dev = torch.device("cuda", bank.device)
+    toks = torch.tensor([context[-1]], dtype=torch.int64).to(torch.int32).to(dev)
+    prior = torch.tensor([list(context[:-1])], dtype=torch.int64).to(torch.int32).to(dev) if N > 1 else None
+    off = torch.tensor([0, 1], dtype=torch.int64, device=dev)
+    ids = hash_ids(bank, toks, off, prior)
+    bank.sync_errors()
+    return [int(x) for x in ids[0].cpu().numpy().astype(np.uint64)]
+
+
+# ----------------------------------------------------------------------------- forward
+_DT = {torch.float32: abi.NGRAM_F32, torch.bfloat16: abi.NGRAM_BF16}
+
+
+def embed_forward(bank: DeviceBank, tokens: torch.Tensor, seq_offsets: torch.Tensor,
+                  prior: Optional[torch.Tensor] = None, rows: bool = True, merged: bool = False,
+                  out_dtype=torch.float32, stream=None, out_rows: Optional[torch.Tensor] = None,
+                  out_merged: Optional[torch.Tensor] = None):
+    """Batched embed_sequence_cached on device tensors. Returns (rows, merged) (None if not requested)."""
+    T = tokens.numel()
+    nseq = seq_offsets.numel() - 1
+    dev = tokens.device
+    if rows and out_rows is None:
+        out_rows = torch.empty((T, bank.D), dtype=out_dtype, device=dev)
+    if merged and out_merged is None:
+        out_merged = torch.empty((T, bank.D), dtype=out_dtype, device=dev)
+    check(abi.lib().ngram_embed_forward(bank.handle, _ptr(tokens), _ptr(seq_offsets), nseq, T, _ptr(prior),
+                                        _ptr(out_rows if rows else None), _ptr(out_merged if merged else None),
+                                        _DT[out_dtype], _stream(stream)))
+    return (out_rows if rows else None), (out_merged if merged else None)
+
+
+def embed_from_ids(bank: DeviceBank, tokens: torch.Tensor, ids: torch.Tensor, out_dtype=torch.float32,
+                   stream=None) -> torch.Tensor:
+    """embed_from_ids for T tokens (device): ids [T, B] int64 (u64 bits) -> merged [T, D]."""
+    T = tokens.numel()
+    out = torch.empty((T, bank.D), dtype=out_dtype, device=tokens.device)
+    check(abi.lib().ngram_embed_from_ids(bank.handle, _ptr(tokens), _ptr(ids), T, _ptr(out), _DT[out_dtype],
+                                         _stream(stream)))
+    return out
+
+
+def embed_sequence_cached(bank: DeviceBank, tokens: Sequence[int], prior_context: Sequence[int] = (),
+                          out_dtype=np.float32):
+    """embed_sequence_cached (host buffers in and out): (rows, merged), each len x D."""
+    return embed_batch_host(bank, [tokens], [prior_context], want_rows=True, want_merged=True, out_dtype=out_dtype)
+
+
+def embed_sequence(bank: DeviceBank, tokens: Sequence[int], prior_context: Sequence[int] = ()) -> np.ndarray:
+    return embed_batch_host(bank, [tokens], [prior_context], want_rows=True, want_merged=False)[0]
+
+
+def _prior_matrix(N1: int, priors) -> Optional[np.ndarray]:
+    if N1 <= 0 or priors is None or all(len(p) == 0 for p in priors):
+        return None
+    m = np.zeros((len(priors), N1), np.uint32)
+    for i, p in enumerate(priors):
+        tail = list(p)[-N1:]
+        if tail:
+            m[i, N1 - len(tail):] = np.asarray(tail, np.uint32)
+    return m
+
+
+def embed_batch_host(bank: DeviceBank, seqs, priors=None, want_rows=True, want_merged=False, out_dtype=np.float32,
+                     out_rows: Optional[np.ndarray] = None, out_merged: Optional[np.ndarray] = None):
+    """The host-buffer C-ABI entry (ngram_embed_sequence_host) over a list of sequences."""
+    lens = [len(s) for s in seqs]
+    off = np.zeros(len(seqs) + 1, np.int64)
+    off[1:] = np.cumsum(lens)
+    T = int(off[-1])
+    toks = np.ascontiguousarray(np.concatenate([np.asarray(s, np.uint32) for s in seqs]) if T else
+                                np.zeros(1, np.uint32))
+    pm = _prior_matrix(bank.N - 1, priors)
+    odt = abi.NGRAM_F32 if out_dtype == np.float32 else abi.NGRAM_BF16
+    npdt = np.float32 if odt == abi.NGRAM_F32 else np.uint16
+    rows = out_rows if out_rows is not None else (np.empty((T, bank.D), npdt) if want_rows else None)
+    merged = out_merged if out_merged is not None else (np.empty((T, bank.D), npdt) if want_merged else None)
+    check(abi.lib().ngram_embed_sequence_host(bank.handle, toks.ctypes.data, off.ctypes.data, len(seqs),
+                                              None if pm is None else pm.ctypes.data,
+                                              None if rows is None else rows.ctypes.data,
+                                              None if merged is None else merged.ctypes.data, odt))
+    return rows, merged
+
+
+# ----------------------------------------------------------------------------- decode
+class DecodeState:
+    """A batch of device-resident sequence_cache streams (cache.hpp:38-80)."""
+
+    def __init__(self, bank: DeviceBank, batch: int, max_draft: int = 8):
+        self.bank, self.batch, self.max_draft = bank, batch, max_draft
+        h = C.c_void_p()
+        check(abi.lib().ngram_decode_create(bank.handle, batch, max_draft, C.byref(h)))
+        self.handle = h
+        self.dev = torch.device("cuda", bank.device)
+
+    def close(self):
+        if self.handle:
+            abi.lib().ngram_decode_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def reset(self, prior: Optional[torch.Tensor] = None, lengths: Optional[torch.Tensor] = None, stream=None):
+        check(abi.lib().ngram_decode_reset(self.handle, _ptr(prior), _ptr(lengths), _stream(stream)))
+
+    def step(self, tokens: torch.Tensor, want_ids=True, want_merged=True, out_dtype=torch.float32, stream=None,
+             out: Optional[torch.Tensor] = None):
+        ids = torch.empty((self.batch, self.bank.B), dtype=torch.int64, device=self.dev) if want_ids else None
+        if want_merged and out is None:
+            out = torch.empty((self.batch, self.bank.D), dtype=out_dtype, device=self.dev)
+        check(abi.lib().ngram_decode_step(self.handle, _ptr(tokens), _ptr(ids), _ptr(out if want_merged else None),
+                                          _DT[out_dtype], _stream(stream)))
+        return ids, (out if want_merged else None)
+
+    def verify(self, draft: torch.Tensor, out_dtype=torch.float32, stream=None, out: Optional[torch.Tensor] = None):
+        L = draft.shape[1]
+        if out is None:
+            out = torch.empty((self.batch, L, self.bank.D), dtype=out_dtype, device=self.dev)
+        check(abi.lib().ngram_verify_block(self.handle, _ptr(draft), L, _ptr(out), _DT[out_dtype], _stream(stream)))
+        return out
+
+    def commit(self, draft: torch.Tensor, accept: torch.Tensor, stream=None):
+        check(abi.lib().ngram_commit(self.handle, _ptr(draft), draft.shape[1], _ptr(accept), _stream(stream)))
+
+    def state(self):
+        R = max(self.bank.N - 1, 0)
+        ring = np.zeros((self.batch, max(R, 1)), np.uint32)
+        length = np.zeros(self.batch, np.uint64)
+        last = np.zeros(self.batch, np.uint32)
+        check(abi.lib().ngram_decode_get_state(self.handle, ring.ctypes.data, length.ctypes.data, last.ctypes.data))
+        return ring[:, :R], length, last
+
+
+class SequenceCache:
+    """sequence_cache (cache.hpp:38-80) for one stream, state resident on the device.
+
+    snapshot/rollback/discard keep the reference's handle semantics (cache.cpp:59-96);
+    a snapshot is a copy of the device ring state."""
+
+    _uid = 0
+
+    def __init__(self, bank: DeviceBank, max_draft: int = 8):
+        self.bank = bank
+        self.st = DecodeState(bank, 1, max_draft)
+        SequenceCache._uid += 1
+        self.uid = SequenceCache._uid
+        self.snaps = []
+        self.next_serial = 1
+
+    def append(self, token: int) -> list:
+        if int(token) >= self.bank.info.base_vocab:
+            raise OutOfRange(f"sequence_cache: token {token} out of range")
+        t = torch.tensor([int(token)], dtype=torch.int64).to(torch.int32).to(self.st.dev)
+        ids, _ = self.st.step(t, want_ids=True, want_merged=False)
+        self.bank.sync_errors()
+        return [int(x) for x in ids[0].cpu().numpy().astype(np.uint64)]
+
+    def ring(self):
+        return self.st.state()[0][0]
+
+    def length(self) -> int:
+        return int(self.st.state()[1][0])
+
+    def last_token(self) -> int:
+        return int(self.st.state()[2][0])
+
+    def snapshot_depth(self) -> int:
+        return len(self.snaps)
+
+    def snapshot(self):
+        ring, length, last = self.st.state()
+        serial = self.next_serial
+        self.next_serial += 1
+        self.snaps.append((serial, ring.copy(), length.copy()))
+        return (self.uid, serial, len(self.snaps) - 1)
+
+    def _check(self, h):
+        owner, serial, slot = h
+        if owner != self.uid:
+            raise InvalidArgument("sequence_cache: handle belongs to another state")
+        if slot >= len(self.snaps) or self.snaps[slot][0] != serial:
+            raise InvalidArgument("sequence_cache: stale snapshot handle")
+
+    def rollback(self, h):
+        self._check(h)
+        _, ring, length = self.snaps[h[2]]
+        R = self.bank.N - 1
+        prior = torch.from_numpy(ring.astype(np.int64)).to(torch.int32).to(self.st.dev) if R > 0 else None
+        lens = torch.from_numpy(length.astype(np.int64)).to(self.st.dev)
+        self.st.reset(prior, lens)
+        del self.snaps[h[2] + 1:]
+
+    def discard(self, h):
+        self._check(h)
+        if h[2] + 1 != len(self.snaps):
+            raise InvalidArgument("sequence_cache: only the top snapshot can be discarded")
+        self.snaps.pop()
+
+
+def draft_verify(state: SequenceCache, bank: DeviceBank, draft: Sequence[int], accept_count: int) -> list:
+    """draft_verify (cache.cpp:152-195) for one stream: merged embeddings of the accepted prefix.
+
+    The verify block computes every draft position's embedding from ring ++ draft in one
+    batched call (the memo's warm-up), then commit() advances the state by accept_count."""
+    if accept_count > len(draft):
+        raise InvalidArgument("draft_verify: accept count exceeds draft length")
+    if len(draft) == 0:
+        return []
+    for t in draft:
+        if int(t) >= bank.info.base_vocab:
+            raise OutOfRange(f"sequence_cache: token {t} out of range")
+    d = torch.tensor([list(draft)], dtype=torch.int64).to(torch.int32).to(state.st.dev)
+    out = state.st.verify(d)
+    acc = torch.tensor([accept_count], dtype=torch.int32, device=state.st.dev)
+    state.st.commit(d, acc)
+    bank.sync_errors()
+    res = out[0, :accept_count].cpu().numpy()
+    return [res[i] for i in range(accept_count)]
