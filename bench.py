@@ -1,0 +1,376 @@
+#!/usr/bin/env python3
+"""bench.py -- N-gram Embedding forward throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload C|B|A]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU)
+
+A "step" is one pass of the hot path -- hash-index (K1) + gather/projection/epilogue
+(K2+K3) -- over one batch of synthetic tokens, inputs resident in HBM.  The headline
+workload is SURVEY.md 8(d) config C (LongCat-Flash-Lite-scale tables: V0=128000, N=4,
+K=4, D=3072, d=256, 31.46B sub-table params in bf16 + E0 + W_cat, prefill 8 x 8192
+tokens), tables generated on device by the counter-based generator (no checkpoint).
+
+Timing: W untimed warm-ups, then K steps, each bracketed by CUDA events on the launch
+stream; L2 is flushed (512 MiB write) between timed steps, outside the events.  With
+N > 1 the 8 sequences are split across ranks (strong scaling) and the step time is the
+max over ranks.  Stage times (K1 vs K2+K3) come from the library's own events
+(ngram_profile_*), recorded on the stream the kernels run on.
+
+One JSON line on rank 0.  `e2e` is the same metric through the host-buffer C-ABI entry
+(ngram_embed_sequence_host: tokens H2D, forward, embeddings D2H into pinned memory).
+`cpu_baseline` (rank 0, N=1) times the REFERENCE implementation (oracle/_ref, the
+unmodified reference sources) on this host's cores over a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return PEAKS_FALLBACK, "fallback"
+
+
+def workload(name: str):
+    """SURVEY.md 8(d) configs; returns (config dict, nseq, seq_len, label)."""
+    if name == "C":
+        sv = [(2 * (74 + b) + 1) * 64000 for b in range(12)]
+        cfg = {"max_order": 4, "sub_tables": 4, "base_vocab": 128000, "dim": 3072, "variant": "subtable_v2",
+               "amplification": "scale_sqrt_d",
+               "sub_vocab": [{"n": 2 + b // 4, "k": 1 + b % 4, "vocab": sv[b]} for b in range(12)]}
+        return cfg, 8, 8192, "longcat_flash_lite_prefill_8x8192"
+    from paper_2601_21204_b200 import ngram as G
+    if name == "B":
+        return G.make_default_config(128000, 768, 4, 4), 16, 4096, "mid_prefill_16x4096"
+    if name == "A":
+        return G.make_default_config(32000, 256, 3, 2), 4, 512, "toy_4x512"
+    raise SystemExit(f"unknown workload {name}")
+
+
+def param_count(cfg):
+    B = (cfg["max_order"] - 1) * cfg["sub_tables"]
+    d = cfg["dim"] // B
+    sub = sum(e["vocab"] for e in cfg["sub_vocab"]) * d
+    return cfg["base_vocab"] * cfg["dim"] + sub + cfg["dim"] * cfg["dim"], sub
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.samples, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- CPU (reference) leg
+def reference_cpu_rate(cfg_c, seconds: float, seq_len: int = 16, max_rounds: int | None = None):
+    """Reference embed_sequence<float> (oracle/_ref = unmodified reference sources) on this
+    host's cores, one sequence per std::thread, over a reduced-vocabulary bank with the
+    workload's D / N / K (the 127 GB fp32 LongCat bank cannot exist on the host; the
+    per-token cost is the D^2 projection, independent of vocabulary size)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O  # noqa: E402  (test/baseline infrastructure only)
+    if not O.ref_available():
+        return None
+    R = O.ref()
+    N, K, D = cfg_c["max_order"], cfg_c["sub_tables"], cfg_c["dim"]
+    buf = C.create_string_buffer(1 << 16)
+    R.ref_make_default_config_json(1000, D, N, K, buf, len(buf))
+    small = json.loads(buf.value)
+    small["amplification"] = cfg_c["amplification"]
+    h = R.ref_bank_create(json.dumps(small).encode(), 1234, 1)
+    cores = os.cpu_count() or 1
+    rng = np.random.default_rng(7)
+    nseq = cores
+    toks = rng.integers(0, 1000, size=nseq * seq_len, dtype=np.uint32)
+    off = np.arange(0, nseq * seq_len + 1, seq_len, dtype=np.int64)
+    out = np.zeros((nseq * seq_len, D), np.float32)
+    done, t0, rounds, times = 0, time.perf_counter(), 0, []
+    while True:
+        t1 = time.perf_counter()
+        rc = R.ref_embed_batch_mt(h, toks, off, nseq, cores, out)
+        times.append(time.perf_counter() - t1)
+        if rc:
+            raise RuntimeError("reference embed failed")
+        done += nseq * seq_len
+        rounds += 1
+        if (max_rounds and rounds >= max_rounds) or (not max_rounds and time.perf_counter() - t0 >= seconds):
+            break
+    el = time.perf_counter() - t0
+    R.ref_bank_destroy(h)
+    try:
+        model = subprocess.run(["bash", "-c", "lscpu | grep 'Model name' | head -1"], capture_output=True,
+                               text=True).stdout.split(":")[-1].strip()
+    except Exception:
+        model = "?"
+    return {"value": done / el, "cores": cores, "tokens": done, "seconds": el, "step_times": times,
+            "cpu_model": model,
+            "sample": f"{done} tokens of the workload's shape (D={D}, N={N}, K={K}) through the reference "
+                      f"embed_sequence<float>, {nseq} sequences x {seq_len} tokens per round, one std::thread per "
+                      f"sequence on {cores} host threads, reduced-vocabulary bank (V0=1000, default V_nk) -- "
+                      f"per-token cost is the D^2 projection (embedding.hpp:189-195)"}
+
+
+def run_reference(args):
+    cfg, nseq, seq_len, label = workload(args.workload)
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    # each step: one bounded sample (one round of cores x 16 tokens)
+    r = reference_cpu_rate(cfg, 0, seq_len=16, max_rounds=args.warmup + args.steps)
+    if r is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libngram_ref.so not built"}))
+        return
+    times = r["step_times"][args.warmup:]
+    toks_per_step = r["cores"] * 16
+    v = toks_per_step / (sum(times) / len(times))
+    line = {"metric": "ngram_embedding_tokens_per_sec", "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": label, "note": "CPU reference, bounded sample per step"},
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": r["cores"], "kind": "reference",
+                             "sample": r["sample"], "cpu_model": r["cpu_model"]},
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+# ----------------------------------------------------------------------------- GPU leg
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2601_21204_b200 import abi
+    from paper_2601_21204_b200 import ngram as G
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    cfg, nseq, seq_len, label = workload(args.workload)
+    if nseq % world != 0:
+        raise SystemExit(f"{nseq} sequences do not split over {world} ranks")
+    my_nseq = nseq // world
+    T = my_nseq * seq_len
+    total_tokens = nseq * seq_len
+    peaks, peak_src = load_peaks()
+
+    bank = G.DeviceBank(cfg, device=local)
+    bank.generate(1234)
+    bank.reserve(T)
+    rng = np.random.default_rng(42)
+    all_tokens = rng.integers(0, cfg["base_vocab"], size=total_tokens, dtype=np.int64).astype(np.int32)
+    toks = torch.from_numpy(all_tokens[rank * T:(rank + 1) * T].copy()).to(dev)
+    off = torch.arange(0, T + 1, seq_len, dtype=torch.int64, device=dev)
+    out_dtype = torch.bfloat16 if args.out_dtype == "bf16" else torch.float32
+    rows = torch.empty((T, bank.D), dtype=out_dtype, device=dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    abi.check(abi.lib().ngram_profile_enable(bank.handle, 1))
+
+    def step():
+        G.embed_forward(bank, toks, off, rows=True, merged=False, out_dtype=out_dtype, out_rows=rows)
+
+    for _ in range(args.warmup):
+        step()
+    bank.sync_errors()
+    torch.cuda.synchronize()
+
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    stage = np.zeros((args.steps, 2), np.float32)
+    sbuf = (C.c_float * 2)()
+    launches0 = abi.lib().ngram_kernel_launches()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.fill_(i & 0xff)  # > L2 (126 MB): every step starts cold
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+        abi.check(abi.lib().ngram_profile_read(bank.handle, sbuf, 2))
+        stage[i] = [sbuf[0], sbuf[1]]
+    torch.cuda.synchronize()
+    launches = abi.lib().ngram_kernel_launches() - launches0
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    bank.sync_errors()
+    step_ms = np.array([a.elapsed_time(b) for a, b in ev])
+    ms = float(step_ms.mean())
+    hash_ms = float(stage[:, 0].mean())
+    proj_ms = float(stage[:, 1].mean())
+    if world > 1:
+        t = torch.tensor([ms, hash_ms, proj_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, hash_ms, proj_ms = [float(x) for x in t.tolist()]
+
+    # ---------------------------------------------------------------- e2e (host buffers)
+    e2e = None
+    e2e_steps = max(2, min(args.steps, 5))
+    host_tok = torch.from_numpy(all_tokens[rank * T:(rank + 1) * T].copy()).pin_memory()
+    host_out = torch.empty((T, bank.D), dtype=out_dtype).pin_memory()
+    host_off = np.arange(0, T + 1, seq_len, dtype=np.int64)
+    odt = abi.NGRAM_BF16 if out_dtype == torch.bfloat16 else abi.NGRAM_F32
+
+    def e2e_step():
+        abi.check(abi.lib().ngram_embed_sequence_host(bank.handle, C.c_void_p(host_tok.data_ptr()),
+                                                      host_off.ctypes.data, my_nseq, None,
+                                                      C.c_void_p(host_out.data_ptr()), None, odt))
+
+    e2e_step()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    esz = 2 if out_dtype == torch.bfloat16 else 4
+    e2e = {"value": total_tokens / e2e_s, "unit": "tokens/s", "h2d_bytes_per_step": int(T * 4 + host_off.nbytes),
+           "d2h_bytes_per_step": int(T * bank.D * esz), "ms_per_step": e2e_s * 1e3,
+           "path": "ngram_embed_sequence_host (pinned host tokens -> HBM -> pinned host embeddings)"}
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # ---------------------------------------------------------------- roofline
+    D, B = cfg["dim"], (cfg["max_order"] - 1) * cfg["sub_tables"]
+    d = D // B
+    flops = 2.0 * T * D * D
+    tflops = flops / (proj_ms * 1e-3) / 1e12
+    # algorithmic HBM bytes of the fused forward: token + sub rows + E0 row + output
+    bytes_tok = 4 + 2 * B * d + 2 * D + esz * D
+    hbm_bytes = T * bytes_tok + 2 * D * D
+    hbm_gbs = hbm_bytes / (ms * 1e-3) / 1e9
+    hash_bytes = T * (4 + 4 * B)  # tokens in, storage rows out (u32 each)
+    nparams, nsub = param_count(cfg)
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            with open(tp) as f:
+                tj = json.load(f)
+            if tj.get("workload") == label and tj.get("T") == T:
+                traffic = tj.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": "ngram_embedding_tokens_per_sec", "value": total_tokens / (ms * 1e-3), "unit": "tokens/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (device-generated counter-based tables, uniform tokens seed 42)",
+        "config": {"workload": label, "V0": cfg["base_vocab"], "N": cfg["max_order"], "K": cfg["sub_tables"], "D": D,
+                   "d": d, "tokens": total_tokens, "sequences": nseq, "seq_len": seq_len,
+                   "embedding_params": nparams, "sub_table_params": nsub, "table_dtype": "bf16",
+                   "out_dtype": args.out_dtype, "amplification": cfg["amplification"],
+                   "sharding": "replica" if world > 1 else "single", "l2": "flushed (512 MiB write) between timed steps",
+                   "tensor_core_path": bank.tensor_core_path},
+        "roofline": {"bound": "tensor", "kernel": "forward_tc_kernel (K2 gather + K3 tcgen05 projection)",
+                     "achieved": tflops, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                     "frac": tflops / peaks["bf16_tflops"], "traffic": traffic, "peak_source": peak_src,
+                     "flops_per_launch": flops, "launch_ms": proj_ms},
+        "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": peaks["hbm_gbs"], "frac": hbm_gbs / peaks["hbm_gbs"],
+                "algorithmic_bytes_per_token": bytes_tok,
+                "hash_stage": {"ms": hash_ms, "gbs": hash_bytes / (hash_ms * 1e-3) / 1e9,
+                               "frac": hash_bytes / (hash_ms * 1e-3) / 1e9 / peaks["hbm_gbs"]}},
+        "stages_ms": {"hash_index": hash_ms, "gather_projection_epilogue": proj_ms},
+        "clocks": clocks, "e2e": e2e, "gpu_launches": int(launches),
+    }
+    if world == 1 and not args.no_cpu:
+        r = reference_cpu_rate(cfg, args.cpu_seconds)
+        if r is not None:
+            line["cpu_baseline"] = {"value": r["value"], "unit": "tokens/s", "cores": r["cores"], "kind": "reference",
+                                    "sample": r["sample"], "cpu_model": r["cpu_model"]}
+    print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="C")
+    ap.add_argument("--out-dtype", choices=["fp32", "bf16"], default="fp32")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -141,6 +141,13 @@ int ngram_sync_errors(ngram_bank* bank, void* stream);
 int ngram_embed_sequence_host(ngram_bank* bank, const uint32_t* tokens, const int64_t* seq_offsets, int64_t nseq,
                               const uint32_t* prior, void* rows_out, void* merged_out, int out_dtype);
 
+/* Stage profiling: when enabled, every forward records CUDA events on its launch stream
+ * around K1 (hash-index) and K2+K3 (gather + projection [+ LayerNorm]).
+ * ngram_profile_read synchronises on the last event and returns the stage times (ms)
+ * of the most recent forward: stage_ms[0] = hash, stage_ms[1] = projection. */
+int ngram_profile_enable(ngram_bank* bank, int enable);
+int ngram_profile_read(ngram_bank* bank, float* stage_ms, int n);
+
 /* ------------------------------------------------------------------ decode / verify */
 /* A batch of `batch` decode streams (sequence_cache, cache.hpp:38-80): per-stream ring
  * of the trailing N-1 confirmed tokens (zero-initialised), length and last token,

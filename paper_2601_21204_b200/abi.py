@@ -23,7 +23,7 @@ SYMBOLS = [
     "ngram_make_default_config", "ngram_bank_create", "ngram_bank_destroy", "ngram_bank_upload_f32",
     "ngram_bank_generate", "ngram_bank_load_file", "ngram_bank_reserve", "ngram_bank_get_info",
     "ngram_rolling_hash_batch", "ngram_hash_ids", "ngram_embed_forward", "ngram_embed_from_ids", "ngram_sync_errors",
-    "ngram_embed_sequence_host", "ngram_decode_create", "ngram_decode_destroy", "ngram_decode_reset",
+    "ngram_embed_sequence_host", "ngram_profile_enable", "ngram_profile_read", "ngram_decode_create", "ngram_decode_destroy", "ngram_decode_reset",
     "ngram_decode_step", "ngram_verify_block", "ngram_commit", "ngram_decode_get_state",
     "ngram_shard_group_create", "ngram_shard_group_destroy", "ngram_shard_export", "ngram_shard_open",
     "ngram_shard_scatter_rows", "ngram_shard_project",
@@ -108,6 +108,8 @@ def lib() -> C.CDLL:
         "ngram_embed_from_ids": ([vp, vp, vp, i64, vp, i32, vp], i32),
         "ngram_sync_errors": ([vp, vp], i32),
         "ngram_embed_sequence_host": ([vp, vp, vp, i64, vp, vp, vp, i32], i32),
+        "ngram_profile_enable": ([vp, i32], i32),
+        "ngram_profile_read": ([vp, C.POINTER(C.c_float), i32], i32),
         "ngram_decode_create": ([vp, i64, i32, C.POINTER(vp)], i32),
         "ngram_decode_destroy": ([vp], i32),
         "ngram_decode_reset": ([vp, vp, vp, vp], i32),

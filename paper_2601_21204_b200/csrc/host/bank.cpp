@@ -88,6 +88,8 @@ uint64_t ngram_bank::device_bytes() const {
 
 ngram_bank::~ngram_bank() {
     DeviceGuard g(device);
+    for (auto& e : prof_ev)
+        if (e) cudaEventDestroy(e);
     for (int i = 0; i < 2; ++i) {
         if (host_streams[i]) cudaStreamDestroy(host_streams[i]);
         if (pinned[i]) cudaFreeHost(pinned[i]);
@@ -274,6 +276,26 @@ int ngram_bank_generate(ngram_bank* b, uint64_t seed, void* stream) {
     }
     if (b->cfg.variant == 1 && B > 0) ngk::launch_synth_wcat(b->wcat.p, seed, D, d, B, s_proj, st);
     NGH_CUDA(cudaGetLastError());
+    NGRAM_API_END
+}
+
+int ngram_profile_enable(ngram_bank* b, int enable) {
+    NGRAM_API_BEGIN
+    if (!b) throw Error(NGRAM_EINVAL, "null bank");
+    DeviceGuard g(b->device);
+    if (enable && !b->prof_ev[0])
+        for (auto& e : b->prof_ev) NGH_CUDA(cudaEventCreate(&e));
+    b->prof = enable != 0;
+    NGRAM_API_END
+}
+
+int ngram_profile_read(ngram_bank* b, float* stage_ms, int n) {
+    NGRAM_API_BEGIN
+    if (!b || !stage_ms || n < 2 || !b->prof_ev[0]) throw Error(NGRAM_EINVAL, "ngram_profile_read: not enabled");
+    DeviceGuard g(b->device);
+    NGH_CUDA(cudaEventSynchronize(b->prof_ev[2]));
+    NGH_CUDA(cudaEventElapsedTime(&stage_ms[0], b->prof_ev[0], b->prof_ev[1]));
+    NGH_CUDA(cudaEventElapsedTime(&stage_ms[1], b->prof_ev[1], b->prof_ev[2]));
     NGRAM_API_END
 }
 

@@ -93,6 +93,13 @@ struct ngram_bank {
     void* pinned[2] = {nullptr, nullptr};
     size_t pinned_bytes = 0;
 
+    // stage profiling (ngram_profile_enable)
+    bool prof = false;
+    cudaEvent_t prof_ev[3] = {nullptr, nullptr, nullptr};
+    void prof_record(int i, cudaStream_t st) {
+        if (prof) cudaEventRecord(prof_ev[i], st);
+    }
+
     uint64_t device_bytes() const;
     ~ngram_bank();
 };

@@ -140,10 +140,13 @@ int ngram_embed_forward(ngram_bank* b, const uint32_t* tokens, const int64_t* se
     const int64_t Tpad = round_up(std::max<int64_t>(total_tokens, 1), 128);
     reset_error_word(b, st);
     if (total_tokens == 0) return NGRAM_OK;
+    b->prof_record(0, st);
     ngk::launch_hash_ids(b->shape, b->ht.p, tokens, seq_offsets, nseq, total_tokens, prior, nullptr, 0, b->ws.grow.p,
                          Tpad, b->err.p, st);
+    b->prof_record(1, st);
     run_projection(b, tokens, b->ws.grow.p, Tpad, total_tokens, rows_out, merged_out, out_dtype == NGRAM_BF16,
                    b->ws.merged_f32.p, nullptr, st, -1);
+    b->prof_record(2, st);
     NGRAM_API_END
 }
 
