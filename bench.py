@@ -236,8 +236,8 @@ def run_ours(args):
     clk.start()
     time.sleep(0.3)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    stage = np.zeros((args.steps, 2), np.float32)
-    sbuf = (C.c_float * 2)()
+    stage = np.zeros((args.steps, 3), np.float32)
+    sbuf = (C.c_float * 3)()
     launches0 = abi.lib().ngram_kernel_launches()
     if world > 1:
         dist.barrier()
@@ -247,8 +247,8 @@ def run_ours(args):
         ev[i][0].record(stream)
         step()
         ev[i][1].record(stream)
-        abi.check(abi.lib().ngram_profile_read(bank.handle, sbuf, 2))
-        stage[i] = [sbuf[0], sbuf[1]]
+        abi.check(abi.lib().ngram_profile_read(bank.handle, sbuf, 3))
+        stage[i] = [sbuf[0], sbuf[1], sbuf[2]]
     torch.cuda.synchronize()
     launches = abi.lib().ngram_kernel_launches() - launches0
     if world > 1:
@@ -258,11 +258,12 @@ def run_ours(args):
     step_ms = np.array([a.elapsed_time(b) for a, b in ev])
     ms = float(step_ms.mean())
     hash_ms = float(stage[:, 0].mean())
-    proj_ms = float(stage[:, 1].mean())
+    gather_ms = float(stage[:, 1].mean())
+    proj_ms = float(stage[:, 2].mean())
     if world > 1:
-        t = torch.tensor([ms, hash_ms, proj_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms, hash_ms, gather_ms, proj_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, hash_ms, proj_ms = [float(x) for x in t.tolist()]
+        ms, hash_ms, gather_ms, proj_ms = [float(x) for x in t.tolist()]
 
     # ---------------------------------------------------------------- e2e (host buffers)
     e2e = None
@@ -309,6 +310,7 @@ def run_ours(args):
     hbm_bytes = T * bytes_tok + 2 * D * D
     hbm_gbs = hbm_bytes / (ms * 1e-3) / 1e9
     hash_bytes = T * (4 + 4 * B)  # tokens in, storage rows out (u32 each)
+    gather_bytes = T * (4 * B + 2 * B * d + 2 * D)  # storage rows in, sub rows in, X out
     nparams, nsub = param_count(cfg)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -331,15 +333,17 @@ def run_ours(args):
                    "out_dtype": args.out_dtype, "amplification": cfg["amplification"],
                    "sharding": "replica" if world > 1 else "single", "l2": "flushed (512 MiB write) between timed steps",
                    "tensor_core_path": bank.tensor_core_path},
-        "roofline": {"bound": "tensor", "kernel": "forward_tc_kernel (K2 gather + K3 tcgen05 projection)",
+        "roofline": {"bound": "tensor", "kernel": "forward_tc2_kernel (K3: tcgen05 cta_group::2 projection + base/scale/amplify epilogue)",
                      "achieved": tflops, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
                      "frac": tflops / peaks["bf16_tflops"], "traffic": traffic, "peak_source": peak_src,
                      "flops_per_launch": flops, "launch_ms": proj_ms},
         "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": peaks["hbm_gbs"], "frac": hbm_gbs / peaks["hbm_gbs"],
                 "algorithmic_bytes_per_token": bytes_tok,
                 "hash_stage": {"ms": hash_ms, "gbs": hash_bytes / (hash_ms * 1e-3) / 1e9,
-                               "frac": hash_bytes / (hash_ms * 1e-3) / 1e9 / peaks["hbm_gbs"]}},
-        "stages_ms": {"hash_index": hash_ms, "gather_projection_epilogue": proj_ms},
+                               "frac": hash_bytes / (hash_ms * 1e-3) / 1e9 / peaks["hbm_gbs"]},
+                "gather_stage": {"ms": gather_ms, "gbs": gather_bytes / max(gather_ms, 1e-9) / 1e6,
+                                 "frac": gather_bytes / max(gather_ms, 1e-9) / 1e6 / peaks["hbm_gbs"]}},
+        "stages_ms": {"k1_hash_index": hash_ms, "k2_gather": gather_ms, "k3_projection_epilogue": proj_ms},
         "clocks": clocks, "e2e": e2e, "gpu_launches": int(launches),
     }
     if world == 1 and not args.no_cpu:

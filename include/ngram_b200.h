@@ -144,7 +144,7 @@ int ngram_embed_sequence_host(ngram_bank* bank, const uint32_t* tokens, const in
 /* Stage profiling: when enabled, every forward records CUDA events on its launch stream
  * around K1 (hash-index) and K2+K3 (gather + projection [+ LayerNorm]).
  * ngram_profile_read synchronises on the last event and returns the stage times (ms)
- * of the most recent forward: stage_ms[0] = hash, stage_ms[1] = projection. */
+ * of the most recent forward: stage_ms[0] = hash, stage_ms[1] = gather (K2), stage_ms[2] = projection (K3). */
 int ngram_profile_enable(ngram_bank* bank, int enable);
 int ngram_profile_read(ngram_bank* bank, float* stage_ms, int n);
 

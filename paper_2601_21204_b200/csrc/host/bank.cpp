@@ -70,11 +70,19 @@ void make_tensor_map_2d(CUtensorMap* map, const void* base, uint64_t inner, uint
     if (r != CUDA_SUCCESS) throw Error(NGRAM_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
 }
 
+void XBuf::ensure(int64_t nrows, int D) {
+    if (nrows <= rows) return;
+    x.alloc(size_t(nrows) * size_t(D));
+    make_tensor_map_2d(&map, x.p, uint64_t(D), uint64_t(nrows), uint64_t(D) * 2, 64, 128);
+    rows = nrows;
+}
+
 void ensure_workspace(ngram_bank* b, int64_t T) {
     if (T <= b->ws.tokens_cap) return;
-    const int64_t Tpad = round_up(std::max<int64_t>(T, 1), 128);
+    const int64_t Tpad = round_up(std::max<int64_t>(T, 1), kRowPad);
     b->ws.grow.ensure(size_t(std::max(b->shape.B, 1)) * size_t(Tpad));
     if (b->cfg.amp == 2) b->ws.merged_f32.ensure(size_t(Tpad) * size_t(b->cfg.dim));
+    if (b->tc_path) b->ws.xbuf.ensure(Tpad, b->cfg.dim);
     b->ws.tokens_cap = Tpad;
 }
 
@@ -179,6 +187,7 @@ int ngram_bank_create(const char* config_json, int device, int shard_rank, int s
                            uint64_t(d) * 2, 64, 1);
         make_tensor_map_2d(&b->tmap_w, b->wcat.p, uint64_t(D), uint64_t(D), uint64_t(D) * 2, 64,
                            D % 256 == 0 ? 256 : 128);
+        make_tensor_map_2d(&b->tmap_w2, b->wcat.p, uint64_t(D), uint64_t(D), uint64_t(D) * 2, 64, 128);
     }
     NGH_CUDA(cudaDeviceSynchronize());
     *out = b.release();
@@ -293,9 +302,10 @@ int ngram_profile_read(ngram_bank* b, float* stage_ms, int n) {
     NGRAM_API_BEGIN
     if (!b || !stage_ms || n < 2 || !b->prof_ev[0]) throw Error(NGRAM_EINVAL, "ngram_profile_read: not enabled");
     DeviceGuard g(b->device);
-    NGH_CUDA(cudaEventSynchronize(b->prof_ev[2]));
+    NGH_CUDA(cudaEventSynchronize(b->prof_ev[3]));
     NGH_CUDA(cudaEventElapsedTime(&stage_ms[0], b->prof_ev[0], b->prof_ev[1]));
     NGH_CUDA(cudaEventElapsedTime(&stage_ms[1], b->prof_ev[1], b->prof_ev[2]));
+    if (n >= 3) NGH_CUDA(cudaEventElapsedTime(&stage_ms[2], b->prof_ev[2], b->prof_ev[3]));
     NGRAM_API_END
 }
 

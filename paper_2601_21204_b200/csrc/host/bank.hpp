@@ -55,6 +55,14 @@ struct DevBuf {
     }
 };
 
+// A materialised X buffer (T x D bf16) with its TMA descriptor (box 64 x 128 rows).
+struct XBuf {
+    DevBuf<__nv_bfloat16> x;
+    CUtensorMap map{};
+    int64_t rows = 0;
+    void ensure(int64_t nrows, int D);
+};
+
 struct Workspace {
     int64_t tokens_cap = 0;
     DevBuf<int32_t> grow;           // [B][Tpad]
@@ -62,6 +70,7 @@ struct Workspace {
     DevBuf<uint32_t> tokens;        // host-API staging / decode tokens
     DevBuf<int64_t> offsets;
     DevBuf<uint32_t> prior;
+    XBuf xbuf;                      // K2 output / K3 A operand
 };
 
 }  // namespace ngh
@@ -81,7 +90,7 @@ struct ngram_bank {
     ngh::DevBuf<ngk::HashTables> ht;
     ngh::DevBuf<unsigned long long> err;
 
-    CUtensorMap tmap_sub{}, tmap_w{};
+    CUtensorMap tmap_sub{}, tmap_w{}, tmap_w2{};
     ngh::Workspace ws;
 
     // host-buffer pipeline (ngram_embed_sequence_host)
@@ -90,12 +99,13 @@ struct ngram_bank {
     ngh::DevBuf<uint8_t> host_merged[2];
     ngh::DevBuf<int64_t> host_off[2];
     ngh::DevBuf<uint32_t> host_prior[2];
+    ngh::XBuf host_x[2];
     void* pinned[2] = {nullptr, nullptr};
     size_t pinned_bytes = 0;
 
     // stage profiling (ngram_profile_enable)
     bool prof = false;
-    cudaEvent_t prof_ev[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t prof_ev[4] = {nullptr, nullptr, nullptr, nullptr};
     void prof_record(int i, cudaStream_t st) {
         if (prof) cudaEventRecord(prof_ev[i], st);
     }
@@ -114,6 +124,7 @@ struct ngram_decode {
     ngh::DevBuf<int64_t> seq_off;           // [max_draft][batch+1] = s * L
     ngh::DevBuf<int32_t> grow;              // [B][round_up(batch*max_draft, 128)]
     ngh::DevBuf<unsigned long long> derr;   // decode error word
+    ngh::XBuf xbuf;                         // gathered block rows
 };
 
 namespace ngh {
@@ -122,4 +133,6 @@ void make_tensor_map_2d(CUtensorMap* map, const void* base, uint64_t inner, uint
                         uint32_t box_inner, uint32_t box_rows);
 void ensure_workspace(ngram_bank* b, int64_t T);
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+// Row padding of every per-token workspace: the 2-CTA GEMM tile is 256 tokens.
+constexpr int64_t kRowPad = 256;
 }  // namespace ngh

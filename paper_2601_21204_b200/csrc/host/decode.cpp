@@ -12,7 +12,7 @@
 namespace ngh {
 void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, int64_t gstride, int64_t T,
                     void* rows, void* merged, int out_bf16, float* ln_scratch, const CUtensorMap* tmap_x,
-                    cudaStream_t st, int amp);
+                    cudaStream_t st, int amp, XBuf* xb);
 void reset_error_word(ngram_bank* b, cudaStream_t st);
 }  // namespace ngh
 
@@ -25,14 +25,14 @@ void decode_block(ngram_decode* d, const uint32_t* draft, int L, uint64_t* ids_o
                   cudaStream_t st) {
     ngram_bank* b = d->bank;
     const int64_t T = d->batch * L;
-    const int64_t Tpad = round_up(T, 128);
+    const int64_t Tpad = round_up(T, kRowPad);
     reset_error_word(b, st);
     const int R = b->cfg.max_order - 1;
     ngk::launch_hash_ids(b->shape, b->ht.p, draft, d->seq_off.p + size_t(L - 1) * size_t(d->batch + 1), d->batch, T,
                          R > 0 ? d->ring.p : nullptr, ids_out, 1, d->grow.p, Tpad, b->err.p, st);
     if (merged_out)
         run_projection(b, draft, d->grow.p, Tpad, T, nullptr, merged_out, out_dtype == NGRAM_BF16, nullptr, nullptr,
-                       st, 0);
+                       st, 0, &d->xbuf);
 }
 
 }  // namespace
@@ -54,7 +54,7 @@ int ngram_decode_create(ngram_bank* b, int64_t batch, int max_draft, ngram_decod
     d->length.alloc(size_t(batch));
     d->last.alloc(size_t(batch));
     const int64_t Tmax = batch * max_draft;
-    d->grow.alloc(size_t(std::max(b->shape.B, 1)) * size_t(round_up(Tmax, 128)));
+    d->grow.alloc(size_t(std::max(b->shape.B, 1)) * size_t(round_up(Tmax, kRowPad)));
     d->derr.alloc(1);
     // per-L sequence offsets {0, L, 2L, ..., batch*L} for L = 1..max_draft
     std::vector<int64_t> off(size_t(max_draft) * size_t(batch + 1));

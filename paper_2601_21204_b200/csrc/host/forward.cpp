@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -28,11 +29,24 @@ static void check_offsets(const int64_t* off, int64_t nseq, int64_t T) {
         if (off[i + 1] < off[i]) throw Error(NGRAM_EINVAL, "seq_offsets must be non-decreasing");
 }
 
+// Fused gather (TMA gather4 straight into the GEMM's smem) vs K2 -> X -> K3.  Measured on
+// B200: fused wins when the GEMM is short in K (D <= 1024: the epilogue
+// dominates and X's HBM round trip does not pay), X wins for LongCat-scale D (the
+// gather4 stream cannot keep 512-cycle K-blocks fed).  NGRAM_FUSED_GATHER=0/1 overrides.
+static bool fused_gather(int D) {
+    static const int env = [] {
+        const char* e = getenv("NGRAM_FUSED_GATHER");
+        return e ? atoi(e) : -1;
+    }();
+    return env >= 0 ? env != 0 : D <= 1024;
+}
+
 // One forward over T rows whose storage rows are already in `grow` (stride gstride).
-// Writes merged/rows per the bank's amplification; LayerNorm via a second kernel.
+// Tensor-core path: K2 gathers X (T x D bf16) into `xb`, K3 projects it.  Writes
+// merged/rows per the amplification; LayerNorm via a third kernel.
 void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, int64_t gstride, int64_t T,
                     void* rows, void* merged, int out_bf16, float* ln_scratch, const CUtensorMap* tmap_x,
-                    cudaStream_t st, int amp) {
+                    cudaStream_t st, int amp, XBuf* xb) {
     if (T <= 0) return;
     ngk::FwdArgs a{};
     a.s = b->shape;
@@ -50,6 +64,7 @@ void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, 
     a.err = b->err.p;
     a.tmap_sub = &b->tmap_sub;
     a.tmap_w = &b->tmap_w;
+    a.tmap_w2 = &b->tmap_w2;
     a.tmap_x = tmap_x;
     const bool ln = a.s.amp == 2;
     float* ln_merged = nullptr;
@@ -63,6 +78,13 @@ void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, 
         a.rows_out = rows;
         a.out_bf16 = out_bf16;
     }
+    if (b->tc_path && !tmap_x && !fused_gather(b->shape.D)) {
+        if (!xb) xb = &b->ws.xbuf;
+        xb->ensure(round_up(T, kRowPad), b->shape.D);
+        ngk::launch_gather_rows(a.s, grow, gstride, T, b->sub.p, xb->x.p, b->err.p, st);
+        a.tmap_x = &xb->map;
+    }
+    b->prof_record(2, st);
     if (b->tc_path) ngk::launch_forward_tc(a, b->num_sms, st);
     else ngk::launch_forward_simt(a, st);
     if (ln)
@@ -137,7 +159,7 @@ int ngram_embed_forward(ngram_bank* b, const uint32_t* tokens, const int64_t* se
     DeviceGuard g(b->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     ensure_workspace(b, total_tokens);
-    const int64_t Tpad = round_up(std::max<int64_t>(total_tokens, 1), 128);
+    const int64_t Tpad = round_up(std::max<int64_t>(total_tokens, 1), kRowPad);
     reset_error_word(b, st);
     if (total_tokens == 0) return NGRAM_OK;
     b->prof_record(0, st);
@@ -145,8 +167,8 @@ int ngram_embed_forward(ngram_bank* b, const uint32_t* tokens, const int64_t* se
                          Tpad, b->err.p, st);
     b->prof_record(1, st);
     run_projection(b, tokens, b->ws.grow.p, Tpad, total_tokens, rows_out, merged_out, out_dtype == NGRAM_BF16,
-                   b->ws.merged_f32.p, nullptr, st, -1);
-    b->prof_record(2, st);
+                   b->ws.merged_f32.p, nullptr, st, -1, nullptr);
+    b->prof_record(3, st);
     NGRAM_API_END
 }
 
@@ -158,13 +180,13 @@ int ngram_embed_from_ids(ngram_bank* b, const uint32_t* tokens, const uint64_t* 
     DeviceGuard g(b->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     ensure_workspace(b, T);
-    const int64_t Tpad = round_up(std::max<int64_t>(T, 1), 128);
+    const int64_t Tpad = round_up(std::max<int64_t>(T, 1), kRowPad);
     reset_error_word(b, st);
     if (T == 0) return NGRAM_OK;
     ngk::launch_ids_to_rows(b->shape, b->ht.p, ids, tokens, T, b->ws.grow.p, Tpad, b->err.p, st);
     // embed_from_ids returns the merged (pre-amplification) vector: run with amp = none.
     run_projection(b, tokens, b->ws.grow.p, Tpad, T, nullptr, merged_out, out_dtype == NGRAM_BF16, nullptr, nullptr,
-                   st, 0);
+                   st, 0, nullptr);
     NGRAM_API_END
 }
 
@@ -199,7 +221,7 @@ int ngram_embed_sequence_host(ngram_bank* b, const uint32_t* tokens, const int64
     cudaStream_t s0 = b->host_streams[0], s1 = b->host_streams[1];
     const int N1 = std::max(b->cfg.max_order - 1, 0);
     ensure_workspace(b, T);
-    const int64_t Tpad = round_up(std::max<int64_t>(T, 1), 128);
+    const int64_t Tpad = round_up(std::max<int64_t>(T, 1), kRowPad);
     b->ws.tokens.ensure(size_t(std::max<int64_t>(T, 1)));
     b->ws.offsets.ensure(size_t(nseq + 1));
     if (prior && N1 > 0) b->ws.prior.ensure(size_t(nseq) * size_t(N1));
@@ -275,7 +297,8 @@ int ngram_embed_sequence_host(ngram_bank* b, const uint32_t* tokens, const int64
         void* drows = rows_out ? b->host_out[slot].p : nullptr;
         void* dmerged = merged_out ? b->host_merged[slot].p : nullptr;
         run_projection(b, b->ws.tokens.p + c0, b->ws.grow.p + c0, Tpad, n, drows, dmerged, out_dtype == NGRAM_BF16,
-                       b->ws.merged_f32.p ? b->ws.merged_f32.p + size_t(c0) * size_t(D) : nullptr, nullptr, st, -1);
+                       b->ws.merged_f32.p ? b->ws.merged_f32.p + size_t(c0) * size_t(D) : nullptr, nullptr, st, -1,
+                       &b->host_x[slot]);
         const size_t bytes = size_t(n) * size_t(D) * esz;
         if (direct) {
             if (rows_out)

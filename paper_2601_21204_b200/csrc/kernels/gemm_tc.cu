@@ -9,18 +9,22 @@
 // embedding.hpp:189-195) becomes ONE bf16 GEMM with K = (N-1)K*d = D (branch-
 // concatenated), fp32 accumulation in TMEM.
 //
-// Structure (persistent, 1 CTA per SM, 6 warps, warp-specialised):
-//   warp 0      TMA producer.  Per K-block (64 columns = one 128-B swizzle atom): the 32
-//               lanes each issue one tile::gather4 (4 gathered rows of the sub-table, row
-//               coordinate = storage row of bucket id_b(t)) -> A tile 128 x 64; lane 0
-//               issues the W_cat tile 256 x 64.  Both land SWIZZLE_128B, K-major.
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN, K=16).
-//   warps 2..5  epilogue: tcgen05.ld accumulator rows -> + E0 row -> * 1/denom -> * amp
-//               -> fp32/bf16 stores.  TMEM is double-buffered (2 x BN columns) so the
-//               epilogue of tile i overlaps the MMAs of tile i+1.
+// Structure (persistent, 1 CTA per SM, warp-specialised):
+//   warps 0..NP-1   A producers, 32 tile rows each.  Per K-block (64 columns = one 128-B
+//                   swizzle atom) every producer warp moves its 32 gathered rows of the
+//                   sub-table into the SWIZZLE_128B K-major A tile, either with
+//                   TMA tile::gather4 (MODE 0: 8 instructions of 4 rows) or with cp.async
+//                   16-B copies placed at their swizzled addresses (MODE 1: 8 per lane,
+//                   retired LAG K-blocks later with a proxy fence + mbarrier arrive).
+//                   Warp 0 / lane 0 also TMA-loads the W_cat tile (BN x 64).
+//   warp NP         TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN, K=16).
+//   warps NP+1..+4  epilogue: tcgen05.ld accumulator rows -> + E0 row -> * 1/denom -> * amp
+//                   -> fp32/bf16 stores.  TMEM is double-buffered (2 x BN columns) so the
+//                   epilogue of tile i overlaps the MMAs of tile i+1.
 // Tiles are ordered n-fastest so the CTAs running concurrently share an m-block's
-// gathered rows through L2; W_cat (2*D^2 bytes) stays L2-resident.
+// gathered rows through L2; W_cat (2*D^2 bytes) stays L2-resident (evict_last).
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.h"
 #include "ptx.cuh"
@@ -32,21 +36,26 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 64;  // one SWIZZLE_128B atom of bf16
 constexpr int kStages = 4;
-constexpr int kThreads = 192;
+constexpr int kLag = 2;  // cp.async mode: K-blocks in flight per producer warp before retiring
 
-template <int BN>
+template <int BN, int NP>
 struct Cfg {
     static constexpr int kABytes = BM * BK * 2;
     static constexpr int kBBytes = BN * BK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
     static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int kMmaWarp = NP;
+    static constexpr int kEpiWarp0 = NP + 1;
+    static constexpr int kThreads = (NP + 5) * 32;
+    static constexpr int kRowsPerWarp = BM / NP;
 };
 
 struct TcParams {
     Shape s;
     const uint32_t* tokens;
     const int32_t* grow;
+    const __nv_bfloat16* sub;
     const __nv_bfloat16* e0;
     void* rows_out;
     void* merged_out;
@@ -56,13 +65,28 @@ struct TcParams {
     float scale, amp;
     const unsigned long long* err;
     int use_x;  // A operand from materialised X (tmap_a is X) instead of gathered sub-table rows
+    int epi_skip;  // diagnostics only (NGRAM_DEBUG_EPI_SKIP): drain TMEM without loads/stores
 };
 
-template <int BN>
-__global__ void __launch_bounds__(kThreads, 1)
+__device__ __forceinline__ void store_chunk(void* out, int out_bf16, int64_t o, const float (&mv)[32]) {
+    if (out_bf16) {
+        uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(out) + o);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            dst[i] = make_uint4(pack_bf16x2(mv[8 * i], mv[8 * i + 1]), pack_bf16x2(mv[8 * i + 2], mv[8 * i + 3]),
+                                pack_bf16x2(mv[8 * i + 4], mv[8 * i + 5]), pack_bf16x2(mv[8 * i + 6], mv[8 * i + 7]));
+    } else {
+        float4* dst = reinterpret_cast<float4*>(static_cast<float*>(out) + o);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dst[i] = make_float4(mv[4 * i], mv[4 * i + 1], mv[4 * i + 2], mv[4 * i + 3]);
+    }
+}
+
+template <int BN, int NP, int MODE>
+__global__ void __launch_bounds__(Cfg<BN, NP>::kThreads, 1)
     forward_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_w,
                       TcParams p) {
-    using C = Cfg<BN>;
+    using C = Cfg<BN, NP>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * C::kStageBytes);
@@ -79,12 +103,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nN = D / BN;
     const int64_t nM = (p.T + BM - 1) / BM;
     const int64_t tiles = nM * nN;
-    const int KB = D / BK;        // K-blocks per tile
-    const int KPB = p.s.d / BK;   // K-blocks per branch (gather mode)
+    const int KB = D / BK;       // K-blocks per tile
+    const int KPB = p.s.d / BK;  // K-blocks per branch (gather mode)
 
     if (warp == 0 && lane == 0) {
+        // full: one arrive per producer warp (+1 for the W TMA in cp.async mode), or one in X mode
+        const uint32_t full_count = p.use_x ? 1u : (MODE == 0 ? (uint32_t)NP : (uint32_t)NP + 1);
         for (int i = 0; i < kStages; ++i) {
-            mbar_init(&full[i], 1);
+            mbar_init(&full[i], full_count);
             mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -95,51 +121,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_prefetch_desc(&tmap_a);
         tma_prefetch_desc(&tmap_w);
     }
-    if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
+    if (warp == C::kMmaWarp) tmem_alloc<C::kTmemCols>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    if (warp == 0) {
-        // ------------------------------------------------------------ producer
+    if (warp < NP) {
+        // ------------------------------------------------------------ producers
         int stage = 0;
         uint32_t phase = 0;
         const uint64_t pol_w = policy_evict_last();
-        for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-            const int64_t m = tile / nN;
-            const int n = (int)(tile - m * nN);
-            const int64_t t0 = m * BM;
-            if (!p.use_x) {
-                int4 rows = *reinterpret_cast<const int4*>(p.grow + t0 + 4 * lane);
-                for (int b = 0; b < p.s.B; ++b) {
-                    int4 next = rows;
-                    if (b + 1 < p.s.B)
-                        next = *reinterpret_cast<const int4*>(p.grow + (int64_t)(b + 1) * p.Tpad + t0 + 4 * lane);
-                    for (int c = 0; c < KPB; ++c) {
-                        mbar_wait(&empty[stage], phase ^ 1);
-                        if (lane == 0) mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
-                        __syncwarp();
-                        uint8_t* a_dst = smem + stage * C::kStageBytes;
-                        tma_gather4(a_dst + lane * 4 * (BK * 2), &tmap_a, &full[stage], c * BK, rows.x, rows.y,
-                                    rows.z, rows.w);
-                        if (lane == 0)
-                            tma_load_2d_hint(a_dst + C::kABytes, &tmap_w, &full[stage], (b * KPB + c) * BK, n * BN,
-                                             pol_w);
-                        if (++stage == kStages) {
-                            stage = 0;
-                            phase ^= 1;
-                        }
-                    }
-                    rows = next;
-                }
-            } else {
+        if (p.use_x) {
+            for (int64_t tile = blockIdx.x; warp == 0 && tile < tiles; tile += gridDim.x) {
+                const int64_t m = tile / nN;
+                const int n = (int)(tile - m * nN);
                 for (int kb = 0; kb < KB; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (lane == 0) {
                         uint8_t* a_dst = smem + stage * C::kStageBytes;
                         mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
-                        tma_load_2d(a_dst, &tmap_a, &full[stage], kb * BK, (int32_t)t0);
+                        tma_load_2d(a_dst, &tmap_a, &full[stage], kb * BK, (int32_t)(m * BM));
                         tma_load_2d_hint(a_dst + C::kABytes, &tmap_w, &full[stage], kb * BK, n * BN, pol_w);
                     }
                     __syncwarp();
@@ -149,8 +151,81 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             }
+        } else {
+        const int r0 = warp * C::kRowsPerWarp;  // first tile row of this warp
+        int retired_stage = 0, pending = 0;     // cp.async mode bookkeeping
+        for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+            const int64_t m = tile / nN;
+            const int n = (int)(tile - m * nN);
+            const int64_t t0 = m * BM;
+            for (int b = 0; b < p.s.B; ++b) {
+                const int32_t* gb = p.grow + (int64_t)b * p.Tpad + t0 + r0;
+                int4 rows4 = make_int4(0, 0, 0, 0);
+                int32_t row1 = 0;
+                if (MODE == 0) {
+                    if (lane < C::kRowsPerWarp / 4) rows4 = *reinterpret_cast<const int4*>(gb + 4 * lane);
+                } else {
+                    row1 = gb[lane];  // lane l holds the storage row of tile row r0 + l
+                }
+                for (int c = 0; c < KPB; ++c) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t* a_dst = smem + stage * C::kStageBytes;
+                    const int kcol = c * BK;
+                    if (MODE == 0) {
+                        if (lane == 0)
+                            mbar_arrive_expect_tx(&full[stage],
+                                                  (warp == 0 ? C::kBBytes : 0) + C::kRowsPerWarp * BK * 2);
+                        __syncwarp();
+                        if (lane < C::kRowsPerWarp / 4)
+                            tma_gather4(a_dst + (r0 + 4 * lane) * (BK * 2), &tmap_a, &full[stage], kcol, rows4.x,
+                                        rows4.y, rows4.z, rows4.w);
+                        if (warp == 0 && lane == 0)
+                            tma_load_2d_hint(a_dst + C::kABytes, &tmap_w, &full[stage], (b * KPB + c) * BK, n * BN,
+                                             pol_w);
+                    } else {
+                        if (warp == 0 && lane == 0) {
+                            mbar_arrive_expect_tx(&full[stage], C::kBBytes);
+                            tma_load_2d_hint(a_dst + C::kABytes, &tmap_w, &full[stage], (b * KPB + c) * BK, n * BN,
+                                             pol_w);
+                        }
+                        const uint32_t a_base = smem_u32(a_dst);
+                        const int q = lane & 7;  // 16-B chunk of the 128-B row segment
+#pragma unroll
+                        for (int j = 0; j < C::kRowsPerWarp / 4; ++j) {
+                            const int rl = 4 * j + (lane >> 3);  // row within this warp's slab
+                            const int r = r0 + rl;               // row within the tile
+                            const int32_t src_row = __shfl_sync(0xffffffffu, row1, rl);
+                            const __nv_bfloat16* src = p.sub + (int64_t)src_row * p.s.d + kcol + q * 8;
+                            cp_async_16(a_base + r * 128 + ((q ^ (r & 7)) << 4), src);
+                        }
+                        cp_async_commit();
+                        if (++pending > kLag) {  // retire the K-block issued kLag steps ago
+                            cp_async_wait<kLag>();
+                            fence_proxy_async_smem();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(&full[retired_stage]);
+                            if (++retired_stage == kStages) retired_stage = 0;
+                            --pending;
+                        }
+                    }
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
         }
-    } else if (warp == 1) {
+        if (MODE == 1) {
+            cp_async_wait<0>();
+            fence_proxy_async_smem();
+            __syncwarp();
+            for (; pending > 0; --pending) {
+                if (lane == 0) mbar_arrive(&full[retired_stage]);
+                if (++retired_stage == kStages) retired_stage = 0;
+            }
+        }
+        }  // gather mode
+    } else if (warp == C::kMmaWarp) {
         // ------------------------------------------------------------ MMA issuer
         constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
         int stage = 0;
@@ -199,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int64_t m = tile / nN;
             const int n = (int)(tile - m * nN);
             const int64_t t = m * BM + r;
-            const bool valid = t < p.T;
+            const bool valid = t < p.T && !p.epi_skip;
             const uint32_t tok = valid ? __ldg(p.tokens + t) : 0u;
             const __nv_bfloat16* e0row = p.e0 + (int64_t)tok * D + n * BN;
             mbar_wait(&tfull[acc], acc_phase);
@@ -229,39 +304,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     }
                     const int64_t o = t * D + (int64_t)n * BN + c * 32;
-                    if (p.merged_out) {
-                        if (p.out_bf16) {
-                            uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.merged_out) + o);
-#pragma unroll
-                            for (int i = 0; i < 4; ++i)
-                                dst[i] = make_uint4(pack_bf16x2(mv[8 * i], mv[8 * i + 1]),
-                                                    pack_bf16x2(mv[8 * i + 2], mv[8 * i + 3]),
-                                                    pack_bf16x2(mv[8 * i + 4], mv[8 * i + 5]),
-                                                    pack_bf16x2(mv[8 * i + 6], mv[8 * i + 7]));
-                        } else {
-                            float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.merged_out) + o);
-#pragma unroll
-                            for (int i = 0; i < 8; ++i)
-                                dst[i] = make_float4(mv[4 * i], mv[4 * i + 1], mv[4 * i + 2], mv[4 * i + 3]);
-                        }
-                    }
+                    if (p.merged_out) store_chunk(p.merged_out, p.out_bf16, o, mv);
                     if (p.write_rows) {
 #pragma unroll
                         for (int j = 0; j < 32; ++j) mv[j] = __fmul_rn(mv[j], p.amp);
-                        if (p.out_bf16) {
-                            uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.rows_out) + o);
-#pragma unroll
-                            for (int i = 0; i < 4; ++i)
-                                dst[i] = make_uint4(pack_bf16x2(mv[8 * i], mv[8 * i + 1]),
-                                                    pack_bf16x2(mv[8 * i + 2], mv[8 * i + 3]),
-                                                    pack_bf16x2(mv[8 * i + 4], mv[8 * i + 5]),
-                                                    pack_bf16x2(mv[8 * i + 6], mv[8 * i + 7]));
-                        } else {
-                            float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.rows_out) + o);
-#pragma unroll
-                            for (int i = 0; i < 8; ++i)
-                                dst[i] = make_float4(mv[4 * i], mv[4 * i + 1], mv[4 * i + 2], mv[4 * i + 3]);
-                        }
+                        store_chunk(p.rows_out, p.out_bf16, o, mv);
                     }
                 }
             }
@@ -277,19 +324,264 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) {
+    if (warp == C::kMmaWarp) {
         tc_fence_after();
         tmem_dealloc<C::kTmemCols>(tmem_base);
     }
 }
 
-template <int BN>
-void launch_bn(const FwdArgs& a, int num_sms, cudaStream_t st) {
-    using C = Cfg<BN>;
+
+// ============================================================================ 2-CTA variant
+// cta_group::2: a CTA pair computes a 256 x 256 tile (M = 256 tokens, 128 per CTA; the
+// W tile is split, 128 rows per CTA), so each SM streams 16 KB of W per K-block instead
+// of 32 KB -- shared-memory traffic per SM drops from 96 KB to 64 KB per K-block, under
+// the ~128 B/clk smem port.  The leader CTA (rank 0) owns the full barriers and the
+// accumulator-empty barrier and issues every tcgen05.mma.cta_group::2; the peer's TMA
+// loads (.cta_group::2) complete on the leader's barriers, the leader's commits arrive on
+// both CTAs' empty / accumulator-full barriers (multicast).
+constexpr int BM2 = 256;   // tokens per pair tile
+constexpr int BN2 = 256;   // output columns per pair tile
+constexpr int kStages2 = 6;
+constexpr int NP2 = 4;     // producer warps per CTA
+
+constexpr int kEpiWarps2 = 8;  // two per TMEM lane quadrant, each owning half the columns
+
+struct Cfg2 {
+    static constexpr int kABytes = 128 * BK * 2;           // this CTA's 128 token rows
+    static constexpr int kBBytes = (BN2 / 2) * BK * 2;     // this CTA's half of the W tile
+    static constexpr int kStageBytes = kABytes + kBBytes;  // 32 KB
+    static constexpr int kTmemCols = 2 * BN2;              // double-buffered 128 x 256 fp32
+    static constexpr int kSmemBytes = kStages2 * kStageBytes + 1024 + 256;
+    static constexpr int kMmaWarp = NP2;
+    static constexpr int kThreads = (NP2 + 1 + kEpiWarps2) * 32;
+    static constexpr int kRowsPerWarp = 128 / NP2;
+};
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::kThreads, 1)
+    forward_tc2_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_w,
+                       TcParams p) {
+    using C = Cfg2;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages2 * C::kStageBytes);
+    uint64_t* empty = full + kStages2;
+    uint64_t* tfull = empty + kStages2;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    if (*p.err != ~0ull) return;  // uniform across the grid
+
+    const int warp = threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    const int64_t pair = cluster_id_x();
+    const int64_t npairs = nclusters_x();
+    const int D = p.s.D;
+    const int nN = D / BN2;
+    const int64_t nM = (p.T + BM2 - 1) / BM2;
+    const int64_t tiles = nM * nN;
+    const int KB = D / BK;
+    const int KPB = p.s.d / BK;
+
+    if (warp == 0 && lane == 0) {
+        for (int i = 0; i < kStages2; ++i) {
+            mbar_init(&full[i], p.use_x ? 1 : NP2);  // leader's: one arrive per leader producer warp
+            mbar_init(&empty[i], 1);                 // leader's multicast commit
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 2 * kEpiWarps2);  // epilogue warps of both CTAs (leader's copy)
+        }
+        fence_mbar_init();
+        tma_prefetch_desc(&tmap_a);
+        tma_prefetch_desc(&tmap_w);
+    }
+    if (warp == C::kMmaWarp) tmem_alloc_2cta<C::kTmemCols>(tmem_slot);
+    tc_fence_before();
+    cluster_sync();  // barriers of both CTAs initialised, TMEM allocated, before any remote signal
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp < NP2) {
+        // ------------------------------------------------------------ producers (both CTAs)
+        int stage = 0;
+        uint32_t phase = 0;
+        const uint64_t pol_w = policy_evict_last();
+        const int r0 = warp * C::kRowsPerWarp;
+        for (int64_t tile = pair; tile < tiles; tile += npairs) {
+            const int64_t m = tile / nN;
+            const int n = (int)(tile - m * nN);
+            const int64_t t0 = m * BM2 + (int64_t)rank * 128;  // this CTA's first token row
+            const int wrow = n * BN2 + (int)rank * (BN2 / 2);  // this CTA's first W row
+            if (p.use_x) {
+                for (int kb = 0; kb < KB; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    if (warp == 0 && lane == 0) {
+                        uint8_t* a_dst = smem + stage * C::kStageBytes;
+                        if (leader) mbar_arrive_expect_tx(&full[stage], 2 * C::kStageBytes);
+                        tma_load_2d_2cta(a_dst, &tmap_a, leader_bar(&full[stage]), kb * BK, (int32_t)t0, 0);
+                        tma_load_2d_2cta(a_dst + C::kABytes, &tmap_w, leader_bar(&full[stage]), kb * BK, wrow, pol_w);
+                    }
+                    __syncwarp();
+                    if (++stage == kStages2) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                continue;
+            }
+            for (int b = 0; b < p.s.B; ++b) {
+                int4 rows4 = make_int4(0, 0, 0, 0);
+                if (lane < C::kRowsPerWarp / 4)
+                    rows4 = *reinterpret_cast<const int4*>(p.grow + (int64_t)b * p.Tpad + t0 + r0 + 4 * lane);
+                for (int c = 0; c < KPB; ++c) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t* a_dst = smem + stage * C::kStageBytes;
+                    if (leader && lane == 0)  // expect this warp's rows of BOTH CTAs (+ both W halves)
+                        mbar_arrive_expect_tx(&full[stage], 2 * (C::kRowsPerWarp * BK * 2) +
+                                                                (warp == 0 ? 2 * C::kBBytes : 0));
+                    __syncwarp();
+                    if (lane < C::kRowsPerWarp / 4)
+                        tma_gather4_2cta(a_dst + (r0 + 4 * lane) * (BK * 2), &tmap_a, leader_bar(&full[stage]),
+                                         c * BK, rows4.x, rows4.y, rows4.z, rows4.w);
+                    if (warp == 0 && lane == 0)
+                        tma_load_2d_2cta(a_dst + C::kABytes, &tmap_w, leader_bar(&full[stage]), (b * KPB + c) * BK,
+                                         wrow, pol_w);
+                    if (++stage == kStages2) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == C::kMmaWarp) {
+        // ------------------------------------------------------------ MMA issuer (leader only)
+        if (leader) {
+            constexpr uint32_t idesc = idesc_bf16_f32(BM2, BN2);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int64_t tile = pair; tile < tiles; tile += npairs) {
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN2);
+                for (int kb = 0; kb < KB; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint32_t a_addr = smem_u32(smem + stage * C::kStageBytes);
+                        const uint64_t adesc = smem_desc_sw128(a_addr);
+                        const uint64_t bdesc = smem_desc_sw128(a_addr + C::kABytes);
+#pragma unroll
+                        for (int k = 0; k < BK / 16; ++k)
+                            tc_mma_bf16_2cta(d_tmem, adesc + (uint64_t)(k * 2), bdesc + (uint64_t)(k * 2), idesc,
+                                             (kb | k) != 0);
+                        tc_commit_2cta_mc(&empty[stage], 0x3);
+                    }
+                    __syncwarp();
+                    if (++stage == kStages2) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                if (lane == 0) tc_commit_2cta_mc(&tfull[acc], 0x3);
+                __syncwarp();
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+        }
+    } else {
+        // ------------------------------------------------------------ epilogue (both CTAs)
+        const int ew = warp - (C::kMmaWarp + 1);  // 0..7
+        const int q = warp & 3;                   // TMEM lane quadrant this warp may access
+        const int half = ew >> 2;                 // column half of the tile this warp owns
+        const int r = q * 32 + lane;
+        const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
+        const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty[1]), 0);
+        constexpr int kChunks = BN2 / 2 / 32;     // 32-column chunks per warp
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int64_t tile = pair; tile < tiles; tile += npairs) {
+            const int64_t m = tile / nN;
+            const int n = (int)(tile - m * nN);
+            const int64_t t = m * BM2 + (int64_t)rank * 128 + r;
+            const bool valid = t < p.T && !p.epi_skip;
+            const uint32_t tok = valid ? __ldg(p.tokens + t) : 0u;
+            const int col0 = n * BN2 + half * (BN2 / 2);
+            const __nv_bfloat16* e0row = p.e0 + (int64_t)tok * D + col0;
+            uint4 e[4], en[4];
+            if (valid) {  // E0 chunk 0, loaded before the accumulator is ready
+#pragma unroll
+                for (int i = 0; i < 4; ++i) e[i] = __ldg(reinterpret_cast<const uint4*>(e0row) + i);
+            }
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < kChunks; ++c) {
+                uint32_t v[32];
+                tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) +
+                                       (uint32_t)(acc * BN2 + half * (BN2 / 2) + c * 32),
+                                   v);
+                if (valid && c + 1 < kChunks) {  // prefetch the next E0 chunk
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) en[i] = __ldg(reinterpret_cast<const uint4*>(e0row + (c + 1) * 32) + i);
+                }
+                tmem_ld_wait();
+                if (valid) {
+                    float mv[32];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const uint32_t w[4] = {e[i].x, e[i].y, e[i].z, e[i].w};
+#pragma unroll
+                        for (int h = 0; h < 4; ++h) {
+                            const int j = i * 8 + h * 2;
+                            mv[j] = __fmul_rn(__fadd_rn(bf16_bits_to_f32(w[h] & 0xffffu), __uint_as_float(v[j])),
+                                              p.scale);
+                            mv[j + 1] = __fmul_rn(
+                                __fadd_rn(bf16_bits_to_f32(w[h] >> 16), __uint_as_float(v[j + 1])), p.scale);
+                        }
+                    }
+                    const int64_t o = t * D + col0 + c * 32;
+                    if (p.merged_out) store_chunk(p.merged_out, p.out_bf16, o, mv);
+                    if (p.write_rows) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) mv[j] = __fmul_rn(mv[j], p.amp);
+                        store_chunk(p.rows_out, p.out_bf16, o, mv);
+                    }
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) e[i] = en[i];
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(acc == 0 ? tempty_leader0 : tempty_leader1);
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    }
+
+    tc_fence_before();
+    cluster_sync();  // every MMA retired and every remote arrive delivered before TMEM is freed
+    if (warp == C::kMmaWarp) {
+        tc_fence_after();
+        tmem_dealloc_2cta<C::kTmemCols>(tmem_base);
+    }
+}
+
+template <int BN, int NP, int MODE>
+void launch_cfg(const FwdArgs& a, int num_sms, cudaStream_t st) {
+    using C = Cfg<BN, NP>;
     TcParams p;
     p.s = a.s;
     p.tokens = a.tokens;
     p.grow = a.grow;
+    p.sub = a.sub;
     p.e0 = a.e0;
     p.rows_out = a.rows_out;
     p.merged_out = a.merged_out;
@@ -301,20 +593,78 @@ void launch_bn(const FwdArgs& a, int num_sms, cudaStream_t st) {
     p.amp = a.s.amp == kAmpSqrt ? (float)__builtin_sqrt((double)a.s.D) : 1.0f;
     p.err = a.err;
     p.use_x = a.tmap_x != nullptr;
+    p.epi_skip = getenv("NGRAM_DEBUG_EPI_SKIP") ? 1 : 0;
     const int64_t tiles = ((a.T + BM - 1) / BM) * (a.s.D / BN);
     int grid = (int)(tiles < num_sms ? tiles : num_sms);
     if (grid < 1) grid = 1;
-    cudaFuncSetAttribute(forward_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-    forward_tc_kernel<BN><<<grid, kThreads, C::kSmemBytes, st>>>(a.tmap_x ? *a.tmap_x : *a.tmap_sub, *a.tmap_w, p);
+    cudaFuncSetAttribute(forward_tc_kernel<BN, NP, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    forward_tc_kernel<BN, NP, MODE><<<grid, C::kThreads, C::kSmemBytes, st>>>(a.tmap_x ? *a.tmap_x : *a.tmap_sub,
+                                                                              *a.tmap_w, p);
     count_launch();
+}
+
+void launch_tc2(const FwdArgs& a, int num_sms, cudaStream_t st) {
+    TcParams p;
+    p.s = a.s;
+    p.tokens = a.tokens;
+    p.grow = a.grow;
+    p.sub = a.sub;
+    p.e0 = a.e0;
+    p.rows_out = a.rows_out;
+    p.merged_out = a.merged_out;
+    p.out_bf16 = a.out_bf16;
+    p.write_rows = (a.rows_out != nullptr && a.s.amp != kAmpLN) ? 1 : 0;
+    p.T = a.T;
+    p.Tpad = a.Tpad;
+    p.scale = 1.0f / (float)a.s.denom;
+    p.amp = a.s.amp == kAmpSqrt ? (float)__builtin_sqrt((double)a.s.D) : 1.0f;
+    p.err = a.err;
+    p.use_x = a.tmap_x != nullptr;
+    p.epi_skip = getenv("NGRAM_DEBUG_EPI_SKIP") ? 1 : 0;
+    const int64_t tiles = ((a.T + BM2 - 1) / BM2) * (a.s.D / BN2);
+    int64_t pairs = num_sms / 2;
+    if (tiles < pairs) pairs = tiles;
+    if (pairs < 1) pairs = 1;
+    cudaFuncSetAttribute(forward_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2::kSmemBytes);
+    forward_tc2_kernel<<<(unsigned)(2 * pairs), Cfg2::kThreads, Cfg2::kSmemBytes, st>>>(
+        a.tmap_x ? *a.tmap_x : *a.tmap_sub, *a.tmap_w2, p);
+    count_launch();
+}
+
+// A-producer: 0 = TMA tile::gather4, 1 = cp.async (default).  NGRAM_PRODUCER overrides
+// (kept for the A/B measurement recorded in DESIGN.md / profiles/).
+int producer_mode() {
+    static int mode = [] {
+        const char* e = getenv("NGRAM_PRODUCER");
+        return e ? atoi(e) : 1;
+    }();
+    return mode;
 }
 
 }  // namespace
 
+int tc_variant() {  // 2 = cta_group::2 pair kernel (default when D % 256 == 0), 1 = single-CTA
+    static int v = [] {
+        const char* e = getenv("NGRAM_TC_VARIANT");
+        return e ? atoi(e) : 2;
+    }();
+    return v;
+}
+
 void launch_forward_tc(const FwdArgs& a, int num_sms, cudaStream_t st) {
     if (a.T <= 0) return;
-    if (a.s.D % 256 == 0) launch_bn<256>(a, num_sms, st);
-    else launch_bn<128>(a, num_sms, st);
+    const bool bn256 = a.s.D % 256 == 0;
+    if (bn256 && tc_variant() == 2 && a.tmap_w2 != nullptr) {
+        launch_tc2(a, num_sms, st);
+        return;
+    }
+    if (producer_mode() == 0) {
+        if (bn256) launch_cfg<256, 4, 0>(a, num_sms, st);
+        else launch_cfg<128, 4, 0>(a, num_sms, st);
+    } else {
+        if (bn256) launch_cfg<256, 4, 1>(a, num_sms, st);
+        else launch_cfg<128, 4, 1>(a, num_sms, st);
+    }
 }
 
 }  // namespace ngk

@@ -76,6 +76,7 @@ struct FwdArgs {
     // tensor maps (tensor-core path)
     const CUtensorMap* tmap_sub;
     const CUtensorMap* tmap_w;
+    const CUtensorMap* tmap_w2;  // W_cat with a 128-row box (2-CTA kernel), or null
     // X (materialised gathered rows, T x D bf16) instead of sub-table gather, or null
     const CUtensorMap* tmap_x;
 };
@@ -83,6 +84,9 @@ struct FwdArgs {
 void launch_forward_tc(const FwdArgs& a, int num_sms, cudaStream_t st);
 // generic CUDA-core path: any shape, v1 and v2, reference float op order (simt.cu).
 void launch_forward_simt(const FwdArgs& a, cudaStream_t st);
+// K2 standalone: materialise X (T x D bf16) from the storage rows (d % 8 == 0).
+void launch_gather_rows(const Shape& s, const int32_t* grow, int64_t Tpad, int64_t T, const __nv_bfloat16* sub,
+                        __nv_bfloat16* X, const unsigned long long* err, cudaStream_t st);
 // LayerNorm amplification over merged rows (f32 merged -> rows) (simt.cu).
 // merged_copy (may be null): also write the merged rows in the output dtype.
 void launch_layernorm_rows(const Shape& s, const float* merged, const float* gain, const float* bias, void* rows,

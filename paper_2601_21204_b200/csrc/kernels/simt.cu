@@ -107,6 +107,41 @@ __global__ void __launch_bounds__(128) forward_v2_simt_kernel(FwdArgs a, float s
     }
 }
 
+// ---------------------------------------------------------------- K2 standalone gather
+// X[t, b*d : (b+1)*d] = E_b[id_b(t)] (bf16, 16-byte vectors; one warp per (t, b) row group).
+// Used when X must be materialised (multi-GPU home buffer) -- the single-GPU forward
+// gathers straight into the GEMM's shared memory instead.
+__global__ void __launch_bounds__(256) gather_rows_kernel(const int32_t* __restrict__ grow, int64_t Tpad, int64_t T,
+                                                          int B, int d, const __nv_bfloat16* __restrict__ sub,
+                                                          __nv_bfloat16* __restrict__ X, const unsigned long long* err) {
+    if (*err != ~0ull) return;
+    constexpr int U = 4;            // independent 16-B loads in flight per thread
+    const int vec_per_row = d / 8;  // 16-byte vectors per sub-table row
+    const int64_t total = T * B * vec_per_row;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v0 < total; v0 += stride * U) {
+        uint4 val[U];
+        int64_t dst[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t v = v0 + u * stride;
+            dst[u] = -1;
+            if (v < total) {
+                const int64_t rowv = v / vec_per_row;
+                const int c = (int)(v - rowv * vec_per_row);
+                const int64_t t = rowv / B;
+                const int b = (int)(rowv - t * B);
+                const int32_t row = __ldg(grow + (int64_t)b * Tpad + t);
+                val[u] = __ldg(reinterpret_cast<const uint4*>(sub + (int64_t)row * d) + c);
+                dst[u] = (t * (int64_t)B * d + (int64_t)b * d) / 8 + c;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (dst[u] >= 0) reinterpret_cast<uint4*>(X)[dst[u]] = val[u];
+    }
+}
+
 // ---------------------------------------------------------------- LayerNorm amplification
 __global__ void __launch_bounds__(256) layernorm_rows_kernel(int D, const float* __restrict__ merged,
                                                              const float* __restrict__ gain,
@@ -154,6 +189,16 @@ void launch_forward_simt(const FwdArgs& a, cudaStream_t st) {
         if (smem > 48 * 1024) cudaFuncSetAttribute(forward_v2_simt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         forward_v2_simt_kernel<<<(unsigned)a.T, 128, smem, st>>>(a, scale, amp);
     }
+    count_launch();
+}
+
+void launch_gather_rows(const Shape& s, const int32_t* grow, int64_t Tpad, int64_t T, const __nv_bfloat16* sub,
+                        __nv_bfloat16* X, const unsigned long long* err, cudaStream_t st) {
+    if (T <= 0) return;
+    const int64_t total = T * s.B * (s.d / 8);
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    gather_rows_kernel<<<(unsigned)blocks, 256, 0, st>>>(grow, Tpad, T, s.B, s.d, sub, X, err);
     count_launch();
 }
 
