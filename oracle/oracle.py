@@ -64,8 +64,39 @@ def lib():
         L.or_cache_append.argtypes = [_u32p, C.c_int, C.c_int, C.c_uint64, _u64p, C.c_uint32, _u64p]
         L.or_hash_throughput_probe.argtypes = [_u32p, C.c_int64, C.c_int, C.c_int, C.c_uint64, _u64p]
         L.or_hash_throughput_probe.restype = C.c_int64
+        L.or_rng_new.argtypes = [C.c_uint64]
+        L.or_rng_new.restype = C.c_void_p
+        L.or_rng_below.argtypes = [C.c_void_p, C.c_uint64]
+        L.or_rng_below.restype = C.c_uint64
+        L.or_rng_next.argtypes = [C.c_void_p]
+        L.or_rng_next.restype = C.c_uint64
+        L.or_rng_gaussian.argtypes = [C.c_void_p]
+        L.or_rng_gaussian.restype = C.c_double
+        L.or_rng_free.argtypes = [C.c_void_p]
         _ORACLE = L
     return _ORACLE
+
+
+class Rng64:
+    """rng64 (std::mt19937_64) + uniform_below / gaussian (rng.hpp:14-40), call by call."""
+
+    def __init__(self, seed):
+        self.h = lib().or_rng_new(seed)
+
+    def below(self, bound):
+        return int(lib().or_rng_below(self.h, bound))
+
+    def __call__(self):
+        return int(lib().or_rng_next(self.h))
+
+    def gaussian(self):
+        return float(lib().or_rng_gaussian(self.h))
+
+    def __del__(self):
+        try:
+            lib().or_rng_free(self.h)
+        except Exception:
+            pass
 
 
 def ref_available() -> bool:

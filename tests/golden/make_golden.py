@@ -1,0 +1,209 @@
+#!/usr/bin/env python3
+"""Generate tests/golden/*.npz from the REFERENCE itself (oracle/_ref/libngram_ref.so, the
+unmodified reference sources compiled by oracle/Makefile).  Run here, where
+/root/reference exists:  python tests/golden/make_golden.py
+
+Every fixture records which reference entry point produced it.  Seeds follow SURVEY.md
+8(d) / the reference tests (test_hashing.cpp:40-57 seed 0x5eed0001, tokens seed 42,
+banks seed 1234, bf16-rounded so the bf16 device bank and the float bank are equal).
+"""
+import ctypes as C
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+import oracle as O  # noqa: E402
+
+R = O.ref()
+
+
+def ref_default_config(v0, dim, N, K):
+    buf = C.create_string_buffer(1 << 16)
+    assert R.ref_make_default_config_json(v0, dim, N, K, buf, len(buf)) == 0
+    return json.loads(buf.value)
+
+
+def ref_hash_sequences(cfg, seqs, priors=None):
+    out = []
+    for i, s in enumerate(seqs):
+        s = np.ascontiguousarray(s, np.uint32)
+        B = (cfg["max_order"] - 1) * cfg["sub_tables"]
+        ids = np.zeros((len(s), max(B, 1)), np.uint64)
+        pr = None if priors is None else np.ascontiguousarray(priors[i], np.uint32)
+        rc = R.ref_hash_sequence(json.dumps(cfg).encode(), s, len(s), None if pr is None else pr.ctypes.data,
+                                 0 if pr is None else len(pr), ids)
+        assert rc == 0, R.ref_last_error()
+        out.append(ids[:, :B])
+    return np.concatenate(out)
+
+
+def ref_bank(cfg, seed):
+    h = R.ref_bank_create(json.dumps(cfg).encode(), seed, 1)
+    assert h, R.ref_last_error()
+    return h
+
+
+def ref_tensor(h, which, b=0):
+    n = C.c_int64()
+    p = R.ref_bank_tensor(h, which, b, C.byref(n))
+    return np.ctypeslib.as_array(p, (n.value,)).copy()
+
+
+def bank_checksum_ref(h, cfg):
+    N, K, D, B, d, v, denom = O.shape(cfg)
+    hb = O.HostBank(cfg, ref_tensor(h, 0), [ref_tensor(h, 1, b) for b in range(B)],
+                    [ref_tensor(h, 2, b) for b in range(B)] if v == 1 else [],
+                    ref_tensor(h, 3) if cfg["amplification"] == "layer_norm" else np.zeros(0, np.float32),
+                    ref_tensor(h, 4) if cfg["amplification"] == "layer_norm" else np.zeros(0, np.float32))
+    return O.bank_checksum(hb)
+
+
+def ref_embed(h, seqs, priors=None, D=None):
+    rows32, merged32, rows64, merged64 = [], [], [], []
+    for i, s in enumerate(seqs):
+        s = np.ascontiguousarray(s, np.uint32)
+        pr = None if priors is None else np.ascontiguousarray(priors[i], np.uint32)
+        a = [np.zeros((len(s), D), np.float32) for _ in range(2)]
+        b = [np.zeros((len(s), D), np.float64) for _ in range(2)]
+        args = (s, len(s), None if pr is None else pr.ctypes.data, 0 if pr is None else len(pr))
+        assert R.ref_embed_sequence_f32(h, *args, a[0].ctypes.data, a[1].ctypes.data) == 0
+        assert R.ref_embed_sequence_f64(h, *args, b[0].ctypes.data, b[1].ctypes.data) == 0
+        rows32.append(a[0]), merged32.append(a[1]), rows64.append(b[0]), merged64.append(b[1])
+    return tuple(np.concatenate(x) for x in (rows32, merged32, rows64, merged64))
+
+
+def save(name, **kw):
+    np.savez_compressed(os.path.join(HERE, name), **kw)
+    print("wrote", name, {k: getattr(v, "shape", v) for k, v in kw.items() if hasattr(v, "shape")})
+
+
+def v2_config(v0, dim, order, k, amp="none"):
+    """tests/test_embedding.cpp:28-44 v2_config."""
+    sv = [13 + 8 * n + 3 * kk for n in range(2, order + 1) for kk in range(1, k + 1)]
+    return O.make_config(v0, dim, order, k, sv, "subtable_v2", amp)
+
+
+def v1_config(v0, dim, order):
+    """tests/test_embedding.cpp:15-26 v1_config."""
+    return O.make_config(v0, dim, order, 1, [17 + 10 * n for n in range(2, order + 1)], "averaged_v1", "none")
+
+
+def main():
+    # 1. rolling_hash: reference's own randomized case stream (test_hashing.cpp:40-57)
+    cnt = 20000
+    n = np.zeros(cnt, np.int32)
+    base = np.zeros(cnt, np.uint64)
+    mod = np.zeros(cnt, np.uint64)
+    win = np.zeros((cnt, 8), np.uint32)
+    h = np.zeros(cnt, np.uint64)
+    assert R.ref_rolling_hash_cases(0x5EED0001, cnt, n, base, mod, win.reshape(-1), h) == 0
+    save("rolling_hash_20k.npz", n=n, base=base, modulus=mod, windows=win, hash=h,
+         source="ref_rolling_hash_cases -> ngram::rolling_hash (hashing.cpp:33-59)")
+
+    # 2. config A ids: make_default_config(32000, 256, 3, 2), 4 x 512 tokens, seed 42
+    cfgA = ref_default_config(32000, 256, 3, 2)
+    toksA = O.uniform_tokens(42, 32000, 4 * 512)
+    idsA = ref_hash_sequences(cfgA, [toksA[i * 512:(i + 1) * 512] for i in range(4)])
+    save("cfgA_ids.npz", config=json.dumps(cfgA), tokens=toksA, ids=idsA, seq_len=512)
+
+    # 3. LongCat-scale (config C) ids, 2 sequences x 1024 with a carried prior on the second
+    sv = [(2 * (74 + b) + 1) * 64000 for b in range(12)]
+    cfgC = O.make_config(128000, 3072, 4, 4, sv, "subtable_v2", "scale_sqrt_d")
+    toksC = O.uniform_tokens(43, 128000, 2048)
+    priorC = O.uniform_tokens(44, 128000, 3)
+    idsC = np.concatenate([ref_hash_sequences(cfgC, [toksC[:1024]]),
+                           ref_hash_sequences(cfgC, [toksC[1024:]], [priorC])])
+    save("cfgC_ids.npz", config=json.dumps(cfgC), tokens=toksC, prior=priorC, ids=idsC)
+
+    # 4. moduli above 2^32 (general 128-bit path): N=5, K=2
+    svb = [(1 << 40) + 12345 * (i + 1) for i in range(8)]
+    cfgBig = O.make_config(1 << 20, 16, 5, 2, svb, "subtable_v2", "none")
+    toksB = O.uniform_tokens(45, 1 << 20, 600)
+    save("bigmod_ids.npz", config=json.dumps(cfgBig), tokens=toksB,
+         ids=ref_hash_sequences(cfgBig, [toksB[:300], toksB[300:]]))
+
+    # 5. embeddings on the tensor-core shape (D=256, d=64), every amplification mode
+    for amp in ["none", "scale_sqrt_d", "layer_norm"]:
+        cfg = ref_default_config(1000, 256, 3, 2)
+        cfg["amplification"] = amp
+        hb = ref_bank(cfg, 1234)
+        if amp == "layer_norm":  # non-trivial gain / bias, as test_embedding.cpp:211-214
+            g = np.random.default_rng(5)
+            gain = (1.0 + 0.1 * g.standard_normal(256)).astype(np.float32)
+            bias = (0.05 * g.standard_normal(256)).astype(np.float32)
+            O.lib().or_round_bf16(gain, gain.size)
+            O.lib().or_round_bf16(bias, bias.size)
+            R.ref_bank_set_ln(hb, gain, bias)
+        toks = O.uniform_tokens(7, 1000, 300)
+        prior = O.uniform_tokens(8, 1000, 2)
+        seqs = [toks[:100], toks[100:300]]
+        r32, m32, r64, m64 = ref_embed(hb, seqs, [np.zeros(0, np.uint32), prior], D=256)
+        extra = {}
+        if amp == "layer_norm":
+            extra = {"ln_gain": ref_tensor(hb, 3), "ln_bias": ref_tensor(hb, 4)}
+        save(f"embed_tc_{amp}.npz", config=json.dumps(cfg), seed=1234, tokens=toks, seq_offsets=np.array([0, 100, 300]),
+             prior1=prior, rows_f32=r32, merged_f32=m32, rows_f64=r64, merged_f64=m64,
+             bank_checksum=np.uint64(bank_checksum_ref(hb, cfg)), **extra)
+        R.ref_bank_destroy(hb)
+
+    # 6. generic shapes (CUDA-core path): the reference tests' v2_config / v1_config banks
+    for name, cfg, seed in [("simt_v2", v2_config(16, 12, 4, 2, "scale_sqrt_d"), 7),
+                            ("simt_v2_k1", v2_config(32, 12, 3, 2, "none"), 11),
+                            ("v1", v1_config(8, 4, 3), 17),
+                            ("v1_wide", O.make_config(500, 512, 4, 1, [3001, 3011, 3019], "averaged_v1",
+                                                      "scale_sqrt_d"), 19)]:
+        hb = ref_bank(cfg, seed)
+        toks = O.uniform_tokens(13, cfg["base_vocab"], 64)
+        r32, m32, r64, m64 = ref_embed(hb, [toks[:20], toks[20:]], None, D=cfg["dim"])
+        save(f"embed_{name}.npz", config=json.dumps(cfg), seed=seed, tokens=toks, seq_offsets=np.array([0, 20, 64]),
+             rows_f32=r32, merged_f32=m32, rows_f64=r64, merged_f64=m64,
+             bank_checksum=np.uint64(bank_checksum_ref(hb, cfg)))
+        R.ref_bank_destroy(hb)
+
+    # 7. full LongCat width D=3072, N=4, K=4 (reduced vocabulary bank), 48 tokens
+    cfgW = ref_default_config(1000, 3072, 4, 4)
+    hb = ref_bank(cfgW, 1234)
+    toks = O.uniform_tokens(21, 1000, 48)
+    r32, m32, r64, m64 = ref_embed(hb, [toks], None, D=3072)
+    save("embed_d3072.npz", config=json.dumps(cfgW), seed=1234, tokens=toks, seq_offsets=np.array([0, 48]),
+         rows_f32=r32, merged_f64=m64, rows_f64=r64, bank_checksum=np.uint64(bank_checksum_ref(hb, cfgW)))
+    R.ref_bank_destroy(hb)
+
+    # 8. decode: draft_verify through the reference (cache.cpp:152-195) after a warm-up append
+    cfgD = ref_default_config(64, 384, 4, 2)  # TC shape (d=64), BN=128 tile
+    cfgD["amplification"] = "none"
+    hb = ref_bank(cfgD, 99)
+    rng = np.random.default_rng(3)
+    cases = {}
+    for trial in range(6):
+        ch = R.ref_cache_create(json.dumps(cfgD).encode())
+        prefix = rng.integers(0, 64, size=int(rng.integers(0, 6)), dtype=np.uint32)
+        pid = np.zeros(16, np.uint64)
+        for t in prefix:
+            assert R.ref_cache_append(ch, int(t), pid) == 0
+        L = int(rng.integers(1, 9))
+        draft = rng.integers(0, 64, size=L, dtype=np.uint32)
+        accept = int(rng.integers(0, L + 1))
+        acc = np.zeros((max(accept, 1), 384), np.float32)
+        cnt8 = np.zeros(8, np.uint64)
+        assert R.ref_draft_verify(ch, hb, draft, L, accept, 256, 0, acc, cnt8) == 0
+        ring = np.zeros(3, np.uint32)
+        length = C.c_uint64()
+        last = C.c_uint32()
+        R.ref_cache_ring(ch, ring, C.byref(length), C.byref(last))
+        i = trial
+        cases.update({f"c{i}_prefix": prefix, f"c{i}_draft": draft, f"c{i}_accept": np.int64(accept),
+                      f"c{i}_accepted": acc[:accept], f"c{i}_ring": ring.copy(), f"c{i}_length": np.uint64(length.value),
+                      f"c{i}_last": np.uint32(last.value), f"c{i}_counters": cnt8})
+        R.ref_cache_destroy(ch)
+    save("draft_verify.npz", config=json.dumps(cfgD), seed=99, ncases=6, **cases)
+    R.ref_bank_destroy(hb)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,66 @@
+"""Shared test helpers: fixture loading, device buffers, the stated tolerances."""
+import json
+import os
+
+import numpy as np
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+# ---------------------------------------------------------------- tolerance contract
+# Tensor-core path (bf16 tables, fp32 TMEM accumulation, different summation order than the
+# reference's sequential float loop), compared with the reference's double path on the same
+# bf16-representable bank:
+ROW_RTOL = 1e-5   # per row: max |err| <= ROW_RTOL * max |ref row|
+REL_L2 = 1e-6     # whole output: ||err||_2 <= REL_L2 * ||ref||_2
+BF16_REL = 2.0 ** -8  # bf16 output: additionally |err| <= 2^-8 |ref| per element
+
+
+class Gold(dict):
+    """An .npz fixture fully loaded (NpzFile re-decompresses on every key access)."""
+
+    @property
+    def files(self):
+        return list(self.keys())
+
+
+def gold(name):
+    with np.load(os.path.join(GOLD, name), allow_pickle=False) as z:
+        return Gold({k: z[k] for k in z.files})
+
+
+def gold_config(g):
+    return json.loads(str(g["config"]))
+
+
+def assert_rows_close(got, ref, bf16=False, row_rtol=ROW_RTOL, rel_l2=REL_L2):
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    assert got.shape == ref.shape
+    err = np.abs(got - ref)
+    rowmax = np.abs(ref).max(axis=1, keepdims=True) + 1e-30
+    if bf16:
+        bound = BF16_REL * np.abs(ref) + row_rtol * rowmax
+        assert (err <= bound).all(), f"bf16 max excess {(err - bound).max()}"
+    else:
+        worst = (err / rowmax).max()
+        assert worst <= row_rtol, f"per-row max err {worst:.3e} > {row_rtol}"
+        rel = np.linalg.norm(got - ref) / (np.linalg.norm(ref) + 1e-30)
+        assert rel <= rel_l2, f"relL2 {rel:.3e} > {rel_l2}"
+
+
+def bf16_to_f32(u16):
+    return (np.asarray(u16, np.uint16).astype(np.uint32) << 16).view(np.float32)
+
+
+def dev_u32(torch, a, device):
+    """uint32 host array -> int32 device tensor with the same bits."""
+    return torch.from_numpy(np.ascontiguousarray(a, np.uint32).view(np.int32)).to(device)
+
+
+def dev_i64(torch, a, device):
+    return torch.from_numpy(np.ascontiguousarray(a, np.int64)).to(device)
+
+
+def u64(t):
+    """int64 device/host tensor holding u64 bits -> numpy uint64."""
+    return t.cpu().numpy().view(np.uint64) if hasattr(t, "cpu") else np.asarray(t).view(np.uint64)

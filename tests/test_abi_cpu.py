@@ -1,0 +1,128 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol the header
+declares, and its host-side config logic (shape algebra, validation, JSON) matches the
+reference (config.cpp:23-183) -- compared with oracle/_ref when it is built, else with
+the reference behaviour the tests state explicitly."""
+import ctypes as C
+import json
+import os
+import re
+
+import pytest
+
+import oracle as O
+from paper_2601_21204_b200 import abi
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    txt = open(os.path.join(ROOT, "include", "ngram_b200.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(ngram_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = abi.lib()
+    declared = header_functions()
+    assert len(declared) >= 30
+    missing = [f for f in declared if not hasattr(L, f)]
+    assert not missing, missing
+    assert set(declared) == set(abi.SYMBOLS)  # the ctypes binding covers the whole header
+
+
+def test_version_and_launch_counter():
+    assert b"sm_100a" in abi.lib().ngram_version()
+    assert abi.lib().ngram_kernel_launches() >= 0
+
+
+def _ours_validate(cfg) -> int:
+    return abi.lib().ngram_config_validate(json.dumps(cfg).encode())
+
+
+def _ref_validate(cfg):
+    if not O.ref_available():
+        return None
+    return O.ref().ref_config_validate_json(json.dumps(cfg).encode())
+
+
+def _v2(v0, dim, order, k, amp="none"):
+    return O.make_config(v0, dim, order, k, [13 + 8 * n + 3 * kk for n in range(2, order + 1)
+                                             for kk in range(1, k + 1)], "subtable_v2", amp)
+
+
+def _bad_configs():  # test_embedding.cpp:424-444 plus the other validate() branches (config.cpp:32-77)
+    c = []
+    x = _v2(16, 8, 3, 2)
+    x["dim"] = 9
+    c.append(("dim not divisible", x))
+    x = _v2(16, 8, 3, 2)
+    x["sub_vocab"] = x["sub_vocab"][:-1]
+    c.append(("missing (3,2)", x))
+    x = O.make_config(16, 8, 3, 1, [37, 47], "averaged_v1", "none")
+    x["sub_tables"] = 2
+    c.append(("v1 with K=2", x))
+    c.append(("base_vocab 1", _v2(1, 8, 3, 2)))
+    x = _v2(16, 8, 3, 2)
+    x["max_order"] = 0
+    c.append(("max_order 0", x))
+    x = _v2(16, 8, 3, 2)
+    x["sub_vocab"][0]["vocab"] = 0
+    c.append(("V_nk 0", x))
+    x = _v2(16, 8, 3, 2)
+    x["sub_vocab"].append({"n": 5, "k": 1, "vocab": 9})
+    c.append(("extra branch", x))
+    x = _v2(16, 8, 3, 2)
+    x["variant"] = "bogus"
+    c.append(("unknown variant", x))
+    x = _v2(16, 8, 3, 2)
+    x["amplification"] = "bogus"
+    c.append(("unknown amplification", x))
+    base_only = O.make_config(16, 8, 1, 1, [], "subtable_v2", "none")
+    base_only["sub_vocab"] = [{"n": 2, "k": 1, "vocab": 5}]
+    c.append(("base-only with sub vocab", base_only))
+    return c
+
+
+@pytest.mark.parametrize("name,cfg", _bad_configs())
+def test_config_validation_rejects_like_reference(name, cfg):
+    assert _ours_validate(cfg) == abi.NGRAM_EINVAL  # std::invalid_argument
+    r = _ref_validate(cfg)
+    if r is not None:
+        assert r == -1, f"reference accepted {name}"
+
+
+def test_config_validation_accepts_like_reference():
+    for cfg in [_v2(16, 8, 3, 2), _v2(128, 24, 4, 2, "layer_norm"), O.make_default_config(32000, 256, 3, 2),
+                O.make_config(16, 8, 1, 1, [], "subtable_v2", "none")]:
+        assert _ours_validate(cfg) == abi.NGRAM_OK
+        r = _ref_validate(cfg)
+        assert r in (None, 0)
+
+
+def test_bad_json_is_a_parse_error():
+    assert abi.lib().ngram_config_validate(b"{not json") == abi.NGRAM_EPARSE
+    assert abi.lib().ngram_config_validate(b'{"max_order": 3}') == abi.NGRAM_EPARSE
+    assert b"JSON" in abi.lib().ngram_last_error()
+
+
+@pytest.mark.parametrize("v0,dim,N,K", [(32000, 256, 3, 2), (128000, 768, 4, 4), (128000, 3072, 4, 4), (50, 24, 4, 2)])
+def test_make_default_config_matches_reference(v0, dim, N, K):  # config.cpp:163-183
+    buf = C.create_string_buffer(1 << 16)
+    assert abi.lib().ngram_make_default_config(v0, dim, N, K, buf, len(buf)) == 0
+    ours = json.loads(buf.value)
+    assert ours == O.make_default_config(v0, dim, N, K)
+    if O.ref_available():
+        rb = C.create_string_buffer(1 << 16)
+        assert O.ref().ref_make_default_config_json(v0, dim, N, K, rb, len(rb)) == 0
+        assert json.loads(rb.value) == ours
+
+
+def test_no_cpu_fallback_without_gpu():
+    """Creating a device bank on a host without a usable GPU fails loudly (ECUDA/ENOMEM)."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    h = C.c_void_p()
+    rc = abi.lib().ngram_bank_create(json.dumps(_v2(16, 8, 3, 2)).encode(), 0, 0, 1, C.byref(h))
+    assert rc in (abi.NGRAM_ECUDA, abi.NGRAM_ENOMEM)
+    assert not h.value

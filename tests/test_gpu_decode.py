@@ -1,0 +1,202 @@
+"""Incremental decode / speculative verification (device-resident sequence_cache state)
+against the reference's semantics -- mirrors proj/tests/test_cache.cpp, plus the
+reference's own draft_verify outputs (tests/golden/draft_verify.npz)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from helpers import assert_rows_close, dev_i64, dev_u32, gold, gold_config, u64
+from paper_2601_21204_b200 import ngram as G
+from paper_2601_21204_b200.abi import InvalidArgument, OutOfRange
+
+pytestmark = pytest.mark.gpu
+
+
+def small_config(v0=32, dim=384, order=4, k=2, amp="none"):  # test_cache.cpp:15-29, widened to a TC shape
+    sv = [23 + 12 * n + 5 * kk for n in range(2, order + 1) for kk in range(1, k + 1)]
+    return O.make_config(v0, dim, order, k, sv, "subtable_v2", amp)
+
+
+def scratch_ids(cfg, confirmed):  # test_cache.cpp:33-38, via the pinned oracle
+    return O.hash_sequence(cfg, confirmed)[-1]
+
+
+@pytest.fixture
+def bank(cuda):
+    cfg = small_config()
+    hb = O.make_bank(cfg, 5, round_bf16=True)
+    return cfg, hb, G.DeviceBank(cfg).upload(hb.base, hb.sub, hb.proj)
+
+
+def test_first_append_hashes_zero_padded_windows(bank):  # test_cache.cpp:40-52
+    cfg, hb, db = bank
+    st = G.SequenceCache(db)
+    ids = st.append(7)
+    assert ids == [int(x) for x in scratch_ids(cfg, [7])]
+    assert st.length() == 1 and st.last_token() == 7
+
+
+def test_append_stream_equals_batch(bank):  # test_cache.cpp:54-65
+    cfg, hb, db = bank
+    st = G.SequenceCache(db)
+    rng = O.Rng64(1)
+    confirmed = []
+    for _ in range(60):
+        t = rng.below(32)
+        ids = st.append(t)
+        confirmed.append(t)
+        assert ids == [int(x) for x in scratch_ids(cfg, confirmed)]
+
+
+def test_snapshot_rollback_and_stale_handles(bank):  # test_cache.cpp:81-126
+    cfg, hb, db = bank
+    st = G.SequenceCache(db)
+    st.append(5)
+    st.append(9)
+    h = st.snapshot()
+    first = [st.append(t) for t in (1, 2, 3)]
+    st.rollback(h)
+    assert [st.append(t) for t in (1, 2, 3)] == first
+    other = G.SequenceCache(db)
+    with pytest.raises(InvalidArgument):
+        other.rollback(h)
+    h1 = st.snapshot()
+    st.append(1)
+    h2 = st.snapshot()
+    st.append(2)
+    st.rollback(h1)
+    with pytest.raises(InvalidArgument):
+        st.rollback(h2)
+    st.rollback(h)
+    assert st.length() == 2
+
+
+def test_randomized_schedules_match_replay_oracle(bank):  # test_cache.cpp:128-153 (fewer schedules)
+    cfg, hb, db = bank
+    rng = O.Rng64(0xCAFE)
+    for _ in range(8):
+        st = G.SequenceCache(db)
+        confirmed, snaps = [], []
+        for _ in range(25):
+            r = rng.below(10)
+            if r < 6:
+                t = rng.below(32)
+                ids = st.append(t)
+                confirmed.append(t)
+                assert ids == [int(x) for x in scratch_ids(cfg, confirmed)]
+            elif r < 8:
+                snaps.append((st.snapshot(), len(confirmed)))
+            elif snaps:
+                pick = rng.below(len(snaps))
+                st.rollback(snaps[pick][0])
+                confirmed = confirmed[:snaps[pick][1]]
+                snaps = snaps[:pick + 1]
+            assert st.length() == len(confirmed)
+
+
+def test_draft_verify_matches_reference_outputs(cuda):  # cache.cpp:152-195 via the reference itself
+    g = gold("draft_verify.npz")
+    cfg = gold_config(g)
+    hb = O.make_bank(cfg, int(g["seed"]), round_bf16=True)
+    db = G.DeviceBank(cfg).upload(hb.base, hb.sub, hb.proj)
+    for i in range(int(g["ncases"])):
+        st = G.SequenceCache(db)
+        for t in g[f"c{i}_prefix"]:
+            st.append(int(t))
+        acc = int(g[f"c{i}_accept"])
+        out = G.draft_verify(st, db, [int(t) for t in g[f"c{i}_draft"]], acc)
+        assert len(out) == acc
+        if acc:
+            assert_rows_close(np.stack(out), g[f"c{i}_accepted"])
+        assert np.array_equal(st.ring(), g[f"c{i}_ring"])
+        assert st.length() == int(g[f"c{i}_length"]) and st.last_token() == int(g[f"c{i}_last"])
+
+
+def test_draft_verify_accept_all_equals_sequential(bank):  # test_cache.cpp:221-243
+    cfg, hb, db = bank
+    st = G.SequenceCache(db)
+    st.append(11)
+    draft = [3, 1, 4, 1, 5]
+    res = G.draft_verify(st, db, draft, len(draft))
+    _, merged = O.embed_sequence(hb, [11] + draft, double=True)
+    assert_rows_close(np.stack(res), merged[1:])
+    assert st.length() == 6 and st.last_token() == 5 and st.snapshot_depth() == 0
+
+
+def test_draft_verify_accept_none_leaves_state(bank):  # test_cache.cpp:245-262
+    cfg, hb, db = bank
+    st = G.SequenceCache(db)
+    st.append(2)
+    st.append(8)
+    assert G.draft_verify(st, db, [9, 9, 9], 0) == []
+    assert st.length() == 2 and st.last_token() == 8
+    with pytest.raises(InvalidArgument):
+        G.draft_verify(st, db, [9, 9, 9], 4)
+    with pytest.raises(OutOfRange):
+        G.draft_verify(st, db, [9, 99], 1)
+
+
+def test_batched_decode_steps_equal_prefill(bank, cuda):
+    """B streams decoded token by token == the same sequences run through the prefill
+    forward (bit-identical merged rows: same ids, same GEMM tile arithmetic)."""
+    cfg, hb, db = bank
+    B, L = 16, 24
+    rng = np.random.default_rng(1)
+    seqs = rng.integers(0, 32, size=(B, L)).astype(np.uint32)
+    st = G.DecodeState(db, B, max_draft=8)
+    outs, idss = [], []
+    for i in range(L):
+        ids, m = st.step(dev_u32(torch, seqs[:, i], cuda))
+        outs.append(m.clone())
+        idss.append(u64(ids))
+    db.sync_errors()
+    dec = torch.stack(outs, 1).reshape(B * L, -1)
+    off = np.arange(0, B * L + 1, L)
+    _, pre = G.embed_forward(db, dev_u32(torch, seqs.reshape(-1), cuda), dev_i64(torch, off, cuda), rows=False,
+                             merged=True)
+    assert torch.equal(dec, pre)
+    ring, length, last = st.state()
+    assert (length == L).all() and np.array_equal(last, seqs[:, -1]) and np.array_equal(ring, seqs[:, -3:])
+    for s in range(B):
+        want = O.hash_sequence(cfg, seqs[s])
+        assert np.array_equal(np.stack([x[s] for x in idss]), want)
+
+
+def test_batched_verify_and_commit(bank, cuda):
+    """batch 64, draft length 4..8 (config E shape): verify-block rows == prefill rows of
+    confirmed ++ draft; commit(accept) == accept sequential appends (ring, length, last)."""
+    cfg, hb, db = bank
+    B = 64
+    rng = np.random.default_rng(2)
+    hist = [list(rng.integers(0, 32, size=5)) for _ in range(B)]
+    st = G.DecodeState(db, B, max_draft=8)
+    for i in range(5):
+        st.step(dev_u32(torch, [h[i] for h in hist], cuda), want_ids=False, want_merged=False)
+    for L in (4, 8, 6):
+        draft = rng.integers(0, 32, size=(B, L)).astype(np.uint32)
+        out = st.verify(dev_u32(torch, draft, cuda))
+        accept = rng.integers(0, L + 1, size=B).astype(np.int32)
+        st.commit(dev_u32(torch, draft, cuda), torch.from_numpy(accept).to(cuda))
+        db.sync_errors()
+        full = [np.array(h + list(draft[s]), np.uint32) for s, h in enumerate(hist)]
+        off = np.concatenate([[0], np.cumsum([len(f) for f in full])])
+        _, pre = G.embed_forward(db, dev_u32(torch, np.concatenate(full), cuda), dev_i64(torch, off, cuda),
+                                 rows=False, merged=True)
+        for s in range(B):
+            assert torch.equal(out[s], pre[off[s] + len(hist[s]):off[s + 1]])
+        hist = [h + [int(x) for x in draft[s, :accept[s]]] for s, h in enumerate(hist)]
+        ring, length, last = st.state()
+        for s in range(B):
+            assert list(ring[s]) == hist[s][-3:] and int(length[s]) == len(hist[s]) and int(last[s]) == hist[s][-1]
+
+
+def test_commit_rejects_accept_above_draft_length(bank, cuda):
+    cfg, hb, db = bank
+    st = G.DecodeState(db, 4, max_draft=4)
+    draft = dev_u32(torch, np.ones((4, 3), np.uint32), cuda)
+    st.commit(draft, torch.tensor([0, 1, 4, 2], dtype=torch.int32, device=cuda))
+    with pytest.raises(InvalidArgument):
+        st.state()
+    ring, length, last = st.state()
+    assert (length == 0).all()  # whole batch left untouched

@@ -1,0 +1,213 @@
+"""Forward parity (K1 + K2 + K3 / CUDA-core paths) through the C-ABI against the
+reference's own outputs (tests/golden, produced by oracle/_ref) and the pinned oracle.
+Mirrors proj/tests/test_embedding.cpp where a case has a device analogue.
+
+Tolerance (tensor-core path, stated in tests/helpers.py): vs the reference's double
+path on the same bf16-representable bank, per-row max |err| <= 1e-5 * max|row| and
+relL2 <= 1e-6 (fp32 out); bf16 out additionally 2^-8 relative per element.  The
+CUDA-core paths keep the reference's float operation order and are checked bit-exact."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from helpers import assert_rows_close, bf16_to_f32, dev_i64, dev_u32, gold, gold_config
+from paper_2601_21204_b200 import ngram as G
+from paper_2601_21204_b200.abi import OutOfRange
+
+pytestmark = pytest.mark.gpu
+
+
+def _bank(g, cuda, cfg=None):
+    cfg = cfg or gold_config(g)
+    hb = O.make_bank(cfg, int(g["seed"]), round_bf16=True)
+    if "ln_gain" in g.files:
+        hb.gain[:] = g["ln_gain"]
+        hb.bias[:] = g["ln_bias"]
+    ln = cfg["amplification"] == "layer_norm"
+    db = G.DeviceBank(cfg).upload(hb.base, hb.sub, hb.proj, hb.gain if ln else None, hb.bias if ln else None)
+    return hb, db
+
+
+def _forward(db, g, cuda, out_dtype=torch.float32):
+    toks = g["tokens"]
+    off = g["seq_offsets"]
+    prior = None
+    if "prior1" in g.files:
+        p = np.zeros((len(off) - 1, db.N - 1), np.uint32)
+        p[1, -len(g["prior1"]):] = g["prior1"]
+        prior = dev_u32(torch, p, cuda)
+    rows, merged = G.embed_forward(db, dev_u32(torch, toks, cuda), dev_i64(torch, off, cuda), prior=prior,
+                                   rows=True, merged=True, out_dtype=out_dtype)
+    db.sync_errors()
+    cv = (lambda t: t.float().cpu().numpy()) if out_dtype == torch.bfloat16 else (lambda t: t.cpu().numpy())
+    return cv(rows), cv(merged)
+
+
+@pytest.mark.parametrize("amp", ["none", "scale_sqrt_d", "layer_norm"])
+def test_tensor_core_path_matches_reference(cuda, amp):  # embed_sequence_cached, every amplification
+    g = gold(f"embed_tc_{amp}.npz")
+    hb, db = _bank(g, cuda)
+    assert db.tensor_core_path
+    rows, merged = _forward(db, g, cuda)
+    assert_rows_close(merged, g["merged_f64"])
+    assert_rows_close(rows, g["rows_f64"])
+    # and against the reference's own float path (it differs from double by ~1e-7)
+    assert_rows_close(rows, g["rows_f32"])
+
+
+@pytest.mark.parametrize("amp", ["none", "scale_sqrt_d", "layer_norm"])
+def test_tensor_core_path_bf16_out(cuda, amp):
+    g = gold(f"embed_tc_{amp}.npz")
+    hb, db = _bank(g, cuda)
+    rows, merged = _forward(db, g, cuda, torch.bfloat16)
+    assert_rows_close(rows, g["rows_f64"], bf16=True)
+    assert_rows_close(merged, g["merged_f64"], bf16=True)
+
+
+@pytest.mark.parametrize("name", ["embed_simt_v2.npz", "embed_simt_v2_k1.npz", "embed_v1.npz", "embed_v1_wide.npz"])
+def test_cuda_core_paths_bitexact_vs_reference_float(cuda, name):
+    g = gold(name)
+    hb, db = _bank(g, cuda)
+    assert not db.tensor_core_path
+    rows, merged = _forward(db, g, cuda)
+    assert np.array_equal(merged, g["merged_f32"])
+    assert np.array_equal(rows, g["rows_f32"])
+
+
+def test_longcat_width_d3072_matches_reference(cuda):  # D=3072, N=4, K=4: the full K=3072 contraction
+    g = gold("embed_d3072.npz")
+    hb, db = _bank(g, cuda)
+    rows, merged = _forward(db, g, cuda)
+    assert_rows_close(merged, g["merged_f64"])
+    assert_rows_close(rows, g["rows_f64"])
+
+
+def test_first_row_uses_zero_padded_window(cuda):  # test_embedding.cpp:143-153
+    cfg = O.make_default_config(1000, 256, 4, 2)
+    cfg["dim"] = 384  # (N-1)K = 6 -> d = 64, tensor-core shape with a 128-wide N tile
+    hb = O.make_bank(cfg, 7, round_bf16=True)
+    db = G.DeviceBank(cfg).upload(hb.base, hb.sub, hb.proj)
+    rows, _ = G.embed_forward(db, dev_u32(torch, [9], cuda), dev_i64(torch, [0, 1], cuda))
+    padded, _ = G.embed_forward(db, dev_u32(torch, [9], cuda), dev_i64(torch, [0, 1], cuda),
+                                prior=dev_u32(torch, np.zeros((1, 3), np.uint32), cuda))
+    assert torch.equal(rows, padded)
+    ref, _ = O.embed_sequence(hb, [9], double=True)
+    assert_rows_close(rows.cpu().numpy(), ref)
+
+
+def test_split_with_carried_context_equals_whole_sequence(cuda):  # test_embedding.cpp:155-174, bit-exact
+    g = gold("embed_tc_scale_sqrt_d.npz")
+    hb, db = _bank(g, cuda)
+    seq = O.uniform_tokens(5, 1000, 700)
+    whole, _ = G.embed_forward(db, dev_u32(torch, seq, cuda), dev_i64(torch, [0, 700], cuda))
+    for cut in (1, 7, 255, 256, 513):
+        prior = np.zeros((2, 2), np.uint32)
+        prior[1, -min(2, cut):] = seq[max(0, cut - 2):cut]
+        parts, _ = G.embed_forward(db, dev_u32(torch, seq, cuda), dev_i64(torch, [0, cut, 700], cuda),
+                                   prior=dev_u32(torch, prior, cuda))
+        assert torch.equal(whole, parts), cut
+
+
+def test_row_results_independent_of_batch_composition(cuda):
+    g = gold("embed_tc_none.npz")
+    hb, db = _bank(g, cuda)
+    seqs = [O.uniform_tokens(s, 1000, n) for s, n in [(1, 300), (2, 17), (3, 512), (4, 1)]]
+    allt = np.concatenate(seqs)
+    off = np.concatenate([[0], np.cumsum([len(s) for s in seqs])])
+    batch, _ = G.embed_forward(db, dev_u32(torch, allt, cuda), dev_i64(torch, off, cuda))
+    for i, s in enumerate(seqs):
+        alone, _ = G.embed_forward(db, dev_u32(torch, s, cuda), dev_i64(torch, [0, len(s)], cuda))
+        assert torch.equal(alone, batch[off[i]:off[i + 1]])
+    again, _ = G.embed_forward(db, dev_u32(torch, allt, cuda), dev_i64(torch, off, cuda))
+    assert torch.equal(batch, again)  # deterministic
+
+
+def test_zero_bank_embeds_to_zero(cuda):  # test_embedding.cpp:176-181
+    cfg = O.make_default_config(64, 256, 3, 2)
+    cfg["amplification"] = "none"
+    hb = O.make_bank(cfg, 1)
+    for a in [hb.base] + hb.sub + hb.proj:
+        a[:] = 0
+    db = G.DeviceBank(cfg).upload(hb.base, hb.sub, hb.proj)
+    rows, _ = G.embed_forward(db, dev_u32(torch, [1, 2, 3, 4], cuda), dev_i64(torch, [0, 4], cuda))
+    assert (rows == 0).all()
+
+
+def test_linearity_in_tables(cuda):  # test_embedding.cpp:283-299 (scale tables x2: exact in bf16)
+    cfg = O.make_default_config(500, 256, 3, 2)
+    cfg["amplification"] = "none"
+    hb = O.make_bank(cfg, 31)
+    db1 = G.DeviceBank(cfg).upload(hb.base, hb.sub, hb.proj)
+    db2 = G.DeviceBank(cfg).upload(hb.base * 2, [s * 2 for s in hb.sub], hb.proj)
+    t = dev_u32(torch, O.uniform_tokens(3, 500, 300), cuda)
+    off = dev_i64(torch, [0, 300], cuda)
+    a, _ = G.embed_forward(db1, t, off)
+    b, _ = G.embed_forward(db2, t, off)
+    assert torch.equal(a * 2, b)
+
+
+def test_embed_from_ids_equals_forward_merged(cuda):  # embedding.hpp:163-201 (the decode-cache entry)
+    g = gold("embed_tc_scale_sqrt_d.npz")
+    hb, db = _bank(g, cuda)
+    toks = dev_u32(torch, g["tokens"][:100], cuda)
+    off = dev_i64(torch, [0, 100], cuda)
+    ids = G.hash_ids(db, toks, off)
+    m = G.embed_from_ids(db, toks, ids)
+    _, merged = G.embed_forward(db, toks, off, rows=False, merged=True)
+    assert torch.equal(m, merged)
+
+
+def test_out_of_range_token_produces_no_output(cuda):  # hashing.cpp:49-54 / embedding.hpp:41-44
+    g = gold("embed_tc_none.npz")
+    hb, db = _bank(g, cuda)
+    toks = O.uniform_tokens(9, 1000, 256)
+    toks[200] = 5000
+    out = torch.full((256, 256), 7.0, device=cuda)
+    G.embed_forward(db, dev_u32(torch, toks, cuda), dev_i64(torch, [0, 256], cuda), out_rows=out)
+    with pytest.raises(OutOfRange):
+        db.sync_errors()
+    assert (out == 7.0).all()  # nothing written, as the reference throws before writing
+    with pytest.raises(OutOfRange):  # host-buffer entry raises before copying anything back
+        G.embed_sequence(db, toks)
+
+
+def test_host_buffer_entry_equals_device_entry(cuda):  # the drop-in embed_sequence(_cached) path
+    g = gold("embed_tc_layer_norm.npz")
+    hb, db = _bank(g, cuda)
+    seqs = [g["tokens"][:100], g["tokens"][100:]]
+    rows_h, merged_h = G.embed_batch_host(db, seqs, [[], g["prior1"]], want_rows=True, want_merged=True)
+    rows_d, merged_d = _forward(db, g, cuda)
+    assert np.array_equal(rows_h, rows_d) and np.array_equal(merged_h, merged_d)
+    r1, m1 = G.embed_sequence_cached(db, seqs[1], g["prior1"])
+    assert np.array_equal(r1, rows_d[100:])
+    # long batch: crosses the host pipeline's 8192-token chunking, pinned output
+    big = O.uniform_tokens(11, 1000, 20000)
+    pin = torch.empty((20000, 256), dtype=torch.float32).pin_memory()
+    G.embed_batch_host(db, [big], want_rows=True, out_rows=pin.numpy())
+    dev, _ = G.embed_forward(db, dev_u32(torch, big, cuda), dev_i64(torch, [0, 20000], cuda))
+    assert torch.equal(pin, dev.cpu())
+
+
+def test_longcat_scale_bank_sampled_tokens(cuda):
+    """Full config C bank (31.9B params, device-generated) and the 8 x 8192 headline batch:
+    sampled rows against the oracle's double evaluation of the same synthetic bank."""
+    g = gold("cfgC_ids.npz")
+    cfg = gold_config(g)
+    db = G.DeviceBank(cfg)
+    db.generate(1234)
+    T = 8 * 8192
+    toks = np.random.default_rng(42).integers(0, 128000, size=T).astype(np.uint32)
+    off = np.arange(0, T + 1, 8192)
+    rows, merged = G.embed_forward(db, dev_u32(torch, toks, cuda), dev_i64(torch, off, cuda), merged=True)
+    db.sync_errors()
+    ids = G.hash_ids(db, dev_u32(torch, toks, cuda), dev_i64(torch, off, cuda)).cpu().numpy().view(np.uint64)
+    pick = [0, 1, 2, 8191, 8192, 40000, 65535]
+    ref = np.stack([O.synth_embed_merged_f64(1234, toks[t], ids[t], 4, 4, 3072) for t in pick])
+    got = merged[pick].cpu().numpy()
+    assert_rows_close(got, ref)
+    assert_rows_close(rows[pick].cpu().numpy(), ref * np.sqrt(3072.0))
+    # size-independent properties of the whole output: finite, amplification = sqrt(D) * merged
+    assert torch.isfinite(rows).all()
+    assert torch.allclose(rows, merged * np.float32(np.sqrt(3072.0)), rtol=0, atol=0)
+    db.close()
