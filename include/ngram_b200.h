@@ -71,6 +71,11 @@ int ngram_make_default_config(uint32_t base_vocab, int dim, int max_order, int s
  * LayerNorm gain/bias f32.  shard_count > 1 keeps only rank shard_rank's contiguous
  * row block of every sub-table (owner(b,h) = floor(h * shard_count / V_b)). */
 int ngram_bank_create(const char* config_json, int device, int shard_rank, int shard_count, ngram_bank** out);
+/* As ngram_bank_create; flags: NGRAM_BANK_HASH_ONLY allocates no tables (hash_all_orders
+ * needs only the config, hashing.cpp:61-81 -- e.g. moduli far beyond device memory). */
+#define NGRAM_BANK_HASH_ONLY 1
+int ngram_bank_create_ex(const char* config_json, int device, int shard_rank, int shard_count, int flags,
+                         ngram_bank** out);
 int ngram_bank_destroy(ngram_bank* bank);
 /* Upload a reference-layout float bank (make_bank / load_bank output) from HOST memory,
  * converting to bf16 (round-to-nearest-even).  sub[b] / proj[b] indexed by branch_index;

@@ -16,11 +16,12 @@ LIB_PATH = os.path.join(_HERE, "libngram_b200.so")
 NGRAM_OK, NGRAM_EINVAL, NGRAM_ERANGE, NGRAM_EIO, NGRAM_EPARSE = 0, 1, 2, 3, 4
 NGRAM_ECONFIG, NGRAM_ENUMERIC, NGRAM_ECUDA, NGRAM_ENCCL, NGRAM_ENOMEM = 5, 6, 7, 8, 9
 NGRAM_F32, NGRAM_BF16 = 0, 1
+NGRAM_BANK_HASH_ONLY = 1
 
 # Exported symbols, in header order (tests check the .so exports every one).
 SYMBOLS = [
     "ngram_last_error", "ngram_version", "ngram_kernel_launches", "ngram_config_validate",
-    "ngram_make_default_config", "ngram_bank_create", "ngram_bank_destroy", "ngram_bank_upload_f32",
+    "ngram_make_default_config", "ngram_bank_create", "ngram_bank_create_ex", "ngram_bank_destroy", "ngram_bank_upload_f32",
     "ngram_bank_generate", "ngram_bank_load_file", "ngram_bank_reserve", "ngram_bank_get_info",
     "ngram_rolling_hash_batch", "ngram_hash_ids", "ngram_embed_forward", "ngram_embed_from_ids", "ngram_sync_errors",
     "ngram_embed_sequence_host", "ngram_profile_enable", "ngram_profile_read", "ngram_decode_create", "ngram_decode_destroy", "ngram_decode_reset",
@@ -96,6 +97,7 @@ def lib() -> C.CDLL:
         "ngram_config_validate": ([C.c_char_p], i32),
         "ngram_make_default_config": ([u32, i32, i32, i32, C.c_char_p, C.c_size_t], i32),
         "ngram_bank_create": ([C.c_char_p, i32, i32, i32, C.POINTER(vp)], i32),
+        "ngram_bank_create_ex": ([C.c_char_p, i32, i32, i32, i32, C.POINTER(vp)], i32),
         "ngram_bank_destroy": ([vp], i32),
         "ngram_bank_upload_f32": ([vp, vp, vp, vp, vp, vp], i32),
         "ngram_bank_generate": ([vp, u64, vp], i32),

@@ -107,6 +107,11 @@ ngram_bank::~ngram_bank() {
 extern "C" {
 
 int ngram_bank_create(const char* config_json, int device, int shard_rank, int shard_count, ngram_bank** out) {
+    return ngram_bank_create_ex(config_json, device, shard_rank, shard_count, 0, out);
+}
+
+int ngram_bank_create_ex(const char* config_json, int device, int shard_rank, int shard_count, int flags,
+                         ngram_bank** out) {
     NGRAM_API_BEGIN
     if (!config_json || !out) throw Error(NGRAM_EINVAL, "ngram_bank_create: null argument");
     *out = nullptr;
@@ -166,13 +171,17 @@ int ngram_bank_create(const char* config_json, int device, int shard_rank, int s
         rows += hi - lo;
     }
     b->local_rows = rows;
-    b->tc_path = cfg.variant == 1 && B > 0 && d % 64 == 0 && D % 128 == 0 && rows < (int64_t(1) << 31) &&
-                 cfg.base_vocab < (1u << 31);
-
-    b->sub.alloc(size_t(rows) * size_t(d));
-    b->e0.alloc(size_t(cfg.base_vocab) * size_t(D));
-    if (cfg.variant == 1 && B > 0) b->wcat.alloc(size_t(D) * size_t(D));
-    if (cfg.amp == 2) {
+    b->hash_only = (flags & NGRAM_BANK_HASH_ONLY) != 0;
+    b->tc_path = !b->hash_only && cfg.variant == 1 && B > 0 && d % 64 == 0 && D % 128 == 0 &&
+                 rows < (int64_t(1) << 31) && cfg.base_vocab < (1u << 31);
+    if (!b->hash_only) {
+        const double bytes = double(rows) * d * 2 + double(cfg.base_vocab) * D * 2 + double(D) * D * 2;
+        if (bytes > 1.0e15) throw Error(NGRAM_ENOMEM, "bank tables too large for a device");
+        b->sub.alloc(size_t(rows) * size_t(d));
+        b->e0.alloc(size_t(cfg.base_vocab) * size_t(D));
+        if (cfg.variant == 1 && B > 0) b->wcat.alloc(size_t(D) * size_t(D));
+    }
+    if (cfg.amp == 2 && !b->hash_only) {
         b->ln_gain.alloc(size_t(D));
         b->ln_bias.alloc(size_t(D));
         ngk::launch_fill_f32(b->ln_gain.p, 1.0f, D, nullptr);
@@ -232,6 +241,7 @@ int ngram_bank_upload_f32(ngram_bank* b, const float* base, const float* const* 
                           const float* ln_gain, const float* ln_bias) {
     NGRAM_API_BEGIN
     if (!b || !base) throw Error(NGRAM_EINVAL, "ngram_bank_upload_f32: null argument");
+    if (b->hash_only) throw Error(NGRAM_EINVAL, "bank was created hash-only");
     DeviceGuard g(b->device);
     const int B = b->shape.B, D = b->shape.D, d = b->shape.d;
     const size_t chunk = size_t(16) << 20;  // floats per staging chunk (64 MB)
@@ -272,6 +282,7 @@ int ngram_bank_upload_f32(ngram_bank* b, const float* base, const float* const* 
 int ngram_bank_generate(ngram_bank* b, uint64_t seed, void* stream) {
     NGRAM_API_BEGIN
     if (!b) throw Error(NGRAM_EINVAL, "null bank");
+    if (b->hash_only) throw Error(NGRAM_EINVAL, "bank was created hash-only");
     DeviceGuard g(b->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int B = b->shape.B, D = b->shape.D, d = b->shape.d;
@@ -322,6 +333,7 @@ int ngram_bank_reserve(ngram_bank* b, int64_t max_tokens) {
 int ngram_bank_load_file(ngram_bank* b, const char* path) {
     NGRAM_API_BEGIN
     if (!b || !path) throw Error(NGRAM_EINVAL, "null argument");
+    if (b->hash_only) throw Error(NGRAM_EINVAL, "bank was created hash-only");
     DeviceGuard g(b->device);
     std::unique_ptr<FILE, int (*)(FILE*)> f(std::fopen(path, "rb"), &std::fclose);
     if (!f) throw Error(NGRAM_EIO, std::string("cannot open bank file: ") + path);

@@ -84,6 +84,7 @@ struct ngram_bank {
     std::vector<int64_t> row_lo, row_hi, row_base;
     int64_t local_rows = 0;
     bool tc_path = false;
+    bool hash_only = false;  // NGRAM_BANK_HASH_ONLY: no tables, hashing entry points only
 
     ngh::DevBuf<__nv_bfloat16> sub, e0, wcat;
     ngh::DevBuf<float> ln_gain, ln_bias;

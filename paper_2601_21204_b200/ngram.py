@@ -70,11 +70,13 @@ def branch_dim(cfg) -> int:
 class DeviceBank:
     """Device-resident embedding bank (bf16 tables, W_cat, E0)."""
 
-    def __init__(self, cfg: dict, device: int = 0, shard_rank: int = 0, shard_count: int = 1):
+    def __init__(self, cfg: dict, device: int = 0, shard_rank: int = 0, shard_count: int = 1, tables: bool = True):
         self.cfg = cfg
         self.device = device
         h = C.c_void_p()
-        check(abi.lib().ngram_bank_create(json.dumps(cfg).encode(), device, shard_rank, shard_count, C.byref(h)))
+        flags = 0 if tables else abi.NGRAM_BANK_HASH_ONLY
+        check(abi.lib().ngram_bank_create_ex(json.dumps(cfg).encode(), device, shard_rank, shard_count, flags,
+                                             C.byref(h)))
         self.handle = h
         self.info = abi.BankInfo()
         check(abi.lib().ngram_bank_get_info(self.handle, C.byref(self.info)))

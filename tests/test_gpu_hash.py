@@ -123,7 +123,7 @@ def test_config_a_batch_ids_bitexact(cuda, u64_out):
 def test_config_c_ids_with_prior_bitexact(cuda):
     g = gold("cfgC_ids.npz")
     cfg = gold_config(g)
-    bank = G.DeviceBank(cfg)
+    bank = G.DeviceBank(cfg, tables=False)
     prior = np.zeros((2, 3), np.uint32)
     prior[1] = g["prior"]
     ids = G.hash_ids(bank, dev_u32(torch, g["tokens"], cuda), dev_i64(torch, [0, 1024, 2048], cuda),
@@ -133,8 +133,7 @@ def test_config_c_ids_with_prior_bitexact(cuda):
 
 def test_moduli_above_2_32_bitexact(cuda):  # the 128-bit general path
     g = gold("bigmod_ids.npz")
-    bank_cfg = gold_config(g)
-    bank = G.DeviceBank(bank_cfg)
+    bank = G.DeviceBank(gold_config(g), tables=False)
     ids = G.hash_ids(bank, dev_u32(torch, g["tokens"], cuda), dev_i64(torch, [0, 300, 600], cuda))
     assert np.array_equal(u64(ids), g["ids"])
 
@@ -142,7 +141,7 @@ def test_moduli_above_2_32_bitexact(cuda):  # the 128-bit general path
 def test_config_c_full_batch_vs_oracle(cuda):  # all 65536 positions of the headline workload
     g = gold("cfgC_ids.npz")
     cfg = gold_config(g)
-    bank = G.DeviceBank(cfg)
+    bank = G.DeviceBank(cfg, tables=False)
     toks = np.random.default_rng(42).integers(0, 128000, size=8 * 8192).astype(np.uint32)
     off = np.arange(0, 8 * 8192 + 1, 8192)
     ids = u64(G.hash_ids(bank, dev_u32(torch, toks, cuda), dev_i64(torch, off, cuda)))
