@@ -202,6 +202,7 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    sharding = args.sharding if world > 1 else "single"
 
     cfg, nseq, seq_len, label = workload(args.workload)
     if nseq % world != 0:
@@ -210,22 +211,54 @@ def run_ours(args):
     T = my_nseq * seq_len
     total_tokens = nseq * seq_len
     peaks, peak_src = load_peaks()
+    out_dtype = torch.bfloat16 if args.out_dtype == "bf16" else torch.float32
+    esz = 2 if out_dtype == torch.bfloat16 else 4
 
-    bank = G.DeviceBank(cfg, device=local)
-    bank.generate(1234)
-    bank.reserve(T)
     rng = np.random.default_rng(42)
     all_tokens = rng.integers(0, cfg["base_vocab"], size=total_tokens, dtype=np.int64).astype(np.int32)
     toks = torch.from_numpy(all_tokens[rank * T:(rank + 1) * T].copy()).to(dev)
     off = torch.arange(0, T + 1, seq_len, dtype=torch.int64, device=dev)
-    out_dtype = torch.bfloat16 if args.out_dtype == "bf16" else torch.float32
-    rows = torch.empty((T, bank.D), dtype=out_dtype, device=dev)
+    rows = torch.empty((T, (cfg["dim"])), dtype=out_dtype, device=dev)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
-    abi.check(abi.lib().ngram_profile_enable(bank.handle, 1))
 
-    def step():
-        G.embed_forward(bank, toks, off, rows=True, merged=False, out_dtype=out_dtype, out_rows=rows)
+    if sharding == "row":
+        # row-sharded tables: this rank keeps 1/world of every sub-table; rows travel over
+        # NVLink by the fused gather + peer-store kernel; one NCCL all-reduce = barrier
+        bank = G.DeviceBank(cfg, device=local, shard_rank=rank, shard_count=world)
+        bank.generate(1234)
+        group = G.ShardGroup(bank, T)
+        G.connect_shard_groups(group)
+        all_t = torch.empty(total_tokens, dtype=torch.int32, device=dev)
+        all_off = torch.arange(0, total_tokens + 1, seq_len, dtype=torch.int64, device=dev)
+        rank_tok = [r * T for r in range(world + 1)]
+        one = torch.ones(1, dtype=torch.float32, device=dev)
+        sev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+
+        def step(record=False):
+            if record:
+                sev[0].record(stream)
+            dist.all_gather_into_tensor(all_t, toks)  # 4 B/token
+            if record:
+                sev[1].record(stream)
+            group.scatter(all_t, all_off, rank_tok)   # K1 + fused gather / NVLink peer store
+            if record:
+                sev[2].record(stream)
+            dist.all_reduce(one)                      # every rank's rows have landed
+            if record:
+                sev[3].record(stream)
+            group.project(toks, out_dtype=out_dtype, out_rows=rows)  # K3 on the home X
+            if record:
+                sev[4].record(stream)
+    else:
+        bank = G.DeviceBank(cfg, device=local)
+        bank.generate(1234)
+        bank.reserve(T)
+        abi.check(abi.lib().ngram_profile_enable(bank.handle, 1))
+        sbuf = (C.c_float * 3)()
+
+        def step(record=False):
+            G.embed_forward(bank, toks, off, rows=True, merged=False, out_dtype=out_dtype, out_rows=rows)
 
     for _ in range(args.warmup):
         step()
@@ -236,8 +269,8 @@ def run_ours(args):
     clk.start()
     time.sleep(0.3)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    stage = np.zeros((args.steps, 3), np.float32)
-    sbuf = (C.c_float * 3)()
+    nst = 4 if sharding == "row" else 3
+    stage = np.zeros((args.steps, nst), np.float32)
     launches0 = abi.lib().ngram_kernel_launches()
     if world > 1:
         dist.barrier()
@@ -245,10 +278,14 @@ def run_ours(args):
     for i in range(args.steps):
         flush.fill_(i & 0xff)  # > L2 (126 MB): every step starts cold
         ev[i][0].record(stream)
-        step()
+        step(record=True)
         ev[i][1].record(stream)
-        abi.check(abi.lib().ngram_profile_read(bank.handle, sbuf, 3))
-        stage[i] = [sbuf[0], sbuf[1], sbuf[2]]
+        if sharding == "row":
+            sev[4].synchronize()
+            stage[i] = [sev[j].elapsed_time(sev[j + 1]) for j in range(4)]
+        else:
+            abi.check(abi.lib().ngram_profile_read(bank.handle, sbuf, 3))
+            stage[i] = [sbuf[0], sbuf[1], sbuf[2]]
     torch.cuda.synchronize()
     launches = abi.lib().ngram_kernel_launches() - launches0
     if world > 1:
@@ -257,26 +294,39 @@ def run_ours(args):
     bank.sync_errors()
     step_ms = np.array([a.elapsed_time(b) for a, b in ev])
     ms = float(step_ms.mean())
-    hash_ms = float(stage[:, 0].mean())
-    gather_ms = float(stage[:, 1].mean())
-    proj_ms = float(stage[:, 2].mean())
+    st_ms = [float(x) for x in stage.mean(axis=0)]
     if world > 1:
-        t = torch.tensor([ms, hash_ms, gather_ms, proj_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms] + st_ms, dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, hash_ms, gather_ms, proj_ms = [float(x) for x in t.tolist()]
+        ms, st_ms = float(t[0]), [float(x) for x in t[1:].tolist()]
+    if sharding == "row":
+        stages = {"all_gather_tokens": st_ms[0], "k1_k2_scatter_nvlink": st_ms[1], "barrier": st_ms[2],
+                  "k3_projection_epilogue": st_ms[3]}
+        proj_ms = st_ms[3]
+    else:
+        stages = {"k1_hash_index": st_ms[0], "k2_gather": st_ms[1], "k3_projection_epilogue": st_ms[2]}
+        proj_ms = st_ms[2]
 
     # ---------------------------------------------------------------- e2e (host buffers)
-    e2e = None
     e2e_steps = max(2, min(args.steps, 5))
     host_tok = torch.from_numpy(all_tokens[rank * T:(rank + 1) * T].copy()).pin_memory()
     host_out = torch.empty((T, bank.D), dtype=out_dtype).pin_memory()
     host_off = np.arange(0, T + 1, seq_len, dtype=np.int64)
     odt = abi.NGRAM_BF16 if out_dtype == torch.bfloat16 else abi.NGRAM_F32
 
-    def e2e_step():
-        abi.check(abi.lib().ngram_embed_sequence_host(bank.handle, C.c_void_p(host_tok.data_ptr()),
-                                                      host_off.ctypes.data, my_nseq, None,
-                                                      C.c_void_p(host_out.data_ptr()), None, odt))
+    if sharding == "row":
+        def e2e_step():
+            toks.copy_(host_tok, non_blocking=True)
+            step()
+            host_out.copy_(rows, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        e2e_path = "pinned host tokens -> H2D -> all-gather -> scatter -> barrier -> K3 -> D2H pinned embeddings"
+    else:
+        def e2e_step():
+            abi.check(abi.lib().ngram_embed_sequence_host(bank.handle, C.c_void_p(host_tok.data_ptr()),
+                                                          host_off.ctypes.data, my_nseq, None,
+                                                          C.c_void_p(host_out.data_ptr()), None, odt))
+        e2e_path = "ngram_embed_sequence_host (pinned host tokens -> HBM -> pinned host embeddings)"
 
     e2e_step()
     if world > 1:
@@ -289,10 +339,8 @@ def run_ours(args):
         t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    esz = 2 if out_dtype == torch.bfloat16 else 4
     e2e = {"value": total_tokens / e2e_s, "unit": "tokens/s", "h2d_bytes_per_step": int(T * 4 + host_off.nbytes),
-           "d2h_bytes_per_step": int(T * bank.D * esz), "ms_per_step": e2e_s * 1e3,
-           "path": "ngram_embed_sequence_host (pinned host tokens -> HBM -> pinned host embeddings)"}
+           "d2h_bytes_per_step": int(T * bank.D * esz), "ms_per_step": e2e_s * 1e3, "path": e2e_path}
 
     if rank != 0:
         if world > 1:
@@ -305,12 +353,9 @@ def run_ours(args):
     d = D // B
     flops = 2.0 * T * D * D
     tflops = flops / (proj_ms * 1e-3) / 1e12
-    # algorithmic HBM bytes of the fused forward: token + sub rows + E0 row + output
-    bytes_tok = 4 + 2 * B * d + 2 * D + esz * D
+    bytes_tok = 4 + 2 * B * d + 2 * D + esz * D  # token + sub rows + E0 row + output
     hbm_bytes = T * bytes_tok + 2 * D * D
     hbm_gbs = hbm_bytes / (ms * 1e-3) / 1e9
-    hash_bytes = T * (4 + 4 * B)  # tokens in, storage rows out (u32 each)
-    gather_bytes = T * (4 * B + 2 * B * d + 2 * D)  # storage rows in, sub rows in, X out
     nparams, nsub = param_count(cfg)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -322,6 +367,15 @@ def run_ours(args):
                 traffic = tj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
+    hbm = {"achieved_gbs": hbm_gbs, "peak_gbs": peaks["hbm_gbs"], "frac": hbm_gbs / peaks["hbm_gbs"],
+           "algorithmic_bytes_per_token": bytes_tok}
+    if sharding != "row":
+        hash_bytes = T * (4 + 4 * B)
+        gather_bytes = T * (4 * B + 2 * B * d + 2 * D)
+        hbm["k1_hash"] = {"ms": st_ms[0], "gbs": hash_bytes / (st_ms[0] * 1e-3) / 1e9,
+                          "frac": hash_bytes / (st_ms[0] * 1e-3) / 1e9 / peaks["hbm_gbs"]}
+        hbm["k2_gather"] = {"ms": st_ms[1], "gbs": gather_bytes / (st_ms[1] * 1e-3) / 1e9,
+                            "frac": gather_bytes / (st_ms[1] * 1e-3) / 1e9 / peaks["hbm_gbs"]}
     line = {
         "metric": "ngram_embedding_tokens_per_sec", "value": total_tokens / (ms * 1e-3), "unit": "tokens/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -330,22 +384,20 @@ def run_ours(args):
         "config": {"workload": label, "V0": cfg["base_vocab"], "N": cfg["max_order"], "K": cfg["sub_tables"], "D": D,
                    "d": d, "tokens": total_tokens, "sequences": nseq, "seq_len": seq_len,
                    "embedding_params": nparams, "sub_table_params": nsub, "table_dtype": "bf16",
-                   "out_dtype": args.out_dtype, "amplification": cfg["amplification"],
-                   "sharding": "replica" if world > 1 else "single", "l2": "flushed (512 MiB write) between timed steps",
-                   "tensor_core_path": bank.tensor_core_path},
-        "roofline": {"bound": "tensor", "kernel": "forward_tc2_kernel (K3: tcgen05 cta_group::2 projection + base/scale/amplify epilogue)",
+                   "out_dtype": args.out_dtype, "amplification": cfg["amplification"], "sharding": sharding,
+                   "l2": "flushed (512 MiB write) between timed steps", "tensor_core_path": bank.tensor_core_path},
+        "roofline": {"bound": "tensor", "kernel": "forward_tc2_kernel (K3: tcgen05 cta_group::2 projection + "
+                                                  "base/scale/amplify epilogue)",
                      "achieved": tflops, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
                      "frac": tflops / peaks["bf16_tflops"], "traffic": traffic, "peak_source": peak_src,
                      "flops_per_launch": flops, "launch_ms": proj_ms},
-        "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": peaks["hbm_gbs"], "frac": hbm_gbs / peaks["hbm_gbs"],
-                "algorithmic_bytes_per_token": bytes_tok,
-                "hash_stage": {"ms": hash_ms, "gbs": hash_bytes / (hash_ms * 1e-3) / 1e9,
-                               "frac": hash_bytes / (hash_ms * 1e-3) / 1e9 / peaks["hbm_gbs"]},
-                "gather_stage": {"ms": gather_ms, "gbs": gather_bytes / max(gather_ms, 1e-9) / 1e6,
-                                 "frac": gather_bytes / max(gather_ms, 1e-9) / 1e6 / peaks["hbm_gbs"]}},
-        "stages_ms": {"k1_hash_index": hash_ms, "k2_gather": gather_ms, "k3_projection_epilogue": proj_ms},
-        "clocks": clocks, "e2e": e2e, "gpu_launches": int(launches),
+        "hbm": hbm, "stages_ms": stages, "clocks": clocks, "e2e": e2e, "gpu_launches": int(launches),
     }
+    if sharding == "row":
+        remote = T * world * B * d * 2 * (world - 1) / world / world  # rows this rank ships to peers
+        line["nvlink"] = {"remote_bytes_per_rank": remote, "scatter_ms": st_ms[1],
+                          "gbs": remote / (st_ms[1] * 1e-3) / 1e9, "peak_gbs": 770.0,
+                          "frac": remote / (st_ms[1] * 1e-3) / 1e9 / 770.0}
     if world == 1 and not args.no_cpu:
         r = reference_cpu_rate(cfg, args.cpu_seconds)
         if r is not None:
@@ -367,6 +419,8 @@ def main():
     ap.add_argument("--out-dtype", choices=["fp32", "bf16"], default="fp32")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--sharding", choices=["row", "replica"], default="row",
+                    help="N > 1: row-sharded tables (default) or full replicas")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

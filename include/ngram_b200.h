@@ -180,24 +180,37 @@ int ngram_commit(ngram_decode* st, const uint32_t* draft, int L, const int32_t* 
 int ngram_decode_get_state(ngram_decode* st, uint32_t* ring, uint64_t* length, uint32_t* last);
 
 /* ------------------------------------------------------------------ multi-GPU (row shards) */
-/* Peer-memory exchange for row-sharded banks.  A process group of
- * shard_count ranks, one GPU each, shares one exchange buffer per rank (X rows of the
- * home rank's tokens).  ngram_shard_export/open exchange CUDA IPC handles (the caller
- * moves the 64-byte handles between ranks, e.g. with torch.distributed). */
+/* Row-sharded exchange.  A process group of shard_count ranks, one GPU
+ * each; rank r's bank holds its row block of every sub-table.  Each rank owns a
+ * double-buffered X (home tokens x D, bf16).  Per step:
+ *   1. all ranks hold the ALL-GATHERED token batch (4 B/token; the caller all-gathers);
+ *   2. ngram_shard_scatter_rows: K1 over the whole batch, then a fused gather + NVLink
+ *      peer-store kernel writes every locally owned row straight into its home rank's X;
+ *   3. a cross-rank barrier on `stream` (e.g. a 1-element NCCL all-reduce);
+ *   4. ngram_shard_project: K3 on this rank's X (its home tokens) -> rows / merged.
+ * X is double-buffered (scatter i+1 writes the other buffer), so one barrier per step is
+ * enough.  Peer buffers are CUDA IPC mappings: ngram_shard_export writes
+ * NGRAM_SHARD_HANDLE_BYTES that the caller moves to every peer for ngram_shard_open.
+ * ngram_shard_set_peer maps a peer's buffers by device pointer instead (all ranks in one
+ * process: the single-GPU emulation used by the tests). */
+#define NGRAM_SHARD_HANDLE_BYTES 128
+/* Host-only: rank r's row block [lo, hi) of a table of V rows over `count` ranks,
+ * lo = ceil(r*V/count) (owner(h) = floor(h*count/V)).  The partition every bank uses. */
+int ngram_shard_rows(uint64_t V, int rank, int count, int64_t* lo, int64_t* hi);
 typedef struct ngram_shard_group ngram_shard_group;
 int ngram_shard_group_create(ngram_bank* bank, int64_t max_home_tokens, ngram_shard_group** out);
 int ngram_shard_group_destroy(ngram_shard_group* g);
-int ngram_shard_export(ngram_shard_group* g, void* handle64_out);
-int ngram_shard_open(ngram_shard_group* g, int peer_rank, const void* handle64);
-/* Fused gather + NVLink peer store: for the ALL-GATHERED token batch (every rank's
- * tokens, rank r's sequences at all_seq_offsets[r .. r+1] sequences), write every row
- * this rank owns straight into its home rank's X buffer.  Stream-ordered; the caller
- * places a cross-rank barrier (e.g. an NCCL all-reduce on `stream`) before the
- * projection reads X. */
+int ngram_shard_export(ngram_shard_group* g, void* handle_out);
+int ngram_shard_open(ngram_shard_group* g, int peer_rank, const void* handle);
+int ngram_shard_local_buffers(ngram_shard_group* g, void** x0, void** x1);
+int ngram_shard_set_peer(ngram_shard_group* g, int peer_rank, void* x0, void* x1);
+/* all_tokens/all_seq_offsets/all_prior: dev, the gathered batch (sequences of rank r are
+ * [rank_seq_offsets[r], rank_seq_offsets[r+1]) of it); rank_token_offsets: HOST int64
+ * shard_count+1 prefix offsets of each rank's home tokens in all_tokens. */
 int ngram_shard_scatter_rows(ngram_shard_group* g, const uint32_t* all_tokens, const int64_t* all_seq_offsets,
                              int64_t all_nseq, int64_t all_tokens_n, const int64_t* rank_token_offsets,
                              const uint32_t* all_prior, void* stream);
-/* Projection + epilogue for this rank's home tokens from its (now complete) X buffer. */
+/* Projection + epilogue of this rank's home tokens (home_tokens: dev, home_T) from its X. */
 int ngram_shard_project(ngram_shard_group* g, const uint32_t* home_tokens, int64_t home_T, void* rows_out,
                         void* merged_out, int out_dtype, void* stream);
 

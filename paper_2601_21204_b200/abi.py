@@ -17,6 +17,7 @@ NGRAM_OK, NGRAM_EINVAL, NGRAM_ERANGE, NGRAM_EIO, NGRAM_EPARSE = 0, 1, 2, 3, 4
 NGRAM_ECONFIG, NGRAM_ENUMERIC, NGRAM_ECUDA, NGRAM_ENCCL, NGRAM_ENOMEM = 5, 6, 7, 8, 9
 NGRAM_F32, NGRAM_BF16 = 0, 1
 NGRAM_BANK_HASH_ONLY = 1
+NGRAM_SHARD_HANDLE_BYTES = 128
 
 # Exported symbols, in header order (tests check the .so exports every one).
 SYMBOLS = [
@@ -26,8 +27,8 @@ SYMBOLS = [
     "ngram_rolling_hash_batch", "ngram_hash_ids", "ngram_embed_forward", "ngram_embed_from_ids", "ngram_sync_errors",
     "ngram_embed_sequence_host", "ngram_profile_enable", "ngram_profile_read", "ngram_decode_create", "ngram_decode_destroy", "ngram_decode_reset",
     "ngram_decode_step", "ngram_verify_block", "ngram_commit", "ngram_decode_get_state",
-    "ngram_shard_group_create", "ngram_shard_group_destroy", "ngram_shard_export", "ngram_shard_open",
-    "ngram_shard_scatter_rows", "ngram_shard_project",
+    "ngram_shard_rows", "ngram_shard_group_create", "ngram_shard_group_destroy", "ngram_shard_export", "ngram_shard_open",
+    "ngram_shard_local_buffers", "ngram_shard_set_peer", "ngram_shard_scatter_rows", "ngram_shard_project",
 ]
 
 
@@ -119,10 +120,13 @@ def lib() -> C.CDLL:
         "ngram_verify_block": ([vp, vp, i32, vp, i32, vp], i32),
         "ngram_commit": ([vp, vp, i32, vp, vp], i32),
         "ngram_decode_get_state": ([vp, vp, vp, vp], i32),
+        "ngram_shard_rows": ([u64, i32, i32, C.POINTER(i64), C.POINTER(i64)], i32),
         "ngram_shard_group_create": ([vp, i64, C.POINTER(vp)], i32),
         "ngram_shard_group_destroy": ([vp], i32),
         "ngram_shard_export": ([vp, vp], i32),
         "ngram_shard_open": ([vp, i32, vp], i32),
+        "ngram_shard_local_buffers": ([vp, C.POINTER(vp), C.POINTER(vp)], i32),
+        "ngram_shard_set_peer": ([vp, i32, vp, vp], i32),
         "ngram_shard_scatter_rows": ([vp, vp, vp, i64, i64, vp, vp, vp], i32),
         "ngram_shard_project": ([vp, vp, i64, vp, vp, i32, vp], i32),
     }

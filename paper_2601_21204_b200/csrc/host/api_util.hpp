@@ -11,6 +11,7 @@ int set_error(int status, const char* msg);
 }
 
 #define NGRAM_API_BEGIN try {
+#define NGRAM_API_RETURN_OK return NGRAM_OK
 #define NGRAM_API_END                                          \
     }                                                          \
     catch (const ::ngh::Error& e) {                            \

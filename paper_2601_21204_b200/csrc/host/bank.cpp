@@ -203,6 +203,14 @@ int ngram_bank_create_ex(const char* config_json, int device, int shard_rank, in
     NGRAM_API_END
 }
 
+int ngram_shard_rows(uint64_t V, int rank, int count, int64_t* lo, int64_t* hi) {
+    NGRAM_API_BEGIN
+    if (!lo || !hi || count < 1 || rank < 0 || rank >= count) throw Error(NGRAM_EINVAL, "bad shard rank/count");
+    *lo = shard_lo(V, rank, count);
+    *hi = shard_lo(V, rank + 1, count);
+    NGRAM_API_END
+}
+
 int ngram_bank_destroy(ngram_bank* bank) {
     NGRAM_API_BEGIN
     delete bank;

@@ -1,15 +1,156 @@
-// shard.cpp -- placeholder, replaced by the row-sharded exchange.
+// shard.cpp -- C-ABI of the row-sharded multi-GPU path: double-buffered
+// home X buffers shared over CUDA IPC, K1 over the gathered batch + the fused
+// gather/peer-store scatter (kernels/shard.cu), then K3 on the local X.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+#include <vector>
+
 #include "api_util.hpp"
 #include "bank.hpp"
+
+namespace ngh {
+void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, int64_t gstride, int64_t T,
+                    void* rows, void* merged, int out_bf16, float* ln_scratch, const CUtensorMap* tmap_x,
+                    cudaStream_t st, int amp, XBuf* xb);
+void reset_error_word(ngram_bank* b, cudaStream_t st);
+}  // namespace ngh
+
 using namespace ngh;
+
+struct ngram_shard_group {
+    ngram_bank* bank = nullptr;
+    int rank = 0, nranks = 1;
+    int64_t max_home = 0;
+    XBuf x[2];
+    __nv_bfloat16* peer[2][64] = {};
+    std::vector<void*> ipc_mapped;
+    DevBuf<int32_t> grow_all;
+    int parity = 0;  // buffer the next scatter writes and the next project reads
+    ~ngram_shard_group() {
+        for (void* p : ipc_mapped) cudaIpcCloseMemHandle(p);
+    }
+};
+
 extern "C" {
-int ngram_shard_group_create(ngram_bank*, int64_t, ngram_shard_group**) { return set_error(NGRAM_EINVAL, "not built"); }
-int ngram_shard_group_destroy(ngram_shard_group*) { return NGRAM_OK; }
-int ngram_shard_export(ngram_shard_group*, void*) { return set_error(NGRAM_EINVAL, "not built"); }
-int ngram_shard_open(ngram_shard_group*, int, const void*) { return set_error(NGRAM_EINVAL, "not built"); }
-int ngram_shard_scatter_rows(ngram_shard_group*, const uint32_t*, const int64_t*, int64_t, int64_t, const int64_t*,
-                             const uint32_t*, void*) { return set_error(NGRAM_EINVAL, "not built"); }
-int ngram_shard_project(ngram_shard_group*, const uint32_t*, int64_t, void*, void*, int, void*) {
-    return set_error(NGRAM_EINVAL, "not built");
+
+int ngram_shard_group_create(ngram_bank* b, int64_t max_home_tokens, ngram_shard_group** out) {
+    NGRAM_API_BEGIN
+    if (!b || !out || max_home_tokens < 1) throw Error(NGRAM_EINVAL, "ngram_shard_group_create: bad argument");
+    if (!b->tc_path) throw Error(NGRAM_EINVAL, "row-sharded exchange needs the tensor-core shape (d%64, D%128)");
+    if (b->shard_count > 64) throw Error(NGRAM_EINVAL, "at most 64 ranks");
+    *out = nullptr;
+    DeviceGuard dg(b->device);
+    auto g = std::make_unique<ngram_shard_group>();
+    g->bank = b;
+    g->rank = b->shard_rank;
+    g->nranks = b->shard_count;
+    g->max_home = max_home_tokens;
+    for (int i = 0; i < 2; ++i) {
+        g->x[i].ensure(round_up(max_home_tokens, kRowPad), b->shape.D);
+        g->peer[i][g->rank] = g->x[i].x.p;
+    }
+    ensure_workspace(b, max_home_tokens);
+    *out = g.release();
+    NGRAM_API_END
 }
+
+int ngram_shard_group_destroy(ngram_shard_group* g) {
+    NGRAM_API_BEGIN
+    if (g) {
+        DeviceGuard dg(g->bank->device);
+        delete g;
+    }
+    NGRAM_API_END
 }
+
+int ngram_shard_export(ngram_shard_group* g, void* handle_out) {
+    NGRAM_API_BEGIN
+    if (!g || !handle_out) throw Error(NGRAM_EINVAL, "null argument");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    DeviceGuard dg(g->bank->device);
+    cudaIpcMemHandle_t h[2];
+    for (int i = 0; i < 2; ++i) NGH_CUDA(cudaIpcGetMemHandle(&h[i], g->x[i].x.p));
+    std::memcpy(handle_out, h, sizeof(h));
+    NGRAM_API_END
+}
+
+int ngram_shard_open(ngram_shard_group* g, int peer_rank, const void* handle) {
+    NGRAM_API_BEGIN
+    if (!g || !handle || peer_rank < 0 || peer_rank >= g->nranks) throw Error(NGRAM_EINVAL, "bad peer");
+    if (peer_rank == g->rank) NGRAM_API_RETURN_OK;
+    DeviceGuard dg(g->bank->device);
+    cudaIpcMemHandle_t h[2];
+    std::memcpy(h, handle, sizeof(h));
+    for (int i = 0; i < 2; ++i) {
+        void* p = nullptr;
+        NGH_CUDA(cudaIpcOpenMemHandle(&p, h[i], cudaIpcMemLazyEnablePeerAccess));
+        g->ipc_mapped.push_back(p);
+        g->peer[i][peer_rank] = static_cast<__nv_bfloat16*>(p);
+    }
+    NGRAM_API_END
+}
+
+int ngram_shard_local_buffers(ngram_shard_group* g, void** x0, void** x1) {
+    NGRAM_API_BEGIN
+    if (!g || !x0 || !x1) throw Error(NGRAM_EINVAL, "null argument");
+    *x0 = g->x[0].x.p;
+    *x1 = g->x[1].x.p;
+    NGRAM_API_END
+}
+
+int ngram_shard_set_peer(ngram_shard_group* g, int peer_rank, void* x0, void* x1) {
+    NGRAM_API_BEGIN
+    if (!g || !x0 || !x1 || peer_rank < 0 || peer_rank >= g->nranks) throw Error(NGRAM_EINVAL, "bad peer");
+    g->peer[0][peer_rank] = static_cast<__nv_bfloat16*>(x0);
+    g->peer[1][peer_rank] = static_cast<__nv_bfloat16*>(x1);
+    NGRAM_API_END
+}
+
+int ngram_shard_scatter_rows(ngram_shard_group* g, const uint32_t* all_tokens, const int64_t* all_seq_offsets,
+                             int64_t all_nseq, int64_t all_T, const int64_t* rank_token_offsets,
+                             const uint32_t* all_prior, void* stream) {
+    NGRAM_API_BEGIN
+    if (!g || !all_tokens || !all_seq_offsets || !rank_token_offsets || all_nseq < 1 || all_T < 0)
+        throw Error(NGRAM_EINVAL, "ngram_shard_scatter_rows: bad argument");
+    if (rank_token_offsets[0] != 0 || rank_token_offsets[g->nranks] != all_T)
+        throw Error(NGRAM_EINVAL, "rank_token_offsets must span the gathered batch");
+    for (int r = 0; r < g->nranks; ++r) {
+        if (rank_token_offsets[r + 1] < rank_token_offsets[r] ||
+            rank_token_offsets[r + 1] - rank_token_offsets[r] > g->max_home)
+            throw Error(NGRAM_EINVAL, "a rank's home tokens exceed max_home_tokens");
+        if (!g->peer[g->parity][r]) throw Error(NGRAM_EINVAL, "peer " + std::to_string(r) + " not opened");
+    }
+    ngram_bank* b = g->bank;
+    DeviceGuard dg(b->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t Tpad = round_up(std::max<int64_t>(all_T, 1), kRowPad);
+    g->grow_all.ensure(size_t(b->shape.B) * size_t(Tpad));
+    reset_error_word(b, st);
+    if (all_T == 0) NGRAM_API_RETURN_OK;
+    ngk::launch_hash_ids(b->shape, b->ht.p, all_tokens, all_seq_offsets, all_nseq, all_T, all_prior, nullptr, 0,
+                         g->grow_all.p, Tpad, b->err.p, st);
+    ngk::launch_shard_scatter(b->shape, g->grow_all.p, Tpad, rank_token_offsets, g->nranks, b->sub.p,
+                              g->peer[g->parity], all_T, b->err.p, st);
+    NGH_CUDA(cudaGetLastError());
+    NGRAM_API_END
+}
+
+int ngram_shard_project(ngram_shard_group* g, const uint32_t* home_tokens, int64_t home_T, void* rows_out,
+                        void* merged_out, int out_dtype, void* stream) {
+    NGRAM_API_BEGIN
+    if (!g || home_T < 0 || home_T > g->max_home || (home_T > 0 && !home_tokens))
+        throw Error(NGRAM_EINVAL, "ngram_shard_project: bad argument");
+    if (out_dtype != NGRAM_F32 && out_dtype != NGRAM_BF16) throw Error(NGRAM_EINVAL, "bad out_dtype");
+    ngram_bank* b = g->bank;
+    DeviceGuard dg(b->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    XBuf& xb = g->x[g->parity];
+    run_projection(b, home_tokens, nullptr, round_up(std::max<int64_t>(home_T, 1), kRowPad), home_T, rows_out,
+                   merged_out, out_dtype == NGRAM_BF16, b->ws.merged_f32.p, &xb.map, st, -1, nullptr);
+    g->parity ^= 1;
+    NGRAM_API_END
+}
+
+}  // extern "C"

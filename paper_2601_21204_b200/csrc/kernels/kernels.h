@@ -104,11 +104,11 @@ void launch_decode_reset(const Shape& s, uint32_t* ring, uint64_t* length, uint3
                          const uint64_t* lengths, int64_t batch, cudaStream_t st);
 
 // ---- multi-GPU (shard.cu)
-// For every (token, branch) of the all-gathered batch whose bucket row is local, copy
-// the row into X of the token's home rank (peer pointer) at [t_home][b*d .. b*d+d).
-void launch_shard_scatter(const Shape& s, const HashTables* ht, const int32_t* grow_all, int64_t Tpad_all,
-                          const int64_t* rank_token_offsets, int nranks, const __nv_bfloat16* sub,
-                          __nv_bfloat16* const* peer_x, int64_t T_all, const unsigned long long* err,
-                          cudaStream_t st);
+// For every (token, branch) of the all-gathered batch whose bucket row is local (grow >= 0),
+// copy the row into X of the token's home rank (peer pointer) at [t_home][b*d .. b*d+d).
+// rank_token_offsets: host, nranks+1 prefix offsets of each rank's home tokens.
+void launch_shard_scatter(const Shape& s, const int32_t* grow_all, int64_t Tpad_all, const int64_t* rank_token_offsets,
+                          int nranks, const __nv_bfloat16* sub, __nv_bfloat16* const* peer_x, int64_t T_all,
+                          const unsigned long long* err, cudaStream_t st);
 
 }  // namespace ngk

@@ -399,3 +399,82 @@ def draft_verify(state: SequenceCache, bank: DeviceBank, draft: Sequence[int], a
     bank.sync_errors()
     res = out[0, :accept_count].cpu().numpy()
     return [res[i] for i in range(accept_count)]
+
+
+# ----------------------------------------------------------------------------- row shards
+class ShardGroup:
+    """Row-sharded exchange of one rank: double-buffered home X, peer buffers
+    mapped over CUDA IPC (multi-process) or by pointer (single-process emulation)."""
+
+    def __init__(self, bank: DeviceBank, max_home_tokens: int):
+        self.bank = bank
+        self.rank, self.nranks = bank.info.shard_rank, bank.info.shard_count
+        h = C.c_void_p()
+        check(abi.lib().ngram_shard_group_create(bank.handle, max_home_tokens, C.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            abi.lib().ngram_shard_group_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def export_handle(self) -> bytes:
+        buf = C.create_string_buffer(abi.NGRAM_SHARD_HANDLE_BYTES)
+        check(abi.lib().ngram_shard_export(self.handle, buf))
+        return buf.raw
+
+    def open_peer(self, peer_rank: int, handle: bytes) -> None:
+        check(abi.lib().ngram_shard_open(self.handle, peer_rank, handle))
+
+    def local_buffers(self):
+        a, b = C.c_void_p(), C.c_void_p()
+        check(abi.lib().ngram_shard_local_buffers(self.handle, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def set_peer(self, peer_rank: int, bufs) -> None:
+        check(abi.lib().ngram_shard_set_peer(self.handle, peer_rank, C.c_void_p(bufs[0]), C.c_void_p(bufs[1])))
+
+    def scatter(self, all_tokens: torch.Tensor, all_seq_offsets: torch.Tensor, rank_token_offsets,
+                all_prior: Optional[torch.Tensor] = None, stream=None) -> None:
+        rto = np.ascontiguousarray(rank_token_offsets, np.int64)
+        check(abi.lib().ngram_shard_scatter_rows(self.handle, _ptr(all_tokens), _ptr(all_seq_offsets),
+                                                 all_seq_offsets.numel() - 1, all_tokens.numel(), rto.ctypes.data,
+                                                 _ptr(all_prior), _stream(stream)))
+
+    def project(self, home_tokens: torch.Tensor, rows: bool = True, merged: bool = False, out_dtype=torch.float32,
+                stream=None, out_rows: Optional[torch.Tensor] = None, out_merged: Optional[torch.Tensor] = None):
+        T = home_tokens.numel()
+        dev = home_tokens.device
+        if rows and out_rows is None:
+            out_rows = torch.empty((T, self.bank.D), dtype=out_dtype, device=dev)
+        if merged and out_merged is None:
+            out_merged = torch.empty((T, self.bank.D), dtype=out_dtype, device=dev)
+        check(abi.lib().ngram_shard_project(self.handle, _ptr(home_tokens), T, _ptr(out_rows if rows else None),
+                                            _ptr(out_merged if merged else None), _DT[out_dtype], _stream(stream)))
+        return (out_rows if rows else None), (out_merged if merged else None)
+
+
+def connect_shard_groups(group: ShardGroup, pg=None) -> None:
+    """Exchange IPC handles across the torch.distributed process group and map every peer."""
+    import torch.distributed as dist
+    mine = group.export_handle()
+    allh = [None] * dist.get_world_size(pg)
+    dist.all_gather_object(allh, (group.rank, mine), group=pg)
+    for r, h in allh:
+        if r != group.rank:
+            group.open_peer(r, h)
+
+
+def emulate_shards_single_process(groups) -> None:
+    """Map every group's buffers into every other group (all ranks in one process)."""
+    bufs = [g.local_buffers() for g in groups]
+    for g in groups:
+        for r, bb in enumerate(bufs):
+            if r != g.rank:
+                g.set_peer(r, bb)
