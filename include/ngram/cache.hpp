@@ -1,0 +1,95 @@
+// cache.hpp -- drop-in for proj/include/ngram/cache.hpp (cache.hpp:14-136).  The decode
+// state (ring of N-1 tokens, length, last) lives on the device (ngram_decode); appends,
+// verification and the accepted-prefix commit run as kernels.
+#pragma once
+#include <cstdint>
+#include <memory>
+#include <span>
+#include <string>
+#include <vector>
+
+#include "ngram/embedding.hpp"
+
+struct ngram_decode;
+
+namespace ngram {
+
+struct cache_counters {
+    std::uint64_t appends = 0;
+    std::uint64_t rollbacks = 0;
+    std::uint64_t memo_hits = 0;
+    std::uint64_t memo_misses = 0;
+    std::uint64_t table_gathers = 0;
+    std::uint64_t projection_madds = 0;
+    std::uint64_t draft_table_gathers = 0;
+    std::uint64_t verify_table_gathers = 0;
+};
+
+std::string counters_to_json(const cache_counters& c);
+
+struct snapshot_handle {
+    std::uint64_t owner = 0;
+    std::uint64_t serial = 0;
+    std::size_t slot = 0;
+};
+
+class sequence_cache {
+  public:
+    explicit sequence_cache(const device_bank& bank);
+    std::vector<std::uint64_t> append(token_id token, cache_counters* counters = nullptr);
+    snapshot_handle snapshot();
+    void rollback(const snapshot_handle& h, cache_counters* counters = nullptr);
+    void discard(const snapshot_handle& h);
+    std::uint64_t length() const;
+    std::size_t snapshot_depth() const { return snaps_.size(); }
+    token_id last_token() const;
+    const ngram_config& config() const { return bank_->config(); }
+    std::vector<token_id> ring() const;
+    ngram_decode* handle() const { return st_.get(); }
+    const device_bank& bank() const { return *bank_; }
+
+  private:
+    struct snap {
+        std::uint64_t serial, length;
+        token_id last;
+        std::vector<token_id> ring;
+    };
+    void check(const snapshot_handle& h) const;
+    void restore(const snap& s);
+    const device_bank* bank_;
+    std::shared_ptr<ngram_decode> st_;
+    std::uint64_t uid_ = 0, next_serial_ = 1;
+    std::vector<snap> snaps_;
+};
+
+// The memo of the reference (cache.hpp:86-113) is subsumed on the GPU: a verify block
+// computes every draft position's embedding in one launch and the accepted prefix is
+// read from it.  The type is kept so reference call sites compile.
+class embedding_memo {
+  public:
+    explicit embedding_memo(std::size_t capacity) : capacity_(capacity) {
+        if (capacity_ < 1) throw std::invalid_argument("embedding_memo: capacity must be >= 1");
+    }
+    std::size_t capacity() const { return capacity_; }
+    std::size_t size() const { return 0; }
+
+  private:
+    std::size_t capacity_;
+};
+
+struct draft_options {
+    bool conventional_draft_embedding = false;
+};
+
+struct draft_result {
+    std::vector<std::vector<float>> accepted;  // merged (pre-amplification) embeddings
+};
+
+// draft_verify (cache.cpp:152-195): verify block + commit of the accepted prefix.
+draft_result draft_verify(sequence_cache& state, const device_bank& bank, std::span<const token_id> draft,
+                          std::size_t accept_count, cache_counters* counters = nullptr, const draft_options& opts = {});
+draft_result draft_verify(sequence_cache& state, embedding_memo& memo, const device_bank& bank,
+                          std::span<const token_id> draft, std::size_t accept_count, cache_counters* counters = nullptr,
+                          const draft_options& opts = {});
+
+}  // namespace ngram

@@ -1,0 +1,160 @@
+// embedding.hpp -- drop-in for proj/include/ngram/embedding.hpp (hot-path parts).
+//
+// embedding_bank_t<T> stays the reference's host-side parameter store (same layout,
+// same make_bank RNG order -> bit-identical banks).  The forward runs on the GPU:
+// a device_bank holds the B200 layout (bf16 tables, W_cat, E0) and every embed_* call
+// goes through the C-ABI (no CPU fallback).  The overloads taking a host
+// embedding_bank_t<float> keep reference call sites compiling: they upload to a
+// transient device_bank per call (convenience for small banks); production code keeps
+// a device_bank.
+#pragma once
+#include <cmath>
+#include <cstdint>
+#include <memory>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "ngram/config.hpp"
+#include "ngram/errors.hpp"
+#include "ngram/hashing.hpp"
+#include "ngram/rng.hpp"
+
+struct ngram_bank;
+
+namespace ngram {
+
+struct embed_counters {
+    std::uint64_t table_gathers = 0;
+    std::uint64_t projection_madds = 0;
+};
+
+template <typename T>
+struct embedding_bank_t {
+    ngram_config config;
+    std::vector<T> base;
+    std::vector<std::vector<T>> sub_tables;
+    std::vector<std::vector<T>> projections;
+    std::vector<T> ln_gain;
+    std::vector<T> ln_bias;
+
+    std::span<const T> base_row(token_id t) const {
+        if (std::uint64_t(t) >= config.base_vocab)
+            throw std::out_of_range("embedding: token " + std::to_string(t) + " out of range for base vocabulary " +
+                                    std::to_string(config.base_vocab));
+        return std::span<const T>(base).subspan(std::size_t(t) * std::size_t(config.dim), std::size_t(config.dim));
+    }
+    std::span<T> base_row(token_id t) {
+        auto r = static_cast<const embedding_bank_t&>(*this).base_row(t);
+        return {const_cast<T*>(r.data()), r.size()};
+    }
+    std::span<const T> sub_row(int branch, std::uint64_t bucket) const {
+        const auto& table = sub_tables.at(std::size_t(branch));
+        const std::size_t w = std::size_t(config.branch_dim());
+        if ((bucket + 1) * w > table.size())
+            throw std::out_of_range("embedding: bucket " + std::to_string(bucket) + " out of range for sub-table " +
+                                    std::to_string(branch));
+        return std::span<const T>(table).subspan(std::size_t(bucket) * w, w);
+    }
+    std::span<T> sub_row(int branch, std::uint64_t bucket) {
+        auto r = static_cast<const embedding_bank_t&>(*this).sub_row(branch, bucket);
+        return {const_cast<T*>(r.data()), r.size()};
+    }
+};
+
+using embedding_bank = embedding_bank_t<float>;
+
+// make_bank (embedding.hpp:76-110): identical RNG consumption order.
+template <typename T>
+embedding_bank_t<T> make_bank(const ngram_config& cfg, std::uint64_t seed) {
+    cfg.validate();
+    embedding_bank_t<T> bank;
+    bank.config = cfg;
+    rng64 g(seed);
+    const std::size_t D = std::size_t(cfg.dim), d = std::size_t(cfg.branch_dim());
+    bank.base.resize(std::size_t(cfg.base_vocab) * D);
+    for (auto& x : bank.base) x = T(0.02 * gaussian(g));
+    const int B = cfg.branch_count();
+    bank.sub_tables.resize(std::size_t(B));
+    bank.projections.resize(cfg.variant == ne_variant::subtable_v2 ? std::size_t(B) : 0);
+    for (int n = 2; n <= cfg.max_order; ++n)
+        for (int k = 1; k <= cfg.sub_tables; ++k) {
+            const int b = cfg.branch_index(n, k);
+            auto& tab = bank.sub_tables[std::size_t(b)];
+            tab.resize(std::size_t(cfg.vocab_of(n, k)) * d);
+            for (auto& x : tab) x = T(0.02 * gaussian(g));
+            if (cfg.variant == ne_variant::subtable_v2) {
+                auto& p = bank.projections[std::size_t(b)];
+                p.resize(D * d);
+                const double sigma = 0.02 / std::sqrt(double(d));
+                for (auto& x : p) x = T(sigma * gaussian(g));
+            }
+        }
+    if (cfg.amplification == amp_mode::layer_norm) {
+        bank.ln_gain.assign(D, T(1));
+        bank.ln_bias.assign(D, T(0));
+    }
+    return bank;
+}
+
+template <typename T>
+embedding_bank_t<T> make_zero_bank(const ngram_config& cfg) {
+    auto bank = make_bank<T>(cfg, 0);
+    for (auto* v : {&bank.base}) std::fill(v->begin(), v->end(), T(0));
+    for (auto& t : bank.sub_tables) std::fill(t.begin(), t.end(), T(0));
+    for (auto& p : bank.projections) std::fill(p.begin(), p.end(), T(0));
+    return bank;
+}
+
+// The B200-resident bank (include/ngram_b200.h, ngram_bank).
+class device_bank {
+  public:
+    explicit device_bank(const ngram_config& cfg, int device = 0, int shard_rank = 0, int shard_count = 1);
+    explicit device_bank(const embedding_bank& host, int device = 0);  // upload (f32 -> bf16)
+    static device_bank from_file(const std::string& path, const ngram_config& cfg, int device = 0);  // save_bank format
+    void upload(const embedding_bank& host);
+    void generate(std::uint64_t seed);  // synthetic LongCat-scale tables, on device
+    const ngram_config& config() const { return cfg_; }
+    ngram_bank* handle() const { return h_.get(); }
+    bool tensor_core_path() const;
+
+  private:
+    ngram_config cfg_;
+    std::shared_ptr<ngram_bank> h_;
+};
+
+// embed_from_ids (embedding.hpp:163-201): merged, pre-amplification.
+void embed_from_ids(token_id token, std::span<const std::uint64_t> ids, const device_bank& bank, std::span<float> out,
+                    embed_counters* counters = nullptr);
+void embed_from_ids(token_id token, std::span<const std::uint64_t> ids, const embedding_bank& bank,
+                    std::span<float> out, embed_counters* counters = nullptr);
+
+// embed_window / embed_v1 / embed_v2 (embedding.hpp:205-237): merged embedding of one window.
+void embed_window(std::span<const token_id> context, const device_bank& bank, std::span<float> out,
+                  embed_counters* counters = nullptr);
+std::vector<float> embed_v1(std::span<const token_id> context, const device_bank& bank);
+std::vector<float> embed_v2(std::span<const token_id> context, const device_bank& bank);
+
+template <typename T>
+struct sequence_embedding {
+    std::vector<T> rows;    // len x D, amplified
+    std::vector<T> merged;  // len x D, before amplification
+};
+
+// embed_sequence(_cached) (embedding.hpp:409-436).
+sequence_embedding<float> embed_sequence_cached(std::span<const token_id> tokens, const device_bank& bank,
+                                                std::span<const token_id> prior_context = {},
+                                                embed_counters* counters = nullptr);
+std::vector<float> embed_sequence(std::span<const token_id> tokens, const device_bank& bank,
+                                  std::span<const token_id> prior_context = {});
+sequence_embedding<float> embed_sequence_cached(std::span<const token_id> tokens, const embedding_bank& bank,
+                                                std::span<const token_id> prior_context = {},
+                                                embed_counters* counters = nullptr);
+std::vector<float> embed_sequence(std::span<const token_id> tokens, const embedding_bank& bank,
+                                  std::span<const token_id> prior_context = {});
+
+// Batched extension: many sequences in one launch (rows concatenated, len_total x D).
+std::vector<float> embed_batch(const std::vector<std::vector<token_id>>& sequences, const device_bank& bank);
+
+}  // namespace ngram

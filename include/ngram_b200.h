@@ -153,6 +153,16 @@ int ngram_embed_sequence_host(ngram_bank* bank, const uint32_t* tokens, const in
 int ngram_profile_enable(ngram_bank* bank, int enable);
 int ngram_profile_read(ngram_bank* bank, float* stage_ms, int n);
 
+/* Host-buffer variants (synchronous) used by the C++ drop-in layer (include/ngram/*.hpp):
+ * same semantics as the device entries above, all pointers host memory. */
+int ngram_hash_ids_host(ngram_bank* bank, const uint32_t* tokens, const int64_t* seq_offsets, int64_t nseq,
+                        const uint32_t* prior, uint64_t* ids_out);
+int ngram_rolling_hash_host(const uint32_t* windows, int64_t stride, const int32_t* lengths, const int32_t* orders,
+                            const uint64_t* bases, const uint64_t* moduli, int64_t count, uint64_t* out,
+                            int32_t* status);
+int ngram_embed_from_ids_host(ngram_bank* bank, const uint32_t* tokens, const uint64_t* ids, int64_t T,
+                              float* merged_out);
+
 /* ------------------------------------------------------------------ decode / verify */
 /* A batch of `batch` decode streams (sequence_cache, cache.hpp:38-80): per-stream ring
  * of the trailing N-1 confirmed tokens (zero-initialised), length and last token,
@@ -176,6 +186,11 @@ int ngram_verify_block(ngram_decode* st, const uint32_t* draft, int L, void* mer
 /* Accept the first accept[s] (0..L) draft tokens of every stream: the state afterwards
  * equals accept[s] sequential appends (cache.cpp:185-193); accept > L -> EINVAL. */
 int ngram_commit(ngram_decode* st, const uint32_t* draft, int L, const int32_t* accept, void* stream);
+/* Host-buffer variants of reset / step / verify+commit for the C++ sequence_cache / draft_verify. */
+int ngram_decode_reset_host(ngram_decode* st, const uint32_t* prior, const uint64_t* lengths);
+int ngram_decode_step_host(ngram_decode* st, const uint32_t* tokens, uint64_t* ids_out, float* merged_out);
+int ngram_verify_commit_host(ngram_decode* st, const uint32_t* draft, int L, const int32_t* accept,
+                             float* merged_out);
 /* Read back the state (host buffers): ring batch x (N-1), length, last token. */
 int ngram_decode_get_state(ngram_decode* st, uint32_t* ring, uint64_t* length, uint32_t* last);
 

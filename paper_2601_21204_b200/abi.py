@@ -25,8 +25,11 @@ SYMBOLS = [
     "ngram_make_default_config", "ngram_bank_create", "ngram_bank_create_ex", "ngram_bank_destroy", "ngram_bank_upload_f32",
     "ngram_bank_generate", "ngram_bank_load_file", "ngram_bank_reserve", "ngram_bank_get_info",
     "ngram_rolling_hash_batch", "ngram_hash_ids", "ngram_embed_forward", "ngram_embed_from_ids", "ngram_sync_errors",
-    "ngram_embed_sequence_host", "ngram_profile_enable", "ngram_profile_read", "ngram_decode_create", "ngram_decode_destroy", "ngram_decode_reset",
-    "ngram_decode_step", "ngram_verify_block", "ngram_commit", "ngram_decode_get_state",
+    "ngram_embed_sequence_host", "ngram_hash_ids_host", "ngram_rolling_hash_host", "ngram_embed_from_ids_host",
+    "ngram_profile_enable", "ngram_profile_read", "ngram_decode_create", "ngram_decode_destroy", "ngram_decode_reset",
+    "ngram_decode_step", "ngram_verify_block", "ngram_commit", "ngram_decode_reset_host", "ngram_decode_step_host",
+    "ngram_verify_commit_host",
+    "ngram_decode_get_state",
     "ngram_shard_rows", "ngram_shard_group_create", "ngram_shard_group_destroy", "ngram_shard_export", "ngram_shard_open",
     "ngram_shard_local_buffers", "ngram_shard_set_peer", "ngram_shard_scatter_rows", "ngram_shard_project",
 ]
@@ -111,6 +114,9 @@ def lib() -> C.CDLL:
         "ngram_embed_from_ids": ([vp, vp, vp, i64, vp, i32, vp], i32),
         "ngram_sync_errors": ([vp, vp], i32),
         "ngram_embed_sequence_host": ([vp, vp, vp, i64, vp, vp, vp, i32], i32),
+        "ngram_hash_ids_host": ([vp, vp, vp, i64, vp, vp], i32),
+        "ngram_rolling_hash_host": ([vp, i64, vp, vp, vp, vp, i64, vp, vp], i32),
+        "ngram_embed_from_ids_host": ([vp, vp, vp, i64, vp], i32),
         "ngram_profile_enable": ([vp, i32], i32),
         "ngram_profile_read": ([vp, C.POINTER(C.c_float), i32], i32),
         "ngram_decode_create": ([vp, i64, i32, C.POINTER(vp)], i32),
@@ -119,6 +125,9 @@ def lib() -> C.CDLL:
         "ngram_decode_step": ([vp, vp, vp, vp, i32, vp], i32),
         "ngram_verify_block": ([vp, vp, i32, vp, i32, vp], i32),
         "ngram_commit": ([vp, vp, i32, vp, vp], i32),
+        "ngram_decode_reset_host": ([vp, vp, vp], i32),
+        "ngram_decode_step_host": ([vp, vp, vp, vp], i32),
+        "ngram_verify_commit_host": ([vp, vp, i32, vp, vp], i32),
         "ngram_decode_get_state": ([vp, vp, vp, vp], i32),
         "ngram_shard_rows": ([u64, i32, i32, C.POINTER(i64), C.POINTER(i64)], i32),
         "ngram_shard_group_create": ([vp, i64, C.POINTER(vp)], i32),

@@ -34,8 +34,10 @@ COMMON = ["-O3", "-std=c++20", "-lineinfo", "-Xcompiler", "-fPIC", "-I" + os.pat
 
 
 def _sources():
-    return sorted(glob.glob(os.path.join(CSRC, "**", "*.cu"), recursive=True) +
-                  glob.glob(os.path.join(CSRC, "**", "*.cpp"), recursive=True))
+    """Sources of libngram_b200.so (kernels + C-ABI host layer); csrc/cxx is the C++ drop-in."""
+    srcs = glob.glob(os.path.join(CSRC, "**", "*.cu"), recursive=True) + \
+        glob.glob(os.path.join(CSRC, "**", "*.cpp"), recursive=True)
+    return sorted(s for s in srcs if os.sep + "cxx" + os.sep not in s)
 
 
 def _headers():
@@ -86,7 +88,36 @@ def build(clean: bool = False, verbose: bool = False) -> str:
         for l in logs:
             if l.strip():
                 print(l)
+    build_cxx()
     return LIB
+
+
+CXX_LIB = os.path.join(PKG, "libngram.so")
+CXX_TEST = os.path.join(ROOT, "tests", "cxx", "test_dropin")  # git-ignored, travels with the snapshot
+
+
+def build_cxx() -> None:
+    """libngram.so: the C++ drop-in API (include/ngram/*.hpp) over the C-ABI, plus the
+    C++ parity test program tests/cxx/test_dropin.cpp linked against it."""
+    srcs = sorted(glob.glob(os.path.join(CSRC, "cxx", "*.cpp")))
+    hdrs = glob.glob(os.path.join(ROOT, "include", "**", "*.h*"), recursive=True)
+    newest = max(os.path.getmtime(f) for f in srcs + hdrs + [LIB])
+    flags = ["-std=c++20", "-O2", "-fPIC", "-I" + os.path.join(ROOT, "include"), "-isystem", JSON_DIR]
+    if not os.path.exists(CXX_LIB) or os.path.getmtime(CXX_LIB) < newest:
+        cmd = ["g++"] + flags + ["-shared", "-o", CXX_LIB] + srcs + ["-L" + PKG, "-lngram_b200",
+                                                                    "-Wl,-rpath,$ORIGIN"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"g++ failed for libngram.so:\n{r.stderr}")
+    test_src = os.path.join(ROOT, "tests", "cxx", "test_dropin.cpp")
+    if os.path.exists(test_src) and (not os.path.exists(CXX_TEST) or os.path.getmtime(CXX_TEST) <
+                                     max(newest, os.path.getmtime(test_src), os.path.getmtime(CXX_LIB))):
+        os.makedirs(os.path.dirname(CXX_TEST), exist_ok=True)
+        cmd = ["g++"] + flags + ["-o", CXX_TEST, test_src, "-L" + PKG, "-lngram", "-lngram_b200",
+                                 "-Wl,-rpath,$ORIGIN/../../paper_2601_21204_b200"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"g++ failed for test_dropin:\n{r.stderr}")
 
 
 if __name__ == "__main__":

@@ -1,0 +1,443 @@
+// dropin.cpp -- the C++ drop-in API (include/ngram/*.hpp) on top of the C-ABI
+// (include/ngram_b200.h).  Host logic only: argument validation in the reference's
+// order, exception mapping, JSON; every hash / embedding is computed by the
+// CUDA kernels behind libngram_b200.so.  Built as libngram.so (g++), linked to it.
+#include <atomic>
+#include <fstream>
+#include <map>
+#include <mutex>
+#include <sstream>
+
+#include <json.hpp>
+
+#include "ngram/cache.hpp"
+#include "ngram/config.hpp"
+#include "ngram/embedding.hpp"
+#include "ngram/errors.hpp"
+#include "ngram/hashing.hpp"
+#include "ngram_b200.h"
+
+namespace ngram {
+
+void throw_status(int st) {
+    if (st == NGRAM_OK) return;
+    const std::string m = ngram_last_error();
+    switch (st) {
+        case NGRAM_EINVAL: throw std::invalid_argument(m);
+        case NGRAM_ERANGE: throw std::out_of_range(m);
+        case NGRAM_EIO: throw io_error(m);
+        case NGRAM_EPARSE: throw parse_error(m, 0, 0);
+        case NGRAM_ECONFIG: throw config_error(m);
+        case NGRAM_ENUMERIC: throw numeric_error(m);
+        default: throw device_error(m);
+    }
+}
+
+// ------------------------------------------------------------------------ config
+const char* to_string(ne_variant v) { return v == ne_variant::averaged_v1 ? "averaged_v1" : "subtable_v2"; }
+const char* to_string(amp_mode m) {
+    return m == amp_mode::none ? "none" : (m == amp_mode::scale_sqrt_d ? "scale_sqrt_d" : "layer_norm");
+}
+
+std::uint64_t ngram_config::vocab_of(int n, int k) const {
+    const auto it = sub_vocab.find({n, k});
+    if (it == sub_vocab.end())
+        throw std::invalid_argument("ngram_config: missing vocabulary size for (n=" + std::to_string(n) +
+                                    ", k=" + std::to_string(k) + ")");
+    return it->second;
+}
+
+std::string to_json_string(const ngram_config& c) {
+    nlohmann::json j;
+    j["max_order"] = c.max_order;
+    j["sub_tables"] = c.sub_tables;
+    j["base_vocab"] = c.base_vocab;
+    j["dim"] = c.dim;
+    j["variant"] = to_string(c.variant);
+    j["amplification"] = to_string(c.amplification);
+    auto& sv = j["sub_vocab"] = nlohmann::json::array();
+    for (const auto& [nk, v] : c.sub_vocab) sv.push_back({{"n", nk.first}, {"k", nk.second}, {"vocab", v}});
+    return j.dump(2);
+}
+
+void ngram_config::validate() const { throw_status(ngram_config_validate(to_json_string(*this).c_str())); }
+
+ngram_config ngram_config_from_json(const std::string& text) {
+    throw_status(ngram_config_validate(text.c_str()));
+    const auto j = nlohmann::json::parse(text);
+    ngram_config c;
+    c.max_order = j.at("max_order").get<int>();
+    c.sub_tables = j.at("sub_tables").get<int>();
+    c.base_vocab = j.at("base_vocab").get<std::uint32_t>();
+    c.dim = j.at("dim").get<int>();
+    c.variant = j.at("variant").get<std::string>() == "averaged_v1" ? ne_variant::averaged_v1 : ne_variant::subtable_v2;
+    const auto a = j.at("amplification").get<std::string>();
+    c.amplification = a == "none" ? amp_mode::none : (a == "scale_sqrt_d" ? amp_mode::scale_sqrt_d : amp_mode::layer_norm);
+    for (const auto& e : j.at("sub_vocab"))
+        c.sub_vocab[{e.at("n").get<int>(), e.at("k").get<int>()}] = e.at("vocab").get<std::uint64_t>();
+    return c;
+}
+
+ngram_config load_ngram_config(const std::string& path) {
+    std::ifstream in(path);
+    if (!in) throw io_error("cannot open config file: " + path);
+    std::ostringstream ss;
+    ss << in.rdbuf();
+    return ngram_config_from_json(ss.str());
+}
+
+void save_ngram_config(const ngram_config& cfg, const std::string& path) {
+    std::ofstream out(path);
+    if (!out) throw io_error("cannot write config file: " + path);
+    out << to_json_string(cfg) << '\n';
+}
+
+ngram_config make_default_config(std::uint32_t base_vocab, int dim, int max_order, int sub_tables) {
+    std::string buf(1 << 16, '\0');
+    throw_status(ngram_make_default_config(base_vocab, dim, max_order, sub_tables, buf.data(), buf.size()));
+    return ngram_config_from_json(buf.c_str());
+}
+
+// ------------------------------------------------------------------------ banks
+device_bank::device_bank(const ngram_config& cfg, int device, int shard_rank, int shard_count) : cfg_(cfg) {
+    ngram_bank* h = nullptr;
+    throw_status(ngram_bank_create(to_json_string(cfg).c_str(), device, shard_rank, shard_count, &h));
+    h_.reset(h, [](ngram_bank* p) { ngram_bank_destroy(p); });
+}
+
+device_bank::device_bank(const embedding_bank& host, int device) : device_bank(host.config, device) { upload(host); }
+
+device_bank device_bank::from_file(const std::string& path, const ngram_config& cfg, int device) {
+    device_bank b(cfg, device);
+    throw_status(ngram_bank_load_file(b.handle(), path.c_str()));
+    return b;
+}
+
+void device_bank::upload(const embedding_bank& host) {
+    std::vector<const float*> sub, proj;
+    for (const auto& t : host.sub_tables) sub.push_back(t.data());
+    for (const auto& p : host.projections) proj.push_back(p.data());
+    throw_status(ngram_bank_upload_f32(h_.get(), host.base.data(), sub.data(), proj.empty() ? nullptr : proj.data(),
+                                       host.ln_gain.empty() ? nullptr : host.ln_gain.data(),
+                                       host.ln_bias.empty() ? nullptr : host.ln_bias.data()));
+}
+
+void device_bank::generate(std::uint64_t seed) {
+    throw_status(ngram_bank_generate(h_.get(), seed, nullptr));
+    throw_status(ngram_sync_errors(h_.get(), nullptr));
+}
+
+bool device_bank::tensor_core_path() const {
+    ngram_bank_info info;
+    throw_status(ngram_bank_get_info(h_.get(), &info));
+    return info.tensor_core_path != 0;
+}
+
+// ------------------------------------------------------------------------ hashing
+void hash_spec::validate() const {
+    if (order < 2) throw std::invalid_argument("hash_spec: order must be >= 2, got " + std::to_string(order));
+    if (base < 2) throw std::invalid_argument("hash_spec: base must be >= 2, got " + std::to_string(base));
+    if (modulus < 1) throw std::invalid_argument("hash_spec: modulus must be >= 1");
+}
+
+std::uint64_t rolling_hash(std::span<const token_id> window, const hash_spec& spec) {
+    spec.validate();
+    if (window.size() != std::size_t(spec.order))
+        throw std::invalid_argument("rolling_hash: window length " + std::to_string(window.size()) +
+                                    " does not match order " + std::to_string(spec.order));
+    const int32_t len = int32_t(window.size()), order = spec.order;
+    uint64_t out = 0;
+    int32_t status = 0;
+    throw_status(ngram_rolling_hash_host(window.data(), len, &len, &order, &spec.base, &spec.modulus, 1, &out, &status));
+    if (status == NGRAM_ERANGE) throw std::out_of_range("rolling_hash: token out of range for base vocabulary");
+    throw_status(status);
+    return out;
+}
+
+namespace {
+// Hash-only device banks keyed by config: hash_all_orders needs only the config.
+std::shared_ptr<ngram_bank> hasher_for(const ngram_config& cfg) {
+    static std::mutex mu;
+    static std::map<std::string, std::shared_ptr<ngram_bank>> cache;
+    const std::string key = to_json_string(cfg);
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    ngram_bank* h = nullptr;
+    throw_status(ngram_bank_create_ex(key.c_str(), 0, 0, 1, NGRAM_BANK_HASH_ONLY, &h));
+    std::shared_ptr<ngram_bank> p(h, [](ngram_bank* b) { ngram_bank_destroy(b); });
+    cache[key] = p;
+    return p;
+}
+
+std::vector<token_id> prior_tail(std::span<const token_id> prior, int N1) {
+    std::vector<token_id> m(std::size_t(std::max(N1, 0)), 0);
+    const std::size_t n = std::min<std::size_t>(prior.size(), m.size());
+    for (std::size_t i = 0; i < n; ++i) m[m.size() - n + i] = prior[prior.size() - n + i];
+    return m;
+}
+}  // namespace
+
+std::vector<std::uint64_t> hash_all_orders(std::span<const token_id> context, const ngram_config& cfg) {
+    cfg.validate();
+    if (context.size() != std::size_t(cfg.max_order))
+        throw std::invalid_argument("hash_all_orders: context length " + std::to_string(context.size()) +
+                                    " does not match max order " + std::to_string(cfg.max_order));
+    std::vector<std::uint64_t> ids(std::size_t(cfg.branch_count()));
+    if (ids.empty()) return ids;
+    auto h = hasher_for(cfg);
+    const int64_t off[2] = {0, 1};
+    throw_status(ngram_hash_ids_host(h.get(), &context.back(), off, 1, context.data(), ids.data()));
+    return ids;
+}
+
+std::vector<std::uint64_t> hash_sequence(std::span<const token_id> tokens, const device_bank& bank,
+                                         std::span<const token_id> prior_context) {
+    const auto& cfg = bank.config();
+    std::vector<std::uint64_t> ids(tokens.size() * std::size_t(cfg.branch_count()));
+    if (tokens.empty() || ids.empty()) return ids;
+    const auto pr = prior_tail(prior_context, cfg.max_order - 1);
+    const int64_t off[2] = {0, int64_t(tokens.size())};
+    throw_status(ngram_hash_ids_host(bank.handle(), tokens.data(), off, 1, pr.empty() ? nullptr : pr.data(), ids.data()));
+    return ids;
+}
+
+// ------------------------------------------------------------------------ forward
+void embed_from_ids(token_id token, std::span<const std::uint64_t> ids, const device_bank& bank, std::span<float> out,
+                    embed_counters* counters) {
+    const auto& cfg = bank.config();
+    if (ids.size() != std::size_t(cfg.branch_count()))
+        throw std::invalid_argument("embed_from_ids: expected " + std::to_string(cfg.branch_count()) +
+                                    " bucket ids, got " + std::to_string(ids.size()));
+    if (out.size() != std::size_t(cfg.dim)) throw std::invalid_argument("embed_from_ids: output size mismatch");
+    throw_status(ngram_embed_from_ids_host(bank.handle(), &token, ids.data(), 1, out.data()));
+    if (counters) {
+        counters->table_gathers += 1 + std::uint64_t(cfg.branch_count());
+        if (cfg.variant == ne_variant::subtable_v2)
+            counters->projection_madds += std::uint64_t(cfg.dim) * std::uint64_t(cfg.branch_dim()) * cfg.branch_count();
+    }
+}
+
+void embed_from_ids(token_id token, std::span<const std::uint64_t> ids, const embedding_bank& bank,
+                    std::span<float> out, embed_counters* counters) {
+    embed_from_ids(token, ids, device_bank(bank), out, counters);
+}
+
+sequence_embedding<float> embed_sequence_cached(std::span<const token_id> tokens, const device_bank& bank,
+                                                std::span<const token_id> prior_context, embed_counters* counters) {
+    const auto& cfg = bank.config();
+    sequence_embedding<float> r;
+    r.rows.resize(tokens.size() * std::size_t(cfg.dim));
+    r.merged.resize(r.rows.size());
+    if (tokens.empty()) return r;
+    const auto pr = prior_tail(prior_context, cfg.max_order - 1);
+    const int64_t off[2] = {0, int64_t(tokens.size())};
+    throw_status(ngram_embed_sequence_host(bank.handle(), tokens.data(), off, 1, pr.empty() ? nullptr : pr.data(),
+                                           r.rows.data(), r.merged.data(), NGRAM_F32));
+    if (counters) {
+        counters->table_gathers += tokens.size() * (1 + std::uint64_t(cfg.branch_count()));
+        if (cfg.variant == ne_variant::subtable_v2)
+            counters->projection_madds +=
+                tokens.size() * std::uint64_t(cfg.dim) * std::uint64_t(cfg.branch_dim()) * cfg.branch_count();
+    }
+    return r;
+}
+
+std::vector<float> embed_sequence(std::span<const token_id> tokens, const device_bank& bank,
+                                  std::span<const token_id> prior_context) {
+    return embed_sequence_cached(tokens, bank, prior_context).rows;
+}
+
+sequence_embedding<float> embed_sequence_cached(std::span<const token_id> tokens, const embedding_bank& bank,
+                                                std::span<const token_id> prior_context, embed_counters* counters) {
+    return embed_sequence_cached(tokens, device_bank(bank), prior_context, counters);
+}
+
+std::vector<float> embed_sequence(std::span<const token_id> tokens, const embedding_bank& bank,
+                                  std::span<const token_id> prior_context) {
+    return embed_sequence_cached(tokens, device_bank(bank), prior_context).rows;
+}
+
+void embed_window(std::span<const token_id> context, const device_bank& bank, std::span<float> out,
+                  embed_counters* counters) {
+    const auto& cfg = bank.config();
+    if (context.size() != std::size_t(cfg.max_order))
+        throw std::invalid_argument("hash_all_orders: context length " + std::to_string(context.size()) +
+                                    " does not match max order " + std::to_string(cfg.max_order));
+    if (out.size() != std::size_t(cfg.dim)) throw std::invalid_argument("embed_from_ids: output size mismatch");
+    auto r = embed_sequence_cached(context.last(1), bank, context.first(context.size() - 1), counters);
+    std::copy(r.merged.begin(), r.merged.end(), out.begin());
+}
+
+std::vector<float> embed_v1(std::span<const token_id> context, const device_bank& bank) {
+    if (bank.config().variant != ne_variant::averaged_v1)
+        throw std::invalid_argument("embed_v1 requires the averaged variant");
+    std::vector<float> out(std::size_t(bank.config().dim));
+    embed_window(context, bank, out);
+    return out;
+}
+
+std::vector<float> embed_v2(std::span<const token_id> context, const device_bank& bank) {
+    if (bank.config().variant != ne_variant::subtable_v2)
+        throw std::invalid_argument("embed_v2 requires the sub-table variant");
+    std::vector<float> out(std::size_t(bank.config().dim));
+    embed_window(context, bank, out);
+    return out;
+}
+
+std::vector<float> embed_batch(const std::vector<std::vector<token_id>>& seqs, const device_bank& bank) {
+    std::vector<int64_t> off(1, 0);
+    std::vector<token_id> all;
+    for (const auto& s : seqs) {
+        all.insert(all.end(), s.begin(), s.end());
+        off.push_back(int64_t(all.size()));
+    }
+    std::vector<float> rows(all.size() * std::size_t(bank.config().dim));
+    if (seqs.empty()) return rows;
+    throw_status(ngram_embed_sequence_host(bank.handle(), all.data(), off.data(), int64_t(seqs.size()), nullptr,
+                                           rows.data(), nullptr, NGRAM_F32));
+    return rows;
+}
+
+// ------------------------------------------------------------------------ cache
+std::string counters_to_json(const cache_counters& c) {
+    std::ostringstream ss;
+    ss << "{\"appends\":" << c.appends << ",\"rollbacks\":" << c.rollbacks << ",\"memo_hits\":" << c.memo_hits
+       << ",\"memo_misses\":" << c.memo_misses << ",\"table_gathers\":" << c.table_gathers
+       << ",\"projection_madds\":" << c.projection_madds << ",\"draft_table_gathers\":" << c.draft_table_gathers
+       << ",\"verify_table_gathers\":" << c.verify_table_gathers << "}";
+    return ss.str();
+}
+
+namespace {
+std::uint64_t next_uid() {
+    static std::atomic<std::uint64_t> u{1};
+    return u.fetch_add(1);
+}
+constexpr int kMaxDraft = 64;
+}  // namespace
+
+sequence_cache::sequence_cache(const device_bank& bank) : bank_(&bank) {
+    bank.config().validate();
+    ngram_decode* d = nullptr;
+    throw_status(ngram_decode_create(bank.handle(), 1, kMaxDraft, &d));
+    st_.reset(d, [](ngram_decode* p) { ngram_decode_destroy(p); });
+    uid_ = next_uid();
+}
+
+std::vector<std::uint64_t> sequence_cache::append(token_id token, cache_counters* counters) {
+    if (std::uint64_t(token) >= config().base_vocab)
+        throw std::out_of_range("sequence_cache: token " + std::to_string(token) + " out of range");
+    std::vector<std::uint64_t> ids(std::size_t(config().branch_count()));
+    throw_status(ngram_decode_step_host(st_.get(), &token, ids.empty() ? nullptr : ids.data(), nullptr));
+    if (counters) counters->appends++;
+    return ids;
+}
+
+std::uint64_t sequence_cache::length() const {
+    uint64_t len = 0;
+    std::vector<token_id> ring(std::size_t(std::max(config().max_order - 1, 1)));
+    token_id last = 0;
+    throw_status(ngram_decode_get_state(st_.get(), ring.data(), &len, &last));
+    return len;
+}
+
+token_id sequence_cache::last_token() const {
+    uint64_t len = 0;
+    std::vector<token_id> ring(std::size_t(std::max(config().max_order - 1, 1)));
+    token_id last = 0;
+    throw_status(ngram_decode_get_state(st_.get(), ring.data(), &len, &last));
+    return last;
+}
+
+std::vector<token_id> sequence_cache::ring() const {
+    uint64_t len = 0;
+    std::vector<token_id> ring(std::size_t(std::max(config().max_order - 1, 0)));
+    token_id last = 0;
+    throw_status(ngram_decode_get_state(st_.get(), ring.empty() ? nullptr : ring.data(), &len, &last));
+    return ring;
+}
+
+snapshot_handle sequence_cache::snapshot() {
+    snap s;
+    s.serial = next_serial_++;
+    s.ring.assign(std::size_t(std::max(config().max_order - 1, 0)), 0);
+    throw_status(ngram_decode_get_state(st_.get(), s.ring.empty() ? nullptr : s.ring.data(), &s.length, &s.last));
+    snaps_.push_back(std::move(s));
+    return {uid_, snaps_.back().serial, snaps_.size() - 1};
+}
+
+void sequence_cache::check(const snapshot_handle& h) const {
+    if (h.owner != uid_) throw std::invalid_argument("sequence_cache: handle belongs to another state");
+    if (h.slot >= snaps_.size() || snaps_[h.slot].serial != h.serial)
+        throw std::invalid_argument("sequence_cache: stale snapshot handle");
+}
+
+void sequence_cache::restore(const snap& s) {
+    throw_status(ngram_decode_reset_host(st_.get(), s.ring.empty() ? nullptr : s.ring.data(), &s.length));
+}
+
+void sequence_cache::rollback(const snapshot_handle& h, cache_counters* counters) {
+    check(h);
+    restore(snaps_[h.slot]);
+    snaps_.resize(h.slot + 1);
+    if (counters) counters->rollbacks++;
+}
+
+void sequence_cache::discard(const snapshot_handle& h) {
+    check(h);
+    if (h.slot + 1 != snaps_.size()) throw std::invalid_argument("sequence_cache: only the top snapshot can be discarded");
+    snaps_.pop_back();
+}
+
+draft_result draft_verify(sequence_cache& state, const device_bank& bank, std::span<const token_id> draft,
+                          std::size_t accept_count, cache_counters* counters, const draft_options& opts) {
+    if (accept_count > draft.size()) throw std::invalid_argument("draft_verify: accept count exceeds draft length");
+    const auto& cfg = bank.config();
+    for (const token_id t : draft)
+        if (std::uint64_t(t) >= cfg.base_vocab)
+            throw std::out_of_range("sequence_cache: token " + std::to_string(t) + " out of range");
+    draft_result res;
+    const std::size_t D = std::size_t(cfg.dim);
+    std::size_t done = 0, remaining = accept_count;
+    while (done < draft.size()) {  // verify blocks of at most kMaxDraft tokens
+        const int L = int(std::min<std::size_t>(kMaxDraft, draft.size() - done));
+        const int32_t acc = int32_t(std::min<std::size_t>(remaining, std::size_t(L)));
+        std::vector<float> out(std::size_t(L) * D);
+        throw_status(ngram_verify_commit_host(state.handle(), draft.data() + done, L, &acc, out.data()));
+        for (int i = 0; i < acc; ++i) res.accepted.emplace_back(out.begin() + i * D, out.begin() + (i + 1) * D);
+        remaining -= std::size_t(acc);
+        done += std::size_t(L);
+        if (acc < L) break;  // the rest of the draft was rejected
+    }
+    if (counters) {  // the reference's work counters, evaluated arithmetically (cache.cpp:164-192)
+        const std::uint64_t L = draft.size(), A = accept_count, g = 1 + std::uint64_t(cfg.branch_count());
+        const std::uint64_t madds = cfg.variant == ne_variant::subtable_v2
+                                        ? std::uint64_t(cfg.dim) * cfg.branch_dim() * cfg.branch_count()
+                                        : 0;
+        counters->appends += L + A;
+        counters->rollbacks += 1;
+        if (opts.conventional_draft_embedding) {
+            counters->table_gathers += L + A * g;
+            counters->draft_table_gathers += L;
+            counters->verify_table_gathers += A * g;
+            counters->memo_misses += A;
+            counters->projection_madds += A * madds;
+        } else {
+            counters->table_gathers += L * g;
+            counters->draft_table_gathers += L * g;
+            counters->memo_misses += L;
+            counters->memo_hits += A;
+            counters->projection_madds += L * madds;
+        }
+    }
+    return res;
+}
+
+draft_result draft_verify(sequence_cache& state, embedding_memo&, const device_bank& bank,
+                          std::span<const token_id> draft, std::size_t accept_count, cache_counters* counters,
+                          const draft_options& opts) {
+    return draft_verify(state, bank, draft, accept_count, counters, opts);
+}
+
+}  // namespace ngram

@@ -142,4 +142,86 @@ int ngram_decode_get_state(ngram_decode* d, uint32_t* ring, uint64_t* length, ui
     NGRAM_API_END
 }
 
+
+int ngram_decode_reset_host(ngram_decode* d, const uint32_t* prior, const uint64_t* lengths) {
+    NGRAM_API_BEGIN
+    if (!d) throw Error(NGRAM_EINVAL, "null decode state");
+    DeviceGuard g(d->bank->device);
+    const int R = std::max(d->bank->cfg.max_order - 1, 0);
+    DevBuf<uint32_t> pr;
+    DevBuf<uint64_t> le;
+    if (prior && R > 0) {
+        pr.alloc(size_t(d->batch) * size_t(R));
+        NGH_CUDA(cudaMemcpy(pr.p, prior, size_t(d->batch) * size_t(R) * 4, cudaMemcpyHostToDevice));
+    }
+    if (lengths) {
+        le.alloc(size_t(d->batch));
+        NGH_CUDA(cudaMemcpy(le.p, lengths, size_t(d->batch) * 8, cudaMemcpyHostToDevice));
+    }
+    int rc = ngram_decode_reset(d, pr.p, le.p, nullptr);
+    if (rc) return rc;
+    NGH_CUDA(cudaDeviceSynchronize());
+    NGRAM_API_END
+}
+
+int ngram_decode_step_host(ngram_decode* d, const uint32_t* tokens, uint64_t* ids_out, float* merged_out) {
+    NGRAM_API_BEGIN
+    if (!d || !tokens) throw Error(NGRAM_EINVAL, "ngram_decode_step_host: bad argument");
+    DeviceGuard g(d->bank->device);
+    ngram_bank* b = d->bank;
+    for (int64_t s = 0; s < d->batch; ++s)  // the reference validates before mutating (cache.cpp:39-42)
+        if (tokens[s] >= b->cfg.base_vocab)
+            throw Error(NGRAM_ERANGE, "sequence_cache: token " + std::to_string(tokens[s]) + " out of range");
+    DevBuf<uint32_t> t;
+    DevBuf<uint64_t> ids;
+    DevBuf<float> out;
+    t.alloc(size_t(d->batch));
+    NGH_CUDA(cudaMemcpy(t.p, tokens, size_t(d->batch) * 4, cudaMemcpyHostToDevice));
+    if (ids_out) ids.alloc(size_t(d->batch) * size_t(std::max(b->shape.B, 1)));
+    if (merged_out) out.alloc(size_t(d->batch) * size_t(b->cfg.dim));
+    int rc = ngram_decode_step(d, t.p, ids.p, out.p, NGRAM_F32, nullptr);
+    if (rc) return rc;
+    rc = ngram_sync_errors(b, nullptr);
+    if (rc) return rc;
+    if (ids_out && b->shape.B > 0)
+        NGH_CUDA(cudaMemcpy(ids_out, ids.p, size_t(d->batch) * size_t(b->shape.B) * 8, cudaMemcpyDeviceToHost));
+    if (merged_out)
+        NGH_CUDA(cudaMemcpy(merged_out, out.p, size_t(d->batch) * size_t(b->cfg.dim) * 4, cudaMemcpyDeviceToHost));
+    NGRAM_API_END
+}
+
+int ngram_verify_commit_host(ngram_decode* d, const uint32_t* draft, int L, const int32_t* accept,
+                             float* merged_out) {
+    NGRAM_API_BEGIN
+    if (!d || !draft || !accept || L < 1 || L > d->max_draft)
+        throw Error(NGRAM_EINVAL, "ngram_verify_commit_host: bad argument");
+    ngram_bank* b = d->bank;
+    for (int64_t s = 0; s < d->batch; ++s) {
+        if (accept[s] < 0 || accept[s] > L) throw Error(NGRAM_EINVAL, "draft_verify: accept count exceeds draft length");
+        for (int i = 0; i < L; ++i)
+            if (draft[s * L + i] >= b->cfg.base_vocab)
+                throw Error(NGRAM_ERANGE, "sequence_cache: token " + std::to_string(draft[s * L + i]) + " out of range");
+    }
+    DeviceGuard g(b->device);
+    DevBuf<uint32_t> dr;
+    DevBuf<int32_t> ac;
+    DevBuf<float> out;
+    dr.alloc(size_t(d->batch) * size_t(L));
+    ac.alloc(size_t(d->batch));
+    out.alloc(size_t(d->batch) * size_t(L) * size_t(b->cfg.dim));
+    NGH_CUDA(cudaMemcpy(dr.p, draft, size_t(d->batch) * size_t(L) * 4, cudaMemcpyHostToDevice));
+    NGH_CUDA(cudaMemcpy(ac.p, accept, size_t(d->batch) * 4, cudaMemcpyHostToDevice));
+    int rc = ngram_verify_block(d, dr.p, L, out.p, NGRAM_F32, nullptr);
+    if (rc) return rc;
+    rc = ngram_commit(d, dr.p, L, ac.p, nullptr);
+    if (rc) return rc;
+    rc = ngram_sync_errors(b, nullptr);
+    if (rc) return rc;
+    if (merged_out)
+        NGH_CUDA(cudaMemcpy(merged_out, out.p, size_t(d->batch) * size_t(L) * size_t(b->cfg.dim) * 4,
+                            cudaMemcpyDeviceToHost));
+    NGRAM_API_END
+}
+
 }  // extern "C"
+

@@ -325,4 +325,89 @@ int ngram_embed_sequence_host(ngram_bank* b, const uint32_t* tokens, const int64
     NGRAM_API_END
 }
 
+
 }  // extern "C"
+
+// ---------------------------------------------------------------- host-buffer variants
+namespace {
+template <typename T>
+struct HostStage {  // device copy of a host array, freed on scope exit
+    DevBuf<T> d;
+    T* put(const T* h, size_t n) {
+        if (!h || n == 0) return nullptr;
+        d.alloc(n);
+        NGH_CUDA(cudaMemcpy(d.p, h, n * sizeof(T), cudaMemcpyHostToDevice));
+        return d.p;
+    }
+};
+}  // namespace
+
+extern "C" {
+
+int ngram_hash_ids_host(ngram_bank* b, const uint32_t* tokens, const int64_t* seq_offsets, int64_t nseq,
+                        const uint32_t* prior, uint64_t* ids_out) {
+    NGRAM_API_BEGIN
+    if (!b || nseq < 1 || !seq_offsets) throw Error(NGRAM_EINVAL, "ngram_hash_ids_host: bad argument");
+    const int64_t T = seq_offsets[nseq];
+    check_offsets(seq_offsets, nseq, T);
+    if (T == 0) NGRAM_API_RETURN_OK;
+    DeviceGuard g(b->device);
+    HostStage<uint32_t> t, p;
+    HostStage<int64_t> o;
+    DevBuf<uint64_t> ids;
+    ids.alloc(size_t(T) * size_t(std::max(b->shape.B, 1)));
+    const int N1 = std::max(b->cfg.max_order - 1, 0);
+    int rc = ngram_hash_ids(b, t.put(tokens, size_t(T)), o.put(seq_offsets, size_t(nseq + 1)), nseq, T,
+                            N1 > 0 ? p.put(prior, size_t(nseq) * size_t(N1)) : nullptr, ids.p, 1, nullptr);
+    if (rc) return rc;
+    rc = ngram_sync_errors(b, nullptr);
+    if (rc) return rc;
+    if (b->shape.B > 0)
+        NGH_CUDA(cudaMemcpy(ids_out, ids.p, size_t(T) * size_t(b->shape.B) * 8, cudaMemcpyDeviceToHost));
+    NGRAM_API_END
+}
+
+int ngram_rolling_hash_host(const uint32_t* windows, int64_t stride, const int32_t* lengths, const int32_t* orders,
+                            const uint64_t* bases, const uint64_t* moduli, int64_t count, uint64_t* out,
+                            int32_t* status) {
+    NGRAM_API_BEGIN
+    if (count <= 0) NGRAM_API_RETURN_OK;
+    HostStage<uint32_t> w;
+    HostStage<int32_t> l, o;
+    HostStage<uint64_t> ba, mo;
+    DevBuf<uint64_t> dout;
+    DevBuf<int32_t> dst;
+    dout.alloc(size_t(count));
+    dst.alloc(size_t(count));
+    int rc = ngram_rolling_hash_batch(w.put(windows, size_t(count) * size_t(stride)), stride,
+                                      lengths ? l.put(lengths, size_t(count)) : nullptr, o.put(orders, size_t(count)),
+                                      ba.put(bases, size_t(count)), mo.put(moduli, size_t(count)), count, dout.p,
+                                      dst.p, nullptr);
+    if (rc) return rc;
+    NGH_CUDA(cudaMemcpy(out, dout.p, size_t(count) * 8, cudaMemcpyDeviceToHost));
+    NGH_CUDA(cudaMemcpy(status, dst.p, size_t(count) * 4, cudaMemcpyDeviceToHost));
+    NGRAM_API_END
+}
+
+int ngram_embed_from_ids_host(ngram_bank* b, const uint32_t* tokens, const uint64_t* ids, int64_t T,
+                              float* merged_out) {
+    NGRAM_API_BEGIN
+    if (!b || T < 0 || (T > 0 && (!tokens || !ids || !merged_out)))
+        throw Error(NGRAM_EINVAL, "ngram_embed_from_ids_host: bad argument");
+    if (T == 0) NGRAM_API_RETURN_OK;
+    DeviceGuard g(b->device);
+    HostStage<uint32_t> t;
+    HostStage<uint64_t> i;
+    DevBuf<float> out;
+    out.alloc(size_t(T) * size_t(b->cfg.dim));
+    int rc = ngram_embed_from_ids(b, t.put(tokens, size_t(T)), i.put(ids, size_t(T) * size_t(std::max(b->shape.B, 1))),
+                                  T, out.p, NGRAM_F32, nullptr);
+    if (rc) return rc;
+    rc = ngram_sync_errors(b, nullptr);
+    if (rc) return rc;
+    NGH_CUDA(cudaMemcpy(merged_out, out.p, size_t(T) * size_t(b->cfg.dim) * 4, cudaMemcpyDeviceToHost));
+    NGRAM_API_END
+}
+
+}  // extern "C"
+

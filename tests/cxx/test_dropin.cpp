@@ -1,0 +1,255 @@
+// test_dropin.cpp -- the reference's own test cases (proj/tests/test_hashing.cpp,
+// test_embedding.cpp, test_cache.cpp), rewritten against the DROP-IN headers
+// include/ngram/*.hpp: same calls, same expected values / exceptions, executed on the
+// GPU through libngram.so -> libngram_b200.so.  Built by paper_2601_21204_b200/build.py,
+// run by tests/test_gpu_dropin.py.
+#include <cmath>
+#include <cstdio>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "ngram/cache.hpp"
+#include "ngram/config.hpp"
+#include "ngram/embedding.hpp"
+#include "ngram/hashing.hpp"
+
+using namespace ngram;
+
+static int g_fail = 0, g_checks = 0;
+#define CHECK(c)                                                                  \
+    do {                                                                          \
+        ++g_checks;                                                               \
+        if (!(c)) {                                                               \
+            ++g_fail;                                                             \
+            std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #c);              \
+        }                                                                         \
+    } while (0)
+#define CHECK_THROWS_AS(expr, T)                                                  \
+    do {                                                                          \
+        ++g_checks;                                                               \
+        bool ok = false;                                                          \
+        try {                                                                     \
+            (void)(expr);                                                         \
+        } catch (const T&) {                                                      \
+            ok = true;                                                            \
+        } catch (...) {                                                           \
+        }                                                                         \
+        if (!ok) {                                                                \
+            ++g_fail;                                                             \
+            std::printf("FAIL %s:%d: %s does not throw %s\n", __FILE__, __LINE__, #expr, #T); \
+        }                                                                         \
+    } while (0)
+
+static void test_case(const char* name, const std::function<void()>& f) {
+    const int before = g_fail;
+    try {
+        f();
+    } catch (const std::exception& e) {
+        ++g_fail;
+        std::printf("FAIL %s: unexpected exception %s\n", name, e.what());
+    }
+    std::printf("%s %s\n", g_fail == before ? "ok  " : "FAIL", name);
+}
+
+static ngram_config v2_config(std::uint32_t v0, int dim, int order, int k, amp_mode amp = amp_mode::none) {
+    ngram_config cfg;
+    cfg.max_order = order;
+    cfg.sub_tables = k;
+    cfg.base_vocab = v0;
+    cfg.dim = dim;
+    cfg.variant = ne_variant::subtable_v2;
+    cfg.amplification = amp;
+    for (int n = 2; n <= order; ++n)
+        for (int kk = 1; kk <= k; ++kk) cfg.sub_vocab[{n, kk}] = 13 + 8 * std::uint64_t(n) + 3 * std::uint64_t(kk);
+    cfg.validate();
+    return cfg;
+}
+
+static bool close_rows(const std::vector<float>& a, const std::vector<float>& b, double tol = 1e-5) {
+    if (a.size() != b.size()) return false;
+    double mx = 0, err = 0;
+    for (std::size_t i = 0; i < a.size(); ++i) {
+        mx = std::max(mx, std::fabs(double(b[i])));
+        err = std::max(err, std::fabs(double(a[i]) - double(b[i])));
+    }
+    return err <= tol * (mx + 1e-30);
+}
+
+int main() {
+    test_case("rolling_hash worked examples", [] {  // test_hashing.cpp:12-26
+        std::vector<token_id> w{3, 5};
+        CHECK(rolling_hash(w, {2, 10, 7}) == 0);
+        std::vector<token_id> zeros(5, 0);
+        CHECK(rolling_hash(zeros, {5, 1000, 12345}) == 0);
+        CHECK(rolling_hash(std::span(zeros).first(2), {2, 7, 3}) == 0);
+        std::vector<token_id> padded{0, 0, 7};
+        CHECK(rolling_hash(padded, {3, 128000, 13}) == 7);
+    });
+    test_case("rolling_hash input validation", [] {  // test_hashing.cpp:28-38
+        std::vector<token_id> w{1, 2, 3};
+        CHECK_THROWS_AS(rolling_hash(w, {2, 10, 7}), std::invalid_argument);
+        CHECK_THROWS_AS(rolling_hash(w, {4, 10, 7}), std::invalid_argument);
+        std::vector<token_id> oob{1, 12};
+        CHECK_THROWS_AS(rolling_hash(oob, {2, 10, 7}), std::out_of_range);
+        CHECK_THROWS_AS(rolling_hash(w, {3, 1, 7}), std::invalid_argument);
+        CHECK_THROWS_AS(rolling_hash(w, {3, 10, 0}), std::invalid_argument);
+        std::vector<token_id> one{5};
+        CHECK_THROWS_AS(rolling_hash(one, {1, 10, 7}), std::invalid_argument);
+    });
+    test_case("hash_all_orders worked example", [] {  // test_hashing.cpp:83-101
+        ngram_config cfg;
+        cfg.max_order = 3;
+        cfg.sub_tables = 1;
+        cfg.base_vocab = 16;
+        cfg.dim = 4;
+        cfg.variant = ne_variant::averaged_v1;
+        cfg.sub_vocab[{2, 1}] = 101;
+        cfg.sub_vocab[{3, 1}] = 103;
+        std::vector<token_id> ctx{0, 4, 9};
+        const auto ids = hash_all_orders(ctx, cfg);
+        CHECK(ids.size() == 2);
+        CHECK(ids[std::size_t(cfg.branch_index(2, 1))] == 73);
+        CHECK(ids[std::size_t(cfg.branch_index(3, 1))] == 73);
+        std::vector<token_id> zeros{0, 0, 0};
+        for (auto id : hash_all_orders(zeros, cfg)) CHECK(id == 0);
+    });
+    test_case("hash_all_orders matches per-window rolling_hash", [] {  // test_hashing.cpp:122-138
+        ngram_config cfg = make_default_config(50, 24, 4, 2);
+        rng64 rng(99);
+        for (int trial = 0; trial < 50; ++trial) {
+            std::vector<token_id> ctx(4);
+            for (auto& t : ctx) t = token_id(uniform_below(rng, 50));
+            const auto ids = hash_all_orders(ctx, cfg);
+            for (int n = 2; n <= 4; ++n)
+                for (int k = 1; k <= 2; ++k)
+                    CHECK(ids[std::size_t(cfg.branch_index(n, k))] ==
+                          rolling_hash(std::span<const token_id>(ctx).last(std::size_t(n)),
+                                       {n, 50, cfg.vocab_of(n, k)}));
+        }
+        std::vector<token_id> bad{0, 3, 10};
+        CHECK_THROWS_AS(hash_all_orders(bad, make_default_config(10, 12, 3, 2)), std::out_of_range);
+        std::vector<token_id> shortc{3, 4};
+        CHECK_THROWS_AS(hash_all_orders(shortc, make_default_config(10, 12, 3, 2)), std::invalid_argument);
+    });
+    test_case("embed_sequence: first row uses the zero-padded window", [] {  // test_embedding.cpp:143-153
+        const auto cfg = v2_config(16, 12, 4, 2);
+        const auto host = make_bank<float>(cfg, 7);
+        const device_bank bank(host);
+        std::vector<token_id> seq{9};
+        const auto rows = embed_sequence(seq, bank);
+        std::vector<token_id> padded{0, 0, 0, 9};
+        const auto want = embed_v2(padded, bank);
+        CHECK(rows.size() == 12);
+        for (std::size_t i = 0; i < 12; ++i) CHECK(rows[i] == want[i]);  // amp none: rows == merged
+    });
+    test_case("embed_sequence: split with carried context equals whole-sequence run", [] {  // :155-174
+        const auto cfg = v2_config(32, 12, 3, 2, amp_mode::scale_sqrt_d);
+        const device_bank bank(make_bank<float>(cfg, 11));
+        rng64 rng(13);
+        std::vector<token_id> seq(20);
+        for (auto& t : seq) t = token_id(uniform_below(rng, 32));
+        const auto whole = embed_sequence(seq, bank);
+        const std::size_t cut = 7;
+        const auto head = std::span<const token_id>(seq).first(cut);
+        const auto tail = std::span<const token_id>(seq).subspan(cut);
+        const auto p1 = embed_sequence(head, bank);
+        const auto p2 = embed_sequence(tail, bank, head);
+        for (std::size_t i = 0; i < cut * 12; ++i) CHECK(whole[i] == p1[i]);
+        for (std::size_t i = 0; i < (seq.size() - cut) * 12; ++i) CHECK(whole[cut * 12 + i] == p2[i]);
+    });
+    test_case("embed_sequence: zero bank is the zero matrix", [] {  // :176-181
+        const auto cfg = v2_config(8, 6, 3, 1);
+        const device_bank bank(make_zero_bank<float>(cfg));
+        std::vector<token_id> seq{1, 2, 3, 4};
+        for (const float x : embed_sequence(seq, bank)) CHECK(x == 0.0f);
+    });
+    test_case("tensor-core shape: device == host-bank overload == embed_from_ids", [] {
+        auto cfg = make_default_config(500, 256, 3, 2);
+        const auto host = make_bank<float>(cfg, 5);
+        const device_bank bank(host);
+        CHECK(bank.tensor_core_path());
+        rng64 rng(3);
+        std::vector<token_id> seq(300);
+        for (auto& t : seq) t = token_id(uniform_below(rng, 500));
+        const auto a = embed_sequence_cached(seq, bank);
+        const auto b = embed_sequence_cached(seq, host);
+        CHECK(a.rows == b.rows && a.merged == b.merged);
+        const auto ids = hash_sequence(seq, bank);
+        std::vector<float> one(256);
+        embed_from_ids(seq[100], std::span<const std::uint64_t>(ids).subspan(100 * 4, 4), bank, one);
+        CHECK(std::equal(one.begin(), one.end(), a.merged.begin() + 100 * 256));
+        CHECK_THROWS_AS(embed_from_ids(seq[0], std::span<const std::uint64_t>(ids).first(3), bank, one),
+                        std::invalid_argument);
+    });
+    test_case("append stream equals from-scratch batch", [] {  // test_cache.cpp:54-65
+        const auto cfg = v2_config(32, 384, 4, 2);
+        const device_bank bank(make_bank<float>(cfg, 5));
+        sequence_cache state(bank);
+        rng64 rng(1);
+        std::vector<token_id> confirmed;
+        for (int i = 0; i < 40; ++i) {
+            const token_id t = token_id(uniform_below(rng, 32));
+            const auto ids = state.append(t);
+            confirmed.push_back(t);
+            const auto all = hash_sequence(confirmed, bank);
+            CHECK(std::equal(ids.begin(), ids.end(), all.end() - long(ids.size())));
+        }
+        CHECK(state.length() == 40);
+        CHECK_THROWS_AS(state.append(32), std::out_of_range);
+    });
+    test_case("snapshot / rollback / stale handles", [] {  // test_cache.cpp:81-126
+        const auto cfg = v2_config(32, 384, 4, 2);
+        const device_bank bank(make_bank<float>(cfg, 5));
+        sequence_cache a(bank), b(bank);
+        const auto ha = a.snapshot();
+        CHECK_THROWS_AS(b.rollback(ha), std::invalid_argument);
+        const auto h1 = a.snapshot();
+        a.append(1);
+        const auto h2 = a.snapshot();
+        a.append(2);
+        a.rollback(h1);
+        CHECK_THROWS_AS(a.rollback(h2), std::invalid_argument);
+        a.rollback(ha);
+        CHECK(a.length() == 0);
+    });
+    test_case("draft_verify: accept all / none / too many", [] {  // test_cache.cpp:221-262
+        const auto cfg = v2_config(32, 384, 4, 2);
+        const device_bank bank(make_bank<float>(cfg, 9));
+        embedding_memo memo(256);
+        sequence_cache state(bank);
+        state.append(11);
+        std::vector<token_id> draft{3, 1, 4, 1, 5};
+        cache_counters c;
+        const auto result = draft_verify(state, memo, bank, draft, draft.size(), &c);
+        CHECK(result.accepted.size() == 5);
+        std::vector<token_id> seq{11, 3, 1, 4, 1, 5};
+        const auto want = embed_sequence_cached(seq, bank).merged;
+        for (std::size_t i = 0; i < 5; ++i)
+            CHECK(close_rows(result.accepted[i], std::vector<float>(want.begin() + long((i + 1) * 384),
+                                                                    want.begin() + long((i + 2) * 384))));
+        CHECK(state.length() == 6 && state.last_token() == 5 && state.snapshot_depth() == 0);
+        CHECK(c.verify_table_gathers == 0 && c.rollbacks == 1);
+        sequence_cache s2(bank);
+        s2.append(2);
+        s2.append(8);
+        std::vector<token_id> d2{9, 9, 9};
+        CHECK(draft_verify(s2, memo, bank, d2, 0).accepted.empty());
+        CHECK(s2.length() == 2 && s2.last_token() == 8);
+        CHECK_THROWS_AS(draft_verify(s2, memo, bank, d2, 4), std::invalid_argument);
+        CHECK(counters_to_json(c).find("\"rollbacks\":1") != std::string::npos);
+    });
+    test_case("config validation and JSON round-trip", [] {  // test_embedding.cpp:424-444
+        ngram_config cfg = v2_config(16, 8, 3, 2);
+        cfg.dim = 9;
+        CHECK_THROWS_AS(cfg.validate(), std::invalid_argument);
+        ngram_config missing = v2_config(16, 8, 3, 2);
+        missing.sub_vocab.erase({3, 2});
+        CHECK_THROWS_AS(missing.validate(), std::invalid_argument);
+        CHECK_THROWS_AS(v2_config(1, 8, 3, 2), std::invalid_argument);
+        const auto c2 = v2_config(128, 24, 4, 2, amp_mode::layer_norm);
+        CHECK(ngram_config_from_json(to_json_string(c2)) == c2);
+    });
+    std::printf("%d checks, %d failures\n", g_checks, g_fail);
+    return g_fail == 0 ? 0 : 1;
+}
