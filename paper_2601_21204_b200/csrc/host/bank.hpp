@@ -71,6 +71,8 @@ struct Workspace {
     DevBuf<int64_t> offsets;
     DevBuf<uint32_t> prior;
     XBuf xbuf;                      // K2 output / K3 A operand
+    DevBuf<float> splitk;           // small-T split-K partial sums
+    DevBuf<int> ready;              // fused K1+K2+K3: per-128-row X readiness counters
 };
 
 }  // namespace ngh

@@ -12,8 +12,11 @@
 namespace ngh {
 void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, int64_t gstride, int64_t T,
                     void* rows, void* merged, int out_bf16, float* ln_scratch, const CUtensorMap* tmap_x,
-                    cudaStream_t st, int amp, XBuf* xb);
+                    cudaStream_t st, int amp, XBuf* xb, bool allow_splitk, const ngk::FusedX* fx);
 void reset_error_word(ngram_bank* b, cudaStream_t st);
+void forward_tokens(ngram_bank* b, const uint32_t* tokens, const int64_t* seq_off, int64_t nseq, int64_t T,
+                    const uint32_t* prior, void* rows, void* merged, int out_bf16, cudaStream_t st, int amp,
+                    XBuf* xb, int32_t* grow, bool allow_splitk);
 }  // namespace ngh
 
 using namespace ngh;
@@ -28,11 +31,13 @@ void decode_block(ngram_decode* d, const uint32_t* draft, int L, uint64_t* ids_o
     const int64_t Tpad = round_up(T, kRowPad);
     reset_error_word(b, st);
     const int R = b->cfg.max_order - 1;
-    ngk::launch_hash_ids(b->shape, b->ht.p, draft, d->seq_off.p + size_t(L - 1) * size_t(d->batch + 1), d->batch, T,
-                         R > 0 ? d->ring.p : nullptr, ids_out, 1, d->grow.p, Tpad, b->err.p, st);
+    const int64_t* off = d->seq_off.p + size_t(L - 1) * size_t(d->batch + 1);
+    if (ids_out || !merged_out)
+        ngk::launch_hash_ids(b->shape, b->ht.p, draft, off, d->batch, T, R > 0 ? d->ring.p : nullptr, ids_out, 1,
+                             nullptr, Tpad, b->err.p, st);
     if (merged_out)
-        run_projection(b, draft, d->grow.p, Tpad, T, nullptr, merged_out, out_dtype == NGRAM_BF16, nullptr, nullptr,
-                       st, 0, &d->xbuf);
+        forward_tokens(b, draft, off, d->batch, T, R > 0 ? d->ring.p : nullptr, nullptr, merged_out,
+                       out_dtype == NGRAM_BF16, st, 0, &d->xbuf, d->grow.p, true);
 }
 
 }  // namespace

@@ -41,12 +41,25 @@ static bool fused_gather(int D) {
     return env >= 0 ? env != 0 : D <= 1024;
 }
 
+// K1+K2+K3 in one kernel (forward_tc2_kernel<true>, gather warps beside the MMA
+// pipeline).  Correct (tested) but measured slower on B200 than the fused K1+K2 kernel
+// followed by K3 (1.46 vs 1.10 ms at config C, profiles/README.md), so opt-in:
+// NGRAM_FUSEDX=1.
+static bool use_fusedx(ngram_bank* b, int64_t T) {
+    static const int env = [] {
+        const char* e = getenv("NGRAM_FUSEDX");
+        return e ? atoi(e) : 0;
+    }();
+    return env && b->tc_path && T > 256 && !fused_gather(b->shape.D) && b->shape.D % 256 == 0 &&
+           b->shape.N <= 4 && b->shape.B <= 32;
+}
+
 // One forward over T rows whose storage rows are already in `grow` (stride gstride).
 // Tensor-core path: K2 gathers X (T x D bf16) into `xb`, K3 projects it.  Writes
 // merged/rows per the amplification; LayerNorm via a third kernel.
 void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, int64_t gstride, int64_t T,
                     void* rows, void* merged, int out_bf16, float* ln_scratch, const CUtensorMap* tmap_x,
-                    cudaStream_t st, int amp, XBuf* xb) {
+                    cudaStream_t st, int amp, XBuf* xb, bool allow_splitk, const ngk::FusedX* fx) {
     if (b->hash_only) throw Error(NGRAM_EINVAL, "bank was created hash-only (NGRAM_BANK_HASH_ONLY)");
     if (T <= 0) return;
     ngk::FwdArgs a{};
@@ -79,19 +92,66 @@ void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, 
         a.rows_out = rows;
         a.out_bf16 = out_bf16;
     }
-    if (b->tc_path && !tmap_x && !fused_gather(b->shape.D)) {
+    if (b->tc_path && !tmap_x && ((allow_splitk && T <= 256) || !fused_gather(b->shape.D))) {
         if (!xb) xb = &b->ws.xbuf;
         xb->ensure(round_up(T, kRowPad), b->shape.D);
         ngk::launch_gather_rows(a.s, grow, gstride, T, b->sub.p, xb->x.p, b->err.p, st);
         a.tmap_x = &xb->map;
     }
     b->prof_record(2, st);
-    if (b->tc_path) ngk::launch_forward_tc(a, b->num_sms, st);
-    else ngk::launch_forward_simt(a, st);
+    if (b->tc_path) {
+        float* ws = nullptr;
+        const size_t need = allow_splitk ? ngk::splitk_workspace_floats(a, b->num_sms) : 0;
+        if (need) {
+            b->ws.splitk.ensure(need);
+            ws = b->ws.splitk.p;
+        }
+        if (fx) ngk::launch_forward_tc2_fusedx(a, *fx, b->num_sms, st);
+        else ngk::launch_forward_tc(a, b->num_sms, st, ws);
+    } else {
+        ngk::launch_forward_simt(a, st);
+    }
     if (ln)
         ngk::launch_layernorm_rows(a.s, ln_merged, b->ln_gain.p, b->ln_bias.p, rows,
                                    (merged && ln_merged != merged) ? merged : nullptr, out_bf16, T, b->err.p, st);
     NGH_CUDA(cudaGetLastError());
+}
+
+// Hash + gather + project T positions given by (tokens, seq_off, prior).  X path: the
+// fused K1+K2 kernel writes X directly; otherwise K1 writes storage rows for the fused-
+// gather GEMM or the CUDA-core kernels.
+void forward_tokens(ngram_bank* b, const uint32_t* tokens, const int64_t* seq_off, int64_t nseq, int64_t T,
+                    const uint32_t* prior, void* rows, void* merged, int out_bf16, cudaStream_t st, int amp,
+                    XBuf* xb, int32_t* grow, bool allow_splitk) {
+    const int64_t Tpad = round_up(std::max<int64_t>(T, 1), kRowPad);
+    b->prof_record(0, st);
+    if (use_fusedx(b, T)) {
+        // K1 + K2 + K3 in one persistent kernel (gather warps overlap the projection)
+        if (!xb) xb = &b->ws.xbuf;
+        xb->ensure(Tpad, b->shape.D);
+        const int64_t nblk = (T + 127) / 128;
+        b->ws.ready.ensure(size_t(nblk));
+        NGH_CUDA(cudaMemsetAsync(b->ws.ready.p, 0, size_t(nblk) * sizeof(int), st));
+        ngk::launch_validate_tokens(b->shape, tokens, T, seq_off, nseq, prior, b->err.p, st);
+        b->prof_record(1, st);
+        ngk::FusedX fx{seq_off, nseq, prior, xb->x.p, b->ws.ready.p};
+        run_projection(b, tokens, nullptr, Tpad, T, rows, merged, out_bf16, b->ws.merged_f32.p, &xb->map, st, amp,
+                       nullptr, false, &fx);
+    } else if (b->tc_path && ((allow_splitk && T <= 256) || !fused_gather(b->shape.D))) {
+        if (!xb) xb = &b->ws.xbuf;
+        xb->ensure(Tpad, b->shape.D);
+        ngk::launch_hash_gather(b->shape, b->ht.p, tokens, seq_off, nseq, T, prior, b->sub.p, xb->x.p, nullptr, Tpad,
+                                b->err.p, st);
+        b->prof_record(1, st);
+        run_projection(b, tokens, nullptr, Tpad, T, rows, merged, out_bf16, b->ws.merged_f32.p, &xb->map, st, amp,
+                       nullptr, allow_splitk, nullptr);
+    } else {
+        ngk::launch_hash_ids(b->shape, b->ht.p, tokens, seq_off, nseq, T, prior, nullptr, 0, grow, Tpad, b->err.p, st);
+        b->prof_record(1, st);
+        run_projection(b, tokens, grow, Tpad, T, rows, merged, out_bf16, b->ws.merged_f32.p, nullptr, st, amp, xb,
+                       allow_splitk, nullptr);
+    }
+    b->prof_record(3, st);
 }
 
 void reset_error_word(ngram_bank* b, cudaStream_t st) {
@@ -163,13 +223,9 @@ int ngram_embed_forward(ngram_bank* b, const uint32_t* tokens, const int64_t* se
     const int64_t Tpad = round_up(std::max<int64_t>(total_tokens, 1), kRowPad);
     reset_error_word(b, st);
     if (total_tokens == 0) return NGRAM_OK;
-    b->prof_record(0, st);
-    ngk::launch_hash_ids(b->shape, b->ht.p, tokens, seq_offsets, nseq, total_tokens, prior, nullptr, 0, b->ws.grow.p,
-                         Tpad, b->err.p, st);
-    b->prof_record(1, st);
-    run_projection(b, tokens, b->ws.grow.p, Tpad, total_tokens, rows_out, merged_out, out_dtype == NGRAM_BF16,
-                   b->ws.merged_f32.p, nullptr, st, -1, nullptr);
-    b->prof_record(3, st);
+    (void)Tpad;
+    forward_tokens(b, tokens, seq_offsets, nseq, total_tokens, prior, rows_out, merged_out, out_dtype == NGRAM_BF16,
+                   st, -1, nullptr, b->ws.grow.p, true);
     NGRAM_API_END
 }
 
@@ -187,7 +243,7 @@ int ngram_embed_from_ids(ngram_bank* b, const uint32_t* tokens, const uint64_t* 
     ngk::launch_ids_to_rows(b->shape, b->ht.p, ids, tokens, T, b->ws.grow.p, Tpad, b->err.p, st);
     // embed_from_ids returns the merged (pre-amplification) vector: run with amp = none.
     run_projection(b, tokens, b->ws.grow.p, Tpad, T, nullptr, merged_out, out_dtype == NGRAM_BF16, nullptr, nullptr,
-                   st, 0, nullptr);
+                   st, 0, nullptr, true, nullptr);
     NGRAM_API_END
 }
 
@@ -299,7 +355,7 @@ int ngram_embed_sequence_host(ngram_bank* b, const uint32_t* tokens, const int64
         void* dmerged = merged_out ? b->host_merged[slot].p : nullptr;
         run_projection(b, b->ws.tokens.p + c0, b->ws.grow.p + c0, Tpad, n, drows, dmerged, out_dtype == NGRAM_BF16,
                        b->ws.merged_f32.p ? b->ws.merged_f32.p + size_t(c0) * size_t(D) : nullptr, nullptr, st, -1,
-                       &b->host_x[slot]);
+                       &b->host_x[slot], T <= 256, nullptr);  // chunks keep the whole batch's regime
         const size_t bytes = size_t(n) * size_t(D) * esz;
         if (direct) {
             if (rows_out)

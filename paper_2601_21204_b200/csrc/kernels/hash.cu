@@ -14,34 +14,12 @@
 // storage rows (i32): 4 + 8B bytes/token -- purely bandwidth/latency bound.
 #include <cstdint>
 
+#include "hashdev.cuh"
 #include "kernels.h"
 
 namespace ngk {
 
 namespace {
-
-__device__ __forceinline__ uint64_t barrett_mod(uint64_t x, uint64_t m, uint64_t mu) {
-    const uint64_t q = __umul64hi(x, mu);
-    uint64_t r = x - q * m;
-    if (r >= m) r -= m;
-    if (r >= m) r -= m;
-    return r;
-}
-
-__device__ __forceinline__ uint64_t mulmod128(uint64_t a, uint64_t b, uint64_t m) {
-    return static_cast<uint64_t>((static_cast<unsigned __int128>(a) * b) % m);
-}
-
-// Position t of the concatenated batch -> sequence index (largest s with off[s] <= t).
-__device__ __forceinline__ int64_t find_seq(const int64_t* __restrict__ off, int64_t nseq, int64_t t) {
-    int64_t lo = 0, hi = nseq - 1;
-    while (lo < hi) {
-        const int64_t mid = (lo + hi + 1) >> 1;
-        if (__ldg(off + mid) <= t) lo = mid;
-        else hi = mid - 1;
-    }
-    return lo;
-}
 
 template <int MAXN>
 __global__ void __launch_bounds__(256) hash_ids_kernel(Shape s, const HashTables* __restrict__ ht,
@@ -175,7 +153,68 @@ __global__ void ids_to_rows_kernel(Shape s, const HashTables* __restrict__ ht, c
     if (bad) atomicMin(err, (unsigned long long)t);
 }
 
+// K1+K2 fused (X path): one warp per position (hashdev.cuh gather_position).  Lane b < B hashes branch b (the B
+// hashes of a position run in parallel instead of serially), then the warp copies the
+// position's B sub-table rows into X[t, b*d:(b+1)*d] with 16-byte vectors, several
+// independent loads in flight per lane.  Also writes the storage rows (for callers that
+// need them) when grow != null.
+template <int MAXN>
+__global__ void __launch_bounds__(256) hash_gather_kernel(Shape s, const HashTables* __restrict__ ht,
+                                                          const uint32_t* __restrict__ tokens,
+                                                          const int64_t* __restrict__ seq_off, int64_t nseq,
+                                                          int64_t T, const uint32_t* __restrict__ prior,
+                                                          const __nv_bfloat16* __restrict__ sub,
+                                                          __nv_bfloat16* __restrict__ X, int32_t* __restrict__ grow,
+                                                          int64_t Tpad, unsigned long long* err) {
+    const int lane = threadIdx.x & 31;
+    const int64_t t = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    if (t >= T) return;
+    uint32_t w[MAXN];
+    if (!load_window<MAXN>(s, tokens, seq_off, nseq, prior, t, w)) {
+        if (lane == 0) atomicMin(err, (unsigned long long)t);
+        return;
+    }
+    gather_position<MAXN, 4>(s, ht, w, sub, X + t * (int64_t)s.D, grow, Tpad, t, lane);
+}
+
+__global__ void validate_tokens_kernel(uint32_t V0, const uint32_t* __restrict__ tokens, int64_t T,
+                                       const int64_t* __restrict__ seq_off, int64_t nseq, const uint32_t* prior,
+                                       int R, unsigned long long* err) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < T) {
+        if (__ldg(tokens + i) >= V0) atomicMin(err, (unsigned long long)i);
+    } else if (prior && i < T + nseq * R) {  // prior tokens are in the window of the sequence's position 0
+        const int64_t k = i - T, sq = k / R;
+        const int64_t a = __ldg(seq_off + sq), b = __ldg(seq_off + sq + 1);
+        if (b > a && __ldg(prior + k) >= V0) atomicMin(err, (unsigned long long)a);
+    }
+}
+
 }  // namespace
+
+void launch_validate_tokens(const Shape& s, const uint32_t* tokens, int64_t T, const int64_t* seq_off, int64_t nseq,
+                            const uint32_t* prior, unsigned long long* err, cudaStream_t st) {
+    const int R = s.N > 1 ? s.N - 1 : 0;
+    const int64_t n = T + (prior ? nseq * R : 0);
+    if (n <= 0) return;
+    validate_tokens_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(s.V0, tokens, T, seq_off, nseq, prior, R, err);
+    count_launch();
+}
+
+void launch_hash_gather(const Shape& s, const HashTables* ht, const uint32_t* tokens, const int64_t* seq_off,
+                        int64_t nseq, int64_t T, const uint32_t* prior, const __nv_bfloat16* sub, __nv_bfloat16* X,
+                        int32_t* grow, int64_t Tpad, unsigned long long* err, cudaStream_t st) {
+    if (T <= 0) return;
+    const unsigned blocks = (unsigned)((T + 7) / 8);  // 8 warps (positions) per block
+    if (s.N <= 4)
+        hash_gather_kernel<4><<<blocks, 256, 0, st>>>(s, ht, tokens, seq_off, nseq, T, prior, sub, X, grow, Tpad, err);
+    else if (s.N <= 8)
+        hash_gather_kernel<8><<<blocks, 256, 0, st>>>(s, ht, tokens, seq_off, nseq, T, prior, sub, X, grow, Tpad, err);
+    else
+        hash_gather_kernel<16><<<blocks, 256, 0, st>>>(s, ht, tokens, seq_off, nseq, T, prior, sub, X, grow, Tpad,
+                                                       err);
+    count_launch();
+}
 
 void launch_hash_ids(const Shape& s, const HashTables* ht, const uint32_t* tokens, const int64_t* seq_off,
                      int64_t nseq, int64_t T, const uint32_t* prior, void* ids_tok, int ids_u64, int32_t* grow,

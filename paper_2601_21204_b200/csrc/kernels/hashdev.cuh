@@ -1,0 +1,126 @@
+// hashdev.cuh -- device helpers of K1 shared by the hash kernels and the gather warps of
+// the fused K1+K2+K3 kernel: Barrett / 128-bit modular products, the sequence lookup,
+// and the warp-per-position hash + row gather (restating hashing.cpp:33-81 over the
+// windows of embedding.hpp:391-405; see hash.cu for the exactness argument).
+#pragma once
+#include <cstdint>
+
+#include "kernels.h"
+
+namespace ngk {
+
+__device__ __forceinline__ uint64_t barrett_mod(uint64_t x, uint64_t m, uint64_t mu) {
+    const uint64_t q = __umul64hi(x, mu);
+    uint64_t r = x - q * m;
+    if (r >= m) r -= m;
+    if (r >= m) r -= m;
+    return r;
+}
+
+__device__ __forceinline__ uint64_t mulmod128(uint64_t a, uint64_t b, uint64_t m) {
+    return static_cast<uint64_t>((static_cast<unsigned __int128>(a) * b) % m);
+}
+
+// Position t of the concatenated batch -> sequence index (largest s with off[s] <= t).
+__device__ __forceinline__ int64_t find_seq(const int64_t* __restrict__ off, int64_t nseq, int64_t t) {
+    int64_t lo = 0, hi = nseq - 1;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (__ldg(off + mid) <= t) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+// Bucket of branch b for the window w (oldest first, N tokens).
+template <int MAXN>
+__device__ __forceinline__ uint64_t branch_hash(const Shape& s, const HashTables* __restrict__ ht,
+                                                const uint32_t (&w)[MAXN], int b) {
+    const int N = s.N;
+    const int n = 2 + b / s.K;
+    const uint64_t m = __ldg(&ht->modulus[b]);
+    if (m <= 1) return 0;
+    if (s.fast_hash) {
+        const uint64_t mu = __ldg(&ht->barrett[b]);
+        uint64_t acc = 0;
+#pragma unroll
+        for (int j = 0; j < MAXN; ++j)
+            if (j < n) {
+                const uint64_t tm = barrett_mod((uint64_t)w[N - 1 - j], m, mu);
+                acc += barrett_mod(tm * __ldg(&ht->pow[b][j]), m, mu);
+            }
+        return barrett_mod(acc, m, mu);  // acc < n * 2^32
+    }
+    uint64_t acc = 0;
+#pragma unroll
+    for (int j = 0; j < MAXN; ++j)
+        if (j < n) acc = (acc + mulmod128((uint64_t)w[N - 1 - j] % m, __ldg(&ht->pow[b][j]), m)) % m;
+    return acc;
+}
+
+// Storage row of bucket h of branch b on this shard (fallback row 0 when not local).
+__device__ __forceinline__ int32_t storage_row(const HashTables* __restrict__ ht, int b, uint64_t h, bool* local) {
+    const int64_t lo = __ldg(&ht->row_lo[b]), hi = __ldg(&ht->row_hi[b]);
+    const bool in = (int64_t)h >= lo && (int64_t)h < hi;
+    if (local) *local = in;
+    return in ? (int32_t)(__ldg(&ht->row_base[b]) + ((int64_t)h - lo)) : 0;
+}
+
+// One warp: window of position t; returns false (warp-uniform) when it holds a token >= V0.
+template <int MAXN>
+__device__ __forceinline__ bool load_window(const Shape& s, const uint32_t* __restrict__ tokens,
+                                            const int64_t* __restrict__ seq_off, int64_t nseq,
+                                            const uint32_t* __restrict__ prior, int64_t t, uint32_t (&w)[MAXN]) {
+    const int N = s.N;
+    const int64_t sq = find_seq(seq_off, nseq, t);
+    const int64_t base = __ldg(seq_off + sq);
+    const int64_t p = t - base;
+    bool bad = false;
+#pragma unroll
+    for (int j = 0; j < MAXN; ++j) {
+        if (j < N) {
+            const int64_t idx = p - (N - 1) + j;
+            const uint32_t v = idx >= 0 ? __ldg(tokens + base + idx)
+                                        : (prior ? __ldg(prior + sq * (N - 1) + (N - 1) + idx) : 0u);
+            w[j] = v;
+            bad |= (v >= s.V0);
+        }
+    }
+    return !bad;
+}
+
+// One warp: hash the B branches of position t (lane = branch) and copy the B d-wide rows
+// into xrow = X + t*D with 16-byte vectors, U independent loads in flight per lane.
+template <int MAXN, int U>
+__device__ __forceinline__ void gather_position(const Shape& s, const HashTables* __restrict__ ht,
+                                                const uint32_t (&w)[MAXN], const __nv_bfloat16* __restrict__ sub,
+                                                __nv_bfloat16* __restrict__ xrow_base, int32_t* grow, int64_t Tpad,
+                                                int64_t t, int lane) {
+    const int B = s.B, d = s.d;
+    for (int b0 = 0; b0 < B; b0 += 32) {
+        const int b = b0 + lane;
+        int32_t row = 0;
+        if (b < B) {
+            row = storage_row(ht, b, branch_hash<MAXN>(s, ht, w, b), nullptr);
+            if (grow) grow[(int64_t)b * Tpad + t] = row;
+        }
+        const int vpr = d / 8;
+        const int nv = min(32, B - b0) * vpr;
+        uint4* xrow = reinterpret_cast<uint4*>(xrow_base + (int64_t)b0 * d);
+        for (int v0 = lane; v0 - lane < nv; v0 += 32 * U) {  // warp-uniform trip count (shfl inside)
+            uint4 val[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int v = v0 + u * 32;
+                const int bb = v / vpr;
+                const int32_t r = __shfl_sync(0xffffffffu, row, bb & 31);
+                if (v < nv) val[u] = __ldg(reinterpret_cast<const uint4*>(sub + (int64_t)r * d) + (v - bb * vpr));
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (v0 + u * 32 < nv) xrow[v0 + u * 32] = val[u];
+        }
+    }
+}
+
+}  // namespace ngk

@@ -39,6 +39,13 @@ uint64_t launches();
 void launch_hash_ids(const Shape& s, const HashTables* ht, const uint32_t* tokens, const int64_t* seq_off,
                      int64_t nseq, int64_t T, const uint32_t* prior, void* ids_tok, int ids_u64, int32_t* grow,
                      int64_t Tpad, unsigned long long* err, cudaStream_t st);
+// K1+K2 fused (X path): hash every position (lane per branch) and gather its rows into X.
+void launch_hash_gather(const Shape& s, const HashTables* ht, const uint32_t* tokens, const int64_t* seq_off,
+                        int64_t nseq, int64_t T, const uint32_t* prior, const __nv_bfloat16* sub, __nv_bfloat16* X,
+                        int32_t* grow, int64_t Tpad, unsigned long long* err, cudaStream_t st);
+// Token range check only (tokens and used prior tokens < V0), min bad window -> err.
+void launch_validate_tokens(const Shape& s, const uint32_t* tokens, int64_t T, const int64_t* seq_off, int64_t nseq,
+                            const uint32_t* prior, unsigned long long* err, cudaStream_t st);
 void launch_rolling_hash_batch(const uint32_t* windows, int64_t stride, const int32_t* lengths, const int32_t* orders,
                                const uint64_t* bases,
                                const uint64_t* moduli, int64_t count, uint64_t* out, int32_t* status,
@@ -80,8 +87,21 @@ struct FwdArgs {
     // X (materialised gathered rows, T x D bf16) instead of sub-table gather, or null
     const CUtensorMap* tmap_x;
 };
+// K1 + K2 + K3 in ONE persistent 2-CTA kernel: gather warps hash and gather X rows ahead
+// of the MMA pipeline (per-128-row ready counters), overlapping the HBM-bound gather with
+// the tensor-bound projection.  Needs D % 256 == 0; tokens must be validated first.
+struct FusedX {
+    const int64_t* seq_off;
+    int64_t nseq;
+    const uint32_t* prior;
+    __nv_bfloat16* X;  // gathered rows (T x D), written by the gather warps
+    int* ready;        // [ceil(T/128)] zeroed counters
+};
+void launch_forward_tc2_fusedx(const FwdArgs& a, const FusedX& fx, int num_sms, cudaStream_t st);
 // tcgen05 projection GEMM with fused gather + base add + scale + amplify (gemm_tc.cu).
-void launch_forward_tc(const FwdArgs& a, int num_sms, cudaStream_t st);
+// splitk_ws (fp32, splitk_workspace_floats() long, may be null): small-T split-K path.
+void launch_forward_tc(const FwdArgs& a, int num_sms, cudaStream_t st, float* splitk_ws = nullptr);
+size_t splitk_workspace_floats(const FwdArgs& a, int num_sms);
 // generic CUDA-core path: any shape, v1 and v2, reference float op order (simt.cu).
 void launch_forward_simt(const FwdArgs& a, cudaStream_t st);
 // K2 standalone: materialise X (T x D bf16) from the storage rows (d % 8 == 0).

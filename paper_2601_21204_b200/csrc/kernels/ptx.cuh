@@ -39,9 +39,13 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+// Bounded wait: a pipeline bug (byte-count mismatch, lost arrive) traps with a launch
+// error after ~2^28 polls instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
+    uint32_t spins = 0;
     while (!mbar_try_wait(a, parity)) {
+        if (++spins == (1u << 28)) __trap();
     }
 }
 
@@ -126,6 +130,27 @@ __device__ __forceinline__ void tma_gather4_2cta(void* smem_dst, const CUtensorM
 
 __device__ __forceinline__ void prefetch_l2(const void* p) {
     asm volatile("prefetch.global.L2::evict_normal [%0];" ::"l"(p));
+}
+
+// Cross-CTA readiness counters (all CTAs of a persistent grid are co-resident).
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+    int x;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(x) : "l"(p) : "memory");
+    return x;
+}
+__device__ __forceinline__ int ld_relaxed_gpu(const int* p) {
+    int x;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(x) : "l"(p) : "memory");
+    return x;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void red_release_gpu_add(int* p, int v) {
+    asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// Order generic-proxy global writes (other SMs' st.global) before this thread's later
+// async-proxy (TMA) reads of the same locations.
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 // cp.async (LDGSTS) 16 B, L2-only caching, plus group bookkeeping.

@@ -139,7 +139,7 @@ def test_draft_verify_accept_none_leaves_state(bank):  # test_cache.cpp:245-262
 
 def test_batched_decode_steps_equal_prefill(bank, cuda):
     """B streams decoded token by token == the same sequences run through the prefill
-    forward (bit-identical merged rows: same ids, same GEMM tile arithmetic)."""
+    forward (ids bit-identical, merged rows within tolerance)."""
     cfg, hb, db = bank
     B, L = 16, 24
     rng = np.random.default_rng(1)
@@ -155,7 +155,8 @@ def test_batched_decode_steps_equal_prefill(bank, cuda):
     off = np.arange(0, B * L + 1, L)
     _, pre = G.embed_forward(db, dev_u32(torch, seqs.reshape(-1), cuda), dev_i64(torch, off, cuda), rows=False,
                              merged=True)
-    assert torch.equal(dec, pre)
+    # decode steps run the small-T split-K GEMM, the prefill the full-K GEMM: tolerance
+    assert_rows_close(dec.cpu().numpy(), pre.cpu().numpy())
     ring, length, last = st.state()
     assert (length == L).all() and np.array_equal(last, seqs[:, -1]) and np.array_equal(ring, seqs[:, -3:])
     for s in range(B):
@@ -183,8 +184,10 @@ def test_batched_verify_and_commit(bank, cuda):
         off = np.concatenate([[0], np.cumsum([len(f) for f in full])])
         _, pre = G.embed_forward(db, dev_u32(torch, np.concatenate(full), cuda), dev_i64(torch, off, cuda),
                                  rows=False, merged=True)
+        got = out.cpu().numpy()
+        want = pre.cpu().numpy()
         for s in range(B):
-            assert torch.equal(out[s], pre[off[s] + len(hist[s]):off[s + 1]])
+            assert_rows_close(got[s], want[off[s] + len(hist[s]):off[s + 1]])
         hist = [h + [int(x) for x in draft[s, :accept[s]]] for s, h in enumerate(hist)]
         ring, length, last = st.state()
         for s in range(B):
