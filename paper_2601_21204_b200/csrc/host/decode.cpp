@@ -12,20 +12,23 @@
 namespace ngh {
 void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, int64_t gstride, int64_t T,
                     void* rows, void* merged, int out_bf16, float* ln_scratch, const CUtensorMap* tmap_x,
-                    cudaStream_t st, int amp, XBuf* xb, bool allow_splitk, const ngk::FusedX* fx);
+                    cudaStream_t st, int amp, XBuf* xb, bool allow_splitk, const ngk::FusedX* fx,
+                    const ngk::DecodeCommit* commit);
 void reset_error_word(ngram_bank* b, cudaStream_t st);
-void forward_tokens(ngram_bank* b, const uint32_t* tokens, const int64_t* seq_off, int64_t nseq, int64_t T,
+bool forward_tokens(ngram_bank* b, const uint32_t* tokens, const int64_t* seq_off, int64_t nseq, int64_t T,
                     const uint32_t* prior, void* rows, void* merged, int out_bf16, cudaStream_t st, int amp,
-                    XBuf* xb, int32_t* grow, bool allow_splitk);
+                    XBuf* xb, int32_t* grow, bool allow_splitk, const ngk::DecodeCommit* commit);
 }  // namespace ngh
 
 using namespace ngh;
 
 namespace {
 
-// Hash + project T = batch * L block positions whose windows are ring ++ draft.
-void decode_block(ngram_decode* d, const uint32_t* draft, int L, uint64_t* ids_out, void* merged_out, int out_dtype,
-                  cudaStream_t st) {
+// Hash + project T = batch * L block positions whose windows are ring ++ draft.  With
+// `commit`, the state update is fused into the projection when possible; returns whether
+// it was (otherwise the caller launches the commit kernel).
+bool decode_block(ngram_decode* d, const uint32_t* draft, int L, uint64_t* ids_out, void* merged_out, int out_dtype,
+                  cudaStream_t st, const ngk::DecodeCommit* commit = nullptr) {
     ngram_bank* b = d->bank;
     const int64_t T = d->batch * L;
     const int64_t Tpad = round_up(T, kRowPad);
@@ -36,8 +39,9 @@ void decode_block(ngram_decode* d, const uint32_t* draft, int L, uint64_t* ids_o
         ngk::launch_hash_ids(b->shape, b->ht.p, draft, off, d->batch, T, R > 0 ? d->ring.p : nullptr, ids_out, 1,
                              nullptr, Tpad, b->err.p, st);
     if (merged_out)
-        forward_tokens(b, draft, off, d->batch, T, R > 0 ? d->ring.p : nullptr, nullptr, merged_out,
-                       out_dtype == NGRAM_BF16, st, 0, &d->xbuf, d->grow.p, true);
+        return forward_tokens(b, draft, off, d->batch, T, R > 0 ? d->ring.p : nullptr, nullptr, merged_out,
+                              out_dtype == NGRAM_BF16, st, 0, &d->xbuf, d->grow.p, true, commit);
+    return false;
 }
 
 }  // namespace
@@ -102,9 +106,11 @@ int ngram_decode_step(ngram_decode* d, const uint32_t* tokens, uint64_t* ids_out
     if (out_dtype != NGRAM_F32 && out_dtype != NGRAM_BF16) throw Error(NGRAM_EINVAL, "bad out_dtype");
     DeviceGuard g(d->bank->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    decode_block(d, tokens, 1, ids_out, merged_out, out_dtype, st);
-    ngk::launch_decode_commit(d->bank->shape, d->ring.p, d->length.p, d->last.p, tokens, 1, nullptr, d->batch,
-                              d->bank->err.p, d->derr.p, st);
+    const ngk::DecodeCommit c{std::max(d->bank->cfg.max_order - 1, 0), d->ring.p, d->length.p, d->last.p,
+                              tokens, 1, nullptr, d->batch, d->derr.p};
+    if (!decode_block(d, tokens, 1, ids_out, merged_out, out_dtype, st, c.R > 0 ? &c : nullptr))
+        ngk::launch_decode_commit(d->bank->shape, d->ring.p, d->length.p, d->last.p, tokens, 1, nullptr, d->batch,
+                                  d->bank->err.p, d->derr.p, st);
     NGH_CUDA(cudaGetLastError());
     NGRAM_API_END
 }

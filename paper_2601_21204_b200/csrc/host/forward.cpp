@@ -59,7 +59,8 @@ static bool use_fusedx(ngram_bank* b, int64_t T) {
 // merged/rows per the amplification; LayerNorm via a third kernel.
 void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, int64_t gstride, int64_t T,
                     void* rows, void* merged, int out_bf16, float* ln_scratch, const CUtensorMap* tmap_x,
-                    cudaStream_t st, int amp, XBuf* xb, bool allow_splitk, const ngk::FusedX* fx) {
+                    cudaStream_t st, int amp, XBuf* xb, bool allow_splitk, const ngk::FusedX* fx,
+                    const ngk::DecodeCommit* commit) {
     if (b->hash_only) throw Error(NGRAM_EINVAL, "bank was created hash-only (NGRAM_BANK_HASH_ONLY)");
     if (T <= 0) return;
     ngk::FwdArgs a{};
@@ -80,6 +81,7 @@ void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, 
     a.tmap_w = &b->tmap_w;
     a.tmap_w2 = &b->tmap_w2;
     a.tmap_x = tmap_x;
+    a.commit = commit;
     const bool ln = a.s.amp == 2;
     float* ln_merged = nullptr;
     if (ln) {
@@ -120,9 +122,11 @@ void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, 
 // Hash + gather + project T positions given by (tokens, seq_off, prior).  X path: the
 // fused K1+K2 kernel writes X directly; otherwise K1 writes storage rows for the fused-
 // gather GEMM or the CUDA-core kernels.
-void forward_tokens(ngram_bank* b, const uint32_t* tokens, const int64_t* seq_off, int64_t nseq, int64_t T,
+// Returns true when `commit` was fused into the projection (decode GEMM path).
+bool forward_tokens(ngram_bank* b, const uint32_t* tokens, const int64_t* seq_off, int64_t nseq, int64_t T,
                     const uint32_t* prior, void* rows, void* merged, int out_bf16, cudaStream_t st, int amp,
-                    XBuf* xb, int32_t* grow, bool allow_splitk) {
+                    XBuf* xb, int32_t* grow, bool allow_splitk, const ngk::DecodeCommit* commit) {
+    bool fused_commit = false;
     const int64_t Tpad = round_up(std::max<int64_t>(T, 1), kRowPad);
     b->prof_record(0, st);
     if (use_fusedx(b, T)) {
@@ -136,22 +140,28 @@ void forward_tokens(ngram_bank* b, const uint32_t* tokens, const int64_t* seq_of
         b->prof_record(1, st);
         ngk::FusedX fx{seq_off, nseq, prior, xb->x.p, b->ws.ready.p};
         run_projection(b, tokens, nullptr, Tpad, T, rows, merged, out_bf16, b->ws.merged_f32.p, &xb->map, st, amp,
-                       nullptr, false, &fx);
+                       nullptr, false, &fx, nullptr);
     } else if (b->tc_path && ((allow_splitk && T <= 256) || !fused_gather(b->shape.D))) {
         if (!xb) xb = &b->ws.xbuf;
         xb->ensure(Tpad, b->shape.D);
-        ngk::launch_hash_gather(b->shape, b->ht.p, tokens, seq_off, nseq, T, prior, b->sub.p, xb->x.p, nullptr, Tpad,
-                                b->err.p, st);
+        if (T <= 1024)
+            ngk::launch_hash_gather_rows(b->shape, b->ht.p, tokens, seq_off, nseq, T, prior, b->sub.p, xb->x.p,
+                                         b->err.p, st);
+        else
+            ngk::launch_hash_gather(b->shape, b->ht.p, tokens, seq_off, nseq, T, prior, b->sub.p, xb->x.p, nullptr,
+                                    Tpad, b->err.p, st);
         b->prof_record(1, st);
+        fused_commit = commit != nullptr;  // every tensor-core projection path consumes it
         run_projection(b, tokens, nullptr, Tpad, T, rows, merged, out_bf16, b->ws.merged_f32.p, &xb->map, st, amp,
-                       nullptr, allow_splitk, nullptr);
+                       nullptr, allow_splitk, nullptr, fused_commit ? commit : nullptr);
     } else {
         ngk::launch_hash_ids(b->shape, b->ht.p, tokens, seq_off, nseq, T, prior, nullptr, 0, grow, Tpad, b->err.p, st);
         b->prof_record(1, st);
         run_projection(b, tokens, grow, Tpad, T, rows, merged, out_bf16, b->ws.merged_f32.p, nullptr, st, amp, xb,
-                       allow_splitk, nullptr);
+                       allow_splitk, nullptr, nullptr);
     }
     b->prof_record(3, st);
+    return fused_commit;
 }
 
 void reset_error_word(ngram_bank* b, cudaStream_t st) {
@@ -225,7 +235,7 @@ int ngram_embed_forward(ngram_bank* b, const uint32_t* tokens, const int64_t* se
     if (total_tokens == 0) return NGRAM_OK;
     (void)Tpad;
     forward_tokens(b, tokens, seq_offsets, nseq, total_tokens, prior, rows_out, merged_out, out_dtype == NGRAM_BF16,
-                   st, -1, nullptr, b->ws.grow.p, true);
+                   st, -1, nullptr, b->ws.grow.p, true, nullptr);
     NGRAM_API_END
 }
 
@@ -243,7 +253,7 @@ int ngram_embed_from_ids(ngram_bank* b, const uint32_t* tokens, const uint64_t* 
     ngk::launch_ids_to_rows(b->shape, b->ht.p, ids, tokens, T, b->ws.grow.p, Tpad, b->err.p, st);
     // embed_from_ids returns the merged (pre-amplification) vector: run with amp = none.
     run_projection(b, tokens, b->ws.grow.p, Tpad, T, nullptr, merged_out, out_dtype == NGRAM_BF16, nullptr, nullptr,
-                   st, 0, nullptr, true, nullptr);
+                   st, 0, nullptr, true, nullptr, nullptr);
     NGRAM_API_END
 }
 
@@ -355,7 +365,7 @@ int ngram_embed_sequence_host(ngram_bank* b, const uint32_t* tokens, const int64
         void* dmerged = merged_out ? b->host_merged[slot].p : nullptr;
         run_projection(b, b->ws.tokens.p + c0, b->ws.grow.p + c0, Tpad, n, drows, dmerged, out_dtype == NGRAM_BF16,
                        b->ws.merged_f32.p ? b->ws.merged_f32.p + size_t(c0) * size_t(D) : nullptr, nullptr, st, -1,
-                       &b->host_x[slot], T <= 256, nullptr);  // chunks keep the whole batch's regime
+                       &b->host_x[slot], T <= 256, nullptr, nullptr);  // chunks keep the whole batch's regime
         const size_t bytes = size_t(n) * size_t(D) * esz;
         if (direct) {
             if (rows_out)

@@ -13,7 +13,8 @@
 namespace ngh {
 void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, int64_t gstride, int64_t T,
                     void* rows, void* merged, int out_bf16, float* ln_scratch, const CUtensorMap* tmap_x,
-                    cudaStream_t st, int amp, XBuf* xb, bool allow_splitk, const ngk::FusedX* fx);
+                    cudaStream_t st, int amp, XBuf* xb, bool allow_splitk, const ngk::FusedX* fx,
+                    const ngk::DecodeCommit* commit);
 void reset_error_word(ngram_bank* b, cudaStream_t st);
 }  // namespace ngh
 
@@ -148,7 +149,7 @@ int ngram_shard_project(ngram_shard_group* g, const uint32_t* home_tokens, int64
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     XBuf& xb = g->x[g->parity];
     run_projection(b, home_tokens, nullptr, round_up(std::max<int64_t>(home_T, 1), kRowPad), home_T, rows_out,
-                   merged_out, out_dtype == NGRAM_BF16, b->ws.merged_f32.p, &xb.map, st, -1, nullptr, false, nullptr);
+                   merged_out, out_dtype == NGRAM_BF16, b->ws.merged_f32.p, &xb.map, st, -1, nullptr, false, nullptr, nullptr);
     g->parity ^= 1;
     NGRAM_API_END
 }

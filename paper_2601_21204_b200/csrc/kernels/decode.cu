@@ -10,43 +10,15 @@
 //   * reset: seed every ring from a prior context (prefill hand-off) or zeros.
 #include <cstdint>
 
+#include "decodedev.cuh"
 #include "kernels.h"
 
 namespace ngk {
 
 namespace {
 
-__global__ void __launch_bounds__(1024) commit_kernel(int R, uint32_t* __restrict__ ring, uint64_t* __restrict__ length,
-                                                      uint32_t* __restrict__ last, const uint32_t* __restrict__ draft,
-                                                      int L, const int32_t* __restrict__ accept, int64_t batch,
-                                                      unsigned long long* err, unsigned long long* derr) {
-    // phase 1: validate the whole batch (single CTA)
-    int bad = 0;
-    for (int64_t s = threadIdx.x; s < batch; s += blockDim.x) {
-        const int a = accept ? accept[s] : L;
-        if (a < 0 || a > L) bad = 1;
-    }
-    bad = __syncthreads_or(bad);
-    if (bad) {
-        if (threadIdx.x == 0) atomicMin(derr, (1ull << 32) | 1ull);  // NGRAM_EINVAL
-        return;
-    }
-    if (*err != ~0ull) return;  // a token of this block was out of range: state unchanged
-    // phase 2: commit
-    for (int64_t s = threadIdx.x; s < batch; s += blockDim.x) {
-        const int a = accept ? accept[s] : L;
-        if (a == 0) continue;
-        uint32_t* rg = ring + s * R;
-        const uint32_t* dr = draft + s * L;
-        uint32_t nr[kMaxOrder];
-        for (int j = 0; j < R; ++j) {  // position j of the new ring = element (a + j) of ring ++ draft
-            const int k = a + j;
-            nr[j] = k < R ? rg[k] : dr[k - R];
-        }
-        for (int j = 0; j < R; ++j) rg[j] = nr[j];
-        length[s] += (uint64_t)a;
-        last[s] = dr[a - 1];
-    }
+__global__ void __launch_bounds__(1024) commit_kernel(DecodeCommit c, const unsigned long long* err) {
+    decode_commit_block(c, err);
 }
 
 __global__ void reset_kernel(int R, uint32_t* __restrict__ ring, uint64_t* __restrict__ length,
@@ -65,9 +37,16 @@ void launch_decode_commit(const Shape& s, uint32_t* ring, uint64_t* length, uint
                           int L, const int32_t* accept, int64_t batch, unsigned long long* err,
                           unsigned long long* derr, cudaStream_t st) {
     if (batch <= 0) return;
-    const int R = s.N > 1 ? s.N - 1 : 0;
+    DecodeCommit c{s.N > 1 ? s.N - 1 : 0, ring, length, last, draft, L, accept, batch, derr};
     const int threads = batch >= 1024 ? 1024 : (int)((batch + 31) / 32 * 32);
-    commit_kernel<<<1, threads, 0, st>>>(R, ring, length, last, draft, L, accept, batch, err, derr);
+    commit_kernel<<<1, threads, 0, st>>>(c, err);
+    count_launch();
+}
+
+void launch_decode_commit_c(const DecodeCommit& c, const unsigned long long* err, cudaStream_t st) {
+    if (c.batch <= 0) return;
+    const int threads = c.batch >= 1024 ? 1024 : (int)((c.batch + 31) / 32 * 32);
+    commit_kernel<<<1, threads, 0, st>>>(c, err);
     count_launch();
 }
 

@@ -27,6 +27,7 @@
 #include <cstdint>
 #include <cstdlib>
 
+#include "decodedev.cuh"
 #include "hashdev.cuh"
 #include "kernels.h"
 #include "ptx.cuh"
@@ -740,7 +741,9 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
                                                             const uint32_t* __restrict__ tokens,
                                                             const __nv_bfloat16* __restrict__ e0, float scale,
                                                             float amp, int write_rows, void* rows, void* merged,
-                                                            int out_bf16, const unsigned long long* err) {
+                                                            int out_bf16, const unsigned long long* err,
+                                                            DecodeCommit commit) {
+    if (commit.ring && blockIdx.x == 0) decode_commit_block(commit, err);  // fused decode-state commit
     if (*err != ~0ull) return;
     const int64_t n4 = T * D / 4;
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n4; v += (int64_t)gridDim.x * blockDim.x) {
@@ -813,14 +816,27 @@ int tc_variant() {  // 2 = cta_group::2 pair kernel (default when D % 256 == 0),
     return v;
 }
 
+// Small-T (decode / verify) projection: NGRAM_DECODE_CLUSTER=1 selects the single-kernel
+// cluster split-K (decode_gemm.cu: reduction + commit fused, measured slower: its in-kernel
+// reduction is latency-bound); default = split-K GEMM + reduce kernel (commit fused there).
+static bool decode_cluster() {
+    static const bool v = getenv("NGRAM_DECODE_CLUSTER") && atoi(getenv("NGRAM_DECODE_CLUSTER")) != 0;
+    return v;
+}
+
 size_t splitk_workspace_floats(const FwdArgs& a, int num_sms) {
     if (a.T > 256 || a.tmap_x == nullptr) return 0;
+    if (decode_cluster()) return decode_gemm_workspace_floats(a.s.D, num_sms);
     const int S = splitk_factor(a, num_sms);
     return S > 1 ? (size_t)S * (size_t)a.T * (size_t)a.s.D : 0;
 }
 
 void launch_forward_tc(const FwdArgs& a, int num_sms, cudaStream_t st, float* splitk_ws) {
     if (a.T <= 0) return;
+    if (splitk_ws && a.T <= 256 && a.tmap_x != nullptr && decode_cluster()) {
+        launch_decode_gemm(a, num_sms, splitk_ws, a.commit, st);
+        return;
+    }
     if (splitk_ws && a.T <= 256 && a.tmap_x != nullptr) {
         const int S = splitk_factor(a, num_sms);
         if (S > 1) {
@@ -830,9 +846,11 @@ void launch_forward_tc(const FwdArgs& a, int num_sms, cudaStream_t st, float* sp
             const int64_t n4 = a.T * a.s.D / 4;
             int64_t blocks = (n4 + 255) / 256;
             if (blocks > num_sms * 8) blocks = num_sms * 8;
+            DecodeCommit c{};
+            if (a.commit) c = *a.commit;
             splitk_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(
                 splitk_ws, S, a.T, a.s.D, a.tokens, a.e0, scale, amp,
-                (a.rows_out != nullptr && a.s.amp != kAmpLN) ? 1 : 0, a.rows_out, a.merged_out, a.out_bf16, a.err);
+                (a.rows_out != nullptr && a.s.amp != kAmpLN) ? 1 : 0, a.rows_out, a.merged_out, a.out_bf16, a.err, c);
             count_launch();
             return;
         }
@@ -840,6 +858,7 @@ void launch_forward_tc(const FwdArgs& a, int num_sms, cudaStream_t st, float* sp
     const bool bn256 = a.s.D % 256 == 0;
     if (bn256 && tc_variant() == 2 && a.tmap_w2 != nullptr) {
         launch_tc2(a, num_sms, st);
+        if (a.commit) launch_decode_commit_c(*a.commit, a.err, st);
         return;
     }
     if (producer_mode() == 0) {
@@ -849,6 +868,7 @@ void launch_forward_tc(const FwdArgs& a, int num_sms, cudaStream_t st, float* sp
         if (bn256) launch_cfg<256, 4, 1>(a, num_sms, st);
         else launch_cfg<128, 4, 1>(a, num_sms, st);
     }
+    if (a.commit) launch_decode_commit_c(*a.commit, a.err, st);
 }
 
 }  // namespace ngk

@@ -177,6 +177,32 @@ __global__ void __launch_bounds__(256) hash_gather_kernel(Shape s, const HashTab
     gather_position<MAXN, 4>(s, ht, w, sub, X + t * (int64_t)s.D, grow, Tpad, t, lane);
 }
 
+// Small-T variant (decode / verify): one warp per (position, branch), so a position's B
+// rows are fetched by B warps in a single round of loads instead of serially by one warp.
+template <int MAXN>
+__global__ void __launch_bounds__(256) hash_gather_rows_kernel(Shape s, const HashTables* __restrict__ ht,
+                                                               const uint32_t* __restrict__ tokens,
+                                                               const int64_t* __restrict__ seq_off, int64_t nseq,
+                                                               int64_t T, const uint32_t* __restrict__ prior,
+                                                               const __nv_bfloat16* __restrict__ sub,
+                                                               __nv_bfloat16* __restrict__ X,
+                                                               unsigned long long* err) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    if (w >= T * s.B) return;
+    const int64_t t = w / s.B;
+    const int b = (int)(w - t * s.B);
+    uint32_t win[MAXN];
+    if (!load_window<MAXN>(s, tokens, seq_off, nseq, prior, t, win)) {
+        if (lane == 0 && b == 0) atomicMin(err, (unsigned long long)t);
+        return;
+    }
+    const int32_t row = storage_row(ht, b, branch_hash<MAXN>(s, ht, win, b), nullptr);
+    const uint4* src = reinterpret_cast<const uint4*>(sub + (int64_t)row * s.d);
+    uint4* dst = reinterpret_cast<uint4*>(X + t * (int64_t)s.D + (int64_t)b * s.d);
+    for (int c = lane; c < s.d / 8; c += 32) dst[c] = __ldg(src + c);
+}
+
 __global__ void validate_tokens_kernel(uint32_t V0, const uint32_t* __restrict__ tokens, int64_t T,
                                        const int64_t* __restrict__ seq_off, int64_t nseq, const uint32_t* prior,
                                        int R, unsigned long long* err) {
@@ -213,6 +239,21 @@ void launch_hash_gather(const Shape& s, const HashTables* ht, const uint32_t* to
     else
         hash_gather_kernel<16><<<blocks, 256, 0, st>>>(s, ht, tokens, seq_off, nseq, T, prior, sub, X, grow, Tpad,
                                                        err);
+    count_launch();
+}
+
+void launch_hash_gather_rows(const Shape& s, const HashTables* ht, const uint32_t* tokens, const int64_t* seq_off,
+                             int64_t nseq, int64_t T, const uint32_t* prior, const __nv_bfloat16* sub,
+                             __nv_bfloat16* X, unsigned long long* err, cudaStream_t st) {
+    const int64_t warps = T * s.B;
+    if (warps <= 0) return;
+    const unsigned blocks = (unsigned)((warps + 7) / 8);
+    if (s.N <= 4)
+        hash_gather_rows_kernel<4><<<blocks, 256, 0, st>>>(s, ht, tokens, seq_off, nseq, T, prior, sub, X, err);
+    else if (s.N <= 8)
+        hash_gather_rows_kernel<8><<<blocks, 256, 0, st>>>(s, ht, tokens, seq_off, nseq, T, prior, sub, X, err);
+    else
+        hash_gather_rows_kernel<16><<<blocks, 256, 0, st>>>(s, ht, tokens, seq_off, nseq, T, prior, sub, X, err);
     count_launch();
 }
 

@@ -43,6 +43,10 @@ void launch_hash_ids(const Shape& s, const HashTables* ht, const uint32_t* token
 void launch_hash_gather(const Shape& s, const HashTables* ht, const uint32_t* tokens, const int64_t* seq_off,
                         int64_t nseq, int64_t T, const uint32_t* prior, const __nv_bfloat16* sub, __nv_bfloat16* X,
                         int32_t* grow, int64_t Tpad, unsigned long long* err, cudaStream_t st);
+// Same, one warp per (position, branch): the small-T (decode / verify) latency variant.
+void launch_hash_gather_rows(const Shape& s, const HashTables* ht, const uint32_t* tokens, const int64_t* seq_off,
+                             int64_t nseq, int64_t T, const uint32_t* prior, const __nv_bfloat16* sub,
+                             __nv_bfloat16* X, unsigned long long* err, cudaStream_t st);
 // Token range check only (tokens and used prior tokens < V0), min bad window -> err.
 void launch_validate_tokens(const Shape& s, const uint32_t* tokens, int64_t T, const int64_t* seq_off, int64_t nseq,
                             const uint32_t* prior, unsigned long long* err, cudaStream_t st);
@@ -86,6 +90,8 @@ struct FwdArgs {
     const CUtensorMap* tmap_w2;  // W_cat with a 128-row box (2-CTA kernel), or null
     // X (materialised gathered rows, T x D bf16) instead of sub-table gather, or null
     const CUtensorMap* tmap_x;
+    // decode step: commit the decode state in the projection kernel's tail (or null)
+    const struct DecodeCommit* commit;
 };
 // K1 + K2 + K3 in ONE persistent 2-CTA kernel: gather warps hash and gather X rows ahead
 // of the MMA pipeline (per-128-row ready counters), overlapping the HBM-bound gather with
@@ -113,7 +119,25 @@ void launch_layernorm_rows(const Shape& s, const float* merged, const float* gai
                            void* merged_copy, int out_bf16, int64_t T, const unsigned long long* err,
                            cudaStream_t st);
 
-// ---- decode (decode.cu)
+// ---- decode (decode.cu, decode_gemm.cu)
+// Arguments of the decode-state commit (decodedev.cuh); ring == null means "no commit".
+struct DecodeCommit {
+    int R;  // N - 1
+    uint32_t* ring;
+    uint64_t* length;
+    uint32_t* last;
+    const uint32_t* draft;  // [batch][L]
+    int L;
+    const int32_t* accept;  // [batch] or null (= L for every stream)
+    int64_t batch;
+    unsigned long long* derr;
+};
+// Small-T projection (T <= 256, D % 128 == 0, tensor-core shape): split-K over a thread-
+// block cluster with the cross-split reduction, epilogue and optional commit fused.
+void launch_decode_commit_c(const DecodeCommit& c, const unsigned long long* err, cudaStream_t st);
+int decode_gemm_splits(int D, int num_sms);
+size_t decode_gemm_workspace_floats(int D, int num_sms);
+void launch_decode_gemm(const FwdArgs& a, int num_sms, float* partial, const DecodeCommit* commit, cudaStream_t st);
 // The hashing of a decode step / verify block is launch_hash_ids with prior = ring and
 // seq_off = {0, L, 2L, ...}; these kernels move the ring.  derr: decode error word
 // ((status << 32) | detail), ~0 when clear.
