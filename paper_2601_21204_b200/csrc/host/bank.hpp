@@ -106,6 +106,9 @@ struct ngram_bank {
     void* pinned[2] = {nullptr, nullptr};
     size_t pinned_bytes = 0;
 
+    // chunked K2/K3 overlap (NGRAM_OVERLAP_CHUNKS)
+    cudaStream_t side_stream = nullptr;
+    cudaEvent_t chunk_ev[9] = {};
     // stage profiling (ngram_profile_enable)
     bool prof = false;
     cudaEvent_t prof_ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -135,6 +138,16 @@ namespace ngh {
 void make_tensor_map_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t rows, uint64_t row_pitch_bytes,
                         uint32_t box_inner, uint32_t box_rows);
 void ensure_workspace(ngram_bank* b, int64_t T);
+
+// Forward building blocks shared by forward.cpp / decode.cpp / shard.cpp.
+void reset_error_word(ngram_bank* b, cudaStream_t st);
+void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, int64_t gstride, int64_t T,
+                    void* rows, void* merged, int out_bf16, float* ln_scratch, const CUtensorMap* tmap_x,
+                    cudaStream_t st, int amp, XBuf* xb, bool allow_splitk, const ngk::FusedX* fx,
+                    const ngk::DecodeCommit* commit, int64_t x_row0 = 0);
+bool forward_tokens(ngram_bank* b, const uint32_t* tokens, const int64_t* seq_off, int64_t nseq, int64_t T,
+                    const uint32_t* prior, void* rows, void* merged, int out_bf16, cudaStream_t st, int amp,
+                    XBuf* xb, int32_t* grow, bool allow_splitk, const ngk::DecodeCommit* commit);
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 // Row padding of every per-token workspace: the 2-CTA GEMM tile is 256 tokens.
 constexpr int64_t kRowPad = 256;

@@ -54,13 +54,24 @@ static bool use_fusedx(ngram_bank* b, int64_t T) {
            b->shape.N <= 4 && b->shape.B <= 32;
 }
 
+// Chunked overlap of K2 (side stream) with K3 for long batches: NGRAM_OVERLAP_CHUNKS
+// (default 0 = off, <= 8).
+static int overlap_chunks(ngram_bank* b, int64_t T) {
+    static const int env = [] {
+        const char* e = getenv("NGRAM_OVERLAP_CHUNKS");
+        return e ? std::min(8, std::max(0, atoi(e))) : 0;
+    }();
+    if (env < 2 || T < int64_t(env) * 4096 || !b->tc_path) return 1;
+    return env;
+}
+
 // One forward over T rows whose storage rows are already in `grow` (stride gstride).
 // Tensor-core path: K2 gathers X (T x D bf16) into `xb`, K3 projects it.  Writes
 // merged/rows per the amplification; LayerNorm via a third kernel.
 void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, int64_t gstride, int64_t T,
                     void* rows, void* merged, int out_bf16, float* ln_scratch, const CUtensorMap* tmap_x,
                     cudaStream_t st, int amp, XBuf* xb, bool allow_splitk, const ngk::FusedX* fx,
-                    const ngk::DecodeCommit* commit) {
+                    const ngk::DecodeCommit* commit, int64_t x_row0) {
     if (b->hash_only) throw Error(NGRAM_EINVAL, "bank was created hash-only (NGRAM_BANK_HASH_ONLY)");
     if (T <= 0) return;
     ngk::FwdArgs a{};
@@ -82,6 +93,7 @@ void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, 
     a.tmap_w2 = &b->tmap_w2;
     a.tmap_x = tmap_x;
     a.commit = commit;
+    a.x_row0 = x_row0;
     const bool ln = a.s.amp == 2;
     float* ln_merged = nullptr;
     if (ln) {
@@ -144,6 +156,37 @@ bool forward_tokens(ngram_bank* b, const uint32_t* tokens, const int64_t* seq_of
     } else if (b->tc_path && ((allow_splitk && T <= 256) || !fused_gather(b->shape.D))) {
         if (!xb) xb = &b->ws.xbuf;
         xb->ensure(Tpad, b->shape.D);
+        const int nchunk = overlap_chunks(b, T);
+        if (nchunk > 1) {
+            // K2 of chunk c+1 (side stream) overlaps K3 of chunk c (caller's stream)
+            if (!b->side_stream) {
+                NGH_CUDA(cudaStreamCreateWithFlags(&b->side_stream, cudaStreamNonBlocking));
+                for (auto& e : b->chunk_ev) NGH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            }
+            NGH_CUDA(cudaEventRecord(b->chunk_ev[0], st));
+            NGH_CUDA(cudaStreamWaitEvent(b->side_stream, b->chunk_ev[0], 0));
+            int64_t bounds[9];
+            for (int c = 0; c <= nchunk; ++c) bounds[c] = std::min<int64_t>(T, round_up(T * c / nchunk, kRowPad));
+            for (int c = 0; c < nchunk; ++c) {
+                ngk::launch_hash_gather(b->shape, b->ht.p, tokens, seq_off, nseq, T, prior, b->sub.p, xb->x.p,
+                                        nullptr, Tpad, b->err.p, b->side_stream, bounds[c], bounds[c + 1]);
+                NGH_CUDA(cudaEventRecord(b->chunk_ev[1 + c], b->side_stream));
+            }
+            b->prof_record(1, st);
+            for (int c = 0; c < nchunk; ++c) {
+                NGH_CUDA(cudaStreamWaitEvent(st, b->chunk_ev[1 + c], 0));
+                const int64_t c0 = bounds[c], n = bounds[c + 1] - c0;
+                const size_t esz = out_bf16 ? 2 : 4;
+                auto off = [&](void* p) -> void* {
+                    return p ? static_cast<uint8_t*>(p) + size_t(c0) * size_t(b->shape.D) * esz : nullptr;
+                };
+                run_projection(b, tokens + c0, nullptr, Tpad, n, off(rows), off(merged), out_bf16,
+                               b->ws.merged_f32.p ? b->ws.merged_f32.p + size_t(c0) * size_t(b->shape.D) : nullptr,
+                               &xb->map, st, amp, nullptr, false, nullptr, nullptr, c0);
+            }
+            b->prof_record(3, st);
+            return false;
+        }
         if (T <= 1024)
             ngk::launch_hash_gather_rows(b->shape, b->ht.p, tokens, seq_off, nseq, T, prior, b->sub.p, xb->x.p,
                                          b->err.p, st);

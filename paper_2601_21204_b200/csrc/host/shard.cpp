@@ -10,13 +10,6 @@
 #include "api_util.hpp"
 #include "bank.hpp"
 
-namespace ngh {
-void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, int64_t gstride, int64_t T,
-                    void* rows, void* merged, int out_bf16, float* ln_scratch, const CUtensorMap* tmap_x,
-                    cudaStream_t st, int amp, XBuf* xb, bool allow_splitk, const ngk::FusedX* fx,
-                    const ngk::DecodeCommit* commit);
-void reset_error_word(ngram_bank* b, cudaStream_t st);
-}  // namespace ngh
 
 using namespace ngh;
 

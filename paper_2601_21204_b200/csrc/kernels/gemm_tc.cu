@@ -68,6 +68,7 @@ struct TcParams {
     float scale, amp;
     const unsigned long long* err;
     int use_x;  // A operand from materialised X (tmap_a is X) instead of gathered sub-table rows
+    int64_t x_row0;  // first X row of this call (chunked K2/K3 overlap)
     int epi_skip;  // diagnostics only (NGRAM_DEBUG_EPI_SKIP): drain TMEM without loads/stores
     int ksplit;      // split-K factor (small-T path); >1 => raw fp32 partials to `partial`
     float* partial;  // [ksplit][T][D] fp32
@@ -156,7 +157,7 @@ __global__ void __launch_bounds__(Cfg<BN, NP>::kThreads, 1)
                     if (lane == 0) {
                         uint8_t* a_dst = smem + stage * C::kStageBytes;
                         mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
-                        tma_load_2d(a_dst, &tmap_a, &full[stage], kb * BK, (int32_t)(m * BM));
+                        tma_load_2d(a_dst, &tmap_a, &full[stage], kb * BK, (int32_t)(m * BM + p.x_row0));
                         tma_load_2d_hint(a_dst + C::kABytes, &tmap_w, &full[stage], kb * BK, n * BN, pol_w);
                     }
                     __syncwarp();
@@ -470,7 +471,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FX ? Cfg2::kThreadsF
                     if (warp == 0 && lane == 0) {
                         uint8_t* a_dst = smem + stage * C::kStageBytes;
                         if (leader) mbar_arrive_expect_tx(&full[stage], 2 * C::kStageBytes);
-                        tma_load_2d_2cta(a_dst, &tmap_a, leader_bar(&full[stage]), kb * BK, (int32_t)t0, 0);
+                        tma_load_2d_2cta(a_dst, &tmap_a, leader_bar(&full[stage]), kb * BK,
+                                         (int32_t)(t0 + p.x_row0), 0);
                         tma_load_2d_2cta(a_dst + C::kABytes, &tmap_w, leader_bar(&full[stage]), kb * BK, wrow, pol_w);
                     }
                     __syncwarp();
@@ -659,6 +661,7 @@ void launch_cfg(const FwdArgs& a, int num_sms, cudaStream_t st, int ksplit = 1, 
     p.amp = a.s.amp == kAmpSqrt ? (float)__builtin_sqrt((double)a.s.D) : 1.0f;
     p.err = a.err;
     p.use_x = a.tmap_x != nullptr;
+    p.x_row0 = a.x_row0;
     p.epi_skip = getenv("NGRAM_DEBUG_EPI_SKIP") ? 1 : 0;
     const int64_t tiles = ((a.T + BM - 1) / BM) * (a.s.D / BN) * ksplit;
     int grid = (int)(tiles < num_sms ? tiles : num_sms);
@@ -690,6 +693,7 @@ void launch_tc2(const FwdArgs& a, int num_sms, cudaStream_t st) {
     p.amp = a.s.amp == kAmpSqrt ? (float)__builtin_sqrt((double)a.s.D) : 1.0f;
     p.err = a.err;
     p.use_x = a.tmap_x != nullptr;
+    p.x_row0 = a.x_row0;
     p.epi_skip = getenv("NGRAM_DEBUG_EPI_SKIP") ? 1 : 0;
     const int64_t tiles = ((a.T + BM2 - 1) / BM2) * (a.s.D / BN2);
     int64_t pairs = num_sms / 2;
@@ -719,6 +723,7 @@ TcParams tc2_params(const FwdArgs& a) {
     p.amp = a.s.amp == kAmpSqrt ? (float)__builtin_sqrt((double)a.s.D) : 1.0f;
     p.err = a.err;
     p.use_x = 1;
+    p.x_row0 = a.x_row0;
     p.epi_skip = getenv("NGRAM_DEBUG_EPI_SKIP") ? 1 : 0;
     return p;
 }

@@ -165,10 +165,11 @@ __global__ void __launch_bounds__(256) hash_gather_kernel(Shape s, const HashTab
                                                           int64_t T, const uint32_t* __restrict__ prior,
                                                           const __nv_bfloat16* __restrict__ sub,
                                                           __nv_bfloat16* __restrict__ X, int32_t* __restrict__ grow,
-                                                          int64_t Tpad, unsigned long long* err) {
+                                                          int64_t Tpad, unsigned long long* err, int64_t t_begin,
+                                                          int64_t t_end) {
     const int lane = threadIdx.x & 31;
-    const int64_t t = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-    if (t >= T) return;
+    const int64_t t = t_begin + (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    if (t >= t_end) return;
     uint32_t w[MAXN];
     if (!load_window<MAXN>(s, tokens, seq_off, nseq, prior, t, w)) {
         if (lane == 0) atomicMin(err, (unsigned long long)t);
@@ -229,16 +230,20 @@ void launch_validate_tokens(const Shape& s, const uint32_t* tokens, int64_t T, c
 
 void launch_hash_gather(const Shape& s, const HashTables* ht, const uint32_t* tokens, const int64_t* seq_off,
                         int64_t nseq, int64_t T, const uint32_t* prior, const __nv_bfloat16* sub, __nv_bfloat16* X,
-                        int32_t* grow, int64_t Tpad, unsigned long long* err, cudaStream_t st) {
-    if (T <= 0) return;
-    const unsigned blocks = (unsigned)((T + 7) / 8);  // 8 warps (positions) per block
+                        int32_t* grow, int64_t Tpad, unsigned long long* err, cudaStream_t st, int64_t t_begin,
+                        int64_t t_end) {
+    if (t_end < 0) t_end = T;
+    if (t_end <= t_begin) return;
+    const unsigned blocks = (unsigned)((t_end - t_begin + 7) / 8);  // 8 warps (positions) per block
     if (s.N <= 4)
-        hash_gather_kernel<4><<<blocks, 256, 0, st>>>(s, ht, tokens, seq_off, nseq, T, prior, sub, X, grow, Tpad, err);
+        hash_gather_kernel<4><<<blocks, 256, 0, st>>>(s, ht, tokens, seq_off, nseq, T, prior, sub, X, grow, Tpad, err,
+                                                      t_begin, t_end);
     else if (s.N <= 8)
-        hash_gather_kernel<8><<<blocks, 256, 0, st>>>(s, ht, tokens, seq_off, nseq, T, prior, sub, X, grow, Tpad, err);
+        hash_gather_kernel<8><<<blocks, 256, 0, st>>>(s, ht, tokens, seq_off, nseq, T, prior, sub, X, grow, Tpad, err,
+                                                      t_begin, t_end);
     else
         hash_gather_kernel<16><<<blocks, 256, 0, st>>>(s, ht, tokens, seq_off, nseq, T, prior, sub, X, grow, Tpad,
-                                                       err);
+                                                       err, t_begin, t_end);
     count_launch();
 }
 

@@ -42,7 +42,8 @@ void launch_hash_ids(const Shape& s, const HashTables* ht, const uint32_t* token
 // K1+K2 fused (X path): hash every position (lane per branch) and gather its rows into X.
 void launch_hash_gather(const Shape& s, const HashTables* ht, const uint32_t* tokens, const int64_t* seq_off,
                         int64_t nseq, int64_t T, const uint32_t* prior, const __nv_bfloat16* sub, __nv_bfloat16* X,
-                        int32_t* grow, int64_t Tpad, unsigned long long* err, cudaStream_t st);
+                        int32_t* grow, int64_t Tpad, unsigned long long* err, cudaStream_t st, int64_t t_begin = 0,
+                        int64_t t_end = -1);
 // Same, one warp per (position, branch): the small-T (decode / verify) latency variant.
 void launch_hash_gather_rows(const Shape& s, const HashTables* ht, const uint32_t* tokens, const int64_t* seq_off,
                              int64_t nseq, int64_t T, const uint32_t* prior, const __nv_bfloat16* sub,
@@ -92,6 +93,7 @@ struct FwdArgs {
     const CUtensorMap* tmap_x;
     // decode step: commit the decode state in the projection kernel's tail (or null)
     const struct DecodeCommit* commit;
+    int64_t x_row0;  // first row of tmap_x used by this call (chunked overlap)
 };
 // K1 + K2 + K3 in ONE persistent 2-CTA kernel: gather warps hash and gather X rows ahead
 // of the MMA pipeline (per-128-row ready counters), overlapping the HBM-bound gather with
