@@ -59,13 +59,15 @@ int64_t shard_lo(uint64_t V, int r, int P) {
 }  // namespace
 
 void make_tensor_map_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t rows, uint64_t row_pitch_bytes,
-                        uint32_t box_inner, uint32_t box_rows) {
+                        uint32_t box_inner, uint32_t box_rows, bool f32, int swizzle_bytes) {
     const cuuint64_t dims[2] = {inner, rows};
     const cuuint64_t strides[1] = {row_pitch_bytes};
     const cuuint32_t box[2] = {box_inner, box_rows};
     const cuuint32_t estr[2] = {1, 1};
-    const CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
-                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+    const CUresult r = encode_fn()(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                                   const_cast<void*>(base), dims, strides,
+                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Error(NGRAM_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
 }
@@ -200,6 +202,9 @@ int ngram_bank_create_ex(const char* config_json, int device, int shard_rank, in
         make_tensor_map_2d(&b->tmap_w, b->wcat.p, uint64_t(D), uint64_t(D), uint64_t(D) * 2, 64,
                            D % 256 == 0 ? 256 : 128);
         make_tensor_map_2d(&b->tmap_w2, b->wcat.p, uint64_t(D), uint64_t(D), uint64_t(D) * 2, 64, 128);
+        // E0 rows gathered by token id (tile::gather4) into the pair kernel's TMA epilogue
+        make_tensor_map_2d(&b->tmap_e0, b->e0.p, uint64_t(D), uint64_t(b->cfg.base_vocab), uint64_t(D) * 2, 32, 1,
+                           false, 64);
     }
     NGH_CUDA(cudaDeviceSynchronize());
     *out = b.release();

@@ -93,7 +93,7 @@ struct ngram_bank {
     ngh::DevBuf<ngk::HashTables> ht;
     ngh::DevBuf<unsigned long long> err;
 
-    CUtensorMap tmap_sub{}, tmap_w{}, tmap_w2{};
+    CUtensorMap tmap_sub{}, tmap_w{}, tmap_w2{}, tmap_e0{};
     ngh::Workspace ws;
 
     // host-buffer pipeline (ngram_embed_sequence_host)
@@ -136,7 +136,7 @@ struct ngram_decode {
 namespace ngh {
 // Build the TMA descriptors of a bank (driver entry point, no libcuda link).
 void make_tensor_map_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t rows, uint64_t row_pitch_bytes,
-                        uint32_t box_inner, uint32_t box_rows);
+                        uint32_t box_inner, uint32_t box_rows, bool f32 = false, int swizzle_bytes = 128);
 void ensure_workspace(ngram_bank* b, int64_t T);
 
 // Forward building blocks shared by forward.cpp / decode.cpp / shard.cpp.

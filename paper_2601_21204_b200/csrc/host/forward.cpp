@@ -73,6 +73,8 @@ void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, 
                     cudaStream_t st, int amp, XBuf* xb, bool allow_splitk, const ngk::FusedX* fx,
                     const ngk::DecodeCommit* commit, int64_t x_row0) {
     if (b->hash_only) throw Error(NGRAM_EINVAL, "bank was created hash-only (NGRAM_BANK_HASH_ONLY)");
+    if (b->tc_path && ((reinterpret_cast<uintptr_t>(rows) | reinterpret_cast<uintptr_t>(merged)) & 15) != 0)
+        throw Error(NGRAM_EINVAL, "output buffers must be 16-byte aligned (tensor-core path: vector / TMA stores)");
     if (T <= 0) return;
     ngk::FwdArgs a{};
     a.s = b->shape;
@@ -113,6 +115,22 @@ void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, 
         a.tmap_x = &xb->map;
     }
     b->prof_record(2, st);
+    // output maps for the pair kernel's TMA epilogue (prefill tiling: not the split-K path)
+    CUtensorMap map_rows, map_merged;
+    if (b->tc_path && b->shape.D % 256 == 0 && (T > 256 || !allow_splitk)) {
+        const uint64_t D = uint64_t(b->shape.D);
+        const bool f32 = !a.out_bf16;
+        const uint64_t pitch = D * (f32 ? 4 : 2);
+        if (a.rows_out) {
+            make_tensor_map_2d(&map_rows, a.rows_out, D, uint64_t(T), pitch, 32, 32, f32, f32 ? 128 : 64);
+            a.tmap_rows_out = &map_rows;
+        }
+        if (a.merged_out) {
+            make_tensor_map_2d(&map_merged, a.merged_out, D, uint64_t(T), pitch, 32, 32, f32, f32 ? 128 : 64);
+            a.tmap_merged_out = &map_merged;
+        }
+        a.tmap_e0 = &b->tmap_e0;
+    }
     if (b->tc_path) {
         float* ws = nullptr;
         const size_t need = allow_splitk ? ngk::splitk_workspace_floats(a, b->num_sms) : 0;

@@ -24,6 +24,7 @@
 //                   epilogue of tile i overlaps the MMAs of tile i+1.
 // Tiles are ordered n-fastest so the CTAs running concurrently share an m-block's
 // gathered rows through L2; W_cat (2*D^2 bytes) stays L2-resident (evict_last).
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 
@@ -69,7 +70,9 @@ struct TcParams {
     const unsigned long long* err;
     int use_x;  // A operand from materialised X (tmap_a is X) instead of gathered sub-table rows
     int64_t x_row0;  // first X row of this call (chunked K2/K3 overlap)
-    int epi_skip;  // diagnostics only (NGRAM_DEBUG_EPI_SKIP): drain TMEM without loads/stores
+    int epi_skip;  // diagnostics only (NGRAM_DEBUG_EPI_SKIP): 1 drain TMEM without loads/stores,
+                   // 2 (pair kernel) skip the E0 loads, 3 (pair kernel) skip the output stores
+    int diag_skip_a;  // diagnostics only (NGRAM_DEBUG_SKIP_A): X-path pair kernel loads W tiles only
     int ksplit;      // split-K factor (small-T path); >1 => raw fp32 partials to `partial`
     float* partial;  // [ksplit][T][D] fp32
     // fused K1+K2 (forward_tc2_kernel<true>): gather warps fill X, producers wait on `ready`
@@ -376,12 +379,25 @@ constexpr int NP2 = 4;     // producer warps per CTA
 
 constexpr int kEpiWarps2 = 8;  // two per TMEM lane quadrant, each owning half the columns
 
+// Epilogue modes.  0: E0 loaded and outputs stored by every thread straight from
+// registers (one token row per lane: 32 rows per warp instruction).  1: all epilogue
+// memory traffic by TMA -- each warp gathers its 32 rows x 32 columns of E0 per chunk with
+// tile::gather4 into a 2-slot SWIZZLE_64B ring (issued two chunks ahead, across tile
+// boundaries) and stages every output box in SWIZZLE_128B (fp32) / SWIZZLE_64B (bf16) smem
+// for a bulk tensor store.  Mode 1 costs one pipeline stage of smem.
+constexpr int stages2(int epi) { return epi ? kStages2 - 1 : kStages2; }
+constexpr int kE0Box = 32 * 32 * 2;   // one E0 chunk: 32 rows x 32 bf16 columns
+constexpr int kOutBox = 32 * 32 * 4;  // one staged output box (fp32 worst case)
+constexpr int epi_smem(int epi) { return epi ? kEpiWarps2 * (2 * kE0Box + kOutBox) : 0; }
+
 struct Cfg2 {
     static constexpr int kABytes = 128 * BK * 2;           // this CTA's 128 token rows
     static constexpr int kBBytes = (BN2 / 2) * BK * 2;     // this CTA's half of the W tile
     static constexpr int kStageBytes = kABytes + kBBytes;  // 32 KB
     static constexpr int kTmemCols = 2 * BN2;              // double-buffered 128 x 256 fp32
-    static constexpr int kSmemBytes = kStages2 * kStageBytes + 1024 + 256;
+    static constexpr int smem_bytes(int epi) {
+        return stages2(epi) * kStageBytes + epi_smem(epi) + 1024 + 512;
+    }
     // Warp roles: producers [0, NP2), epilogue [NP2, NP2+8), gather warps (fused K1+K2
     // variant) next, and the single MMA-issuing warp LAST: the warp arbiter picks the
     // highest eligible warp id first, so the tensor-core issue is never starved.
@@ -393,19 +409,64 @@ struct Cfg2 {
     static constexpr int kRowsPerWarp = 128 / NP2;
 };
 
-template <bool FX>
+// SWIZZLE_64B / SWIZZLE_128B smem address of 16-byte chunk j of row r of a box whose rows
+// are 64 / 128 bytes (buffers 512 / 1024-byte aligned): the TMA unit applies the same XOR
+// of address bits [4, 6) / [4, 7) with bits [7, 9) / [7, 10), and one row per lane makes
+// every warp-wide v4 access bank-conflict free.
+__device__ __forceinline__ uint32_t sw64(uint32_t base, int r, int j) {
+    return base + (uint32_t)r * 64u + (uint32_t)((j ^ ((r >> 1) & 3)) << 4);
+}
+__device__ __forceinline__ uint32_t sw128(uint32_t base, int r, int j) {
+    return base + (uint32_t)r * 128u + (uint32_t)((j ^ (r & 7)) << 4);
+}
+
+// Stage one 32 x 32 output box (lane = row) and hand it to TMA.  The staging buffer is
+// rewritten only after the bulk group that last read it has finished reading smem.
+__device__ __forceinline__ void epi_store_box(uint8_t* obuf, int lane, const float (&mv)[32], float mul, bool scaled,
+                                              int out_bf16, const CUtensorMap* map, int32_t col, int32_t row,
+                                              uint64_t pol) {
+    if (lane == 0) bulk_wait_group_read<0>();
+    __syncwarp();
+    const uint32_t base = smem_u32(obuf);
+    float f[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) f[j] = scaled ? __fmul_rn(mv[j], mul) : mv[j];
+    if (out_bf16) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            st_shared_v4u(sw64(base, lane, j),
+                          make_uint4(pack_bf16x2(f[8 * j], f[8 * j + 1]), pack_bf16x2(f[8 * j + 2], f[8 * j + 3]),
+                                     pack_bf16x2(f[8 * j + 4], f[8 * j + 5]), pack_bf16x2(f[8 * j + 6], f[8 * j + 7])));
+    } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            st_shared_v4(sw128(base, lane, j), make_float4(f[4 * j], f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]));
+    }
+    fence_proxy_async_smem();  // generic-proxy smem writes -> async-proxy (TMA) reads
+    __syncwarp();
+    if (lane == 0) {
+        tma_store_2d(map, obuf, col, row, pol);
+        bulk_commit_group();
+    }
+}
+
+template <bool FX, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FX ? Cfg2::kThreadsFX : Cfg2::kThreads, 1)
     forward_tc2_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_w,
-                       TcParams p) {
+                       const __grid_constant__ CUtensorMap tmap_rows, const __grid_constant__ CUtensorMap tmap_merged,
+                       const __grid_constant__ CUtensorMap tmap_e0, TcParams p) {
     using C = Cfg2;
+    constexpr int kStages2 = stages2(EPI);  // shadows the namespace constant
     constexpr int kMmaWarp = FX ? C::kGatherWarp0 + C::kGatherWarps : C::kGatherWarp0;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages2 * C::kStageBytes);
+    uint8_t* staging = smem + kStages2 * C::kStageBytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(staging + epi_smem(EPI));
     uint64_t* empty = full + kStages2;
     uint64_t* tfull = empty + kStages2;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* e0bar = tempty + 2;  // [kEpiWarps2][2] E0 ring slots (mode 1)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(e0bar + 2 * kEpiWarps2);
 
     if (*p.err != ~0ull) return;  // uniform across the grid
 
@@ -431,6 +492,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FX ? Cfg2::kThreadsF
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], 2 * kEpiWarps2);  // epilogue warps of both CTAs (leader's copy)
         }
+        if (EPI)
+            for (int i = 0; i < 2 * kEpiWarps2; ++i) mbar_init(&e0bar[i], 1);
         fence_mbar_init();
         tma_prefetch_desc(&tmap_a);
         tma_prefetch_desc(&tmap_w);
@@ -470,9 +533,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FX ? Cfg2::kThreadsF
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (warp == 0 && lane == 0) {
                         uint8_t* a_dst = smem + stage * C::kStageBytes;
-                        if (leader) mbar_arrive_expect_tx(&full[stage], 2 * C::kStageBytes);
-                        tma_load_2d_2cta(a_dst, &tmap_a, leader_bar(&full[stage]), kb * BK,
-                                         (int32_t)(t0 + p.x_row0), 0);
+                        if (leader)
+                            mbar_arrive_expect_tx(&full[stage], p.diag_skip_a ? 2 * C::kBBytes : 2 * C::kStageBytes);
+                        if (!p.diag_skip_a)
+                            tma_load_2d_2cta(a_dst, &tmap_a, leader_bar(&full[stage]), kb * BK,
+                                             (int32_t)(t0 + p.x_row0), 0);
                         tma_load_2d_2cta(a_dst + C::kABytes, &tmap_w, leader_bar(&full[stage]), kb * BK, wrow, pol_w);
                     }
                     __syncwarp();
@@ -560,6 +625,95 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FX ? Cfg2::kThreadsF
             __syncwarp();
             if (lane == 0) red_release_gpu_add(p.ready + (t >> 7), 1);
         }
+    } else if (EPI) {
+        // ------------------------------------------------------------ TMA epilogue (both CTAs)
+        // Chunk g of this warp = columns [col0 + 32 (g % 4), +32) of tile pair + (g / 4) npairs.
+        const int ew = warp - C::kEpiWarp0;  // 0..7
+        const int q = warp & 3;              // TMEM lane quadrant this warp may access
+        const int half = ew >> 2;            // column half of the tile this warp owns
+        const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
+        const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty[1]), 0);
+        constexpr int kChunks = BN2 / 2 / 32;
+        uint8_t* e0ring = staging + ew * (2 * kE0Box);
+        uint8_t* obuf = staging + kEpiWarps2 * 2 * kE0Box + ew * kOutBox;
+        uint64_t* ebar = e0bar + 2 * ew;
+        const uint64_t pol_out = policy_evict_first();
+        const int64_t nchunks = ((tiles - pair + npairs - 1) / npairs) * kChunks;
+        // gather E0 rows of chunk g into ring slot g & 1 (4 rows per gather4, lanes 0..7)
+        auto issue_e0 = [&](int64_t g) {
+            const int64_t tile = pair + (g / kChunks) * npairs;
+            const int c = (int)(g % kChunks);
+            const int64_t m = tile / nN;
+            const int n = (int)(tile - m * nN);
+            const int64_t t = m * BM2 + (int64_t)rank * 128 + q * 32 + lane;
+            const int tok = t < p.T ? (int)__ldg(p.tokens + t) : 0;  // rows past T: any valid row
+            const int l4 = 4 * (lane & 7);
+            const int r0 = __shfl_sync(0xffffffffu, tok, l4), r1 = __shfl_sync(0xffffffffu, tok, l4 + 1);
+            const int r2 = __shfl_sync(0xffffffffu, tok, l4 + 2), r3 = __shfl_sync(0xffffffffu, tok, l4 + 3);
+            uint64_t* bar = &ebar[g & 1];
+            if (lane == 0) mbar_arrive_expect_tx(bar, kE0Box);
+            __syncwarp();
+            if (lane < 8)
+                tma_gather4(e0ring + (g & 1) * kE0Box + lane * 4 * 64, &tmap_e0, bar, n * BN2 + half * (BN2 / 2) + c * 32,
+                            r0, r1, r2, r3);
+        };
+        if (nchunks > 0) issue_e0(0);
+        if (nchunks > 1) issue_e0(1);
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        int64_t g = 0;
+        for (int64_t tile = pair; tile < tiles; tile += npairs) {
+            const int64_t m = tile / nN;
+            const int n = (int)(tile - m * nN);
+            const int32_t orow = (int32_t)(m * BM2 + (int64_t)rank * 128 + q * 32);
+            const int col0 = n * BN2 + half * (BN2 / 2);
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < kChunks; ++c, ++g) {
+                uint32_t v[32];
+                tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) +
+                                       (uint32_t)(acc * BN2 + half * (BN2 / 2) + c * 32),
+                                   v);
+                mbar_wait(&ebar[g & 1], (uint32_t)((g >> 1) & 1));
+                const uint32_t eb = smem_u32(e0ring + (g & 1) * kE0Box);
+                uint4 e[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) e[i] = ld_shared_v4u(sw64(eb, lane, i));
+                fence_proxy_async_smem();  // generic reads of the slot before TMA refills it
+                __syncwarp();
+                if (g + 2 < nchunks) issue_e0(g + 2);
+                tmem_ld_wait();
+                float mv[32];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const uint32_t w[4] = {e[i].x, e[i].y, e[i].z, e[i].w};
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        const int j = i * 8 + h * 2;
+                        mv[j] = __fmul_rn(__fadd_rn(bf16_bits_to_f32(w[h] & 0xffffu), __uint_as_float(v[j])),
+                                          p.scale);
+                        mv[j + 1] =
+                            __fmul_rn(__fadd_rn(bf16_bits_to_f32(w[h] >> 16), __uint_as_float(v[j + 1])), p.scale);
+                    }
+                }
+                if (c + 1 == kChunks) {  // accumulator fully read: release it to the MMA warp
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(acc == 0 ? tempty_leader0 : tempty_leader1);
+                }
+                // rows past T are clipped by the output tensor maps
+                if (p.merged_out)
+                    epi_store_box(obuf, lane, mv, 1.0f, false, p.out_bf16, &tmap_merged, col0 + c * 32, orow, pol_out);
+                if (p.write_rows)
+                    epi_store_box(obuf, lane, mv, p.amp, true, p.out_bf16, &tmap_rows, col0 + c * 32, orow, pol_out);
+            }
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+        if (lane == 0) bulk_wait_group<0>();  // output stores complete before exit
     } else {
         // ------------------------------------------------------------ epilogue (both CTAs)
         const int ew = warp - C::kEpiWarp0;  // 0..7
@@ -575,12 +729,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FX ? Cfg2::kThreadsF
             const int64_t m = tile / nN;
             const int n = (int)(tile - m * nN);
             const int64_t t = m * BM2 + (int64_t)rank * 128 + r;
-            const bool valid = t < p.T && !p.epi_skip;
+            const bool valid = t < p.T && p.epi_skip != 1;
+            const bool load_e0 = valid && p.epi_skip != 2;
             const uint32_t tok = valid ? __ldg(p.tokens + t) : 0u;
             const int col0 = n * BN2 + half * (BN2 / 2);
             const __nv_bfloat16* e0row = p.e0 + (int64_t)tok * D + col0;
             uint4 e[4], en[4];
-            if (valid) {  // E0 chunk 0, loaded before the accumulator is ready
+            if (!load_e0) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) e[i] = en[i] = make_uint4(0, 0, 0, 0);
+            }
+            if (load_e0) {  // E0 chunk 0, loaded before the accumulator is ready
 #pragma unroll
                 for (int i = 0; i < 4; ++i) e[i] = __ldg(reinterpret_cast<const uint4*>(e0row) + i);
             }
@@ -592,7 +751,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FX ? Cfg2::kThreadsF
                 tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) +
                                        (uint32_t)(acc * BN2 + half * (BN2 / 2) + c * 32),
                                    v);
-                if (valid && c + 1 < kChunks) {  // prefetch the next E0 chunk
+                if (load_e0 && c + 1 < kChunks) {  // prefetch the next E0 chunk
 #pragma unroll
                     for (int i = 0; i < 4; ++i) en[i] = __ldg(reinterpret_cast<const uint4*>(e0row + (c + 1) * 32) + i);
                 }
@@ -612,6 +771,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FX ? Cfg2::kThreadsF
                         }
                     }
                     const int64_t o = t * D + col0 + c * 32;
+                    if (p.epi_skip == 3 && mv[0] != 1.2345e-30f) continue;  // diagnostics: no stores
                     if (p.merged_out) store_chunk(p.merged_out, p.out_bf16, o, mv);
                     if (p.write_rows) {
 #pragma unroll
@@ -662,7 +822,8 @@ void launch_cfg(const FwdArgs& a, int num_sms, cudaStream_t st, int ksplit = 1, 
     p.err = a.err;
     p.use_x = a.tmap_x != nullptr;
     p.x_row0 = a.x_row0;
-    p.epi_skip = getenv("NGRAM_DEBUG_EPI_SKIP") ? 1 : 0;
+    p.epi_skip = getenv("NGRAM_DEBUG_EPI_SKIP") ? atoi(getenv("NGRAM_DEBUG_EPI_SKIP")) : 0;
+    p.diag_skip_a = getenv("NGRAM_DEBUG_SKIP_A") ? 1 : 0;
     const int64_t tiles = ((a.T + BM - 1) / BM) * (a.s.D / BN) * ksplit;
     int grid = (int)(tiles < num_sms ? tiles : num_sms);
     if (grid < 1) grid = 1;
@@ -672,6 +833,14 @@ void launch_cfg(const FwdArgs& a, int num_sms, cudaStream_t st, int ksplit = 1, 
     forward_tc_kernel<BN, NP, MODE><<<grid, C::kThreads, C::kSmemBytes, st>>>(a.tmap_x ? *a.tmap_x : *a.tmap_sub,
                                                                               *wmap, p);
     count_launch();
+}
+
+int tma_epi_mode() {
+    static const int v = [] {
+        const char* e = getenv("NGRAM_TMA_EPI");
+        return e ? std::min(1, std::max(0, atoi(e))) : 1;
+    }();
+    return v;
 }
 
 void launch_tc2(const FwdArgs& a, int num_sms, cudaStream_t st) {
@@ -694,14 +863,29 @@ void launch_tc2(const FwdArgs& a, int num_sms, cudaStream_t st) {
     p.err = a.err;
     p.use_x = a.tmap_x != nullptr;
     p.x_row0 = a.x_row0;
-    p.epi_skip = getenv("NGRAM_DEBUG_EPI_SKIP") ? 1 : 0;
+    p.epi_skip = getenv("NGRAM_DEBUG_EPI_SKIP") ? atoi(getenv("NGRAM_DEBUG_EPI_SKIP")) : 0;
+    p.diag_skip_a = getenv("NGRAM_DEBUG_SKIP_A") ? 1 : 0;
     const int64_t tiles = ((a.T + BM2 - 1) / BM2) * (a.s.D / BN2);
     int64_t pairs = num_sms / 2;
     if (tiles < pairs) pairs = tiles;
     if (pairs < 1) pairs = 1;
-    cudaFuncSetAttribute(forward_tc2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2::kSmemBytes);
-    forward_tc2_kernel<false><<<(unsigned)(2 * pairs), Cfg2::kThreads, Cfg2::kSmemBytes, st>>>(
-        a.tmap_x ? *a.tmap_x : *a.tmap_sub, *a.tmap_w2, p);
+    // TMA epilogue when every written output has a map (NGRAM_TMA_EPI=0 selects mode 0)
+    const bool maps_ok = a.tmap_e0 && (!p.merged_out || a.tmap_merged_out) && (!p.write_rows || a.tmap_rows_out);
+    const int epi = maps_ok && !p.epi_skip ? tma_epi_mode() : 0;
+    const CUtensorMap& ma = a.tmap_x ? *a.tmap_x : *a.tmap_sub;
+    const CUtensorMap& mr = a.tmap_rows_out ? *a.tmap_rows_out : *a.tmap_w2;
+    const CUtensorMap& mm = a.tmap_merged_out ? *a.tmap_merged_out : *a.tmap_w2;
+    const unsigned grid = (unsigned)(2 * pairs);
+    const CUtensorMap& me = a.tmap_e0 ? *a.tmap_e0 : *a.tmap_w2;
+    if (epi) {
+        cudaFuncSetAttribute(forward_tc2_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Cfg2::smem_bytes(1));
+        forward_tc2_kernel<false, 1><<<grid, Cfg2::kThreads, Cfg2::smem_bytes(1), st>>>(ma, *a.tmap_w2, mr, mm, me, p);
+    } else {
+        cudaFuncSetAttribute(forward_tc2_kernel<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Cfg2::smem_bytes(0));
+        forward_tc2_kernel<false, 0><<<grid, Cfg2::kThreads, Cfg2::smem_bytes(0), st>>>(ma, *a.tmap_w2, mr, mm, me, p);
+    }
     count_launch();
 }
 
@@ -724,7 +908,8 @@ TcParams tc2_params(const FwdArgs& a) {
     p.err = a.err;
     p.use_x = 1;
     p.x_row0 = a.x_row0;
-    p.epi_skip = getenv("NGRAM_DEBUG_EPI_SKIP") ? 1 : 0;
+    p.epi_skip = getenv("NGRAM_DEBUG_EPI_SKIP") ? atoi(getenv("NGRAM_DEBUG_EPI_SKIP")) : 0;
+    p.diag_skip_a = getenv("NGRAM_DEBUG_SKIP_A") ? 1 : 0;
     return p;
 }
 
@@ -807,9 +992,10 @@ void launch_forward_tc2_fusedx(const FwdArgs& a, const FusedX& fx, int num_sms, 
     int64_t pairs = num_sms / 2;  // persistent: every CTA co-resident (the ready waits rely on it)
     if (tiles < pairs) pairs = tiles;
     if (pairs < 1) pairs = 1;
-    cudaFuncSetAttribute(forward_tc2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2::kSmemBytes);
-    forward_tc2_kernel<true><<<(unsigned)(2 * pairs), Cfg2::kThreadsFX, Cfg2::kSmemBytes, st>>>(*a.tmap_x, *a.tmap_w2,
-                                                                                               p);
+    constexpr int smem = Cfg2::smem_bytes(0);
+    cudaFuncSetAttribute(forward_tc2_kernel<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    forward_tc2_kernel<true, 0><<<(unsigned)(2 * pairs), Cfg2::kThreadsFX, smem, st>>>(
+        *a.tmap_x, *a.tmap_w2, *a.tmap_w2, *a.tmap_w2, *a.tmap_w2, p);
     count_launch();
 }
 

@@ -94,6 +94,11 @@ struct FwdArgs {
     // decode step: commit the decode state in the projection kernel's tail (or null)
     const struct DecodeCommit* commit;
     int64_t x_row0;  // first row of tmap_x used by this call (chunked overlap)
+    // TMA epilogue of the pair kernel: [T][D] output maps (32 x 32 box; SWIZZLE_128B fp32 /
+    // SWIZZLE_64B bf16) and the E0 gather map ([V0][D] bf16, 32 x 1 box, SWIZZLE_64B), or null
+    const CUtensorMap* tmap_rows_out;
+    const CUtensorMap* tmap_merged_out;
+    const CUtensorMap* tmap_e0;
 };
 // K1 + K2 + K3 in ONE persistent 2-CTA kernel: gather warps hash and gather X rows ahead
 // of the MMA pipeline (per-128-row ready counters), overlapping the HBM-bound gather with

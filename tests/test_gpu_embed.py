@@ -13,7 +13,7 @@ import torch
 import oracle as O
 from helpers import assert_rows_close, bf16_to_f32, dev_i64, dev_u32, gold, gold_config
 from paper_2601_21204_b200 import ngram as G
-from paper_2601_21204_b200.abi import OutOfRange
+from paper_2601_21204_b200.abi import InvalidArgument, OutOfRange
 
 pytestmark = pytest.mark.gpu
 
@@ -250,3 +250,55 @@ def test_fused_k1_k2_k3_kernel_matches_oracle(cuda):
     with pytest.raises(OutOfRange):
         db.sync_errors()
     assert (out == 3.0).all()
+
+
+@pytest.mark.parametrize("out_dtype", [torch.float32, torch.bfloat16])
+def test_pair_kernel_tma_epilogue_edges(cuda, out_dtype):
+    """The 2-CTA projection's TMA epilogue (E0 rows by tile::gather4, outputs by bulk tensor
+    stores clipped at T): ragged T (not a multiple of 32 / 128 / 256), rows + merged; the
+    direct-store epilogue (NGRAM_TMA_EPI=0 in a subprocess is the A/B switch) computes the
+    same values.  Output buffers that are not 16-byte aligned are rejected up front."""
+    cfg = O.make_default_config(3000, 512, 3, 2)
+    hb = O.make_bank(cfg, 17, round_bf16=True)
+    db = G.DeviceBank(cfg).upload(hb.base, hb.sub, hb.proj)
+    seqs = [O.uniform_tokens(40, 3000, 1001), O.uniform_tokens(41, 3000, 290), O.uniform_tokens(42, 3000, 7)]
+    allt = np.concatenate(seqs)
+    off = np.concatenate([[0], np.cumsum([len(s) for s in seqs])])
+    T = len(allt)
+    t, o = dev_u32(torch, allt, cuda), dev_i64(torch, off, cuda)
+    rows, merged = G.embed_forward(db, t, o, merged=True, out_dtype=out_dtype)
+    db.sync_errors()
+    ref_r, ref_m = zip(*[O.embed_sequence(hb, s, double=True) for s in seqs])
+    bf = out_dtype == torch.bfloat16
+    assert_rows_close(rows.float().cpu().numpy(), np.concatenate(ref_r), bf16=bf)
+    assert_rows_close(merged.float().cpu().numpy(), np.concatenate(ref_m), bf16=bf)
+    buf = torch.empty(T * 512 + 8, dtype=out_dtype, device=cuda)
+    with pytest.raises(InvalidArgument):
+        G.embed_forward(db, t, o, out_dtype=out_dtype, out_rows=buf[1:1 + T * 512].view(T, 512))
+    # the direct-store epilogue (selected once per process) must produce identical bits
+    import os, subprocess, sys, tempfile
+    code = f"""
+import sys, numpy as np, torch
+sys.path[:0] = {[os.path.join(os.path.dirname(__file__)), os.path.dirname(os.path.dirname(__file__)),
+                 os.path.join(os.path.dirname(os.path.dirname(__file__)), "oracle")]!r}
+import oracle as O
+from helpers import dev_i64, dev_u32
+from paper_2601_21204_b200 import ngram as G
+cfg = O.make_default_config(3000, 512, 3, 2)
+hb = O.make_bank(cfg, 17, round_bf16=True)
+db = G.DeviceBank(cfg).upload(hb.base, hb.sub, hb.proj)
+seqs = [O.uniform_tokens(40, 3000, 1001), O.uniform_tokens(41, 3000, 290), O.uniform_tokens(42, 3000, 7)]
+allt = np.concatenate(seqs)
+off = np.concatenate([[0], np.cumsum([len(s) for s in seqs])])
+r, m = G.embed_forward(db, dev_u32(torch, allt, "cuda:0"), dev_i64(torch, off, "cuda:0"), merged=True,
+                       out_dtype=torch.{'bfloat16' if bf else 'float32'})
+db.sync_errors()
+np.save(sys.argv[1], torch.stack([r, m]).view(torch.int16 if r.dtype == torch.bfloat16 else torch.int32).cpu().numpy())
+"""
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "direct.npy")
+        subprocess.run([sys.executable, "-c", code, path], check=True, timeout=300,
+                       env={**os.environ, "NGRAM_TMA_EPI": "0"})
+        direct = np.load(path)
+    ours = torch.stack([rows, merged]).view(torch.int16 if bf else torch.int32).cpu().numpy()
+    assert np.array_equal(ours, direct)
