@@ -385,10 +385,16 @@ constexpr int kEpiWarps2 = 8;  // two per TMEM lane quadrant, each owning half t
 // tile::gather4 into a 2-slot SWIZZLE_64B ring (issued two chunks ahead, across tile
 // boundaries) and stages every output box in SWIZZLE_128B (fp32) / SWIZZLE_64B (bf16) smem
 // for a bulk tensor store.  Mode 1 costs one pipeline stage of smem.
-constexpr int stages2(int epi) { return epi ? kStages2 - 1 : kStages2; }
+// Mode 1 = 5 stages, 2 E0 slots, 1 output buffer per warp.  Measured equal within noise
+// (profiles/README.md): 4 stages with 2 output buffers, or with 4 E0 slots (a tile ahead).
+constexpr int stages2(int epi) { return epi == 0 ? kStages2 : epi == 1 ? kStages2 - 1 : kStages2 - 2; }
+constexpr int epi_ring(int epi) { return epi == 3 ? 4 : 2; }
+constexpr int epi_obufs(int epi) { return epi == 2 ? 2 : 1; }
 constexpr int kE0Box = 32 * 32 * 2;   // one E0 chunk: 32 rows x 32 bf16 columns
 constexpr int kOutBox = 32 * 32 * 4;  // one staged output box (fp32 worst case)
-constexpr int epi_smem(int epi) { return epi ? kEpiWarps2 * (2 * kE0Box + kOutBox) : 0; }
+constexpr int epi_smem(int epi) {
+    return epi ? kEpiWarps2 * (epi_ring(epi) * kE0Box + epi_obufs(epi) * kOutBox) : 0;
+}
 
 struct Cfg2 {
     static constexpr int kABytes = 128 * BK * 2;           // this CTA's 128 token rows
@@ -422,10 +428,11 @@ __device__ __forceinline__ uint32_t sw128(uint32_t base, int r, int j) {
 
 // Stage one 32 x 32 output box (lane = row) and hand it to TMA.  The staging buffer is
 // rewritten only after the bulk group that last read it has finished reading smem.
+template <int NBUF>
 __device__ __forceinline__ void epi_store_box(uint8_t* obuf, int lane, const float (&mv)[32], float mul, bool scaled,
                                               int out_bf16, const CUtensorMap* map, int32_t col, int32_t row,
                                               uint64_t pol) {
-    if (lane == 0) bulk_wait_group_read<0>();
+    if (lane == 0) bulk_wait_group_read<NBUF - 1>();
     __syncwarp();
     const uint32_t base = smem_u32(obuf);
     float f[32];
@@ -465,8 +472,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FX ? Cfg2::kThreadsF
     uint64_t* empty = full + kStages2;
     uint64_t* tfull = empty + kStages2;
     uint64_t* tempty = tfull + 2;
-    uint64_t* e0bar = tempty + 2;  // [kEpiWarps2][2] E0 ring slots (mode 1)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(e0bar + 2 * kEpiWarps2);
+    uint64_t* e0bar = tempty + 2;  // [kEpiWarps2][ring] E0 ring slots (mode 1)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(e0bar + epi_ring(EPI) * kEpiWarps2);
 
     if (*p.err != ~0ull) return;  // uniform across the grid
 
@@ -493,7 +500,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FX ? Cfg2::kThreadsF
             mbar_init(&tempty[i], 2 * kEpiWarps2);  // epilogue warps of both CTAs (leader's copy)
         }
         if (EPI)
-            for (int i = 0; i < 2 * kEpiWarps2; ++i) mbar_init(&e0bar[i], 1);
+            for (int i = 0; i < epi_ring(EPI) * kEpiWarps2; ++i) mbar_init(&e0bar[i], 1);
         fence_mbar_init();
         tma_prefetch_desc(&tmap_a);
         tma_prefetch_desc(&tmap_w);
@@ -634,12 +641,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FX ? Cfg2::kThreadsF
         const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
         const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty[1]), 0);
         constexpr int kChunks = BN2 / 2 / 32;
-        uint8_t* e0ring = staging + ew * (2 * kE0Box);
-        uint8_t* obuf = staging + kEpiWarps2 * 2 * kE0Box + ew * kOutBox;
-        uint64_t* ebar = e0bar + 2 * ew;
+        constexpr int R = epi_ring(EPI);
+        constexpr int OB = epi_obufs(EPI);
+        uint8_t* e0ring = staging + ew * (R * kE0Box);
+        uint8_t* obuf0 = staging + kEpiWarps2 * R * kE0Box + ew * OB * kOutBox;
+        int ob = 0;
+        uint64_t* ebar = e0bar + R * ew;
         const uint64_t pol_out = policy_evict_first();
         const int64_t nchunks = ((tiles - pair + npairs - 1) / npairs) * kChunks;
-        // gather E0 rows of chunk g into ring slot g & 1 (4 rows per gather4, lanes 0..7)
+        // gather E0 rows of chunk g into ring slot g % R (4 rows per gather4, lanes 0..7)
         auto issue_e0 = [&](int64_t g) {
             const int64_t tile = pair + (g / kChunks) * npairs;
             const int c = (int)(g % kChunks);
@@ -650,15 +660,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FX ? Cfg2::kThreadsF
             const int l4 = 4 * (lane & 7);
             const int r0 = __shfl_sync(0xffffffffu, tok, l4), r1 = __shfl_sync(0xffffffffu, tok, l4 + 1);
             const int r2 = __shfl_sync(0xffffffffu, tok, l4 + 2), r3 = __shfl_sync(0xffffffffu, tok, l4 + 3);
-            uint64_t* bar = &ebar[g & 1];
+            uint64_t* bar = &ebar[g % R];
             if (lane == 0) mbar_arrive_expect_tx(bar, kE0Box);
             __syncwarp();
             if (lane < 8)
-                tma_gather4(e0ring + (g & 1) * kE0Box + lane * 4 * 64, &tmap_e0, bar, n * BN2 + half * (BN2 / 2) + c * 32,
+                tma_gather4(e0ring + (g % R) * kE0Box + lane * 4 * 64, &tmap_e0, bar, n * BN2 + half * (BN2 / 2) + c * 32,
                             r0, r1, r2, r3);
         };
-        if (nchunks > 0) issue_e0(0);
-        if (nchunks > 1) issue_e0(1);
+        for (int64_t g0 = 0; g0 < R && g0 < nchunks; ++g0) issue_e0(g0);
         int acc = 0;
         uint32_t acc_phase = 0;
         int64_t g = 0;
@@ -675,14 +684,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FX ? Cfg2::kThreadsF
                 tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) +
                                        (uint32_t)(acc * BN2 + half * (BN2 / 2) + c * 32),
                                    v);
-                mbar_wait(&ebar[g & 1], (uint32_t)((g >> 1) & 1));
-                const uint32_t eb = smem_u32(e0ring + (g & 1) * kE0Box);
+                mbar_wait(&ebar[g % R], (uint32_t)((g / R) & 1));
+                const uint32_t eb = smem_u32(e0ring + (g % R) * kE0Box);
                 uint4 e[4];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) e[i] = ld_shared_v4u(sw64(eb, lane, i));
                 fence_proxy_async_smem();  // generic reads of the slot before TMA refills it
                 __syncwarp();
-                if (g + 2 < nchunks) issue_e0(g + 2);
+                if (g + R < nchunks) issue_e0(g + R);
                 tmem_ld_wait();
                 float mv[32];
 #pragma unroll
@@ -703,10 +712,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FX ? Cfg2::kThreadsF
                     if (lane == 0) mbar_arrive_cluster(acc == 0 ? tempty_leader0 : tempty_leader1);
                 }
                 // rows past T are clipped by the output tensor maps
-                if (p.merged_out)
-                    epi_store_box(obuf, lane, mv, 1.0f, false, p.out_bf16, &tmap_merged, col0 + c * 32, orow, pol_out);
-                if (p.write_rows)
-                    epi_store_box(obuf, lane, mv, p.amp, true, p.out_bf16, &tmap_rows, col0 + c * 32, orow, pol_out);
+                if (p.merged_out) {
+                    epi_store_box<OB>(obuf0 + ob * kOutBox, lane, mv, 1.0f, false, p.out_bf16, &tmap_merged,
+                                      col0 + c * 32, orow, pol_out);
+                    ob = (ob + 1) % OB;
+                }
+                if (p.write_rows) {
+                    epi_store_box<OB>(obuf0 + ob * kOutBox, lane, mv, p.amp, true, p.out_bf16, &tmap_rows,
+                                      col0 + c * 32, orow, pol_out);
+                    ob = (ob + 1) % OB;
+                }
             }
             if (++acc == 2) {
                 acc = 0;
@@ -877,7 +892,7 @@ void launch_tc2(const FwdArgs& a, int num_sms, cudaStream_t st) {
     const CUtensorMap& mm = a.tmap_merged_out ? *a.tmap_merged_out : *a.tmap_w2;
     const unsigned grid = (unsigned)(2 * pairs);
     const CUtensorMap& me = a.tmap_e0 ? *a.tmap_e0 : *a.tmap_w2;
-    if (epi) {
+    if (epi == 1) {
         cudaFuncSetAttribute(forward_tc2_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              Cfg2::smem_bytes(1));
         forward_tc2_kernel<false, 1><<<grid, Cfg2::kThreads, Cfg2::smem_bytes(1), st>>>(ma, *a.tmap_w2, mr, mm, me, p);
