@@ -229,6 +229,32 @@ int ngram_shard_scatter_rows(ngram_shard_group* g, const uint32_t* all_tokens, c
 int ngram_shard_project(ngram_shard_group* g, const uint32_t* home_tokens, int64_t home_T, void* rows_out,
                         void* merged_out, int out_dtype, void* stream);
 
+/* ------------------------------------------------------------------ backward (training) */
+/* embed_sequence_backward (embedding.hpp:438-459) batched on the device: gradients of the
+ * embedding rows w.r.t. every bank parameter, ACCUMULATED (+=) into an fp32 gradient bank
+ * with the device layout (E0 V0 x D, sub-tables concatenated by branch, projections as
+ * W_cat D x D, LN gain / bias D).  amplify_backward (embedding.hpp:291-336) then
+ * embed_backward (:338-376) per position; the dense products dW_cat += U^T X and
+ * dX = U W_cat are fp32 GEMMs (cuBLAS, no TF32); scatters use fp32 atomics, so results
+ * match the reference within an fp32 tolerance (not bit-exact).  Single-shard banks only. */
+typedef struct ngram_grad ngram_grad;
+int ngram_grad_create(ngram_bank* bank, ngram_grad** out); /* zero-initialised */
+int ngram_grad_destroy(ngram_grad* g);
+int ngram_grad_zero(ngram_grad* g, void* stream);
+#define NGRAM_BWD_SKIP_AMPLIFY 1 /* upstream is d(merged) already: embed_backward only */
+/* tokens/seq_offsets/prior as ngram_embed_forward (device); merged: dev f32 [T][D], the
+ * pre-amplification rows of the forward (needed for layer_norm, else may be null);
+ * upstream: dev f32 [T][D], dL/d(rows). */
+int ngram_embed_backward(ngram_grad* g, const uint32_t* tokens, const int64_t* seq_offsets, int64_t nseq,
+                         int64_t total_tokens, const uint32_t* prior, const float* merged, const float* upstream,
+                         int flags, void* stream);
+/* Device view of one gradient tensor: which 0 = E0, 1 = sub-tables (device row layout),
+ * 2 = W_cat, 3 = ln_gain, 4 = ln_bias. */
+int ngram_grad_tensor(ngram_grad* g, int which, float** dev_ptr, int64_t* numel);
+/* Host copy in the reference layout (embedding_bank_t): base V0 x D, sub[b] V_b x d,
+ * proj[b] D x d (v2 only), gain / bias D (layer_norm only); null pointers are skipped. */
+int ngram_grad_download(ngram_grad* g, float* base, float* const* sub, float* const* proj, float* gain, float* bias);
+
 #ifdef __cplusplus
 }
 #endif

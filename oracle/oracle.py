@@ -54,6 +54,10 @@ def lib():
                     _u64p, _f32p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_void_p, C.c_void_p]
         L.or_embed_sequence_f32.argtypes = seq_args + [C.c_void_p, _f32p]
         L.or_embed_sequence_f64.argtypes = seq_args + [C.c_void_p, _f64p]
+        L.or_embed_sequence_backward_f64.argtypes = [
+            _u32p, C.c_int64, C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_uint32, C.c_int, C.c_int, C.c_int, _u64p,
+            C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+            C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_void_p, C.c_void_p]
         L.or_synth_value.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint32, C.c_float]
         L.or_synth_value.restype = C.c_float
         L.or_synth_scale.argtypes = [C.c_double]
@@ -130,6 +134,9 @@ def ref():
                                              C.c_void_p]
         L.ref_embed_batch_mt.argtypes = [C.c_void_p, _u32p, np.ctypeslib.ndpointer(np.int64), C.c_int, C.c_int,
                                          _f32p]
+        L.ref_embed_sequence_backward_f64.argtypes = [C.c_void_p, _u32p, C.c_int64, C.c_void_p, C.c_int64,
+                                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                                      C.c_void_p, C.c_void_p]
         L.ref_cache_create.argtypes = [C.c_char_p]
         L.ref_cache_create.restype = C.c_void_p
         L.ref_cache_destroy.argtypes = [C.c_void_p]
@@ -256,6 +263,38 @@ def embed_sequence(bank: HostBank, tokens, prior=None, double=False):
     if rc:
         raise (IndexError if rc == -2 else ValueError)(f"or_embed_sequence rc={rc}")
     return rows, merged
+
+
+def zero_grads(cfg):
+    """zeros_like(bank) in double (embedding.hpp:123-134): the gradient accumulator."""
+    N, K, D, B, d, v, denom = shape(cfg)
+    sv = sub_vocab_array(cfg)
+    return {"base": np.zeros((cfg["base_vocab"], D)), "sub": [np.zeros((int(sv[b]), d)) for b in range(B)],
+            "proj": [np.zeros((D, d)) for _ in range(B)] if v == 1 else [], "gain": np.zeros(D), "bias": np.zeros(D)}
+
+
+def embed_sequence_backward(bank: HostBank, tokens, merged, upstream, prior=None, grads=None):
+    """embed_sequence_backward<double> restated (embedding.hpp:438-459) over the float bank:
+    amplify_backward then embed_backward per position, accumulated into `grads` (double)."""
+    cfg = bank.cfg
+    N, K, D, B, d, v, denom = shape(cfg)
+    g = grads if grads is not None else zero_grads(cfg)
+    t = np.ascontiguousarray(tokens, np.uint32)
+    m = np.ascontiguousarray(merged, np.float64)
+    u = np.ascontiguousarray(upstream, np.float64)
+    pr = None if prior is None else np.ascontiguousarray(prior, np.uint32)
+    sp = (C.c_void_p * max(B, 1))(*[a.ctypes.data for a in bank.sub])
+    pp = (C.c_void_p * max(B, 1))(*[a.ctypes.data for a in bank.proj])
+    gsp = (C.c_void_p * max(B, 1))(*[a.ctypes.data for a in g["sub"]])
+    gpp = (C.c_void_p * max(B, 1))(*[a.ctypes.data for a in g["proj"]])
+    amp = AMPS[cfg["amplification"]]
+    rc = lib().or_embed_sequence_backward_f64(
+        t, len(t), None if pr is None else pr.ctypes.data, 0 if pr is None else len(pr), N, K, cfg["base_vocab"], D, v,
+        amp, sub_vocab_array(cfg), sp, pp, bank.gain.ctypes.data if amp == 2 else None, m.ctypes.data, u.ctypes.data,
+        g["base"].ctypes.data, gsp, gpp, g["gain"].ctypes.data, g["bias"].ctypes.data)
+    if rc:
+        raise (IndexError if rc == -2 else ValueError)(f"or_embed_sequence_backward rc={rc}")
+    return g
 
 
 def bank_checksum(bank: HostBank) -> int:

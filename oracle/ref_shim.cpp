@@ -217,6 +217,34 @@ int ref_bank_set_ln(void* h, const float* gain, const float* bias) {
     return 0;
 }
 
+// embedding.hpp:438-459 embed_sequence_backward<double> on bank_cast<float,double>, grads
+// accumulated from zeros_like (the reference's gradient-check setup, gradcases.hpp:35-36).
+// Outputs in the reference layout: base V0 x D, sub[b] V_b x d, proj[b] D x d, gain, bias.
+int ref_embed_sequence_backward_f64(void* h, const uint32_t* tokens, int64_t len, const uint32_t* prior,
+                                    int64_t prior_len, const double* merged, const double* upstream, double* g_base,
+                                    double* const* g_sub, double* const* g_proj, double* g_gain, double* g_bias) {
+    try {
+        auto& bk = static_cast<ref_bank*>(h)->bank;
+        const auto bd = bank_cast<float, double>(bk);
+        auto g = zeros_like(bd);
+        const std::size_t D = std::size_t(bk.config.dim);
+        embed_sequence_backward<double>(std::span<const token_id>(tokens, std::size_t(len)), bd,
+                                        std::span<const double>(merged, std::size_t(len) * D),
+                                        std::span<const double>(upstream, std::size_t(len) * D), g,
+                                        std::span<const token_id>(prior, std::size_t(prior_len)));
+        std::memcpy(g_base, g.base.data(), g.base.size() * 8);
+        for (std::size_t b = 0; b < g.sub_tables.size(); ++b)
+            std::memcpy(g_sub[b], g.sub_tables[b].data(), g.sub_tables[b].size() * 8);
+        for (std::size_t b = 0; b < g.projections.size(); ++b)
+            std::memcpy(g_proj[b], g.projections[b].data(), g.projections[b].size() * 8);
+        if (g_gain && !g.ln_gain.empty()) std::memcpy(g_gain, g.ln_gain.data(), g.ln_gain.size() * 8);
+        if (g_bias && !g.ln_bias.empty()) std::memcpy(g_bias, g.ln_bias.data(), g.ln_bias.size() * 8);
+        return 0;
+    } catch (...) {
+        return map_exc();
+    }
+}
+
 // embedding.hpp:409-429 embed_sequence_cached<float>: rows (amplified) and merged.
 int ref_embed_sequence_f32(void* h, const uint32_t* tokens, int64_t len, const uint32_t* prior, int64_t prior_len,
                            float* rows, float* merged) {

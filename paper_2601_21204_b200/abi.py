@@ -17,6 +17,7 @@ NGRAM_OK, NGRAM_EINVAL, NGRAM_ERANGE, NGRAM_EIO, NGRAM_EPARSE = 0, 1, 2, 3, 4
 NGRAM_ECONFIG, NGRAM_ENUMERIC, NGRAM_ECUDA, NGRAM_ENCCL, NGRAM_ENOMEM = 5, 6, 7, 8, 9
 NGRAM_F32, NGRAM_BF16 = 0, 1
 NGRAM_BANK_HASH_ONLY = 1
+NGRAM_BWD_SKIP_AMPLIFY = 1
 NGRAM_SHARD_HANDLE_BYTES = 128
 
 # Exported symbols, in header order (tests check the .so exports every one).
@@ -32,6 +33,8 @@ SYMBOLS = [
     "ngram_decode_get_state",
     "ngram_shard_rows", "ngram_shard_group_create", "ngram_shard_group_destroy", "ngram_shard_export", "ngram_shard_open",
     "ngram_shard_local_buffers", "ngram_shard_set_peer", "ngram_shard_scatter_rows", "ngram_shard_project",
+    "ngram_grad_create", "ngram_grad_destroy", "ngram_grad_zero", "ngram_embed_backward", "ngram_grad_tensor",
+    "ngram_grad_download",
 ]
 
 
@@ -138,6 +141,12 @@ def lib() -> C.CDLL:
         "ngram_shard_set_peer": ([vp, i32, vp, vp], i32),
         "ngram_shard_scatter_rows": ([vp, vp, vp, i64, i64, vp, vp, vp], i32),
         "ngram_shard_project": ([vp, vp, i64, vp, vp, i32, vp], i32),
+        "ngram_grad_create": ([vp, C.POINTER(vp)], i32),
+        "ngram_grad_destroy": ([vp], i32),
+        "ngram_grad_zero": ([vp, vp], i32),
+        "ngram_embed_backward": ([vp, vp, vp, i64, i64, vp, vp, vp, i32, vp], i32),
+        "ngram_grad_tensor": ([vp, i32, C.POINTER(vp), C.POINTER(i64)], i32),
+        "ngram_grad_download": ([vp, vp, vp, vp, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

@@ -1,0 +1,192 @@
+// backward.cpp -- C-ABI of the training-side gradient:
+// embed_sequence_backward (embedding.hpp:438-459) over a batch of sequences on the device.
+//
+//   K1        storage rows of every (position, branch) (hash_ids_kernel, validates tokens)
+//   amp_bwd   U = fp32(1/denom) * amplify_backward(merged, upstream); g_E0[tok] += U;
+//             layer_norm: g_gain / g_bias                               (backward.cu)
+//   v2:  X    = gathered sub-table rows (f32)                           (backward.cu)
+//        g_W += U^T X            fp32 GEMM, D x D x T                   (cuBLAS)
+//        dX   = U W_cat          fp32 GEMM, T x D x D                   (cuBLAS)
+//        g_sub[row_b(t)] += dX[t, b]                                    (backward.cu)
+//   v1:  g_sub[row_b(t)] += U[t]                                        (backward.cu)
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "api_util.hpp"
+#include "bank.hpp"
+
+using namespace ngh;
+
+struct ngram_grad {
+    ngram_bank* bank = nullptr;
+    DevBuf<float> e0, sub, w, gain, bias;  // gradients, device layout
+    DevBuf<float> U, X, dX, wf;            // workspaces
+    DevBuf<int32_t> grow;
+    int64_t cap = 0;
+    cublasHandle_t blas = nullptr;
+    ~ngram_grad() {
+        if (blas) cublasDestroy(blas);
+    }
+};
+
+namespace {
+
+void check_blas(cublasStatus_t s, const char* what) {
+    if (s != CUBLAS_STATUS_SUCCESS)
+        throw Error(NGRAM_ECUDA, std::string(what) + " failed (cublas status " + std::to_string(int(s)) + ")");
+}
+
+void zero_all(ngram_grad* g, cudaStream_t st) {
+    for (DevBuf<float>* b : {&g->e0, &g->sub, &g->w, &g->gain, &g->bias})
+        if (b->n) NGH_CUDA(cudaMemsetAsync(b->p, 0, b->n * sizeof(float), st));
+}
+
+}  // namespace
+
+extern "C" {
+
+int ngram_grad_create(ngram_bank* b, ngram_grad** out) {
+    NGRAM_API_BEGIN
+    if (!b || !out) throw Error(NGRAM_EINVAL, "ngram_grad_create: bad argument");
+    if (b->hash_only) throw Error(NGRAM_EINVAL, "bank was created hash-only (NGRAM_BANK_HASH_ONLY)");
+    if (b->shard_count != 1) throw Error(NGRAM_EINVAL, "ngram_grad_create: row-sharded banks are not supported");
+    DeviceGuard dg(b->device);
+    auto g = std::make_unique<ngram_grad>();
+    g->bank = b;
+    const auto& s = b->shape;
+    g->e0.alloc(size_t(b->cfg.base_vocab) * size_t(s.D));
+    g->sub.alloc(size_t(b->local_rows) * size_t(s.d));
+    if (s.variant == 1 && s.B > 0) g->w.alloc(size_t(s.D) * size_t(s.D));
+    if (s.amp == ngk::kAmpLN) {
+        g->gain.alloc(size_t(s.D));
+        g->bias.alloc(size_t(s.D));
+    }
+    check_blas(cublasCreate(&g->blas), "cublasCreate");
+    check_blas(cublasSetMathMode(g->blas, CUBLAS_PEDANTIC_MATH), "cublasSetMathMode");  // true fp32, no TF32
+    zero_all(g.get(), nullptr);
+    NGH_CUDA(cudaDeviceSynchronize());
+    *out = g.release();
+    NGRAM_API_END
+}
+
+int ngram_grad_destroy(ngram_grad* g) {
+    NGRAM_API_BEGIN
+    if (g) {
+        DeviceGuard dg(g->bank->device);
+        delete g;
+    }
+    NGRAM_API_END
+}
+
+int ngram_grad_zero(ngram_grad* g, void* stream) {
+    NGRAM_API_BEGIN
+    if (!g) throw Error(NGRAM_EINVAL, "null gradient bank");
+    DeviceGuard dg(g->bank->device);
+    zero_all(g, static_cast<cudaStream_t>(stream));
+    NGRAM_API_END
+}
+
+int ngram_embed_backward(ngram_grad* g, const uint32_t* tokens, const int64_t* seq_offsets, int64_t nseq,
+                         int64_t T, const uint32_t* prior, const float* merged, const float* upstream, int flags,
+                         void* stream) {
+    NGRAM_API_BEGIN
+    if (!g || nseq < 1 || T < 0 || !seq_offsets || (T > 0 && (!tokens || !upstream)))
+        throw Error(NGRAM_EINVAL, "ngram_embed_backward: bad argument");
+    ngram_bank* b = g->bank;
+    const auto& s = b->shape;
+    const int amp = (flags & NGRAM_BWD_SKIP_AMPLIFY) ? ngk::kAmpNone : s.amp;
+    if (amp == ngk::kAmpLN && T > 0 && !merged)
+        throw Error(NGRAM_EINVAL, "ngram_embed_backward: layer_norm needs the pre-amplification rows (merged)");
+    DeviceGuard dg(b->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    reset_error_word(b, st);
+    if (T == 0) return NGRAM_OK;
+    const int64_t Tpad = round_up(T, kRowPad);
+    const int D = s.D, B = s.B, d = s.d;
+    if (T > g->cap) {
+        g->U.alloc(size_t(Tpad) * size_t(D));
+        if (s.variant == 1 && B > 0) {
+            g->X.alloc(size_t(Tpad) * size_t(D));
+            g->dX.alloc(size_t(Tpad) * size_t(D));
+        }
+        g->grow.alloc(size_t(std::max(B, 1)) * size_t(Tpad));
+        g->cap = Tpad;
+    }
+    // K1: storage rows (and token validation: a bad token leaves every gradient untouched)
+    ngk::launch_hash_ids(s, b->ht.p, tokens, seq_offsets, nseq, T, prior, nullptr, 0, g->grow.p, g->cap, b->err.p, st);
+    ngk::launch_amp_backward(s, upstream, merged, tokens, T, amp, b->ln_gain.p, g->U.p, g->e0.p, g->gain.p,
+                             g->bias.p, b->err.p, st);
+    if (B > 0 && s.variant == 1) {
+        ngk::launch_gather_rows_f32(s, g->grow.p, g->cap, T, b->sub.p, g->X.p, b->err.p, st);
+        // fp32 W_cat (re-widened every call: the bank may have been re-uploaded)
+        g->wf.ensure(size_t(D) * size_t(D));
+        ngk::launch_bf16_to_f32(b->wcat.p, g->wf.p, int64_t(D) * D, st);
+        check_blas(cublasSetStream(g->blas, st), "cublasSetStream");
+        const float one = 1.0f, zero = 0.0f;
+        // row-major M (r x c) is column-major M^T with ld = c.
+        // g_W (D x D, row-major [i][k]) += U^T X  <=>  col-major g_W^T = X_cm * U_cm^T
+        check_blas(cublasSgemm(g->blas, CUBLAS_OP_N, CUBLAS_OP_T, D, D, int(T), &one, g->X.p, D, g->U.p, D, &one,
+                               g->w.p, D),
+                   "cublasSgemm(dW)");
+        // dX (T x D) = U W_cat  <=>  col-major dX^T = W_cm * U_cm
+        check_blas(cublasSgemm(g->blas, CUBLAS_OP_N, CUBLAS_OP_N, D, int(T), D, &one, g->wf.p, D, g->U.p, D, &zero,
+                               g->dX.p, D),
+                   "cublasSgemm(dX)");
+        ngk::launch_scatter_rows(s, g->grow.p, g->cap, T, d, D, d, g->dX.p, g->sub.p, b->err.p, st);
+    } else if (B > 0) {  // averaged_v1: every branch row receives u (rows are D wide)
+        ngk::launch_scatter_rows(s, g->grow.p, g->cap, T, D, D, 0, g->U.p, g->sub.p, b->err.p, st);
+    }
+    NGH_CUDA(cudaGetLastError());
+    NGRAM_API_END
+}
+
+int ngram_grad_tensor(ngram_grad* g, int which, float** dev_ptr, int64_t* numel) {
+    NGRAM_API_BEGIN
+    if (!g || !dev_ptr || !numel) throw Error(NGRAM_EINVAL, "ngram_grad_tensor: bad argument");
+    DevBuf<float>* t = nullptr;
+    switch (which) {
+        case 0: t = &g->e0; break;
+        case 1: t = &g->sub; break;
+        case 2: t = &g->w; break;
+        case 3: t = &g->gain; break;
+        case 4: t = &g->bias; break;
+        default: throw Error(NGRAM_EINVAL, "ngram_grad_tensor: which must be 0..4");
+    }
+    *dev_ptr = t->p;
+    *numel = int64_t(t->n);
+    NGRAM_API_END
+}
+
+int ngram_grad_download(ngram_grad* g, float* base, float* const* sub, float* const* proj, float* gain, float* bias) {
+    NGRAM_API_BEGIN
+    if (!g) throw Error(NGRAM_EINVAL, "null gradient bank");
+    ngram_bank* b = g->bank;
+    DeviceGuard dg(b->device);
+    NGH_CUDA(cudaDeviceSynchronize());
+    const auto& s = b->shape;
+    if (base) NGH_CUDA(cudaMemcpy(base, g->e0.p, g->e0.n * sizeof(float), cudaMemcpyDeviceToHost));
+    if (sub)
+        for (int i = 0; i < s.B; ++i)
+            if (sub[i])
+                NGH_CUDA(cudaMemcpy(sub[i], g->sub.p + size_t(b->row_base[size_t(i)]) * size_t(s.d),
+                                    size_t(b->row_hi[size_t(i)] - b->row_lo[size_t(i)]) * size_t(s.d) * sizeof(float),
+                                    cudaMemcpyDeviceToHost));
+    if (proj && g->w.n) {  // W_cat[i][b*d + j] -> proj_b[i*d + j]
+        const size_t D = size_t(s.D), d = size_t(s.d);
+        for (int i = 0; i < s.B; ++i)
+            if (proj[i])
+                NGH_CUDA(cudaMemcpy2D(proj[i], d * sizeof(float), g->w.p + size_t(i) * d, D * sizeof(float),
+                                      d * sizeof(float), D, cudaMemcpyDeviceToHost));
+    }
+    if (gain && g->gain.n) NGH_CUDA(cudaMemcpy(gain, g->gain.p, g->gain.n * sizeof(float), cudaMemcpyDeviceToHost));
+    if (bias && g->bias.n) NGH_CUDA(cudaMemcpy(bias, g->bias.p, g->bias.n * sizeof(float), cudaMemcpyDeviceToHost));
+    NGRAM_API_END
+}
+
+}  // extern "C"

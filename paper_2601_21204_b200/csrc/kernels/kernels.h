@@ -70,6 +70,17 @@ void launch_pack_wcat(const float* proj_b, __nv_bfloat16* wcat, int D, int d, in
 void launch_fill_f32(float* dst, float v, int64_t n, cudaStream_t st);
 
 // ---- forward
+// ---- backward (backward.cu): embed_sequence_backward's scatter / elementwise parts
+void launch_amp_backward(const Shape& s, const float* up, const float* pre, const uint32_t* tokens, int64_t T,
+                         int amp, const float* gain, float* U, float* g_e0, float* g_gain, float* g_bias,
+                         const unsigned long long* err, cudaStream_t st);
+void launch_gather_rows_f32(const Shape& s, const int32_t* grow, int64_t Tpad, int64_t T, const __nv_bfloat16* sub,
+                            float* X, const unsigned long long* err, cudaStream_t st);
+void launch_scatter_rows(const Shape& s, const int32_t* grow, int64_t Tpad, int64_t T, int width, int src_stride,
+                         int src_branch_step, const float* src, float* g_sub, const unsigned long long* err,
+                         cudaStream_t st);
+void launch_bf16_to_f32(const __nv_bfloat16* src, float* dst, int64_t n, cudaStream_t st);
+
 struct FwdArgs {
     Shape s;
     const HashTables* ht;

@@ -401,6 +401,70 @@ def draft_verify(state: SequenceCache, bank: DeviceBank, draft: Sequence[int], a
     return [res[i] for i in range(accept_count)]
 
 
+# ----------------------------------------------------------------------------- backward
+class GradBank:
+    """fp32 gradient accumulator of a DeviceBank (embedding_bank_t<T>& grads of
+    embed_sequence_backward, embedding.hpp:438-459), zero-initialised, device layout."""
+
+    def __init__(self, bank: DeviceBank):
+        self.bank = bank
+        h = C.c_void_p()
+        check(abi.lib().ngram_grad_create(bank.handle, C.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            abi.lib().ngram_grad_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def zero(self, stream=None) -> "GradBank":
+        check(abi.lib().ngram_grad_zero(self.handle, _stream(stream)))
+        return self
+
+    def backward(self, tokens: torch.Tensor, seq_offsets: torch.Tensor, upstream: torch.Tensor,
+                 merged: Optional[torch.Tensor] = None, prior: Optional[torch.Tensor] = None,
+                 skip_amplify: bool = False, stream=None) -> None:
+        """embed_sequence_backward on device tensors: upstream = dL/d(rows) f32 [T, D],
+        merged = the forward's pre-amplification rows (layer_norm only)."""
+        T = tokens.numel()
+        flags = abi.NGRAM_BWD_SKIP_AMPLIFY if skip_amplify else 0
+        check(abi.lib().ngram_embed_backward(self.handle, _ptr(tokens), _ptr(seq_offsets), seq_offsets.numel() - 1, T,
+                                             _ptr(prior), _ptr(merged), _ptr(upstream), flags, _stream(stream)))
+
+    def tensor(self, which: int) -> tuple:
+        """(device pointer, numel) of 0 E0, 1 sub-tables, 2 W_cat, 3 ln_gain, 4 ln_bias."""
+        p, n = C.c_void_p(), C.c_int64()
+        check(abi.lib().ngram_grad_tensor(self.handle, which, C.byref(p), C.byref(n)))
+        return p.value, n.value
+
+    def download(self) -> dict:
+        """Host copy in the reference layout: base, sub[b], proj[b] (v2), gain, bias (LN)."""
+        cfg = self.bank.cfg
+        D, B = self.bank.D, self.bank.B
+        V0 = cfg["base_vocab"]
+        v2 = cfg["variant"] == "subtable_v2"
+        d = D // B if (v2 and B) else D
+        sv = [0] * B  # branch b = (n-2)K + (k-1) (config.hpp:41-44)
+        for e in cfg.get("sub_vocab", []):
+            sv[(e["n"] - 2) * cfg["sub_tables"] + e["k"] - 1] = int(e["vocab"])
+        out = {"base": np.zeros((V0, D), np.float32), "sub": [np.zeros((v, d), np.float32) for v in sv],
+               "proj": [np.zeros((D, d), np.float32) for _ in range(B)] if v2 else [],
+               "gain": np.zeros(D, np.float32), "bias": np.zeros(D, np.float32)}
+        sp = (C.c_void_p * max(B, 1))(*[a.ctypes.data for a in out["sub"]])
+        pp = (C.c_void_p * max(B, 1))(*[a.ctypes.data for a in out["proj"]])
+        ln = cfg["amplification"] == "layer_norm"
+        check(abi.lib().ngram_grad_download(self.handle, out["base"].ctypes.data, sp if B else None,
+                                            pp if (v2 and B) else None, out["gain"].ctypes.data if ln else None,
+                                            out["bias"].ctypes.data if ln else None))
+        return out
+
+
 # ----------------------------------------------------------------------------- row shards
 class ShardGroup:
     """Row-sharded exchange of one rank: double-buffered home X, peer buffers

@@ -203,7 +203,69 @@ def main():
         R.ref_cache_destroy(ch)
     save("draft_verify.npz", config=json.dumps(cfgD), seed=99, ncases=6, **cases)
     R.ref_bank_destroy(hb)
+    backward_goldens()
+
+
+def backward_goldens():
+    # 9. backward: embed_sequence_backward<double> (embedding.hpp:438-459), two sequences
+    #    (the second with a carried prior), gradients summed over the two calls.  Sparse
+    #    storage of the touched E0 / sub-table rows; projections and LN dense.
+    for name, cfg, seed in [("tc_none", dict(ref_default_config(1000, 256, 3, 2), amplification="none"), 1234),
+                            ("tc_scale_sqrt_d", ref_default_config(1000, 256, 3, 2), 1234),
+                            ("tc_layer_norm", dict(ref_default_config(1000, 256, 3, 2), amplification="layer_norm"),
+                             1234),
+                            ("simt_v2", v2_config(16, 12, 4, 2, "scale_sqrt_d"), 7),
+                            ("v1_wide", O.make_config(500, 512, 4, 1, [3001, 3011, 3019], "averaged_v1",
+                                                      "layer_norm"), 19)]:
+        hb = ref_bank(cfg, seed)
+        D = cfg["dim"]
+        extra = {}
+        if cfg["amplification"] == "layer_norm":
+            g = np.random.default_rng(6)
+            gain = (1.0 + 0.1 * g.standard_normal(D)).astype(np.float32)
+            bias = (0.05 * g.standard_normal(D)).astype(np.float32)
+            O.lib().or_round_bf16(gain, gain.size)
+            O.lib().or_round_bf16(bias, bias.size)
+            R.ref_bank_set_ln(hb, gain, bias)
+            extra = {"ln_gain": gain, "ln_bias": bias}
+        toks = O.uniform_tokens(31, cfg["base_vocab"], 120)
+        prior = O.uniform_tokens(32, cfg["base_vocab"], cfg["max_order"] - 1)
+        seqs, priors = [toks[:40], toks[40:]], [np.zeros(0, np.uint32), prior]
+        _, _, _, m64 = ref_embed(hb, seqs, priors, D=D)
+        up = np.random.default_rng(9).standard_normal((len(toks), D)).astype(np.float32).astype(np.float64)
+        acc = O.zero_grads(cfg)
+        for (a, b), pr in zip([(0, 40), (40, 120)], priors):
+            gr = O.zero_grads(cfg)
+            sp = (C.c_void_p * max(len(gr["sub"]), 1))(*[x.ctypes.data for x in gr["sub"]])
+            pp = (C.c_void_p * max(len(gr["proj"]), 1))(*[x.ctypes.data for x in gr["proj"]])
+            mm = np.ascontiguousarray(m64[a:b])
+            uu = np.ascontiguousarray(up[a:b])
+            assert R.ref_embed_sequence_backward_f64(hb, toks[a:b], b - a, pr.ctypes.data if len(pr) else None, len(pr),
+                                                     mm.ctypes.data, uu.ctypes.data, gr["base"].ctypes.data, sp, pp,
+                                                     gr["gain"].ctypes.data, gr["bias"].ctypes.data) == 0
+            for k in ("base", "gain", "bias"):
+                acc[k] += gr[k]
+            for k in ("sub", "proj"):
+                for x, y in zip(acc[k], gr[k]):
+                    x += y
+        out = {}
+        nz = np.nonzero(np.any(acc["base"] != 0, axis=1))[0]
+        out["g_base_idx"], out["g_base_val"] = nz, acc["base"][nz]
+        for b, x in enumerate(acc["sub"]):
+            nz = np.nonzero(np.any(x != 0, axis=1))[0]
+            out[f"g_sub{b}_idx"], out[f"g_sub{b}_val"] = nz, x[nz]
+        if acc["proj"]:
+            out["g_proj"] = np.stack(acc["proj"])
+        if cfg["amplification"] == "layer_norm":
+            out["g_gain"], out["g_bias"] = acc["gain"], acc["bias"]
+        save(f"backward_{name}.npz", config=json.dumps(cfg), seed=seed, tokens=toks, seq_offsets=np.array([0, 40, 120]),
+             prior1=prior, merged_f64=m64, upstream=up, bank_checksum=np.uint64(bank_checksum_ref(hb, cfg)),
+             **extra, **out)
+        R.ref_bank_destroy(hb)
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["backward"]:  # regenerate only section 9
+        backward_goldens()
+    else:
+        main()

@@ -64,3 +64,49 @@ def dev_i64(torch, a, device):
 def u64(t):
     """int64 device/host tensor holding u64 bits -> numpy uint64."""
     return t.cpu().numpy().view(np.uint64) if hasattr(t, "cpu") else np.asarray(t).view(np.uint64)
+
+
+# ---------------------------------------------------------------- backward (gradients)
+# Device backward: fp32 atomics + fp32 GEMMs vs the reference's double path.  Per gradient
+# tensor: ||err||_2 <= GRAD_REL_L2 * ||ref||_2 and max |err| <= GRAD_MAX_RTOL * max |ref|.
+GRAD_REL_L2 = 1e-5
+GRAD_MAX_RTOL = 1e-5
+BACKWARD = ["backward_tc_none.npz", "backward_tc_scale_sqrt_d.npz", "backward_tc_layer_norm.npz",
+            "backward_simt_v2.npz", "backward_v1_wide.npz"]
+
+
+def golden_grads(g, zero):
+    """Dense gradients (reference layout) from a backward fixture's sparse storage."""
+    out = {k: ([x.copy() for x in v] if isinstance(v, list) else v.copy()) for k, v in zero.items()}
+    out["base"][g["g_base_idx"]] = g["g_base_val"]
+    for b in range(len(out["sub"])):
+        out["sub"][b][g[f"g_sub{b}_idx"]] = g[f"g_sub{b}_val"]
+    if "g_proj" in g.files:
+        for b in range(len(out["proj"])):
+            out["proj"][b][:] = g["g_proj"][b]
+    if "g_gain" in g.files:
+        out["gain"][:], out["bias"][:] = g["g_gain"], g["g_bias"]
+    return out
+
+
+def grad_items(gr, ln):
+    yield "base", gr["base"]
+    for b, x in enumerate(gr["sub"]):
+        yield f"sub{b}", x
+    for b, x in enumerate(gr["proj"]):
+        yield f"proj{b}", x
+    if ln:
+        yield "gain", gr["gain"]
+        yield "bias", gr["bias"]
+
+
+def assert_grads_close(got, ref, ln, rel_l2=GRAD_REL_L2, max_rtol=GRAD_MAX_RTOL):
+    for (name, a), (_, b) in zip(grad_items(got, ln), grad_items(ref, ln)):
+        a = np.asarray(a, np.float64)
+        b = np.asarray(b, np.float64)
+        assert a.shape == b.shape, name
+        err = np.abs(a - b)
+        scale = np.abs(b).max() + 1e-30
+        assert err.max() <= max_rtol * scale, f"{name}: max err {err.max() / scale:.3e} of max|ref|"
+        rel = np.linalg.norm(a - b) / (np.linalg.norm(b) + 1e-30)
+        assert rel <= rel_l2, f"{name}: relL2 {rel:.3e}"

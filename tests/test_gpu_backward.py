@@ -1,0 +1,98 @@
+"""Device backward (embed_sequence_backward, embedding.hpp:291-459) vs
+the reference's double path: the golden fixtures (tests/golden/backward_*.npz, produced by the
+reference itself) and the pinned oracle.  fp32 atomics + fp32 GEMMs: per-tensor relL2 and
+max-error bounds in tests/helpers.py (GRAD_REL_L2, GRAD_MAX_RTOL)."""
+import json
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from helpers import BACKWARD, assert_grads_close, dev_i64, dev_u32, gold, golden_grads
+from paper_2601_21204_b200 import ngram as G
+from paper_2601_21204_b200.abi import OutOfRange
+
+pytestmark = pytest.mark.gpu
+
+
+def _setup(name, cuda):
+    g = gold(name)
+    cfg = json.loads(str(g["config"]))
+    hb = O.make_bank(cfg, int(g["seed"]), round_bf16=True)
+    ln = cfg["amplification"] == "layer_norm"
+    if ln:
+        hb.gain[:], hb.bias[:] = g["ln_gain"], g["ln_bias"]
+    db = G.DeviceBank(cfg).upload(hb.base, hb.sub, hb.proj, hb.gain if ln else None, hb.bias if ln else None)
+    prior = np.zeros((2, cfg["max_order"] - 1), np.uint32)
+    prior[1] = g["prior1"]
+    args = dict(tokens=dev_u32(torch, g["tokens"], cuda), seq_offsets=dev_i64(torch, g["seq_offsets"], cuda),
+                upstream=torch.from_numpy(g["upstream"].astype(np.float32)).to(cuda),
+                merged=torch.from_numpy(g["merged_f64"].astype(np.float32)).to(cuda),
+                prior=dev_u32(torch, prior, cuda) if cfg["max_order"] > 1 else None)
+    return g, cfg, hb, db, args, ln
+
+
+@pytest.mark.parametrize("name", BACKWARD)
+def test_backward_matches_reference(cuda, name):
+    g, cfg, hb, db, args, ln = _setup(name, cuda)
+    gb = G.GradBank(db)
+    gb.backward(**args)
+    db.sync_errors()
+    assert_grads_close(gb.download(), golden_grads(g, O.zero_grads(cfg)), ln)
+
+
+def test_backward_accumulates_and_zeroes(cuda):
+    g, cfg, hb, db, args, ln = _setup("backward_tc_scale_sqrt_d.npz", cuda)
+    gb = G.GradBank(db)
+    gb.backward(**args)
+    gb.backward(**args)
+    db.sync_errors()
+    ref = golden_grads(g, O.zero_grads(cfg))
+    twice = {k: ([2 * x for x in v] if isinstance(v, list) else 2 * v) for k, v in ref.items()}
+    assert_grads_close(gb.download(), twice, ln)
+    gb.zero()
+    torch.cuda.synchronize()
+    got = gb.download()
+    assert not got["base"].any() and not any(x.any() for x in got["sub"]) and not any(x.any() for x in got["proj"])
+
+
+def test_skip_amplify_takes_d_merged(cuda):  # embed_backward alone (embedding.hpp:338-376)
+    g, cfg, hb, db, args, ln = _setup("backward_tc_scale_sqrt_d.npz", cuda)
+    a = G.GradBank(db)
+    a.backward(**args)
+    b = G.GradBank(db)
+    d_pre = args["upstream"] * np.float32(np.sqrt(np.float64(db.D)))  # amplify_backward of scale_sqrt_d
+    b.backward(**dict(args, upstream=d_pre), skip_amplify=True)
+    db.sync_errors()
+    assert_grads_close(b.download(), a.download(), ln)
+
+
+def test_out_of_range_token_leaves_gradients_untouched(cuda):  # hashing.cpp:49-54
+    g, cfg, hb, db, args, ln = _setup("backward_tc_none.npz", cuda)
+    gb = G.GradBank(db)
+    bad = args["tokens"].clone()
+    bad[77] = cfg["base_vocab"]
+    gb.backward(**dict(args, tokens=bad))
+    with pytest.raises(OutOfRange):
+        db.sync_errors()
+    got = gb.download()
+    assert not got["base"].any() and not any(x.any() for x in got["sub"])
+
+
+def test_forward_then_backward_at_longcat_width(cuda):
+    """D = 3072, N = 4, K = 4 (12 branches, d = 256): merged from the device forward, then the
+    device backward vs the oracle's double backward on the same inputs."""
+    cfg = O.make_default_config(1000, 3072, 4, 4)
+    hb = O.make_bank(cfg, 5, round_bf16=True)
+    db = G.DeviceBank(cfg).upload(hb.base, hb.sub, hb.proj)
+    toks = O.uniform_tokens(51, 1000, 48)
+    t, off = dev_u32(torch, toks, cuda), dev_i64(torch, [0, 48], cuda)
+    _, merged = G.embed_forward(db, t, off, rows=False, merged=True)
+    up = torch.from_numpy(np.random.default_rng(4).standard_normal((48, 3072)).astype(np.float32)).to(cuda)
+    gb = G.GradBank(db)
+    gb.backward(t, off, up, merged=merged)
+    db.sync_errors()
+    ref = O.embed_sequence_backward(hb, toks, merged.cpu().numpy().astype(np.float64),
+                                    up.cpu().numpy().astype(np.float64))
+    assert_grads_close(gb.download(), ref, False)

@@ -17,6 +17,7 @@ import oracle as O
 GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
+import helpers  # noqa: E402
 from helpers import gold  # noqa: E402
 
 
@@ -223,3 +224,27 @@ def test_synthetic_generator_statistics():
     assert abs(v.mean()) < 2e-4 and abs(v.std() - 0.02) < 5e-4
     w = O.synth_rows(1234, 105, 0, 64, 256, 0.02 / 16)
     assert abs(w.std() - 0.02 / 16) < 1e-4
+
+
+@pytest.mark.parametrize("name", helpers.BACKWARD)
+def test_backward_restatement_matches_reference(name):  # embedding.hpp:291-459 in double
+    g = gold(name)
+    cfg = json.loads(str(g["config"]))
+    bank = O.make_bank(cfg, int(g["seed"]), round_bf16=True)
+    assert O.bank_checksum(bank) == int(g["bank_checksum"]) or "ln_gain" in g.files
+    if "ln_gain" in g.files:
+        bank.gain[:], bank.bias[:] = g["ln_gain"], g["ln_bias"]
+    off = g["seq_offsets"]
+    acc = O.zero_grads(cfg)
+    for s, prior in enumerate([None, g["prior1"]]):
+        a, b = int(off[s]), int(off[s + 1])
+        part = O.embed_sequence_backward(bank, g["tokens"][a:b], g["merged_f64"][a:b], g["upstream"][a:b], prior)
+        for k in ("base", "gain", "bias"):
+            acc[k] += part[k]
+        for k in ("sub", "proj"):
+            for x, y in zip(acc[k], part[k]):
+                x += y
+    ref = helpers.golden_grads(g, O.zero_grads(cfg))
+    ln = cfg["amplification"] == "layer_norm"
+    for (n, a), (_, b) in zip(helpers.grad_items(acc, ln), helpers.grad_items(ref, ln)):
+        assert np.array_equal(a, b), n  # same double operation order as the reference
