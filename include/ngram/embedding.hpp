@@ -157,4 +157,32 @@ std::vector<float> embed_sequence(std::span<const token_id> tokens, const embedd
 // Batched extension: many sequences in one launch (rows concatenated, len_total x D).
 std::vector<float> embed_batch(const std::vector<std::vector<token_id>>& sequences, const device_bank& bank);
 
+// zeros_like (embedding.hpp:123-134): a zero bank of the same shape (the gradient store).
+template <typename T>
+embedding_bank_t<T> zeros_like(const embedding_bank_t<T>& bank) {
+    embedding_bank_t<T> z;
+    z.config = bank.config;
+    z.base.assign(bank.base.size(), T(0));
+    for (const auto& t : bank.sub_tables) z.sub_tables.emplace_back(t.size(), T(0));
+    for (const auto& p : bank.projections) z.projections.emplace_back(p.size(), T(0));
+    z.ln_gain.assign(bank.ln_gain.size(), T(0));
+    z.ln_bias.assign(bank.ln_bias.size(), T(0));
+    return z;
+}
+
+// Backward (embedding.hpp:338-459), computed on the device (ngram_embed_backward_host:
+// fp32 atomics + fp32 GEMMs) and ACCUMULATED into the host gradient bank `grads`.
+// embed_backward: `upstream` is d(merged) of one window (no amplification step).
+void embed_backward(std::span<const token_id> context, const device_bank& bank, std::span<const float> upstream,
+                    embedding_bank& grads);
+void embed_backward(std::span<const token_id> context, const embedding_bank& bank, std::span<const float> upstream,
+                    embedding_bank& grads);
+// embed_sequence_backward: `merged` = embed_sequence_cached(...).merged, `upstream` = dL/d(rows).
+void embed_sequence_backward(std::span<const token_id> tokens, const device_bank& bank, std::span<const float> merged,
+                             std::span<const float> upstream, embedding_bank& grads,
+                             std::span<const token_id> prior_context = {});
+void embed_sequence_backward(std::span<const token_id> tokens, const embedding_bank& bank,
+                             std::span<const float> merged, std::span<const float> upstream, embedding_bank& grads,
+                             std::span<const token_id> prior_context = {});
+
 }  // namespace ngram

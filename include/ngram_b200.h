@@ -248,6 +248,10 @@ int ngram_grad_zero(ngram_grad* g, void* stream);
 int ngram_embed_backward(ngram_grad* g, const uint32_t* tokens, const int64_t* seq_offsets, int64_t nseq,
                          int64_t total_tokens, const uint32_t* prior, const float* merged, const float* upstream,
                          int flags, void* stream);
+/* Same with HOST buffers (tokens, seq_offsets, prior, merged, upstream); synchronous; an
+ * out-of-range token returns NGRAM_ERANGE and leaves the gradients untouched. */
+int ngram_embed_backward_host(ngram_grad* g, const uint32_t* tokens, const int64_t* seq_offsets, int64_t nseq,
+                              const uint32_t* prior, const float* merged, const float* upstream, int flags);
 /* Device view of one gradient tensor: which 0 = E0, 1 = sub-tables (device row layout),
  * 2 = W_cat, 3 = ln_gain, 4 = ln_bias. */
 int ngram_grad_tensor(ngram_grad* g, int which, float** dev_ptr, int64_t* numel);

@@ -34,7 +34,7 @@ SYMBOLS = [
     "ngram_shard_rows", "ngram_shard_group_create", "ngram_shard_group_destroy", "ngram_shard_export", "ngram_shard_open",
     "ngram_shard_local_buffers", "ngram_shard_set_peer", "ngram_shard_scatter_rows", "ngram_shard_project",
     "ngram_grad_create", "ngram_grad_destroy", "ngram_grad_zero", "ngram_embed_backward", "ngram_grad_tensor",
-    "ngram_grad_download",
+    "ngram_grad_download", "ngram_embed_backward_host",
 ]
 
 
@@ -147,6 +147,7 @@ def lib() -> C.CDLL:
         "ngram_embed_backward": ([vp, vp, vp, i64, i64, vp, vp, vp, i32, vp], i32),
         "ngram_grad_tensor": ([vp, i32, C.POINTER(vp), C.POINTER(i64)], i32),
         "ngram_grad_download": ([vp, vp, vp, vp, vp, vp], i32),
+        "ngram_embed_backward_host": ([vp, vp, vp, i64, vp, vp, vp, i32], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

@@ -258,6 +258,72 @@ std::vector<float> embed_sequence(std::span<const token_id> tokens, const embedd
     return embed_sequence_cached(tokens, device_bank(bank), prior_context).rows;
 }
 
+namespace {
+// Run one device backward into a fresh fp32 gradient bank and add it into the host grads.
+void backward_into(const device_bank& bank, std::span<const token_id> tokens, std::span<const token_id> prior,
+                   const float* merged, const float* upstream, int flags, embedding_bank& grads) {
+    const auto& cfg = bank.config();
+    if (grads.base.size() != std::size_t(cfg.base_vocab) * std::size_t(cfg.dim) ||
+        grads.sub_tables.size() != std::size_t(cfg.branch_count()))
+        throw std::invalid_argument("embed_backward: gradient bank shape does not match the bank");
+    ngram_grad* g = nullptr;
+    throw_status(ngram_grad_create(bank.handle(), &g));
+    std::unique_ptr<ngram_grad, int (*)(ngram_grad*)> guard(g, ngram_grad_destroy);
+    const auto pr = prior_tail(prior, cfg.max_order - 1);
+    const int64_t off[2] = {0, int64_t(tokens.size())};
+    throw_status(ngram_embed_backward_host(g, tokens.data(), off, 1, pr.empty() ? nullptr : pr.data(), merged, upstream,
+                                           flags));
+    embedding_bank d = zeros_like(grads);
+    std::vector<float*> sp, pp;
+    for (auto& t : d.sub_tables) sp.push_back(t.data());
+    for (auto& p : d.projections) pp.push_back(p.data());
+    throw_status(ngram_grad_download(g, d.base.data(), sp.empty() ? nullptr : sp.data(),
+                                     pp.empty() ? nullptr : pp.data(), d.ln_gain.empty() ? nullptr : d.ln_gain.data(),
+                                     d.ln_bias.empty() ? nullptr : d.ln_bias.data()));
+    auto add = [](std::vector<float>& a, const std::vector<float>& b) {
+        for (std::size_t i = 0; i < a.size() && i < b.size(); ++i) a[i] += b[i];
+    };
+    add(grads.base, d.base);
+    for (std::size_t b = 0; b < grads.sub_tables.size(); ++b) add(grads.sub_tables[b], d.sub_tables[b]);
+    for (std::size_t b = 0; b < grads.projections.size() && b < d.projections.size(); ++b)
+        add(grads.projections[b], d.projections[b]);
+    add(grads.ln_gain, d.ln_gain);
+    add(grads.ln_bias, d.ln_bias);
+}
+}  // namespace
+
+void embed_backward(std::span<const token_id> context, const device_bank& bank, std::span<const float> upstream,
+                    embedding_bank& grads) {
+    const auto& cfg = bank.config();
+    if (upstream.size() != std::size_t(cfg.dim)) throw std::invalid_argument("embed_backward: upstream size mismatch");
+    if (context.size() != std::size_t(cfg.max_order))
+        throw std::invalid_argument("hash_all_orders: context length " + std::to_string(context.size()) +
+                                    " does not match max order " + std::to_string(cfg.max_order));
+    backward_into(bank, context.last(1), context.first(context.size() - 1), nullptr, upstream.data(),
+                  NGRAM_BWD_SKIP_AMPLIFY, grads);
+}
+
+void embed_backward(std::span<const token_id> context, const embedding_bank& bank, std::span<const float> upstream,
+                    embedding_bank& grads) {
+    embed_backward(context, device_bank(bank), upstream, grads);
+}
+
+void embed_sequence_backward(std::span<const token_id> tokens, const device_bank& bank, std::span<const float> merged,
+                             std::span<const float> upstream, embedding_bank& grads,
+                             std::span<const token_id> prior_context) {
+    const std::size_t n = tokens.size() * std::size_t(bank.config().dim);
+    if (upstream.size() != n || merged.size() != n)
+        throw std::invalid_argument("embed_sequence_backward: merged / upstream size mismatch");
+    if (tokens.empty()) return;
+    backward_into(bank, tokens, prior_context, merged.data(), upstream.data(), 0, grads);
+}
+
+void embed_sequence_backward(std::span<const token_id> tokens, const embedding_bank& bank,
+                             std::span<const float> merged, std::span<const float> upstream, embedding_bank& grads,
+                             std::span<const token_id> prior_context) {
+    embed_sequence_backward(tokens, device_bank(bank), merged, upstream, grads, prior_context);
+}
+
 void embed_window(std::span<const token_id> context, const device_bank& bank, std::span<float> out,
                   embed_counters* counters) {
     const auto& cfg = bank.config();

@@ -29,6 +29,9 @@ struct ngram_grad {
     DevBuf<float> U, X, dX, wf;            // workspaces
     DevBuf<int32_t> grow;
     int64_t cap = 0;
+    DevBuf<uint32_t> h_tokens, h_prior;  // host-buffer entry staging
+    DevBuf<int64_t> h_off;
+    DevBuf<float> h_merged, h_up;
     cublasHandle_t blas = nullptr;
     ~ngram_grad() {
         if (blas) cublasDestroy(blas);
@@ -143,6 +146,44 @@ int ngram_embed_backward(ngram_grad* g, const uint32_t* tokens, const int64_t* s
         ngk::launch_scatter_rows(s, g->grow.p, g->cap, T, D, D, 0, g->U.p, g->sub.p, b->err.p, st);
     }
     NGH_CUDA(cudaGetLastError());
+    NGRAM_API_END
+}
+
+int ngram_embed_backward_host(ngram_grad* g, const uint32_t* tokens, const int64_t* seq_offsets, int64_t nseq,
+                              const uint32_t* prior, const float* merged, const float* upstream, int flags) {
+    NGRAM_API_BEGIN
+    if (!g || nseq < 1 || !seq_offsets) throw Error(NGRAM_EINVAL, "ngram_embed_backward_host: bad argument");
+    ngram_bank* b = g->bank;
+    const int64_t T = seq_offsets[nseq];
+    if (seq_offsets[0] != 0 || T < 0) throw Error(NGRAM_EINVAL, "seq_offsets must start at 0");
+    for (int64_t i = 0; i < nseq; ++i)
+        if (seq_offsets[i + 1] < seq_offsets[i]) throw Error(NGRAM_EINVAL, "seq_offsets must be non-decreasing");
+    if (T > 0 && (!tokens || !upstream)) throw Error(NGRAM_EINVAL, "ngram_embed_backward_host: bad argument");
+    DeviceGuard dg(b->device);
+    const size_t D = size_t(b->cfg.dim);
+    const int N1 = std::max(b->cfg.max_order - 1, 0);
+    g->h_tokens.ensure(size_t(std::max<int64_t>(T, 1)));
+    g->h_off.ensure(size_t(nseq + 1));
+    g->h_up.ensure(std::max<size_t>(size_t(T) * D, 1));
+    if (merged) g->h_merged.ensure(std::max<size_t>(size_t(T) * D, 1));
+    if (prior && N1 > 0) g->h_prior.ensure(size_t(nseq) * size_t(N1));
+    if (T > 0) {
+        NGH_CUDA(cudaMemcpy(g->h_tokens.p, tokens, size_t(T) * 4, cudaMemcpyHostToDevice));
+        NGH_CUDA(cudaMemcpy(g->h_up.p, upstream, size_t(T) * D * 4, cudaMemcpyHostToDevice));
+        if (merged) NGH_CUDA(cudaMemcpy(g->h_merged.p, merged, size_t(T) * D * 4, cudaMemcpyHostToDevice));
+    }
+    NGH_CUDA(cudaMemcpy(g->h_off.p, seq_offsets, size_t(nseq + 1) * 8, cudaMemcpyHostToDevice));
+    if (prior && N1 > 0)
+        NGH_CUDA(cudaMemcpy(g->h_prior.p, prior, size_t(nseq) * size_t(N1) * 4, cudaMemcpyHostToDevice));
+    const int rc = ngram_embed_backward(g, g->h_tokens.p, g->h_off.p, nseq, T, (prior && N1 > 0) ? g->h_prior.p : nullptr,
+                                        merged ? g->h_merged.p : nullptr, g->h_up.p, flags, nullptr);
+    if (rc != NGRAM_OK) return rc;
+    unsigned long long e = 0;
+    NGH_CUDA(cudaMemcpy(&e, b->err.p, sizeof(e), cudaMemcpyDeviceToHost));
+    if (e != ~0ull)
+        throw Error(NGRAM_ERANGE, "embedding: token out of range for base vocabulary " +
+                                      std::to_string(b->cfg.base_vocab) + " (first bad window at position " +
+                                      std::to_string(e) + ")");
     NGRAM_API_END
 }
 

@@ -250,6 +250,43 @@ int main() {
         const auto c2 = v2_config(128, 24, 4, 2, amp_mode::layer_norm);
         CHECK(ngram_config_from_json(to_json_string(c2)) == c2);
     });
+    test_case("backward: sequence backward == sum of per-window embed_backward, accumulates", [] {
+        auto cfg = make_default_config(500, 256, 3, 2);
+        cfg.amplification = amp_mode::none;  // embed_backward takes d(merged) directly
+        const auto host = make_bank<float>(cfg, 11);
+        const device_bank bank(host);
+        rng64 rng(21);
+        std::vector<token_id> seq(40);
+        for (auto& t : seq) t = token_id(uniform_below(rng, 500));
+        std::vector<float> up(seq.size() * 256);
+        for (auto& u : up) u = float(gaussian(rng));
+        const auto fwd = embed_sequence_cached(seq, bank);
+        auto a = zeros_like(host);
+        embed_sequence_backward(seq, bank, fwd.merged, up, a);
+        auto b = zeros_like(host);
+        for (std::size_t pos = 0; pos < seq.size(); ++pos) {
+            std::vector<token_id> ctx(3, 0);
+            for (int j = 0; j < 3; ++j)
+                if (long(pos) - 2 + j >= 0) ctx[std::size_t(j)] = seq[pos - 2 + std::size_t(j)];
+            embed_backward(ctx, bank, std::span<const float>(up).subspan(pos * 256, 256), b);
+        }
+        CHECK(close_rows(a.base, b.base));
+        for (std::size_t i = 0; i < a.sub_tables.size(); ++i) CHECK(close_rows(a.sub_tables[i], b.sub_tables[i]));
+        for (std::size_t i = 0; i < a.projections.size(); ++i) CHECK(close_rows(a.projections[i], b.projections[i]));
+        auto twice = a;
+        embed_sequence_backward(seq, bank, fwd.merged, up, twice);
+        std::vector<float> dbl(a.base.size());
+        for (std::size_t i = 0; i < dbl.size(); ++i) dbl[i] = 2.0f * a.base[i];
+        CHECK(close_rows(twice.base, dbl));
+        CHECK_THROWS_AS(embed_backward(std::span<const token_id>(seq).first(3), bank,
+                                       std::span<const float>(up).first(255), b),
+                        std::invalid_argument);
+        auto bad = seq;
+        bad[7] = 500;
+        const auto before = a.base;
+        CHECK_THROWS_AS(embed_sequence_backward(bad, bank, fwd.merged, up, a), std::out_of_range);
+        CHECK(a.base == before);
+    });
     std::printf("%d checks, %d failures\n", g_checks, g_fail);
     return g_fail == 0 ? 0 : 1;
 }
