@@ -13,6 +13,7 @@
 // HBM: reads N tokens (L1/L2 hits, 4 B/token from DRAM), writes B ids (u32) and B
 // storage rows (i32): 4 + 8B bytes/token -- purely bandwidth/latency bound.
 #include <cstdint>
+#include <cstdlib>
 
 #include "hashdev.cuh"
 #include "kernels.h"
@@ -178,6 +179,65 @@ __global__ void __launch_bounds__(256) hash_gather_kernel(Shape s, const HashTab
     gather_position<MAXN, 4>(s, ht, w, sub, X + t * (int64_t)s.D, grow, Tpad, t, lane);
 }
 
+// K1+K2, block-decoupled form (default when D == B*d, B <= 32 and d/8 is a power of two):
+// a block takes P positions at a time; phase A hashes all P*B (position, branch) pairs in
+// parallel, one thread each, into shared memory; phase B streams the P*D*2 bytes of X as
+// one flat array of 16-byte vectors (X rows of consecutive positions are contiguous), U
+// independent loads in flight per thread -- the access pattern of a plain row gather.
+template <int MAXN, int LOG_VPR, int U, int kGatherP>
+__global__ void __launch_bounds__(256) hash_gather_block_kernel(Shape s, const HashTables* __restrict__ ht,
+                                                                const uint32_t* __restrict__ tokens,
+                                                                const int64_t* __restrict__ seq_off, int64_t nseq,
+                                                                int64_t T, const uint32_t* __restrict__ prior,
+                                                                const __nv_bfloat16* __restrict__ sub,
+                                                                __nv_bfloat16* __restrict__ X,
+                                                                int32_t* __restrict__ grow, int64_t Tpad,
+                                                                unsigned long long* err, int64_t t_begin,
+                                                                int64_t t_end) {
+    __shared__ int32_t srow[kGatherP * 32];
+    const int B = s.B;
+    constexpr int VPR = 1 << LOG_VPR;  // 16-byte vectors per sub-table row
+    const uint4* sub4 = reinterpret_cast<const uint4*>(sub);
+    uint4* X4 = reinterpret_cast<uint4*>(X);
+    const int64_t vpos = (int64_t)B * VPR;  // vectors per X row
+    for (int64_t t0 = t_begin + (int64_t)blockIdx.x * kGatherP; t0 < t_end; t0 += (int64_t)gridDim.x * kGatherP) {
+        const int np = (int)(t_end - t0 < kGatherP ? t_end - t0 : kGatherP);
+        for (int i = threadIdx.x; i < np * B; i += blockDim.x) {
+            const int p = i / B, b = i - p * B;
+            const int64_t t = t0 + p;
+            uint32_t w[MAXN];
+            int32_t row = -1;
+            if (load_window<MAXN>(s, tokens, seq_off, nseq, prior, t, w)) {
+                row = storage_row(ht, b, branch_hash<MAXN>(s, ht, w, b), nullptr);
+                if (grow) grow[(int64_t)b * Tpad + t] = row;
+            } else if (b == 0) {
+                atomicMin(err, (unsigned long long)t);
+            }
+            srow[i] = row;
+        }
+        __syncthreads();
+        const int n = np * B * VPR;
+        uint4* dst = X4 + t0 * vpos;
+        for (int v0 = threadIdx.x; v0 < n; v0 += blockDim.x * U) {
+            uint4 val[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int v = v0 + u * (int)blockDim.x;
+                if (v < n) {
+                    const int32_t row = srow[v >> LOG_VPR];
+                    if (row >= 0) val[u] = __ldg(sub4 + (int64_t)row * VPR + (v & (VPR - 1)));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int v = v0 + u * (int)blockDim.x;
+                if (v < n && srow[v >> LOG_VPR] >= 0) dst[v] = val[u];
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // Small-T variant (decode / verify): one warp per (position, branch), so a position's B
 // rows are fetched by B warps in a single round of loads instead of serially by one warp.
 template <int MAXN>
@@ -234,6 +294,44 @@ void launch_hash_gather(const Shape& s, const HashTables* ht, const uint32_t* to
                         int64_t t_end) {
     if (t_end < 0) t_end = T;
     if (t_end <= t_begin) return;
+    static const bool warp_form = getenv("NGRAM_GATHER_WARP") != nullptr;  // A/B switch
+    const int vpr = s.d / 8;
+    const bool block_form = !warp_form && s.variant == 1 && s.B >= 1 && s.B <= 32 && s.d % 8 == 0 &&
+                            (vpr & (vpr - 1)) == 0 && vpr <= 64 && s.N <= 8 && (int64_t)s.B * s.d == s.D;
+    if (block_form) {
+        // one P-position tile per block, not persistent: block turnover overlaps one block's
+        // hashing phase with its neighbours' copy phases (measured: 0.145 vs 0.153 ms persistent)
+        constexpr int P = 16;
+        const int64_t blocks = (t_end - t_begin + P - 1) / P;
+        auto go = [&](auto kern) {
+            kern<<<(unsigned)blocks, 256, 0, st>>>(s, ht, tokens, seq_off, nseq, T, prior, sub, X, grow, Tpad, err,
+                                                    t_begin, t_end);
+        };
+        const int lv = __builtin_ctz((unsigned)vpr);
+        if (s.N <= 4) {
+            switch (lv) {
+                case 0: go(hash_gather_block_kernel<4, 0, 8, P>); break;
+                case 1: go(hash_gather_block_kernel<4, 1, 8, P>); break;
+                case 2: go(hash_gather_block_kernel<4, 2, 8, P>); break;
+                case 3: go(hash_gather_block_kernel<4, 3, 8, P>); break;
+                case 4: go(hash_gather_block_kernel<4, 4, 8, P>); break;
+                case 5: go(hash_gather_block_kernel<4, 5, 8, P>); break;
+                default: go(hash_gather_block_kernel<4, 6, 8, P>); break;
+            }
+        } else {
+            switch (lv) {
+                case 0: go(hash_gather_block_kernel<8, 0, 8, P>); break;
+                case 1: go(hash_gather_block_kernel<8, 1, 8, P>); break;
+                case 2: go(hash_gather_block_kernel<8, 2, 8, P>); break;
+                case 3: go(hash_gather_block_kernel<8, 3, 8, P>); break;
+                case 4: go(hash_gather_block_kernel<8, 4, 8, P>); break;
+                case 5: go(hash_gather_block_kernel<8, 5, 8, P>); break;
+                default: go(hash_gather_block_kernel<8, 6, 8, P>); break;
+            }
+        }
+        count_launch();
+        return;
+    }
     const unsigned blocks = (unsigned)((t_end - t_begin + 7) / 8);  // 8 warps (positions) per block
     if (s.N <= 4)
         hash_gather_kernel<4><<<blocks, 256, 0, st>>>(s, ht, tokens, seq_off, nseq, T, prior, sub, X, grow, Tpad, err,
