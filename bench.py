@@ -222,13 +222,28 @@ def run_ours(args):
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
+    fallback = None
     if sharding == "row":
         # row-sharded tables: this rank keeps 1/world of every sub-table; rows travel over
-        # NVLink by the fused gather + peer-store kernel; one NCCL all-reduce = barrier
-        bank = G.DeviceBank(cfg, device=local, shard_rank=rank, shard_count=world)
-        bank.generate(1234)
-        group = G.ShardGroup(bank, T)
-        G.connect_shard_groups(group)
+        # NVLink by the fused gather + peer-store kernel; one NCCL all-reduce = barrier.
+        # Set-up is agreed collectively: if any rank cannot map its peers (CUDA IPC), every
+        # rank falls back to replicas and the JSON line says so.
+        ok, why = 1, ""
+        try:
+            bank = G.DeviceBank(cfg, device=local, shard_rank=rank, shard_count=world)
+            bank.generate(1234)
+            group = G.ShardGroup(bank, T)
+            G.connect_shard_groups(group)
+        except Exception as e:  # noqa: BLE001 -- reported, then agreed across ranks
+            ok, why = 0, f"rank {rank}: {type(e).__name__}: {e}"
+        flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 0:
+            fallback = why or "a peer rank failed to set up the row-sharded exchange"
+            group = bank = None
+            torch.cuda.synchronize()
+            sharding = "replica"
+    if sharding == "row":
         all_t = torch.empty(total_tokens, dtype=torch.int32, device=dev)
         all_off = torch.arange(0, total_tokens + 1, seq_len, dtype=torch.int64, device=dev)
         rank_tok = [r * T for r in range(world + 1)]
@@ -392,6 +407,8 @@ def run_ours(args):
                      "flops_per_launch": flops, "launch_ms": proj_ms},
         "hbm": hbm, "stages_ms": stages, "clocks": clocks, "e2e": e2e, "gpu_launches": int(launches),
     }
+    if fallback:
+        line["config"]["sharding_fallback"] = fallback
     if sharding == "row":
         remote = T * world * B * d * 2 * (world - 1) / world / world  # rows this rank ships to peers
         line["nvlink"] = {"remote_bytes_per_rank": remote, "scatter_ms": st_ms[1],

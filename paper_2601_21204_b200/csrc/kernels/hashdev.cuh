@@ -23,6 +23,13 @@ __device__ __forceinline__ uint64_t mulmod128(uint64_t a, uint64_t b, uint64_t m
 
 // Position t of the concatenated batch -> sequence index (largest s with off[s] <= t).
 __device__ __forceinline__ int64_t find_seq(const int64_t* __restrict__ off, int64_t nseq, int64_t t) {
+    // equal-length batches (decode steps, verify blocks, uniform prefill): two dependent
+    // loads instead of log2(nseq); the check keeps the result identical to the search below
+    const int64_t total = __ldg(off + nseq);
+    if (nseq > 1 && total > 0 && total % nseq == 0) {
+        const int64_t sq = t / (total / nseq);
+        if (sq < nseq && __ldg(off + sq) <= t && __ldg(off + sq + 1) > t) return sq;
+    }
     int64_t lo = 0, hi = nseq - 1;
     while (lo < hi) {
         const int64_t mid = (lo + hi + 1) >> 1;
