@@ -259,6 +259,26 @@ int ngram_grad_tensor(ngram_grad* g, int which, float** dev_ptr, int64_t* numel)
  * proj[b] D x d (v2 only), gain / bias D (layer_norm only); null pointers are skipped. */
 int ngram_grad_download(ngram_grad* g, float* base, float* const* sub, float* const* proj, float* gain, float* bias);
 
+/* ------------------------------------------------------------------ PLNE (per-layer FFN) */
+/* ffn_plne (ple.hpp:168-181) batched on the device: y = W_d (SiLU(W_g x) (.) g) with g the
+ * layer bank's merged embedding of each position's window (layer bank: amplification none,
+ * dim = hidden).  gate: dev f32 [hidden][d_model]; down: dev f32 [d_model][hidden];
+ * x, y: dev f32 [T][d_model]; tokens / seq_offsets / prior as ngram_embed_forward.  fp32
+ * GEMMs (cuBLAS, no TF32).  ffn_ple (table-row gate) = a base-only layer bank (max_order 1).
+ * Outputs are unspecified when a token is out of range (NGRAM_ERANGE at the next sync). */
+typedef struct ngram_plne ngram_plne;
+int ngram_plne_create(ngram_bank* layer_bank, int d_model, ngram_plne** out);
+int ngram_plne_destroy(ngram_plne* p);
+int ngram_plne_forward(ngram_plne* p, const float* gate, const float* down, const float* x, const uint32_t* tokens,
+                       const int64_t* seq_offsets, int64_t nseq, int64_t total_tokens, const uint32_t* prior, float* y,
+                       void* stream);
+/* ffn_plne_backward (ple.hpp:183-196): ACCUMULATES d_gate, d_down, dx (dev f32, shapes as
+ * gate / down / x) and, when bank_grads is not null, the layer bank's gradients. */
+int ngram_plne_backward(ngram_plne* p, ngram_grad* bank_grads, const float* gate, const float* down, const float* x,
+                        const uint32_t* tokens, const int64_t* seq_offsets, int64_t nseq, int64_t total_tokens,
+                        const uint32_t* prior, const float* upstream, float* d_gate, float* d_down, float* dx,
+                        void* stream);
+
 #ifdef __cplusplus
 }
 #endif

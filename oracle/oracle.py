@@ -58,6 +58,10 @@ def lib():
             _u32p, C.c_int64, C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_uint32, C.c_int, C.c_int, C.c_int, _u64p,
             C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
             C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_void_p, C.c_void_p]
+        plne = [C.c_void_p, _u32p, C.c_int, C.c_int, C.c_uint32, C.c_int, C.c_int, _u64p, _f32p,
+                C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_void_p, C.c_void_p, C.c_int]
+        L.or_ffn_plne_f64.argtypes = plne + [C.c_void_p]
+        L.or_ffn_plne_backward_f64.argtypes = plne + [C.c_void_p] * 4 + [C.POINTER(C.c_void_p)] * 2 + [C.c_void_p]
         L.or_synth_value.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint32, C.c_float]
         L.or_synth_value.restype = C.c_float
         L.or_synth_scale.argtypes = [C.c_double]
@@ -137,6 +141,10 @@ def ref():
         L.ref_embed_sequence_backward_f64.argtypes = [C.c_void_p, _u32p, C.c_int64, C.c_void_p, C.c_int64,
                                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                                       C.c_void_p, C.c_void_p]
+        L.ref_ffn_plne_f64.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, _u32p, C.c_void_p]
+        L.ref_ffn_plne_backward_f64.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, _u32p,
+                                                C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                                C.c_void_p, C.c_void_p]
         L.ref_cache_create.argtypes = [C.c_char_p]
         L.ref_cache_create.restype = C.c_void_p
         L.ref_cache_destroy.argtypes = [C.c_void_p]
@@ -295,6 +303,55 @@ def embed_sequence_backward(bank: HostBank, tokens, merged, upstream, prior=None
     if rc:
         raise (IndexError if rc == -2 else ValueError)(f"or_embed_sequence_backward rc={rc}")
     return g
+
+
+def window(tokens, pos, N, prior=None):
+    """detail::fill_context (embedding.hpp:391-405): the N-token window ending at pos."""
+    pr = [] if prior is None else list(prior)
+    out = []
+    for j in range(N):
+        i = pos - (N - 1) + j
+        if i >= 0:
+            out.append(int(tokens[i]))
+        else:
+            k = len(pr) + i
+            out.append(int(pr[k]) if k >= 0 else 0)
+    return np.array(out, np.uint32)
+
+
+def ffn_plne(bank: HostBank, gate, down, x, ctx):
+    """ffn_plne<double> restated (ple.hpp:168-181, 76-100): one position."""
+    cfg = bank.cfg
+    N, K, D, B, d, v, denom = shape(cfg)
+    Dm = gate.shape[1]
+    y = np.zeros(Dm)
+    sp = (C.c_void_p * max(B, 1))(*[a.ctypes.data for a in bank.sub])
+    pp = (C.c_void_p * max(B, 1))(*[a.ctypes.data for a in bank.proj])
+    g64, d64, x64 = (np.ascontiguousarray(a, np.float64) for a in (gate, down, x))
+    rc = lib().or_ffn_plne_f64(x64.ctypes.data, np.ascontiguousarray(ctx, np.uint32), N, K, cfg["base_vocab"], D, v,
+                               sub_vocab_array(cfg), bank.base, sp, pp, g64.ctypes.data, d64.ctypes.data, Dm,
+                               y.ctypes.data)
+    if rc:
+        raise (IndexError if rc == -2 else ValueError)(f"or_ffn_plne rc={rc}")
+    return y
+
+
+def ffn_plne_backward(bank: HostBank, gate, down, x, ctx, up, g_gate, g_down, grads, dx):
+    """ffn_plne_backward<double> restated (ple.hpp:183-196, 102-142); accumulates."""
+    cfg = bank.cfg
+    N, K, D, B, d, v, denom = shape(cfg)
+    Dm = gate.shape[1]
+    sp = (C.c_void_p * max(B, 1))(*[a.ctypes.data for a in bank.sub])
+    pp = (C.c_void_p * max(B, 1))(*[a.ctypes.data for a in bank.proj])
+    gsp = (C.c_void_p * max(B, 1))(*[a.ctypes.data for a in grads["sub"]])
+    gpp = (C.c_void_p * max(B, 1))(*[a.ctypes.data for a in grads["proj"]])
+    g64, d64, x64, u64_ = (np.ascontiguousarray(a, np.float64) for a in (gate, down, x, up))
+    rc = lib().or_ffn_plne_backward_f64(x64.ctypes.data, np.ascontiguousarray(ctx, np.uint32), N, K,
+                                        cfg["base_vocab"], D, v, sub_vocab_array(cfg), bank.base, sp, pp,
+                                        g64.ctypes.data, d64.ctypes.data, Dm, u64_.ctypes.data, g_gate.ctypes.data,
+                                        g_down.ctypes.data, grads["base"].ctypes.data, gsp, gpp, dx.ctypes.data)
+    if rc:
+        raise (IndexError if rc == -2 else ValueError)(f"or_ffn_plne_backward rc={rc}")
 
 
 def bank_checksum(bank: HostBank) -> int:

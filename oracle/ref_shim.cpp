@@ -22,6 +22,7 @@
 #include "ngram/embedding.hpp"
 #include "ngram/errors.hpp"
 #include "ngram/hashing.hpp"
+#include "ngram/ple.hpp"
 
 using namespace ngram;
 
@@ -239,6 +240,62 @@ int ref_embed_sequence_backward_f64(void* h, const uint32_t* tokens, int64_t len
             std::memcpy(g_proj[b], g.projections[b].data(), g.projections[b].size() * 8);
         if (g_gain && !g.ln_gain.empty()) std::memcpy(g_gain, g.ln_gain.data(), g.ln_gain.size() * 8);
         if (g_bias && !g.ln_bias.empty()) std::memcpy(g_bias, g.ln_bias.data(), g.ln_bias.size() * 8);
+        return 0;
+    } catch (...) {
+        return map_exc();
+    }
+}
+
+// ple.hpp:168-181 ffn_plne<double> on bank_cast<float,double> (n-gram form: empty table).
+static ple_params_t<double> plne_params(const double* gate, const double* down, int d_model, int hidden,
+                                        std::uint32_t v0) {
+    ple_params_t<double> p;
+    p.d_model = d_model;
+    p.hidden = hidden;
+    p.base_vocab = v0;
+    p.gate.assign(gate, gate + std::size_t(hidden) * std::size_t(d_model));
+    p.down.assign(down, down + std::size_t(d_model) * std::size_t(hidden));
+    return p;
+}
+
+int ref_ffn_plne_f64(void* h, const double* gate, const double* down, int d_model, const double* x,
+                     const uint32_t* ctx, double* y) {
+    try {
+        auto& bk = static_cast<ref_bank*>(h)->bank;
+        const auto bd = bank_cast<float, double>(bk);
+        const auto p = plne_params(gate, down, d_model, bk.config.dim, bk.config.base_vocab);
+        const auto r = ffn_plne<double>(std::span<const double>(x, std::size_t(d_model)),
+                                        std::span<const token_id>(ctx, std::size_t(bk.config.max_order)), bd, p);
+        std::memcpy(y, r.data(), r.size() * 8);
+        return 0;
+    } catch (...) {
+        return map_exc();
+    }
+}
+
+// ple.hpp:183-196 ffn_plne_backward<double>: fresh zero grads per call (ple_zeros_like,
+// zeros_like), copied out in the reference layouts; dx starts at zero.
+int ref_ffn_plne_backward_f64(void* h, const double* gate, const double* down, int d_model, const double* x,
+                              const uint32_t* ctx, const double* up, double* g_gate, double* g_down, double* g_base,
+                              double* const* g_sub, double* const* g_proj, double* dx) {
+    try {
+        auto& bk = static_cast<ref_bank*>(h)->bank;
+        const auto bd = bank_cast<float, double>(bk);
+        const auto p = plne_params(gate, down, d_model, bk.config.dim, bk.config.base_vocab);
+        auto gp = ple_zeros_like(p);
+        auto gb = zeros_like(bd);
+        std::vector<double> d(std::size_t(d_model), 0.0);
+        ffn_plne_backward<double>(std::span<const double>(x, std::size_t(d_model)),
+                                  std::span<const token_id>(ctx, std::size_t(bk.config.max_order)), bd, p,
+                                  std::span<const double>(up, std::size_t(d_model)), gp, gb, std::span<double>(d));
+        std::memcpy(g_gate, gp.gate.data(), gp.gate.size() * 8);
+        std::memcpy(g_down, gp.down.data(), gp.down.size() * 8);
+        std::memcpy(g_base, gb.base.data(), gb.base.size() * 8);
+        for (std::size_t b = 0; b < gb.sub_tables.size(); ++b)
+            std::memcpy(g_sub[b], gb.sub_tables[b].data(), gb.sub_tables[b].size() * 8);
+        for (std::size_t b = 0; b < gb.projections.size(); ++b)
+            std::memcpy(g_proj[b], gb.projections[b].data(), gb.projections[b].size() * 8);
+        std::memcpy(dx, d.data(), d.size() * 8);
         return 0;
     } catch (...) {
         return map_exc();

@@ -35,6 +35,7 @@ SYMBOLS = [
     "ngram_shard_local_buffers", "ngram_shard_set_peer", "ngram_shard_scatter_rows", "ngram_shard_project",
     "ngram_grad_create", "ngram_grad_destroy", "ngram_grad_zero", "ngram_embed_backward", "ngram_grad_tensor",
     "ngram_grad_download", "ngram_embed_backward_host",
+    "ngram_plne_create", "ngram_plne_destroy", "ngram_plne_forward", "ngram_plne_backward",
 ]
 
 
@@ -148,6 +149,10 @@ def lib() -> C.CDLL:
         "ngram_grad_tensor": ([vp, i32, C.POINTER(vp), C.POINTER(i64)], i32),
         "ngram_grad_download": ([vp, vp, vp, vp, vp, vp], i32),
         "ngram_embed_backward_host": ([vp, vp, vp, i64, vp, vp, vp, i32], i32),
+        "ngram_plne_create": ([vp, i32, C.POINTER(vp)], i32),
+        "ngram_plne_destroy": ([vp], i32),
+        "ngram_plne_forward": ([vp, vp, vp, vp, vp, vp, i64, i64, vp, vp, vp], i32),
+        "ngram_plne_backward": ([vp, vp, vp, vp, vp, vp, vp, i64, i64, vp, vp, vp, vp, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

@@ -38,6 +38,10 @@ struct ngram_grad {
     }
 };
 
+namespace ngh {
+ngram_bank* grad_bank(ngram_grad* g) { return g->bank; }
+}  // namespace ngh
+
 namespace {
 
 void check_blas(cublasStatus_t s, const char* what) {

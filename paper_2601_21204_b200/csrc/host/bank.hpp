@@ -151,4 +151,5 @@ bool forward_tokens(ngram_bank* b, const uint32_t* tokens, const int64_t* seq_of
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 // Row padding of every per-token workspace: the 2-CTA GEMM tile is 256 tokens.
 constexpr int64_t kRowPad = 256;
+ngram_bank* grad_bank(ngram_grad* g);  // backward.cpp
 }  // namespace ngh

@@ -1,0 +1,148 @@
+// plne.cpp -- C-ABI of the per-layer N-gram FFN (PLNE, ple.hpp:168-196):
+//   y = W_d (SiLU(W_g x) (.) g),   g = the layer bank's merged embedding (no amplification).
+// Batched over T positions: G from the N-gram forward (K1+K2 -> K3, amp none), U = X W_g^T and
+// Y = Hh W_d^T as fp32 GEMMs (cuBLAS, no TF32), SiLU gating elementwise (plne.cu).  The plain
+// per-layer form ffn_ple (a table row as the gate) is PLNE with a base-only layer bank
+// (max_order 1, E0 = the table), as the reference's own test states (test_ple.cpp:150-172).
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <string>
+
+#include "api_util.hpp"
+#include "bank.hpp"
+
+using namespace ngh;
+
+struct ngram_plne {
+    ngram_bank* bank = nullptr;
+    int d_model = 0, hidden = 0;
+    cublasHandle_t blas = nullptr;
+    DevBuf<float> U, G, Hh, dHh, dG, dU;
+    int64_t cap = 0;
+    ~ngram_plne() {
+        if (blas) cublasDestroy(blas);
+    }
+};
+
+namespace {
+
+void blas_ok(cublasStatus_t s, const char* what) {
+    if (s != CUBLAS_STATUS_SUCCESS)
+        throw Error(NGRAM_ECUDA, std::string(what) + " failed (cublas status " + std::to_string(int(s)) + ")");
+}
+
+void status_ok(int rc) {
+    if (rc != NGRAM_OK) throw Error(rc, ngram_last_error());
+}
+
+void ensure(ngram_plne* p, int64_t T, bool backward) {
+    if (T <= p->cap && (!backward || p->dHh.n)) return;
+    const int64_t cap = std::max<int64_t>(T, p->cap);
+    const size_t n = size_t(cap) * size_t(p->hidden);
+    for (DevBuf<float>* b : {&p->U, &p->G, &p->Hh}) b->ensure(n);
+    if (backward)
+        for (DevBuf<float>* b : {&p->dHh, &p->dG, &p->dU}) b->ensure(n);
+    p->cap = cap;
+}
+
+// G = merged layer-bank rows, U = X W_g^T, Hh = SiLU(U) * G.  Row-major M (r x c) is the
+// column-major M^T with ld = c, so U^T (H x T) = gate_cm^T X_cm etc.
+void forward_common(ngram_plne* p, const float* gate, const float* x, const uint32_t* tokens, const int64_t* off,
+                    int64_t nseq, int64_t T, const uint32_t* prior, cudaStream_t st) {
+    status_ok(ngram_embed_forward(p->bank, tokens, off, nseq, T, prior, nullptr, p->G.p, NGRAM_F32, st));
+    const float one = 1.0f, zero = 0.0f;
+    const int H = p->hidden, Dm = p->d_model;
+    blas_ok(cublasSetStream(p->blas, st), "cublasSetStream");
+    blas_ok(cublasSgemm(p->blas, CUBLAS_OP_T, CUBLAS_OP_N, H, int(T), Dm, &one, gate, Dm, x, Dm, &zero, p->U.p, H),
+            "cublasSgemm(U = X W_g^T)");
+    ngk::launch_silu_gate(p->U.p, p->G.p, p->Hh.p, T * H, p->bank->err.p, st);
+}
+
+}  // namespace
+
+extern "C" {
+
+int ngram_plne_create(ngram_bank* b, int d_model, ngram_plne** out) {
+    NGRAM_API_BEGIN
+    if (!b || !out) throw Error(NGRAM_EINVAL, "ngram_plne_create: bad argument");
+    if (d_model < 1) throw Error(NGRAM_EINVAL, "ple: d_model and hidden must be >= 1");
+    if (b->hash_only) throw Error(NGRAM_EINVAL, "bank was created hash-only (NGRAM_BANK_HASH_ONLY)");
+    if (b->shape.amp != ngk::kAmpNone) throw Error(NGRAM_EINVAL, "ffn_plne: layer banks use no amplification");
+    DeviceGuard dg(b->device);
+    auto p = std::make_unique<ngram_plne>();
+    p->bank = b;
+    p->d_model = d_model;
+    p->hidden = b->shape.D;
+    blas_ok(cublasCreate(&p->blas), "cublasCreate");
+    blas_ok(cublasSetMathMode(p->blas, CUBLAS_PEDANTIC_MATH), "cublasSetMathMode");  // true fp32
+    *out = p.release();
+    NGRAM_API_END
+}
+
+int ngram_plne_destroy(ngram_plne* p) {
+    NGRAM_API_BEGIN
+    if (p) {
+        DeviceGuard dg(p->bank->device);
+        delete p;
+    }
+    NGRAM_API_END
+}
+
+int ngram_plne_forward(ngram_plne* p, const float* gate, const float* down, const float* x, const uint32_t* tokens,
+                       const int64_t* seq_offsets, int64_t nseq, int64_t T, const uint32_t* prior, float* y,
+                       void* stream) {
+    NGRAM_API_BEGIN
+    if (!p || !seq_offsets || nseq < 1 || T < 0 || (T > 0 && (!gate || !down || !x || !tokens || !y)))
+        throw Error(NGRAM_EINVAL, "ngram_plne_forward: bad argument");
+    DeviceGuard dg(p->bank->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (T == 0) return NGRAM_OK;
+    ensure(p, T, false);
+    forward_common(p, gate, x, tokens, seq_offsets, nseq, T, prior, st);
+    const float one = 1.0f, zero = 0.0f;
+    const int H = p->hidden, Dm = p->d_model;
+    blas_ok(cublasSgemm(p->blas, CUBLAS_OP_T, CUBLAS_OP_N, Dm, int(T), H, &one, down, H, p->Hh.p, H, &zero, y, Dm),
+            "cublasSgemm(Y = Hh W_d^T)");
+    NGRAM_API_END
+}
+
+int ngram_plne_backward(ngram_plne* p, ngram_grad* bank_grads, const float* gate, const float* down, const float* x,
+                        const uint32_t* tokens, const int64_t* seq_offsets, int64_t nseq, int64_t T,
+                        const uint32_t* prior, const float* upstream, float* d_gate, float* d_down, float* dx,
+                        void* stream) {
+    NGRAM_API_BEGIN
+    if (!p || !seq_offsets || nseq < 1 || T < 0 ||
+        (T > 0 && (!gate || !down || !x || !tokens || !upstream || !d_gate || !d_down || !dx)))
+        throw Error(NGRAM_EINVAL, "ngram_plne_backward: bad argument");
+    if (bank_grads && grad_bank(bank_grads) != p->bank)
+        throw Error(NGRAM_EINVAL, "ngram_plne_backward: gradient bank belongs to another bank");
+    DeviceGuard dg(p->bank->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (T == 0) return NGRAM_OK;
+    ensure(p, T, true);
+    forward_common(p, gate, x, tokens, seq_offsets, nseq, T, prior, st);  // recompute, as the reference
+    const float one = 1.0f, zero = 0.0f;
+    const int H = p->hidden, Dm = p->d_model;
+    const int n = int(T);
+    // g_down (Dm x H) += dY^T Hh  <=>  col-major g_down^T (H x Dm) += Hh_cm dY_cm^T
+    blas_ok(cublasSgemm(p->blas, CUBLAS_OP_N, CUBLAS_OP_T, H, Dm, n, &one, p->Hh.p, H, upstream, Dm, &one, d_down, H),
+            "cublasSgemm(dW_d)");
+    // dHh (T x H) = dY W_d  <=>  col-major dHh^T = down_cm dY_cm
+    blas_ok(cublasSgemm(p->blas, CUBLAS_OP_N, CUBLAS_OP_N, H, n, Dm, &one, down, H, upstream, Dm, &zero, p->dHh.p, H),
+            "cublasSgemm(dHh)");
+    ngk::launch_silu_gate_backward(p->dHh.p, p->U.p, p->G.p, p->dG.p, p->dU.p, T * H, p->bank->err.p, st);
+    if (bank_grads)  // embed_backward of dL/dg (ple.hpp:195)
+        status_ok(ngram_embed_backward(bank_grads, tokens, seq_offsets, nseq, T, prior, nullptr, p->dG.p,
+                                       NGRAM_BWD_SKIP_AMPLIFY, st));
+    // g_gate (H x Dm) += dU^T X  <=>  col-major g_gate^T (Dm x H) += X_cm dU_cm^T
+    blas_ok(cublasSgemm(p->blas, CUBLAS_OP_N, CUBLAS_OP_T, Dm, H, n, &one, x, Dm, p->dU.p, H, &one, d_gate, Dm),
+            "cublasSgemm(dW_g)");
+    // dx (T x Dm) += dU W_g  <=>  col-major dx^T += gate_cm dU_cm
+    blas_ok(cublasSgemm(p->blas, CUBLAS_OP_N, CUBLAS_OP_N, Dm, n, H, &one, gate, Dm, p->dU.p, H, &one, dx, Dm),
+            "cublasSgemm(dx)");
+    NGRAM_API_END
+}
+
+}  // extern "C"

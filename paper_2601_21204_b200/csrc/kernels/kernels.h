@@ -81,6 +81,12 @@ void launch_scatter_rows(const Shape& s, const int32_t* grow, int64_t Tpad, int6
                          cudaStream_t st);
 void launch_bf16_to_f32(const __nv_bfloat16* src, float* dst, int64_t n, cudaStream_t st);
 
+// ---- PLNE (plne.cu): SwiGLU gating by the layer bank's embedding
+void launch_silu_gate(const float* U, const float* G, float* Hh, int64_t n, const unsigned long long* err,
+                      cudaStream_t st);
+void launch_silu_gate_backward(const float* dHh, const float* U, const float* G, float* dG, float* dU, int64_t n,
+                               const unsigned long long* err, cudaStream_t st);
+
 struct FwdArgs {
     Shape s;
     const HashTables* ht;

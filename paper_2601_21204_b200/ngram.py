@@ -465,6 +465,49 @@ class GradBank:
         return out
 
 
+# ----------------------------------------------------------------------------- PLNE
+class PlneLayer:
+    """Per-layer N-gram FFN (ffn_plne / ffn_plne_backward, ple.hpp:168-196) over a device
+    layer bank (amplification none, dim = hidden): y = W_d (SiLU(W_g x) * g).  gate:
+    [hidden, d_model] f32, down: [d_model, hidden] f32, x / y: [T, d_model] f32 (device).
+    ffn_ple (table-row gate) = a base-only layer bank (max_order 1, E0 = the table)."""
+
+    def __init__(self, layer_bank: DeviceBank, d_model: int):
+        self.bank, self.d_model, self.hidden = layer_bank, d_model, layer_bank.D
+        h = C.c_void_p()
+        check(abi.lib().ngram_plne_create(layer_bank.handle, d_model, C.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            abi.lib().ngram_plne_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def forward(self, gate: torch.Tensor, down: torch.Tensor, x: torch.Tensor, tokens: torch.Tensor,
+                seq_offsets: torch.Tensor, prior: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
+                stream=None) -> torch.Tensor:
+        T = tokens.numel()
+        y = out if out is not None else torch.empty((T, self.d_model), dtype=torch.float32, device=x.device)
+        check(abi.lib().ngram_plne_forward(self.handle, _ptr(gate), _ptr(down), _ptr(x), _ptr(tokens),
+                                           _ptr(seq_offsets), seq_offsets.numel() - 1, T, _ptr(prior), _ptr(y),
+                                           _stream(stream)))
+        return y
+
+    def backward(self, gate, down, x, tokens, seq_offsets, upstream, d_gate, d_down, dx,
+                 bank_grads: Optional["GradBank"] = None, prior=None, stream=None) -> None:
+        """Accumulates d_gate, d_down, dx and (optionally) the layer bank's gradients."""
+        check(abi.lib().ngram_plne_backward(self.handle, bank_grads.handle if bank_grads else None, _ptr(gate),
+                                            _ptr(down), _ptr(x), _ptr(tokens), _ptr(seq_offsets),
+                                            seq_offsets.numel() - 1, tokens.numel(), _ptr(prior), _ptr(upstream),
+                                            _ptr(d_gate), _ptr(d_down), _ptr(dx), _stream(stream)))
+
+
 # ----------------------------------------------------------------------------- row shards
 class ShardGroup:
     """Row-sharded exchange of one rank: double-buffered home X, peer buffers

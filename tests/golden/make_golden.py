@@ -204,6 +204,7 @@ def main():
     save("draft_verify.npz", config=json.dumps(cfgD), seed=99, ncases=6, **cases)
     R.ref_bank_destroy(hb)
     backward_goldens()
+    plne_goldens()
 
 
 def backward_goldens():
@@ -264,8 +265,64 @@ def backward_goldens():
         R.ref_bank_destroy(hb)
 
 
+def plne_goldens():
+    # 10. PLNE (ple.hpp:168-196): ffn_plne<double> / ffn_plne_backward<double> per position of
+    #     two sequences (the second with a carried prior); params are float-representable.
+    for name, cfg, seed, dm in [("tc", dict(ref_default_config(1000, 256, 3, 2), amplification="none"), 77, 128),
+                                ("small", O.make_config(10, 6, 3, 1, [25, 31], "subtable_v2", "none"), 21, 4)]:
+        hb = ref_bank(cfg, seed)
+        H, N = cfg["dim"], cfg["max_order"]
+        r = np.random.default_rng(seed)
+        gate = (0.02 * r.standard_normal((H, dm))).astype(np.float32).astype(np.float64)
+        down = (0.02 * r.standard_normal((dm, H))).astype(np.float32).astype(np.float64)
+        toks = O.uniform_tokens(61, cfg["base_vocab"], 48)
+        prior = O.uniform_tokens(62, cfg["base_vocab"], N - 1)
+        T = len(toks)
+        x = r.standard_normal((T, dm)).astype(np.float32).astype(np.float64)
+        up = r.standard_normal((T, dm)).astype(np.float32).astype(np.float64)
+        y = np.zeros((T, dm))
+        dx = np.zeros((T, dm))
+        g_gate, g_down = np.zeros((H, dm)), np.zeros((dm, H))
+        acc = O.zero_grads(cfg)
+        for (a, b), pr in zip([(0, 16), (16, T)], [None, prior]):
+            for pos in range(b - a):
+                ctx = O.window(toks[a:b], pos, N, pr)
+                t = a + pos
+                assert R.ref_ffn_plne_f64(hb, gate.ctypes.data, down.ctypes.data, dm, x[t].ctypes.data, ctx,
+                                          y[t].ctypes.data) == 0
+                gg, gd, d1 = np.zeros((H, dm)), np.zeros((dm, H)), np.zeros(dm)
+                gr = O.zero_grads(cfg)
+                sp = (C.c_void_p * max(len(gr["sub"]), 1))(*[q.ctypes.data for q in gr["sub"]])
+                pp = (C.c_void_p * max(len(gr["proj"]), 1))(*[q.ctypes.data for q in gr["proj"]])
+                uu = np.ascontiguousarray(up[t])
+                assert R.ref_ffn_plne_backward_f64(hb, gate.ctypes.data, down.ctypes.data, dm, x[t].ctypes.data,
+                                                   ctx, uu.ctypes.data, gg.ctypes.data, gd.ctypes.data,
+                                                   gr["base"].ctypes.data, sp, pp, d1.ctypes.data) == 0
+                g_gate += gg
+                g_down += gd
+                dx[t] = d1
+                acc["base"] += gr["base"]
+                for k in ("sub", "proj"):
+                    for q1, q2 in zip(acc[k], gr[k]):
+                        q1 += q2
+        out = {}
+        nz = np.nonzero(np.any(acc["base"] != 0, axis=1))[0]
+        out["g_base_idx"], out["g_base_val"] = nz, acc["base"][nz]
+        for b, q in enumerate(acc["sub"]):
+            nz = np.nonzero(np.any(q != 0, axis=1))[0]
+            out[f"g_sub{b}_idx"], out[f"g_sub{b}_val"] = nz, q[nz]
+        if acc["proj"]:
+            out["g_proj"] = np.stack(acc["proj"])
+        save(f"plne_{name}.npz", config=json.dumps(cfg), seed=seed, d_model=dm, gate=gate, down=down, tokens=toks,
+             seq_offsets=np.array([0, 16, T]), prior1=prior, x=x, y=y, upstream=up, g_gate=g_gate, g_down=g_down,
+             dx=dx, bank_checksum=np.uint64(bank_checksum_ref(hb, cfg)), **out)
+        R.ref_bank_destroy(hb)
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["backward"]:  # regenerate only section 9
         backward_goldens()
+    elif sys.argv[1:] == ["plne"]:  # regenerate only section 10
+        plne_goldens()
     else:
         main()

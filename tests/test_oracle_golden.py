@@ -248,3 +248,29 @@ def test_backward_restatement_matches_reference(name):  # embedding.hpp:291-459 
     ln = cfg["amplification"] == "layer_norm"
     for (n, a), (_, b) in zip(helpers.grad_items(acc, ln), helpers.grad_items(ref, ln)):
         assert np.array_equal(a, b), n  # same double operation order as the reference
+
+
+@pytest.mark.parametrize("name", ["plne_tc.npz", "plne_small.npz"])
+def test_plne_restatement_matches_reference(name):  # ple.hpp:76-196 in double
+    g = gold(name)
+    cfg = json.loads(str(g["config"]))
+    bank = O.make_bank(cfg, int(g["seed"]), round_bf16=True)
+    assert O.bank_checksum(bank) == int(g["bank_checksum"])
+    N, off, toks = cfg["max_order"], g["seq_offsets"], g["tokens"]
+    H, dm = g["gate"].shape
+    y = np.zeros_like(g["y"])
+    dx = np.zeros_like(g["dx"])
+    g_gate, g_down = np.zeros((H, dm)), np.zeros((dm, H))
+    acc = O.zero_grads(cfg)
+    for s, prior in enumerate([None, g["prior1"]]):
+        a, b = int(off[s]), int(off[s + 1])
+        for pos in range(b - a):
+            ctx = O.window(toks[a:b], pos, N, prior)
+            y[a + pos] = O.ffn_plne(bank, g["gate"], g["down"], g["x"][a + pos], ctx)
+            O.ffn_plne_backward(bank, g["gate"], g["down"], g["x"][a + pos], ctx, g["upstream"][a + pos], g_gate,
+                                g_down, acc, dx[a + pos])
+    close = lambda a, b: np.abs(a - b).max() <= 1e-12 * max(1.0, np.abs(b).max())  # noqa: E731
+    assert close(y, g["y"]) and close(dx, g["dx"]) and close(g_gate, g["g_gate"]) and close(g_down, g["g_down"])
+    ref = helpers.golden_grads(g, O.zero_grads(cfg))
+    for (n, a), (_, b) in zip(helpers.grad_items(acc, False), helpers.grad_items(ref, False)):
+        assert close(a, b), n
