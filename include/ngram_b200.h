@@ -278,6 +278,14 @@ int ngram_plne_backward(ngram_plne* p, ngram_grad* bank_grads, const float* gate
                         const uint32_t* tokens, const int64_t* seq_offsets, int64_t nseq, int64_t total_tokens,
                         const uint32_t* prior, const float* upstream, float* d_gate, float* d_down, float* dx,
                         void* stream);
+/* Host-buffer variants (synchronous; total_tokens = seq_offsets[nseq]); a token out of range
+ * returns NGRAM_ERANGE.  The backward accumulates into the host d_gate / d_down / dx. */
+int ngram_plne_forward_host(ngram_plne* p, const float* gate, const float* down, const float* x,
+                            const uint32_t* tokens, const int64_t* seq_offsets, int64_t nseq, const uint32_t* prior,
+                            float* y);
+int ngram_plne_backward_host(ngram_plne* p, ngram_grad* bank_grads, const float* gate, const float* down,
+                             const float* x, const uint32_t* tokens, const int64_t* seq_offsets, int64_t nseq,
+                             const uint32_t* prior, const float* upstream, float* d_gate, float* d_down, float* dx);
 
 #ifdef __cplusplus
 }

@@ -36,6 +36,7 @@ SYMBOLS = [
     "ngram_grad_create", "ngram_grad_destroy", "ngram_grad_zero", "ngram_embed_backward", "ngram_grad_tensor",
     "ngram_grad_download", "ngram_embed_backward_host",
     "ngram_plne_create", "ngram_plne_destroy", "ngram_plne_forward", "ngram_plne_backward",
+    "ngram_plne_forward_host", "ngram_plne_backward_host",
 ]
 
 
@@ -153,6 +154,8 @@ def lib() -> C.CDLL:
         "ngram_plne_destroy": ([vp], i32),
         "ngram_plne_forward": ([vp, vp, vp, vp, vp, vp, i64, i64, vp, vp, vp], i32),
         "ngram_plne_backward": ([vp, vp, vp, vp, vp, vp, vp, i64, i64, vp, vp, vp, vp, vp, vp], i32),
+        "ngram_plne_forward_host": ([vp, vp, vp, vp, vp, vp, i64, vp, vp], i32),
+        "ngram_plne_backward_host": ([vp, vp, vp, vp, vp, vp, vp, i64, vp, vp, vp, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

@@ -15,6 +15,7 @@
 #include "ngram/embedding.hpp"
 #include "ngram/errors.hpp"
 #include "ngram/hashing.hpp"
+#include "ngram/ple.hpp"
 #include "ngram_b200.h"
 
 namespace ngram {
@@ -259,6 +260,8 @@ std::vector<float> embed_sequence(std::span<const token_id> tokens, const embedd
 }
 
 namespace {
+void add_device_grads(ngram_grad* g, embedding_bank& grads);
+
 // Run one device backward into a fresh fp32 gradient bank and add it into the host grads.
 void backward_into(const device_bank& bank, std::span<const token_id> tokens, std::span<const token_id> prior,
                    const float* merged, const float* upstream, int flags, embedding_bank& grads) {
@@ -273,6 +276,11 @@ void backward_into(const device_bank& bank, std::span<const token_id> tokens, st
     const int64_t off[2] = {0, int64_t(tokens.size())};
     throw_status(ngram_embed_backward_host(g, tokens.data(), off, 1, pr.empty() ? nullptr : pr.data(), merged, upstream,
                                            flags));
+    add_device_grads(g, grads);
+}
+
+// grads += the device gradient bank (reference layout download).
+void add_device_grads(ngram_grad* g, embedding_bank& grads) {
     embedding_bank d = zeros_like(grads);
     std::vector<float*> sp, pp;
     for (auto& t : d.sub_tables) sp.push_back(t.data());
@@ -504,6 +512,102 @@ draft_result draft_verify(sequence_cache& state, embedding_memo&, const device_b
                           std::span<const token_id> draft, std::size_t accept_count, cache_counters* counters,
                           const draft_options& opts) {
     return draft_verify(state, bank, draft, accept_count, counters, opts);
+}
+
+// ---------------------------------------------------------------- per-layer FFN (ple.hpp)
+namespace {
+using plne_ptr = std::unique_ptr<ngram_plne, int (*)(ngram_plne*)>;
+
+plne_ptr make_plne(const device_bank& bank, const ple_params& p, std::span<const float> x) {
+    if (x.size() != std::size_t(p.d_model) || bank.config().dim != p.hidden)
+        throw std::invalid_argument("ple: input/gate width mismatch");
+    ngram_plne* h = nullptr;
+    throw_status(ngram_plne_create(bank.handle(), p.d_model, &h));
+    return plne_ptr(h, ngram_plne_destroy);
+}
+
+void check_layer_bank(const device_bank& bank, const ple_params& p, std::span<const token_id> context) {
+    const auto& cfg = bank.config();
+    if (cfg.dim != p.hidden) throw std::invalid_argument("ffn_plne: layer bank width must equal gate width");
+    if (cfg.amplification != amp_mode::none) throw std::invalid_argument("ffn_plne: layer banks use no amplification");
+    if (context.size() != std::size_t(cfg.max_order))
+        throw std::invalid_argument("hash_all_orders: context length " + std::to_string(context.size()) +
+                                    " does not match max order " + std::to_string(cfg.max_order));
+}
+
+// ffn_ple's table as a base-only layer bank (max_order 1, merge scale 1, E0 = table)
+device_bank table_bank(const ple_params& p) {
+    ngram_config cfg;
+    cfg.max_order = 1;
+    cfg.sub_tables = 1;
+    cfg.base_vocab = p.base_vocab;
+    cfg.dim = p.hidden;
+    cfg.variant = ne_variant::subtable_v2;
+    cfg.amplification = amp_mode::none;
+    embedding_bank host;
+    host.config = cfg;
+    host.base = p.table;
+    return device_bank(host);
+}
+}  // namespace
+
+std::vector<float> ffn_plne(std::span<const float> x, std::span<const token_id> context, const device_bank& layer_bank,
+                            const ple_params& p) {
+    check_layer_bank(layer_bank, p, context);
+    auto h = make_plne(layer_bank, p, x);
+    const auto pr = prior_tail(context.first(context.size() - 1), layer_bank.config().max_order - 1);
+    const int64_t off[2] = {0, 1};
+    std::vector<float> y(std::size_t(p.d_model));
+    throw_status(ngram_plne_forward_host(h.get(), p.gate.data(), p.down.data(), x.data(), context.data() + context.size() - 1,
+                                         off, 1, pr.empty() ? nullptr : pr.data(), y.data()));
+    return y;
+}
+
+std::vector<float> ffn_plne(std::span<const float> x, std::span<const token_id> context,
+                            const embedding_bank& layer_bank, const ple_params& p) {
+    return ffn_plne(x, context, device_bank(layer_bank), p);
+}
+
+void ffn_plne_backward(std::span<const float> x, std::span<const token_id> context, const device_bank& layer_bank,
+                       const ple_params& p, std::span<const float> upstream, ple_params& grads,
+                       embedding_bank& bank_grads, std::span<float> dx) {
+    check_layer_bank(layer_bank, p, context);
+    if (upstream.size() != std::size_t(p.d_model) || dx.size() != std::size_t(p.d_model))
+        throw std::invalid_argument("ple: input/gate width mismatch");
+    auto h = make_plne(layer_bank, p, x);
+    ngram_grad* g = nullptr;
+    throw_status(ngram_grad_create(layer_bank.handle(), &g));
+    std::unique_ptr<ngram_grad, int (*)(ngram_grad*)> guard(g, ngram_grad_destroy);
+    const auto pr = prior_tail(context.first(context.size() - 1), layer_bank.config().max_order - 1);
+    const int64_t off[2] = {0, 1};
+    throw_status(ngram_plne_backward_host(h.get(), g, p.gate.data(), p.down.data(), x.data(),
+                                          context.data() + context.size() - 1, off, 1, pr.empty() ? nullptr : pr.data(),
+                                          upstream.data(), grads.gate.data(), grads.down.data(), dx.data()));
+    add_device_grads(g, bank_grads);
+}
+
+void ffn_plne_backward(std::span<const float> x, std::span<const token_id> context, const embedding_bank& layer_bank,
+                       const ple_params& p, std::span<const float> upstream, ple_params& grads,
+                       embedding_bank& bank_grads, std::span<float> dx) {
+    ffn_plne_backward(x, context, device_bank(layer_bank), p, upstream, grads, bank_grads, dx);
+}
+
+std::vector<float> ffn_ple(std::span<const float> x, token_id token, const ple_params& p) {
+    if (std::uint64_t(token) >= p.base_vocab) throw std::out_of_range("ffn_ple: token out of range");
+    const token_id ctx[1] = {token};
+    return ffn_plne(x, ctx, table_bank(p), p);
+}
+
+void ffn_ple_backward(std::span<const float> x, token_id token, const ple_params& p, std::span<const float> upstream,
+                      ple_params& grads, std::span<float> dx) {
+    if (std::uint64_t(token) >= p.base_vocab) throw std::out_of_range("ffn_ple: token out of range");
+    const device_bank bank = table_bank(p);
+    embedding_bank bg;  // the base-only bank's gradient: its E0 rows are the table's
+    bg.config = bank.config();
+    bg.base.assign(grads.table.size(), 0.0f);
+    const token_id ctx[1] = {token};
+    ffn_plne_backward(x, ctx, bank, p, upstream, grads, bg, dx);
+    for (std::size_t i = 0; i < grads.table.size(); ++i) grads.table[i] += bg.base[i];
 }
 
 }  // namespace ngram

@@ -7,6 +7,7 @@
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <memory>
 #include <string>
 
@@ -21,6 +22,10 @@ struct ngram_plne {
     cublasHandle_t blas = nullptr;
     DevBuf<float> U, G, Hh, dHh, dG, dU;
     int64_t cap = 0;
+    // host-buffer entry staging
+    DevBuf<float> h_gate, h_down, h_x, h_y, h_up, h_dgate, h_ddown, h_dx;
+    DevBuf<uint32_t> h_tok, h_prior;
+    DevBuf<int64_t> h_off;
     ~ngram_plne() {
         if (blas) cublasDestroy(blas);
     }
@@ -142,6 +147,95 @@ int ngram_plne_backward(ngram_plne* p, ngram_grad* bank_grads, const float* gate
     // dx (T x Dm) += dU W_g  <=>  col-major dx^T += gate_cm dU_cm
     blas_ok(cublasSgemm(p->blas, CUBLAS_OP_N, CUBLAS_OP_N, Dm, n, H, &one, gate, Dm, p->dU.p, H, &one, dx, Dm),
             "cublasSgemm(dx)");
+    NGRAM_API_END
+}
+
+// Host-buffer variants (synchronous): stage through device buffers, accumulate on the device.
+static void stage_common(ngram_plne* p, const float* gate, const float* down, const float* x, const uint32_t* tokens,
+                         const int64_t* off, int64_t nseq, int64_t T, const uint32_t* prior) {
+    const size_t H = size_t(p->hidden), Dm = size_t(p->d_model);
+    const int N1 = std::max(p->bank->cfg.max_order - 1, 0);
+    p->h_gate.ensure(H * Dm);
+    p->h_down.ensure(H * Dm);
+    p->h_x.ensure(std::max<size_t>(size_t(T) * Dm, 1));
+    p->h_tok.ensure(size_t(std::max<int64_t>(T, 1)));
+    p->h_off.ensure(size_t(nseq + 1));
+    NGH_CUDA(cudaMemcpy(p->h_gate.p, gate, H * Dm * 4, cudaMemcpyHostToDevice));
+    NGH_CUDA(cudaMemcpy(p->h_down.p, down, H * Dm * 4, cudaMemcpyHostToDevice));
+    NGH_CUDA(cudaMemcpy(p->h_x.p, x, size_t(T) * Dm * 4, cudaMemcpyHostToDevice));
+    NGH_CUDA(cudaMemcpy(p->h_tok.p, tokens, size_t(T) * 4, cudaMemcpyHostToDevice));
+    NGH_CUDA(cudaMemcpy(p->h_off.p, off, size_t(nseq + 1) * 8, cudaMemcpyHostToDevice));
+    if (prior && N1 > 0) {
+        p->h_prior.ensure(size_t(nseq) * size_t(N1));
+        NGH_CUDA(cudaMemcpy(p->h_prior.p, prior, size_t(nseq) * size_t(N1) * 4, cudaMemcpyHostToDevice));
+    }
+}
+
+static void check_host_offsets(const int64_t* off, int64_t nseq) {
+    if (off[0] != 0) throw Error(NGRAM_EINVAL, "seq_offsets must start at 0");
+    for (int64_t i = 0; i < nseq; ++i)
+        if (off[i + 1] < off[i]) throw Error(NGRAM_EINVAL, "seq_offsets must be non-decreasing");
+}
+
+static void raise_token_error(ngram_bank* b) {
+    unsigned long long e = 0;
+    NGH_CUDA(cudaMemcpy(&e, b->err.p, sizeof(e), cudaMemcpyDeviceToHost));
+    if (e != ~0ull)
+        throw Error(NGRAM_ERANGE, "embedding: token out of range for base vocabulary " +
+                                      std::to_string(b->cfg.base_vocab) + " (first bad window at position " +
+                                      std::to_string(e) + ")");
+}
+
+int ngram_plne_forward_host(ngram_plne* p, const float* gate, const float* down, const float* x,
+                            const uint32_t* tokens, const int64_t* seq_offsets, int64_t nseq, const uint32_t* prior,
+                            float* y) {
+    NGRAM_API_BEGIN
+    if (!p || !seq_offsets || nseq < 1) throw Error(NGRAM_EINVAL, "ngram_plne_forward_host: bad argument");
+    check_host_offsets(seq_offsets, nseq);
+    const int64_t T = seq_offsets[nseq];
+    if (T == 0) return NGRAM_OK;
+    if (!gate || !down || !x || !tokens || !y) throw Error(NGRAM_EINVAL, "ngram_plne_forward_host: bad argument");
+    DeviceGuard dg(p->bank->device);
+    stage_common(p, gate, down, x, tokens, seq_offsets, nseq, T, prior);
+    const size_t Dm = size_t(p->d_model);
+    p->h_y.ensure(size_t(T) * Dm);
+    const int N1 = std::max(p->bank->cfg.max_order - 1, 0);
+    status_ok(ngram_plne_forward(p, p->h_gate.p, p->h_down.p, p->h_x.p, p->h_tok.p, p->h_off.p, nseq, T,
+                                 (prior && N1 > 0) ? p->h_prior.p : nullptr, p->h_y.p, nullptr));
+    raise_token_error(p->bank);
+    NGH_CUDA(cudaMemcpy(y, p->h_y.p, size_t(T) * Dm * 4, cudaMemcpyDeviceToHost));
+    NGRAM_API_END
+}
+
+int ngram_plne_backward_host(ngram_plne* p, ngram_grad* bank_grads, const float* gate, const float* down,
+                             const float* x, const uint32_t* tokens, const int64_t* seq_offsets, int64_t nseq,
+                             const uint32_t* prior, const float* upstream, float* d_gate, float* d_down, float* dx) {
+    NGRAM_API_BEGIN
+    if (!p || !seq_offsets || nseq < 1) throw Error(NGRAM_EINVAL, "ngram_plne_backward_host: bad argument");
+    check_host_offsets(seq_offsets, nseq);
+    const int64_t T = seq_offsets[nseq];
+    if (T == 0) return NGRAM_OK;
+    if (!gate || !down || !x || !tokens || !upstream || !d_gate || !d_down || !dx)
+        throw Error(NGRAM_EINVAL, "ngram_plne_backward_host: bad argument");
+    DeviceGuard dg(p->bank->device);
+    stage_common(p, gate, down, x, tokens, seq_offsets, nseq, T, prior);
+    const size_t H = size_t(p->hidden), Dm = size_t(p->d_model), n = size_t(T) * Dm;
+    p->h_up.ensure(n);
+    p->h_dx.ensure(n);
+    p->h_dgate.ensure(H * Dm);
+    p->h_ddown.ensure(H * Dm);
+    NGH_CUDA(cudaMemcpy(p->h_up.p, upstream, n * 4, cudaMemcpyHostToDevice));
+    NGH_CUDA(cudaMemcpy(p->h_dx.p, dx, n * 4, cudaMemcpyHostToDevice));  // accumulated on the device
+    NGH_CUDA(cudaMemcpy(p->h_dgate.p, d_gate, H * Dm * 4, cudaMemcpyHostToDevice));
+    NGH_CUDA(cudaMemcpy(p->h_ddown.p, d_down, H * Dm * 4, cudaMemcpyHostToDevice));
+    const int N1 = std::max(p->bank->cfg.max_order - 1, 0);
+    status_ok(ngram_plne_backward(p, bank_grads, p->h_gate.p, p->h_down.p, p->h_x.p, p->h_tok.p, p->h_off.p, nseq, T,
+                                  (prior && N1 > 0) ? p->h_prior.p : nullptr, p->h_up.p, p->h_dgate.p, p->h_ddown.p,
+                                  p->h_dx.p, nullptr));
+    raise_token_error(p->bank);
+    NGH_CUDA(cudaMemcpy(dx, p->h_dx.p, n * 4, cudaMemcpyDeviceToHost));
+    NGH_CUDA(cudaMemcpy(d_gate, p->h_dgate.p, H * Dm * 4, cudaMemcpyDeviceToHost));
+    NGH_CUDA(cudaMemcpy(d_down, p->h_ddown.p, H * Dm * 4, cudaMemcpyDeviceToHost));
     NGRAM_API_END
 }
 

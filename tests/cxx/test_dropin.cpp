@@ -5,6 +5,7 @@
 // run by tests/test_gpu_dropin.py.
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <functional>
 #include <string>
 #include <vector>
@@ -12,6 +13,7 @@
 #include "ngram/cache.hpp"
 #include "ngram/config.hpp"
 #include "ngram/embedding.hpp"
+#include "ngram/ple.hpp"
 #include "ngram/hashing.hpp"
 
 using namespace ngram;
@@ -286,6 +288,135 @@ int main() {
         const auto before = a.base;
         CHECK_THROWS_AS(embed_sequence_backward(bad, bank, fwd.merged, up, a), std::out_of_range);
         CHECK(a.base == before);
+    });
+    // ---- per-layer FFN (test_ple.cpp:60-200, float + bf16-representable tables)
+    auto bf16 = [](std::vector<float>& v) {
+        for (auto& x : v) {
+            std::uint32_t u;
+            std::memcpy(&u, &x, 4);
+            u = (u + 0x7fffu + ((u >> 16) & 1u)) & 0xffff0000u;
+            std::memcpy(&x, &u, 4);
+        }
+    };
+    auto layer_config = [](std::uint32_t v0, int width, int order, int k) {  // test_ple.cpp:43-57
+        ngram_config cfg;
+        cfg.max_order = order;
+        cfg.sub_tables = k;
+        cfg.base_vocab = v0;
+        cfg.dim = width;
+        cfg.variant = ne_variant::subtable_v2;
+        cfg.amplification = amp_mode::none;
+        for (int n = 2; n <= order; ++n)
+            for (int kk = 1; kk <= k; ++kk) cfg.sub_vocab[{n, kk}] = 19 + 6 * std::uint64_t(n) + std::uint64_t(kk);
+        cfg.validate();
+        return cfg;
+    };
+    test_case("ffn_ple: zero input / zero table row give zero output", [&] {
+        auto p = make_ple_params<float>(4, 6, 10, 1);
+        bf16(p.table);
+        std::vector<float> x(4, 0.0f);
+        for (const float y : ffn_ple(x, 3, p)) CHECK(y == 0.0f);
+        std::fill(p.table.begin() + 3 * 6, p.table.begin() + 4 * 6, 0.0f);
+        rng64 rng(4);
+        for (auto& v : x) v = float(gaussian(rng));
+        for (const float y : ffn_ple(x, 3, p)) CHECK(y == 0.0f);
+    });
+    test_case("ffn_ple matches the straight-line oracle; rejects bad tokens / shapes", [&] {
+        auto p = make_ple_params<float>(4, 6, 10, 7);
+        bf16(p.table);
+        rng64 rng(8);
+        for (int trial = 0; trial < 20; ++trial) {
+            std::vector<float> x(4);
+            for (auto& v : x) v = float(gaussian(rng));
+            const token_id t = token_id(uniform_below(rng, 10));
+            const auto got = ffn_ple(x, t, p);
+            std::vector<float> want(4);
+            std::vector<double> h(6);
+            for (int r = 0; r < 6; ++r) {
+                double u = 0;
+                for (int c = 0; c < 4; ++c) u += double(p.gate[r * 4 + c]) * x[c];
+                h[r] = u / (1.0 + std::exp(-u)) * p.table[t * 6 + r];
+            }
+            for (int r = 0; r < 4; ++r) {
+                double acc = 0;
+                for (int c = 0; c < 6; ++c) acc += double(p.down[r * 6 + c]) * h[c];
+                want[r] = float(acc);
+            }
+            CHECK(close_rows(got, want, 1e-5));
+        }
+        std::vector<float> x(4, 0.1f), short_x(3, 0.1f);
+        CHECK_THROWS_AS(ffn_ple(x, 10, p), std::out_of_range);
+        CHECK_THROWS_AS(ffn_ple(short_x, 2, p), std::invalid_argument);
+    });
+    test_case("ffn_plne: zero bank, all-pad context = ffn_ple / denom, base-only bank = ffn_ple", [&] {
+        const auto cfg = layer_config(10, 6, 3, 3);
+        auto p = make_ple_params<float>(4, 6, 10, 5);
+        bf16(p.table);
+        rng64 rng(9);
+        std::vector<float> x(4);
+        for (auto& v : x) v = float(gaussian(rng));
+        std::vector<token_id> ctx{1, 2, 3}, pads{0, 0, 0};
+        for (const float y : ffn_plne(x, ctx, make_zero_bank<float>(cfg), p)) CHECK(y == 0.0f);
+        auto bank = make_zero_bank<float>(cfg);
+        bank.base = p.table;
+        const auto plne = ffn_plne(x, pads, bank, p);
+        auto ple = ffn_ple(x, 0, p);
+        for (auto& v : ple) v /= float(cfg.merge_denominator());
+        CHECK(close_rows(plne, ple, 1e-5));
+        ngram_config c1;
+        c1.max_order = 1;
+        c1.sub_tables = 1;
+        c1.base_vocab = 10;
+        c1.dim = 6;
+        c1.variant = ne_variant::subtable_v2;
+        c1.validate();
+        auto b1 = make_zero_bank<float>(c1);
+        b1.base = p.table;
+        const device_bank d1(b1);
+        for (token_id t = 0; t < 10; ++t) {
+            const token_id one[1] = {t};
+            CHECK(ffn_plne(x, one, d1, p) == ffn_ple(x, t, p));
+        }
+        CHECK_THROWS_AS(ffn_plne(x, ctx, make_bank<float>(layer_config(10, 8, 3, 2), 2), p), std::invalid_argument);
+    });
+    test_case("ffn_plne_backward: dx matches finite differences; ffn_ple_backward == base-only plne", [&] {
+        const auto cfg = layer_config(10, 8, 3, 2);
+        auto host = make_bank<float>(cfg, 3);
+        for (auto* v : {&host.base}) bf16(*v);
+        for (auto& t : host.sub_tables) bf16(t);
+        for (auto& w : host.projections) bf16(w);
+        const device_bank bank(host);
+        auto p = make_ple_params<float>(5, 8, 10, 6);
+        rng64 rng(12);
+        std::vector<float> x(5), u(5);
+        for (auto& v : x) v = float(gaussian(rng));
+        for (auto& v : u) v = float(gaussian(rng));
+        std::vector<token_id> ctx{4, 7, 1};
+        auto grads = ple_zeros_like(p);
+        auto bg = zeros_like(host);
+        std::vector<float> dx(5, 0.0f);
+        ffn_plne_backward(x, ctx, bank, p, u, grads, bg, dx);
+        for (int c = 0; c < 5; ++c) {
+            auto xp = x, xm = x;
+            xp[c] += 1e-2f;
+            xm[c] -= 1e-2f;
+            const auto yp = ffn_plne(xp, ctx, bank, p), ym = ffn_plne(xm, ctx, bank, p);
+            double fd = 0;
+            for (int r = 0; r < 5; ++r) fd += double(u[r]) * (double(yp[r]) - double(ym[r])) / 2e-2;
+            CHECK(std::fabs(fd - dx[c]) <= 1e-3 * std::max(1.0, std::fabs(fd)) + 1e-6);
+        }
+        bool any = false;
+        for (const float v : bg.base) any = any || v != 0.0f;
+        CHECK(any);
+        auto p2 = make_ple_params<float>(4, 6, 10, 7);
+        bf16(p2.table);
+        auto g1 = ple_zeros_like(p2);
+        std::vector<float> x2(4, 0.3f), u2(4, 1.0f), d1(4, 0.0f);
+        ffn_ple_backward(x2, 2, p2, u2, g1, d1);
+        bool row = false;
+        for (int i = 0; i < 6; ++i) row = row || g1.table[2 * 6 + i] != 0.0f;
+        CHECK(row);
+        CHECK(g1.table[3 * 6] == 0.0f);
     });
     std::printf("%d checks, %d failures\n", g_checks, g_fail);
     return g_fail == 0 ? 0 : 1;
