@@ -141,10 +141,16 @@ void ensure_workspace(ngram_bank* b, int64_t T);
 
 // Forward building blocks shared by forward.cpp / decode.cpp / shard.cpp.
 void reset_error_word(ngram_bank* b, cudaStream_t st);
+// Windows of the call's tokens for kernels that hash on the fly (small-T MODE 2 GEMM).
+struct HashCtx {
+    const int64_t* seq_off;
+    int64_t nseq;
+    const uint32_t* prior;
+};
 void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, int64_t gstride, int64_t T,
                     void* rows, void* merged, int out_bf16, float* ln_scratch, const CUtensorMap* tmap_x,
                     cudaStream_t st, int amp, XBuf* xb, bool allow_splitk, const ngk::FusedX* fx,
-                    const ngk::DecodeCommit* commit, int64_t x_row0 = 0);
+                    const ngk::DecodeCommit* commit, int64_t x_row0 = 0, const HashCtx* hc = nullptr);
 bool forward_tokens(ngram_bank* b, const uint32_t* tokens, const int64_t* seq_off, int64_t nseq, int64_t T,
                     const uint32_t* prior, void* rows, void* merged, int out_bf16, cudaStream_t st, int amp,
                     XBuf* xb, int32_t* grow, bool allow_splitk, const ngk::DecodeCommit* commit);

@@ -65,13 +65,24 @@ static int overlap_chunks(ngram_bank* b, int64_t T) {
     return env;
 }
 
+// Small-T split-K GEMM with the hash in its producers (MODE 2), opt-in NGRAM_DECODE_HASH_IN_GEMM=1:
+// measured 2x slower than gather kernel + GEMM on X (every split's 24 n-tile CTAs re-gather
+// the same rows through L2 one K-block at a time, behind a window-load + hash prologue).
+static bool hash_in_gemm(const ngram_bank* b) {
+    static const bool env = getenv("NGRAM_DECODE_HASH_IN_GEMM") && atoi(getenv("NGRAM_DECODE_HASH_IN_GEMM")) != 0;
+    if (!env || b->shape.N > 8 || b->shape.variant != 1) return false;
+    ngk::FwdArgs a{};
+    a.s = b->shape;
+    return ngk::splitk_factor(a, b->num_sms) > 1;
+}
+
 // One forward over T rows whose storage rows are already in `grow` (stride gstride).
 // Tensor-core path: K2 gathers X (T x D bf16) into `xb`, K3 projects it.  Writes
 // merged/rows per the amplification; LayerNorm via a third kernel.
 void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, int64_t gstride, int64_t T,
                     void* rows, void* merged, int out_bf16, float* ln_scratch, const CUtensorMap* tmap_x,
                     cudaStream_t st, int amp, XBuf* xb, bool allow_splitk, const ngk::FusedX* fx,
-                    const ngk::DecodeCommit* commit, int64_t x_row0) {
+                    const ngk::DecodeCommit* commit, int64_t x_row0, const HashCtx* hc) {
     if (b->hash_only) throw Error(NGRAM_EINVAL, "bank was created hash-only (NGRAM_BANK_HASH_ONLY)");
     if (b->tc_path && ((reinterpret_cast<uintptr_t>(rows) | reinterpret_cast<uintptr_t>(merged)) & 15) != 0)
         throw Error(NGRAM_EINVAL, "output buffers must be 16-byte aligned (tensor-core path: vector / TMA stores)");
@@ -108,7 +119,11 @@ void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, 
         a.rows_out = rows;
         a.out_bf16 = out_bf16;
     }
-    if (b->tc_path && !tmap_x && ((allow_splitk && T <= 256) || !fused_gather(b->shape.D))) {
+    if (hc) {  // the GEMM producers hash and gather the rows themselves
+        a.seq_off = hc->seq_off;
+        a.nseq = hc->nseq;
+        a.prior = hc->prior;
+    } else if (b->tc_path && !tmap_x && ((allow_splitk && T <= 256) || !fused_gather(b->shape.D))) {
         if (!xb) xb = &b->ws.xbuf;
         xb->ensure(round_up(T, kRowPad), b->shape.D);
         ngk::launch_gather_rows(a.s, grow, gstride, T, b->sub.p, xb->x.p, b->err.p, st);
@@ -171,6 +186,13 @@ bool forward_tokens(ngram_bank* b, const uint32_t* tokens, const int64_t* seq_of
         ngk::FusedX fx{seq_off, nseq, prior, xb->x.p, b->ws.ready.p};
         run_projection(b, tokens, nullptr, Tpad, T, rows, merged, out_bf16, b->ws.merged_f32.p, &xb->map, st, amp,
                        nullptr, false, &fx, nullptr);
+    } else if (b->tc_path && allow_splitk && T <= 256 && hash_in_gemm(b)) {
+        // decode / verify: K1 fused into the split-K GEMM's producers (2 launches per step)
+        b->prof_record(1, st);
+        fused_commit = commit != nullptr;
+        const HashCtx hc{seq_off, nseq, prior};
+        run_projection(b, tokens, nullptr, Tpad, T, rows, merged, out_bf16, b->ws.merged_f32.p, nullptr, st, amp,
+                       nullptr, true, nullptr, fused_commit ? commit : nullptr, 0, &hc);
     } else if (b->tc_path && ((allow_splitk && T <= 256) || !fused_gather(b->shape.D))) {
         if (!xb) xb = &b->ws.xbuf;
         xb->ensure(Tpad, b->shape.D);

@@ -41,6 +41,7 @@ constexpr int BM = 128;
 constexpr int BK = 64;  // one SWIZZLE_128B atom of bf16
 constexpr int kStages = 4;
 constexpr int kLag = 2;  // cp.async mode: K-blocks in flight per producer warp before retiring
+constexpr int kMaxDecodeN = 8;  // MODE 2 (hash in the producer): max_order <= 8
 
 template <int BN, int NP>
 struct Cfg {
@@ -125,7 +126,7 @@ __global__ void __launch_bounds__(Cfg<BN, NP>::kThreads, 1)
 
     if (warp == 0 && lane == 0) {
         // full: one arrive per producer warp (+1 for the W TMA in cp.async mode), or one in X mode
-        const uint32_t full_count = p.use_x ? 1u : (MODE == 0 ? (uint32_t)NP : (uint32_t)NP + 1);
+        const uint32_t full_count = p.use_x ? 1u : (MODE != 1 ? (uint32_t)NP : (uint32_t)NP + 1);
         for (int i = 0; i < kStages; ++i) {
             mbar_init(&full[i], full_count);
             mbar_init(&empty[i], 1);
@@ -164,6 +165,59 @@ __global__ void __launch_bounds__(Cfg<BN, NP>::kThreads, 1)
                         tma_load_2d_hint(a_dst + C::kABytes, &tmap_w, &full[stage], kb * BK, n * BN, pol_w);
                     }
                     __syncwarp();
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        } else if (MODE == 2) {
+            // Small-T split-K with K1 fused into the producer: each lane of a producer warp
+            // hashes 4 of the warp's 32 tile rows for the branch its K-blocks belong to and
+            // gathers them with tile::gather4 straight from the sub-tables (no X round trip,
+            // no separate gather launch).  Rows past T gather row 0 (never stored); a bad
+            // window sets the error word, which the reduce kernel checks before any output.
+            const int r0 = warp * C::kRowsPerWarp;
+            for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+                const int64_t mn = tile % (nM * nN);
+                const int ks = (int)(tile / (nM * nN));
+                const int64_t m = mn / nN;
+                const int n = (int)(mn - m * nN);
+                uint32_t win[4][kMaxDecodeN];
+                bool ok[4];
+                if (lane < C::kRowsPerWarp / 4) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int64_t t = m * BM + r0 + 4 * lane + i;
+                        ok[i] = t < p.T && load_window<kMaxDecodeN>(p.s, p.tokens, p.seq_off, p.nseq, p.prior, t,
+                                                                     win[i]);
+                        if (t < p.T && !ok[i]) atomicMin(const_cast<unsigned long long*>(p.err),
+                                                         (unsigned long long)t);
+                    }
+                }
+                int cur_b = -1;
+                int4 rows4 = make_int4(0, 0, 0, 0);
+                for (int kb = ks * KB; kb < (ks + 1) * KB; ++kb) {
+                    const int b = kb / KPB, c = kb - b * KPB;
+                    if (b != cur_b && lane < C::kRowsPerWarp / 4) {
+                        int r[4];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            r[i] = ok[i] ? storage_row(p.ht, b, branch_hash<kMaxDecodeN>(p.s, p.ht, win[i], b), nullptr)
+                                         : 0;
+                        rows4 = make_int4(r[0], r[1], r[2], r[3]);
+                    }
+                    cur_b = b;
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t* a_dst = smem + stage * C::kStageBytes;
+                    if (lane == 0)
+                        mbar_arrive_expect_tx(&full[stage], (warp == 0 ? C::kBBytes : 0) + C::kRowsPerWarp * BK * 2);
+                    __syncwarp();
+                    if (lane < C::kRowsPerWarp / 4)
+                        tma_gather4(a_dst + (r0 + 4 * lane) * (BK * 2), &tmap_a, &full[stage], c * BK, rows4.x,
+                                    rows4.y, rows4.z, rows4.w);
+                    if (warp == 0 && lane == 0)
+                        tma_load_2d_hint(a_dst + C::kABytes, &tmap_w, &full[stage], kb * BK, n * BN, pol_w);
                     if (++stage == kStages) {
                         stage = 0;
                         phase ^= 1;
@@ -839,6 +893,10 @@ void launch_cfg(const FwdArgs& a, int num_sms, cudaStream_t st, int ksplit = 1, 
     p.x_row0 = a.x_row0;
     p.epi_skip = getenv("NGRAM_DEBUG_EPI_SKIP") ? atoi(getenv("NGRAM_DEBUG_EPI_SKIP")) : 0;
     p.diag_skip_a = getenv("NGRAM_DEBUG_SKIP_A") ? 1 : 0;
+    p.ht = a.ht;
+    p.seq_off = a.seq_off;
+    p.nseq = a.nseq;
+    p.prior = a.prior;
     const int64_t tiles = ((a.T + BM - 1) / BM) * (a.s.D / BN) * ksplit;
     int grid = (int)(tiles < num_sms ? tiles : num_sms);
     if (grid < 1) grid = 1;
@@ -1031,7 +1089,7 @@ static bool decode_cluster() {
 }
 
 size_t splitk_workspace_floats(const FwdArgs& a, int num_sms) {
-    if (a.T > 256 || a.tmap_x == nullptr) return 0;
+    if (a.T > 256 || (a.tmap_x == nullptr && a.seq_off == nullptr)) return 0;
     if (decode_cluster()) return decode_gemm_workspace_floats(a.s.D, num_sms);
     const int S = splitk_factor(a, num_sms);
     return S > 1 ? (size_t)S * (size_t)a.T * (size_t)a.s.D : 0;
@@ -1043,10 +1101,11 @@ void launch_forward_tc(const FwdArgs& a, int num_sms, cudaStream_t st, float* sp
         launch_decode_gemm(a, num_sms, splitk_ws, a.commit, st);
         return;
     }
-    if (splitk_ws && a.T <= 256 && a.tmap_x != nullptr) {
+    if (splitk_ws && a.T <= 256 && (a.tmap_x != nullptr || a.seq_off != nullptr)) {
         const int S = splitk_factor(a, num_sms);
         if (S > 1) {
-            launch_cfg<128, 4, 0>(a, num_sms, st, S, splitk_ws);
+            if (a.tmap_x) launch_cfg<128, 4, 0>(a, num_sms, st, S, splitk_ws);  // A from X
+            else launch_cfg<128, 4, 2>(a, num_sms, st, S, splitk_ws);           // hash + gather4 in-kernel
             const float scale = 1.0f / (float)a.s.denom;
             const float amp = a.s.amp == kAmpSqrt ? (float)__builtin_sqrt((double)a.s.D) : 1.0f;
             const int64_t n4 = a.T * a.s.D / 4;

@@ -116,6 +116,11 @@ struct FwdArgs {
     const CUtensorMap* tmap_rows_out;
     const CUtensorMap* tmap_merged_out;
     const CUtensorMap* tmap_e0;
+    // small-T split-K with the hash fused into the GEMM producer (MODE 2): the windows of
+    // `tokens` (seq_off / nseq / prior as ngram_embed_forward); null seq_off = not used
+    const int64_t* seq_off;
+    int64_t nseq;
+    const uint32_t* prior;
 };
 // K1 + K2 + K3 in ONE persistent 2-CTA kernel: gather warps hash and gather X rows ahead
 // of the MMA pipeline (per-128-row ready counters), overlapping the HBM-bound gather with
@@ -132,6 +137,7 @@ void launch_forward_tc2_fusedx(const FwdArgs& a, const FusedX& fx, int num_sms, 
 // splitk_ws (fp32, splitk_workspace_floats() long, may be null): small-T split-K path.
 void launch_forward_tc(const FwdArgs& a, int num_sms, cudaStream_t st, float* splitk_ws = nullptr);
 size_t splitk_workspace_floats(const FwdArgs& a, int num_sms);
+int splitk_factor(const FwdArgs& a, int num_sms);  // small-T split: depends on D (and the SM count) only
 // generic CUDA-core path: any shape, v1 and v2, reference float op order (simt.cu).
 void launch_forward_simt(const FwdArgs& a, cudaStream_t st);
 // K2 standalone: materialise X (T x D bf16) from the storage rows (d % 8 == 0).
