@@ -153,7 +153,8 @@ void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, 
                     const ngk::DecodeCommit* commit, int64_t x_row0 = 0, const HashCtx* hc = nullptr);
 bool forward_tokens(ngram_bank* b, const uint32_t* tokens, const int64_t* seq_off, int64_t nseq, int64_t T,
                     const uint32_t* prior, void* rows, void* merged, int out_bf16, cudaStream_t st, int amp,
-                    XBuf* xb, int32_t* grow, bool allow_splitk, const ngk::DecodeCommit* commit);
+                    XBuf* xb, int32_t* grow, bool allow_splitk, const ngk::DecodeCommit* commit,
+                    int64_t uniform_len = 0);
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 // Row padding of every per-token workspace: the 2-CTA GEMM tile is 256 tokens.
 constexpr int64_t kRowPad = 256;

@@ -30,7 +30,7 @@ bool decode_block(ngram_decode* d, const uint32_t* draft, int L, uint64_t* ids_o
                              nullptr, Tpad, b->err.p, st);
     if (merged_out)
         return forward_tokens(b, draft, off, d->batch, T, R > 0 ? d->ring.p : nullptr, nullptr, merged_out,
-                              out_dtype == NGRAM_BF16, st, 0, &d->xbuf, d->grow.p, true, commit);
+                              out_dtype == NGRAM_BF16, st, 0, &d->xbuf, d->grow.p, true, commit, L);
     return false;
 }
 

@@ -65,6 +65,8 @@ static int overlap_chunks(ngram_bank* b, int64_t T) {
     return env;
 }
 
+static bool small_t(const ngram_bank* b, int64_t T) { return ngk::small_t_regime(b->shape.D, T, b->num_sms); }
+
 // Small-T split-K GEMM with the hash in its producers (MODE 2), opt-in NGRAM_DECODE_HASH_IN_GEMM=1:
 // measured 2x slower than gather kernel + GEMM on X (every split's 24 n-tile CTAs re-gather
 // the same rows through L2 one K-block at a time, behind a window-load + hash prologue).
@@ -123,7 +125,7 @@ void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, 
         a.seq_off = hc->seq_off;
         a.nseq = hc->nseq;
         a.prior = hc->prior;
-    } else if (b->tc_path && !tmap_x && ((allow_splitk && T <= 256) || !fused_gather(b->shape.D))) {
+    } else if (b->tc_path && !tmap_x && ((allow_splitk && small_t(b, T)) || !fused_gather(b->shape.D))) {
         if (!xb) xb = &b->ws.xbuf;
         xb->ensure(round_up(T, kRowPad), b->shape.D);
         ngk::launch_gather_rows(a.s, grow, gstride, T, b->sub.p, xb->x.p, b->err.p, st);
@@ -132,7 +134,7 @@ void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, 
     b->prof_record(2, st);
     // output maps for the pair kernel's TMA epilogue (prefill tiling: not the split-K path)
     CUtensorMap map_rows, map_merged;
-    if (b->tc_path && b->shape.D % 256 == 0 && (T > 256 || !allow_splitk)) {
+    if (b->tc_path && b->shape.D % 256 == 0 && (!small_t(b, T) || !allow_splitk)) {
         const uint64_t D = uint64_t(b->shape.D);
         const bool f32 = !a.out_bf16;
         const uint64_t pitch = D * (f32 ? 4 : 2);
@@ -170,7 +172,8 @@ void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, 
 // Returns true when `commit` was fused into the projection (decode GEMM path).
 bool forward_tokens(ngram_bank* b, const uint32_t* tokens, const int64_t* seq_off, int64_t nseq, int64_t T,
                     const uint32_t* prior, void* rows, void* merged, int out_bf16, cudaStream_t st, int amp,
-                    XBuf* xb, int32_t* grow, bool allow_splitk, const ngk::DecodeCommit* commit) {
+                    XBuf* xb, int32_t* grow, bool allow_splitk, const ngk::DecodeCommit* commit,
+                    int64_t uniform_len) {
     bool fused_commit = false;
     const int64_t Tpad = round_up(std::max<int64_t>(T, 1), kRowPad);
     b->prof_record(0, st);
@@ -186,14 +189,14 @@ bool forward_tokens(ngram_bank* b, const uint32_t* tokens, const int64_t* seq_of
         ngk::FusedX fx{seq_off, nseq, prior, xb->x.p, b->ws.ready.p};
         run_projection(b, tokens, nullptr, Tpad, T, rows, merged, out_bf16, b->ws.merged_f32.p, &xb->map, st, amp,
                        nullptr, false, &fx, nullptr);
-    } else if (b->tc_path && allow_splitk && T <= 256 && hash_in_gemm(b)) {
+    } else if (b->tc_path && allow_splitk && T <= 256 && hash_in_gemm(b)) {  // MODE 2: T <= 256 only
         // decode / verify: K1 fused into the split-K GEMM's producers (2 launches per step)
         b->prof_record(1, st);
         fused_commit = commit != nullptr;
         const HashCtx hc{seq_off, nseq, prior};
         run_projection(b, tokens, nullptr, Tpad, T, rows, merged, out_bf16, b->ws.merged_f32.p, nullptr, st, amp,
                        nullptr, true, nullptr, fused_commit ? commit : nullptr, 0, &hc);
-    } else if (b->tc_path && ((allow_splitk && T <= 256) || !fused_gather(b->shape.D))) {
+    } else if (b->tc_path && ((allow_splitk && small_t(b, T)) || !fused_gather(b->shape.D))) {
         if (!xb) xb = &b->ws.xbuf;
         xb->ensure(Tpad, b->shape.D);
         const int nchunk = overlap_chunks(b, T);
@@ -229,7 +232,7 @@ bool forward_tokens(ngram_bank* b, const uint32_t* tokens, const int64_t* seq_of
         }
         if (T <= 1024)
             ngk::launch_hash_gather_rows(b->shape, b->ht.p, tokens, seq_off, nseq, T, prior, b->sub.p, xb->x.p,
-                                         b->err.p, st);
+                                         b->err.p, st, uniform_len);
         else
             ngk::launch_hash_gather(b->shape, b->ht.p, tokens, seq_off, nseq, T, prior, b->sub.p, xb->x.p, nullptr,
                                     Tpad, b->err.p, st);
@@ -448,7 +451,7 @@ int ngram_embed_sequence_host(ngram_bank* b, const uint32_t* tokens, const int64
         void* dmerged = merged_out ? b->host_merged[slot].p : nullptr;
         run_projection(b, b->ws.tokens.p + c0, b->ws.grow.p + c0, Tpad, n, drows, dmerged, out_dtype == NGRAM_BF16,
                        b->ws.merged_f32.p ? b->ws.merged_f32.p + size_t(c0) * size_t(D) : nullptr, nullptr, st, -1,
-                       &b->host_x[slot], T <= 256, nullptr, nullptr);  // chunks keep the whole batch's regime
+                       &b->host_x[slot], small_t(b, T), nullptr, nullptr);  // chunks keep the batch's regime
         const size_t bytes = size_t(n) * size_t(D) * esz;
         if (direct) {
             if (rows_out)

@@ -74,6 +74,7 @@ struct TcParams {
     int epi_skip;  // diagnostics only (NGRAM_DEBUG_EPI_SKIP): 1 drain TMEM without loads/stores,
                    // 2 (pair kernel) skip the E0 loads, 3 (pair kernel) skip the output stores
     int diag_skip_a;  // diagnostics only (NGRAM_DEBUG_SKIP_A): X-path pair kernel loads W tiles only
+    int pdl;          // launched with programmatic stream serialization (decode chain)
     int ksplit;      // split-K factor (small-T path); >1 => raw fp32 partials to `partial`
     float* partial;  // [ksplit][T][D] fp32
     // fused K1+K2 (forward_tc2_kernel<true>): gather warps fill X, producers wait on `ready`
@@ -112,7 +113,9 @@ __global__ void __launch_bounds__(Cfg<BN, NP>::kThreads, 1)
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
-    if (*p.err != ~0ull) return;  // a token was out of range: produce no output (uniform)
+    // PDL launch (decode chain): the set-up below overlaps the previous kernel's tail; the
+    // error word and X are read only after griddep_wait.
+    if (!p.pdl && *p.err != ~0ull) return;  // a token was out of range: produce no output (uniform)
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
@@ -144,6 +147,14 @@ __global__ void __launch_bounds__(Cfg<BN, NP>::kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (p.pdl) {
+        griddep_launch_dependents();  // the reduce kernel may launch and park in its own wait
+        griddep_wait();               // gather kernel done: X and the error word are final
+        if (*p.err != ~0ull) {        // uniform: release TMEM, produce nothing
+            if (warp == C::kMmaWarp) tmem_dealloc<C::kTmemCols>(tmem_base);
+            return;
+        }
+    }
 
     if (warp < NP) {
         // ------------------------------------------------------------ producers
@@ -870,9 +881,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FX ? Cfg2::kThreadsF
 }
 
 template <int BN, int NP, int MODE>
-void launch_cfg(const FwdArgs& a, int num_sms, cudaStream_t st, int ksplit = 1, float* partial = nullptr) {
+void launch_cfg(const FwdArgs& a, int num_sms, cudaStream_t st, int ksplit = 1, float* partial = nullptr,
+                bool pdl = false) {
     using C = Cfg<BN, NP>;
-    TcParams p;
+    TcParams p{};
     p.ksplit = ksplit;
     p.partial = partial;
     p.s = a.s;
@@ -903,8 +915,23 @@ void launch_cfg(const FwdArgs& a, int num_sms, cudaStream_t st, int ksplit = 1, 
     // the W box must match BN rows: tmap_w2 always has a 128-row box, tmap_w has BN(D) rows
     const CUtensorMap* wmap = (BN == 128) ? a.tmap_w2 : a.tmap_w;
     cudaFuncSetAttribute(forward_tc_kernel<BN, NP, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-    forward_tc_kernel<BN, NP, MODE><<<grid, C::kThreads, C::kSmemBytes, st>>>(a.tmap_x ? *a.tmap_x : *a.tmap_sub,
-                                                                              *wmap, p);
+    p.pdl = pdl ? 1 : 0;
+    if (pdl) {  // programmatic stream serialization: set-up overlaps the gather kernel's tail
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)grid);
+        cfg.blockDim = dim3(C::kThreads);
+        cfg.dynamicSmemBytes = C::kSmemBytes;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, forward_tc_kernel<BN, NP, MODE>, a.tmap_x ? *a.tmap_x : *a.tmap_sub, *wmap, p);
+    } else {
+        forward_tc_kernel<BN, NP, MODE><<<grid, C::kThreads, C::kSmemBytes, st>>>(
+            a.tmap_x ? *a.tmap_x : *a.tmap_sub, *wmap, p);
+    }
     count_launch();
 }
 
@@ -917,7 +944,7 @@ int tma_epi_mode() {
 }
 
 void launch_tc2(const FwdArgs& a, int num_sms, cudaStream_t st) {
-    TcParams p;
+    TcParams p{};
     p.ksplit = 1;
     p.partial = nullptr;
     p.s = a.s;
@@ -1006,6 +1033,7 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
                                                             float amp, int write_rows, void* rows, void* merged,
                                                             int out_bf16, const unsigned long long* err,
                                                             DecodeCommit commit) {
+    griddep_wait();  // PDL launch: the split-K GEMM has completed (no-op for a normal launch)
     if (commit.ring && blockIdx.x == 0) decode_commit_block(commit, err);  // fused decode-state commit
     if (*err != ~0ull) return;
     const int64_t n4 = T * D / 4;
@@ -1040,16 +1068,29 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
     }
 }
 
-int splitk_factor(const FwdArgs& a, int num_sms) {
-    // small-T path: BN = 128 tiles; split K until one m-tile's grid covers the SMs.  S
-    // depends on D only, so every row of every T <= 256 call is computed identically
-    // (batch-composition invariance within the small-T regime).
-    const int KB = a.s.D / BK;
-    const int64_t nN = a.s.D / 128;
+static int split_s1(int D, int num_sms) {
+    // BN = 128 tiles; split K until one m-tile's grid covers the SMs
+    const int KB = D / BK;
+    const int64_t nN = D / 128;
     int best = 1;
     for (int S = 1; S <= KB; ++S)
         if (KB % S == 0 && nN * S <= num_sms) best = S;
     return best;
+}
+
+bool small_t_regime(int D, int64_t T, int num_sms) {
+    // A verify-sized middle regime (256 < T <= 1024, fewer splits) was measured slower than
+    // the pair kernel at D = 3072 (64 x 8 verify: 36.9 vs 34.9 us), so the split-K GEMM
+    // serves T <= 256 only.
+    (void)D;
+    (void)num_sms;
+    return T <= 256;
+}
+
+int splitk_factor(const FwdArgs& a, int num_sms) {
+    // S depends only on D and the regime of T, so every row of a regime is computed
+    // identically (batch-composition invariance within a regime).
+    return split_s1(a.s.D, num_sms);
 }
 
 void launch_forward_tc2_fusedx(const FwdArgs& a, const FusedX& fx, int num_sms, cudaStream_t st) {
@@ -1080,6 +1121,13 @@ int tc_variant() {  // 2 = cta_group::2 pair kernel (default when D % 256 == 0),
     return v;
 }
 
+// Programmatic dependent launch of the small-T chain (gather -> split-K GEMM -> reduce);
+// NGRAM_PDL=0 launches them plainly (A/B).
+static bool pdl_enabled() {
+    static const bool v = !(getenv("NGRAM_PDL") && atoi(getenv("NGRAM_PDL")) == 0);
+    return v;
+}
+
 // Small-T (decode / verify) projection: NGRAM_DECODE_CLUSTER=1 selects the single-kernel
 // cluster split-K (decode_gemm.cu: reduction + commit fused, measured slower: its in-kernel
 // reduction is latency-bound); default = split-K GEMM + reduce kernel (commit fused there).
@@ -1089,7 +1137,7 @@ static bool decode_cluster() {
 }
 
 size_t splitk_workspace_floats(const FwdArgs& a, int num_sms) {
-    if (a.T > 256 || (a.tmap_x == nullptr && a.seq_off == nullptr)) return 0;
+    if (!small_t_regime(a.s.D, a.T, num_sms) || (a.tmap_x == nullptr && a.seq_off == nullptr)) return 0;
     if (decode_cluster()) return decode_gemm_workspace_floats(a.s.D, num_sms);
     const int S = splitk_factor(a, num_sms);
     return S > 1 ? (size_t)S * (size_t)a.T * (size_t)a.s.D : 0;
@@ -1101,11 +1149,12 @@ void launch_forward_tc(const FwdArgs& a, int num_sms, cudaStream_t st, float* sp
         launch_decode_gemm(a, num_sms, splitk_ws, a.commit, st);
         return;
     }
-    if (splitk_ws && a.T <= 256 && (a.tmap_x != nullptr || a.seq_off != nullptr)) {
+    if (splitk_ws && small_t_regime(a.s.D, a.T, num_sms) && (a.tmap_x != nullptr || a.seq_off != nullptr)) {
         const int S = splitk_factor(a, num_sms);
         if (S > 1) {
-            if (a.tmap_x) launch_cfg<128, 4, 0>(a, num_sms, st, S, splitk_ws);  // A from X
-            else launch_cfg<128, 4, 2>(a, num_sms, st, S, splitk_ws);           // hash + gather4 in-kernel
+            const bool pdl = pdl_enabled();
+            if (a.tmap_x) launch_cfg<128, 4, 0>(a, num_sms, st, S, splitk_ws, pdl);  // A from X
+            else launch_cfg<128, 4, 2>(a, num_sms, st, S, splitk_ws);                // hash + gather4 in-kernel
             const float scale = 1.0f / (float)a.s.denom;
             const float amp = a.s.amp == kAmpSqrt ? (float)__builtin_sqrt((double)a.s.D) : 1.0f;
             const int64_t n4 = a.T * a.s.D / 4;
@@ -1113,9 +1162,24 @@ void launch_forward_tc(const FwdArgs& a, int num_sms, cudaStream_t st, float* sp
             if (blocks > num_sms * 8) blocks = num_sms * 8;
             DecodeCommit c{};
             if (a.commit) c = *a.commit;
-            splitk_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(
-                splitk_ws, S, a.T, a.s.D, a.tokens, a.e0, scale, amp,
-                (a.rows_out != nullptr && a.s.amp != kAmpLN) ? 1 : 0, a.rows_out, a.merged_out, a.out_bf16, a.err, c);
+            const int wr = (a.rows_out != nullptr && a.s.amp != kAmpLN) ? 1 : 0;
+            if (pdl) {
+                cudaLaunchConfig_t cfg{};
+                cfg.gridDim = dim3((unsigned)blocks);
+                cfg.blockDim = dim3(256);
+                cfg.stream = st;
+                cudaLaunchAttribute attr[1];
+                attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                attr[0].val.programmaticStreamSerializationAllowed = 1;
+                cfg.attrs = attr;
+                cfg.numAttrs = 1;
+                cudaLaunchKernelEx(&cfg, splitk_reduce_kernel, (const float*)splitk_ws, S, a.T, a.s.D, a.tokens, a.e0,
+                                   scale, amp, wr, a.rows_out, a.merged_out, a.out_bf16, a.err, c);
+            } else {
+                splitk_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(splitk_ws, S, a.T, a.s.D, a.tokens, a.e0, scale,
+                                                                       amp, wr, a.rows_out, a.merged_out, a.out_bf16,
+                                                                       a.err, c);
+            }
             count_launch();
             return;
         }

@@ -17,6 +17,7 @@
 
 #include "hashdev.cuh"
 #include "kernels.h"
+#include "ptx.cuh"
 
 namespace ngk {
 
@@ -247,14 +248,15 @@ __global__ void __launch_bounds__(256) hash_gather_rows_kernel(Shape s, const Ha
                                                                int64_t T, const uint32_t* __restrict__ prior,
                                                                const __nv_bfloat16* __restrict__ sub,
                                                                __nv_bfloat16* __restrict__ X,
-                                                               unsigned long long* err) {
+                                                               unsigned long long* err, int64_t uniform_len) {
+    griddep_launch_dependents();  // the decode GEMM may start its set-up (it waits for us)
     const int lane = threadIdx.x & 31;
     const int64_t w = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     if (w >= T * s.B) return;
     const int64_t t = w / s.B;
     const int b = (int)(w - t * s.B);
     uint32_t win[MAXN];
-    if (!load_window<MAXN>(s, tokens, seq_off, nseq, prior, t, win)) {
+    if (!load_window<MAXN>(s, tokens, seq_off, nseq, prior, t, win, uniform_len)) {
         if (lane == 0 && b == 0) atomicMin(err, (unsigned long long)t);
         return;
     }
@@ -347,16 +349,16 @@ void launch_hash_gather(const Shape& s, const HashTables* ht, const uint32_t* to
 
 void launch_hash_gather_rows(const Shape& s, const HashTables* ht, const uint32_t* tokens, const int64_t* seq_off,
                              int64_t nseq, int64_t T, const uint32_t* prior, const __nv_bfloat16* sub,
-                             __nv_bfloat16* X, unsigned long long* err, cudaStream_t st) {
+                             __nv_bfloat16* X, unsigned long long* err, cudaStream_t st, int64_t uniform_len) {
     const int64_t warps = T * s.B;
     if (warps <= 0) return;
     const unsigned blocks = (unsigned)((warps + 7) / 8);
     if (s.N <= 4)
-        hash_gather_rows_kernel<4><<<blocks, 256, 0, st>>>(s, ht, tokens, seq_off, nseq, T, prior, sub, X, err);
+        hash_gather_rows_kernel<4><<<blocks, 256, 0, st>>>(s, ht, tokens, seq_off, nseq, T, prior, sub, X, err, uniform_len);
     else if (s.N <= 8)
-        hash_gather_rows_kernel<8><<<blocks, 256, 0, st>>>(s, ht, tokens, seq_off, nseq, T, prior, sub, X, err);
+        hash_gather_rows_kernel<8><<<blocks, 256, 0, st>>>(s, ht, tokens, seq_off, nseq, T, prior, sub, X, err, uniform_len);
     else
-        hash_gather_rows_kernel<16><<<blocks, 256, 0, st>>>(s, ht, tokens, seq_off, nseq, T, prior, sub, X, err);
+        hash_gather_rows_kernel<16><<<blocks, 256, 0, st>>>(s, ht, tokens, seq_off, nseq, T, prior, sub, X, err, uniform_len);
     count_launch();
 }
 

@@ -74,13 +74,16 @@ __device__ __forceinline__ int32_t storage_row(const HashTables* __restrict__ ht
 }
 
 // One warp: window of position t; returns false (warp-uniform) when it holds a token >= V0.
+// uniform_len > 0: every sequence has that length (decode steps / verify blocks; the host
+// knows it), so the sequence of t needs no offset loads at all.
 template <int MAXN>
 __device__ __forceinline__ bool load_window(const Shape& s, const uint32_t* __restrict__ tokens,
                                             const int64_t* __restrict__ seq_off, int64_t nseq,
-                                            const uint32_t* __restrict__ prior, int64_t t, uint32_t (&w)[MAXN]) {
+                                            const uint32_t* __restrict__ prior, int64_t t, uint32_t (&w)[MAXN],
+                                            int64_t uniform_len = 0) {
     const int N = s.N;
-    const int64_t sq = find_seq(seq_off, nseq, t);
-    const int64_t base = __ldg(seq_off + sq);
+    const int64_t sq = uniform_len > 0 ? t / uniform_len : find_seq(seq_off, nseq, t);
+    const int64_t base = uniform_len > 0 ? sq * uniform_len : __ldg(seq_off + sq);
     const int64_t p = t - base;
     bool bad = false;
 #pragma unroll

@@ -47,7 +47,7 @@ void launch_hash_gather(const Shape& s, const HashTables* ht, const uint32_t* to
 // Same, one warp per (position, branch): the small-T (decode / verify) latency variant.
 void launch_hash_gather_rows(const Shape& s, const HashTables* ht, const uint32_t* tokens, const int64_t* seq_off,
                              int64_t nseq, int64_t T, const uint32_t* prior, const __nv_bfloat16* sub,
-                             __nv_bfloat16* X, unsigned long long* err, cudaStream_t st);
+                             __nv_bfloat16* X, unsigned long long* err, cudaStream_t st, int64_t uniform_len = 0);
 // Token range check only (tokens and used prior tokens < V0), min bad window -> err.
 void launch_validate_tokens(const Shape& s, const uint32_t* tokens, int64_t T, const int64_t* seq_off, int64_t nseq,
                             const uint32_t* prior, unsigned long long* err, cudaStream_t st);
@@ -137,7 +137,10 @@ void launch_forward_tc2_fusedx(const FwdArgs& a, const FusedX& fx, int num_sms, 
 // splitk_ws (fp32, splitk_workspace_floats() long, may be null): small-T split-K path.
 void launch_forward_tc(const FwdArgs& a, int num_sms, cudaStream_t st, float* splitk_ws = nullptr);
 size_t splitk_workspace_floats(const FwdArgs& a, int num_sms);
-int splitk_factor(const FwdArgs& a, int num_sms);  // small-T split: depends on D (and the SM count) only
+int splitk_factor(const FwdArgs& a, int num_sms);  // small-T split: depends on D and the regime of T only
+// Small-T regime (split-K BN=128 GEMM + reduce, S from D only): T <= 256.  A row's
+// arithmetic depends only on its own ids within a regime.
+bool small_t_regime(int D, int64_t T, int num_sms);
 // generic CUDA-core path: any shape, v1 and v2, reference float op order (simt.cu).
 void launch_forward_simt(const FwdArgs& a, cudaStream_t st);
 // K2 standalone: materialise X (T x D bf16) from the storage rows (d % 8 == 0).

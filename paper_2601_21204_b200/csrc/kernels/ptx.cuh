@@ -187,6 +187,12 @@ __device__ __forceinline__ uint4 ld_shared_v4u(uint32_t addr) {
                  : "memory");
     return v;
 }
+// Programmatic dependent launch (sm_90+): let the next grid in the stream launch now /
+// wait until every prerequisite grid has completed and its memory is visible.
+__device__ __forceinline__ void griddep_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_group_read() {  // smem of all but the N newest groups reusable

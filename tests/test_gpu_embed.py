@@ -226,14 +226,13 @@ def test_longcat_scale_bank_sampled_tokens(cuda):
 
 
 def test_fused_k1_k2_k3_kernel_matches_oracle(cuda):
-    """D > 1024 and T > 256 runs K1 + K2 + K3 in one persistent kernel (gather warps fill X
-    behind per-block ready counters): vs the oracle's double path, and bit-identical across
-    batch compositions in that regime."""
+    """D > 1024, T > 256: the fused K1+K2 kernel writes X and the pair kernel projects it:
+    vs the oracle's double path and bit-identical across batch compositions in that regime."""
     cfg = O.make_default_config(500, 1536, 4, 4)  # d = 128
     cfg["amplification"] = "scale_sqrt_d"
     hb = O.make_bank(cfg, 21, round_bf16=True)
     db = G.DeviceBank(cfg).upload(hb.base, hb.sub, hb.proj)
-    seqs = [O.uniform_tokens(s, 500, n) for s, n in [(1, 700), (2, 300), (3, 1000)]]
+    seqs = [O.uniform_tokens(s, 500, n) for s, n in [(1, 1100), (2, 300), (3, 1200)]]
     allt = np.concatenate(seqs)
     off = np.concatenate([[0], np.cumsum([len(s) for s in seqs])])
     rows, merged = G.embed_forward(db, dev_u32(torch, allt, cuda), dev_i64(torch, off, cuda), merged=True)
@@ -242,9 +241,12 @@ def test_fused_k1_k2_k3_kernel_matches_oracle(cuda):
     assert_rows_close(merged.cpu().numpy(), ref)
     for i, s in enumerate(seqs):
         alone, _ = G.embed_forward(db, dev_u32(torch, s, cuda), dev_i64(torch, [0, len(s)], cuda))
-        assert torch.equal(alone, rows[off[i]:off[i + 1]])
+        if len(s) > 256:
+            assert torch.equal(alone, rows[off[i]:off[i + 1]])
+        else:
+            assert_rows_close(alone.cpu().numpy(), rows[off[i]:off[i + 1]].cpu().numpy())
     bad = allt.copy()
-    bad[1500] = 500
+    bad[1500] = 500  # inside the second sequence
     out = torch.full((len(bad), 1536), 3.0, device=cuda)
     G.embed_forward(db, dev_u32(torch, bad, cuda), dev_i64(torch, off, cuda), out_rows=out)
     with pytest.raises(OutOfRange):
@@ -302,3 +304,53 @@ np.save(sys.argv[1], torch.stack([r, m]).view(torch.int16 if r.dtype == torch.bf
         direct = np.load(path)
     ours = torch.stack([rows, merged]).view(torch.int16 if bf else torch.int32).cpu().numpy()
     assert np.array_equal(ours, direct)
+
+
+def test_small_t_hash_in_gemm_variant_is_bit_identical(cuda):
+    """The opt-in small-T GEMM that hashes and gathers in its producers (MODE 2,
+    NGRAM_DECODE_HASH_IN_GEMM=1, selected once per process) computes the same split-K sums
+    as the default gather-kernel + X path: bit-identical outputs, incl. a carried prior."""
+    import os, subprocess, sys, tempfile
+    code = f"""
+import sys, numpy as np, torch
+sys.path[:0] = {[os.path.dirname(__file__), os.path.dirname(os.path.dirname(__file__)),
+                 os.path.join(os.path.dirname(os.path.dirname(__file__)), "oracle")]!r}
+import oracle as O
+from helpers import dev_i64, dev_u32
+from paper_2601_21204_b200 import ngram as G
+cfg = O.make_default_config(3000, 768, 4, 2)
+hb = O.make_bank(cfg, 23, round_bf16=True)
+db = G.DeviceBank(cfg).upload(hb.base, hb.sub, hb.proj)
+toks = O.uniform_tokens(81, 3000, 200)
+prior = np.zeros((4, 3), np.uint32); prior[2] = [5, 6, 7]
+r, m = G.embed_forward(db, dev_u32(torch, toks, "cuda:0"), dev_i64(torch, [0, 50, 120, 190, 200], "cuda:0"),
+                       prior=dev_u32(torch, prior, "cuda:0"), merged=True)
+db.sync_errors()
+np.save(sys.argv[1], torch.stack([r, m]).view(torch.int32).cpu().numpy())
+"""
+    outs = []
+    with tempfile.TemporaryDirectory() as td:
+        for v in ("0", "1"):
+            path = os.path.join(td, f"o{v}.npy")
+            subprocess.run([sys.executable, "-c", code, path], check=True, timeout=300,
+                           env={**os.environ, "NGRAM_DECODE_HASH_IN_GEMM": v})
+            outs.append(np.load(path))
+    assert np.array_equal(outs[0], outs[1])
+
+
+def test_verify_sized_regime_at_longcat_width(cuda):
+    """D = 3072, verify-sized T (500 / 600): the pair-kernel regime at LongCat width matches the
+    reference within tolerance and is batch-composition invariant."""
+    cfg = O.make_default_config(1000, 3072, 4, 4)
+    hb = O.make_bank(cfg, 31, round_bf16=True)
+    db = G.DeviceBank(cfg).upload(hb.base, hb.sub, hb.proj)
+    seqs = [O.uniform_tokens(90 + i, 1000, n) for i, n in enumerate([300, 200, 100])]
+    allt = np.concatenate(seqs)
+    off = np.concatenate([[0], np.cumsum([len(s) for s in seqs])])
+    rows, merged = G.embed_forward(db, dev_u32(torch, allt, cuda), dev_i64(torch, off, cuda), merged=True)
+    db.sync_errors()
+    ref_r, ref_m = zip(*[O.embed_sequence(hb, s, double=True) for s in seqs])
+    assert_rows_close(rows.cpu().numpy(), np.concatenate(ref_r))
+    assert_rows_close(merged.cpu().numpy(), np.concatenate(ref_m))
+    a01, _ = G.embed_forward(db, dev_u32(torch, np.concatenate(seqs[:2]), cuda), dev_i64(torch, off[:3], cuda))
+    assert torch.equal(a01, rows[:500])  # T = 500 and T = 600: same regime, same bits
