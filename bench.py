@@ -41,6 +41,97 @@ sys.path.insert(0, ROOT)
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
+# ------------------------------------------------------------------ token streams
+class _MT64:
+    """std::mt19937_64 (the reference's rng64, rng.hpp:14), numpy-vectorised twist."""
+    N, M = 312, 156
+
+    def __init__(self, seed: int):
+        mask = (1 << 64) - 1
+        mt = [seed & mask]
+        for i in range(1, self.N):
+            mt.append((6364136223846793005 * (mt[-1] ^ (mt[-1] >> 62)) + i) & mask)
+        self.mt = np.array(mt, dtype=np.uint64)
+        self.out, self.pos = None, self.N
+
+    def _twist(self):
+        mt, N, M = self.mt, self.N, self.M
+        up, lo, a = np.uint64(0xFFFFFFFF80000000), np.uint64(0x7FFFFFFF), np.uint64(0xB5026F5AA96619E9)
+        for i0, i1 in ((0, N - M), (N - M, N - 1), (N - 1, N)):  # the recurrence's three dependency ranges
+            i = np.arange(i0, i1)
+            x = (mt[i] & up) | (mt[(i + 1) % N] & lo)
+            xa = (x >> np.uint64(1)) ^ np.where((x & np.uint64(1)) == 1, a, np.uint64(0))
+            mt[i] = mt[(i + M) % N] ^ xa
+        y = mt.copy()
+        y ^= (y >> np.uint64(29)) & np.uint64(0x5555555555555555)
+        y ^= (y << np.uint64(17)) & np.uint64(0x71D67FFFEDA60000)
+        y ^= (y << np.uint64(37)) & np.uint64(0xFFF7EEE000000000)
+        y ^= y >> np.uint64(43)
+        self.out, self.pos = [int(v) for v in y], 0
+
+    def __call__(self) -> int:
+        if self.pos >= self.N:
+            self._twist()
+        self.pos += 1
+        return self.out[self.pos - 1]
+
+    def uniform01(self) -> float:  # rng.hpp:17-19
+        return (self() >> 11) * 2.0 ** -53
+
+    def below(self, bound: int) -> int:  # rng.hpp:22-29
+        limit = (2 ** 64 - 1) - (2 ** 64 - 1) % bound
+        while True:
+            x = self()
+            if x < limit:
+                return x % bound
+
+
+def zipf_markov_tokens(vocab, sequences, seq_len, seed=20260809, exponent=1.1, markov_prob=0.35):
+    """generate_zipf_markov (corpus.cpp:211-271) restated for the bench's token input:
+    text-like skew (Zipf fresh draws, a function-token pool, Markov successors).
+    tests/test_abi_cpu.py pins it to the reference generator token for token."""
+    import bisect
+    rng = _MT64(seed)
+    cdf = np.cumsum(1.0 / np.power(np.arange(1, vocab + 1, dtype=np.float64), exponent))
+    cdf = (cdf / cdf[-1]).tolist()
+
+    def zipf():
+        i = bisect.bisect_right(cdf, rng.uniform01())
+        return i if i < vocab else vocab - 1
+
+    pool = min(vocab, max(2, vocab * 3 // 50))
+    block = max(1, vocab // 20)
+    active = max(pool, vocab // 2)
+    succ = []
+    for v in range(vocab):
+        if v < pool:
+            s = zipf()
+            while s >= pool:
+                s = zipf()
+            succ.append(s)
+        else:
+            succ.append((2 * (v // block) + 1) % pool)
+    out = np.zeros((sequences, seq_len), np.uint32)
+    for q in range(sequences):
+        prev, fresh = 0, True
+        row = out[q]
+        for i in range(seq_len):
+            if not fresh and rng.uniform01() >= markov_prob:
+                if rng.uniform01() < 0.001:
+                    nxt = rng.below(vocab)
+                else:
+                    nxt = zipf()
+                    while nxt >= active:
+                        nxt = zipf()
+                fresh = True
+            else:
+                nxt = succ[prev]
+                fresh = False
+            row[i] = nxt
+            prev = nxt
+    return out
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -214,8 +305,11 @@ def run_ours(args):
     out_dtype = torch.bfloat16 if args.out_dtype == "bf16" else torch.float32
     esz = 2 if out_dtype == torch.bfloat16 else 4
 
-    rng = np.random.default_rng(42)
-    all_tokens = rng.integers(0, cfg["base_vocab"], size=total_tokens, dtype=np.int64).astype(np.int32)
+    if args.tokens == "zipf":  # generate_zipf_markov(V0, nseq, len, 20260809, 1.1, 0.35)
+        all_tokens = zipf_markov_tokens(cfg["base_vocab"], nseq, seq_len).reshape(-1).astype(np.int32)
+    else:
+        rng = np.random.default_rng(42)
+        all_tokens = rng.integers(0, cfg["base_vocab"], size=total_tokens, dtype=np.int64).astype(np.int32)
     toks = torch.from_numpy(all_tokens[rank * T:(rank + 1) * T].copy()).to(dev)
     off = torch.arange(0, T + 1, seq_len, dtype=torch.int64, device=dev)
     rows = torch.empty((T, (cfg["dim"])), dtype=out_dtype, device=dev)
@@ -394,7 +488,9 @@ def run_ours(args):
         "metric": "ngram_embedding_tokens_per_sec", "value": total_tokens / (ms * 1e-3), "unit": "tokens/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic (device-generated counter-based tables, uniform tokens seed 42)",
+        "data": "synthetic (device-generated counter-based tables, " + (
+            "Zipf-Markov tokens generate_zipf_markov(V0, nseq, len, 20260809, 1.1, 0.35))" if args.tokens == "zipf"
+            else "uniform tokens seed 42)"),
         "config": {"workload": label, "V0": cfg["base_vocab"], "N": cfg["max_order"], "K": cfg["sub_tables"], "D": D,
                    "d": d, "tokens": total_tokens, "sequences": nseq, "seq_len": seq_len,
                    "embedding_params": nparams, "sub_table_params": nsub, "table_dtype": "bf16",
@@ -483,6 +579,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default="C")
     ap.add_argument("--out-dtype", choices=["fp32", "bf16"], default="fp32")
+    ap.add_argument("--tokens", choices=["uniform", "zipf"], default="uniform",
+                    help="token stream: iid uniform (headline) or the reference's Zipf-Markov text model")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--batches", default="1,8,64,256", help="decode / verify batch sizes (workloads D, E)")

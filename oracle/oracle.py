@@ -145,6 +145,8 @@ def ref():
         L.ref_ffn_plne_backward_f64.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, _u32p,
                                                 C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                                 C.c_void_p, C.c_void_p]
+        L.ref_generate_zipf_markov.argtypes = [C.c_uint32, C.c_int64, C.c_int64, C.c_uint64, C.c_double, C.c_double,
+                                               _u32p]
         L.ref_cache_create.argtypes = [C.c_char_p]
         L.ref_cache_create.restype = C.c_void_p
         L.ref_cache_destroy.argtypes = [C.c_void_p]

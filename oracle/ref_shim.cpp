@@ -19,6 +19,7 @@
 
 #include "ngram/cache.hpp"
 #include "ngram/config.hpp"
+#include "ngram/corpus.hpp"
 #include "ngram/embedding.hpp"
 #include "ngram/errors.hpp"
 #include "ngram/hashing.hpp"
@@ -296,6 +297,20 @@ int ref_ffn_plne_backward_f64(void* h, const double* gate, const double* down, i
         for (std::size_t b = 0; b < gb.projections.size(); ++b)
             std::memcpy(g_proj[b], gb.projections[b].data(), gb.projections[b].size() * 8);
         std::memcpy(dx, d.data(), d.size() * 8);
+        return 0;
+    } catch (...) {
+        return map_exc();
+    }
+}
+
+// corpus.cpp:211-271 generate_zipf_markov: sequences x seq_len tokens, row-major.
+int ref_generate_zipf_markov(uint32_t vocab, int64_t sequences, int64_t seq_len, uint64_t seed, double exponent,
+                             double markov_prob, uint32_t* out) {
+    try {
+        const auto c = generate_zipf_markov(vocab, std::size_t(sequences), std::size_t(seq_len), seed, exponent,
+                                            markov_prob);
+        for (std::size_t s = 0; s < c.size(); ++s)
+            std::memcpy(out + s * std::size_t(seq_len), c[s].data(), c[s].size() * 4);
         return 0;
     } catch (...) {
         return map_exc();

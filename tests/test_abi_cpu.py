@@ -7,6 +7,7 @@ import json
 import os
 import re
 
+import numpy as np
 import pytest
 
 import oracle as O
@@ -126,3 +127,16 @@ def test_no_cpu_fallback_without_gpu():
     rc = abi.lib().ngram_bank_create(json.dumps(_v2(16, 8, 3, 2)).encode(), 0, 0, 1, C.byref(h))
     assert rc in (abi.NGRAM_ECUDA, abi.NGRAM_ENOMEM)
     assert not h.value
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="reference not built here")
+def test_bench_zipf_markov_stream_is_the_reference_generator():  # corpus.cpp:211-271
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    for vocab, nseq, n, seed in [(1000, 3, 400, 20260809), (128000, 2, 2000, 7)]:
+        ours = bench.zipf_markov_tokens(vocab, nseq, n, seed)
+        ref = np.zeros((nseq, n), np.uint32)
+        assert O.ref().ref_generate_zipf_markov(vocab, nseq, n, seed, 1.1, 0.35, ref.reshape(-1)) == 0
+        assert np.array_equal(ours, ref)
