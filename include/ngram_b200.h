@@ -239,6 +239,23 @@ int ngram_shard_project(ngram_shard_group* g, const uint32_t* home_tokens, int64
  * match the reference within an fp32 tolerance (not bit-exact).  Single-shard banks only. */
 typedef struct ngram_grad ngram_grad;
 int ngram_grad_create(ngram_bank* bank, ngram_grad** out); /* zero-initialised */
+/* NGRAM_GRAD_SPARSE_ROWS: the sub-table gradient is kept row-sparse instead of dense -- every
+ * backward call APPENDS its (storage row, d-wide gradient row) pairs for all T x B
+ * (position, branch) rows (duplicates not merged: their sum is the dense gradient).  E0,
+ * W_cat and LN gradients stay dense.  Needed at LongCat scale, where a dense fp32 copy of
+ * the 31.5 B sub-table parameters (126 GB) does not fit beside the tables. */
+#define NGRAM_GRAD_SPARSE_ROWS 1
+/* NGRAM_GRAD_TF32: the two backward GEMMs on TF32 tensor cores (10-bit mantissa inputs, fp32
+ * accumulation) instead of pedantic fp32 -- ~10x faster at LongCat scale; gradients agree
+ * with the reference to ~1e-3 relative (training precision), not the 1e-5 fp32 contract. */
+#define NGRAM_GRAD_TF32 2
+int ngram_grad_create_ex(ngram_bank* bank, int flags, ngram_grad** out);
+/* Row-sparse gradient view: rows = dev int32 [count] storage rows (the device layout of
+ * ngram_grad_tensor(1)), vals = dev f32 [count][branch_dim]; count resets on ngram_grad_zero. */
+int ngram_grad_sparse_rows(ngram_grad* g, int32_t** rows, float** vals, int64_t* count);
+/* Copy pairs [first, first + count) to caller buffers (host or device; stream-ordered).
+ * Pairs appended by a call whose tokens were out of range carry row -1 (no gradient). */
+int ngram_grad_sparse_read(ngram_grad* g, int64_t first, int64_t count, int32_t* rows, float* vals, void* stream);
 int ngram_grad_destroy(ngram_grad* g);
 int ngram_grad_zero(ngram_grad* g, void* stream);
 #define NGRAM_BWD_SKIP_AMPLIFY 1 /* upstream is d(merged) already: embed_backward only */

@@ -18,6 +18,8 @@ NGRAM_ECONFIG, NGRAM_ENUMERIC, NGRAM_ECUDA, NGRAM_ENCCL, NGRAM_ENOMEM = 5, 6, 7,
 NGRAM_F32, NGRAM_BF16 = 0, 1
 NGRAM_BANK_HASH_ONLY = 1
 NGRAM_BWD_SKIP_AMPLIFY = 1
+NGRAM_GRAD_SPARSE_ROWS = 1
+NGRAM_GRAD_TF32 = 2
 NGRAM_SHARD_HANDLE_BYTES = 128
 
 # Exported symbols, in header order (tests check the .so exports every one).
@@ -37,6 +39,7 @@ SYMBOLS = [
     "ngram_grad_download", "ngram_embed_backward_host",
     "ngram_plne_create", "ngram_plne_destroy", "ngram_plne_forward", "ngram_plne_backward",
     "ngram_plne_forward_host", "ngram_plne_backward_host",
+    "ngram_grad_create_ex", "ngram_grad_sparse_rows", "ngram_grad_sparse_read",
 ]
 
 
@@ -155,6 +158,9 @@ def lib() -> C.CDLL:
         "ngram_plne_forward": ([vp, vp, vp, vp, vp, vp, i64, i64, vp, vp, vp], i32),
         "ngram_plne_backward": ([vp, vp, vp, vp, vp, vp, vp, i64, i64, vp, vp, vp, vp, vp, vp], i32),
         "ngram_plne_forward_host": ([vp, vp, vp, vp, vp, vp, i64, vp, vp], i32),
+        "ngram_grad_create_ex": ([vp, i32, C.POINTER(vp)], i32),
+        "ngram_grad_sparse_rows": ([vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(i64)], i32),
+        "ngram_grad_sparse_read": ([vp, i64, i64, vp, vp, vp], i32),
         "ngram_plne_backward_host": ([vp, vp, vp, vp, vp, vp, vp, i64, vp, vp, vp, vp, vp], i32),
     }
     for name, (args, res) in sig.items():

@@ -29,6 +29,10 @@ struct ngram_grad {
     DevBuf<float> U, X, dX, wf;            // workspaces
     DevBuf<int32_t> grow;
     int64_t cap = 0;
+    bool sparse = false;                 // NGRAM_GRAD_SPARSE_ROWS
+    DevBuf<int32_t> sp_rows;             // [sp_cap] storage rows
+    DevBuf<float> sp_vals;               // [sp_cap][d]
+    int64_t sp_count = 0, sp_cap = 0;
     DevBuf<uint32_t> h_tokens, h_prior;  // host-buffer entry staging
     DevBuf<int64_t> h_off;
     DevBuf<float> h_merged, h_up;
@@ -52,30 +56,58 @@ void check_blas(cublasStatus_t s, const char* what) {
 void zero_all(ngram_grad* g, cudaStream_t st) {
     for (DevBuf<float>* b : {&g->e0, &g->sub, &g->w, &g->gain, &g->bias})
         if (b->n) NGH_CUDA(cudaMemsetAsync(b->p, 0, b->n * sizeof(float), st));
+    g->sp_count = 0;
+}
+
+// Make room for `more` sparse (row, gradient row) pairs, preserving the ones already held.
+void sparse_reserve(ngram_grad* g, int64_t more, int d, cudaStream_t st) {
+    const int64_t need = g->sp_count + more;
+    if (need <= g->sp_cap) return;
+    const int64_t cap = std::max<int64_t>(need, g->sp_cap * 2);
+    DevBuf<int32_t> r;
+    DevBuf<float> v;
+    r.alloc(size_t(cap));
+    v.alloc(size_t(cap) * size_t(d));
+    if (g->sp_count) {
+        NGH_CUDA(cudaMemcpyAsync(r.p, g->sp_rows.p, size_t(g->sp_count) * 4, cudaMemcpyDeviceToDevice, st));
+        NGH_CUDA(cudaMemcpyAsync(v.p, g->sp_vals.p, size_t(g->sp_count) * size_t(d) * 4, cudaMemcpyDeviceToDevice, st));
+        NGH_CUDA(cudaStreamSynchronize(st));
+    }
+    std::swap(g->sp_rows.p, r.p);
+    std::swap(g->sp_rows.n, r.n);
+    std::swap(g->sp_vals.p, v.p);
+    std::swap(g->sp_vals.n, v.n);
+    g->sp_cap = cap;
 }
 
 }  // namespace
 
 extern "C" {
 
-int ngram_grad_create(ngram_bank* b, ngram_grad** out) {
+int ngram_grad_create(ngram_bank* b, ngram_grad** out) { return ngram_grad_create_ex(b, 0, out); }
+
+int ngram_grad_create_ex(ngram_bank* b, int flags, ngram_grad** out) {
     NGRAM_API_BEGIN
-    if (!b || !out) throw Error(NGRAM_EINVAL, "ngram_grad_create: bad argument");
+    if (!b || !out || (flags & ~(NGRAM_GRAD_SPARSE_ROWS | NGRAM_GRAD_TF32)))
+        throw Error(NGRAM_EINVAL, "ngram_grad_create: bad argument");
     if (b->hash_only) throw Error(NGRAM_EINVAL, "bank was created hash-only (NGRAM_BANK_HASH_ONLY)");
     if (b->shard_count != 1) throw Error(NGRAM_EINVAL, "ngram_grad_create: row-sharded banks are not supported");
     DeviceGuard dg(b->device);
     auto g = std::make_unique<ngram_grad>();
     g->bank = b;
     const auto& s = b->shape;
+    g->sparse = (flags & NGRAM_GRAD_SPARSE_ROWS) != 0;
     g->e0.alloc(size_t(b->cfg.base_vocab) * size_t(s.D));
-    g->sub.alloc(size_t(b->local_rows) * size_t(s.d));
+    if (!g->sparse) g->sub.alloc(size_t(b->local_rows) * size_t(s.d));
     if (s.variant == 1 && s.B > 0) g->w.alloc(size_t(s.D) * size_t(s.D));
     if (s.amp == ngk::kAmpLN) {
         g->gain.alloc(size_t(s.D));
         g->bias.alloc(size_t(s.D));
     }
     check_blas(cublasCreate(&g->blas), "cublasCreate");
-    check_blas(cublasSetMathMode(g->blas, CUBLAS_PEDANTIC_MATH), "cublasSetMathMode");  // true fp32, no TF32
+    check_blas(cublasSetMathMode(g->blas, (flags & NGRAM_GRAD_TF32) ? CUBLAS_TF32_TENSOR_OP_MATH
+                                                                    : CUBLAS_PEDANTIC_MATH),  // default: true fp32
+               "cublasSetMathMode");
     zero_all(g.get(), nullptr);
     NGH_CUDA(cudaDeviceSynchronize());
     *out = g.release();
@@ -145,9 +177,27 @@ int ngram_embed_backward(ngram_grad* g, const uint32_t* tokens, const int64_t* s
         check_blas(cublasSgemm(g->blas, CUBLAS_OP_N, CUBLAS_OP_N, D, int(T), D, &one, g->wf.p, D, g->U.p, D, &zero,
                                g->dX.p, D),
                    "cublasSgemm(dX)");
-        ngk::launch_scatter_rows(s, g->grow.p, g->cap, T, d, D, d, g->dX.p, g->sub.p, b->err.p, st);
+        if (g->sparse) {  // dX is [T][B][d]: exactly the appended values, rows transposed from grow
+            sparse_reserve(g, T * B, d, st);
+            NGH_CUDA(cudaMemcpyAsync(g->sp_vals.p + size_t(g->sp_count) * size_t(d), g->dX.p,
+                                     size_t(T) * size_t(D) * 4, cudaMemcpyDeviceToDevice, st));
+            ngk::launch_rows_to_coo(s, g->grow.p, g->cap, T, g->sp_rows.p + g->sp_count, b->err.p, st);
+            g->sp_count += T * B;
+        } else {
+            ngk::launch_scatter_rows(s, g->grow.p, g->cap, T, d, D, d, g->dX.p, g->sub.p, b->err.p, st);
+        }
     } else if (B > 0) {  // averaged_v1: every branch row receives u (rows are D wide)
-        ngk::launch_scatter_rows(s, g->grow.p, g->cap, T, D, D, 0, g->U.p, g->sub.p, b->err.p, st);
+        if (g->sparse) {
+            sparse_reserve(g, T * B, D, st);
+            for (int i = 0; i < B; ++i)  // value of pair (t, b) = U[t]
+                NGH_CUDA(cudaMemcpy2DAsync(g->sp_vals.p + (size_t(g->sp_count) + size_t(i)) * size_t(D),
+                                           size_t(B) * size_t(D) * 4, g->U.p, size_t(D) * 4, size_t(D) * 4,
+                                           size_t(T), cudaMemcpyDeviceToDevice, st));
+            ngk::launch_rows_to_coo(s, g->grow.p, g->cap, T, g->sp_rows.p + g->sp_count, b->err.p, st);
+            g->sp_count += T * B;
+        } else {
+            ngk::launch_scatter_rows(s, g->grow.p, g->cap, T, D, D, 0, g->U.p, g->sub.p, b->err.p, st);
+        }
     }
     NGH_CUDA(cudaGetLastError());
     NGRAM_API_END
@@ -191,6 +241,31 @@ int ngram_embed_backward_host(ngram_grad* g, const uint32_t* tokens, const int64
     NGRAM_API_END
 }
 
+int ngram_grad_sparse_rows(ngram_grad* g, int32_t** rows, float** vals, int64_t* count) {
+    NGRAM_API_BEGIN
+    if (!g || !rows || !vals || !count) throw Error(NGRAM_EINVAL, "ngram_grad_sparse_rows: bad argument");
+    if (!g->sparse) throw Error(NGRAM_EINVAL, "gradient bank was not created with NGRAM_GRAD_SPARSE_ROWS");
+    *rows = g->sp_rows.p;
+    *vals = g->sp_vals.p;
+    *count = g->sp_count;
+    NGRAM_API_END
+}
+
+int ngram_grad_sparse_read(ngram_grad* g, int64_t first, int64_t count, int32_t* rows, float* vals, void* stream) {
+    NGRAM_API_BEGIN
+    if (!g || first < 0 || count < 0 || first + count > g->sp_count)
+        throw Error(NGRAM_EINVAL, "ngram_grad_sparse_read: bad range");
+    if (!g->sparse) throw Error(NGRAM_EINVAL, "gradient bank was not created with NGRAM_GRAD_SPARSE_ROWS");
+    DeviceGuard dg(g->bank->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t d = size_t(g->bank->shape.d);
+    if (rows && count)
+        NGH_CUDA(cudaMemcpyAsync(rows, g->sp_rows.p + first, size_t(count) * 4, cudaMemcpyDefault, st));
+    if (vals && count)
+        NGH_CUDA(cudaMemcpyAsync(vals, g->sp_vals.p + size_t(first) * d, size_t(count) * d * 4, cudaMemcpyDefault, st));
+    NGRAM_API_END
+}
+
 int ngram_grad_tensor(ngram_grad* g, int which, float** dev_ptr, int64_t* numel) {
     NGRAM_API_BEGIN
     if (!g || !dev_ptr || !numel) throw Error(NGRAM_EINVAL, "ngram_grad_tensor: bad argument");
@@ -216,6 +291,8 @@ int ngram_grad_download(ngram_grad* g, float* base, float* const* sub, float* co
     NGH_CUDA(cudaDeviceSynchronize());
     const auto& s = b->shape;
     if (base) NGH_CUDA(cudaMemcpy(base, g->e0.p, g->e0.n * sizeof(float), cudaMemcpyDeviceToHost));
+    if (sub && g->sparse)
+        throw Error(NGRAM_EINVAL, "row-sparse gradient bank: read sub-table gradients with ngram_grad_sparse_rows");
     if (sub)
         for (int i = 0; i < s.B; ++i)
             if (sub[i])

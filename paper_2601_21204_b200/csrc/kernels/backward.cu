@@ -156,6 +156,18 @@ __global__ void scatter_rows_kernel(const int32_t* __restrict__ grow, int64_t Tp
     }
 }
 
+// rows[t * B + b] = grow[b][t]: the storage rows of the appended sparse pairs, (t, b) order
+__global__ void rows_to_coo_kernel(const int32_t* __restrict__ grow, int64_t Tpad, int64_t T, int B,
+                                   int32_t* __restrict__ rows, const unsigned long long* __restrict__ err) {
+    const bool bad = *err != ~0ull;  // a call with an out-of-range token appends no gradient
+    const int64_t n = T * B;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = i / B;
+        const int b = (int)(i - t * B);
+        rows[i] = bad ? -1 : grow[(int64_t)b * Tpad + t];
+    }
+}
+
 __global__ void bf16_to_f32_kernel(const __nv_bfloat16* __restrict__ src, float* __restrict__ dst, int64_t n) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         dst[i] = __bfloat162float(src[i]);
@@ -202,6 +214,13 @@ void launch_scatter_rows(const Shape& s, const int32_t* grow, int64_t Tpad, int6
     if (T <= 0 || s.B == 0) return;
     scatter_rows_kernel<<<grid_for(T * s.B * width, 256), 256, 0, st>>>(grow, Tpad, T, s.B, width, src_stride,
                                                                        src_branch_step, src, g_sub, err);
+    count_launch();
+}
+
+void launch_rows_to_coo(const Shape& s, const int32_t* grow, int64_t Tpad, int64_t T, int32_t* rows,
+                        const unsigned long long* err, cudaStream_t st) {
+    if (T <= 0 || s.B == 0) return;
+    rows_to_coo_kernel<<<grid_for(T * s.B, 256), 256, 0, st>>>(grow, Tpad, T, s.B, rows, err);
     count_launch();
 }
 

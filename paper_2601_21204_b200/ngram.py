@@ -406,10 +406,12 @@ class GradBank:
     """fp32 gradient accumulator of a DeviceBank (embedding_bank_t<T>& grads of
     embed_sequence_backward, embedding.hpp:438-459), zero-initialised, device layout."""
 
-    def __init__(self, bank: DeviceBank):
+    def __init__(self, bank: DeviceBank, sparse_rows: bool = False, tf32: bool = False):
         self.bank = bank
+        self.sparse_rows = sparse_rows
         h = C.c_void_p()
-        check(abi.lib().ngram_grad_create(bank.handle, C.byref(h)))
+        flags = (abi.NGRAM_GRAD_SPARSE_ROWS if sparse_rows else 0) | (abi.NGRAM_GRAD_TF32 if tf32 else 0)
+        check(abi.lib().ngram_grad_create_ex(bank.handle, flags, C.byref(h)))
         self.handle = h
 
     def close(self):
@@ -437,6 +439,18 @@ class GradBank:
         check(abi.lib().ngram_embed_backward(self.handle, _ptr(tokens), _ptr(seq_offsets), seq_offsets.numel() - 1, T,
                                              _ptr(prior), _ptr(merged), _ptr(upstream), flags, _stream(stream)))
 
+    def sparse(self, device=None):
+        """Row-sparse sub-table gradient (sparse_rows=True): (rows int32 [n], vals f32 [n, d])
+        on the device, duplicates not merged (their sum is the dense gradient)."""
+        p_r, p_v, n = C.c_void_p(), C.c_void_p(), C.c_int64()
+        check(abi.lib().ngram_grad_sparse_rows(self.handle, C.byref(p_r), C.byref(p_v), C.byref(n)))
+        dev = device or torch.device("cuda", self.bank.device)
+        d = branch_dim(self.bank.cfg)
+        rows = torch.empty(n.value, dtype=torch.int32, device=dev)
+        vals = torch.empty((n.value, d), dtype=torch.float32, device=dev)
+        check(abi.lib().ngram_grad_sparse_read(self.handle, 0, n.value, _ptr(rows), _ptr(vals), _stream()))
+        return rows, vals
+
     def tensor(self, which: int) -> tuple:
         """(device pointer, numel) of 0 E0, 1 sub-tables, 2 W_cat, 3 ln_gain, 4 ln_bias."""
         p, n = C.c_void_p(), C.c_int64()
@@ -459,7 +473,8 @@ class GradBank:
         sp = (C.c_void_p * max(B, 1))(*[a.ctypes.data for a in out["sub"]])
         pp = (C.c_void_p * max(B, 1))(*[a.ctypes.data for a in out["proj"]])
         ln = cfg["amplification"] == "layer_norm"
-        check(abi.lib().ngram_grad_download(self.handle, out["base"].ctypes.data, sp if B else None,
+        check(abi.lib().ngram_grad_download(self.handle, out["base"].ctypes.data,
+                                            sp if (B and not self.sparse_rows) else None,
                                             pp if (v2 and B) else None, out["gain"].ctypes.data if ln else None,
                                             out["bias"].ctypes.data if ln else None))
         return out

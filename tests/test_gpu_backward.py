@@ -96,3 +96,52 @@ def test_forward_then_backward_at_longcat_width(cuda):
     ref = O.embed_sequence_backward(hb, toks, merged.cpu().numpy().astype(np.float64),
                                     up.cpu().numpy().astype(np.float64))
     assert_grads_close(gb.download(), ref, False)
+
+
+def _densify(rows, vals, cfg):
+    """Row-sparse pairs (device storage rows) -> dense per-branch sub-table gradients."""
+    sv = O.sub_vocab_array(cfg)
+    base = np.concatenate([[0], np.cumsum(sv)]).astype(np.int64)
+    d = vals.shape[1]
+    dense = [np.zeros((int(v), d)) for v in sv]
+    rows = rows.astype(np.int64)
+    keep = rows >= 0
+    rows, vals = rows[keep], vals[keep].astype(np.float64)
+    b = np.searchsorted(base, rows, side="right") - 1
+    for i in range(len(sv)):
+        m = b == i
+        np.add.at(dense[i], rows[m] - base[i], vals[m])
+    return dense
+
+
+@pytest.mark.parametrize("name", ["backward_tc_layer_norm.npz", "backward_v1_wide.npz"])
+def test_row_sparse_gradients_sum_to_the_dense_ones(cuda, name):
+    g, cfg, hb, db, args, ln = _setup(name, cuda)
+    gb = G.GradBank(db, sparse_rows=True)
+    gb.backward(**args)
+    gb.backward(**args)  # appends: every (position, branch) pair twice
+    db.sync_errors()
+    rows, vals = gb.sparse()
+    assert rows.numel() == 2 * len(g["tokens"]) * db.B
+    got = gb.download()
+    got["base"] = got["base"] / 2
+    got["gain"], got["bias"] = got["gain"] / 2, got["bias"] / 2
+    got["proj"] = [p / 2 for p in got["proj"]]
+    got["sub"] = [x / 2 for x in _densify(rows.cpu().numpy(), vals.cpu().numpy(), cfg)]
+    assert_grads_close(got, golden_grads(g, O.zero_grads(cfg)), ln)
+    gb.zero()
+    bad = args["tokens"].clone()
+    bad[5] = cfg["base_vocab"]
+    gb.backward(**dict(args, tokens=bad))
+    with pytest.raises(OutOfRange):
+        db.sync_errors()
+    rows, _ = gb.sparse()
+    assert (rows.cpu().numpy() == -1).all()
+
+
+def test_tf32_backward_within_training_precision(cuda):  # NGRAM_GRAD_TF32
+    g, cfg, hb, db, args, ln = _setup("backward_tc_scale_sqrt_d.npz", cuda)
+    gb = G.GradBank(db, tf32=True)
+    gb.backward(**args)
+    db.sync_errors()
+    assert_grads_close(gb.download(), golden_grads(g, O.zero_grads(cfg)), ln, rel_l2=3e-3, max_rtol=1e-2)
