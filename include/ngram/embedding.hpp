@@ -157,6 +157,31 @@ std::vector<float> embed_sequence(std::span<const token_id> tokens, const embedd
 // Batched extension: many sequences in one launch (rows concatenated, len_total x D).
 std::vector<float> embed_batch(const std::vector<std::vector<token_id>>& sequences, const device_bank& bank);
 
+// ---- parameter accounting (embedding.hpp:461-484, embedding.cpp:13-56): host arithmetic
+struct param_count_report {
+    std::uint64_t base = 0;
+    std::uint64_t sub_tables = 0;
+    std::uint64_t projections = 0;
+    std::uint64_t total = 0;
+};
+param_count_report param_count(const ngram_config& cfg);
+
+struct budget_info {
+    std::uint64_t embedding_params = 0;
+    std::uint64_t other_params = 0;
+    double fraction = 0.0;     // embedding / (embedding + other)
+    bool over_budget = false;  // fraction strictly above 1/2
+};
+budget_info budget_report(std::uint64_t embedding_params, std::uint64_t other_params);
+budget_info budget_report(const ngram_config& cfg, std::uint64_t other_params);
+std::string budget_guidance(const budget_info& info);
+
+// ---- serialization (embedding.hpp:486-493): the reference's single-file format (u32 LE
+// header length, JSON config, raw LE f32 tensors).  A device_bank reads the same file with
+// device_bank::from_file (streamed f32 -> bf16 on the GPU).
+void save_bank(const embedding_bank& bank, const std::string& path);
+embedding_bank load_bank(const std::string& path);
+
 // zeros_like (embedding.hpp:123-134): a zero bank of the same shape (the gradient store).
 template <typename T>
 embedding_bank_t<T> zeros_like(const embedding_bank_t<T>& bank) {

@@ -514,6 +514,102 @@ draft_result draft_verify(sequence_cache& state, embedding_memo&, const device_b
     return draft_verify(state, bank, draft, accept_count, counters, opts);
 }
 
+// ---------------------------------------------------------------- accounting / serialization
+param_count_report param_count(const ngram_config& cfg) {
+    cfg.validate();
+    param_count_report r;
+    const std::uint64_t D = std::uint64_t(cfg.dim), d = std::uint64_t(cfg.branch_dim());
+    r.base = std::uint64_t(cfg.base_vocab) * D;
+    for (const auto& kv : cfg.sub_vocab) r.sub_tables += kv.second * d;
+    if (cfg.variant == ne_variant::subtable_v2) r.projections = std::uint64_t(cfg.branch_count()) * D * d;
+    r.total = r.base + r.sub_tables + r.projections;
+    return r;
+}
+
+budget_info budget_report(std::uint64_t embedding_params, std::uint64_t other_params) {
+    budget_info b;
+    b.embedding_params = embedding_params;
+    b.other_params = other_params;
+    const double all = double(embedding_params) + double(other_params);
+    b.fraction = all > 0.0 ? double(embedding_params) / all : 0.0;
+    b.over_budget = b.fraction > 0.5;
+    return b;
+}
+
+budget_info budget_report(const ngram_config& cfg, std::uint64_t other_params) {
+    return budget_report(param_count(cfg).total, other_params);
+}
+
+std::string budget_guidance(const budget_info& info) {
+    std::string s = "embedding parameters take " + std::to_string(int(info.fraction * 100.0 + 0.5)) +
+                    "% of the total budget; keep this at or below 50%. ";
+    if (info.over_budget)
+        s += "This configuration is over budget: past the halfway point the same parameters buy more as FFN "
+             "capacity. ";
+    s += "Reference point: a production 68.5B-parameter model allocates 31.4B parameters (46% of the total) to "
+         "n-gram embeddings.";
+    return s;
+}
+
+namespace {
+void put_f32(std::ofstream& f, const std::vector<float>& v) {
+    f.write(reinterpret_cast<const char*>(v.data()), std::streamsize(v.size() * 4));
+}
+void get_f32(std::ifstream& f, std::vector<float>& v, const std::string& path) {
+    f.read(reinterpret_cast<char*>(v.data()), std::streamsize(v.size() * 4));
+    if (!f) throw parse_error("bank file truncated: " + path, 0, std::size_t(f.gcount()));
+}
+}  // namespace
+
+void save_bank(const embedding_bank& bank, const std::string& path) {
+    std::ofstream f(path, std::ios::binary);
+    if (!f) throw io_error("cannot write bank file: " + path);
+    const std::string head = to_json_string(bank.config);
+    const std::uint32_t n = std::uint32_t(head.size());
+    const unsigned char len[4] = {static_cast<unsigned char>(n), static_cast<unsigned char>(n >> 8),
+                                  static_cast<unsigned char>(n >> 16), static_cast<unsigned char>(n >> 24)};
+    f.write(reinterpret_cast<const char*>(len), 4);
+    f.write(head.data(), std::streamsize(head.size()));
+    put_f32(f, bank.base);
+    for (const auto& t : bank.sub_tables) put_f32(f, t);
+    for (const auto& w : bank.projections) put_f32(f, w);
+    if (bank.config.amplification == amp_mode::layer_norm) {
+        put_f32(f, bank.ln_gain);
+        put_f32(f, bank.ln_bias);
+    }
+    if (!f) throw io_error("short write to bank file: " + path);
+}
+
+embedding_bank load_bank(const std::string& path) {
+    std::ifstream f(path, std::ios::binary);
+    if (!f) throw io_error("cannot open bank file: " + path);
+    unsigned char len[4];
+    f.read(reinterpret_cast<char*>(len), 4);
+    if (!f) throw parse_error("bank file too short for header: " + path, 0, 0);
+    const std::uint32_t n = std::uint32_t(len[0]) | (std::uint32_t(len[1]) << 8) | (std::uint32_t(len[2]) << 16) |
+                            (std::uint32_t(len[3]) << 24);
+    std::string head(n, '\0');
+    f.read(head.data(), std::streamsize(n));
+    if (!f) throw parse_error("bank file truncated in header: " + path, 0, 4);
+    ngram_config cfg;
+    try {
+        cfg = ngram_config_from_json(head);
+    } catch (const nlohmann::json::exception& e) {
+        throw parse_error(std::string("bad bank header JSON: ") + e.what(), 0, 4);
+    }
+    embedding_bank bank = make_zero_bank<float>(cfg);
+    get_f32(f, bank.base, path);
+    for (auto& t : bank.sub_tables) get_f32(f, t, path);
+    for (auto& w : bank.projections) get_f32(f, w, path);
+    if (cfg.amplification == amp_mode::layer_norm) {
+        get_f32(f, bank.ln_gain, path);
+        get_f32(f, bank.ln_bias, path);
+    }
+    char extra;
+    if (f.read(&extra, 1)) throw parse_error("bank file longer than its header declares: " + path, 0, 0);
+    return bank;
+}
+
 // ---------------------------------------------------------------- per-layer FFN (ple.hpp)
 namespace {
 using plne_ptr = std::unique_ptr<ngram_plne, int (*)(ngram_plne*)>;

@@ -418,6 +418,27 @@ int main() {
         CHECK(row);
         CHECK(g1.table[3 * 6] == 0.0f);
     });
+    test_case("param_count / budget_report / save_bank round trip", [] {  // test_embedding.cpp accounting
+        const auto cfg = make_default_config(1000, 256, 3, 2);
+        const auto pc = param_count(cfg);
+        CHECK(pc.base == 1000ull * 256);
+        CHECK(pc.projections == 4ull * 256 * 64);
+        CHECK(pc.total == pc.base + pc.sub_tables + pc.projections);
+        const auto b = budget_report(cfg, pc.total);
+        CHECK(b.fraction == 0.5 && !b.over_budget);
+        CHECK(budget_report(3, 1).over_budget);
+        CHECK(budget_guidance(budget_report(3, 1)).find("over budget") != std::string::npos);
+        auto host = make_bank<float>(make_default_config(50, 128, 3, 1), 4);
+        const std::string path = "/tmp/ngram_dropin_bank.bin";
+        save_bank(host, path);
+        const auto back = load_bank(path);
+        CHECK(back.base == host.base && back.sub_tables == host.sub_tables && back.projections == host.projections);
+        CHECK(back.config == host.config);
+        CHECK_THROWS_AS(load_bank("/nonexistent/dir/bank.bin"), io_error);
+        const device_bank a(host), c = device_bank::from_file(path, host.config);
+        std::vector<token_id> seq{1, 2, 3, 4, 5};
+        CHECK(embed_sequence(seq, a) == embed_sequence(seq, c));
+    });
     std::printf("%d checks, %d failures\n", g_checks, g_fail);
     return g_fail == 0 ? 0 : 1;
 }
