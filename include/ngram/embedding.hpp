@@ -182,6 +182,24 @@ std::string budget_guidance(const budget_info& info);
 void save_bank(const embedding_bank& bank, const std::string& path);
 embedding_bank load_bank(const std::string& path);
 
+// bank_cast (embedding.hpp:140-156): element-wise conversion of a host bank.
+template <typename From, typename To>
+embedding_bank_t<To> bank_cast(const embedding_bank_t<From>& bank) {
+    auto conv = [](const std::vector<From>& v) { return std::vector<To>(v.begin(), v.end()); };
+    embedding_bank_t<To> out;
+    out.config = bank.config;
+    out.base = conv(bank.base);
+    for (const auto& t : bank.sub_tables) out.sub_tables.push_back(conv(t));
+    for (const auto& p : bank.projections) out.projections.push_back(conv(p));
+    out.ln_gain = conv(bank.ln_gain);
+    out.ln_bias = conv(bank.ln_bias);
+    return out;
+}
+
+// amplify (embedding.hpp:239-287) of one merged row, on the device (float).
+void amplify(std::span<const float> e, amp_mode mode, std::span<const float> gain, std::span<const float> bias,
+             std::span<float> out);
+
 // zeros_like (embedding.hpp:123-134): a zero bank of the same shape (the gradient store).
 template <typename T>
 embedding_bank_t<T> zeros_like(const embedding_bank_t<T>& bank) {

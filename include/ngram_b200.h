@@ -229,6 +229,11 @@ int ngram_shard_scatter_rows(ngram_shard_group* g, const uint32_t* all_tokens, c
 int ngram_shard_project(ngram_shard_group* g, const uint32_t* home_tokens, int64_t home_T, void* rows_out,
                         void* merged_out, int out_dtype, void* stream);
 
+/* amplify (embedding.hpp:239-287) of `rows` HOST rows of width D on the current device:
+ * amp_mode 0 none, 1 scale_sqrt_d, 2 layer_norm (gain / bias of size D). Synchronous. */
+int ngram_amplify_host(int amp_mode, int D, int64_t rows, const float* gain, const float* bias, const float* in,
+                       float* out);
+
 /* ------------------------------------------------------------------ backward (training) */
 /* embed_sequence_backward (embedding.hpp:438-459) batched on the device: gradients of the
  * embedding rows w.r.t. every bank parameter, ACCUMULATED (+=) into an fp32 gradient bank

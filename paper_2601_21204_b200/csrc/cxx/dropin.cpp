@@ -514,6 +514,17 @@ draft_result draft_verify(sequence_cache& state, embedding_memo&, const device_b
     return draft_verify(state, bank, draft, accept_count, counters, opts);
 }
 
+void amplify(std::span<const float> e, amp_mode mode, std::span<const float> gain, std::span<const float> bias,
+             std::span<float> out) {
+    const std::size_t D = e.size();
+    if (out.size() != D) throw std::invalid_argument("amplify: output size mismatch");
+    if (mode == amp_mode::layer_norm && (gain.size() != D || bias.size() != D))
+        throw std::invalid_argument("amplify: layer_norm needs gain/bias of size D");
+    const int m = mode == amp_mode::none ? 0 : mode == amp_mode::scale_sqrt_d ? 1 : 2;
+    throw_status(ngram_amplify_host(m, int(D), D ? 1 : 0, m == 2 ? gain.data() : nullptr,
+                                    m == 2 ? bias.data() : nullptr, e.data(), out.data()));
+}
+
 // ---------------------------------------------------------------- accounting / serialization
 param_count_report param_count(const ngram_config& cfg) {
     cfg.validate();

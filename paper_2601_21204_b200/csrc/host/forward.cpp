@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -263,6 +264,37 @@ extern "C" {
 const char* ngram_last_error(void) { return g_last_error.c_str(); }
 const char* ngram_version(void) { return "ngram_b200 0.1 (sm_100a)"; }
 uint64_t ngram_kernel_launches(void) { return ngk::launches(); }
+
+// amplify (embedding.hpp:239-287) of `rows` host rows of width D on the current device.
+int ngram_amplify_host(int amp_mode, int D, int64_t rows, const float* gain, const float* bias, const float* in,
+                       float* out) {
+    NGRAM_API_BEGIN
+    if (D < 1 || rows < 0 || amp_mode < 0 || amp_mode > 2 || (rows > 0 && (!in || !out)))
+        throw Error(NGRAM_EINVAL, "ngram_amplify_host: bad argument");
+    if (amp_mode == 2 && (!gain || !bias)) throw Error(NGRAM_EINVAL, "amplify: layer_norm needs gain/bias of size D");
+    if (rows == 0) return NGRAM_OK;
+    const size_t n = size_t(rows) * size_t(D);
+    DevBuf<float> din, dout, g, b;
+    DevBuf<unsigned long long> err;
+    din.alloc(n);
+    dout.alloc(n);
+    NGH_CUDA(cudaMemcpy(din.p, in, n * 4, cudaMemcpyHostToDevice));
+    if (amp_mode == 2) {
+        g.alloc(size_t(D));
+        b.alloc(size_t(D));
+        err.alloc(1);
+        NGH_CUDA(cudaMemcpy(g.p, gain, size_t(D) * 4, cudaMemcpyHostToDevice));
+        NGH_CUDA(cudaMemcpy(b.p, bias, size_t(D) * 4, cudaMemcpyHostToDevice));
+        NGH_CUDA(cudaMemset(err.p, 0xff, sizeof(unsigned long long)));
+        ngk::Shape s{};
+        s.D = D;
+        ngk::launch_layernorm_rows(s, din.p, g.p, b.p, dout.p, nullptr, 0, rows, err.p, nullptr);
+    } else {
+        ngk::launch_scale(din.p, dout.p, int64_t(n), amp_mode == 1 ? float(std::sqrt(double(D))) : 1.0f, nullptr);
+    }
+    NGH_CUDA(cudaMemcpy(out, dout.p, n * 4, cudaMemcpyDeviceToHost));
+    NGRAM_API_END
+}
 
 int ngram_config_validate(const char* config_json) {
     NGRAM_API_BEGIN

@@ -89,6 +89,9 @@ void launch_silu_gate(const float* U, const float* G, float* Hh, int64_t n, cons
 void launch_silu_gate_backward(const float* dHh, const float* U, const float* G, float* dG, float* dU, int64_t n,
                                const unsigned long long* err, cudaStream_t st);
 
+// standalone amplify (simt.cu): out = in * s
+void launch_scale(const float* in, float* out, int64_t n, float s, cudaStream_t st);
+
 struct FwdArgs {
     Shape s;
     const HashTables* ht;

@@ -202,6 +202,21 @@ void launch_gather_rows(const Shape& s, const int32_t* grow, int64_t Tpad, int64
     count_launch();
 }
 
+namespace {
+__global__ void scale_rows_kernel(const float* __restrict__ in, float* __restrict__ out, int64_t n, float s) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = in[i] * s;
+}
+}  // namespace
+
+void launch_scale(const float* in, float* out, int64_t n, float s, cudaStream_t st) {
+    if (n <= 0) return;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    scale_rows_kernel<<<(unsigned)blocks, 256, 0, st>>>(in, out, n, s);
+    count_launch();
+}
+
 void launch_layernorm_rows(const Shape& s, const float* merged, const float* gain, const float* bias, void* rows,
                            void* merged_copy, int out_bf16, int64_t T, const unsigned long long* err,
                            cudaStream_t st) {

@@ -439,6 +439,32 @@ int main() {
         std::vector<token_id> seq{1, 2, 3, 4, 5};
         CHECK(embed_sequence(seq, a) == embed_sequence(seq, c));
     });
+    test_case("amplify (device) matches the reference formulas; bank_cast round trip", [] {
+        rng64 rng(17);
+        std::vector<float> e(300), gain(300), bias(300), out(300);
+        for (auto& v : e) v = float(gaussian(rng));
+        for (auto& v : gain) v = 1.0f + 0.1f * float(gaussian(rng));
+        for (auto& v : bias) v = 0.05f * float(gaussian(rng));
+        amplify(e, amp_mode::none, {}, {}, out);
+        CHECK(out == e);
+        amplify(e, amp_mode::scale_sqrt_d, {}, {}, out);
+        const float s = float(std::sqrt(300.0));
+        for (int i = 0; i < 300; ++i) CHECK(out[i] == e[i] * s);
+        amplify(e, amp_mode::layer_norm, gain, bias, out);
+        double mean = 0, var = 0;
+        for (float v : e) mean += v;
+        mean /= 300;
+        for (float v : e) var += (v - mean) * (v - mean);
+        var /= 300;
+        std::vector<float> want(300);
+        for (int i = 0; i < 300; ++i) want[i] = float(gain[i] * (e[i] - mean) / std::sqrt(var + 1e-5) + bias[i]);
+        CHECK(close_rows(out, want, 1e-5));
+        CHECK_THROWS_AS(amplify(e, amp_mode::layer_norm, std::span<const float>(gain).first(3), bias, out),
+                        std::invalid_argument);
+        const auto host = make_bank<float>(make_default_config(40, 64, 3, 1), 2);
+        const auto back = bank_cast<double, float>(bank_cast<float, double>(host));
+        CHECK(back.base == host.base && back.sub_tables == host.sub_tables);
+    });
     std::printf("%d checks, %d failures\n", g_checks, g_fail);
     return g_fail == 0 ? 0 : 1;
 }
