@@ -100,9 +100,6 @@ ngram_bank::~ngram_bank() {
     DeviceGuard g(device);
     for (auto& e : prof_ev)
         if (e) cudaEventDestroy(e);
-    for (auto& e : chunk_ev)
-        if (e) cudaEventDestroy(e);
-    if (side_stream) cudaStreamDestroy(side_stream);
     for (int i = 0; i < 2; ++i) {
         if (host_streams[i]) cudaStreamDestroy(host_streams[i]);
         if (pinned[i]) cudaFreeHost(pinned[i]);

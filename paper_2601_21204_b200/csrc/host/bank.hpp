@@ -72,7 +72,6 @@ struct Workspace {
     DevBuf<uint32_t> prior;
     XBuf xbuf;                      // K2 output / K3 A operand
     DevBuf<float> splitk;           // small-T split-K partial sums
-    DevBuf<int> ready;              // fused K1+K2+K3: per-128-row X readiness counters
 };
 
 }  // namespace ngh
@@ -106,9 +105,6 @@ struct ngram_bank {
     void* pinned[2] = {nullptr, nullptr};
     size_t pinned_bytes = 0;
 
-    // chunked K2/K3 overlap (NGRAM_OVERLAP_CHUNKS)
-    cudaStream_t side_stream = nullptr;
-    cudaEvent_t chunk_ev[9] = {};
     // stage profiling (ngram_profile_enable)
     bool prof = false;
     cudaEvent_t prof_ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -149,8 +145,8 @@ struct HashCtx {
 };
 void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, int64_t gstride, int64_t T,
                     void* rows, void* merged, int out_bf16, float* ln_scratch, const CUtensorMap* tmap_x,
-                    cudaStream_t st, int amp, XBuf* xb, bool allow_splitk, const ngk::FusedX* fx,
-                    const ngk::DecodeCommit* commit, int64_t x_row0 = 0, const HashCtx* hc = nullptr);
+                    cudaStream_t st, int amp, XBuf* xb, bool allow_splitk, const ngk::DecodeCommit* commit,
+                    const HashCtx* hc = nullptr);
 bool forward_tokens(ngram_bank* b, const uint32_t* tokens, const int64_t* seq_off, int64_t nseq, int64_t T,
                     const uint32_t* prior, void* rows, void* merged, int out_bf16, cudaStream_t st, int amp,
                     XBuf* xb, int32_t* grow, bool allow_splitk, const ngk::DecodeCommit* commit,

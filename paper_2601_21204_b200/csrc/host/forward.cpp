@@ -42,30 +42,6 @@ static bool fused_gather(int D) {
     return env >= 0 ? env != 0 : D <= 1024;
 }
 
-// K1+K2+K3 in one kernel (forward_tc2_kernel<true>, gather warps beside the MMA
-// pipeline).  Correct (tested) but measured slower on B200 than the fused K1+K2 kernel
-// followed by K3 (1.46 vs 1.10 ms at config C, profiles/README.md), so opt-in:
-// NGRAM_FUSEDX=1.
-static bool use_fusedx(ngram_bank* b, int64_t T) {
-    static const int env = [] {
-        const char* e = getenv("NGRAM_FUSEDX");
-        return e ? atoi(e) : 0;
-    }();
-    return env && b->tc_path && T > 256 && !fused_gather(b->shape.D) && b->shape.D % 256 == 0 &&
-           b->shape.N <= 4 && b->shape.B <= 32;
-}
-
-// Chunked overlap of K2 (side stream) with K3 for long batches: NGRAM_OVERLAP_CHUNKS
-// (default 0 = off, <= 8).
-static int overlap_chunks(ngram_bank* b, int64_t T) {
-    static const int env = [] {
-        const char* e = getenv("NGRAM_OVERLAP_CHUNKS");
-        return e ? std::min(8, std::max(0, atoi(e))) : 0;
-    }();
-    if (env < 2 || T < int64_t(env) * 4096 || !b->tc_path) return 1;
-    return env;
-}
-
 static bool small_t(const ngram_bank* b, int64_t T) { return ngk::small_t_regime(b->shape.D, T, b->num_sms); }
 
 // Small-T split-K GEMM with the hash in its producers (MODE 2), opt-in NGRAM_DECODE_HASH_IN_GEMM=1:
@@ -84,8 +60,8 @@ static bool hash_in_gemm(const ngram_bank* b) {
 // merged/rows per the amplification; LayerNorm via a third kernel.
 void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, int64_t gstride, int64_t T,
                     void* rows, void* merged, int out_bf16, float* ln_scratch, const CUtensorMap* tmap_x,
-                    cudaStream_t st, int amp, XBuf* xb, bool allow_splitk, const ngk::FusedX* fx,
-                    const ngk::DecodeCommit* commit, int64_t x_row0, const HashCtx* hc) {
+                    cudaStream_t st, int amp, XBuf* xb, bool allow_splitk, const ngk::DecodeCommit* commit,
+                    const HashCtx* hc) {
     if (b->hash_only) throw Error(NGRAM_EINVAL, "bank was created hash-only (NGRAM_BANK_HASH_ONLY)");
     if (b->tc_path && ((reinterpret_cast<uintptr_t>(rows) | reinterpret_cast<uintptr_t>(merged)) & 15) != 0)
         throw Error(NGRAM_EINVAL, "output buffers must be 16-byte aligned (tensor-core path: vector / TMA stores)");
@@ -109,7 +85,6 @@ void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, 
     a.tmap_w2 = &b->tmap_w2;
     a.tmap_x = tmap_x;
     a.commit = commit;
-    a.x_row0 = x_row0;
     const bool ln = a.s.amp == 2;
     float* ln_merged = nullptr;
     if (ln) {
@@ -156,8 +131,7 @@ void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, 
             b->ws.splitk.ensure(need);
             ws = b->ws.splitk.p;
         }
-        if (fx) ngk::launch_forward_tc2_fusedx(a, *fx, b->num_sms, st);
-        else ngk::launch_forward_tc(a, b->num_sms, st, ws);
+        ngk::launch_forward_tc(a, b->num_sms, st, ws);
     } else {
         ngk::launch_forward_simt(a, st);
     }
@@ -178,59 +152,16 @@ bool forward_tokens(ngram_bank* b, const uint32_t* tokens, const int64_t* seq_of
     bool fused_commit = false;
     const int64_t Tpad = round_up(std::max<int64_t>(T, 1), kRowPad);
     b->prof_record(0, st);
-    if (use_fusedx(b, T)) {
-        // K1 + K2 + K3 in one persistent kernel (gather warps overlap the projection)
-        if (!xb) xb = &b->ws.xbuf;
-        xb->ensure(Tpad, b->shape.D);
-        const int64_t nblk = (T + 127) / 128;
-        b->ws.ready.ensure(size_t(nblk));
-        NGH_CUDA(cudaMemsetAsync(b->ws.ready.p, 0, size_t(nblk) * sizeof(int), st));
-        ngk::launch_validate_tokens(b->shape, tokens, T, seq_off, nseq, prior, b->err.p, st);
-        b->prof_record(1, st);
-        ngk::FusedX fx{seq_off, nseq, prior, xb->x.p, b->ws.ready.p};
-        run_projection(b, tokens, nullptr, Tpad, T, rows, merged, out_bf16, b->ws.merged_f32.p, &xb->map, st, amp,
-                       nullptr, false, &fx, nullptr);
-    } else if (b->tc_path && allow_splitk && T <= 256 && hash_in_gemm(b)) {  // MODE 2: T <= 256 only
+    if (b->tc_path && allow_splitk && T <= 256 && hash_in_gemm(b)) {  // MODE 2: T <= 256 only
         // decode / verify: K1 fused into the split-K GEMM's producers (2 launches per step)
         b->prof_record(1, st);
         fused_commit = commit != nullptr;
         const HashCtx hc{seq_off, nseq, prior};
         run_projection(b, tokens, nullptr, Tpad, T, rows, merged, out_bf16, b->ws.merged_f32.p, nullptr, st, amp,
-                       nullptr, true, nullptr, fused_commit ? commit : nullptr, 0, &hc);
+                       nullptr, true, fused_commit ? commit : nullptr, &hc);
     } else if (b->tc_path && ((allow_splitk && small_t(b, T)) || !fused_gather(b->shape.D))) {
         if (!xb) xb = &b->ws.xbuf;
         xb->ensure(Tpad, b->shape.D);
-        const int nchunk = overlap_chunks(b, T);
-        if (nchunk > 1) {
-            // K2 of chunk c+1 (side stream) overlaps K3 of chunk c (caller's stream)
-            if (!b->side_stream) {
-                NGH_CUDA(cudaStreamCreateWithFlags(&b->side_stream, cudaStreamNonBlocking));
-                for (auto& e : b->chunk_ev) NGH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-            }
-            NGH_CUDA(cudaEventRecord(b->chunk_ev[0], st));
-            NGH_CUDA(cudaStreamWaitEvent(b->side_stream, b->chunk_ev[0], 0));
-            int64_t bounds[9];
-            for (int c = 0; c <= nchunk; ++c) bounds[c] = std::min<int64_t>(T, round_up(T * c / nchunk, kRowPad));
-            for (int c = 0; c < nchunk; ++c) {
-                ngk::launch_hash_gather(b->shape, b->ht.p, tokens, seq_off, nseq, T, prior, b->sub.p, xb->x.p,
-                                        nullptr, Tpad, b->err.p, b->side_stream, bounds[c], bounds[c + 1]);
-                NGH_CUDA(cudaEventRecord(b->chunk_ev[1 + c], b->side_stream));
-            }
-            b->prof_record(1, st);
-            for (int c = 0; c < nchunk; ++c) {
-                NGH_CUDA(cudaStreamWaitEvent(st, b->chunk_ev[1 + c], 0));
-                const int64_t c0 = bounds[c], n = bounds[c + 1] - c0;
-                const size_t esz = out_bf16 ? 2 : 4;
-                auto off = [&](void* p) -> void* {
-                    return p ? static_cast<uint8_t*>(p) + size_t(c0) * size_t(b->shape.D) * esz : nullptr;
-                };
-                run_projection(b, tokens + c0, nullptr, Tpad, n, off(rows), off(merged), out_bf16,
-                               b->ws.merged_f32.p ? b->ws.merged_f32.p + size_t(c0) * size_t(b->shape.D) : nullptr,
-                               &xb->map, st, amp, nullptr, false, nullptr, nullptr, c0);
-            }
-            b->prof_record(3, st);
-            return false;
-        }
         if (T <= 1024)
             ngk::launch_hash_gather_rows(b->shape, b->ht.p, tokens, seq_off, nseq, T, prior, b->sub.p, xb->x.p,
                                          b->err.p, st, uniform_len);
@@ -240,12 +171,12 @@ bool forward_tokens(ngram_bank* b, const uint32_t* tokens, const int64_t* seq_of
         b->prof_record(1, st);
         fused_commit = commit != nullptr;  // every tensor-core projection path consumes it
         run_projection(b, tokens, nullptr, Tpad, T, rows, merged, out_bf16, b->ws.merged_f32.p, &xb->map, st, amp,
-                       nullptr, allow_splitk, nullptr, fused_commit ? commit : nullptr);
+                       nullptr, allow_splitk, fused_commit ? commit : nullptr);
     } else {
         ngk::launch_hash_ids(b->shape, b->ht.p, tokens, seq_off, nseq, T, prior, nullptr, 0, grow, Tpad, b->err.p, st);
         b->prof_record(1, st);
         run_projection(b, tokens, grow, Tpad, T, rows, merged, out_bf16, b->ws.merged_f32.p, nullptr, st, amp, xb,
-                       allow_splitk, nullptr, nullptr);
+                       allow_splitk, nullptr);
     }
     b->prof_record(3, st);
     return fused_commit;
@@ -371,7 +302,7 @@ int ngram_embed_from_ids(ngram_bank* b, const uint32_t* tokens, const uint64_t* 
     ngk::launch_ids_to_rows(b->shape, b->ht.p, ids, tokens, T, b->ws.grow.p, Tpad, b->err.p, st);
     // embed_from_ids returns the merged (pre-amplification) vector: run with amp = none.
     run_projection(b, tokens, b->ws.grow.p, Tpad, T, nullptr, merged_out, out_dtype == NGRAM_BF16, nullptr, nullptr,
-                   st, 0, nullptr, true, nullptr, nullptr);
+                   st, 0, nullptr, true, nullptr);
     NGRAM_API_END
 }
 
@@ -483,7 +414,7 @@ int ngram_embed_sequence_host(ngram_bank* b, const uint32_t* tokens, const int64
         void* dmerged = merged_out ? b->host_merged[slot].p : nullptr;
         run_projection(b, b->ws.tokens.p + c0, b->ws.grow.p + c0, Tpad, n, drows, dmerged, out_dtype == NGRAM_BF16,
                        b->ws.merged_f32.p ? b->ws.merged_f32.p + size_t(c0) * size_t(D) : nullptr, nullptr, st, -1,
-                       &b->host_x[slot], small_t(b, T), nullptr, nullptr);  // chunks keep the batch's regime
+                       &b->host_x[slot], small_t(b, T), nullptr);  // chunks keep the batch's regime
         const size_t bytes = size_t(n) * size_t(D) * esz;
         if (direct) {
             if (rows_out)

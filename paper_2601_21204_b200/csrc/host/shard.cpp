@@ -142,7 +142,7 @@ int ngram_shard_project(ngram_shard_group* g, const uint32_t* home_tokens, int64
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     XBuf& xb = g->x[g->parity];
     run_projection(b, home_tokens, nullptr, round_up(std::max<int64_t>(home_T, 1), kRowPad), home_T, rows_out,
-                   merged_out, out_dtype == NGRAM_BF16, b->ws.merged_f32.p, &xb.map, st, -1, nullptr, false, nullptr, nullptr);
+                   merged_out, out_dtype == NGRAM_BF16, b->ws.merged_f32.p, &xb.map, st, -1, nullptr, false, nullptr);
     g->parity ^= 1;
     NGRAM_API_END
 }

@@ -70,20 +70,17 @@ struct TcParams {
     float scale, amp;
     const unsigned long long* err;
     int use_x;  // A operand from materialised X (tmap_a is X) instead of gathered sub-table rows
-    int64_t x_row0;  // first X row of this call (chunked K2/K3 overlap)
     int epi_skip;  // diagnostics only (NGRAM_DEBUG_EPI_SKIP): 1 drain TMEM without loads/stores,
                    // 2 (pair kernel) skip the E0 loads, 3 (pair kernel) skip the output stores
     int diag_skip_a;  // diagnostics only (NGRAM_DEBUG_SKIP_A): X-path pair kernel loads W tiles only
     int pdl;          // launched with programmatic stream serialization (decode chain)
     int ksplit;      // split-K factor (small-T path); >1 => raw fp32 partials to `partial`
     float* partial;  // [ksplit][T][D] fp32
-    // fused K1+K2 (forward_tc2_kernel<true>): gather warps fill X, producers wait on `ready`
+    // MODE 2 (small-T GEMM hashing in its producers): the windows of `tokens`
     const HashTables* ht;
     const int64_t* seq_off;
     int64_t nseq;
     const uint32_t* prior;
-    __nv_bfloat16* xw;
-    int* ready;
 };
 
 __device__ __forceinline__ void store_chunk(void* out, int out_bf16, int64_t o, const float (&mv)[32]) {
@@ -172,7 +169,7 @@ __global__ void __launch_bounds__(Cfg<BN, NP>::kThreads, 1)
                     if (lane == 0) {
                         uint8_t* a_dst = smem + stage * C::kStageBytes;
                         mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
-                        tma_load_2d(a_dst, &tmap_a, &full[stage], kb * BK, (int32_t)(m * BM + p.x_row0));
+                        tma_load_2d(a_dst, &tmap_a, &full[stage], kb * BK, (int32_t)(m * BM));
                         tma_load_2d_hint(a_dst + C::kABytes, &tmap_w, &full[stage], kb * BK, n * BN, pol_w);
                     }
                     __syncwarp();
@@ -469,14 +466,12 @@ struct Cfg2 {
     static constexpr int smem_bytes(int epi) {
         return stages2(epi) * kStageBytes + epi_smem(epi) + 1024 + 512;
     }
-    // Warp roles: producers [0, NP2), epilogue [NP2, NP2+8), gather warps (fused K1+K2
-    // variant) next, and the single MMA-issuing warp LAST: the warp arbiter picks the
-    // highest eligible warp id first, so the tensor-core issue is never starved.
+    // Warp roles: producers [0, NP2), epilogue [NP2, NP2+8), and the single MMA-issuing warp
+    // LAST: the warp arbiter picks the highest eligible warp id first, so the tensor-core
+    // issue is never starved.
     static constexpr int kEpiWarp0 = NP2;
-    static constexpr int kGatherWarp0 = NP2 + kEpiWarps2;
-    static constexpr int kGatherWarps = 4;
+    static constexpr int kMmaWarp = NP2 + kEpiWarps2;
     static constexpr int kThreads = (NP2 + kEpiWarps2 + 1) * 32;
-    static constexpr int kThreadsFX = kThreads + kGatherWarps * 32;
     static constexpr int kRowsPerWarp = 128 / NP2;
 };
 
@@ -522,14 +517,14 @@ __device__ __forceinline__ void epi_store_box(uint8_t* obuf, int lane, const flo
     }
 }
 
-template <bool FX, int EPI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FX ? Cfg2::kThreadsFX : Cfg2::kThreads, 1)
+template <int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::kThreads, 1)
     forward_tc2_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_w,
                        const __grid_constant__ CUtensorMap tmap_rows, const __grid_constant__ CUtensorMap tmap_merged,
                        const __grid_constant__ CUtensorMap tmap_e0, TcParams p) {
     using C = Cfg2;
     constexpr int kStages2 = stages2(EPI);  // shadows the namespace constant
-    constexpr int kMmaWarp = FX ? C::kGatherWarp0 + C::kGatherWarps : C::kGatherWarp0;
+    constexpr int kMmaWarp = C::kMmaWarp;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* staging = smem + kStages2 * C::kStageBytes;
@@ -588,19 +583,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FX ? Cfg2::kThreadsF
             const int64_t t0 = m * BM2 + (int64_t)rank * 128;  // this CTA's first token row
             const int wrow = n * BN2 + (int)rank * (BN2 / 2);  // this CTA's first W row
             if (p.use_x) {
-                if (FX && warp == 0) {
-                    // wait until the gather warps (any CTA) have written this CTA's 128 X rows
-                    if (lane == 0 && t0 < p.T) {
-                        const int need = (int)(p.T - t0 < 128 ? p.T - t0 : 128);
-                        const int* flag = p.ready + (t0 >> 7);
-                        uint32_t spins = 0;
-                        while (ld_relaxed_gpu(flag) < need)
-                            if (++spins == (1u << 24)) __trap();  // never legit: trap, don't hang
-                        fence_acq_rel_gpu();         // acquire the gather warps' X writes
-                        fence_proxy_async_global();  // generic-proxy X writes -> TMA reads
-                    }
-                    __syncwarp();
-                }
                 for (int kb = 0; kb < KB; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (warp == 0 && lane == 0) {
@@ -609,7 +591,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FX ? Cfg2::kThreadsF
                             mbar_arrive_expect_tx(&full[stage], p.diag_skip_a ? 2 * C::kBBytes : 2 * C::kStageBytes);
                         if (!p.diag_skip_a)
                             tma_load_2d_2cta(a_dst, &tmap_a, leader_bar(&full[stage]), kb * BK,
-                                             (int32_t)(t0 + p.x_row0), 0);
+                                             (int32_t)t0, 0);
                         tma_load_2d_2cta(a_dst + C::kABytes, &tmap_w, leader_bar(&full[stage]), kb * BK, wrow, pol_w);
                     }
                     __syncwarp();
@@ -682,20 +664,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FX ? Cfg2::kThreadsF
                     acc_phase ^= 1;
                 }
             }
-        }
-    } else if (FX && warp >= C::kGatherWarp0) {
-        // ------------------------------------------------------------ gather warps (K1 + K2)
-        // position t is gathered by global gather warp t % (#CTAs x 4): early X blocks become
-        // ready first, all SMs share the gather; each finished position bumps ready[t / 128].
-        const int64_t gid = (int64_t)blockIdx.x * C::kGatherWarps + (warp - C::kGatherWarp0);
-        const int64_t ngw = (int64_t)gridDim.x * C::kGatherWarps;
-        for (int64_t t = gid; t < p.T; t += ngw) {
-            uint32_t w[4];
-            load_window<4>(p.s, p.tokens, p.seq_off, p.nseq, p.prior, t, w);  // validated before launch
-            gather_position<4, 12>(p.s, p.ht, w, p.sub, p.xw + t * (int64_t)D, nullptr, 0, t, lane);
-            fence_acq_rel_gpu();  // this lane's X stores before the warp's release below
-            __syncwarp();
-            if (lane == 0) red_release_gpu_add(p.ready + (t >> 7), 1);
         }
     } else if (EPI) {
         // ------------------------------------------------------------ TMA epilogue (both CTAs)
@@ -902,7 +870,6 @@ void launch_cfg(const FwdArgs& a, int num_sms, cudaStream_t st, int ksplit = 1, 
     p.amp = a.s.amp == kAmpSqrt ? (float)__builtin_sqrt((double)a.s.D) : 1.0f;
     p.err = a.err;
     p.use_x = a.tmap_x != nullptr;
-    p.x_row0 = a.x_row0;
     p.epi_skip = getenv("NGRAM_DEBUG_EPI_SKIP") ? atoi(getenv("NGRAM_DEBUG_EPI_SKIP")) : 0;
     p.diag_skip_a = getenv("NGRAM_DEBUG_SKIP_A") ? 1 : 0;
     p.ht = a.ht;
@@ -962,7 +929,6 @@ void launch_tc2(const FwdArgs& a, int num_sms, cudaStream_t st) {
     p.amp = a.s.amp == kAmpSqrt ? (float)__builtin_sqrt((double)a.s.D) : 1.0f;
     p.err = a.err;
     p.use_x = a.tmap_x != nullptr;
-    p.x_row0 = a.x_row0;
     p.epi_skip = getenv("NGRAM_DEBUG_EPI_SKIP") ? atoi(getenv("NGRAM_DEBUG_EPI_SKIP")) : 0;
     p.diag_skip_a = getenv("NGRAM_DEBUG_SKIP_A") ? 1 : 0;
     const int64_t tiles = ((a.T + BM2 - 1) / BM2) * (a.s.D / BN2);
@@ -978,13 +944,13 @@ void launch_tc2(const FwdArgs& a, int num_sms, cudaStream_t st) {
     const unsigned grid = (unsigned)(2 * pairs);
     const CUtensorMap& me = a.tmap_e0 ? *a.tmap_e0 : *a.tmap_w2;
     if (epi == 1) {
-        cudaFuncSetAttribute(forward_tc2_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(forward_tc2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              Cfg2::smem_bytes(1));
-        forward_tc2_kernel<false, 1><<<grid, Cfg2::kThreads, Cfg2::smem_bytes(1), st>>>(ma, *a.tmap_w2, mr, mm, me, p);
+        forward_tc2_kernel<1><<<grid, Cfg2::kThreads, Cfg2::smem_bytes(1), st>>>(ma, *a.tmap_w2, mr, mm, me, p);
     } else {
-        cudaFuncSetAttribute(forward_tc2_kernel<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(forward_tc2_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              Cfg2::smem_bytes(0));
-        forward_tc2_kernel<false, 0><<<grid, Cfg2::kThreads, Cfg2::smem_bytes(0), st>>>(ma, *a.tmap_w2, mr, mm, me, p);
+        forward_tc2_kernel<0><<<grid, Cfg2::kThreads, Cfg2::smem_bytes(0), st>>>(ma, *a.tmap_w2, mr, mm, me, p);
     }
     count_launch();
 }
@@ -1007,7 +973,6 @@ TcParams tc2_params(const FwdArgs& a) {
     p.amp = a.s.amp == kAmpSqrt ? (float)__builtin_sqrt((double)a.s.D) : 1.0f;
     p.err = a.err;
     p.use_x = 1;
-    p.x_row0 = a.x_row0;
     p.epi_skip = getenv("NGRAM_DEBUG_EPI_SKIP") ? atoi(getenv("NGRAM_DEBUG_EPI_SKIP")) : 0;
     p.diag_skip_a = getenv("NGRAM_DEBUG_SKIP_A") ? 1 : 0;
     return p;
@@ -1093,25 +1058,6 @@ int splitk_factor(const FwdArgs& a, int num_sms) {
     return split_s1(a.s.D, num_sms);
 }
 
-void launch_forward_tc2_fusedx(const FwdArgs& a, const FusedX& fx, int num_sms, cudaStream_t st) {
-    if (a.T <= 0) return;
-    TcParams p = tc2_params(a);
-    p.ht = a.ht;
-    p.seq_off = fx.seq_off;
-    p.nseq = fx.nseq;
-    p.prior = fx.prior;
-    p.xw = fx.X;
-    p.ready = fx.ready;
-    const int64_t tiles = ((a.T + BM2 - 1) / BM2) * (a.s.D / BN2);
-    int64_t pairs = num_sms / 2;  // persistent: every CTA co-resident (the ready waits rely on it)
-    if (tiles < pairs) pairs = tiles;
-    if (pairs < 1) pairs = 1;
-    constexpr int smem = Cfg2::smem_bytes(0);
-    cudaFuncSetAttribute(forward_tc2_kernel<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    forward_tc2_kernel<true, 0><<<(unsigned)(2 * pairs), Cfg2::kThreadsFX, smem, st>>>(
-        *a.tmap_x, *a.tmap_w2, *a.tmap_w2, *a.tmap_w2, *a.tmap_w2, p);
-    count_launch();
-}
 
 int tc_variant() {  // 2 = cta_group::2 pair kernel (default when D % 256 == 0), 1 = single-CTA
     static int v = [] {
@@ -1128,27 +1074,14 @@ static bool pdl_enabled() {
     return v;
 }
 
-// Small-T (decode / verify) projection: NGRAM_DECODE_CLUSTER=1 selects the single-kernel
-// cluster split-K (decode_gemm.cu: reduction + commit fused, measured slower: its in-kernel
-// reduction is latency-bound); default = split-K GEMM + reduce kernel (commit fused there).
-static bool decode_cluster() {
-    static const bool v = getenv("NGRAM_DECODE_CLUSTER") && atoi(getenv("NGRAM_DECODE_CLUSTER")) != 0;
-    return v;
-}
-
 size_t splitk_workspace_floats(const FwdArgs& a, int num_sms) {
     if (!small_t_regime(a.s.D, a.T, num_sms) || (a.tmap_x == nullptr && a.seq_off == nullptr)) return 0;
-    if (decode_cluster()) return decode_gemm_workspace_floats(a.s.D, num_sms);
     const int S = splitk_factor(a, num_sms);
     return S > 1 ? (size_t)S * (size_t)a.T * (size_t)a.s.D : 0;
 }
 
 void launch_forward_tc(const FwdArgs& a, int num_sms, cudaStream_t st, float* splitk_ws) {
     if (a.T <= 0) return;
-    if (splitk_ws && a.T <= 256 && a.tmap_x != nullptr && decode_cluster()) {
-        launch_decode_gemm(a, num_sms, splitk_ws, a.commit, st);
-        return;
-    }
     if (splitk_ws && small_t_regime(a.s.D, a.T, num_sms) && (a.tmap_x != nullptr || a.seq_off != nullptr)) {
         const int S = splitk_factor(a, num_sms);
         if (S > 1) {

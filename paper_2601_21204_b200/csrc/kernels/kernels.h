@@ -115,7 +115,6 @@ struct FwdArgs {
     const CUtensorMap* tmap_x;
     // decode step: commit the decode state in the projection kernel's tail (or null)
     const struct DecodeCommit* commit;
-    int64_t x_row0;  // first row of tmap_x used by this call (chunked overlap)
     // TMA epilogue of the pair kernel: [T][D] output maps (32 x 32 box; SWIZZLE_128B fp32 /
     // SWIZZLE_64B bf16) and the E0 gather map ([V0][D] bf16, 32 x 1 box, SWIZZLE_64B), or null
     const CUtensorMap* tmap_rows_out;
@@ -127,17 +126,6 @@ struct FwdArgs {
     int64_t nseq;
     const uint32_t* prior;
 };
-// K1 + K2 + K3 in ONE persistent 2-CTA kernel: gather warps hash and gather X rows ahead
-// of the MMA pipeline (per-128-row ready counters), overlapping the HBM-bound gather with
-// the tensor-bound projection.  Needs D % 256 == 0; tokens must be validated first.
-struct FusedX {
-    const int64_t* seq_off;
-    int64_t nseq;
-    const uint32_t* prior;
-    __nv_bfloat16* X;  // gathered rows (T x D), written by the gather warps
-    int* ready;        // [ceil(T/128)] zeroed counters
-};
-void launch_forward_tc2_fusedx(const FwdArgs& a, const FusedX& fx, int num_sms, cudaStream_t st);
 // tcgen05 projection GEMM with fused gather + base add + scale + amplify (gemm_tc.cu).
 // splitk_ws (fp32, splitk_workspace_floats() long, may be null): small-T split-K path.
 void launch_forward_tc(const FwdArgs& a, int num_sms, cudaStream_t st, float* splitk_ws = nullptr);
@@ -157,7 +145,7 @@ void launch_layernorm_rows(const Shape& s, const float* merged, const float* gai
                            void* merged_copy, int out_bf16, int64_t T, const unsigned long long* err,
                            cudaStream_t st);
 
-// ---- decode (decode.cu, decode_gemm.cu)
+// ---- decode (decode.cu)
 // Arguments of the decode-state commit (decodedev.cuh); ring == null means "no commit".
 struct DecodeCommit {
     int R;  // N - 1
@@ -173,9 +161,6 @@ struct DecodeCommit {
 // Small-T projection (T <= 256, D % 128 == 0, tensor-core shape): split-K over a thread-
 // block cluster with the cross-split reduction, epilogue and optional commit fused.
 void launch_decode_commit_c(const DecodeCommit& c, const unsigned long long* err, cudaStream_t st);
-int decode_gemm_splits(int D, int num_sms);
-size_t decode_gemm_workspace_floats(int D, int num_sms);
-void launch_decode_gemm(const FwdArgs& a, int num_sms, float* partial, const DecodeCommit* commit, cudaStream_t st);
 // The hashing of a decode step / verify block is launch_hash_ids with prior = ring and
 // seq_off = {0, L, 2L, ...}; these kernels move the ring.  derr: decode error word
 // ((status << 32) | detail), ~0 when clear.
