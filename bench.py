@@ -241,6 +241,11 @@ def reference_cpu_rate(cfg_c, seconds: float, seq_len: int = 16, max_rounds: int
         if (max_rounds and rounds >= max_rounds) or (not max_rounds and time.perf_counter() - t0 >= seconds):
             break
     el = time.perf_counter() - t0
+    # one host thread (SURVEY 8(d) also asks for the single-core rate): 2 sequences x seq_len
+    t1 = time.perf_counter()
+    if R.ref_embed_batch_mt(h, toks[:2 * seq_len], off[:3], 2, 1, out):
+        raise RuntimeError("reference embed failed")
+    one_thread = 2 * seq_len / (time.perf_counter() - t1)
     R.ref_bank_destroy(h)
     try:
         model = subprocess.run(["bash", "-c", "lscpu | grep 'Model name' | head -1"], capture_output=True,
@@ -248,6 +253,7 @@ def reference_cpu_rate(cfg_c, seconds: float, seq_len: int = 16, max_rounds: int
     except Exception:
         model = "?"
     return {"value": done / el, "cores": cores, "tokens": done, "seconds": el, "step_times": times,
+            "value_1thread": one_thread,
             "cpu_model": model,
             "sample": f"{done} tokens of the workload's shape (D={D}, N={N}, K={K}) through the reference "
                       f"embed_sequence<float>, {nseq} sequences x {seq_len} tokens per round, one std::thread per "
@@ -514,7 +520,8 @@ def run_ours(args):
         r = reference_cpu_rate(cfg, args.cpu_seconds)
         if r is not None:
             line["cpu_baseline"] = {"value": r["value"], "unit": "tokens/s", "cores": r["cores"], "kind": "reference",
-                                    "sample": r["sample"], "cpu_model": r["cpu_model"]}
+                                    "sample": r["sample"], "cpu_model": r["cpu_model"],
+                                    "value_1thread": r["value_1thread"]}
     print(json.dumps(line))
     if world > 1:
         dist.barrier()
