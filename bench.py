@@ -261,6 +261,14 @@ def reference_cpu_rate(cfg_c, seconds: float, seq_len: int = 16, max_rounds: int
                       f"per-token cost is the D^2 projection (embedding.hpp:189-195)"}
 
 
+def workload_config(cfg, label, nseq, seq_len, args):
+    """The `config` keys both arms report for a workload (the reference arm runs the same
+    shape on a reduced-vocabulary bank; see cpu_baseline.sample)."""
+    return {"workload": label, "V0": cfg["base_vocab"], "N": cfg["max_order"], "K": cfg["sub_tables"],
+            "D": cfg["dim"], "tokens": nseq * seq_len, "sequences": nseq, "seq_len": seq_len,
+            "out_dtype": args.out_dtype, "amplification": cfg["amplification"], "token_stream": args.tokens}
+
+
 def run_reference(args):
     cfg, nseq, seq_len, label = workload(args.workload)
     rank = int(os.environ.get("RANK", "0"))
@@ -278,7 +286,8 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": label, "note": "CPU reference, bounded sample per step"},
+            "config": dict(workload_config(cfg, label, nseq, seq_len, args),
+                           note="CPU reference (oracle/_ref = the reference sources), bounded sample per step"),
             "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": r["cores"], "kind": "reference",
                              "sample": r["sample"], "cpu_model": r["cpu_model"]},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -497,11 +506,9 @@ def run_ours(args):
         "data": "synthetic (device-generated counter-based tables, " + (
             "Zipf-Markov tokens generate_zipf_markov(V0, nseq, len, 20260809, 1.1, 0.35))" if args.tokens == "zipf"
             else "uniform tokens seed 42)"),
-        "config": {"workload": label, "V0": cfg["base_vocab"], "N": cfg["max_order"], "K": cfg["sub_tables"], "D": D,
-                   "d": d, "tokens": total_tokens, "sequences": nseq, "seq_len": seq_len,
-                   "embedding_params": nparams, "sub_table_params": nsub, "table_dtype": "bf16",
-                   "out_dtype": args.out_dtype, "amplification": cfg["amplification"], "sharding": sharding,
-                   "l2": "flushed (512 MiB write) between timed steps", "tensor_core_path": bank.tensor_core_path},
+        "config": dict(workload_config(cfg, label, nseq, seq_len, args), d=d, embedding_params=nparams,
+                       sub_table_params=nsub, table_dtype="bf16", sharding=sharding,
+                       l2="flushed (512 MiB write) between timed steps", tensor_core_path=bank.tensor_core_path),
         "roofline": {"bound": "tensor", "kernel": "forward_tc2_kernel (K3: tcgen05 cta_group::2 projection + "
                                                   "base/scale/amplify epilogue)",
                      "achieved": tflops, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",

@@ -140,3 +140,18 @@ def test_bench_zipf_markov_stream_is_the_reference_generator():  # corpus.cpp:21
         ref = np.zeros((nseq, n), np.uint32)
         assert O.ref().ref_generate_zipf_markov(vocab, nseq, n, seed, 1.1, 0.35, ref.reshape(-1)) == 0
         assert np.array_equal(ours, ref)
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="reference not built here")
+def test_bench_reference_arm_json_contract():
+    import subprocess, sys
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "3", "--workload", "A"], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "impl", "cpu_baseline", "e2e"):
+        assert k in line, k
+    assert line["impl"] == "reference" and line["warmup"] >= 3
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+    assert line["cpu_baseline"]["kind"] == "reference" and line["config"]["workload"]
