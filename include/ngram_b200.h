@@ -21,6 +21,10 @@
  *     recorded in a device error word: every later kernel of the same call skips its
  *     writes (no output is produced, as the reference raises before writing) and the
  *     error surfaces as NGRAM_ERANGE from ngram_sync_errors() / any host-buffer call.
+ *   - Threading: host-buffer entry points (*_host) may be called on one bank from many
+ *     threads (serialised per bank, like the reference's read-only shared bank).  The
+ *     stream-ordered device entry points share the bank's workspaces and error word:
+ *     issue them for one bank on one stream at a time (as with a cuBLAS handle).
  *   - There is no CPU fallback: every compute entry point runs CUDA kernels.
  */
 #ifndef NGRAM_B200_H

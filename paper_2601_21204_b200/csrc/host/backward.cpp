@@ -208,6 +208,7 @@ int ngram_embed_backward_host(ngram_grad* g, const uint32_t* tokens, const int64
     NGRAM_API_BEGIN
     if (!g || nseq < 1 || !seq_offsets) throw Error(NGRAM_EINVAL, "ngram_embed_backward_host: bad argument");
     ngram_bank* b = g->bank;
+    std::lock_guard<std::mutex> host_lock(g->bank->host_mu);
     const int64_t T = seq_offsets[nseq];
     if (seq_offsets[0] != 0 || T < 0) throw Error(NGRAM_EINVAL, "seq_offsets must start at 0");
     for (int64_t i = 0; i < nseq; ++i)

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -95,6 +96,9 @@ struct ngram_bank {
     CUtensorMap tmap_sub{}, tmap_w{}, tmap_w2{}, tmap_e0{};
     ngh::Workspace ws;
 
+    // Serialises the host-buffer entry points (the reference's bank is shareable across
+    // threads; this bank's workspaces and error word are not)
+    std::mutex host_mu;
     // host-buffer pipeline (ngram_embed_sequence_host)
     cudaStream_t host_streams[2] = {nullptr, nullptr};
     ngh::DevBuf<uint8_t> host_out[2];

@@ -147,6 +147,7 @@ int ngram_decode_get_state(ngram_decode* d, uint32_t* ring, uint64_t* length, ui
 int ngram_decode_reset_host(ngram_decode* d, const uint32_t* prior, const uint64_t* lengths) {
     NGRAM_API_BEGIN
     if (!d) throw Error(NGRAM_EINVAL, "null decode state");
+    std::lock_guard<std::mutex> host_lock(d->bank->host_mu);
     DeviceGuard g(d->bank->device);
     const int R = std::max(d->bank->cfg.max_order - 1, 0);
     DevBuf<uint32_t> pr;
@@ -168,6 +169,7 @@ int ngram_decode_reset_host(ngram_decode* d, const uint32_t* prior, const uint64
 int ngram_decode_step_host(ngram_decode* d, const uint32_t* tokens, uint64_t* ids_out, float* merged_out) {
     NGRAM_API_BEGIN
     if (!d || !tokens) throw Error(NGRAM_EINVAL, "ngram_decode_step_host: bad argument");
+    std::lock_guard<std::mutex> host_lock(d->bank->host_mu);
     DeviceGuard g(d->bank->device);
     ngram_bank* b = d->bank;
     for (int64_t s = 0; s < d->batch; ++s)  // the reference validates before mutating (cache.cpp:39-42)
@@ -196,6 +198,7 @@ int ngram_verify_commit_host(ngram_decode* d, const uint32_t* draft, int L, cons
     NGRAM_API_BEGIN
     if (!d || !draft || !accept || L < 1 || L > d->max_draft)
         throw Error(NGRAM_EINVAL, "ngram_verify_commit_host: bad argument");
+    std::lock_guard<std::mutex> host_lock(d->bank->host_mu);
     ngram_bank* b = d->bank;
     for (int64_t s = 0; s < d->batch; ++s) {
         if (accept[s] < 0 || accept[s] > L) throw Error(NGRAM_EINVAL, "draft_verify: accept count exceeds draft length");

@@ -331,6 +331,7 @@ int ngram_embed_sequence_host(ngram_bank* b, const uint32_t* tokens, const int64
     if (out_dtype != NGRAM_F32 && out_dtype != NGRAM_BF16) throw Error(NGRAM_EINVAL, "bad out_dtype");
     const int64_t T = seq_offsets[nseq];
     check_offsets(seq_offsets, nseq, T);
+    std::lock_guard<std::mutex> host_lock(b->host_mu);
     DeviceGuard g(b->device);
     for (int i = 0; i < 2; ++i)
         if (!b->host_streams[i]) NGH_CUDA(cudaStreamCreateWithFlags(&b->host_streams[i], cudaStreamNonBlocking));
@@ -465,6 +466,7 @@ int ngram_hash_ids_host(ngram_bank* b, const uint32_t* tokens, const int64_t* se
     if (!b || nseq < 1 || !seq_offsets) throw Error(NGRAM_EINVAL, "ngram_hash_ids_host: bad argument");
     const int64_t T = seq_offsets[nseq];
     check_offsets(seq_offsets, nseq, T);
+    std::lock_guard<std::mutex> host_lock(b->host_mu);
     if (T == 0) NGRAM_API_RETURN_OK;
     DeviceGuard g(b->device);
     HostStage<uint32_t> t, p;
@@ -509,6 +511,7 @@ int ngram_embed_from_ids_host(ngram_bank* b, const uint32_t* tokens, const uint6
     NGRAM_API_BEGIN
     if (!b || T < 0 || (T > 0 && (!tokens || !ids || !merged_out)))
         throw Error(NGRAM_EINVAL, "ngram_embed_from_ids_host: bad argument");
+    std::lock_guard<std::mutex> host_lock(b->host_mu);
     if (T == 0) NGRAM_API_RETURN_OK;
     DeviceGuard g(b->device);
     HostStage<uint32_t> t;

@@ -192,6 +192,7 @@ int ngram_plne_forward_host(ngram_plne* p, const float* gate, const float* down,
     NGRAM_API_BEGIN
     if (!p || !seq_offsets || nseq < 1) throw Error(NGRAM_EINVAL, "ngram_plne_forward_host: bad argument");
     check_host_offsets(seq_offsets, nseq);
+    std::lock_guard<std::mutex> host_lock(p->bank->host_mu);
     const int64_t T = seq_offsets[nseq];
     if (T == 0) return NGRAM_OK;
     if (!gate || !down || !x || !tokens || !y) throw Error(NGRAM_EINVAL, "ngram_plne_forward_host: bad argument");
@@ -213,6 +214,7 @@ int ngram_plne_backward_host(ngram_plne* p, ngram_grad* bank_grads, const float*
     NGRAM_API_BEGIN
     if (!p || !seq_offsets || nseq < 1) throw Error(NGRAM_EINVAL, "ngram_plne_backward_host: bad argument");
     check_host_offsets(seq_offsets, nseq);
+    std::lock_guard<std::mutex> host_lock(p->bank->host_mu);
     const int64_t T = seq_offsets[nseq];
     if (T == 0) return NGRAM_OK;
     if (!gate || !down || !x || !tokens || !upstream || !d_gate || !d_down || !dx)

@@ -8,6 +8,7 @@
 #include <cstring>
 #include <functional>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "ngram/cache.hpp"
@@ -464,6 +465,30 @@ int main() {
         const auto host = make_bank<float>(make_default_config(40, 64, 3, 1), 2);
         const auto back = bank_cast<double, float>(bank_cast<float, double>(host));
         CHECK(back.base == host.base && back.sub_tables == host.sub_tables);
+    });
+    test_case("one device_bank shared by host threads (bank read-only across threads, SPEC.md:283)", [] {
+        const auto host = make_bank<float>(make_default_config(500, 256, 3, 2), 8);
+        const device_bank bank(host);
+        std::vector<std::vector<token_id>> seqs(4);
+        rng64 rng(5);
+        for (auto& q : seqs) {
+            q.resize(100 + 37 * (&q - seqs.data()));
+            for (auto& t : q) t = token_id(uniform_below(rng, 500));
+        }
+        std::vector<std::vector<float>> want;
+        for (const auto& q : seqs) want.push_back(embed_sequence(q, bank));
+        std::vector<int> ok(seqs.size(), 1);
+        std::vector<std::thread> th;
+        for (std::size_t i = 0; i < seqs.size(); ++i)
+            th.emplace_back([&, i] {
+                sequence_cache cache(bank);
+                for (int rep = 0; rep < 10; ++rep) {
+                    if (embed_sequence(seqs[i], bank) != want[i]) ok[i] = 0;
+                    cache.append(seqs[i][std::size_t(rep)]);
+                }
+            });
+        for (auto& t : th) t.join();
+        for (const int v : ok) CHECK(v == 1);
     });
     std::printf("%d checks, %d failures\n", g_checks, g_fail);
     return g_fail == 0 ? 0 : 1;
