@@ -3,6 +3,8 @@
 // verification and the accepted-prefix commit run as kernels.
 #pragma once
 #include <cstdint>
+#include <list>
+#include <map>
 #include <memory>
 #include <span>
 #include <string>
@@ -62,19 +64,29 @@ class sequence_cache {
     std::vector<snap> snaps_;
 };
 
-// The memo of the reference (cache.hpp:86-113) is subsumed on the GPU: a verify block
-// computes every draft position's embedding in one launch and the accepted prefix is
-// read from it.  The type is kept so reference call sites compile.
+// embedding_memo (cache.hpp:82-113, cache.cpp:98-150): an LRU of merged (pre-amplification)
+// vectors keyed by the exact (token, bucket ids); a miss runs embed_from_ids on the GPU and
+// inserts, a hit returns the stored vector (bit-identical to recomputing).  draft_verify does
+// not need it on the GPU -- a verify block computes every draft position in one launch and
+// the accepted prefix is read from it -- but direct lookups behave as the reference's.
+// Externally synchronised when shared, as the reference's.
 class embedding_memo {
   public:
     explicit embedding_memo(std::size_t capacity) : capacity_(capacity) {
         if (capacity_ < 1) throw std::invalid_argument("embedding_memo: capacity must be >= 1");
     }
+    std::vector<float> lookup(token_id token, std::span<const std::uint64_t> ids, const device_bank& bank,
+                              cache_counters* counters = nullptr);
+    std::vector<float> lookup(token_id token, std::span<const std::uint64_t> ids, const embedding_bank& bank,
+                              cache_counters* counters = nullptr);
     std::size_t capacity() const { return capacity_; }
-    std::size_t size() const { return 0; }
+    std::size_t size() const { return lru_.size(); }
 
   private:
+    using key = std::vector<std::uint64_t>;  // token, then the ids
     std::size_t capacity_;
+    std::list<std::pair<key, std::vector<float>>> lru_;  // front = most recently used
+    std::map<key, decltype(lru_)::iterator> where_;
 };
 
 struct draft_options {

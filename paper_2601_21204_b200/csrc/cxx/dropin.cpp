@@ -464,6 +464,39 @@ void sequence_cache::discard(const snapshot_handle& h) {
     snaps_.pop_back();
 }
 
+std::vector<float> embedding_memo::lookup(token_id token, std::span<const std::uint64_t> ids, const device_bank& bank,
+                                          cache_counters* counters) {
+    key k;
+    k.reserve(ids.size() + 1);
+    k.push_back(token);
+    k.insert(k.end(), ids.begin(), ids.end());
+    if (const auto it = where_.find(k); it != where_.end()) {
+        lru_.splice(lru_.begin(), lru_, it->second);
+        if (counters) counters->memo_hits++;
+        return it->second->second;
+    }
+    std::vector<float> e(std::size_t(bank.config().dim));
+    embed_counters ec;
+    embed_from_ids(token, ids, bank, e, &ec);
+    if (counters) {
+        counters->memo_misses++;
+        counters->table_gathers += ec.table_gathers;
+        counters->projection_madds += ec.projection_madds;
+    }
+    if (lru_.size() == capacity_) {
+        where_.erase(lru_.back().first);
+        lru_.pop_back();
+    }
+    lru_.emplace_front(std::move(k), e);
+    where_[lru_.front().first] = lru_.begin();
+    return e;
+}
+
+std::vector<float> embedding_memo::lookup(token_id token, std::span<const std::uint64_t> ids,
+                                          const embedding_bank& bank, cache_counters* counters) {
+    return lookup(token, ids, device_bank(bank), counters);
+}
+
 draft_result draft_verify(sequence_cache& state, const device_bank& bank, std::span<const token_id> draft,
                           std::size_t accept_count, cache_counters* counters, const draft_options& opts) {
     if (accept_count > draft.size()) throw std::invalid_argument("draft_verify: accept count exceeds draft length");

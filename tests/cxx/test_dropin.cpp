@@ -490,6 +490,26 @@ int main() {
         for (auto& t : th) t.join();
         for (const int v : ok) CHECK(v == 1);
     });
+    test_case("embedding_memo: hits are bit-identical, LRU eviction, counters (test_cache.cpp:264-314)", [] {
+        const auto cfg = make_default_config(300, 256, 3, 2);
+        const device_bank bank(make_bank<float>(cfg, 13));
+        embedding_memo memo(2);
+        cache_counters c;
+        const std::vector<token_id> a{1, 2, 3}, b{4, 5, 6}, d{7, 8, 9};
+        const auto ia = hash_all_orders(a, cfg), ib = hash_all_orders(b, cfg), id = hash_all_orders(d, cfg);
+        const auto x1 = memo.lookup(3, ia, bank, &c);
+        const auto x2 = memo.lookup(3, ia, bank, &c);
+        CHECK(x1 == x2 && c.memo_hits == 1 && c.memo_misses == 1);
+        std::vector<float> direct(256);
+        embed_from_ids(3, ia, bank, direct);
+        CHECK(x1 == direct);
+        memo.lookup(6, ib, bank, &c);
+        memo.lookup(9, id, bank, &c);  // evicts the least recently used (token 3)
+        CHECK(memo.size() == 2 && c.memo_misses == 3);
+        memo.lookup(3, ia, bank, &c);
+        CHECK(c.memo_misses == 4 && c.table_gathers == 4 * 5);
+        CHECK_THROWS_AS(embedding_memo(0), std::invalid_argument);
+    });
     std::printf("%d checks, %d failures\n", g_checks, g_fail);
     return g_fail == 0 ? 0 : 1;
 }
