@@ -213,6 +213,13 @@ embedding_bank_t<T> zeros_like(const embedding_bank_t<T>& bank) {
     return z;
 }
 
+// amplify_backward (embedding.hpp:291-336) of one row, on the device: d_pre from the
+// amplification input `pre` and `upstream`; layer_norm accumulates grads.ln_gain / ln_bias.
+void amplify_backward(std::span<const float> pre, std::span<const float> upstream, const device_bank& bank,
+                      embedding_bank& grads, std::span<float> d_pre);
+void amplify_backward(std::span<const float> pre, std::span<const float> upstream, const embedding_bank& bank,
+                      embedding_bank& grads, std::span<float> d_pre);
+
 // Backward (embedding.hpp:338-459), computed on the device (ngram_embed_backward_host:
 // fp32 atomics + fp32 GEMMs) and ACCUMULATED into the host gradient bank `grads`.
 // embed_backward: `upstream` is d(merged) of one window (no amplification step).

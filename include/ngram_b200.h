@@ -278,6 +278,11 @@ int ngram_embed_backward(ngram_grad* g, const uint32_t* tokens, const int64_t* s
  * out-of-range token returns NGRAM_ERANGE and leaves the gradients untouched. */
 int ngram_embed_backward_host(ngram_grad* g, const uint32_t* tokens, const int64_t* seq_offsets, int64_t nseq,
                               const uint32_t* prior, const float* merged, const float* upstream, int flags);
+/* amplify_backward (embedding.hpp:291-336) of `rows` HOST rows with the bank's amplification
+ * and LN gain: d_pre = d(amplify)/d(pre) . upstream; layer_norm ACCUMULATES the gain / bias
+ * gradients into g_gain / g_bias (host, size D; null skips). Synchronous. */
+int ngram_amplify_backward_host(ngram_bank* bank, int64_t rows, const float* pre, const float* upstream, float* d_pre,
+                                float* g_gain, float* g_bias);
 /* Device view of one gradient tensor: which 0 = E0, 1 = sub-tables (device row layout),
  * 2 = W_cat, 3 = ln_gain, 4 = ln_bias. */
 int ngram_grad_tensor(ngram_grad* g, int which, float** dev_ptr, int64_t* numel);

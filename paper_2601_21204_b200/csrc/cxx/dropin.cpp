@@ -300,6 +300,23 @@ void add_device_grads(ngram_grad* g, embedding_bank& grads) {
 }
 }  // namespace
 
+void amplify_backward(std::span<const float> pre, std::span<const float> upstream, const device_bank& bank,
+                      embedding_bank& grads, std::span<float> d_pre) {
+    const std::size_t D = std::size_t(bank.config().dim);
+    if (pre.size() != D || upstream.size() != D || d_pre.size() != D)
+        throw std::invalid_argument("amplify_backward: size mismatch");
+    const bool ln = bank.config().amplification == amp_mode::layer_norm;
+    if (ln && (grads.ln_gain.size() != D || grads.ln_bias.size() != D))
+        throw std::invalid_argument("amplify_backward: gradient bank has no layer-norm parameters");
+    throw_status(ngram_amplify_backward_host(bank.handle(), 1, pre.data(), upstream.data(), d_pre.data(),
+                                             ln ? grads.ln_gain.data() : nullptr, ln ? grads.ln_bias.data() : nullptr));
+}
+
+void amplify_backward(std::span<const float> pre, std::span<const float> upstream, const embedding_bank& bank,
+                      embedding_bank& grads, std::span<float> d_pre) {
+    amplify_backward(pre, upstream, device_bank(bank), grads, d_pre);
+}
+
 void embed_backward(std::span<const token_id> context, const device_bank& bank, std::span<const float> upstream,
                     embedding_bank& grads) {
     const auto& cfg = bank.config();

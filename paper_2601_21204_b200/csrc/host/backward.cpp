@@ -242,6 +242,47 @@ int ngram_embed_backward_host(ngram_grad* g, const uint32_t* tokens, const int64
     NGRAM_API_END
 }
 
+int ngram_amplify_backward_host(ngram_bank* b, int64_t rows, const float* pre, const float* upstream, float* d_pre,
+                                float* g_gain, float* g_bias) {
+    NGRAM_API_BEGIN
+    if (!b || rows < 0 || (rows > 0 && (!pre || !upstream || !d_pre)))
+        throw Error(NGRAM_EINVAL, "ngram_amplify_backward_host: bad argument");
+    if (b->hash_only) throw Error(NGRAM_EINVAL, "bank was created hash-only (NGRAM_BANK_HASH_ONLY)");
+    if (rows == 0) return NGRAM_OK;
+    std::lock_guard<std::mutex> host_lock(b->host_mu);
+    DeviceGuard dg(b->device);
+    ngk::Shape s = b->shape;
+    s.denom = 1;  // d_pre itself: no 1/denom merge scale here (that is embed_backward's)
+    const size_t D = size_t(s.D), n = size_t(rows) * D;
+    const bool ln = s.amp == ngk::kAmpLN;
+    DevBuf<float> dp, du, dd, ge0, gg, gb;
+    DevBuf<uint32_t> tok;
+    DevBuf<unsigned long long> err;
+    dp.alloc(n);
+    du.alloc(n);
+    dd.alloc(n);
+    ge0.alloc(D);  // the kernel's E0-row scatter lands here (token 0) and is discarded
+    tok.alloc(size_t(rows));
+    err.alloc(1);
+    NGH_CUDA(cudaMemcpy(dp.p, pre, n * 4, cudaMemcpyHostToDevice));
+    NGH_CUDA(cudaMemcpy(du.p, upstream, n * 4, cudaMemcpyHostToDevice));
+    NGH_CUDA(cudaMemset(tok.p, 0, size_t(rows) * 4));
+    NGH_CUDA(cudaMemset(err.p, 0xff, 8));
+    if (ln) {
+        gg.alloc(D);
+        gb.alloc(D);
+        if (g_gain) NGH_CUDA(cudaMemcpy(gg.p, g_gain, D * 4, cudaMemcpyHostToDevice));
+        else NGH_CUDA(cudaMemset(gg.p, 0, D * 4));
+        if (g_bias) NGH_CUDA(cudaMemcpy(gb.p, g_bias, D * 4, cudaMemcpyHostToDevice));
+        else NGH_CUDA(cudaMemset(gb.p, 0, D * 4));
+    }
+    ngk::launch_amp_backward(s, du.p, dp.p, tok.p, rows, s.amp, b->ln_gain.p, dd.p, ge0.p, gg.p, gb.p, err.p, nullptr);
+    NGH_CUDA(cudaMemcpy(d_pre, dd.p, n * 4, cudaMemcpyDeviceToHost));
+    if (ln && g_gain) NGH_CUDA(cudaMemcpy(g_gain, gg.p, D * 4, cudaMemcpyDeviceToHost));
+    if (ln && g_bias) NGH_CUDA(cudaMemcpy(g_bias, gb.p, D * 4, cudaMemcpyDeviceToHost));
+    NGRAM_API_END
+}
+
 int ngram_grad_sparse_rows(ngram_grad* g, int32_t** rows, float** vals, int64_t* count) {
     NGRAM_API_BEGIN
     if (!g || !rows || !vals || !count) throw Error(NGRAM_EINVAL, "ngram_grad_sparse_rows: bad argument");

@@ -510,6 +510,29 @@ int main() {
         CHECK(c.memo_misses == 4 && c.table_gathers == 4 * 5);
         CHECK_THROWS_AS(embedding_memo(0), std::invalid_argument);
     });
+    test_case("amplify_backward + embed_backward == embed_sequence_backward for one window (layer_norm)", [] {
+        auto cfg = make_default_config(300, 256, 3, 2);
+        cfg.amplification = amp_mode::layer_norm;
+        auto host = make_bank<float>(cfg, 23);
+        rng64 rng(3);
+        for (auto& g : host.ln_gain) g = 1.0f + 0.1f * float(gaussian(rng));
+        const device_bank bank(host);
+        const std::vector<token_id> ctx{5, 9, 11};
+        std::vector<float> up(256);
+        for (auto& u : up) u = float(gaussian(rng));
+        std::vector<float> merged(256);
+        embed_window(ctx, bank, merged);
+        auto a = zeros_like(host);
+        std::vector<float> d_pre(256);
+        amplify_backward(merged, up, bank, a, d_pre);
+        embed_backward(ctx, bank, d_pre, a);
+        auto b = zeros_like(host);
+        embed_sequence_backward(std::span<const token_id>(ctx).last(1), bank, merged, up, b,
+                                std::span<const token_id>(ctx).first(2));
+        CHECK(close_rows(a.base, b.base, 1e-5) && close_rows(a.ln_gain, b.ln_gain, 1e-5) &&
+              close_rows(a.ln_bias, b.ln_bias, 1e-5));
+        for (std::size_t i = 0; i < a.projections.size(); ++i) CHECK(close_rows(a.projections[i], b.projections[i], 1e-5));
+    });
     std::printf("%d checks, %d failures\n", g_checks, g_fail);
     return g_fail == 0 ? 0 : 1;
 }
