@@ -848,6 +848,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::kThreads, 1)
     }
 }
 
+// Diagnostics switches (read once): NGRAM_DEBUG_EPI_SKIP=1/2/3, NGRAM_DEBUG_SKIP_A.
+static int debug_epi_skip() {
+    static const int v = getenv("NGRAM_DEBUG_EPI_SKIP") ? atoi(getenv("NGRAM_DEBUG_EPI_SKIP")) : 0;
+    return v;
+}
+static int debug_skip_a() {
+    static const int v = getenv("NGRAM_DEBUG_SKIP_A") ? 1 : 0;
+    return v;
+}
+
 template <int BN, int NP, int MODE>
 void launch_cfg(const FwdArgs& a, int num_sms, cudaStream_t st, int ksplit = 1, float* partial = nullptr,
                 bool pdl = false) {
@@ -870,8 +880,8 @@ void launch_cfg(const FwdArgs& a, int num_sms, cudaStream_t st, int ksplit = 1, 
     p.amp = a.s.amp == kAmpSqrt ? (float)__builtin_sqrt((double)a.s.D) : 1.0f;
     p.err = a.err;
     p.use_x = a.tmap_x != nullptr;
-    p.epi_skip = getenv("NGRAM_DEBUG_EPI_SKIP") ? atoi(getenv("NGRAM_DEBUG_EPI_SKIP")) : 0;
-    p.diag_skip_a = getenv("NGRAM_DEBUG_SKIP_A") ? 1 : 0;
+    p.epi_skip = debug_epi_skip();
+    p.diag_skip_a = debug_skip_a();
     p.ht = a.ht;
     p.seq_off = a.seq_off;
     p.nseq = a.nseq;
@@ -929,8 +939,8 @@ void launch_tc2(const FwdArgs& a, int num_sms, cudaStream_t st) {
     p.amp = a.s.amp == kAmpSqrt ? (float)__builtin_sqrt((double)a.s.D) : 1.0f;
     p.err = a.err;
     p.use_x = a.tmap_x != nullptr;
-    p.epi_skip = getenv("NGRAM_DEBUG_EPI_SKIP") ? atoi(getenv("NGRAM_DEBUG_EPI_SKIP")) : 0;
-    p.diag_skip_a = getenv("NGRAM_DEBUG_SKIP_A") ? 1 : 0;
+    p.epi_skip = debug_epi_skip();
+    p.diag_skip_a = debug_skip_a();
     const int64_t tiles = ((a.T + BM2 - 1) / BM2) * (a.s.D / BN2);
     int64_t pairs = num_sms / 2;
     if (tiles < pairs) pairs = tiles;
@@ -973,8 +983,8 @@ TcParams tc2_params(const FwdArgs& a) {
     p.amp = a.s.amp == kAmpSqrt ? (float)__builtin_sqrt((double)a.s.D) : 1.0f;
     p.err = a.err;
     p.use_x = 1;
-    p.epi_skip = getenv("NGRAM_DEBUG_EPI_SKIP") ? atoi(getenv("NGRAM_DEBUG_EPI_SKIP")) : 0;
-    p.diag_skip_a = getenv("NGRAM_DEBUG_SKIP_A") ? 1 : 0;
+    p.epi_skip = debug_epi_skip();
+    p.diag_skip_a = debug_skip_a();
     return p;
 }
 
