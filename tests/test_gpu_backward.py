@@ -145,3 +145,37 @@ def test_tf32_backward_within_training_precision(cuda):  # NGRAM_GRAD_TF32
     gb.backward(**args)
     db.sync_errors()
     assert_grads_close(gb.download(), golden_grads(g, O.zero_grads(cfg)), ln, rel_l2=3e-3, max_rtol=1e-2)
+
+
+def test_longcat_scale_sparse_backward_sampled(cuda):
+    """Full LongCat width and table scale (D = 3072, N = 4, K = 4, ~19 M sub-table rows,
+    counter-based device tables): the row-sparse backward of a 64-token sequence, checked
+    entry by entry against double-precision sums over the generator's table values."""
+    cfg = O.make_default_config(128000, 3072, 4, 4)  # amplification scale_sqrt_d
+    seed, T, D, d, B = 77, 64, 3072, 256, 12
+    db = G.DeviceBank(cfg).generate(seed)
+    toks = O.uniform_tokens(5, 128000, T)
+    up = np.random.default_rng(6).standard_normal((T, D)).astype(np.float32)
+    gb = G.GradBank(db, sparse_rows=True)
+    t_dev = dev_u32(torch, toks, cuda)
+    gb.backward(t_dev, dev_i64(torch, [0, T], cuda), torch.from_numpy(up).to(cuda))
+    db.sync_errors()
+    rows, vals = (x.cpu().numpy() for x in gb.sparse())
+    ids = O.hash_sequence(cfg, toks).astype(np.int64)  # [T][B] bucket ids
+    base = np.concatenate([[0], np.cumsum(O.sub_vocab_array(cfg))]).astype(np.int64)
+    assert np.array_equal(rows.reshape(T, B), ids + base[:B])  # storage rows, (t, b) order
+    # u_t = fp32(1/denom) * (upstream * fp32(sqrt D)) -- amplify_backward then the merge scale
+    u = (np.float32(1.0 / 13.0) * (up * np.float32(np.sqrt(D)))).astype(np.float64)
+    for t, b in [(0, 0), (17, 5), (63, 11)]:
+        w_b = O.synth_rows(seed, 100 + b, 0, D, d, 0.02 / np.sqrt(d)).astype(np.float64)  # W_b [D][d]
+        want = u[t] @ w_b
+        got = vals[t * B + b]
+        assert np.abs(got - want).max() <= 1e-5 * np.abs(want).max()
+    g = gb.download()
+    for t in (3, 40):  # E0 gradient row of the token: u_t (tokens are distinct here)
+        assert np.allclose(g["base"][toks[t]], u[t], rtol=1e-6, atol=1e-12)
+    # projection gradient entries: dW_b[i][j] = sum_t u_t[i] * E_b[id_b(t)][j]
+    for b, i, j in [(2, 100, 7), (9, 3000, 255)]:
+        x = np.stack([O.synth_rows(seed, 1 + b, int(ids[t, b]), 1, d, 0.02)[0] for t in range(T)]).astype(np.float64)
+        want = float(u[:, i] @ x[:, j])
+        assert abs(g["proj"][b][i, j] - want) <= 1e-5 * max(abs(want), np.abs(u[:, i]).max() * 1e-2)
