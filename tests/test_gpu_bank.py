@@ -100,3 +100,25 @@ def test_row_shards_partition_every_table(cuda, P):
         for r in range(P):
             for h in (los[r][b], his[r][b] - 1):
                 assert h * P // V[b] == r
+
+
+def test_load_file_into_row_shards(small, cuda):  # ingest sliced per shard
+    """Each shard bank streams only its row block of every sub-table from the same file; the
+    sharded forward over those banks equals the unsharded forward bit for bit."""
+    cfg, hb, path = small
+    full = G.DeviceBank(cfg).load_file(path)
+    P, nseq, L = 2, 4, 120
+    toks = O.uniform_tokens(9, cfg["base_vocab"], nseq * L)
+    t_all, off_all = dev_u32(torch, toks, cuda), dev_i64(torch, np.arange(0, nseq * L + 1, L), cuda)
+    ref, _ = G.embed_forward(full, t_all, off_all)
+    per = nseq // P
+    rank_tok = [r * per * L for r in range(P + 1)]
+    banks = [G.DeviceBank(cfg, shard_rank=r, shard_count=P).load_file(path) for r in range(P)]
+    groups = [G.ShardGroup(b, per * L) for b in banks]
+    G.emulate_shards_single_process(groups)
+    for g in groups:
+        g.scatter(t_all, off_all, rank_tok)
+    torch.cuda.synchronize()
+    for r, g in enumerate(groups):
+        rows, _ = g.project(t_all[rank_tok[r]:rank_tok[r + 1]])
+        assert torch.equal(rows, ref[rank_tok[r]:rank_tok[r + 1]])
