@@ -1,29 +1,27 @@
-// gemm_tc.cu -- K2+K3 fused: the sub-table gather and the projection GEMM on the 5th-gen
-// tensor cores, with the base-row add, 1/denom scale and amplification in the epilogue.
+// gemm_tc.cu -- K3: the projection GEMM on the 5th-gen tensor cores, with the base-row
+// add, 1/denom scale and amplification in the epilogue.
 //
 //   Y[t, :] = amplify( (E0[tok_t, :] + X[t, :] . W_cat^T) * fp32(1/denom) )
-//   X[t, b*d:(b+1)*d] = E_b[id_b(t)]   (never materialised: gathered straight into smem)
+//   X[t, b*d:(b+1)*d] = E_b[id_b(t)]
 //
-// This is embed_from_ids (embedding.hpp:163-201) + amplify (:239-287) for a tile of 128
-// positions: the reference's per-token D x d matvec per branch (its >99% hot loop,
-// embedding.hpp:189-195) becomes ONE bf16 GEMM with K = (N-1)K*d = D (branch-
-// concatenated), fp32 accumulation in TMEM.
+// This is embed_from_ids (embedding.hpp:163-201) + amplify (:239-287): the reference's
+// per-token D x d matvec per branch (its >99% hot loop, embedding.hpp:189-195) becomes ONE
+// bf16 GEMM with K = (N-1)K*d = D (branch-concatenated), fp32 accumulation in TMEM.  The A
+// operand is either X materialised by the fused K1+K2 kernel (hash.cu; TMA 2D tiles) or the
+// sub-table rows gathered straight into shared memory (tile::gather4 / cp.async).
 //
-// Structure (persistent, 1 CTA per SM, warp-specialised; the MMA issuer is the highest
-// warp id because the warp arbiter serves the highest eligible id first):
-//   warps 0..NP-1   A producers, 32 tile rows each.  Per K-block (64 columns = one 128-B
-//                   swizzle atom) every producer warp moves its 32 gathered rows of the
-//                   sub-table into the SWIZZLE_128B K-major A tile, either with
-//                   TMA tile::gather4 (MODE 0: 8 instructions of 4 rows) or with cp.async
-//                   16-B copies placed at their swizzled addresses (MODE 1: 8 per lane,
-//                   retired LAG K-blocks later with a proxy fence + mbarrier arrive).
-//                   Warp 0 / lane 0 also TMA-loads the W_cat tile (BN x 64).
-//   warps NP..NP+3  epilogue: tcgen05.ld accumulator rows -> + E0 row -> * 1/denom -> * amp
-//   warp NP+4       TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN, K=16).
-//                   -> fp32/bf16 stores.  TMEM is double-buffered (2 x BN columns) so the
-//                   epilogue of tile i overlaps the MMAs of tile i+1.
-// Tiles are ordered n-fastest so the CTAs running concurrently share an m-block's
-// gathered rows through L2; W_cat (2*D^2 bytes) stays L2-resident (evict_last).
+// Kernels (persistent, warp-specialised; the MMA issuer is always the highest warp id
+// because the warp arbiter serves the highest eligible id first):
+//   forward_tc2_kernel   2-CTA pairs (cta_group::2), 256 x 256 tiles, 8 epilogue warps,
+//                        TMEM double-buffered; the production path for D % 256 == 0 and
+//                        T > 256.  EPI 1: all epilogue traffic by TMA (E0 rows gathered
+//                        into a smem ring, outputs staged and bulk-stored); EPI 0: direct.
+//   forward_tc_kernel    1 CTA, 128 x BN tiles: shapes the pair kernel does not take, and
+//                        the small-T split-K GEMM (raw fp32 partials, BN = 128; MODE 2
+//                        hashes in its producers, opt-in).
+//   splitk_reduce_kernel S partials + E0 + scales (+ the decode-state commit), PDL-launched.
+// Tiles are ordered n-fastest so the CTAs running concurrently share an m-block's A rows
+// through L2; W_cat (2*D^2 bytes) stays L2-resident (evict_last).
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
