@@ -1,5 +1,5 @@
 // bank.cu -- device-side bank construction: the counter-based synthetic generator for
-// LongCat-scale tables, f32 -> bf16 conversion of uploaded reference banks,
+// LongCat-scale tables (defined in oracle/ngram_oracle.c, evaluated identically here), f32 -> bf16 conversion of uploaded reference banks,
 // and W_b -> W_cat packing.  Pure HBM-write kernels, grid-stride, 16-byte stores.
 #include <atomic>
 #include <cstdint>

@@ -12,6 +12,12 @@
 //
 // HBM: reads N tokens (L1/L2 hits, 4 B/token from DRAM), writes B ids (u32) and B
 // storage rows (i32): 4 + 8B bytes/token -- purely bandwidth/latency bound.
+//
+// Kernels: hash_ids_kernel (K1 alone: ids / storage rows), rolling_hash_kernel (the
+// reference's single-window API), hash_gather_block_kernel (K1+K2 fused, the prefill
+// default: 16 positions per block hashed in parallel, then their X rows streamed as one
+// flat array), hash_gather_kernel (warp-per-position fallback), hash_gather_rows_kernel
+// (warp per (position, branch): small T), validate_tokens_kernel.
 #include <cstdint>
 #include <cstdlib>
 
