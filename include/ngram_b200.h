@@ -123,7 +123,9 @@ int ngram_rolling_hash_batch(const uint32_t* windows, int64_t stride, const int3
 /* hash_all_orders at every position of a batch of sequences (hashing.cpp:61-81 with the
  * windows of embed_sequence, embedding.hpp:391-405).
  *   tokens:      dev u32, total_tokens, sequences concatenated
- *   seq_offsets: dev i64, nseq+1 prefix offsets (seq s = tokens[off[s], off[s+1]))
+ *   seq_offsets: dev i64, nseq+1 prefix offsets (seq s = tokens[off[s], off[s+1])); the
+ *     device entry points trust them (0 = off[0] <= ... <= off[nseq] = total_tokens; the
+ *     host entry points check) -- a malformed window is reported like a bad token
  *   prior:       dev u32 nseq x (N-1), the N-1 tokens preceding each sequence
  *                (prior_context, right-aligned, 0 = pad), or NULL for none
  *   ids_out:     dev, total_tokens x branch_count, u64 if ids_u64 else u32, entry

@@ -85,6 +85,7 @@ __device__ __forceinline__ bool load_window(const Shape& s, const uint32_t* __re
     const int64_t sq = uniform_len > 0 ? t / uniform_len : find_seq(seq_off, nseq, t);
     const int64_t base = uniform_len > 0 ? sq * uniform_len : __ldg(seq_off + sq);
     const int64_t p = t - base;
+    if (p < 0) return false;  // malformed device offsets (off[0] > t): never read out of bounds
     bool bad = false;
 #pragma unroll
     for (int j = 0; j < MAXN; ++j) {
