@@ -30,16 +30,17 @@ static void check_offsets(const int64_t* off, int64_t nseq, int64_t T) {
         if (off[i + 1] < off[i]) throw Error(NGRAM_EINVAL, "seq_offsets must be non-decreasing");
 }
 
-// Fused gather (TMA gather4 straight into the GEMM's smem) vs K2 -> X -> K3.  Measured on
-// B200: fused wins when the GEMM is short in K (D <= 1024: the epilogue
-// dominates and X's HBM round trip does not pay), X wins for LongCat-scale D (the
-// gather4 stream cannot keep 512-cycle K-blocks fed).  NGRAM_FUSED_GATHER=0/1 overrides.
+// Fused gather (TMA gather4 straight into the GEMM's smem) vs K1+K2 -> X -> K3.  Measured
+// on B200 (profiles/README.md): with the block K1+K2 kernel and the all-TMA epilogue the X
+// path wins at every width (config A 56 vs 53 M tok/s, B 399 vs 375 M, C 64 vs 42 M: the
+// gather4 stream cannot keep the K-blocks fed).  NGRAM_FUSED_GATHER=1 selects the fused path.
 static bool fused_gather(int D) {
     static const int env = [] {
         const char* e = getenv("NGRAM_FUSED_GATHER");
-        return e ? atoi(e) : -1;
+        return e ? atoi(e) : 0;
     }();
-    return env >= 0 ? env != 0 : D <= 1024;
+    (void)D;
+    return env != 0;
 }
 
 static bool small_t(const ngram_bank* b, int64_t T) { return ngk::small_t_regime(b->shape.D, T, b->num_sms); }

@@ -354,3 +354,33 @@ def test_verify_sized_regime_at_longcat_width(cuda):
     assert_rows_close(merged.cpu().numpy(), np.concatenate(ref_m))
     a01, _ = G.embed_forward(db, dev_u32(torch, np.concatenate(seqs[:2]), cuda), dev_i64(torch, off[:3], cuda))
     assert torch.equal(a01, rows[:500])  # T = 500 and T = 600: same regime, same bits
+
+
+def test_fused_gather_variant_is_bit_identical(cuda):
+    """The opt-in fused-gather GEMM (A rows gathered by tile::gather4 straight into shared
+    memory, NGRAM_FUSED_GATHER=1, selected once per process) feeds the tensor cores the same
+    bf16 rows in the same K order as the default X path: identical bits (D = 768, T = 900)."""
+    import os, subprocess, sys, tempfile
+    code = f"""
+import sys, numpy as np, torch
+sys.path[:0] = {[os.path.dirname(__file__), os.path.dirname(os.path.dirname(__file__)),
+                 os.path.join(os.path.dirname(os.path.dirname(__file__)), "oracle")]!r}
+import oracle as O
+from helpers import dev_i64, dev_u32
+from paper_2601_21204_b200 import ngram as G
+cfg = O.make_default_config(3000, 768, 4, 4)
+hb = O.make_bank(cfg, 29, round_bf16=True)
+db = G.DeviceBank(cfg).upload(hb.base, hb.sub, hb.proj)
+toks = O.uniform_tokens(83, 3000, 900)
+r, m = G.embed_forward(db, dev_u32(torch, toks, "cuda:0"), dev_i64(torch, [0, 400, 900], "cuda:0"), merged=True)
+db.sync_errors()
+np.save(sys.argv[1], torch.stack([r, m]).view(torch.int32).cpu().numpy())
+"""
+    outs = []
+    with tempfile.TemporaryDirectory() as td:
+        for v in ("0", "1"):
+            path = os.path.join(td, f"o{v}.npy")
+            subprocess.run([sys.executable, "-c", code, path], check=True, timeout=300,
+                           env={**os.environ, "NGRAM_FUSED_GATHER": v})
+            outs.append(np.load(path))
+    assert np.array_equal(outs[0], outs[1])
