@@ -107,7 +107,7 @@ def test_load_file_into_row_shards(small, cuda):  # ingest sl
     sharded forward over those banks equals the unsharded forward bit for bit."""
     cfg, hb, path = small
     full = G.DeviceBank(cfg).load_file(path)
-    P, nseq, L = 2, 4, 120
+    P, nseq, L = 2, 4, 300  # T = 1200 > 1024: both sides in the prefill regime
     toks = O.uniform_tokens(9, cfg["base_vocab"], nseq * L)
     t_all, off_all = dev_u32(torch, toks, cuda), dev_i64(torch, np.arange(0, nseq * L + 1, L), cuda)
     ref, _ = G.embed_forward(full, t_all, off_all)
