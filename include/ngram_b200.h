@@ -199,6 +199,14 @@ int ngram_verify_commit_host(ngram_decode* st, const uint32_t* draft, int L, con
                              float* merged_out);
 /* Read back the state (host buffers): ring batch x (N-1), length, last token. */
 int ngram_decode_get_state(ngram_decode* st, uint32_t* ring, uint64_t* length, uint32_t* last);
+/* Device pointer of the rings [batch][max_order-1] (oldest first): the `prior` of a decode
+ * step / verify block.  On a row-sharded bank a decode state holds only ring state
+ * (create / reset / commit / get_state); its steps run through the shard group: all-gather
+ * the step's tokens and the rings, ngram_shard_scatter_rows(all_prior = gathered rings),
+ * barrier, ngram_shard_project (merged out), then ngram_commit on the local state. */
+int ngram_decode_ring(ngram_decode* st, uint32_t** ring);
+/* Stream-ordered copy of the rings [batch][max_order-1] into dst (device or host). */
+int ngram_decode_copy_ring(ngram_decode* st, uint32_t* dst, void* stream);
 
 /* ------------------------------------------------------------------ multi-GPU (row shards) */
 /* Row-sharded exchange.  A process group of shard_count ranks, one GPU

@@ -40,7 +40,7 @@ SYMBOLS = [
     "ngram_plne_create", "ngram_plne_destroy", "ngram_plne_forward", "ngram_plne_backward",
     "ngram_plne_forward_host", "ngram_plne_backward_host",
     "ngram_grad_create_ex", "ngram_grad_sparse_rows", "ngram_grad_sparse_read", "ngram_amplify_host",
-    "ngram_amplify_backward_host",
+    "ngram_amplify_backward_host", "ngram_decode_ring", "ngram_decode_copy_ring",
 ]
 
 
@@ -164,6 +164,8 @@ def lib() -> C.CDLL:
         "ngram_grad_sparse_read": ([vp, i64, i64, vp, vp, vp], i32),
         "ngram_amplify_host": ([i32, i32, i64, vp, vp, vp, vp], i32),
         "ngram_amplify_backward_host": ([vp, i64, vp, vp, vp, vp, vp], i32),
+        "ngram_decode_ring": ([vp, C.POINTER(vp)], i32),
+        "ngram_decode_copy_ring": ([vp, vp, vp], i32),
         "ngram_plne_backward_host": ([vp, vp, vp, vp, vp, vp, vp, i64, vp, vp, vp, vp, vp], i32),
     }
     for name, (args, res) in sig.items():

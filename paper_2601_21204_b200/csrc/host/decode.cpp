@@ -20,6 +20,9 @@ namespace {
 bool decode_block(ngram_decode* d, const uint32_t* draft, int L, uint64_t* ids_out, void* merged_out, int out_dtype,
                   cudaStream_t st, const ngk::DecodeCommit* commit = nullptr) {
     ngram_bank* b = d->bank;
+    if (b->shard_count != 1)
+        throw Error(NGRAM_EINVAL, "decode steps on a row-sharded bank run through the shard group "
+                                  "(ngram_shard_scatter_rows with the rings as prior + ngram_shard_project)");
     const int64_t T = d->batch * L;
     const int64_t Tpad = round_up(T, kRowPad);
     reset_error_word(b, st);
@@ -41,7 +44,6 @@ extern "C" {
 int ngram_decode_create(ngram_bank* b, int64_t batch, int max_draft, ngram_decode** out) {
     NGRAM_API_BEGIN
     if (!b || !out || batch < 1 || max_draft < 1) throw Error(NGRAM_EINVAL, "ngram_decode_create: bad argument");
-    if (b->shard_count != 1) throw Error(NGRAM_EINVAL, "decode state needs a full (unsharded) bank");
     *out = nullptr;
     DeviceGuard g(b->device);
     auto d = std::make_unique<ngram_decode>();
@@ -122,6 +124,23 @@ int ngram_commit(ngram_decode* d, const uint32_t* draft, int L, const int32_t* a
     ngk::launch_decode_commit(d->bank->shape, d->ring.p, d->length.p, d->last.p, draft, L, accept, d->batch,
                               d->bank->err.p, d->derr.p, static_cast<cudaStream_t>(stream));
     NGH_CUDA(cudaGetLastError());
+    NGRAM_API_END
+}
+
+int ngram_decode_ring(ngram_decode* d, uint32_t** ring) {
+    NGRAM_API_BEGIN
+    if (!d || !ring) throw Error(NGRAM_EINVAL, "ngram_decode_ring: bad argument");
+    *ring = d->ring.p;
+    NGRAM_API_END
+}
+
+int ngram_decode_copy_ring(ngram_decode* d, uint32_t* dst, void* stream) {
+    NGRAM_API_BEGIN
+    if (!d || !dst) throw Error(NGRAM_EINVAL, "ngram_decode_copy_ring: bad argument");
+    DeviceGuard g(d->bank->device);
+    const size_t R = size_t(std::max(d->bank->cfg.max_order - 1, 0));
+    if (R) NGH_CUDA(cudaMemcpyAsync(dst, d->ring.p, size_t(d->batch) * R * 4, cudaMemcpyDefault,
+                                    static_cast<cudaStream_t>(stream)));
     NGRAM_API_END
 }
 

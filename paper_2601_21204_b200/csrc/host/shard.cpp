@@ -141,8 +141,11 @@ int ngram_shard_project(ngram_shard_group* g, const uint32_t* home_tokens, int64
     DeviceGuard dg(b->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     XBuf& xb = g->x[g->parity];
+    // small home batches (sharded decode / verify) take the split-K GEMM, as the unsharded
+    // decode path does: the same regime as the single-GPU result for the same rows
     run_projection(b, home_tokens, nullptr, round_up(std::max<int64_t>(home_T, 1), kRowPad), home_T, rows_out,
-                   merged_out, out_dtype == NGRAM_BF16, b->ws.merged_f32.p, &xb.map, st, -1, nullptr, false, nullptr);
+                   merged_out, out_dtype == NGRAM_BF16, b->ws.merged_f32.p, &xb.map, st, -1, nullptr,
+                   ngk::small_t_regime(b->shape.D, home_T, b->num_sms), nullptr);
     g->parity ^= 1;
     NGRAM_API_END
 }

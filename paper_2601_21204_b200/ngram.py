@@ -305,6 +305,13 @@ class DecodeState:
     def commit(self, draft: torch.Tensor, accept: torch.Tensor, stream=None):
         check(abi.lib().ngram_commit(self.handle, _ptr(draft), draft.shape[1], _ptr(accept), _stream(stream)))
 
+    def rings(self, stream=None) -> torch.Tensor:
+        """Device copy of the rings [batch, N-1] (int32 storage): the decode windows' prior."""
+        R = max(self.bank.N - 1, 0)
+        out = torch.empty((self.batch, max(R, 1)), dtype=torch.int32, device=self.dev)[:, :R]
+        check(abi.lib().ngram_decode_copy_ring(self.handle, _ptr(out), _stream(stream)))
+        return out
+
     def state(self):
         R = max(self.bank.N - 1, 0)
         ring = np.zeros((self.batch, max(R, 1)), np.uint32)
@@ -580,6 +587,35 @@ class ShardGroup:
         check(abi.lib().ngram_shard_project(self.handle, _ptr(home_tokens), T, _ptr(out_rows if rows else None),
                                             _ptr(out_merged if merged else None), _DT[out_dtype], _stream(stream)))
         return (out_rows if rows else None), (out_merged if merged else None)
+
+
+def sharded_verify_block(group: ShardGroup, state: DecodeState, draft: torch.Tensor, out_dtype=torch.bfloat16,
+                         pg=None, barrier=None) -> torch.Tensor:
+    """A verify block (L = 1: a decode step) of this rank's home streams on row-sharded tables
+    (DESIGN.md 7): all-gather the drafts and the decode rings (the windows' prior), scatter the
+    owned rows into every home X, barrier, project the home rows (merged, pre-amplification,
+    cache.hpp:122-124).  `state` is this rank's DecodeState on its shard bank; commit with
+    state.commit(draft, accept) afterwards.  Every rank must hold the same number of streams."""
+    import torch.distributed as dist
+    world = dist.get_world_size(pg)
+    Bh, L = draft.shape
+    R = max(state.bank.N - 1, 0)
+    all_draft = torch.empty((world * Bh, L), dtype=torch.int32, device=draft.device)
+    dist.all_gather_into_tensor(all_draft, draft.contiguous().to(torch.int32), group=pg)
+    all_ring = None
+    if R:
+        all_ring = torch.empty((world * Bh, R), dtype=torch.int32, device=draft.device)
+        dist.all_gather_into_tensor(all_ring, state.rings().contiguous(), group=pg)
+    all_off = torch.arange(0, world * Bh * L + 1, L, dtype=torch.int64, device=draft.device)
+    group.scatter(all_draft.view(-1), all_off, [r * Bh * L for r in range(world + 1)], all_ring)
+    if barrier is not None:
+        barrier()
+    else:
+        one = torch.ones(1, device=draft.device)
+        dist.all_reduce(one, group=pg)  # stream-ordered (NCCL): every rank's rows have landed
+    _, merged = group.project(draft.contiguous().view(-1).to(torch.int32), rows=False, merged=True,
+                              out_dtype=out_dtype)
+    return merged.view(Bh, L, -1)
 
 
 def connect_shard_groups(group: ShardGroup, pg=None) -> None:

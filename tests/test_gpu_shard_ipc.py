@@ -78,3 +78,70 @@ def test_two_process_ipc_exchange_bit_identical(cuda):
         for p in procs:
             assert p.wait(timeout=300) == 0
         assert all(int(np.load(o)[0]) == 1 for o in outs)
+
+
+VERIFY_WORKER = r"""
+import os, sys
+import numpy as np, torch, torch.distributed as dist
+sys.path[:0] = [{root!r}, {tests!r}, os.path.join({root!r}, "oracle")]
+import oracle as O
+from paper_2601_21204_b200 import ngram as G
+rank, world = int(sys.argv[1]), 2
+dist.init_process_group("gloo", init_method="tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+torch.cuda.set_device(0)
+dev = torch.device("cuda", 0)
+cfg = O.make_default_config(4000, 768, 4, 4)
+cfg["amplification"] = "none"  # the cache path returns merged vectors
+Bh, L = 6, 4
+rng = np.random.default_rng(11)
+prior = torch.from_numpy(rng.integers(0, 4000, size=(world * Bh, 3)).astype(np.int32)).to(dev)
+lengths = torch.full((world * Bh,), 100, dtype=torch.int64, device=dev)
+draft = torch.from_numpy(rng.integers(0, 4000, size=(world * Bh, L)).astype(np.int32)).to(dev)
+accept = torch.from_numpy(rng.integers(0, L + 1, size=world * Bh).astype(np.int32)).to(dev)
+# single-GPU reference: every stream on the full bank
+full = G.DeviceBank(cfg).generate(5)
+ref_state = G.DecodeState(full, world * Bh, max_draft=L)
+ref_state.reset(prior, lengths)
+ref = ref_state.verify(draft, out_dtype=torch.float32)
+ref_state.commit(draft, accept)
+ref_ring = ref_state.state()[0]
+# this rank: its home streams on its shard bank
+home = slice(rank * Bh, (rank + 1) * Bh)
+bank = G.DeviceBank(cfg, shard_rank=rank, shard_count=world).generate(5)
+group = G.ShardGroup(bank, Bh * L)
+G.connect_shard_groups(group)
+st = G.DecodeState(bank, Bh, max_draft=L)
+st.reset(prior[home].contiguous(), lengths[home].contiguous())
+
+def barrier():
+    torch.cuda.synchronize()
+    dist.barrier()
+
+ok = True
+for step in range(2):  # both halves of the double-buffered X
+    merged = G.sharded_verify_block(group, st, draft[home], out_dtype=torch.float32, barrier=barrier)
+    torch.cuda.synchronize()
+    dist.barrier()  # nobody scatters into a buffer a peer still projects from
+    ok = ok and torch.equal(merged, ref[home])
+st.commit(draft[home].contiguous(), accept[home].contiguous())
+ok = ok and np.array_equal(st.state()[0], ref_ring[home])
+np.save(sys.argv[2], np.array([1 if ok else 0]))
+dist.barrier()
+dist.destroy_process_group()
+"""
+
+
+def test_two_process_sharded_verify_and_commit(cuda):
+    """Config E on row-sharded tables, two ranks: all-gathered drafts + rings, owned rows
+    scattered over CUDA IPC, split-K projection of the home block, local commit -- identical
+    to the single-GPU verify + commit of the same streams."""
+    code = VERIFY_WORKER.format(root=ROOT, tests=HERE, port=_free_port())
+    with tempfile.TemporaryDirectory() as td:
+        procs, outs = [], []
+        for r in range(2):
+            out = os.path.join(td, f"r{r}.npy")
+            outs.append(out)
+            procs.append(subprocess.Popen([sys.executable, "-c", code, str(r), out]))
+        for p in procs:
+            assert p.wait(timeout=300) == 0
+        assert all(int(np.load(o)[0]) == 1 for o in outs)
