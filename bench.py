@@ -304,10 +304,19 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # NGRAM_BENCH_ONE_DEVICE=1 (functional test of the multi-rank flow on a 1-GPU box): every
+    # rank on cuda:0 over gloo.  The kernels never wait on each other (the barrier is a host
+    # collective), but the numbers are not multi-GPU numbers.
+    one_dev = os.environ.get("NGRAM_BENCH_ONE_DEVICE") == "1"
+    if one_dev:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     sharding = args.sharding if world > 1 else "single"
 
     cfg, nseq, seq_len, label = workload(args.workload)
@@ -518,6 +527,8 @@ def run_ours(args):
     }
     if fallback:
         line["config"]["sharding_fallback"] = fallback
+    if one_dev and world > 1:
+        line["config"]["one_device_test"] = "all ranks on cuda:0 over gloo (functional only)"
     if sharding == "row":
         remote = T * world * B * d * 2 * (world - 1) / world / world  # rows this rank ships to peers
         line["nvlink"] = {"remote_bytes_per_rank": remote, "scatter_ms": st_ms[1],

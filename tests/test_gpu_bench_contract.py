@@ -29,3 +29,30 @@ def test_bench_json_contract(cuda):
     for k in ("sm_mhz", "sm_max_mhz", "reasons"):
         assert k in line["clocks"], k
     assert line["gpu_launches"] > 0 and line["config"]["workload"]
+
+
+@pytest.mark.parametrize("sharding", ["row", "replica"])
+def test_bench_two_ranks_one_device(cuda, sharding):
+    """The N > 1 flow of bench.py (torchrun, row-sharded exchange over CUDA IPC or replicas,
+    max-over-ranks timing, rank-0 JSON line) run functionally with both ranks on cuda:0 over
+    gloo -- the pool has one GPU, so this is the only way to execute it before the driver's
+    multi-GPU run."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, NGRAM_BENCH_ONE_DEVICE="1")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                          "--gpus", "2", "--steps", "3", "--warmup", "3", "--workload", "B", "--sharding", sharding],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1  # rank 0 only
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["gpu_launches"] > 0
+    assert line["config"]["sharding"] == sharding and "sharding_fallback" not in line["config"]
+    assert line["e2e"]["value"] > 0 and "cpu_baseline" not in line
+    if sharding == "row":
+        assert set(line["stages_ms"]) == {"all_gather_tokens", "k1_k2_scatter_nvlink", "barrier",
+                                          "k3_projection_epilogue"}
