@@ -596,6 +596,78 @@ def run_decode(args):
                       "cuda_graph": True, "out_dtype": "bf16", "results": res}))
 
 
+def run_decode_sharded(args):
+    """Configs D / E on row-sharded tables (8 GPUs): every rank serves B home
+    streams on its 1/world row block; per step the drafts and rings are all-gathered, owned rows
+    scattered into the home X over NVLink peer stores, one NCCL all-reduce is the barrier, the
+    home block is projected (split-K) and committed.  Eager launches (no CUDA graph: the
+    collectives run through torch.distributed); time = max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2601_21204_b200 import ngram as G
+    world, rank = int(os.environ["WORLD_SIZE"]), int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    one_dev = os.environ.get("NGRAM_BENCH_ONE_DEVICE") == "1"
+    if one_dev:
+        local = 0
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if one_dev:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg, _, _, _ = workload("C" if not os.environ.get("NGRAM_BENCH_DECODE_CFG") else os.environ["NGRAM_BENCH_DECODE_CFG"])
+    cfg = dict(cfg)
+    cfg["amplification"] = "none"  # the cache path returns merged vectors (cache.hpp:122-124)
+    bank = G.DeviceBank(cfg, device=local, shard_rank=rank, shard_count=world).generate(1234)
+    L = 1 if args.workload == "D" else args.draft
+    batches = [int(b) for b in args.batches.split(",")]
+    group = G.ShardGroup(bank, max(batches) * L)
+    G.connect_shard_groups(group)
+    rng = np.random.default_rng(1 + rank)
+    res = {}
+    stream = torch.cuda.current_stream()
+    barrier = (lambda: (torch.cuda.synchronize(), dist.barrier())) if one_dev else None
+    for B in batches:
+        st = G.DecodeState(bank, B, max_draft=L)
+        prior = torch.from_numpy(rng.integers(0, cfg["base_vocab"], size=(B, cfg["max_order"] - 1))
+                                 .astype(np.int32)).to(dev)
+        st.reset(prior, torch.full((B,), 4096, dtype=torch.int64, device=dev))
+        toks = torch.from_numpy(rng.integers(0, cfg["base_vocab"], size=(B, L)).astype(np.int32)).to(dev)
+        acc = torch.from_numpy(rng.integers(0, L + 1, size=B).astype(np.int32)).to(dev)
+
+        def one():
+            G.sharded_verify_block(group, st, toks, out_dtype=torch.bfloat16, barrier=barrier)
+            st.commit(toks, acc)
+        for _ in range(args.warmup):
+            one()
+        torch.cuda.synchronize()
+        dist.barrier()
+        n = args.steps * 10
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record(stream)
+        for _ in range(n):
+            one()
+        ev[1].record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([ev[0].elapsed_time(ev[1]) / n], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        res[B] = {"us_per_step": ms * 1e3, "tokens_per_s": world * B * L / (ms * 1e-3)}
+        st.close()
+    bank.sync_errors()
+    if rank == 0:
+        line = {"metric": "ngram_decode_tokens_per_sec" if args.workload == "D" else "ngram_verify_tokens_per_sec",
+                "workload": args.workload, "draft": L, "n_gpus": world, "sharding": "row",
+                "scaling": "weak", "home_streams_per_rank": batches, "cuda_graph": False, "out_dtype": "bf16",
+                "results": res}
+        if one_dev:
+            line["one_device_test"] = "all ranks on cuda:0 over gloo (functional only)"
+        print(json.dumps(line))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -617,6 +689,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload in ("D", "E") and int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        run_decode_sharded(args)
     elif args.workload in ("D", "E"):
         run_decode(args)
     else:

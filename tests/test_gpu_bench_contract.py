@@ -56,3 +56,22 @@ def test_bench_two_ranks_one_device(cuda, sharding):
     if sharding == "row":
         assert set(line["stages_ms"]) == {"all_gather_tokens", "k1_k2_scatter_nvlink", "barrier",
                                           "k3_projection_epilogue"}
+
+
+def test_bench_sharded_verify_two_ranks_one_device(cuda):
+    """bench.py --workload E at N = 2 (row-sharded verify + commit), functional, one device."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, NGRAM_BENCH_ONE_DEVICE="1", NGRAM_BENCH_DECODE_CFG="B")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                          "--gpus", "2", "--steps", "1", "--warmup", "3", "--workload", "E", "--batches", "1,8",
+                          "--draft", "4"], capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and set(line["results"]) == {"1", "8"}
+    assert all(v["tokens_per_s"] > 0 for v in line["results"].values())
