@@ -328,6 +328,32 @@ int ngram_plne_backward_host(ngram_plne* p, ngram_grad* bank_grads, const float*
                              const float* x, const uint32_t* tokens, const int64_t* seq_offsets, int64_t nseq,
                              const uint32_t* prior, const float* upstream, float* d_gate, float* d_down, float* dx);
 
+/* ------------------------------------------------------------------ corpus analysis */
+/* Replaces corpus_analyzer (analysis.hpp:45-93, analysis.cpp:44-176): every position of every
+ * sequence contributes one zero-padded window per order; counts windows seen, distinct windows
+ * (exact, by their 128-bit polynomial value) and distinct buckets per (order, modulus).
+ * Create checks and messages follow analysis.cpp:47-85 (EINVAL).  A token >= base_vocab:
+ * like add_sequence/add_corpus, the sequences up to and including the bad one are counted
+ * (with their full length) and the positions before the bad token are analysed; the error is
+ * NGRAM_ERANGE from ngram_analyzer_add_host, or from ngram_analyzer_sync_errors after the
+ * device entry.  Not thread-safe across concurrent adds to one analyzer (serialised). */
+typedef struct ngram_analyzer ngram_analyzer;
+int ngram_analyzer_create(int device, uint64_t base_vocab, const int* orders, int n_orders, const uint64_t* moduli,
+                          int n_moduli, ngram_analyzer** out);
+void ngram_analyzer_destroy(ngram_analyzer* a);
+/* tokens: dev u32 [T]; seq_offsets: dev i64 [nseq+1], 0 = off[0] <= ... <= off[nseq] = T. */
+int ngram_analyzer_add(ngram_analyzer* a, const uint32_t* tokens, const int64_t* seq_offsets, int64_t nseq, int64_t T,
+                       void* stream);
+/* Host tokens / offsets (checked), synchronous. */
+int ngram_analyzer_add_host(ngram_analyzer* a, const uint32_t* tokens, const int64_t* seq_offsets, int64_t nseq);
+/* Set-union merge (analysis.cpp:125-141): same base / orders / moduli, same device. */
+int ngram_analyzer_merge(ngram_analyzer* dst, ngram_analyzer* src, void* stream);
+int ngram_analyzer_sync_errors(ngram_analyzer* a);
+/* Synchronous.  ngrams_seen / distinct_ngrams: [n_orders]; distinct_buckets: [n_orders][n_moduli]
+ * (order-major, the reference's layout).  Any pointer may be NULL. */
+int ngram_analyzer_stats(ngram_analyzer* a, uint64_t* sequences, uint64_t* tokens, uint64_t* ngrams_seen,
+                         uint64_t* distinct_ngrams, uint64_t* distinct_buckets);
+
 #ifdef __cplusplus
 }
 #endif

@@ -62,6 +62,9 @@ def lib():
                 C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_void_p, C.c_void_p, C.c_int]
         L.or_ffn_plne_f64.argtypes = plne + [C.c_void_p]
         L.or_ffn_plne_backward_f64.argtypes = plne + [C.c_void_p] * 4 + [C.POINTER(C.c_void_p)] * 2 + [C.c_void_p]
+        an = [C.c_uint64, C.c_void_p, C.c_int, C.c_void_p, C.c_int, _u32p, C.c_void_p, C.c_int64, _u64p, _u64p,
+              _u64p, _u64p]
+        L.or_corpus_analyze.argtypes = an
         L.or_synth_value.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint32, C.c_float]
         L.or_synth_value.restype = C.c_float
         L.or_synth_scale.argtypes = [C.c_double]
@@ -145,6 +148,8 @@ def ref():
         L.ref_ffn_plne_backward_f64.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, _u32p,
                                                 C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                                 C.c_void_p, C.c_void_p]
+        L.ref_corpus_analyze.argtypes = [C.c_uint64, C.c_void_p, C.c_int, C.c_void_p, C.c_int, _u32p, C.c_void_p,
+                                         C.c_int64, _u64p, _u64p, _u64p, _u64p]
         L.ref_generate_zipf_markov.argtypes = [C.c_uint32, C.c_int64, C.c_int64, C.c_uint64, C.c_double, C.c_double,
                                                _u32p]
         L.ref_cache_create.argtypes = [C.c_char_p]
@@ -403,3 +408,43 @@ def synth_host_bank(cfg, seed):
     gain = np.ones(D, np.float32) if amp == 2 else np.zeros(0, np.float32)
     bias = np.zeros(D, np.float32) if amp == 2 else np.zeros(0, np.float32)
     return HostBank(cfg, base, sub, proj, gain, bias)
+
+
+# ----------------------------------------------------------------------------- analysis
+def _flat(seqs):
+    off = np.zeros(len(seqs) + 1, np.int64)
+    off[1:] = np.cumsum([len(q) for q in seqs])
+    toks = np.ascontiguousarray(np.concatenate([np.asarray(q, np.uint32) for q in seqs])
+                                if seqs and off[-1] else np.zeros(1, np.uint32), np.uint32)
+    return toks, off
+
+
+def _analyze(fn, v0, orders, moduli, seqs):
+    toks, off = _flat(seqs)
+    o = (C.c_int * len(orders))(*orders)
+    m = (C.c_uint64 * len(moduli))(*moduli)
+    meta, seen, dist = np.zeros(2, np.uint64), np.zeros(len(orders), np.uint64), np.zeros(len(orders), np.uint64)
+    bk = np.zeros(len(orders) * len(moduli), np.uint64)
+    rc = fn(v0, o, len(orders), m, len(moduli), toks, off.ctypes.data, len(seqs), meta, seen, dist, bk)
+    return rc, {"sequences_seen": int(meta[0]), "tokens_seen": int(meta[1]),
+                "ngrams_seen": {o_: int(seen[i]) for i, o_ in enumerate(orders)},
+                "distinct_ngrams": {o_: int(dist[i]) for i, o_ in enumerate(orders)},
+                "distinct_buckets": {(o_, m_): int(bk[i * len(moduli) + j]) for i, o_ in enumerate(orders)
+                                     for j, m_ in enumerate(moduli)}}
+
+
+def corpus_analyze(v0, orders, moduli, seqs):
+    """corpus_analyzer restated (analysis.cpp:44-176): (status, stats) -- status -2 = a token
+    out of range (stats then hold the reference's partial counts)."""
+    return _analyze(lib().or_corpus_analyze, v0, orders, moduli, seqs)
+
+
+def ref_corpus_analyze(v0, orders, moduli, seqs):
+    """The reference corpus_analyzer itself (oracle/_ref)."""
+    return _analyze(ref().ref_corpus_analyze, v0, orders, moduli, seqs)
+
+
+def ref_zipf_markov(vocab, sequences, seq_len, seed, exponent=1.1, markov_prob=0.35):
+    out = np.zeros(sequences * seq_len, np.uint32)
+    assert ref().ref_generate_zipf_markov(vocab, sequences, seq_len, seed, exponent, markov_prob, out) == 0
+    return [out[i * seq_len:(i + 1) * seq_len] for i in range(sequences)]

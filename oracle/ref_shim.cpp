@@ -17,6 +17,7 @@
 #include <thread>
 #include <vector>
 
+#include "ngram/analysis.hpp"
 #include "ngram/cache.hpp"
 #include "ngram/config.hpp"
 #include "ngram/corpus.hpp"
@@ -298,6 +299,38 @@ int ref_ffn_plne_backward_f64(void* h, const double* gate, const double* down, i
             std::memcpy(g_proj[b], gb.projections[b].data(), gb.projections[b].size() * 8);
         std::memcpy(dx, d.data(), d.size() * 8);
         return 0;
+    } catch (...) {
+        return map_exc();
+    }
+}
+
+// analysis.cpp:44-176: corpus_analyzer over the batch (add_sequence per sequence, the error of
+// a bad token caught), then stats().  meta: [sequences, tokens]; seen / distinct [n_orders];
+// buckets [n_orders][n_moduli].  Returns the add's status (-2 = out_of_range) after filling
+// the stats, or the constructor's error.
+int ref_corpus_analyze(uint64_t v0, const int* orders, int n_orders, const uint64_t* moduli, int n_moduli,
+                       const uint32_t* tokens, const int64_t* off, int64_t nseq, uint64_t* meta, uint64_t* seen,
+                       uint64_t* distinct, uint64_t* buckets) {
+    try {
+        corpus_analyzer an(v0, std::vector<int>(orders, orders + n_orders),
+                           std::vector<std::uint64_t>(moduli, moduli + n_moduli));
+        int rc = 0;
+        try {
+            for (int64_t s = 0; s < nseq; ++s)
+                an.add_sequence(std::span<const token_id>(tokens + off[s], std::size_t(off[s + 1] - off[s])));
+        } catch (...) {
+            rc = map_exc();
+        }
+        const auto st = an.stats();
+        meta[0] = st.sequences_seen;
+        meta[1] = st.tokens_seen;
+        for (int i = 0; i < n_orders; ++i) {
+            seen[i] = st.ngrams_seen.at(orders[i]);
+            distinct[i] = st.distinct_ngrams.at(orders[i]);
+            for (int j = 0; j < n_moduli; ++j)
+                buckets[i * n_moduli + j] = st.distinct_buckets.at({orders[i], moduli[j]});
+        }
+        return rc;
     } catch (...) {
         return map_exc();
     }

@@ -41,6 +41,8 @@ SYMBOLS = [
     "ngram_plne_forward_host", "ngram_plne_backward_host",
     "ngram_grad_create_ex", "ngram_grad_sparse_rows", "ngram_grad_sparse_read", "ngram_amplify_host",
     "ngram_amplify_backward_host", "ngram_decode_ring", "ngram_decode_copy_ring",
+    "ngram_analyzer_create", "ngram_analyzer_destroy", "ngram_analyzer_add", "ngram_analyzer_add_host",
+    "ngram_analyzer_merge", "ngram_analyzer_sync_errors", "ngram_analyzer_stats",
 ]
 
 
@@ -167,6 +169,13 @@ def lib() -> C.CDLL:
         "ngram_decode_ring": ([vp, C.POINTER(vp)], i32),
         "ngram_decode_copy_ring": ([vp, vp, vp], i32),
         "ngram_plne_backward_host": ([vp, vp, vp, vp, vp, vp, vp, i64, vp, vp, vp, vp, vp], i32),
+        "ngram_analyzer_create": ([i32, u64, vp, i32, vp, i32, C.POINTER(vp)], i32),
+        "ngram_analyzer_destroy": ([vp], None),
+        "ngram_analyzer_add": ([vp, vp, vp, i64, i64, vp], i32),
+        "ngram_analyzer_add_host": ([vp, vp, vp, i64], i32),
+        "ngram_analyzer_merge": ([vp, vp, vp], i32),
+        "ngram_analyzer_sync_errors": ([vp], i32),
+        "ngram_analyzer_stats": ([vp, vp, vp, vp, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

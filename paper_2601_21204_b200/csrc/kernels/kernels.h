@@ -178,4 +178,42 @@ void launch_shard_scatter(const Shape& s, const int32_t* grow_all, int64_t Tpad_
                           int nranks, const __nv_bfloat16* sub, __nv_bfloat16* const* peer_x, int64_t T_all,
                           const unsigned long long* err, cudaStream_t st);
 
+// ---- corpus analysis (analysis.cu; corpus_analyzer, analysis.cpp:93-121)
+// Open-addressing set of 128-bit keys (x = low word); all-ones = empty slot; mask = slots - 1.
+struct AnSet {
+    ulonglong2* slots;
+    uint64_t mask;
+};
+// Distinct-bucket store of one (order, modulus): a bitmap of m bits, or (bits == null) a set.
+struct AnBucket {
+    unsigned long long* bits;
+    AnSet set;
+};
+struct AnDev {
+    uint64_t V0;
+    int n_orders, n_moduli;
+    const int* orders;              // [n_orders]
+    const ulonglong2* vpow;         // [max_order] V0^j as 128-bit (x = low word)
+    const uint64_t* moduli;         // [n_moduli]
+    const uint64_t* barrett;        // floor(2^64 / m) for 2 <= m <= 2^32, else 0
+    const uint64_t* c64;            // 2^64 mod m (Barrett path)
+    const AnSet* ngram_sets;        // [n_orders]
+    const AnBucket* buckets;        // [n_orders * n_moduli], order-major (analysis.hpp:92)
+    unsigned long long* counts;     // [n_orders] distinct windows, then [n_orders * n_moduli] buckets
+    unsigned long long* err;        // set to 1 if a set overflowed (host load bound violated)
+};
+// validate -> account (counters, insert limit, first error) -> insert.  first_bad: device
+// scratch word, preset to ~0 by the caller.  meta: [sequences, tokens, ngrams_seen per order].
+// err_pos: [position, token] of the analyzer's first bad token (~0 when clear).
+void launch_an_add(const AnDev& a, const uint32_t* tokens, const int64_t* off, int64_t nseq, int64_t T,
+                   unsigned long long* first_bad, unsigned long long* meta, unsigned long long* err_pos,
+                   int num_sms, cudaStream_t st);
+void launch_an_rehash(const ulonglong2* old_slots, uint64_t old_n, const AnSet& dst, unsigned long long* err,
+                      int num_sms, cudaStream_t st);
+void launch_an_merge_set(const ulonglong2* src, uint64_t n, const AnSet& dst, unsigned long long* counter,
+                         unsigned long long* err, int num_sms, cudaStream_t st);
+void launch_an_merge_bits(const unsigned long long* src, uint64_t nwords, unsigned long long* dst,
+                          unsigned long long* counter, int num_sms, cudaStream_t st);
+void launch_an_merge_meta(const unsigned long long* src, unsigned long long* dst, int n, cudaStream_t st);
+
 }  // namespace ngk

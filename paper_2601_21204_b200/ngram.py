@@ -530,6 +530,89 @@ class PlneLayer:
                                             _ptr(d_gate), _ptr(d_down), _ptr(dx), _stream(stream)))
 
 
+# ----------------------------------------------------------------------------- corpus analysis
+class CorpusAnalyzer:
+    """corpus_analyzer (analysis.hpp:45-93) on the device: windows seen, exact distinct windows
+    and distinct buckets per (order, modulus) over every position of every sequence.  add()
+    takes device tensors (tokens u32/i32 [T], offsets i64 [nseq+1]); add_host() numpy arrays
+    or a list of sequences.  stats() / reports() mirror the reference's structs."""
+
+    def __init__(self, base_vocab: int, orders: Sequence[int], moduli: Sequence[int], device: int = 0):
+        self.base_vocab, self.orders, self.moduli = int(base_vocab), [int(o) for o in orders], [int(m) for m in moduli]
+        o = (C.c_int * max(len(self.orders), 1))(*self.orders)
+        m = (C.c_uint64 * max(len(self.moduli), 1))(*self.moduli)
+        h = C.c_void_p()
+        check(abi.lib().ngram_analyzer_create(device, self.base_vocab, o, len(self.orders), m, len(self.moduli),
+                                              C.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            abi.lib().ngram_analyzer_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def add(self, tokens: torch.Tensor, seq_offsets: torch.Tensor, stream=None) -> None:
+        check(abi.lib().ngram_analyzer_add(self.handle, _ptr(tokens), _ptr(seq_offsets), seq_offsets.numel() - 1,
+                                           tokens.numel(), _stream(stream)))
+
+    def add_host(self, seqs) -> None:
+        """seqs: a list of token sequences, or (flat u32 tokens, i64 offsets)."""
+        if isinstance(seqs, tuple):
+            toks, off = np.ascontiguousarray(seqs[0], np.uint32), np.ascontiguousarray(seqs[1], np.int64)
+        else:
+            lens = [len(q) for q in seqs]
+            off = np.zeros(len(seqs) + 1, np.int64)
+            off[1:] = np.cumsum(lens)
+            toks = np.ascontiguousarray(np.concatenate([np.asarray(q, np.uint64) for q in seqs])
+                                        if seqs and off[-1] else np.zeros(0, np.uint64))
+            if toks.size and int(toks.max()) > 0xFFFFFFFF:
+                raise OverflowError("token ids are u32")
+            toks = toks.astype(np.uint32)
+        check(abi.lib().ngram_analyzer_add_host(self.handle, toks.ctypes.data if toks.size else None,
+                                                off.ctypes.data, off.size - 1))
+
+    def add_sequence(self, seq) -> None:
+        self.add_host([seq])
+
+    def merge(self, other: "CorpusAnalyzer", stream=None) -> None:
+        check(abi.lib().ngram_analyzer_merge(self.handle, other.handle, _stream(stream)))
+
+    def sync_errors(self) -> None:
+        check(abi.lib().ngram_analyzer_sync_errors(self.handle))
+
+    def stats(self) -> dict:
+        no, nm = len(self.orders), len(self.moduli)
+        sq, tk = C.c_uint64(), C.c_uint64()
+        seen, dist = (C.c_uint64 * no)(), (C.c_uint64 * no)()
+        bk = (C.c_uint64 * (no * nm))()
+        check(abi.lib().ngram_analyzer_stats(self.handle, C.byref(sq), C.byref(tk), seen, dist, bk))
+        return {"sequences_seen": sq.value, "tokens_seen": tk.value,
+                "ngrams_seen": {o: seen[i] for i, o in enumerate(self.orders)},
+                "distinct_ngrams": {o: dist[i] for i, o in enumerate(self.orders)},
+                "distinct_buckets": {(o, m): bk[i * nm + j] for i, o in enumerate(self.orders)
+                                     for j, m in enumerate(self.moduli)}}
+
+    def reports(self, corpus_id: str = "") -> list:
+        """collision_report per (order, modulus), order-major (analysis.cpp:158-181)."""
+        s = self.stats()
+        if s["tokens_seen"] == 0:
+            raise ValueError("corpus_analyzer: empty corpus")
+        out = []
+        for o in self.orders:
+            for m in self.moduli:
+                b = s["distinct_buckets"][(o, m)]
+                out.append({"order": o, "modulus": m, "hit_rate": float(b) / float(m),
+                            "collision_count": s["distinct_ngrams"][o] - b, "corpus_id": corpus_id,
+                            "tokens_processed": s["tokens_seen"]})
+        return out
+
+
 # ----------------------------------------------------------------------------- row shards
 class ShardGroup:
     """Row-sharded exchange of one rank: double-buffered home X, peer buffers

@@ -7,10 +7,13 @@
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <set>
+#include <sstream>
 #include <string>
 #include <thread>
 #include <vector>
 
+#include "ngram/analysis.hpp"
 #include "ngram/cache.hpp"
 #include "ngram/config.hpp"
 #include "ngram/embedding.hpp"
@@ -77,6 +80,37 @@ static bool close_rows(const std::vector<float>& a, const std::vector<float>& b,
         err = std::max(err, std::fabs(double(a[i]) - double(b[i])));
     }
     return err <= tol * (mx + 1e-30);
+}
+
+// test_analysis.cpp:18-48: two-pass set oracle and random corpora (the reference's bigint
+// polynomial hash is exact here in 128 bits: V0 < 2^8, order <= 4).
+struct two_pass_counts {
+    std::uint64_t ngrams = 0, buckets = 0;
+};
+
+static two_pass_counts two_pass(const std::vector<token_sequence>& corpus, std::uint64_t v0, int order,
+                                std::uint64_t m) {
+    std::set<std::vector<token_id>> ng;
+    std::set<std::uint64_t> bk;
+    std::vector<token_id> w;
+    for (const auto& seq : corpus)
+        for (std::size_t pos = 0; pos < seq.size(); ++pos) {
+            window_at(seq, pos, order, w);
+            ng.insert(w);
+            unsigned __int128 h = 0;
+            for (const token_id t : w) h = h * v0 + t;
+            bk.insert(std::uint64_t(h % m));
+        }
+    return {ng.size(), bk.size()};
+}
+
+static std::vector<token_sequence> random_corpus(rng64& rng, std::uint32_t v0, std::size_t seqs, std::size_t max_len) {
+    std::vector<token_sequence> c(seqs);
+    for (auto& q : c) {
+        q.resize(1 + uniform_below(rng, max_len));
+        for (auto& t : q) t = token_id(uniform_below(rng, v0));
+    }
+    return c;
 }
 
 int main() {
@@ -532,6 +566,125 @@ int main() {
         CHECK(close_rows(a.base, b.base, 1e-5) && close_rows(a.ln_gain, b.ln_gain, 1e-5) &&
               close_rows(a.ln_bias, b.ln_bias, 1e-5));
         for (std::size_t i = 0; i < a.projections.size(); ++i) CHECK(close_rows(a.projections[i], b.projections[i], 1e-5));
+    });
+    test_case("generate_zipf_markov reproduces the reference stream", [] {  // corpus.cpp:211-271
+        // values printed by the reference (oracle/_ref) for vocab 1000, 2 x 64, seed 99
+        const auto z = generate_zipf_markov(1000, 2, 64, 99, 1.1, 0.85);
+        const std::vector<token_id> head{7, 4, 0, 7, 4, 9, 1, 43, 0, 7, 4, 9}, tail{296, 11, 14, 0, 7, 4};
+        CHECK(z.size() == 2 && z[0].size() == 64);
+        CHECK(std::equal(head.begin(), head.end(), z[0].begin()));
+        CHECK(std::equal(tail.begin(), tail.end(), z[1].end() - 6));
+        std::uint64_t sum = 0;
+        for (const auto& q : z)
+            for (auto t : q) sum += t;
+        CHECK(sum == 1946);
+    });
+    test_case("analysis: hit rates and worked collision examples", [] {  // test_analysis.cpp:50-113
+        std::vector<token_sequence> one{{5}};
+        CHECK(std::fabs(compute_hit_rate(one, {2, 10, 100}) - 0.01) < 1e-12);
+        std::vector<token_sequence> pairs;
+        for (std::uint32_t a = 0; a < 7; ++a)
+            for (std::uint32_t b = 0; b < 7; ++b) pairs.push_back({a, b});
+        CHECK(compute_hit_rate(pairs, {2, 7, 49}) == 1.0);
+        CHECK(compute_hit_rate(pairs, {2, 7, 30}) == 1.0);
+        const auto z = generate_zipf_markov(1000, 16, 4096, 99, 1.1, 0.85);
+        CHECK(compute_hit_rate(z, {4, 1000, 4999}) > compute_hit_rate(z, {2, 1000, 4999}));
+        std::vector<token_sequence> ex{{1, 5}, {3, 5}, {5, 5}};
+        CHECK(count_collisions(ex, {2, 10, 20}) == 2);
+        CHECK(count_collisions(ex, {2, 10, 23}) == 0);
+        std::vector<token_sequence> inj{{1, 2, 3, 4, 5, 6, 7, 8, 9}};
+        CHECK(count_collisions(inj, {2, 10, 1000000}) == 0);
+        rng64 rng(42);
+        for (int trial = 0; trial < 20; ++trial) {
+            const auto c = random_corpus(rng, 6, 4, 50);
+            CHECK(count_collisions(c, {2, 6, 36}) == 0);
+            CHECK(count_collisions(c, {3, 6, 216}) == 0);
+        }
+    });
+    test_case("analysis: streaming equals the two-pass oracle", [] {  // test_analysis.cpp:115-129
+        rng64 rng(0xabc);
+        for (int trial = 0; trial < 25; ++trial) {
+            const std::uint32_t v0 = 3 + std::uint32_t(uniform_below(rng, 200));
+            const auto c = random_corpus(rng, v0, 1 + uniform_below(rng, 6), 80);
+            const int order = 2 + int(uniform_below(rng, 3));
+            const std::uint64_t m = 1 + uniform_below(rng, 3000);
+            const auto want = two_pass(c, v0, order, m);
+            const hash_spec spec{order, v0, m};
+            CHECK(compute_hit_rate(c, spec) == double(want.buckets) / double(m));
+            CHECK(count_collisions(c, spec) == want.ngrams - want.buckets);
+        }
+    });
+    test_case("analysis: sweeps, advised sizes, monotonicity", [] {  // test_analysis.cpp:131-195
+        const auto corpus = generate_zipf_markov(100, 8, 512, 7, 1.1, 0.85);
+        const std::vector<std::uint64_t> moduli{101, 250, 999};
+        const auto r = sweep_vocab_sizes(corpus, 2, 100, moduli, "c");
+        CHECK(r.size() == 3);
+        for (std::size_t i = 0; i < r.size(); ++i) {
+            CHECK(r[i].modulus == moduli[i] && r[i].order == 2 && r[i].corpus_id == "c");
+            CHECK(r[i].hit_rate == compute_hit_rate(corpus, {2, 100, moduli[i]}));
+            CHECK(r[i].collision_count == count_collisions(corpus, {2, 100, moduli[i]}));
+            CHECK(r[i].tokens_processed == total_tokens(corpus));
+        }
+        CHECK(sweep_vocab_sizes(corpus, 2, 100, {}).empty());
+        CHECK_THROWS_AS(sweep_vocab_sizes(corpus, 2, 100, {250, 101}), std::invalid_argument);
+        const auto big = generate_zipf_markov(1000, 24, 4096, 20260809, 1.1, 0.85);
+        const auto rr = sweep_vocab_sizes(big, 2, 1000, {2000, 2500});
+        CHECK(rr.size() == 2 && rr[0].collision_count > rr[1].collision_count);
+        const auto o1 = two_pass(big, 1000, 2, 2000), o2 = two_pass(big, 1000, 2, 2500);
+        CHECK(rr[0].collision_count == o1.ngrams - o1.buckets && rr[1].collision_count == o2.ngrams - o2.buckets);
+        CHECK(advise_vocab_size(128000, 30) == 3904000 && advise_vocab_size(10, 2) == 25 && advise_vocab_size(2, 1) == 3);
+        CHECK_THROWS_AS(advise_vocab_size(1, 3), std::invalid_argument);
+        CHECK_THROWS_AS(advise_vocab_size(10, 0), std::invalid_argument);
+        CHECK(advise_vocab_size(1000, 30) == 30500);
+        CHECK(count_collisions(big, {2, 1000, 30500}) <= count_collisions(big, {2, 1000, 30000}));
+        rng64 rng(0xfeed);
+        for (int trial = 0; trial < 10; ++trial) {
+            auto c = random_corpus(rng, 50, 6, 60);
+            std::vector<token_sequence> prefix(c.begin(), c.begin() + 3);
+            CHECK(compute_hit_rate(c, {2, 50, 40}) >= compute_hit_rate(prefix, {2, 50, 40}));
+            CHECK(count_collisions(c, {2, 50, 40}) >= count_collisions(prefix, {2, 50, 40}));
+        }
+    });
+    test_case("analysis: sharded analyzers merge to the single pass", [] {  // test_analysis.cpp:197-240
+        rng64 rng(0x5eed);
+        const auto corpus = random_corpus(rng, 120, 9, 100);
+        const std::vector<int> orders{2, 3};
+        const std::vector<std::uint64_t> moduli{37, 240, 4000};
+        corpus_analyzer whole(120, orders, moduli);
+        whole.add_corpus(corpus);
+        corpus_analyzer a(120, orders, moduli), b(120, orders, moduli), c(120, orders, moduli);
+        for (std::size_t i = 0; i < corpus.size(); ++i) (i % 3 == 0 ? a : i % 3 == 1 ? b : c).add_sequence(corpus[i]);
+        c.merge(a);
+        c.merge(b);
+        const auto sw = whole.stats(), sc = c.stats();
+        CHECK(sw.sequences_seen == sc.sequences_seen && sw.ngrams_seen == sc.ngrams_seen);
+        CHECK(sw.distinct_ngrams == sc.distinct_ngrams && sw.distinct_buckets == sc.distinct_buckets);
+        rng64 r2(31337);
+        const auto c2 = random_corpus(r2, 40, 8, 120);
+        corpus_analyzer an(40, {2, 3, 4}, {17, 1000, 70000});
+        an.add_corpus(c2);
+        const auto s = an.stats();
+        for (const auto& [order, distinct] : s.distinct_ngrams) {
+            CHECK(distinct <= s.ngrams_seen.at(order));
+            for (const auto& [key, nb] : s.distinct_buckets)
+                if (key.first == order) CHECK(nb <= distinct && nb <= key.second);
+        }
+    });
+    test_case("analysis: error paths and CSV", [] {  // test_analysis.cpp:241-262
+        std::vector<token_sequence> empty;
+        CHECK_THROWS_AS(compute_hit_rate(empty, {2, 10, 5}), std::invalid_argument);
+        std::vector<token_sequence> empty_seqs{{}, {}};
+        CHECK_THROWS_AS(compute_hit_rate(empty_seqs, {2, 10, 5}), std::invalid_argument);
+        std::vector<token_sequence> oob{{3, 11}};
+        CHECK_THROWS_AS(count_collisions(oob, {2, 10, 5}), std::out_of_range);
+        CHECK_THROWS_AS(corpus_analyzer(1 << 17, {8}, {100}), std::invalid_argument);
+        std::vector<collision_report> reports(2);
+        reports[0] = {2, 2000, 0.5, 123, "c", 4096};
+        reports[1] = {3, 2500, 0.125, 0, "c", 4096};
+        std::ostringstream ss;
+        write_reports_csv(ss, reports);
+        CHECK(ss.str() == "order,modulus,hit_rate,collision_count,tokens_processed\n2,2000,0.5,123,4096\n"
+                          "3,2500,0.125,0,4096\n");
     });
     std::printf("%d checks, %d failures\n", g_checks, g_fail);
     return g_fail == 0 ? 0 : 1;

@@ -205,6 +205,7 @@ def main():
     R.ref_bank_destroy(hb)
     backward_goldens()
     plne_goldens()
+    analysis_goldens()
 
 
 def backward_goldens():
@@ -319,10 +320,44 @@ def plne_goldens():
         R.ref_bank_destroy(hb)
 
 
+def analysis_goldens():
+    # 11. corpus_analyzer (analysis.cpp:44-176) on the reference itself: the worked examples of
+    #     test_analysis.cpp, its Zipf-Markov corpora, random corpora, a bad token (partial
+    #     counts), moduli above 2^32 and near 2^64, order-100 windows over V0 = 2 (128-bit keys).
+    r = np.random.default_rng(2026)
+    cases = [
+        ("worked20", 10, [2], [20, 23], [[1, 5], [3, 5], [5, 5]]),
+        ("single", 10, [2], [100], [[5]]),
+        ("allpairs", 7, [2], [49, 30], [[a, b] for a in range(7) for b in range(7)]),
+        ("zipf1000", 1000, [2, 3, 4], [4999, 2000, 2500, 30000, 30500],
+         O.ref_zipf_markov(1000, 16, 4096, 99, 1.1, 0.85)),
+        ("random", 120, [2, 3], [37, 240, 4000], [r.integers(0, 120, size=int(r.integers(1, 101))) for _ in range(9)]),
+        ("badtoken", 10, [2, 3], [5, 7], [[1, 2, 3], [3, 11, 4], [5]]),
+        ("bigmod", 128000, [2, 3], [(1 << 40) + 15, (1 << 33) + 1, 10944000, 1],
+         O.ref_zipf_markov(128000, 8, 2048, 20260809)),
+        ("wide_v0", 4000000000, [2, 3], [1 << 32, (1 << 32) + 1, (1 << 64) - 59, 3],
+         [r.integers(3999990000, 4000000000, size=400) for _ in range(3)]),
+        ("order100", 2, [2, 64, 100], [97, 1 << 35], [r.integers(0, 2, size=300) for _ in range(4)]),
+        ("empty_seqs", 50, [2], [40], [[], [3, 4], [], [4, 3, 4]]),
+    ]
+    for name, v0, orders, moduli, seqs in cases:
+        seqs = [np.asarray(q, np.uint32) for q in seqs]
+        rc, st = O.ref_corpus_analyze(v0, orders, moduli, seqs)
+        toks, off = O._flat(seqs)
+        save(f"analysis_{name}.npz", v0=np.uint64(v0), orders=np.array(orders, np.int32),
+             moduli=np.array(moduli, np.uint64), tokens=toks[:off[-1]], seq_offsets=off, status=rc,
+             meta=np.array([st["sequences_seen"], st["tokens_seen"]], np.uint64),
+             seen=np.array([st["ngrams_seen"][o] for o in orders], np.uint64),
+             distinct=np.array([st["distinct_ngrams"][o] for o in orders], np.uint64),
+             buckets=np.array([st["distinct_buckets"][(o, m)] for o in orders for m in moduli], np.uint64))
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["backward"]:  # regenerate only section 9
         backward_goldens()
     elif sys.argv[1:] == ["plne"]:  # regenerate only section 10
         plne_goldens()
+    elif sys.argv[1:] == ["analysis"]:  # regenerate only section 11
+        analysis_goldens()
     else:
         main()

@@ -110,3 +110,24 @@ def assert_grads_close(got, ref, ln, rel_l2=GRAD_REL_L2, max_rtol=GRAD_MAX_RTOL)
         assert err.max() <= max_rtol * scale, f"{name}: max err {err.max() / scale:.3e} of max|ref|"
         rel = np.linalg.norm(a - b) / (np.linalg.norm(b) + 1e-30)
         assert rel <= rel_l2, f"{name}: relL2 {rel:.3e}"
+
+
+ANALYSIS = ["worked20", "single", "allpairs", "zipf1000", "random", "badtoken", "bigmod", "wide_v0", "order100",
+            "empty_seqs"]
+
+
+def analysis_case(name):
+    """(v0, orders, moduli, sequences, expected (status, meta, seen, distinct, buckets)) of a
+    tests/golden/analysis_*.npz made by the reference corpus_analyzer."""
+    g = gold(f"analysis_{name}.npz")
+    off = g["seq_offsets"]
+    seqs = [g["tokens"][off[i]:off[i + 1]] for i in range(len(off) - 1)]
+    return (int(g["v0"]), [int(o) for o in g["orders"]], [int(m) for m in g["moduli"]], seqs,
+            (int(g["status"]), g["meta"], g["seen"], g["distinct"], g["buckets"]))
+
+
+def stats_arrays(st, orders, moduli):
+    return (np.array([st["sequences_seen"], st["tokens_seen"]], np.uint64),
+            np.array([st["ngrams_seen"][o] for o in orders], np.uint64),
+            np.array([st["distinct_ngrams"][o] for o in orders], np.uint64),
+            np.array([st["distinct_buckets"][(o, m)] for o in orders for m in moduli], np.uint64))

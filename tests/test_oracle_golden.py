@@ -274,3 +274,30 @@ def test_plne_restatement_matches_reference(name):  # ple.hpp:76-196 in double
     ref = helpers.golden_grads(g, O.zero_grads(cfg))
     for (n, a), (_, b) in zip(helpers.grad_items(acc, False), helpers.grad_items(ref, False)):
         assert close(a, b), n
+
+
+@pytest.mark.parametrize("name", helpers.ANALYSIS)
+def test_analysis_restatement_matches_reference(name):  # analysis.cpp:44-176
+    v0, orders, moduli, seqs, (status, meta, seen, distinct, buckets) = helpers.analysis_case(name)
+    rc, st = O.corpus_analyze(v0, orders, moduli, seqs)
+    assert rc == status
+    got = helpers.stats_arrays(st, orders, moduli)
+    for a, b in zip(got, (meta, seen, distinct, buckets)):
+        np.testing.assert_array_equal(a, b)
+
+
+def test_analysis_reference_worked_examples():  # test_analysis.cpp:50-113
+    def hit(corpus, order, v0, m):
+        _, st = O.corpus_analyze(v0, [order], [m], corpus)
+        return st["distinct_buckets"][(order, m)] / m
+
+    def coll(corpus, order, v0, m):
+        _, st = O.corpus_analyze(v0, [order], [m], corpus)
+        return st["distinct_ngrams"][order] - st["distinct_buckets"][(order, m)]
+
+    assert hit([[5]], 2, 10, 100) == pytest.approx(0.01)
+    pairs = [[a, b] for a in range(7) for b in range(7)]
+    assert hit(pairs, 2, 7, 49) == pytest.approx(1.0) and hit(pairs, 2, 7, 30) == pytest.approx(1.0)
+    assert coll([[1, 5], [3, 5], [5, 5]], 2, 10, 20) == 2 and coll([[1, 5], [3, 5], [5, 5]], 2, 10, 23) == 0
+    assert coll([list(range(1, 10))], 2, 10, 1000000) == 0
+    assert O.corpus_analyze(1 << 17, [8], [100], [[1]])[0] == -1  # V0^order beyond 128 bits
