@@ -668,6 +668,63 @@ def run_decode_sharded(args):
     dist.destroy_process_group()
 
 
+def run_analysis(args):
+    """Corpus collision analysis (corpus_analyzer, analysis.cpp:93-121):
+    the collision table of config C's twelve sub-table moduli, orders 2..4, V0 = 128000.  Each
+    step streams a fresh batch of 16 x 65536 uniform tokens (device-resident; uniform = the most
+    distinct windows, the sets' worst case) into one growing analyzer; the reference arm is the
+    reference corpus_analyzer (single-threaded, as shipped) on a bounded sample."""
+    import torch
+    from paper_2601_21204_b200 import abi
+    from paper_2601_21204_b200 import ngram as G
+    dev = torch.device("cuda", 0)
+    v0, orders = 128000, [2, 3, 4]
+    moduli = [(2 * (74 + b) + 1) * 64000 for b in range(12)]
+    nseq, L = 16, 65536
+    T = nseq * L
+    gen = torch.Generator(device=dev).manual_seed(42)
+    batches = [torch.randint(0, v0, (T,), dtype=torch.int32, device=dev, generator=gen)
+               for _ in range(args.warmup + args.steps)]
+    off = torch.arange(0, T + 1, L, dtype=torch.int64, device=dev)
+    an = G.CorpusAnalyzer(v0, orders, moduli)
+    an.reserve(T * (args.warmup + args.steps))  # sized up front (unordered_set::reserve): no rehash timed
+    for i in range(args.warmup):
+        an.add(batches[i], off)
+    torch.cuda.synchronize()
+    l0 = abi.lib().ngram_kernel_launches()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.steps):
+        ev[i][0].record()
+        an.add(batches[args.warmup + i], off)
+        ev[i][1].record()
+    torch.cuda.synchronize()
+    launches = abi.lib().ngram_kernel_launches() - l0
+    an.sync_errors()
+    ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    st = an.stats()
+    line = {"metric": "corpus_analysis_tokens_per_sec", "value": T / (ms * 1e-3), "unit": "tokens/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "dtype": "u32/u128", "data": "synthetic (uniform tokens, fresh batch per step)",
+            "config": {"workload": "collision_table_longcat_moduli", "V0": v0, "orders": orders, "moduli": moduli,
+                       "tokens_per_step": T, "sequences": nseq},
+            "inserts_per_token": len(orders) * (1 + len(moduli)),
+            "final_stats": {"tokens_seen": st["tokens_seen"], "distinct_ngrams": st["distinct_ngrams"]},
+            "gpu_launches": int(launches)}
+    if not args.no_cpu and os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libngram_ref.so")):
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O
+        rng = np.random.default_rng(1)
+        sample = [rng.integers(0, v0, size=16384).astype(np.uint32) for _ in range(16)]
+        t0 = time.perf_counter()
+        rc, _ = O.ref_corpus_analyze(v0, orders, moduli, sample)
+        dt = time.perf_counter() - t0
+        assert rc == 0
+        line["cpu_baseline"] = {"value": 16 * 16384 / dt, "unit": "tokens/s", "cores": 1, "kind": "reference",
+                                "sample": "16 x 16384 uniform tokens through the reference corpus_analyzer "
+                                          "(add_sequence per sequence, single-threaded as shipped)"}
+    print(json.dumps(line))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -689,6 +746,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload == "analysis":
+        run_analysis(args)
     elif args.workload in ("D", "E") and int(os.environ.get("WORLD_SIZE", "1")) > 1:
         run_decode_sharded(args)
     elif args.workload in ("D", "E"):

@@ -348,6 +348,9 @@ int ngram_analyzer_add(ngram_analyzer* a, const uint32_t* tokens, const int64_t*
 int ngram_analyzer_add_host(ngram_analyzer* a, const uint32_t* tokens, const int64_t* seq_offsets, int64_t nseq);
 /* Set-union merge (analysis.cpp:125-141): same base / orders / moduli, same device. */
 int ngram_analyzer_merge(ngram_analyzer* dst, ngram_analyzer* src, void* stream);
+/* Pre-size every set for `windows` more positions (no rehash inside the next adds;
+ * the reference's unordered_set::reserve).  Synchronous. */
+int ngram_analyzer_reserve(ngram_analyzer* a, uint64_t windows);
 int ngram_analyzer_sync_errors(ngram_analyzer* a);
 /* Synchronous.  ngrams_seen / distinct_ngrams: [n_orders]; distinct_buckets: [n_orders][n_moduli]
  * (order-major, the reference's layout).  Any pointer may be NULL. */

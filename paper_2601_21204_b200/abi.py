@@ -42,7 +42,7 @@ SYMBOLS = [
     "ngram_grad_create_ex", "ngram_grad_sparse_rows", "ngram_grad_sparse_read", "ngram_amplify_host",
     "ngram_amplify_backward_host", "ngram_decode_ring", "ngram_decode_copy_ring",
     "ngram_analyzer_create", "ngram_analyzer_destroy", "ngram_analyzer_add", "ngram_analyzer_add_host",
-    "ngram_analyzer_merge", "ngram_analyzer_sync_errors", "ngram_analyzer_stats",
+    "ngram_analyzer_merge", "ngram_analyzer_sync_errors", "ngram_analyzer_stats", "ngram_analyzer_reserve",
 ]
 
 
@@ -175,6 +175,7 @@ def lib() -> C.CDLL:
         "ngram_analyzer_add_host": ([vp, vp, vp, i64], i32),
         "ngram_analyzer_merge": ([vp, vp, vp], i32),
         "ngram_analyzer_sync_errors": ([vp], i32),
+        "ngram_analyzer_reserve": ([vp, u64], i32),
         "ngram_analyzer_stats": ([vp, vp, vp, vp, vp, vp], i32),
     }
     for name, (args, res) in sig.items():

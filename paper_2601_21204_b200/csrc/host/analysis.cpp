@@ -348,6 +348,16 @@ int ngram_analyzer_merge(ngram_analyzer* dst, ngram_analyzer* src, void* stream)
     NGRAM_API_END
 }
 
+int ngram_analyzer_reserve(ngram_analyzer* a, uint64_t windows) {
+    NGRAM_API_BEGIN
+    if (!a) throw Error(NGRAM_EINVAL, "ngram_analyzer_reserve: null analyzer");
+    std::lock_guard<std::mutex> lk(a->mu);
+    DeviceGuard g(a->device);
+    // like unordered_set::reserve: grow now so the next `windows` positions add no rehash
+    a->reserve(windows, nullptr);
+    NGRAM_API_END
+}
+
 int ngram_analyzer_sync_errors(ngram_analyzer* a) {
     NGRAM_API_BEGIN
     if (!a) throw Error(NGRAM_EINVAL, "ngram_analyzer_sync_errors: null analyzer");

@@ -95,9 +95,20 @@ __device__ __forceinline__ uint64_t poly_mod(unsigned __int128 poly, uint64_t m,
 // Thread per position t < limit (positions >= limit belong to or follow the first sequence
 // holding a bad token, analysis.cpp:101-106).  The loop bound is warp-uniform so the
 // per-warp ballots see every lane.
+// New-entry counters: per block in shared memory (one global atomicAdd per counter per block
+// at the end) when they fit, else straight to global.  All counters of an analyzer share a
+// few L2 lines, so per-warp global atomics would serialise on one L2 slice.
 __global__ void __launch_bounds__(256) an_insert_kernel(AnDev a, const uint32_t* __restrict__ tokens,
                                                         const int64_t* __restrict__ off, int64_t nseq,
-                                                        const unsigned long long* __restrict__ limit_p) {
+                                                        const unsigned long long* __restrict__ limit_p,
+                                                        int smem_counts) {
+    extern __shared__ unsigned long long s_cnt[];
+    const int ncnt = a.n_orders * (1 + a.n_moduli);
+    if (smem_counts) {
+        for (int i = threadIdx.x; i < ncnt; i += blockDim.x) s_cnt[i] = 0;
+        __syncthreads();
+    }
+    unsigned long long* cnt = smem_counts ? s_cnt : a.counts;
     const int64_t limit = (int64_t)*limit_p;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < limit; base += stride) {
@@ -118,14 +129,14 @@ __global__ void __launch_bounds__(256) an_insert_kernel(AnDev a, const uint32_t*
             }
             const uint64_t plo = (uint64_t)poly, phi = (uint64_t)(poly >> 64);
             const bool nw = live && set_insert(a.ngram_sets[oi], plo, phi, a.err);
-            warp_count(nw, a.counts + oi);
+            warp_count(nw, cnt + oi);
             for (int mi = 0; mi < a.n_moduli; ++mi) {
                 const int k = oi * a.n_moduli + mi;
                 bool bn = false;
                 if (live) {
                     const uint64_t bucket = poly_mod(poly, a.moduli[mi], a.barrett[mi], a.c64[mi]);
                     const AnBucket& bk = a.buckets[k];
-                    if (bk.bits) {
+                    if (bk.bits) {  // a plain read first: most bits are set after warm-up
                         unsigned long long* w = bk.bits + (bucket >> 6);
                         const unsigned long long bit = 1ull << (bucket & 63);
                         if (!(*reinterpret_cast<volatile unsigned long long*>(w) & bit))
@@ -134,9 +145,14 @@ __global__ void __launch_bounds__(256) an_insert_kernel(AnDev a, const uint32_t*
                         bn = set_insert(bk.set, bucket, 0, a.err);
                     }
                 }
-                warp_count(bn, a.counts + a.n_orders + k);
+                warp_count(bn, cnt + a.n_orders + k);
             }
         }
+    }
+    if (smem_counts) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < ncnt; i += blockDim.x)
+            if (s_cnt[i]) atomicAdd(a.counts + i, s_cnt[i]);
     }
 }
 
@@ -236,7 +252,9 @@ void launch_an_add(const AnDev& a, const uint32_t* tokens, const int64_t* off, i
     an_account_kernel<<<1, 1, 0, st>>>(tokens, off, nseq, first_bad, meta, a.n_orders, err_pos);
     count_launch();
     if (T > 0) {
-        an_insert_kernel<<<grid_for(T, num_sms), 256, 0, st>>>(a, tokens, off, nseq, first_bad);
+        const int ncnt = a.n_orders * (1 + a.n_moduli);
+        const int smem = ncnt <= 6144 ? ncnt * 8 : 0;
+        an_insert_kernel<<<grid_for(T, num_sms), 256, smem, st>>>(a, tokens, off, nseq, first_bad, smem != 0);
         count_launch();
     }
 }

@@ -586,6 +586,10 @@ class CorpusAnalyzer:
     def sync_errors(self) -> None:
         check(abi.lib().ngram_analyzer_sync_errors(self.handle))
 
+    def reserve(self, windows: int) -> None:
+        """Pre-size the sets for `windows` more positions (no rehash inside the next adds)."""
+        check(abi.lib().ngram_analyzer_reserve(self.handle, int(windows)))
+
     def stats(self) -> dict:
         no, nm = len(self.orders), len(self.moduli)
         sq, tk = C.c_uint64(), C.c_uint64()
