@@ -126,3 +126,16 @@ def test_longcat_moduli_on_zipf_stream(cuda):
     rc, ref = O.corpus_analyze(128000, [2, 3, 4], sv, seqs)
     _, an = run(128000, [2, 3, 4], sv, seqs, mode="device")
     assert rc == 0 and an.stats() == ref
+
+
+def test_reserve_then_add_equals_growth(cuda):
+    rng = np.random.default_rng(9)
+    seqs = [rng.integers(0, 50000, size=30000).astype(np.uint32) for _ in range(4)]
+    a, b = G.CorpusAnalyzer(50000, [2, 3], [40009, (1 << 34) + 1]), G.CorpusAnalyzer(50000, [2, 3], [40009, (1 << 34) + 1])
+    b.reserve(120000)
+    for q in seqs:
+        a.add_sequence(q)
+        b.add_sequence(q)
+    assert a.stats() == b.stats()
+    rc, ref = O.corpus_analyze(50000, [2, 3], [40009, (1 << 34) + 1], seqs)
+    assert rc == 0 and a.stats() == ref
