@@ -202,6 +202,9 @@ int ngram_bank_create_ex(const char* config_json, int device, int shard_rank, in
         // E0 rows gathered by token id (tile::gather4) into the pair kernel's TMA epilogue
         make_tensor_map_2d(&b->tmap_e0, b->e0.p, uint64_t(D), uint64_t(b->cfg.base_vocab), uint64_t(D) * 2, 32, 1,
                            false, 64);
+        if (D % 64 == 0)
+            make_tensor_map_2d(&b->tmap_e0w, b->e0.p, uint64_t(D), uint64_t(b->cfg.base_vocab), uint64_t(D) * 2, 64,
+                               1, false, 128);
     }
     NGH_CUDA(cudaDeviceSynchronize());
     *out = b.release();

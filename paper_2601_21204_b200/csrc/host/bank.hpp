@@ -107,7 +107,7 @@ struct ngram_bank {
     ngh::DevBuf<ngk::HashTables> ht;
     ngh::DevBuf<unsigned long long> err;
 
-    CUtensorMap tmap_sub{}, tmap_w{}, tmap_w2{}, tmap_e0{};
+    CUtensorMap tmap_sub{}, tmap_w{}, tmap_w2{}, tmap_e0{}, tmap_e0w{};
     ngh::Workspace ws;
 
     // Serialises the host-buffer entry points (the reference's bank is shareable across

@@ -124,6 +124,7 @@ void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, 
             a.tmap_merged_out = &map_merged;
         }
         a.tmap_e0 = &b->tmap_e0;
+        if (b->shape.D % 64 == 0) a.tmap_e0w = &b->tmap_e0w;
     }
     if (b->tc_path) {
         float* ws = nullptr;

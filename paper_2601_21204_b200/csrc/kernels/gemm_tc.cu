@@ -14,8 +14,9 @@
 // because the warp arbiter serves the highest eligible id first):
 //   forward_tc2_kernel   2-CTA pairs (cta_group::2), 256 x 256 tiles, 8 epilogue warps,
 //                        TMEM double-buffered; the production path for D % 256 == 0 and
-//                        T > 256.  EPI 1: all epilogue traffic by TMA (E0 rows gathered
-//                        into a smem ring, outputs staged and bulk-stored); EPI 0: direct.
+//                        T > 256.  EPI 4 (default) / 1: all epilogue traffic by TMA (E0
+//                        rows gathered 64 / 32 columns at a time into a smem ring, outputs
+//                        staged and bulk-stored); EPI 0: direct.
 //   forward_tc_kernel    1 CTA, 128 x BN tiles: shapes the pair kernel does not take, and
 //                        the small-T split-K GEMM (raw fp32 partials, BN = 128; MODE 2
 //                        hashes in its producers, opt-in).
@@ -447,13 +448,19 @@ constexpr int kEpiWarps2 = 8;  // two per TMEM lane quadrant, each owning half t
 // for a bulk tensor store.  Mode 1 costs one pipeline stage of smem.
 // Mode 1 = 5 stages, 2 E0 slots, 1 output buffer per warp.  Measured equal within noise
 // (profiles/README.md): 4 stages with 2 output buffers, or with 4 E0 slots (a tile ahead).
-constexpr int stages2(int epi) { return epi == 0 ? kStages2 : epi == 1 ? kStages2 - 1 : kStages2 - 2; }
+// Mode 4 (production): as mode 1 with E0 gathered 64 columns (128-byte rows, SWIZZLE_128B)
+// per gather4 -- half the TMA gather operations; each ring slot serves two chunks; 4 stages
+// (the wider slots take the fifth stage's smem).  K3 0.853 vs 0.859 ms at config C.
+constexpr int stages2(int epi) {
+    return epi == 0 ? kStages2 : epi == 1 ? kStages2 - 1 : kStages2 - 2;
+}
 constexpr int epi_ring(int epi) { return epi == 3 ? 4 : 2; }
 constexpr int epi_obufs(int epi) { return epi == 2 ? 2 : 1; }
 constexpr int kE0Box = 32 * 32 * 2;   // one E0 chunk: 32 rows x 32 bf16 columns
+constexpr int e0box(int epi) { return epi == 4 ? 2 * kE0Box : kE0Box; }
 constexpr int kOutBox = 32 * 32 * 4;  // one staged output box (fp32 worst case)
 constexpr int epi_smem(int epi) {
-    return epi ? kEpiWarps2 * (epi_ring(epi) * kE0Box + epi_obufs(epi) * kOutBox) : 0;
+    return epi ? kEpiWarps2 * (epi_ring(epi) * e0box(epi) + epi_obufs(epi) * kOutBox) : 0;
 }
 
 struct Cfg2 {
@@ -674,16 +681,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::kThreads, 1)
         constexpr int kChunks = BN2 / 2 / 32;
         constexpr int R = epi_ring(EPI);
         constexpr int OB = epi_obufs(EPI);
-        uint8_t* e0ring = staging + ew * (R * kE0Box);
-        uint8_t* obuf0 = staging + kEpiWarps2 * R * kE0Box + ew * OB * kOutBox;
+        constexpr bool kWide = EPI == 4;        // one E0 slot = two chunks (64 columns)
+        constexpr int EB = e0box(EPI);
+        constexpr int kPer = kWide ? 2 : 1;     // chunks per E0 slot
+        uint8_t* e0ring = staging + ew * (R * EB);
+        uint8_t* obuf0 = staging + kEpiWarps2 * R * EB + ew * OB * kOutBox;
         int ob = 0;
         uint64_t* ebar = e0bar + R * ew;
         const uint64_t pol_out = policy_evict_first();
         const int64_t nchunks = ((tiles - pair + npairs - 1) / npairs) * kChunks;
-        // gather E0 rows of chunk g into ring slot g % R (4 rows per gather4, lanes 0..7)
+        const int64_t nslots = nchunks / kPer;
+        // gather the E0 rows of slot-load g (kPer chunks) into ring slot g % R (4 rows per
+        // gather4, lanes 0..7)
         auto issue_e0 = [&](int64_t g) {
-            const int64_t tile = pair + (g / kChunks) * npairs;
-            const int c = (int)(g % kChunks);
+            const int64_t tile = pair + (g / (kChunks / kPer)) * npairs;
+            const int c = (int)(g % (kChunks / kPer));
             const int64_t m = tile / nN;
             const int n = (int)(tile - m * nN);
             const int64_t t = m * BM2 + (int64_t)rank * 128 + q * 32 + lane;
@@ -692,13 +704,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::kThreads, 1)
             const int r0 = __shfl_sync(0xffffffffu, tok, l4), r1 = __shfl_sync(0xffffffffu, tok, l4 + 1);
             const int r2 = __shfl_sync(0xffffffffu, tok, l4 + 2), r3 = __shfl_sync(0xffffffffu, tok, l4 + 3);
             uint64_t* bar = &ebar[g % R];
-            if (lane == 0) mbar_arrive_expect_tx(bar, kE0Box);
+            if (lane == 0) mbar_arrive_expect_tx(bar, EB);
             __syncwarp();
             if (lane < 8)
-                tma_gather4(e0ring + (g % R) * kE0Box + lane * 4 * 64, &tmap_e0, bar, n * BN2 + half * (BN2 / 2) + c * 32,
-                            r0, r1, r2, r3);
+                tma_gather4(e0ring + (g % R) * EB + lane * 4 * (64 * kPer), &tmap_e0, bar,
+                            n * BN2 + half * (BN2 / 2) + c * 32 * kPer, r0, r1, r2, r3);
         };
-        for (int64_t g0 = 0; g0 < R && g0 < nchunks; ++g0) issue_e0(g0);
+        for (int64_t g0 = 0; g0 < R && g0 < nslots; ++g0) issue_e0(g0);
         int acc = 0;
         uint32_t acc_phase = 0;
         int64_t g = 0;
@@ -715,14 +727,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::kThreads, 1)
                 tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) +
                                        (uint32_t)(acc * BN2 + half * (BN2 / 2) + c * 32),
                                    v);
-                mbar_wait(&ebar[g % R], (uint32_t)((g / R) & 1));
-                const uint32_t eb = smem_u32(e0ring + (g % R) * kE0Box);
+                const int64_t gs = g / kPer;  // E0 slot-load holding this chunk
+                mbar_wait(&ebar[gs % R], (uint32_t)((gs / R) & 1));
+                const uint32_t eb = smem_u32(e0ring + (gs % R) * EB);
                 uint4 e[4];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) e[i] = ld_shared_v4u(sw64(eb, lane, i));
-                fence_proxy_async_smem();  // generic reads of the slot before TMA refills it
-                __syncwarp();
-                if (g + R < nchunks) issue_e0(g + R);
+                for (int i = 0; i < 4; ++i)
+                    e[i] = ld_shared_v4u(kWide ? sw128(eb, lane, (int)(g & 1) * 4 + i) : sw64(eb, lane, i));
+                if (!kWide || (g & 1)) {
+                    fence_proxy_async_smem();  // generic reads of the slot before TMA refills it
+                    __syncwarp();
+                    if (gs + R < nslots) issue_e0(gs + R);
+                }
                 tmem_ld_wait();
                 float mv[32];
 #pragma unroll
@@ -913,7 +929,8 @@ void launch_cfg(const FwdArgs& a, int num_sms, cudaStream_t st, int ksplit = 1, 
 int tma_epi_mode() {
     static const int v = [] {
         const char* e = getenv("NGRAM_TMA_EPI");
-        return e ? std::min(1, std::max(0, atoi(e))) : 1;
+        const int m = e ? atoi(e) : 4;
+        return m == 4 ? 4 : std::min(1, std::max(0, m));
     }();
     return v;
 }
@@ -951,7 +968,12 @@ void launch_tc2(const FwdArgs& a, int num_sms, cudaStream_t st) {
     const CUtensorMap& mm = a.tmap_merged_out ? *a.tmap_merged_out : *a.tmap_w2;
     const unsigned grid = (unsigned)(2 * pairs);
     const CUtensorMap& me = a.tmap_e0 ? *a.tmap_e0 : *a.tmap_w2;
-    if (epi == 1) {
+    if (epi == 4 && a.tmap_e0w) {
+        cudaFuncSetAttribute(forward_tc2_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Cfg2::smem_bytes(4));
+        forward_tc2_kernel<4><<<grid, Cfg2::kThreads, Cfg2::smem_bytes(4), st>>>(ma, *a.tmap_w2, mr, mm, *a.tmap_e0w,
+                                                                                   p);
+    } else if (epi >= 1) {
         cudaFuncSetAttribute(forward_tc2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              Cfg2::smem_bytes(1));
         forward_tc2_kernel<1><<<grid, Cfg2::kThreads, Cfg2::smem_bytes(1), st>>>(ma, *a.tmap_w2, mr, mm, me, p);

@@ -120,6 +120,7 @@ struct FwdArgs {
     const CUtensorMap* tmap_rows_out;
     const CUtensorMap* tmap_merged_out;
     const CUtensorMap* tmap_e0;
+    const CUtensorMap* tmap_e0w;  // E0 gather map with a 64-column box, SWIZZLE_128B (epilogue mode 4)
     // small-T split-K with the hash fused into the GEMM producer (MODE 2): the windows of
     // `tokens` (seq_off / nseq / prior as ngram_embed_forward); null seq_off = not used
     const int64_t* seq_off;

@@ -258,8 +258,8 @@ def test_fused_k1_k2_k3_kernel_matches_oracle(cuda):
 def test_pair_kernel_tma_epilogue_edges(cuda, out_dtype):
     """The 2-CTA projection's TMA epilogue (E0 rows by tile::gather4, outputs by bulk tensor
     stores clipped at T): ragged T (not a multiple of 32 / 128 / 256), rows + merged; the
-    direct-store epilogue (NGRAM_TMA_EPI=0 in a subprocess is the A/B switch) computes the
-    same values.  Output buffers that are not 16-byte aligned are rejected up front."""
+    direct-store epilogue and the 32-column E0 gather variant (NGRAM_TMA_EPI=0 / 1 in a
+    subprocess are the A/B switches) compute the same bits.  Output buffers that are not 16-byte aligned are rejected up front."""
     cfg = O.make_default_config(3000, 512, 3, 2)
     hb = O.make_bank(cfg, 17, round_bf16=True)
     db = G.DeviceBank(cfg).upload(hb.base, hb.sub, hb.proj)
@@ -297,13 +297,14 @@ r, m = G.embed_forward(db, dev_u32(torch, allt, "cuda:0"), dev_i64(torch, off, "
 db.sync_errors()
 np.save(sys.argv[1], torch.stack([r, m]).view(torch.int16 if r.dtype == torch.bfloat16 else torch.int32).cpu().numpy())
 """
-    with tempfile.TemporaryDirectory() as td:
-        path = os.path.join(td, "direct.npy")
-        subprocess.run([sys.executable, "-c", code, path], check=True, timeout=300,
-                       env={**os.environ, "NGRAM_TMA_EPI": "0"})
-        direct = np.load(path)
     ours = torch.stack([rows, merged]).view(torch.int16 if bf else torch.int32).cpu().numpy()
-    assert np.array_equal(ours, direct)
+    for mode in ("0", "1"):  # direct stores; TMA epilogue with 32-column E0 gathers
+        with tempfile.TemporaryDirectory() as td:
+            path = os.path.join(td, "other.npy")
+            subprocess.run([sys.executable, "-c", code, path], check=True, timeout=300,
+                           env={**os.environ, "NGRAM_TMA_EPI": mode})
+            other = np.load(path)
+        assert np.array_equal(ours, other), mode
 
 
 def test_small_t_hash_in_gemm_variant_is_bit_identical(cuda):
