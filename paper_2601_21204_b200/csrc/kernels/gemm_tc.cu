@@ -446,16 +446,14 @@ constexpr int kEpiWarps2 = 8;  // two per TMEM lane quadrant, each owning half t
 // tile::gather4 into a 2-slot SWIZZLE_64B ring (issued two chunks ahead, across tile
 // boundaries) and stages every output box in SWIZZLE_128B (fp32) / SWIZZLE_64B (bf16) smem
 // for a bulk tensor store.  Mode 1 costs one pipeline stage of smem.
-// Mode 1 = 5 stages, 2 E0 slots, 1 output buffer per warp.  Measured equal within noise
-// (profiles/README.md): 4 stages with 2 output buffers, or with 4 E0 slots (a tile ahead).
+// Mode 1 = 5 stages, 2 E0 slots, 1 output buffer per warp.  Measured equal within noise and
+// removed (profiles/README.md): 4 stages with 2 output buffers, or with 4 E0 slots.
 // Mode 4 (production): as mode 1 with E0 gathered 64 columns (128-byte rows, SWIZZLE_128B)
 // per gather4 -- half the TMA gather operations; each ring slot serves two chunks; 4 stages
 // (the wider slots take the fifth stage's smem).  K3 0.853 vs 0.859 ms at config C.
-constexpr int stages2(int epi) {
-    return epi == 0 ? kStages2 : epi == 1 ? kStages2 - 1 : kStages2 - 2;
-}
-constexpr int epi_ring(int epi) { return epi == 3 ? 4 : 2; }
-constexpr int epi_obufs(int epi) { return epi == 2 ? 2 : 1; }
+constexpr int stages2(int epi) { return epi == 0 ? kStages2 : epi == 1 ? kStages2 - 1 : kStages2 - 2; }
+constexpr int epi_ring(int) { return 2; }
+constexpr int epi_obufs(int) { return 1; }
 constexpr int kE0Box = 32 * 32 * 2;   // one E0 chunk: 32 rows x 32 bf16 columns
 constexpr int e0box(int epi) { return epi == 4 ? 2 * kE0Box : kE0Box; }
 constexpr int kOutBox = 32 * 32 * 4;  // one staged output box (fp32 worst case)
