@@ -155,3 +155,29 @@ def test_bench_reference_arm_json_contract():
     assert line["impl"] == "reference" and line["warmup"] >= 3
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
     assert line["cpu_baseline"]["kind"] == "reference" and line["config"]["workload"]
+
+
+def test_analyzer_argument_checks_and_no_gpu():
+    """corpus_analyzer's constructor checks (analysis.cpp:47-85) run on the host before any
+    device work, with the reference's messages; a valid analyzer needs a GPU (fails loudly)."""
+    import torch
+    L = abi.lib()
+
+    def create(v0, orders, moduli):
+        o = (C.c_int * max(len(orders), 1))(*orders)
+        m = (C.c_uint64 * max(len(moduli), 1))(*moduli)
+        h = C.c_void_p()
+        rc = L.ngram_analyzer_create(0, v0, o, len(orders), m, len(moduli), C.byref(h))
+        return rc, h, L.ngram_last_error().decode()
+
+    for args, msg in [((1, [2], [5]), "base vocabulary must be >= 2"),
+                      ((10, [], [5]), "need at least one order and one modulus"),
+                      ((10, [2], []), "need at least one order and one modulus"),
+                      ((10, [1], [5]), "orders must be >= 2"),
+                      ((10, [2], [0]), "moduli must be >= 1"),
+                      ((1 << 17, [8], [100]), "V0^order exceeds 128 bits")]:
+        rc, h, err = create(*args)
+        assert rc == abi.NGRAM_EINVAL and not h.value and msg in err
+    if not torch.cuda.is_available():
+        rc, h, _ = create(10, [2], [5])
+        assert rc in (abi.NGRAM_ECUDA, abi.NGRAM_ENOMEM) and not h.value
