@@ -268,6 +268,10 @@ int ngram_grad_create(ngram_bank* bank, ngram_grad** out); /* zero-initialised *
  * accumulation) instead of pedantic fp32 -- ~10x faster at LongCat scale; gradients agree
  * with the reference to ~1e-3 relative (training precision), not the 1e-5 fp32 contract. */
 #define NGRAM_GRAD_TF32 2
+/* NGRAM_GRAD_PEDANTIC: the two backward GEMMs as pedantic fp32 (CUDA cores).  The default
+ * runs them as two-term TF32 on the tensor cores: X and W_cat are bf16 values (exact in TF32),
+ * U = U_hi + U_lo is split so both products are fp32-accurate (the default tolerance holds). */
+#define NGRAM_GRAD_PEDANTIC 4
 int ngram_grad_create_ex(ngram_bank* bank, int flags, ngram_grad** out);
 /* Row-sparse gradient view: rows = dev int32 [count] storage rows (the device layout of
  * ngram_grad_tensor(1)), vals = dev f32 [count][branch_dim]; count resets on ngram_grad_zero. */

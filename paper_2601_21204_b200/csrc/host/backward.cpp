@@ -26,7 +26,8 @@ using namespace ngh;
 struct ngram_grad {
     ngram_bank* bank = nullptr;
     DevBuf<float> e0, sub, w, gain, bias;  // gradients, device layout
-    DevBuf<float> U, X, dX, wf;            // workspaces
+    DevBuf<float> U, X, dX, wf, Ulo;       // workspaces (Ulo: TF32 remainder of U)
+    int gemm_mode = 0;                     // 0 two-term TF32 (default), 1 TF32, 2 pedantic fp32
     DevBuf<int32_t> grow;
     int64_t cap = 0;
     bool sparse = false;                 // NGRAM_GRAD_SPARSE_ROWS
@@ -88,7 +89,8 @@ int ngram_grad_create(ngram_bank* b, ngram_grad** out) { return ngram_grad_creat
 
 int ngram_grad_create_ex(ngram_bank* b, int flags, ngram_grad** out) {
     NGRAM_API_BEGIN
-    if (!b || !out || (flags & ~(NGRAM_GRAD_SPARSE_ROWS | NGRAM_GRAD_TF32)))
+    if (!b || !out || (flags & ~(NGRAM_GRAD_SPARSE_ROWS | NGRAM_GRAD_TF32 | NGRAM_GRAD_PEDANTIC)) ||
+        ((flags & NGRAM_GRAD_TF32) && (flags & NGRAM_GRAD_PEDANTIC)))
         throw Error(NGRAM_EINVAL, "ngram_grad_create: bad argument");
     if (b->hash_only) throw Error(NGRAM_EINVAL, "bank was created hash-only (NGRAM_BANK_HASH_ONLY)");
     if (b->shard_count != 1) throw Error(NGRAM_EINVAL, "ngram_grad_create: row-sharded banks are not supported");
@@ -105,8 +107,8 @@ int ngram_grad_create_ex(ngram_bank* b, int flags, ngram_grad** out) {
         g->bias.alloc(size_t(s.D));
     }
     check_blas(cublasCreate(&g->blas), "cublasCreate");
-    check_blas(cublasSetMathMode(g->blas, (flags & NGRAM_GRAD_TF32) ? CUBLAS_TF32_TENSOR_OP_MATH
-                                                                    : CUBLAS_PEDANTIC_MATH),  // default: true fp32
+    g->gemm_mode = (flags & NGRAM_GRAD_TF32) ? 1 : (flags & NGRAM_GRAD_PEDANTIC) ? 2 : 0;
+    check_blas(cublasSetMathMode(g->blas, g->gemm_mode == 2 ? CUBLAS_PEDANTIC_MATH : CUBLAS_TF32_TENSOR_OP_MATH),
                "cublasSetMathMode");
     zero_all(g.get(), nullptr);
     NGH_CUDA(cudaDeviceSynchronize());
@@ -153,6 +155,7 @@ int ngram_embed_backward(ngram_grad* g, const uint32_t* tokens, const int64_t* s
         if (s.variant == 1 && B > 0) {
             g->X.alloc(size_t(Tpad) * size_t(D));
             g->dX.alloc(size_t(Tpad) * size_t(D));
+            if (g->gemm_mode == 0) g->Ulo.alloc(size_t(Tpad) * size_t(D));
         }
         g->grow.alloc(size_t(std::max(B, 1)) * size_t(Tpad));
         g->cap = Tpad;
@@ -168,15 +171,22 @@ int ngram_embed_backward(ngram_grad* g, const uint32_t* tokens, const int64_t* s
         ngk::launch_bf16_to_f32(b->wcat.p, g->wf.p, int64_t(D) * D, st);
         check_blas(cublasSetStream(g->blas, st), "cublasSetStream");
         const float one = 1.0f, zero = 0.0f;
+        // Default: two-term TF32.  X (gathered bf16 rows) and W_cat (bf16) are exact in TF32, so
+        // splitting only U = U_hi + U_lo (U_hi TF32-exact, U_lo's TF32 rounding ~2^-21 |U|)
+        // makes both products fp32-accurate on the tensor cores with two GEMMs each.
+        const bool two = g->gemm_mode == 0;
+        if (two) ngk::launch_split_tf32(g->U.p, g->Ulo.p, int64_t(T) * D, st);
         // row-major M (r x c) is column-major M^T with ld = c.
         // g_W (D x D, row-major [i][k]) += U^T X  <=>  col-major g_W^T = X_cm * U_cm^T
-        check_blas(cublasSgemm(g->blas, CUBLAS_OP_N, CUBLAS_OP_T, D, D, int(T), &one, g->X.p, D, g->U.p, D, &one,
-                               g->w.p, D),
-                   "cublasSgemm(dW)");
+        for (int h = 0; h < (two ? 2 : 1); ++h)
+            check_blas(cublasSgemm(g->blas, CUBLAS_OP_N, CUBLAS_OP_T, D, D, int(T), &one, g->X.p, D,
+                                   h ? g->Ulo.p : g->U.p, D, &one, g->w.p, D),
+                       "cublasSgemm(dW)");
         // dX (T x D) = U W_cat  <=>  col-major dX^T = W_cm * U_cm
-        check_blas(cublasSgemm(g->blas, CUBLAS_OP_N, CUBLAS_OP_N, D, int(T), D, &one, g->wf.p, D, g->U.p, D, &zero,
-                               g->dX.p, D),
-                   "cublasSgemm(dX)");
+        for (int h = 0; h < (two ? 2 : 1); ++h)
+            check_blas(cublasSgemm(g->blas, CUBLAS_OP_N, CUBLAS_OP_N, D, int(T), D, &one, g->wf.p, D,
+                                   h ? g->Ulo.p : g->U.p, D, h ? &one : &zero, g->dX.p, D),
+                       "cublasSgemm(dX)");
         if (g->sparse) {  // dX is [T][B][d]: exactly the appended values, rows transposed from grow
             sparse_reserve(g, T * B, d, st);
             NGH_CUDA(cudaMemcpyAsync(g->sp_vals.p + size_t(g->sp_count) * size_t(d), g->dX.p,

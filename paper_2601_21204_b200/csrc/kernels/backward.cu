@@ -173,6 +173,19 @@ __global__ void bf16_to_f32_kernel(const __nv_bfloat16* __restrict__ src, float*
         dst[i] = __bfloat162float(src[i]);
 }
 
+// u -> (hi, lo): hi = u rounded to the nearest TF32 value (exact in a TF32 GEMM), lo = u - hi
+// (exact in fp32).  hi is written over u.
+__global__ void split_tf32_kernel(float* __restrict__ u, float* __restrict__ lo, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float x = u[i];
+        uint32_t h;
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+        const float hf = __uint_as_float(h);
+        u[i] = hf;
+        lo[i] = x - hf;
+    }
+}
+
 int grid_for(int64_t n, int threads) {
     int64_t g = (n + threads - 1) / threads;
     if (g > 148 * 16) g = 148 * 16;
@@ -221,6 +234,12 @@ void launch_rows_to_coo(const Shape& s, const int32_t* grow, int64_t Tpad, int64
                         const unsigned long long* err, cudaStream_t st) {
     if (T <= 0 || s.B == 0) return;
     rows_to_coo_kernel<<<grid_for(T * s.B, 256), 256, 0, st>>>(grow, Tpad, T, s.B, rows, err);
+    count_launch();
+}
+
+void launch_split_tf32(float* u, float* lo, int64_t n, cudaStream_t st) {
+    if (n <= 0) return;
+    split_tf32_kernel<<<grid_for(n, 256), 256, 0, st>>>(u, lo, n);
     count_launch();
 }
 

@@ -147,6 +147,15 @@ def test_tf32_backward_within_training_precision(cuda):  # NGRAM_GRAD_TF32
     assert_grads_close(gb.download(), golden_grads(g, O.zero_grads(cfg)), ln, rel_l2=3e-3, max_rtol=1e-2)
 
 
+@pytest.mark.parametrize("name", ["backward_tc_scale_sqrt_d.npz", "backward_tc_layer_norm.npz"])
+def test_pedantic_fp32_backward(cuda, name):  # NGRAM_GRAD_PEDANTIC: CUDA-core fp32 GEMMs
+    g, cfg, hb, db, args, ln = _setup(name, cuda)
+    gb = G.GradBank(db, pedantic=True)
+    gb.backward(**args)
+    db.sync_errors()
+    assert_grads_close(gb.download(), golden_grads(g, O.zero_grads(cfg)), ln)
+
+
 def test_longcat_scale_sparse_backward_sampled(cuda):
     """Full LongCat width and table scale (D = 3072, N = 4, K = 4, ~19 M sub-table rows,
     counter-based device tables): the row-sparse backward of a 64-token sequence, checked
