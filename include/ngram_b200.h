@@ -264,9 +264,9 @@ int ngram_grad_create(ngram_bank* bank, ngram_grad** out); /* zero-initialised *
  * W_cat and LN gradients stay dense.  Needed at LongCat scale, where a dense fp32 copy of
  * the 31.5 B sub-table parameters (126 GB) does not fit beside the tables. */
 #define NGRAM_GRAD_SPARSE_ROWS 1
-/* NGRAM_GRAD_TF32: the two backward GEMMs on TF32 tensor cores (10-bit mantissa inputs, fp32
- * accumulation) instead of pedantic fp32 -- ~10x faster at LongCat scale; gradients agree
- * with the reference to ~1e-3 relative (training precision), not the 1e-5 fp32 contract. */
+/* NGRAM_GRAD_TF32: the two backward GEMMs as single-term TF32 (U rounded to TF32, fp32
+ * accumulation) -- ~1.8x faster than the default at LongCat scale; gradients agree with the
+ * reference to ~1e-3 relative (training precision), not the 1e-5 fp32 contract. */
 #define NGRAM_GRAD_TF32 2
 /* NGRAM_GRAD_PEDANTIC: the two backward GEMMs as pedantic fp32 (CUDA cores).  The default
  * runs them as two-term TF32 on the tensor cores: X and W_cat are bf16 values (exact in TF32),
