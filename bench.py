@@ -668,6 +668,49 @@ def run_decode_sharded(args):
     dist.destroy_process_group()
 
 
+def run_backward(args):
+    """Backward of config C (embed_sequence_backward, embedding.hpp:438-459; SURVEY.md 8(f) row
+    3): 8 x 8192 tokens, random fp32 upstream gradient, row-sparse sub-table gradients (a dense
+    fp32 copy of the 31.5 B sub-table parameters does not fit beside the tables), gradient bank
+    zeroed every step.  Lines for the default two-term TF32 GEMMs (fp32 tolerance), single TF32
+    and pedantic fp32."""
+    import torch
+    from paper_2601_21204_b200 import ngram as G
+    dev = torch.device("cuda", 0)
+    cfg, nseq, seq_len, label = workload("C")
+    bank = G.DeviceBank(cfg).generate(1234)
+    T = nseq * seq_len
+    gen = torch.Generator(device=dev).manual_seed(42)
+    toks = torch.randint(0, cfg["base_vocab"], (T,), dtype=torch.int32, device=dev, generator=gen)
+    off = torch.arange(0, T + 1, seq_len, dtype=torch.int64, device=dev)
+    up = torch.randn((T, cfg["dim"]), dtype=torch.float32, device=dev, generator=gen)
+    res = {}
+    for name, kw in (("two_term_tf32", {}), ("tf32", {"tf32": True}), ("pedantic_fp32", {"pedantic": True})):
+        gb = G.GradBank(bank, sparse_rows=True, **kw)
+        for _ in range(args.warmup):
+            gb.zero()
+            gb.backward(toks, off, up)
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        for i in range(args.steps):
+            ev[i][0].record()
+            gb.zero()
+            gb.backward(toks, off, up)
+            ev[i][1].record()
+        torch.cuda.synchronize()
+        ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+        res[name] = {"ms_per_step": ms, "tokens_per_s": T / (ms * 1e-3)}
+        gb.close()
+    bank.sync_errors()
+    print(json.dumps({"metric": "ngram_backward_tokens_per_sec", "value": res["two_term_tf32"]["tokens_per_s"],
+                      "unit": "tokens/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+                      "higher_is_better": True, "data": "synthetic (device tables, uniform tokens, randn upstream)",
+                      "config": {"workload": label + "_backward", "tokens": T, "sparse_rows": True,
+                                 "includes": "gradient-bank zeroing + K1 + amplify/E0 backward + gather + 2 GEMMs "
+                                             "(x2 terms by default) + COO append"},
+                      "results": res}))
+
+
 def run_analysis(args):
     """Corpus collision analysis (corpus_analyzer, analysis.cpp:93-121):
     the collision table of config C's twelve sub-table moduli, orders 2..4, V0 = 128000.  Each
@@ -748,6 +791,8 @@ def main():
         run_reference(args)
     elif args.workload == "analysis":
         run_analysis(args)
+    elif args.workload == "backward":
+        run_backward(args)
     elif args.workload in ("D", "E") and int(os.environ.get("WORLD_SIZE", "1")) > 1:
         run_decode_sharded(args)
     elif args.workload in ("D", "E"):
