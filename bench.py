@@ -4,6 +4,10 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload C|B|A]
     torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU)
 
+Secondary lines (not the driver's headline): --workload D | E (decode steps / verify blocks,
+CUDA-graph replay; sharded under torchrun), --workload backward (config C gradients),
+--workload analysis (corpus collision analysis); --tokens zipf (the reference's text model).
+
 A "step" is one pass of the hot path -- hash-index (K1) + gather/projection/epilogue
 (K2+K3) -- over one batch of synthetic tokens, inputs resident in HBM.  The headline
 workload is SURVEY.md 8(d) config C (LongCat-Flash-Lite-scale tables: V0=128000, N=4,
