@@ -203,3 +203,40 @@ def test_commit_rejects_accept_above_draft_length(bank, cuda):
         st.state()
     ring, length, last = st.state()
     assert (length == 0).all()  # whole batch left untouched
+
+
+@pytest.mark.parametrize("order,k", [(2, 2), (7, 1)])
+def test_decode_and_verify_other_orders(cuda, order, k):
+    """Ring sizes 1 and 6 (N = 2 / 7): decode steps and a verify block + commit equal the
+    prefill of the same sequences (ids bit-exact, rows within tolerance, ring = last N-1)."""
+    cfg = small_config(v0=50, dim=384, order=order, k=k)
+    hb = O.make_bank(cfg, 9, round_bf16=True)
+    db = G.DeviceBank(cfg).upload(hb.base, hb.sub, hb.proj)
+    B, L, Ld = 8, 10, 5
+    rng = np.random.default_rng(order)
+    seqs = rng.integers(0, 50, size=(B, L)).astype(np.uint32)
+    st = G.DecodeState(db, B, max_draft=Ld)
+    outs = []
+    for i in range(L):
+        ids, m = st.step(dev_u32(torch, seqs[:, i], cuda))
+        outs.append(m.clone())
+        for s in range(B):
+            assert np.array_equal(u64(ids)[s], O.hash_sequence(cfg, seqs[s, :i + 1])[-1])
+    draft = rng.integers(0, 50, size=(B, Ld)).astype(np.uint32)
+    ver = st.verify(dev_u32(torch, draft, cuda))
+    accept = rng.integers(0, Ld + 1, size=B).astype(np.int32)
+    st.commit(dev_u32(torch, draft, cuda), torch.from_numpy(accept).to(cuda))
+    db.sync_errors()
+    full = np.concatenate([seqs, draft], 1)
+    off = np.arange(0, B * (L + Ld) + 1, L + Ld)
+    _, pre = G.embed_forward(db, dev_u32(torch, full.reshape(-1), cuda), dev_i64(torch, off, cuda), rows=False,
+                             merged=True)
+    pre = pre.cpu().numpy().reshape(B, L + Ld, -1)
+    assert_rows_close(torch.stack(outs, 1).cpu().numpy().reshape(B * L, -1), pre[:, :L].reshape(B * L, -1))
+    assert_rows_close(ver.cpu().numpy().reshape(B * Ld, -1), pre[:, L:].reshape(B * Ld, -1))
+    ring, length, last = st.state()
+    R = order - 1
+    for s in range(B):
+        hist = list(seqs[s]) + list(draft[s, :accept[s]])
+        assert list(ring[s]) == [int(x) for x in hist[-R:]] and int(length[s]) == len(hist)
+        assert int(last[s]) == int(hist[-1])
