@@ -240,3 +240,40 @@ def test_decode_and_verify_other_orders(cuda, order, k):
         hist = list(seqs[s]) + list(draft[s, :accept[s]])
         assert list(ring[s]) == [int(x) for x in hist[-R:]] and int(length[s]) == len(hist)
         assert int(last[s]) == int(hist[-1])
+
+
+def test_decode_step_and_verify_replay_in_cuda_graph(bank, cuda):
+    """A decode step and a verify block + commit are capturable in a CUDA graph (the serving
+    pattern of bench.py --workload D/E): replays advance the device state exactly like eager
+    calls do."""
+    cfg, hb, db = bank
+    B = 8
+    rng = np.random.default_rng(5)
+    toks = dev_u32(torch, rng.integers(0, 32, size=B), cuda)
+    draft = dev_u32(torch, rng.integers(0, 32, size=(B, 4)), cuda)
+    acc = torch.from_numpy(rng.integers(0, 5, size=B).astype(np.int32)).to(cuda)
+    eager, graph = G.DecodeState(db, B, max_draft=4), G.DecodeState(db, B, max_draft=4)
+    out_e = torch.empty((B, 4, db.D), dtype=torch.float32, device=cuda)
+    out_g = torch.empty_like(out_e)
+    step_e = torch.empty((B, db.D), dtype=torch.float32, device=cuda)
+    step_g = torch.empty_like(step_e)
+
+    def one(st, so, vo):
+        st.step(toks, want_ids=False, out=so, out_dtype=torch.float32)
+        st.verify(draft, out=vo, out_dtype=torch.float32)
+        st.commit(draft, acc)
+
+    one(graph, step_g, out_g)  # warm-up (allocations happen outside the capture)
+    torch.cuda.synchronize()
+    one(eager, step_e, out_e)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        one(graph, step_g, out_g)
+    for _ in range(3):
+        g.replay()
+        one(eager, step_e, out_e)
+    torch.cuda.synchronize()
+    db.sync_errors()
+    assert torch.equal(step_e, step_g) and torch.equal(out_e, out_g)
+    for a, b in zip(eager.state(), graph.state()):
+        assert np.array_equal(a, b)
