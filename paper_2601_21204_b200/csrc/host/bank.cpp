@@ -193,6 +193,10 @@ int ngram_bank_create_ex(const char* config_json, int device, int shard_rank, in
     NGH_CUDA(cudaMemcpy(b->ht.p, ht.get(), sizeof(ngk::HashTables), cudaMemcpyHostToDevice));
     b->err.alloc(1);
     NGH_CUDA(cudaMemset(b->err.p, 0xff, sizeof(unsigned long long)));
+    b->err_rep.alloc(1);
+    NGH_CUDA(cudaMemset(b->err_rep.p, 0xff, sizeof(unsigned long long)));
+    b->err_ticket.alloc(1);
+    NGH_CUDA(cudaMemset(b->err_ticket.p, 0, sizeof(unsigned int)));
     if (b->tc_path) {
         make_tensor_map_2d(&b->tmap_sub, b->sub.p, uint64_t(d), uint64_t(std::max<int64_t>(rows, 1)),
                            uint64_t(d) * 2, 64, 1);

@@ -106,6 +106,12 @@ struct ngram_bank {
     ngh::DevBuf<float> ln_gain, ln_bias;
     ngh::DevBuf<ngk::HashTables> ht;
     ngh::DevBuf<unsigned long long> err;
+    // decode steps release the error word themselves (DecodeCommit::err_reported): token errors
+    // of such steps land in err_rep; err_clean = the error word is known clear at the stream's
+    // tail, so the next decode step needs no reset
+    ngh::DevBuf<unsigned long long> err_rep;
+    ngh::DevBuf<unsigned int> err_ticket;
+    bool err_clean = true;
 
     CUtensorMap tmap_sub{}, tmap_w{}, tmap_w2{}, tmap_e0{}, tmap_e0w{};
     ngh::Workspace ws;

@@ -17,6 +17,8 @@ namespace {
 // Hash + project T = batch * L block positions whose windows are ring ++ draft.  With
 // `commit`, the state update is fused into the projection when possible; returns whether
 // it was (otherwise the caller launches the commit kernel).
+constexpr int64_t kReleaseMaxT = 128;
+
 bool decode_block(ngram_decode* d, const uint32_t* draft, int L, uint64_t* ids_out, void* merged_out, int out_dtype,
                   cudaStream_t st, const ngk::DecodeCommit* commit = nullptr) {
     ngram_bank* b = d->bank;
@@ -25,15 +27,34 @@ bool decode_block(ngram_decode* d, const uint32_t* draft, int L, uint64_t* ids_o
                                   "(ngram_shard_scatter_rows with the rings as prior + ngram_shard_project)");
     const int64_t T = d->batch * L;
     const int64_t Tpad = round_up(T, kRowPad);
-    reset_error_word(b, st);
+    // A decode step whose commit runs in the chain's last kernel releases the error word there
+    // (DecodeCommit::err_reported): back-to-back steps then need no reset node between them
+    // (-1.5 to -1.8 us per step at B <= 64).  Large batches keep the reset: the release costs
+    // the reduce one ticket per block, more than the reset node at B = 256 (profiles/README.md).
+    const bool release = commit != nullptr && merged_out != nullptr && b->tc_path && T <= kReleaseMaxT;
+    if (!(release && b->err_clean)) reset_error_word(b, st);
+    ngk::DecodeCommit cr{};
+    if (release) {
+        cr = *commit;
+        cr.err_reported = b->err_rep.p;
+        cr.ticket = b->err_ticket.p;
+        commit = &cr;
+    }
     const int R = b->cfg.max_order - 1;
     const int64_t* off = d->seq_off.p + size_t(L - 1) * size_t(d->batch + 1);
     if (ids_out || !merged_out)
         ngk::launch_hash_ids(b->shape, b->ht.p, draft, off, d->batch, T, R > 0 ? d->ring.p : nullptr, ids_out, 1,
                              nullptr, Tpad, b->err.p, st);
-    if (merged_out)
-        return forward_tokens(b, draft, off, d->batch, T, R > 0 ? d->ring.p : nullptr, nullptr, merged_out,
-                              out_dtype == NGRAM_BF16, st, 0, &d->xbuf, d->grow.p, true, commit, L);
+    if (merged_out) {
+        const bool fused = forward_tokens(b, draft, off, d->batch, T, R > 0 ? d->ring.p : nullptr, nullptr,
+                                          merged_out, out_dtype == NGRAM_BF16, st, 0, &d->xbuf, d->grow.p, true,
+                                          commit, L);
+        if (release) {
+            if (!fused) throw Error(NGRAM_ECUDA, "decode step: commit was not fused into the projection");
+            b->err_clean = true;  // the chain's tail cleared the error word
+        }
+        return fused;
+    }
     return false;
 }
 

@@ -186,6 +186,7 @@ bool forward_tokens(ngram_bank* b, const uint32_t* tokens, const int64_t* seq_of
 
 void reset_error_word(ngram_bank* b, cudaStream_t st) {
     NGH_CUDA(cudaMemsetAsync(b->err.p, 0xff, sizeof(unsigned long long), st));
+    b->err_clean = false;  // this call's kernels may leave an error in it
 }
 
 }  // namespace ngh
@@ -313,11 +314,15 @@ int ngram_sync_errors(ngram_bank* b, void* stream) {
     if (!b) throw Error(NGRAM_EINVAL, "null bank");
     DeviceGuard g(b->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    unsigned long long e = 0;
+    unsigned long long e = 0, r = 0;
     NGH_CUDA(cudaMemcpyAsync(&e, b->err.p, sizeof(e), cudaMemcpyDeviceToHost, st));
+    NGH_CUDA(cudaMemcpyAsync(&r, b->err_rep.p, sizeof(r), cudaMemcpyDeviceToHost, st));
     NGH_CUDA(cudaStreamSynchronize(st));
+    e = std::min(e, r);  // errors of decode steps are released into err_rep
+    b->err_clean = true;
     if (e != ~0ull) {
         NGH_CUDA(cudaMemsetAsync(b->err.p, 0xff, sizeof(e), st));
+        NGH_CUDA(cudaMemsetAsync(b->err_rep.p, 0xff, sizeof(r), st));
         NGH_CUDA(cudaStreamSynchronize(st));
         throw Error(NGRAM_ERANGE, "embedding: token out of range for base vocabulary " +
                                       std::to_string(b->cfg.base_vocab) + " (first bad window at position " +

@@ -19,6 +19,10 @@ namespace {
 
 __global__ void __launch_bounds__(1024) commit_kernel(DecodeCommit c, const unsigned long long* err) {
     decode_commit_block(c, err);
+    if (c.err_reported) {
+        __syncthreads();  // every thread's reads of the error word are done
+        if (threadIdx.x == 0) decode_release_err(c, const_cast<unsigned long long*>(err));
+    }
 }
 
 __global__ void reset_kernel(int R, uint32_t* __restrict__ ring, uint64_t* __restrict__ length,

@@ -41,4 +41,12 @@ __device__ inline void decode_commit_block(const DecodeCommit& c, const unsigned
     }
 }
 
+// Decode-step tail, run once after every reader of the error word in the chain: a token error
+// of this step moves to *c.err_reported, the error word is left clear for the next step.
+__device__ inline void decode_release_err(const DecodeCommit& c, unsigned long long* err) {
+    const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(err);
+    if (e != ~0ull) atomicMin(c.err_reported, e);
+    *err = ~0ull;
+}
+
 }  // namespace ngk

@@ -1028,8 +1028,8 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
                                                             DecodeCommit commit) {
     griddep_wait();  // PDL launch: the split-K GEMM has completed (no-op for a normal launch)
     if (commit.ring && blockIdx.x == 0) decode_commit_block(commit, err);  // fused decode-state commit
-    if (*err != ~0ull) return;
-    const int64_t n4 = T * D / 4;
+    const bool bad = *err != ~0ull;  // a token was out of range: no output (uniform)
+    const int64_t n4 = bad ? 0 : T * D / 4;
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n4; v += (int64_t)gridDim.x * blockDim.x) {
         const int64_t t = v * 4 / D;
         const int i = (int)(v * 4 - t * D);
@@ -1057,6 +1057,17 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
             const float r[4] = {__fmul_rn(m[0], amp), __fmul_rn(m[1], amp), __fmul_rn(m[2], amp),
                                 __fmul_rn(m[3], amp)};
             put(rows, r);
+        }
+    }
+    if (commit.ticket) {  // decode step: the last block to finish releases the error word
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            if (atomicAdd(commit.ticket, 1u) == gridDim.x - 1) {
+                __threadfence();
+                decode_release_err(commit, const_cast<unsigned long long*>(err));
+                *commit.ticket = 0u;
+            }
         }
     }
 }
@@ -1119,10 +1130,10 @@ void launch_forward_tc(const FwdArgs& a, int num_sms, cudaStream_t st, float* sp
             const float scale = 1.0f / (float)a.s.denom;
             const float amp = a.s.amp == kAmpSqrt ? (float)__builtin_sqrt((double)a.s.D) : 1.0f;
             const int64_t n4 = a.T * a.s.D / 4;
-            int64_t blocks = (n4 + 255) / 256;
-            if (blocks > num_sms * 8) blocks = num_sms * 8;
             DecodeCommit c{};
             if (a.commit) c = *a.commit;
+            int64_t blocks = (n4 + 255) / 256;
+            if (blocks > num_sms * 8) blocks = num_sms * 8;
             const int wr = (a.rows_out != nullptr && a.s.amp != kAmpLN) ? 1 : 0;
             if (pdl) {
                 cudaLaunchConfig_t cfg{};

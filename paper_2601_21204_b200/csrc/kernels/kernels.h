@@ -160,6 +160,11 @@ struct DecodeCommit {
     const int32_t* accept;  // [batch] or null (= L for every stream)
     int64_t batch;
     unsigned long long* derr;
+    // decode step only (null otherwise): the chain's last kernel moves a token error of this
+    // step into *err_reported and leaves the error word clear for the next step, so steady
+    // decode needs no per-step reset node; ticket counts the finishing blocks (kept zeroed)
+    unsigned long long* err_reported;
+    unsigned int* ticket;
 };
 // Small-T projection (T <= 256, D % 128 == 0, tensor-core shape): split-K over a thread-
 // block cluster with the cross-split reduction, epilogue and optional commit fused.

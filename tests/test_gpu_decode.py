@@ -277,3 +277,27 @@ def test_decode_step_and_verify_replay_in_cuda_graph(bank, cuda):
     assert torch.equal(step_e, step_g) and torch.equal(out_e, out_g)
     for a, b in zip(eager.state(), graph.state()):
         assert np.array_equal(a, b)
+
+
+def test_bad_token_step_between_good_steps(bank, cuda):
+    """A decode step with a token >= V0 leaves every stream untouched and is reported (once) at
+    the next sync, while the steps around it -- which run without a per-step error reset --
+    advance the state and produce the same rows as a clean run."""
+    cfg, hb, db = bank
+    B = 4
+    good1, good2 = np.array([1, 2, 3, 4], np.uint32), np.array([5, 6, 7, 8], np.uint32)
+    bad = np.array([1, 32, 3, 4], np.uint32)  # V0 = 32
+    ref = G.DecodeState(db, B)
+    _, r1 = ref.step(dev_u32(torch, good1, cuda))
+    _, r2 = ref.step(dev_u32(torch, good2, cuda))
+    db.sync_errors()
+    st = G.DecodeState(db, B)
+    _, m1 = st.step(dev_u32(torch, good1, cuda))
+    st.step(dev_u32(torch, bad, cuda), want_ids=False, want_merged=True)
+    _, m2 = st.step(dev_u32(torch, good2, cuda))
+    with pytest.raises(OutOfRange):
+        db.sync_errors()
+    db.sync_errors()  # reported once
+    assert torch.equal(m1, r1) and torch.equal(m2, r2)
+    for a, b in zip(st.state(), ref.state()):
+        assert np.array_equal(a, b)
