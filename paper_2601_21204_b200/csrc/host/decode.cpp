@@ -32,7 +32,11 @@ bool decode_block(ngram_decode* d, const uint32_t* draft, int L, uint64_t* ids_o
     // (-1.5 to -1.8 us per step at B <= 64).  Large batches keep the reset: the release costs
     // the reduce one ticket per block, more than the reset node at B = 256 (profiles/README.md).
     const bool release = commit != nullptr && merged_out != nullptr && b->tc_path && T <= kReleaseMaxT;
-    if (!(release && b->err_clean)) reset_error_word(b, st);
+    // A verify block (no commit here) leaves the word to the ngram_commit that follows it, which
+    // releases it; so a verify needs no reset either when the word is known clear.
+    const bool verify = commit == nullptr && merged_out != nullptr && ids_out == nullptr;
+    if (!((release || verify) && b->err_clean)) reset_error_word(b, st);
+    b->err_clean = false;
     ngk::DecodeCommit cr{};
     if (release) {
         cr = *commit;
@@ -142,9 +146,11 @@ int ngram_commit(ngram_decode* d, const uint32_t* draft, int L, const int32_t* a
     NGRAM_API_BEGIN
     if (!d || !draft || !accept || L < 1 || L > d->max_draft) throw Error(NGRAM_EINVAL, "ngram_commit: bad argument");
     DeviceGuard g(d->bank->device);
-    ngk::launch_decode_commit(d->bank->shape, d->ring.p, d->length.p, d->last.p, draft, L, accept, d->batch,
-                              d->bank->err.p, d->derr.p, static_cast<cudaStream_t>(stream));
+    ngram_bank* b = d->bank;
+    ngk::launch_decode_commit(b->shape, d->ring.p, d->length.p, d->last.p, draft, L, accept, d->batch, b->err.p,
+                              d->derr.p, static_cast<cudaStream_t>(stream), b->err_rep.p);
     NGH_CUDA(cudaGetLastError());
+    b->err_clean = true;  // this commit, the last reader of its verify's error word, released it
     NGRAM_API_END
 }
 

@@ -39,9 +39,9 @@ __global__ void reset_kernel(int R, uint32_t* __restrict__ ring, uint64_t* __res
 
 void launch_decode_commit(const Shape& s, uint32_t* ring, uint64_t* length, uint32_t* last, const uint32_t* draft,
                           int L, const int32_t* accept, int64_t batch, unsigned long long* err,
-                          unsigned long long* derr, cudaStream_t st) {
+                          unsigned long long* derr, cudaStream_t st, unsigned long long* err_reported) {
     if (batch <= 0) return;
-    DecodeCommit c{s.N > 1 ? s.N - 1 : 0, ring, length, last, draft, L, accept, batch, derr};
+    DecodeCommit c{s.N > 1 ? s.N - 1 : 0, ring, length, last, draft, L, accept, batch, derr, err_reported, nullptr};
     const int threads = batch >= 1024 ? 1024 : (int)((batch + 31) / 32 * 32);
     commit_kernel<<<1, threads, 0, st>>>(c, err);
     count_launch();

@@ -171,10 +171,12 @@ struct DecodeCommit {
 void launch_decode_commit_c(const DecodeCommit& c, const unsigned long long* err, cudaStream_t st);
 // The hashing of a decode step / verify block is launch_hash_ids with prior = ring and
 // seq_off = {0, L, 2L, ...}; these kernels move the ring.  derr: decode error word
-// ((status << 32) | detail), ~0 when clear.
+// ((status << 32) | detail), ~0 when clear.  err_reported (or null): the commit releases the
+// token-error word of the verify block it commits (DecodeCommit::err_reported).
 void launch_decode_commit(const Shape& s, uint32_t* ring, uint64_t* length, uint32_t* last, const uint32_t* draft,
                           int L, const int32_t* accept, int64_t batch, unsigned long long* err,
-                          unsigned long long* derr, cudaStream_t st);
+                          unsigned long long* derr, cudaStream_t st,
+                          unsigned long long* err_reported = nullptr);
 void launch_decode_reset(const Shape& s, uint32_t* ring, uint64_t* length, uint32_t* last, const uint32_t* prior,
                          const uint64_t* lengths, int64_t batch, cudaStream_t st);
 

@@ -301,3 +301,29 @@ def test_bad_token_step_between_good_steps(bank, cuda):
     assert torch.equal(m1, r1) and torch.equal(m2, r2)
     for a, b in zip(st.state(), ref.state()):
         assert np.array_equal(a, b)
+
+
+def test_bad_token_verify_then_commit_is_refused_and_reported(bank, cuda):
+    """verify + commit without a per-call reset: a draft holding a token >= V0 makes the commit
+    leave every stream untouched and is reported once at the next sync; the next verify +
+    commit works normally."""
+    cfg, hb, db = bank
+    B, L = 4, 3
+    st = G.DecodeState(db, B, max_draft=L)
+    good = dev_u32(torch, np.array([[1, 2, 3]] * B, np.uint32), cuda)
+    bad = dev_u32(torch, np.array([[1, 2, 3], [4, 40, 6], [7, 8, 9], [1, 1, 1]], np.uint32), cuda)
+    acc = torch.full((B,), L, dtype=torch.int32, device=cuda)
+    st.verify(good)
+    st.commit(good, acc)
+    db.sync_errors()
+    before = st.state()
+    st.verify(bad)
+    st.commit(bad, acc)
+    with pytest.raises(OutOfRange):
+        db.sync_errors()
+    for a, b in zip(st.state(), before):
+        assert np.array_equal(a, b)
+    st.verify(good)
+    st.commit(good, acc)
+    db.sync_errors()
+    assert (st.state()[1] == 2 * L).all()
