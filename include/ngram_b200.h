@@ -144,7 +144,10 @@ int ngram_embed_forward(ngram_bank* bank, const uint32_t* tokens, const int64_t*
 int ngram_embed_from_ids(ngram_bank* bank, const uint32_t* tokens, const uint64_t* ids, int64_t T, void* merged_out,
                          int out_dtype, void* stream);
 /* Synchronise `stream` and report (then clear) the bank's device error word:
- * NGRAM_ERANGE with the offending token when a token >= V0 was seen. */
+ * NGRAM_ERANGE with the offending token when a token >= V0 was seen.  Decode steps and
+ * verify + commit pairs do not reset the word per call: their last kernel moves a token error
+ * into a reported word instead (so back-to-back steps need no reset node); this call reports
+ * the earliest of both since the last sync. */
 int ngram_sync_errors(ngram_bank* bank, void* stream);
 /* Host-buffer entry (the drop-in embed_sequence path): copies tokens/prior from host,
  * runs the forward, copies rows/merged back to host (NULL to skip), overlapping the
