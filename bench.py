@@ -42,6 +42,9 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# a rank that dies mid-run must not leave the others blocked in a collective forever
+_PG_TIMEOUT = __import__("datetime").timedelta(minutes=10)
+
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
@@ -318,9 +321,9 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     if world > 1:
         if one_dev:
-            dist.init_process_group("gloo")
+            dist.init_process_group("gloo", timeout=_PG_TIMEOUT)
         else:
-            dist.init_process_group("nccl", device_id=dev)
+            dist.init_process_group("nccl", device_id=dev, timeout=_PG_TIMEOUT)
     sharding = args.sharding if world > 1 else "single"
 
     cfg, nseq, seq_len, label = workload(args.workload)
@@ -617,9 +620,9 @@ def run_decode_sharded(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if one_dev:
-        dist.init_process_group("gloo")
+        dist.init_process_group("gloo", timeout=_PG_TIMEOUT)
     else:
-        dist.init_process_group("nccl", device_id=dev)
+        dist.init_process_group("nccl", device_id=dev, timeout=_PG_TIMEOUT)
     cfg, _, _, _ = workload("C" if not os.environ.get("NGRAM_BENCH_DECODE_CFG") else os.environ["NGRAM_BENCH_DECODE_CFG"])
     cfg = dict(cfg)
     cfg["amplification"] = "none"  # the cache path returns merged vectors (cache.hpp:122-124)
