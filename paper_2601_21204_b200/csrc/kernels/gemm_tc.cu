@@ -1060,11 +1060,11 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
         }
     }
     if (commit.ticket) {  // decode step: the last block to finish releases the error word
-        __syncthreads();
+        __syncthreads();  // the block's reads of the error word precede thread 0's release
         if (threadIdx.x == 0) {
-            __threadfence();
-            if (atomicAdd(commit.ticket, 1u) == gridDim.x - 1) {
-                __threadfence();
+            unsigned prev;
+            asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(commit.ticket) : "memory");
+            if (prev == gridDim.x - 1) {  // acquired every other block's release
                 decode_release_err(commit, const_cast<unsigned long long*>(err));
                 *commit.ticket = 0u;
             }
