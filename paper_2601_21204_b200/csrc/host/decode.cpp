@@ -17,7 +17,7 @@ namespace {
 // Hash + project T = batch * L block positions whose windows are ring ++ draft.  With
 // `commit`, the state update is fused into the projection when possible; returns whether
 // it was (otherwise the caller launches the commit kernel).
-constexpr int64_t kReleaseMaxT = 128;
+constexpr int64_t kReleaseMaxT = 256;  // the small-T (split-K + reduce) regime
 
 bool decode_block(ngram_decode* d, const uint32_t* draft, int L, uint64_t* ids_out, void* merged_out, int out_dtype,
                   cudaStream_t st, const ngk::DecodeCommit* commit = nullptr) {
@@ -29,8 +29,7 @@ bool decode_block(ngram_decode* d, const uint32_t* draft, int L, uint64_t* ids_o
     const int64_t Tpad = round_up(T, kRowPad);
     // A decode step whose commit runs in the chain's last kernel releases the error word there
     // (DecodeCommit::err_reported): back-to-back steps then need no reset node between them
-    // (-1.5 to -1.8 us per step at B <= 64).  Large batches keep the reset: the release costs
-    // the reduce one ticket per block, more than the reset node at B = 256 (profiles/README.md).
+    // (-1.4 to -1.6 us per step, profiles/README.md).
     const bool release = commit != nullptr && merged_out != nullptr && b->tc_path && T <= kReleaseMaxT;
     // A verify block (no commit here) leaves the word to the ngram_commit that follows it, which
     // releases it; so a verify needs no reset either when the word is known clear.
