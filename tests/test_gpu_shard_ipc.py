@@ -92,7 +92,7 @@ torch.cuda.set_device(0)
 dev = torch.device("cuda", 0)
 cfg = O.make_default_config(4000, 768, 4, 4)
 cfg["amplification"] = "none"  # the cache path returns merged vectors
-Bh, L = 6, 4
+Bh, L = 6, int(sys.argv[3])
 rng = np.random.default_rng(11)
 prior = torch.from_numpy(rng.integers(0, 4000, size=(world * Bh, 3)).astype(np.int32)).to(dev)
 lengths = torch.full((world * Bh,), 100, dtype=torch.int64, device=dev)
@@ -131,17 +131,18 @@ dist.destroy_process_group()
 """
 
 
-def test_two_process_sharded_verify_and_commit(cuda):
+@pytest.mark.parametrize("L", [1, 4])
+def test_two_process_sharded_verify_and_commit(cuda, L):
     """Config E on row-sharded tables, two ranks: all-gathered drafts + rings, owned rows
     scattered over CUDA IPC, split-K projection of the home block, local commit -- identical
-    to the single-GPU verify + commit of the same streams."""
+    to the single-GPU verify + commit of the same streams.  L = 1 is a sharded decode step."""
     code = VERIFY_WORKER.format(root=ROOT, tests=HERE, port=_free_port())
     with tempfile.TemporaryDirectory() as td:
         procs, outs = [], []
         for r in range(2):
             out = os.path.join(td, f"r{r}.npy")
             outs.append(out)
-            procs.append(subprocess.Popen([sys.executable, "-c", code, str(r), out]))
+            procs.append(subprocess.Popen([sys.executable, "-c", code, str(r), out, str(L)]))
         for p in procs:
             assert p.wait(timeout=300) == 0
         assert all(int(np.load(o)[0]) == 1 for o in outs)
