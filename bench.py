@@ -6,7 +6,8 @@
 
 Secondary lines (not the driver's headline): --workload D | E (decode steps / verify blocks,
 CUDA-graph replay; sharded under torchrun), --workload backward (config C gradients),
---workload analysis (corpus collision analysis); --tokens zipf (the reference's text model).
+--workload analysis (corpus collision analysis), --workload plne (per-layer N-gram FFN);
+--tokens zipf (the reference's text model).
 
 A "step" is one pass of the hot path -- hash-index (K1) + gather/projection/epilogue
 (K2+K3) -- over one batch of synthetic tokens, inputs resident in HBM.  The headline
@@ -718,6 +719,55 @@ def run_backward(args):
                       "results": res}))
 
 
+def run_plne(args):
+    """Per-layer N-gram FFN (ffn_plne / ffn_plne_backward, ple.hpp:168-196)
+    at a LongCat-like width: d_model = hidden = 3072, layer bank make_default_config(8000, 3072,
+    4, 4) (amplification none), 8 x 1024 tokens.  Forward and forward+backward (gate / down / x
+    gradients, no bank gradients) for the default three-term TF32 GEMMs and pedantic fp32."""
+    import torch
+    from paper_2601_21204_b200 import ngram as G
+    dev = torch.device("cuda", 0)
+    cfg = G.make_default_config(8000, 3072, 4, 4)
+    cfg["amplification"] = "none"
+    bank = G.DeviceBank(cfg).generate(7)
+    nseq, L, Dm, H = 8, 1024, 3072, 3072
+    T = nseq * L
+    gen = torch.Generator(device=dev).manual_seed(3)
+    toks = torch.randint(0, 8000, (T,), dtype=torch.int32, device=dev, generator=gen)
+    off = torch.arange(0, T + 1, L, dtype=torch.int64, device=dev)
+    gate = 0.02 * torch.randn((H, Dm), device=dev, generator=gen)
+    down = 0.02 * torch.randn((Dm, H), device=dev, generator=gen)
+    x = torch.randn((T, Dm), device=dev, generator=gen)
+    up = torch.randn((T, Dm), device=dev, generator=gen)
+    dg, dd, dx = torch.zeros_like(gate), torch.zeros_like(down), torch.zeros_like(x)
+    res = {}
+    for name, ped in (("three_term_tf32", False), ("pedantic_fp32", True)):
+        layer = G.PlneLayer(bank, Dm, pedantic=ped)
+        out = {}
+        for what, fn in (("forward", lambda: layer.forward(gate, down, x, toks, off)),
+                         ("forward_backward", lambda: layer.backward(gate, down, x, toks, off, up, dg, dd, dx))):
+            for _ in range(args.warmup):
+                fn()
+            torch.cuda.synchronize()
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            e[0].record()
+            for _ in range(args.steps):
+                fn()
+            e[1].record()
+            torch.cuda.synchronize()
+            ms = e[0].elapsed_time(e[1]) / args.steps
+            out[what] = {"ms_per_step": ms, "tokens_per_s": T / (ms * 1e-3)}
+        res[name] = out
+        layer.close()
+    bank.sync_errors()
+    print(json.dumps({"metric": "ngram_plne_tokens_per_sec", "value": res["three_term_tf32"]["forward"]["tokens_per_s"],
+                      "unit": "tokens/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+                      "higher_is_better": True, "data": "synthetic (device layer bank, uniform tokens, randn x)",
+                      "config": {"workload": "plne_d3072_h3072_8x1024", "V0": 8000, "N": 4, "K": 4,
+                                 "d_model": Dm, "hidden": H, "tokens": T},
+                      "results": res}))
+
+
 def run_analysis(args):
     """Corpus collision analysis (corpus_analyzer, analysis.cpp:93-121):
     the collision table of config C's twelve sub-table moduli, orders 2..4, V0 = 128000.  Each
@@ -800,6 +850,8 @@ def main():
         run_analysis(args)
     elif args.workload == "backward":
         run_backward(args)
+    elif args.workload == "plne":
+        run_plne(args)
     elif args.workload in ("D", "E") and int(os.environ.get("WORLD_SIZE", "1")) > 1:
         run_decode_sharded(args)
     elif args.workload in ("D", "E"):

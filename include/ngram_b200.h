@@ -257,8 +257,9 @@ int ngram_amplify_host(int amp_mode, int D, int64_t rows, const float* gain, con
  * with the device layout (E0 V0 x D, sub-tables concatenated by branch, projections as
  * W_cat D x D, LN gain / bias D).  amplify_backward (embedding.hpp:291-336) then
  * embed_backward (:338-376) per position; the dense products dW_cat += U^T X and
- * dX = U W_cat are fp32 GEMMs (cuBLAS, no TF32); scatters use fp32 atomics, so results
- * match the reference within an fp32 tolerance (not bit-exact).  Single-shard banks only. */
+ * dX = U W_cat are fp32-accurate GEMMs (cuBLAS two-term TF32; see the flags below);
+ * scatters use fp32 atomics, so results match the reference within an fp32 tolerance (not
+ * bit-exact).  Single-shard banks only. */
 typedef struct ngram_grad ngram_grad;
 int ngram_grad_create(ngram_bank* bank, ngram_grad** out); /* zero-initialised */
 /* NGRAM_GRAD_SPARSE_ROWS: the sub-table gradient is kept row-sparse instead of dense -- every
@@ -311,11 +312,16 @@ int ngram_grad_download(ngram_grad* g, float* base, float* const* sub, float* co
 /* ffn_plne (ple.hpp:168-181) batched on the device: y = W_d (SiLU(W_g x) (.) g) with g the
  * layer bank's merged embedding of each position's window (layer bank: amplification none,
  * dim = hidden).  gate: dev f32 [hidden][d_model]; down: dev f32 [d_model][hidden];
- * x, y: dev f32 [T][d_model]; tokens / seq_offsets / prior as ngram_embed_forward.  fp32
- * GEMMs (cuBLAS, no TF32).  ffn_ple (table-row gate) = a base-only layer bank (max_order 1).
+ * x, y: dev f32 [T][d_model]; tokens / seq_offsets / prior as ngram_embed_forward.  fp32-
+ * accurate GEMMs (cuBLAS; three-term TF32 by default, see ngram_plne_create_ex).  ffn_ple (table-row gate) = a base-only layer bank (max_order 1).
  * Outputs are unspecified when a token is out of range (NGRAM_ERANGE at the next sync). */
 typedef struct ngram_plne ngram_plne;
 int ngram_plne_create(ngram_bank* layer_bank, int d_model, ngram_plne** out);
+/* flags: NGRAM_PLNE_PEDANTIC -- the GEMMs as pedantic fp32 on the CUDA cores.  Default: three-term
+ * TF32 on the tensor cores (A = A_hi + A_lo, B = B_hi + B_lo, A_hi B_hi + A_hi B_lo + A_lo B_hi:
+ * fp32-accurate, the default tolerance holds). */
+#define NGRAM_PLNE_PEDANTIC 1
+int ngram_plne_create_ex(ngram_bank* layer_bank, int d_model, int flags, ngram_plne** out);
 int ngram_plne_destroy(ngram_plne* p);
 int ngram_plne_forward(ngram_plne* p, const float* gate, const float* down, const float* x, const uint32_t* tokens,
                        const int64_t* seq_offsets, int64_t nseq, int64_t total_tokens, const uint32_t* prior, float* y,

@@ -21,6 +21,7 @@ NGRAM_BWD_SKIP_AMPLIFY = 1
 NGRAM_GRAD_SPARSE_ROWS = 1
 NGRAM_GRAD_TF32 = 2
 NGRAM_GRAD_PEDANTIC = 4
+NGRAM_PLNE_PEDANTIC = 1
 NGRAM_SHARD_HANDLE_BYTES = 128
 
 # Exported symbols, in header order (tests check the .so exports every one).
@@ -44,6 +45,7 @@ SYMBOLS = [
     "ngram_amplify_backward_host", "ngram_decode_ring", "ngram_decode_copy_ring",
     "ngram_analyzer_create", "ngram_analyzer_destroy", "ngram_analyzer_add", "ngram_analyzer_add_host",
     "ngram_analyzer_merge", "ngram_analyzer_sync_errors", "ngram_analyzer_stats", "ngram_analyzer_reserve",
+    "ngram_plne_create_ex",
 ]
 
 
@@ -177,6 +179,7 @@ def lib() -> C.CDLL:
         "ngram_analyzer_merge": ([vp, vp, vp], i32),
         "ngram_analyzer_sync_errors": ([vp], i32),
         "ngram_analyzer_reserve": ([vp, u64], i32),
+        "ngram_plne_create_ex": ([vp, i32, i32, C.POINTER(vp)], i32),
         "ngram_analyzer_stats": ([vp, vp, vp, vp, vp, vp], i32),
     }
     for name, (args, res) in sig.items():

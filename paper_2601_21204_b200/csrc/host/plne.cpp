@@ -26,6 +26,8 @@ struct ngram_plne {
     DevBuf<float> h_gate, h_down, h_x, h_y, h_up, h_dgate, h_ddown, h_dx;
     DevBuf<uint32_t> h_tok, h_prior;
     DevBuf<int64_t> h_off;
+    bool three = true;                 // three-term TF32 GEMMs (default) vs pedantic fp32
+    DevBuf<float> ah, al, bh, bl;      // TF32 hi / lo splits of the two GEMM operands
     ~ngram_plne() {
         if (blas) cublasDestroy(blas);
     }
@@ -36,6 +38,29 @@ namespace {
 void blas_ok(cublasStatus_t s, const char* what) {
     if (s != CUBLAS_STATUS_SUCCESS)
         throw Error(NGRAM_ECUDA, std::string(what) + " failed (cublas status " + std::to_string(int(s)) + ")");
+}
+
+// C = A op B (+ beta C).  Default: three-term TF32 on the tensor cores -- A = Ah + Al and
+// B = Bh + Bl with Ah, Bh TF32-exact; Ah Bh + Ah Bl + Al Bh is fp32-accurate (the dropped Al Bl
+// and the TF32 rounding of the lo terms are ~2^-21 relative).  nA / nB: element counts of the
+// stored operands (split elementwise, whatever the op).  NGRAM_PLNE_PEDANTIC: one fp32 GEMM.
+void gemm(ngram_plne* p, cublasOperation_t ta, cublasOperation_t tb, int m, int n, int k, const float* A, size_t nA,
+          int lda, const float* B, size_t nB, int ldb, float beta, float* C, int ldc, cudaStream_t st,
+          const char* what) {
+    const float one = 1.0f;
+    if (!p->three) {
+        blas_ok(cublasSgemm(p->blas, ta, tb, m, n, k, &one, A, lda, B, ldb, &beta, C, ldc), what);
+        return;
+    }
+    p->ah.ensure(nA);
+    p->al.ensure(nA);
+    p->bh.ensure(nB);
+    p->bl.ensure(nB);
+    ngk::launch_split_tf32_copy(A, p->ah.p, p->al.p, int64_t(nA), st);
+    ngk::launch_split_tf32_copy(B, p->bh.p, p->bl.p, int64_t(nB), st);
+    blas_ok(cublasSgemm(p->blas, ta, tb, m, n, k, &one, p->ah.p, lda, p->bh.p, ldb, &beta, C, ldc), what);
+    blas_ok(cublasSgemm(p->blas, ta, tb, m, n, k, &one, p->ah.p, lda, p->bl.p, ldb, &one, C, ldc), what);
+    blas_ok(cublasSgemm(p->blas, ta, tb, m, n, k, &one, p->al.p, lda, p->bh.p, ldb, &one, C, ldc), what);
 }
 
 void status_ok(int rc) {
@@ -60,8 +85,9 @@ void forward_common(ngram_plne* p, const float* gate, const float* x, const uint
     const float one = 1.0f, zero = 0.0f;
     const int H = p->hidden, Dm = p->d_model;
     blas_ok(cublasSetStream(p->blas, st), "cublasSetStream");
-    blas_ok(cublasSgemm(p->blas, CUBLAS_OP_T, CUBLAS_OP_N, H, int(T), Dm, &one, gate, Dm, x, Dm, &zero, p->U.p, H),
-            "cublasSgemm(U = X W_g^T)");
+    (void)one;
+    gemm(p, CUBLAS_OP_T, CUBLAS_OP_N, H, int(T), Dm, gate, size_t(H) * Dm, Dm, x, size_t(T) * Dm, Dm, zero, p->U.p, H,
+         st, "cublasSgemm(U = X W_g^T)");
     ngk::launch_silu_gate(p->U.p, p->G.p, p->Hh.p, T * H, p->bank->err.p, st);
 }
 
@@ -69,8 +95,11 @@ void forward_common(ngram_plne* p, const float* gate, const float* x, const uint
 
 extern "C" {
 
-int ngram_plne_create(ngram_bank* b, int d_model, ngram_plne** out) {
+int ngram_plne_create(ngram_bank* b, int d_model, ngram_plne** out) { return ngram_plne_create_ex(b, d_model, 0, out); }
+
+int ngram_plne_create_ex(ngram_bank* b, int d_model, int flags, ngram_plne** out) {
     NGRAM_API_BEGIN
+    if (flags & ~NGRAM_PLNE_PEDANTIC) throw Error(NGRAM_EINVAL, "ngram_plne_create_ex: unknown flags");
     if (!b || !out) throw Error(NGRAM_EINVAL, "ngram_plne_create: bad argument");
     if (d_model < 1) throw Error(NGRAM_EINVAL, "ple: d_model and hidden must be >= 1");
     if (b->hash_only) throw Error(NGRAM_EINVAL, "bank was created hash-only (NGRAM_BANK_HASH_ONLY)");
@@ -81,7 +110,9 @@ int ngram_plne_create(ngram_bank* b, int d_model, ngram_plne** out) {
     p->d_model = d_model;
     p->hidden = b->shape.D;
     blas_ok(cublasCreate(&p->blas), "cublasCreate");
-    blas_ok(cublasSetMathMode(p->blas, CUBLAS_PEDANTIC_MATH), "cublasSetMathMode");  // true fp32
+    p->three = !(flags & NGRAM_PLNE_PEDANTIC);
+    blas_ok(cublasSetMathMode(p->blas, p->three ? CUBLAS_TF32_TENSOR_OP_MATH : CUBLAS_PEDANTIC_MATH),
+            "cublasSetMathMode");
     *out = p.release();
     NGRAM_API_END
 }
@@ -108,8 +139,9 @@ int ngram_plne_forward(ngram_plne* p, const float* gate, const float* down, cons
     forward_common(p, gate, x, tokens, seq_offsets, nseq, T, prior, st);
     const float one = 1.0f, zero = 0.0f;
     const int H = p->hidden, Dm = p->d_model;
-    blas_ok(cublasSgemm(p->blas, CUBLAS_OP_T, CUBLAS_OP_N, Dm, int(T), H, &one, down, H, p->Hh.p, H, &zero, y, Dm),
-            "cublasSgemm(Y = Hh W_d^T)");
+    (void)one;
+    gemm(p, CUBLAS_OP_T, CUBLAS_OP_N, Dm, int(T), H, down, size_t(H) * Dm, H, p->Hh.p, size_t(T) * H, H, zero, y, Dm,
+         st, "cublasSgemm(Y = Hh W_d^T)");
     NGRAM_API_END
 }
 
@@ -132,21 +164,21 @@ int ngram_plne_backward(ngram_plne* p, ngram_grad* bank_grads, const float* gate
     const int H = p->hidden, Dm = p->d_model;
     const int n = int(T);
     // g_down (Dm x H) += dY^T Hh  <=>  col-major g_down^T (H x Dm) += Hh_cm dY_cm^T
-    blas_ok(cublasSgemm(p->blas, CUBLAS_OP_N, CUBLAS_OP_T, H, Dm, n, &one, p->Hh.p, H, upstream, Dm, &one, d_down, H),
-            "cublasSgemm(dW_d)");
+    gemm(p, CUBLAS_OP_N, CUBLAS_OP_T, H, Dm, n, p->Hh.p, size_t(n) * H, H, upstream, size_t(n) * Dm, Dm, one, d_down,
+         H, st, "cublasSgemm(dW_d)");
     // dHh (T x H) = dY W_d  <=>  col-major dHh^T = down_cm dY_cm
-    blas_ok(cublasSgemm(p->blas, CUBLAS_OP_N, CUBLAS_OP_N, H, n, Dm, &one, down, H, upstream, Dm, &zero, p->dHh.p, H),
-            "cublasSgemm(dHh)");
+    gemm(p, CUBLAS_OP_N, CUBLAS_OP_N, H, n, Dm, down, size_t(H) * Dm, H, upstream, size_t(n) * Dm, Dm, zero, p->dHh.p,
+         H, st, "cublasSgemm(dHh)");
     ngk::launch_silu_gate_backward(p->dHh.p, p->U.p, p->G.p, p->dG.p, p->dU.p, T * H, p->bank->err.p, st);
     if (bank_grads)  // embed_backward of dL/dg (ple.hpp:195)
         status_ok(ngram_embed_backward(bank_grads, tokens, seq_offsets, nseq, T, prior, nullptr, p->dG.p,
                                        NGRAM_BWD_SKIP_AMPLIFY, st));
     // g_gate (H x Dm) += dU^T X  <=>  col-major g_gate^T (Dm x H) += X_cm dU_cm^T
-    blas_ok(cublasSgemm(p->blas, CUBLAS_OP_N, CUBLAS_OP_T, Dm, H, n, &one, x, Dm, p->dU.p, H, &one, d_gate, Dm),
-            "cublasSgemm(dW_g)");
+    gemm(p, CUBLAS_OP_N, CUBLAS_OP_T, Dm, H, n, x, size_t(n) * Dm, Dm, p->dU.p, size_t(n) * H, H, one, d_gate, Dm, st,
+         "cublasSgemm(dW_g)");
     // dx (T x Dm) += dU W_g  <=>  col-major dx^T += gate_cm dU_cm
-    blas_ok(cublasSgemm(p->blas, CUBLAS_OP_N, CUBLAS_OP_N, Dm, n, H, &one, gate, Dm, p->dU.p, H, &one, dx, Dm),
-            "cublasSgemm(dx)");
+    gemm(p, CUBLAS_OP_N, CUBLAS_OP_N, Dm, n, H, gate, size_t(H) * Dm, Dm, p->dU.p, size_t(n) * H, H, one, dx, Dm, st,
+         "cublasSgemm(dx)");
     NGRAM_API_END
 }
 

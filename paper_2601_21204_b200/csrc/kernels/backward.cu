@@ -186,6 +186,17 @@ __global__ void split_tf32_kernel(float* __restrict__ u, float* __restrict__ lo,
     }
 }
 
+__global__ void split_tf32_copy_kernel(const float* __restrict__ a, float* __restrict__ hi, float* __restrict__ lo,
+                                       int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float x = a[i];
+        uint32_t h;
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+        hi[i] = __uint_as_float(h);
+        lo[i] = x - __uint_as_float(h);
+    }
+}
+
 int grid_for(int64_t n, int threads) {
     int64_t g = (n + threads - 1) / threads;
     if (g > 148 * 16) g = 148 * 16;
@@ -234,6 +245,12 @@ void launch_rows_to_coo(const Shape& s, const int32_t* grow, int64_t Tpad, int64
                         const unsigned long long* err, cudaStream_t st) {
     if (T <= 0 || s.B == 0) return;
     rows_to_coo_kernel<<<grid_for(T * s.B, 256), 256, 0, st>>>(grow, Tpad, T, s.B, rows, err);
+    count_launch();
+}
+
+void launch_split_tf32_copy(const float* a, float* hi, float* lo, int64_t n, cudaStream_t st) {
+    if (n <= 0) return;
+    split_tf32_copy_kernel<<<grid_for(n, 256), 256, 0, st>>>(a, hi, lo, n);
     count_launch();
 }
 

@@ -82,6 +82,7 @@ void launch_scatter_rows(const Shape& s, const int32_t* grow, int64_t Tpad, int6
 void launch_bf16_to_f32(const __nv_bfloat16* src, float* dst, int64_t n, cudaStream_t st);
 // u <- TF32-rounded u (round to nearest), lo <- the fp32 remainder (two-term TF32 GEMMs)
 void launch_split_tf32(float* u, float* lo, int64_t n, cudaStream_t st);
+void launch_split_tf32_copy(const float* a, float* hi, float* lo, int64_t n, cudaStream_t st);
 void launch_rows_to_coo(const Shape& s, const int32_t* grow, int64_t Tpad, int64_t T, int32_t* rows,
                         const unsigned long long* err, cudaStream_t st);
 

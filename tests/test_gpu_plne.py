@@ -34,19 +34,21 @@ def _setup(name, cuda):
     return g, cfg, hb, db, a
 
 
+@pytest.mark.parametrize("pedantic", [False, True])  # three-term TF32 (default) / CUDA-core fp32
 @pytest.mark.parametrize("name", ["plne_tc.npz", "plne_small.npz"])
-def test_plne_forward_matches_reference(cuda, name):
+def test_plne_forward_matches_reference(cuda, name, pedantic):
     g, cfg, hb, db, a = _setup(name, cuda)
-    layer = G.PlneLayer(db, int(g["d_model"]))
+    layer = G.PlneLayer(db, int(g["d_model"]), pedantic=pedantic)
     y = layer.forward(**a)
     db.sync_errors()
     assert_rows_close(y.cpu().numpy(), g["y"])
 
 
+@pytest.mark.parametrize("pedantic", [False, True])
 @pytest.mark.parametrize("name", ["plne_tc.npz", "plne_small.npz"])
-def test_plne_backward_matches_reference(cuda, name):
+def test_plne_backward_matches_reference(cuda, name, pedantic):
     g, cfg, hb, db, a = _setup(name, cuda)
-    layer = G.PlneLayer(db, int(g["d_model"]))
+    layer = G.PlneLayer(db, int(g["d_model"]), pedantic=pedantic)
     gb = G.GradBank(db)
     d_gate = torch.zeros_like(a["gate"])
     d_down = torch.zeros_like(a["down"])
