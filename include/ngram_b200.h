@@ -257,7 +257,8 @@ int ngram_amplify_host(int amp_mode, int D, int64_t rows, const float* gain, con
  * with the device layout (E0 V0 x D, sub-tables concatenated by branch, projections as
  * W_cat D x D, LN gain / bias D).  amplify_backward (embedding.hpp:291-336) then
  * embed_backward (:338-376) per position; the dense products dW_cat += U^T X and
- * dX = U W_cat are fp32-accurate GEMMs (cuBLAS two-term TF32; see the flags below);
+ * dX = U W_cat are fp32-accurate GEMMs on the tensor cores (U split into three bf16 terms,
+ * X / W_cat bf16-exact; two-term TF32 on CUDA-core-shaped banks; see the flags below);
  * scatters use fp32 atomics, so results match the reference within an fp32 tolerance (not
  * bit-exact).  Single-shard banks only. */
 typedef struct ngram_grad ngram_grad;
@@ -273,8 +274,8 @@ int ngram_grad_create(ngram_bank* bank, ngram_grad** out); /* zero-initialised *
  * reference to ~1e-3 relative (training precision), not the 1e-5 fp32 contract. */
 #define NGRAM_GRAD_TF32 2
 /* NGRAM_GRAD_PEDANTIC: the two backward GEMMs as pedantic fp32 (CUDA cores).  The default
- * runs them as two-term TF32 on the tensor cores: X and W_cat are bf16 values (exact in TF32),
- * U = U_hi + U_lo is split so both products are fp32-accurate (the default tolerance holds). */
+ * runs them fp32-accurate on the tensor cores: X and W_cat are bf16 values, U is split into
+ * three bf16 terms (two TF32 terms on CUDA-core-shaped banks), the default tolerance holds. */
 #define NGRAM_GRAD_PEDANTIC 4
 int ngram_grad_create_ex(ngram_bank* bank, int flags, ngram_grad** out);
 /* Row-sparse gradient view: rows = dev int32 [count] storage rows (the device layout of

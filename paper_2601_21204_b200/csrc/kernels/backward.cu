@@ -197,6 +197,21 @@ __global__ void split_tf32_copy_kernel(const float* __restrict__ a, float* __res
     }
 }
 
+// u -> u1 + u2 + u3, three bf16 terms (round to nearest each): 24 mantissa bits, |u - sum| ~2^-25 |u|
+__global__ void split_bf16x3_kernel(const float* __restrict__ u, __nv_bfloat16* __restrict__ u1,
+                                    __nv_bfloat16* __restrict__ u2, __nv_bfloat16* __restrict__ u3, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float x = u[i];
+        const __nv_bfloat16 a = __float2bfloat16_rn(x);
+        const float r1 = x - __bfloat162float(a);
+        const __nv_bfloat16 b = __float2bfloat16_rn(r1);
+        const float r2 = r1 - __bfloat162float(b);
+        u1[i] = a;
+        u2[i] = b;
+        u3[i] = __float2bfloat16_rn(r2);
+    }
+}
+
 int grid_for(int64_t n, int threads) {
     int64_t g = (n + threads - 1) / threads;
     if (g > 148 * 16) g = 148 * 16;
@@ -245,6 +260,13 @@ void launch_rows_to_coo(const Shape& s, const int32_t* grow, int64_t Tpad, int64
                         const unsigned long long* err, cudaStream_t st) {
     if (T <= 0 || s.B == 0) return;
     rows_to_coo_kernel<<<grid_for(T * s.B, 256), 256, 0, st>>>(grow, Tpad, T, s.B, rows, err);
+    count_launch();
+}
+
+void launch_split_bf16x3(const float* u, __nv_bfloat16* u1, __nv_bfloat16* u2, __nv_bfloat16* u3, int64_t n,
+                         cudaStream_t st) {
+    if (n <= 0) return;
+    split_bf16x3_kernel<<<grid_for(n, 256), 256, 0, st>>>(u, u1, u2, u3, n);
     count_launch();
 }
 

@@ -83,6 +83,9 @@ void launch_bf16_to_f32(const __nv_bfloat16* src, float* dst, int64_t n, cudaStr
 // u <- TF32-rounded u (round to nearest), lo <- the fp32 remainder (two-term TF32 GEMMs)
 void launch_split_tf32(float* u, float* lo, int64_t n, cudaStream_t st);
 void launch_split_tf32_copy(const float* a, float* hi, float* lo, int64_t n, cudaStream_t st);
+// u -> u1 + u2 + u3 in bf16 (three-term split for bf16 tensor-core GEMMs with fp32-level accuracy)
+void launch_split_bf16x3(const float* u, __nv_bfloat16* u1, __nv_bfloat16* u2, __nv_bfloat16* u3, int64_t n,
+                         cudaStream_t st);
 void launch_rows_to_coo(const Shape& s, const int32_t* grow, int64_t Tpad, int64_t T, int32_t* rows,
                         const unsigned long long* err, cudaStream_t st);
 
