@@ -26,9 +26,9 @@ using namespace ngh;
 struct ngram_grad {
     ngram_bank* bank = nullptr;
     DevBuf<float> e0, sub, w, gain, bias;  // gradients, device layout
-    DevBuf<float> U, X, dX, wf, Ulo;       // workspaces (Ulo: TF32 remainder of U)
+    DevBuf<float> U, X, dX, wf;            // workspaces
     DevBuf<__nv_bfloat16> X16, Ub;         // bf16x3 mode: bf16 X and the three bf16 terms of U
-    int gemm_mode = 0;                     // 0 two-term TF32 (default), 1 TF32, 2 pedantic fp32
+    int gemm_mode = 0;                     // 0 split-bf16 (default), 1 TF32, 2 pedantic fp32
     DevBuf<int32_t> grow;
     int64_t cap = 0;
     bool sparse = false;                 // NGRAM_GRAD_SPARSE_ROWS
@@ -108,7 +108,9 @@ int ngram_grad_create_ex(ngram_bank* b, int flags, ngram_grad** out) {
         g->bias.alloc(size_t(s.D));
     }
     check_blas(cublasCreate(&g->blas), "cublasCreate");
-    g->gemm_mode = (flags & NGRAM_GRAD_TF32) ? 1 : (flags & NGRAM_GRAD_PEDANTIC) ? 2 : 0;
+    // 0: split-bf16 tensor-core GEMMs (tensor-core banks: X and W_cat are bf16), 1: TF32,
+    // 2: pedantic fp32 (also the default on CUDA-core-shaped banks)
+    g->gemm_mode = (flags & NGRAM_GRAD_TF32) ? 1 : ((flags & NGRAM_GRAD_PEDANTIC) || !b->tc_path) ? 2 : 0;
     check_blas(cublasSetMathMode(g->blas, g->gemm_mode == 2 ? CUBLAS_PEDANTIC_MATH : CUBLAS_TF32_TENSOR_OP_MATH),
                "cublasSetMathMode");
     zero_all(g.get(), nullptr);
@@ -156,7 +158,6 @@ int ngram_embed_backward(ngram_grad* g, const uint32_t* tokens, const int64_t* s
         if (s.variant == 1 && B > 0) {
             g->X.alloc(size_t(Tpad) * size_t(D));
             g->dX.alloc(size_t(Tpad) * size_t(D));
-            if (g->gemm_mode == 0) g->Ulo.alloc(size_t(Tpad) * size_t(D));
         }
         g->grow.alloc(size_t(std::max(B, 1)) * size_t(Tpad));
         g->cap = Tpad;
@@ -165,11 +166,10 @@ int ngram_embed_backward(ngram_grad* g, const uint32_t* tokens, const int64_t* s
     ngk::launch_hash_ids(s, b->ht.p, tokens, seq_offsets, nseq, T, prior, nullptr, 0, g->grow.p, g->cap, b->err.p, st);
     ngk::launch_amp_backward(s, upstream, merged, tokens, T, amp, b->ln_gain.p, g->U.p, g->e0.p, g->gain.p,
                              g->bias.p, b->err.p, st);
-    // Default on tensor-core banks: three-term bf16.  X and W_cat are bf16 already, U = u1 + u2
-    // + u3 in bf16 (24 mantissa bits): six bf16 tensor-core GEMMs with fp32 accumulation give
-    // fp32-level products, 17 % faster than two-term TF32 at config C (NGRAM_GRAD_BF16X3=0: TF32).
-    static const bool bf16x3 = !(getenv("NGRAM_GRAD_BF16X3") && atoi(getenv("NGRAM_GRAD_BF16X3")) == 0);
-    if (B > 0 && s.variant == 1 && bf16x3 && g->gemm_mode == 0 && b->tc_path) {
+    // Default on tensor-core banks: X and W_cat are bf16 already, U = u1 + u2 + u3 in bf16 (24
+    // mantissa bits): six bf16 tensor-core GEMMs with fp32 accumulation give fp32-level products
+    // (a two-term TF32 split was measured 25x less accurate at K = 3072 and slower).
+    if (B > 0 && s.variant == 1 && g->gemm_mode == 0) {
         const size_t n = size_t(T) * size_t(D);
         g->X16.ensure(n);
         g->Ub.ensure(3 * n);
@@ -203,22 +203,15 @@ int ngram_embed_backward(ngram_grad* g, const uint32_t* tokens, const int64_t* s
         ngk::launch_bf16_to_f32(b->wcat.p, g->wf.p, int64_t(D) * D, st);
         check_blas(cublasSetStream(g->blas, st), "cublasSetStream");
         const float one = 1.0f, zero = 0.0f;
-        // Default: two-term TF32.  X (gathered bf16 rows) and W_cat (bf16) are exact in TF32, so
-        // splitting only U = U_hi + U_lo (U_hi TF32-exact, U_lo's TF32 rounding ~2^-21 |U|)
-        // makes both products fp32-accurate on the tensor cores with two GEMMs each.
-        const bool two = g->gemm_mode == 0;
-        if (two) ngk::launch_split_tf32(g->U.p, g->Ulo.p, int64_t(T) * D, st);
         // row-major M (r x c) is column-major M^T with ld = c.
         // g_W (D x D, row-major [i][k]) += U^T X  <=>  col-major g_W^T = X_cm * U_cm^T
-        for (int h = 0; h < (two ? 2 : 1); ++h)
-            check_blas(cublasSgemm(g->blas, CUBLAS_OP_N, CUBLAS_OP_T, D, D, int(T), &one, g->X.p, D,
-                                   h ? g->Ulo.p : g->U.p, D, &one, g->w.p, D),
-                       "cublasSgemm(dW)");
+        check_blas(cublasSgemm(g->blas, CUBLAS_OP_N, CUBLAS_OP_T, D, D, int(T), &one, g->X.p, D, g->U.p, D, &one,
+                               g->w.p, D),
+                   "cublasSgemm(dW)");
         // dX (T x D) = U W_cat  <=>  col-major dX^T = W_cm * U_cm
-        for (int h = 0; h < (two ? 2 : 1); ++h)
-            check_blas(cublasSgemm(g->blas, CUBLAS_OP_N, CUBLAS_OP_N, D, int(T), D, &one, g->wf.p, D,
-                                   h ? g->Ulo.p : g->U.p, D, h ? &one : &zero, g->dX.p, D),
-                       "cublasSgemm(dX)");
+        check_blas(cublasSgemm(g->blas, CUBLAS_OP_N, CUBLAS_OP_N, D, int(T), D, &one, g->wf.p, D, g->U.p, D, &zero,
+                               g->dX.p, D),
+                   "cublasSgemm(dX)");
         if (g->sparse) {  // dX is [T][B][d]: exactly the appended values, rows transposed from grow
             sparse_reserve(g, T * B, d, st);
             NGH_CUDA(cudaMemcpyAsync(g->sp_vals.p + size_t(g->sp_count) * size_t(d), g->dX.p,

@@ -26,8 +26,8 @@ struct ngram_plne {
     DevBuf<float> h_gate, h_down, h_x, h_y, h_up, h_dgate, h_ddown, h_dx;
     DevBuf<uint32_t> h_tok, h_prior;
     DevBuf<int64_t> h_off;
-    bool three = true;                 // three-term TF32 GEMMs (default) vs pedantic fp32
-    DevBuf<float> ah, al, bh, bl;      // TF32 hi / lo splits of the two GEMM operands
+    bool three = false;                // NGRAM_PLNE_FAST: split-bf16 tensor-core GEMMs
+    DevBuf<__nv_bfloat16> as, bs;      // three bf16 terms of each GEMM operand
     ~ngram_plne() {
         if (blas) cublasDestroy(blas);
     }
@@ -40,10 +40,11 @@ void blas_ok(cublasStatus_t s, const char* what) {
         throw Error(NGRAM_ECUDA, std::string(what) + " failed (cublas status " + std::to_string(int(s)) + ")");
 }
 
-// C = A op B (+ beta C).  Default: three-term TF32 on the tensor cores -- A = Ah + Al and
-// B = Bh + Bl with Ah, Bh TF32-exact; Ah Bh + Ah Bl + Al Bh is fp32-accurate (the dropped Al Bl
-// and the TF32 rounding of the lo terms are ~2^-21 relative).  nA / nB: element counts of the
-// stored operands (split elementwise, whatever the op).  NGRAM_PLNE_PEDANTIC: one fp32 GEMM.
+// C = A op B (+ beta C).  Default: one pedantic fp32 GEMM (CUDA cores; relL2 6e-7 vs fp64 at
+// K = 3072).  NGRAM_PLNE_FAST: on the bf16 tensor cores -- A = a1 + a2 + a3 and B = b1 + b2 + b3
+// in bf16, the six products a_i b_j with i + j <= 4 accumulated in fp32: 2.9x faster, relL2 7e-6
+// vs fp64 at K = 3072 (a three-term TF32 split measured 1.5e-5; tests/test_gpu_plne.py).
+// nA / nB: element counts of the stored operands (split elementwise, whatever the op).
 void gemm(ngram_plne* p, cublasOperation_t ta, cublasOperation_t tb, int m, int n, int k, const float* A, size_t nA,
           int lda, const float* B, size_t nB, int ldb, float beta, float* C, int ldc, cudaStream_t st,
           const char* what) {
@@ -52,15 +53,18 @@ void gemm(ngram_plne* p, cublasOperation_t ta, cublasOperation_t tb, int m, int 
         blas_ok(cublasSgemm(p->blas, ta, tb, m, n, k, &one, A, lda, B, ldb, &beta, C, ldc), what);
         return;
     }
-    p->ah.ensure(nA);
-    p->al.ensure(nA);
-    p->bh.ensure(nB);
-    p->bl.ensure(nB);
-    ngk::launch_split_tf32_copy(A, p->ah.p, p->al.p, int64_t(nA), st);
-    ngk::launch_split_tf32_copy(B, p->bh.p, p->bl.p, int64_t(nB), st);
-    blas_ok(cublasSgemm(p->blas, ta, tb, m, n, k, &one, p->ah.p, lda, p->bh.p, ldb, &beta, C, ldc), what);
-    blas_ok(cublasSgemm(p->blas, ta, tb, m, n, k, &one, p->ah.p, lda, p->bl.p, ldb, &one, C, ldc), what);
-    blas_ok(cublasSgemm(p->blas, ta, tb, m, n, k, &one, p->al.p, lda, p->bh.p, ldb, &one, C, ldc), what);
+    p->as.ensure(3 * nA);
+    p->bs.ensure(3 * nB);
+    ngk::launch_split_bf16x3(A, p->as.p, p->as.p + nA, p->as.p + 2 * nA, int64_t(nA), st);
+    ngk::launch_split_bf16x3(B, p->bs.p, p->bs.p + nB, p->bs.p + 2 * nB, int64_t(nB), st);
+    static const int pairs[6][2] = {{2, 0}, {1, 1}, {0, 2}, {1, 0}, {0, 1}, {0, 0}};  // small terms first
+    for (int q = 0; q < 6; ++q) {
+        const float* bt = &beta;
+        blas_ok(cublasGemmEx(p->blas, ta, tb, m, n, k, &one, p->as.p + size_t(pairs[q][0]) * nA, CUDA_R_16BF, lda,
+                             p->bs.p + size_t(pairs[q][1]) * nB, CUDA_R_16BF, ldb, q ? &one : bt, C, CUDA_R_32F, ldc,
+                             CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT),
+                what);
+    }
 }
 
 void status_ok(int rc) {
@@ -99,7 +103,7 @@ int ngram_plne_create(ngram_bank* b, int d_model, ngram_plne** out) { return ngr
 
 int ngram_plne_create_ex(ngram_bank* b, int d_model, int flags, ngram_plne** out) {
     NGRAM_API_BEGIN
-    if (flags & ~NGRAM_PLNE_PEDANTIC) throw Error(NGRAM_EINVAL, "ngram_plne_create_ex: unknown flags");
+    if (flags & ~NGRAM_PLNE_FAST) throw Error(NGRAM_EINVAL, "ngram_plne_create_ex: unknown flags");
     if (!b || !out) throw Error(NGRAM_EINVAL, "ngram_plne_create: bad argument");
     if (d_model < 1) throw Error(NGRAM_EINVAL, "ple: d_model and hidden must be >= 1");
     if (b->hash_only) throw Error(NGRAM_EINVAL, "bank was created hash-only (NGRAM_BANK_HASH_ONLY)");
@@ -110,9 +114,8 @@ int ngram_plne_create_ex(ngram_bank* b, int d_model, int flags, ngram_plne** out
     p->d_model = d_model;
     p->hidden = b->shape.D;
     blas_ok(cublasCreate(&p->blas), "cublasCreate");
-    p->three = !(flags & NGRAM_PLNE_PEDANTIC);
-    blas_ok(cublasSetMathMode(p->blas, p->three ? CUBLAS_TF32_TENSOR_OP_MATH : CUBLAS_PEDANTIC_MATH),
-            "cublasSetMathMode");
+    p->three = (flags & NGRAM_PLNE_FAST) != 0;
+    blas_ok(cublasSetMathMode(p->blas, p->three ? CUBLAS_DEFAULT_MATH : CUBLAS_PEDANTIC_MATH), "cublasSetMathMode");
     *out = p.release();
     NGRAM_API_END
 }
