@@ -1072,13 +1072,13 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
     }
 }
 
-static int split_s1(int D, int num_sms) {
-    // BN = 128 tiles; split K until one m-tile's grid covers the SMs
+static int split_s1(int D, int num_sms, int mtiles = 1) {
+    // BN = 128 tiles; split K until the m-tiles' grid covers the SMs (one wave)
     const int KB = D / BK;
     const int64_t nN = D / 128;
     int best = 1;
     for (int S = 1; S <= KB; ++S)
-        if (KB % S == 0 && nN * S <= num_sms) best = S;
+        if (KB % S == 0 && nN * mtiles * S <= num_sms) best = S;
     return best;
 }
 
@@ -1093,8 +1093,10 @@ bool small_t_regime(int D, int64_t T, int num_sms) {
 
 int splitk_factor(const FwdArgs& a, int num_sms) {
     // S depends only on D and the regime of T, so every row of a regime is computed
-    // identically (batch-composition invariance within a regime).
-    return split_s1(a.s.D, num_sms);
+    // identically (batch-composition invariance within a regime).  Two sub-regimes: T <= 128
+    // (one m-tile) and 128 < T <= 256 (two m-tiles: half the splits keep the grid at one wave).
+    static const bool by_m = !(getenv("NGRAM_SPLITK_BY_M") && atoi(getenv("NGRAM_SPLITK_BY_M")) == 0);
+    return split_s1(a.s.D, num_sms, (by_m && a.T > 128) ? 2 : 1);
 }
 
 

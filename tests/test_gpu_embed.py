@@ -135,6 +135,27 @@ def test_row_results_independent_of_batch_composition(cuda):
     assert torch.equal(batch, again)  # deterministic
 
 
+def test_split_k_sub_regimes_are_batch_composition_invariant(cuda):
+    """The split-K small-batch GEMM has two sub-regimes (T <= 128 and 128 < T <= 256: the split
+    count depends on D and the sub-regime only).  Within each, a row's result does not depend on
+    the batch; across them, the K summation order differs (tolerance)."""
+    g = gold("embed_tc_none.npz")
+    hb, db = _bank(g, cuda)
+    a, b, c = (O.uniform_tokens(s, 1000, n) for s, n in [(11, 140), (12, 60), (13, 30)])
+
+    def fwd(*parts):
+        toks = np.concatenate(parts)
+        o = np.concatenate([[0], np.cumsum([len(q) for q in parts])])
+        out, _ = G.embed_forward(db, dev_u32(torch, toks, cuda), dev_i64(torch, o, cuda))
+        return out
+
+    alone_a = fwd(a)                                       # T = 140
+    assert torch.equal(fwd(a, b)[:140], alone_a)           # T = 200, same sub-regime
+    alone_c = fwd(c)                                       # T = 30
+    assert torch.equal(fwd(c, b)[:30], alone_c)            # T = 90, same sub-regime
+    assert_rows_close(fwd(c, a)[:30].cpu().numpy(), alone_c.cpu().numpy())  # T = 170: other sub-regime
+
+
 def test_zero_bank_embeds_to_zero(cuda):  # test_embedding.cpp:176-181
     cfg = O.make_default_config(64, 256, 3, 2)
     cfg["amplification"] = "none"
