@@ -159,6 +159,8 @@ def ref():
         L.ref_cache_ring.argtypes = [C.c_void_p, _u32p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint32)]
         L.ref_draft_verify.argtypes = [C.c_void_p, C.c_void_p, _u32p, C.c_int64, C.c_int64, C.c_int64, C.c_int,
                                        _f32p, _u64p]
+        L.ref_embed_positions_f64.argtypes = [C.c_void_p, _u32p, np.ctypeslib.ndpointer(np.int64), C.c_int64,
+                                              np.ctypeslib.ndpointer(np.int64), C.c_int64, C.c_void_p, C.c_void_p]
         _REF = L
     return _REF
 

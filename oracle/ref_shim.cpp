@@ -7,6 +7,7 @@
 //   * generate tests/golden/ (tests/golden/make_golden.py),
 //   * pin oracle/ngram_oracle.c against the reference (tests/test_oracle_golden.py),
 //   * time the reference CPU path for bench.py --impl reference / cpu_baseline.
+#include <algorithm>
 #include <atomic>
 #include <cstdint>
 #include <cstring>
@@ -375,6 +376,33 @@ int ref_embed_sequence_f64(void* h, const uint32_t* tokens, int64_t len, const u
                                                std::span<const token_id>(prior, std::size_t(prior_len)));
         if (rows) std::memcpy(rows, r.rows.data(), r.rows.size() * 8);
         if (merged) std::memcpy(merged, r.merged.data(), r.merged.size() * 8);
+        return 0;
+    } catch (...) {
+        return map_exc();
+    }
+}
+
+// embed_sequence_cached<double> (embedding.hpp:409-429) evaluated at selected positions of a
+// batch, the bank cast to double ONCE (a LongCat/config-B-size bank is ~9 GB in float): position
+// p of sequence s is the single-token call on tokens[p] with prior_context = the (up to) N-1
+// tokens of s before p -- the same window fill_context builds for p in the whole-sequence call
+// (embedding.hpp:391-405).  positions: global indices into tokens; rows / merged: npos x D.
+int ref_embed_positions_f64(void* h, const uint32_t* tokens, const int64_t* seq_offsets, int64_t nseq,
+                            const int64_t* positions, int64_t npos, double* rows, double* merged) {
+    try {
+        auto& bk = static_cast<ref_bank*>(h)->bank;
+        const auto bd = bank_cast<float, double>(bk);
+        const int64_t D = bk.config.dim, ctx = bk.config.max_order - 1;
+        for (int64_t i = 0; i < npos; ++i) {
+            const int64_t p = positions[i];
+            int64_t s = 0;
+            while (s + 1 < nseq && seq_offsets[s + 1] <= p) ++s;
+            const int64_t a = std::max(seq_offsets[s], p - ctx);
+            auto r = embed_sequence_cached<double>(std::span<const token_id>(tokens + p, 1), bd,
+                                                   std::span<const token_id>(tokens + a, std::size_t(p - a)));
+            if (rows) std::memcpy(rows + i * D, r.rows.data(), std::size_t(D) * 8);
+            if (merged) std::memcpy(merged + i * D, r.merged.data(), std::size_t(D) * 8);
+        }
         return 0;
     } catch (...) {
         return map_exc();

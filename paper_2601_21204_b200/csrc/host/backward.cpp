@@ -156,7 +156,7 @@ int ngram_embed_backward(ngram_grad* g, const uint32_t* tokens, const int64_t* s
     if (T > g->cap) {
         g->U.alloc(size_t(Tpad) * size_t(D));
         if (s.variant == 1 && B > 0) {
-            g->X.alloc(size_t(Tpad) * size_t(D));
+            if (g->gemm_mode != 0) g->X.alloc(size_t(Tpad) * size_t(D));  // fp32 X: TF32 / pedantic GEMMs only
             g->dX.alloc(size_t(Tpad) * size_t(D));
         }
         g->grow.alloc(size_t(std::max(B, 1)) * size_t(Tpad));
@@ -171,7 +171,11 @@ int ngram_embed_backward(ngram_grad* g, const uint32_t* tokens, const int64_t* s
     // (a two-term TF32 split was measured 25x less accurate at K = 3072 and slower).
     if (B > 0 && s.variant == 1 && g->gemm_mode == 0) {
         const size_t n = size_t(T) * size_t(D);
+        const size_t had = g->X16.n;
         g->X16.ensure(n);
+        // fresh workspace holds arbitrary bits: zero it once, so that after a bad token (U = 0,
+        // the gather skipped) the products are exact zeros, never 0 * NaN
+        if (g->X16.n != had) NGH_CUDA(cudaMemsetAsync(g->X16.p, 0, g->X16.n * sizeof(*g->X16.p), st));
         g->Ub.ensure(3 * n);
         ngk::launch_gather_rows(s, g->grow.p, g->cap, T, b->sub.p, g->X16.p, b->err.p, st);
         ngk::launch_split_bf16x3(g->U.p, g->Ub.p, g->Ub.p + n, g->Ub.p + 2 * n, int64_t(n), st);

@@ -170,7 +170,7 @@ struct HashCtx {
 void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, int64_t gstride, int64_t T,
                     void* rows, void* merged, int out_bf16, float* ln_scratch, const CUtensorMap* tmap_x,
                     cudaStream_t st, int amp, XBuf* xb, bool allow_splitk, const ngk::DecodeCommit* commit,
-                    const HashCtx* hc = nullptr);
+                    const HashCtx* hc = nullptr, int64_t regime_T = 0);
 bool forward_tokens(ngram_bank* b, const uint32_t* tokens, const int64_t* seq_off, int64_t nseq, int64_t T,
                     const uint32_t* prior, void* rows, void* merged, int out_bf16, cudaStream_t st, int amp,
                     XBuf* xb, int32_t* grow, bool allow_splitk, const ngk::DecodeCommit* commit,

@@ -43,6 +43,16 @@ static bool fused_gather(int D) {
     return env != 0;
 }
 
+// Entry points that gather rows themselves need every row on this device: a row-sharded bank
+// (shard_count > 1) holds only its row block, its forward runs through the shard group.
+static void require_unsharded(const ngram_bank* b, const char* what) {
+    if (b->shard_count != 1)
+        throw Error(NGRAM_EINVAL, std::string(what) + ": the bank is row-sharded (shard_count " +
+                                      std::to_string(b->shard_count) +
+                                      "); its forward runs through the shard group (ngram_shard_scatter_rows + "
+                                      "ngram_shard_project)");
+}
+
 static bool small_t(const ngram_bank* b, int64_t T) { return ngk::small_t_regime(b->shape.D, T, b->num_sms); }
 
 // Small-T split-K GEMM with the hash in its producers (MODE 2), opt-in NGRAM_DECODE_HASH_IN_GEMM=1:
@@ -62,7 +72,7 @@ static bool hash_in_gemm(const ngram_bank* b) {
 void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, int64_t gstride, int64_t T,
                     void* rows, void* merged, int out_bf16, float* ln_scratch, const CUtensorMap* tmap_x,
                     cudaStream_t st, int amp, XBuf* xb, bool allow_splitk, const ngk::DecodeCommit* commit,
-                    const HashCtx* hc) {
+                    const HashCtx* hc, int64_t regime_T) {
     if (b->hash_only) throw Error(NGRAM_EINVAL, "bank was created hash-only (NGRAM_BANK_HASH_ONLY)");
     if (b->tc_path && ((reinterpret_cast<uintptr_t>(rows) | reinterpret_cast<uintptr_t>(merged)) & 15) != 0)
         throw Error(NGRAM_EINVAL, "output buffers must be 16-byte aligned (tensor-core path: vector / TMA stores)");
@@ -86,6 +96,8 @@ void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, 
     a.tmap_w2 = &b->tmap_w2;
     a.tmap_x = tmap_x;
     a.commit = commit;
+    const int64_t rT = regime_T > 0 ? regime_T : T;  // the T whose kernel regime this call follows
+    a.regime_T = rT;
     const bool ln = a.s.amp == 2;
     float* ln_merged = nullptr;
     if (ln) {
@@ -102,7 +114,7 @@ void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, 
         a.seq_off = hc->seq_off;
         a.nseq = hc->nseq;
         a.prior = hc->prior;
-    } else if (b->tc_path && !tmap_x && ((allow_splitk && small_t(b, T)) || !fused_gather(b->shape.D))) {
+    } else if (b->tc_path && !tmap_x && ((allow_splitk && small_t(b, rT)) || !fused_gather(b->shape.D))) {
         if (!xb) xb = &b->ws.xbuf;
         xb->ensure(round_up(T, kRowPad), b->shape.D);
         ngk::launch_gather_rows(a.s, grow, gstride, T, b->sub.p, xb->x.p, b->err.p, st);
@@ -111,7 +123,7 @@ void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, 
     b->prof_record(2, st);
     // output maps for the pair kernel's TMA epilogue (prefill tiling: not the split-K path)
     CUtensorMap map_rows, map_merged;
-    if (b->tc_path && b->shape.D % 256 == 0 && (!small_t(b, T) || !allow_splitk)) {
+    if (b->tc_path && b->shape.D % 256 == 0 && (!small_t(b, rT) || !allow_splitk)) {
         const uint64_t D = uint64_t(b->shape.D);
         const bool f32 = !a.out_bf16;
         const uint64_t pitch = D * (f32 ? 4 : 2);
@@ -279,6 +291,7 @@ int ngram_embed_forward(ngram_bank* b, const uint32_t* tokens, const int64_t* se
     if (!b || nseq < 1 || total_tokens < 0 || !seq_offsets || (total_tokens > 0 && !tokens))
         throw Error(NGRAM_EINVAL, "ngram_embed_forward: bad argument");
     if (out_dtype != NGRAM_F32 && out_dtype != NGRAM_BF16) throw Error(NGRAM_EINVAL, "bad out_dtype");
+    require_unsharded(b, "ngram_embed_forward");
     DeviceGuard g(b->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     ensure_workspace(b, total_tokens);
@@ -296,6 +309,7 @@ int ngram_embed_from_ids(ngram_bank* b, const uint32_t* tokens, const uint64_t* 
     NGRAM_API_BEGIN
     if (!b || T < 0 || (T > 0 && (!tokens || !ids || !merged_out)))
         throw Error(NGRAM_EINVAL, "ngram_embed_from_ids: bad argument");
+    require_unsharded(b, "ngram_embed_from_ids");
     DeviceGuard g(b->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     ensure_workspace(b, T);
@@ -336,6 +350,7 @@ int ngram_embed_sequence_host(ngram_bank* b, const uint32_t* tokens, const int64
     NGRAM_API_BEGIN
     if (!b || nseq < 1 || !seq_offsets) throw Error(NGRAM_EINVAL, "ngram_embed_sequence_host: bad argument");
     if (out_dtype != NGRAM_F32 && out_dtype != NGRAM_BF16) throw Error(NGRAM_EINVAL, "bad out_dtype");
+    require_unsharded(b, "ngram_embed_sequence_host");
     const int64_t T = seq_offsets[nseq];
     check_offsets(seq_offsets, nseq, T);
     std::lock_guard<std::mutex> host_lock(b->host_mu);

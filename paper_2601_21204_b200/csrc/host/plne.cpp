@@ -107,6 +107,7 @@ int ngram_plne_create_ex(ngram_bank* b, int d_model, int flags, ngram_plne** out
     if (!b || !out) throw Error(NGRAM_EINVAL, "ngram_plne_create: bad argument");
     if (d_model < 1) throw Error(NGRAM_EINVAL, "ple: d_model and hidden must be >= 1");
     if (b->hash_only) throw Error(NGRAM_EINVAL, "bank was created hash-only (NGRAM_BANK_HASH_ONLY)");
+    if (b->shard_count != 1) throw Error(NGRAM_EINVAL, "ngram_plne_create: row-sharded layer banks are not supported");
     if (b->shape.amp != ngk::kAmpNone) throw Error(NGRAM_EINVAL, "ffn_plne: layer banks use no amplification");
     DeviceGuard dg(b->device);
     auto p = std::make_unique<ngram_plne>();

@@ -22,6 +22,7 @@ struct ngram_shard_group {
     std::vector<void*> ipc_mapped;
     DevBuf<int32_t> grow_all;
     int parity = 0;  // buffer the next scatter writes and the next project reads
+    int64_t regime_T = 0;  // size of the gathered batch of the last scatter: the projection's kernel regime
     ~ngram_shard_group() {
         for (void* p : ipc_mapped) cudaIpcCloseMemHandle(p);
     }
@@ -122,6 +123,7 @@ int ngram_shard_scatter_rows(ngram_shard_group* g, const uint32_t* all_tokens, c
     const int64_t Tpad = round_up(std::max<int64_t>(all_T, 1), kRowPad);
     g->grow_all.ensure(size_t(b->shape.B) * size_t(Tpad));
     reset_error_word(b, st);
+    g->regime_T = all_T;
     if (all_T == 0) NGRAM_API_RETURN_OK;
     ngk::launch_hash_ids(b->shape, b->ht.p, all_tokens, all_seq_offsets, all_nseq, all_T, all_prior, nullptr, 0,
                          g->grow_all.p, Tpad, b->err.p, st);
@@ -141,11 +143,13 @@ int ngram_shard_project(ngram_shard_group* g, const uint32_t* home_tokens, int64
     DeviceGuard dg(b->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     XBuf& xb = g->x[g->parity];
-    // small home batches (sharded decode / verify) take the split-K GEMM, as the unsharded
-    // decode path does: the same regime as the single-GPU result for the same rows
+    // The kernel regime (pair GEMM vs split-K, and the split-K sub-regime) follows the GATHERED
+    // batch of the preceding scatter, not home_T: the 1-GPU call over the same streams sees that
+    // T, so every row is computed with the same K split and summation order (bit-identical).
+    const int64_t rT = g->regime_T > 0 ? g->regime_T : home_T;
     run_projection(b, home_tokens, nullptr, round_up(std::max<int64_t>(home_T, 1), kRowPad), home_T, rows_out,
                    merged_out, out_dtype == NGRAM_BF16, b->ws.merged_f32.p, &xb.map, st, -1, nullptr,
-                   ngk::small_t_regime(b->shape.D, home_T, b->num_sms), nullptr);
+                   ngk::small_t_regime(b->shape.D, rT, b->num_sms), nullptr, nullptr, rT);
     g->parity ^= 1;
     NGRAM_API_END
 }

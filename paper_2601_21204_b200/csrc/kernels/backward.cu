@@ -36,8 +36,14 @@ __global__ void __launch_bounds__(kBwdWarps * 32) amp_backward_kernel(
     float* __restrict__ g_e0, float* __restrict__ g_gain, float* __restrict__ g_bias,
     const unsigned long long* __restrict__ err) {
     extern __shared__ float s_ln[];  // [2][D] gain / bias partials (layer_norm only)
-    if (*err != ~0ull) return;       // a bad token: no gradient is produced (hashing.cpp:49-54)
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (*err != ~0ull) {  // a bad token: no gradient is produced (hashing.cpp:49-54)
+        // U = 0, so the dense products that follow (library or own GEMMs, which may not read the
+        // error word) add exact zeros to the W_cat gradient instead of stale workspace contents
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < T * D; i += (int64_t)gridDim.x * blockDim.x)
+            U[i] = 0.0f;
+        return;
+    }
     if (amp == kAmpLN) {
         for (int i = threadIdx.x; i < 2 * D; i += blockDim.x) s_ln[i] = 0.0f;
         __syncthreads();
@@ -98,14 +104,15 @@ __global__ void __launch_bounds__(kBwdWarps * 32) amp_backward_kernel(
 __global__ void gather_rows_f32_scalar_kernel(const int32_t* __restrict__ grow, int64_t Tpad, int64_t T, int B, int d,
                                               const __nv_bfloat16* __restrict__ sub, float* __restrict__ X,
                                               const unsigned long long* __restrict__ err) {
-    if (*err != ~0ull) return;
+    const bool bad = *err != ~0ull;  // X = 0 then: the GEMMs after it must add exact zeros
     const int64_t n = T * B * d;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int j = (int)(i % d);
         const int64_t tb = i / d;
         const int b = (int)(tb % B);
         const int64_t t = tb / B;
-        X[i] = __bfloat162float(sub[(int64_t)grow[(int64_t)b * Tpad + t] * d + j]);
+        const int32_t row = bad ? -1 : grow[(int64_t)b * Tpad + t];
+        X[i] = row >= 0 ? __bfloat162float(sub[(int64_t)row * d + j]) : 0.0f;
     }
 }
 
@@ -113,7 +120,7 @@ __global__ void gather_rows_f32_scalar_kernel(const int32_t* __restrict__ grow, 
 __global__ void gather_rows_f32_kernel(const int32_t* __restrict__ grow, int64_t Tpad, int64_t T, int B, int d,
                                        const __nv_bfloat16* __restrict__ sub, float* __restrict__ X,
                                        const unsigned long long* __restrict__ err) {
-    if (*err != ~0ull) return;
+    const bool bad = *err != ~0ull;  // X = 0 then: the GEMMs after it must add exact zeros
     const int per_row = d / 8;
     const int64_t n = T * B * per_row;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -121,8 +128,9 @@ __global__ void gather_rows_f32_kernel(const int32_t* __restrict__ grow, int64_t
         const int64_t tb = i / per_row;
         const int b = (int)(tb % B);
         const int64_t t = tb / B;
-        const int32_t row = grow[(int64_t)b * Tpad + t];
-        const uint4 v = *reinterpret_cast<const uint4*>(sub + (int64_t)row * d + c * 8);
+        const int32_t row = bad ? -1 : grow[(int64_t)b * Tpad + t];
+        const uint4 v = row >= 0 ? *reinterpret_cast<const uint4*>(sub + (int64_t)row * d + c * 8)
+                                 : make_uint4(0u, 0u, 0u, 0u);
         const uint32_t w[4] = {v.x, v.y, v.z, v.w};
         float* dst = X + t * (int64_t)B * d + (int64_t)b * d + c * 8;
         float4 lo, hi;

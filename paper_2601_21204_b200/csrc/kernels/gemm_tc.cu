@@ -1096,7 +1096,8 @@ int splitk_factor(const FwdArgs& a, int num_sms) {
     // identically (batch-composition invariance within a regime).  Two sub-regimes: T <= 128
     // (one m-tile) and 128 < T <= 256 (two m-tiles: half the splits keep the grid at one wave).
     static const bool by_m = !(getenv("NGRAM_SPLITK_BY_M") && atoi(getenv("NGRAM_SPLITK_BY_M")) == 0);
-    return split_s1(a.s.D, num_sms, (by_m && a.T > 128) ? 2 : 1);
+    const int64_t rt = a.regime_T > 0 ? a.regime_T : a.T;
+    return split_s1(a.s.D, num_sms, (by_m && rt > 128) ? 2 : 1);
 }
 
 
@@ -1116,14 +1117,14 @@ static bool pdl_enabled() {
 }
 
 size_t splitk_workspace_floats(const FwdArgs& a, int num_sms) {
-    if (!small_t_regime(a.s.D, a.T, num_sms) || (a.tmap_x == nullptr && a.seq_off == nullptr)) return 0;
+    if (!small_t_regime(a.s.D, a.regime_T > 0 ? a.regime_T : a.T, num_sms) || (a.tmap_x == nullptr && a.seq_off == nullptr)) return 0;
     const int S = splitk_factor(a, num_sms);
     return S > 1 ? (size_t)S * (size_t)a.T * (size_t)a.s.D : 0;
 }
 
 void launch_forward_tc(const FwdArgs& a, int num_sms, cudaStream_t st, float* splitk_ws) {
     if (a.T <= 0) return;
-    if (splitk_ws && small_t_regime(a.s.D, a.T, num_sms) && (a.tmap_x != nullptr || a.seq_off != nullptr)) {
+    if (splitk_ws && small_t_regime(a.s.D, a.regime_T > 0 ? a.regime_T : a.T, num_sms) && (a.tmap_x != nullptr || a.seq_off != nullptr)) {
         const int S = splitk_factor(a, num_sms);
         if (S > 1) {
             const bool pdl = pdl_enabled();

@@ -132,6 +132,9 @@ struct FwdArgs {
     const int64_t* seq_off;
     int64_t nseq;
     const uint32_t* prior;
+    // T that selects the split-K sub-regime (0 = T): a row-sharded projection of home_T rows
+    // takes the regime of the gathered batch, so its rows are computed as the 1-GPU call's
+    int64_t regime_T;
 };
 // tcgen05 projection GEMM with fused gather + base add + scale + amplify (gemm_tc.cu).
 // splitk_ws (fp32, splitk_workspace_floats() long, may be null): small-T split-K path.

@@ -132,7 +132,9 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const int32_t* __restr
                 const int64_t t = rowv / B;
                 const int b = (int)(rowv - t * B);
                 const int32_t row = __ldg(grow + (int64_t)b * Tpad + t);
-                val[u] = __ldg(reinterpret_cast<const uint4*>(sub + (int64_t)row * d) + c);
+                // row < 0: not stored on this shard -- a zero row, never an out-of-bounds read
+                val[u] = row >= 0 ? __ldg(reinterpret_cast<const uint4*>(sub + (int64_t)row * d) + c)
+                                  : make_uint4(0u, 0u, 0u, 0u);
                 dst[u] = (t * (int64_t)B * d + (int64_t)b * d) / 8 + c;
             }
         }

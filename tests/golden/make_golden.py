@@ -352,8 +352,143 @@ def analysis_goldens():
              buckets=np.array([st["distinct_buckets"][(o, m)] for o in orders for m in moduli], np.uint64))
 
 
+def _bf16_bits(a):
+    """float32 values that are bf16-exact -> their uint16 bf16 bit patterns."""
+    u = np.ascontiguousarray(a, np.float32).view(np.uint32)
+    assert not (u & 0xFFFF).any()
+    return (u >> 16).astype(np.uint16)
+
+
+def _prefixed_streams(rng, n, v0, max_prefix=6):
+    """n decode streams, each primed by 0..max_prefix appended tokens: (prefix matrix, lengths)."""
+    lens = rng.integers(0, max_prefix + 1, size=n)
+    pref = np.zeros((n, max_prefix), np.uint32)
+    for s in range(n):
+        pref[s, :lens[s]] = rng.integers(0, v0, size=lens[s])
+    return pref, lens.astype(np.int64)
+
+
+def _ref_stream_cases(cfg, hb, pref, lens, draft, accept):
+    """Per stream: reference sequence_cache fed the prefix (cache.cpp:37-57), then draft_verify
+    (cache.cpp:152-195) with a fresh memo.  Returns accepted rows (concatenated in stream order),
+    and the rings / lengths / last tokens afterwards."""
+    n, L = draft.shape
+    D = cfg["dim"]
+    acc_rows, rings, lengths, lasts = [], [], [], []
+    pid = np.zeros(64, np.uint64)
+    for s in range(n):
+        ch = R.ref_cache_create(json.dumps(cfg).encode())
+        for t in pref[s, :lens[s]]:
+            assert R.ref_cache_append(ch, int(t), pid) == 0
+        out = np.zeros((max(int(accept[s]), 1), D), np.float32)
+        cnt8 = np.zeros(8, np.uint64)
+        assert R.ref_draft_verify(ch, hb, np.ascontiguousarray(draft[s]), L, int(accept[s]), 4096, 0, out, cnt8) == 0
+        acc_rows.append(out[:int(accept[s])])
+        ring = np.zeros(cfg["max_order"] - 1, np.uint32)
+        length, last = C.c_uint64(), C.c_uint32()
+        R.ref_cache_ring(ch, ring, C.byref(length), C.byref(last))
+        rings.append(ring)
+        lengths.append(length.value)
+        lasts.append(last.value)
+        R.ref_cache_destroy(ch)
+    return (np.concatenate(acc_rows), np.stack(rings), np.array(lengths, np.uint64), np.array(lasts, np.uint32))
+
+
+def r2_goldens():
+    """Round-2 fixtures: the regimes and banks the round-1 goldens did not reach.
+    12. D=3072 prefix calls of T = 129 / 200 / 256 (the split-K GEMM's second sub-regime).
+    13. verify block + commit at D=3072, 64 streams x 4 drafts (config E shape; T = 256).
+    14. decode step at D=3072 with 256 streams (config D's largest batch; T = 256).
+    15. config A's actual bank make_bank(make_default_config(32000, 256, 3, 2), 1234), full 4 x 512.
+    16. config B's actual bank make_bank(make_default_config(128000, 768, 4, 4), 1234), 16 x 4096
+        tokens, 128 sampled positions (with the bank rows they touch).
+    17. Barrett fast-path edge: V0 = 2^32 - 5, moduli in (2^31, 2^32]."""
+    # 12
+    cfgW = ref_default_config(1000, 3072, 4, 4)
+    hb = ref_bank(cfgW, 1234)
+    toks = O.uniform_tokens(23, 1000, 256)
+    _, _, r64, m64 = ref_embed(hb, [toks], None, D=3072)
+    save("regime2_d3072.npz", config=json.dumps(cfgW), seed=1234, tokens=toks, rows_f64_f32=r64.astype(np.float32),
+         bank_checksum=np.uint64(bank_checksum_ref(hb, cfgW)),
+         source="embed_sequence_cached<double> (embedding.hpp:409-429), rows rounded to f32")
+    R.ref_bank_destroy(hb)
+
+    # 13 / 14: the cache path (amplification none: merged vectors, cache.hpp:122-124)
+    cfgE = dict(ref_default_config(1000, 3072, 4, 4), amplification="none")
+    hb = ref_bank(cfgE, 1234)
+    rng = np.random.default_rng(2027)
+    pref, lens = _prefixed_streams(rng, 64, 1000)
+    draft = rng.integers(0, 1000, size=(64, 4), dtype=np.uint32)
+    accept = rng.integers(0, 5, size=64)
+    accept[:3] = [0, 4, 4]
+    acc, rings, lengths, lasts = _ref_stream_cases(cfgE, hb, pref, lens, draft, accept)
+    save("verify_d3072_64x4.npz", config=json.dumps(cfgE), seed=1234, prefix=pref, prefix_len=lens, draft=draft,
+         accept=accept.astype(np.int64), accepted=acc, ring=rings, length=lengths, last=lasts,
+         source="sequence_cache::append + draft_verify (cache.cpp:37-57, 152-195), float path")
+    pref, lens = _prefixed_streams(rng, 256, 1000)
+    step = rng.integers(0, 1000, size=(256, 1), dtype=np.uint32)
+    acc, rings, lengths, lasts = _ref_stream_cases(cfgE, hb, pref, lens, step, np.ones(256, np.int64))
+    save("decode_d3072_b256.npz", config=json.dumps(cfgE), seed=1234, prefix=pref, prefix_len=lens, token=step[:, 0],
+         merged=acc, ring=rings, length=lengths, last=lasts,
+         source="sequence_cache::append + draft_verify(accept = L = 1) (cache.cpp:152-195), float path")
+    R.ref_bank_destroy(hb)
+
+    # 15
+    cfgA = ref_default_config(32000, 256, 3, 2)
+    hb = ref_bank(cfgA, 1234)
+    toksA = O.uniform_tokens(42, 32000, 4 * 512)
+    _, _, r64, m64 = ref_embed(hb, [toksA[i * 512:(i + 1) * 512] for i in range(4)], None, D=256)
+    save("cfgA_bank_embed.npz", config=json.dumps(cfgA), seed=1234, tokens=toksA, seq_len=512,
+         rows_f64_f32=r64.astype(np.float32), bank_checksum=np.uint64(bank_checksum_ref(hb, cfgA)),
+         source="make_bank<float>(config A, 1234) bf16-rounded; embed_sequence_cached<double>")
+    R.ref_bank_destroy(hb)
+
+    # 16
+    cfgB = ref_default_config(128000, 768, 4, 4)
+    hb = ref_bank(cfgB, 1234)
+    N, K, D, B, d, v, denom = O.shape(cfgB)
+    toksB = O.uniform_tokens(42, 128000, 16 * 4096)
+    off = np.arange(0, 16 * 4096 + 1, 4096, dtype=np.int64)
+    rs = np.random.default_rng(16)
+    pos = np.unique(np.concatenate([[0, 1, 2, 3, 4095, 4096, 4097, 4098, 65535],
+                                    rs.choice(65536, size=119, replace=False)]))[:128].astype(np.int64)
+    rows = np.zeros((len(pos), D), np.float64)
+    merged = np.zeros((len(pos), D), np.float64)
+    assert R.ref_embed_positions_f64(hb, toksB, off, 16, pos, len(pos), rows.ctypes.data, merged.ctypes.data) == 0, \
+        R.ref_last_error()
+    ids = np.concatenate([ref_hash_sequences(cfgB, [toksB[off[s]:off[s + 1]]]) for s in range(16)])[pos]
+    base = ref_tensor(hb, 0).reshape(-1, D)
+    sub_rows = np.stack([ref_tensor(hb, 1, b).reshape(-1, d)[ids[:, b].astype(np.int64)] for b in range(B)], axis=1)
+    proj = np.stack([ref_tensor(hb, 2, b) for b in range(B)])
+    save("cfgB_sampled.npz", config=json.dumps(cfgB), seed=1234, tokens=toksB, seq_offsets=off, positions=pos,
+         ids=ids, e0_rows_bf16=_bf16_bits(base[toksB[pos]]), sub_rows_bf16=_bf16_bits(sub_rows),
+         proj_bf16=_bf16_bits(proj), rows_f64_f32=rows.astype(np.float32), merged_f64_f32=merged.astype(np.float32),
+         bank_checksum=np.uint64(bank_checksum_ref(hb, cfgB)),
+         source="make_bank<float>(config B, 1234) bf16-rounded; embed_sequence_cached<double> at sampled positions")
+    R.ref_bank_destroy(hb)
+
+    # 17: products up to (2^32-1)^2 -- the Barrett quotient's worst case (hashdev.cuh barrett_mod)
+    v0 = (1 << 32) - 5
+    moduli = [(1 << 31) + 1, 3000000019, (1 << 32) - 5, (1 << 32) - 1, 1 << 32, (1 << 32) - 65,
+              (1 << 31) + 11, 4000000007, 3 * (1 << 30)]
+    cfgX = O.make_config(v0, 18, 4, 3, moduli, "subtable_v2", "none")
+    rx = np.random.default_rng(17)
+    edge = np.array([0, 1, v0 - 1, v0 - 2, (1 << 31), (1 << 31) + 1, (1 << 31) - 1, 3000000018, 3000000019,
+                     (1 << 32) - 6, (1 << 32) - 66, (1 << 32) - 65, 4000000006], np.uint64)
+    seqs = [rx.integers(0, v0, size=700, dtype=np.uint64).astype(np.uint32),
+            rx.choice(edge, size=500).astype(np.uint32),
+            rx.integers(v0 - 1000, v0, size=300, dtype=np.uint64).astype(np.uint32),
+            np.concatenate([rx.choice(edge, size=100), rx.integers(0, v0, size=100, dtype=np.uint64)]).astype(np.uint32)]
+    tk = np.concatenate(seqs)
+    so = np.concatenate([[0], np.cumsum([len(q) for q in seqs])]).astype(np.int64)
+    save("barrett_edge_ids.npz", config=json.dumps(cfgX), tokens=tk, seq_offsets=so, ids=ref_hash_sequences(cfgX, seqs),
+         source="hash_all_orders (hashing.cpp:61-81) over fill_context windows")
+
+
 if __name__ == "__main__":
-    if sys.argv[1:] == ["backward"]:  # regenerate only section 9
+    if sys.argv[1:] == ["r2"]:  # regenerate only sections 12-17
+        r2_goldens()
+    elif sys.argv[1:] == ["backward"]:  # regenerate only section 9
         backward_goldens()
     elif sys.argv[1:] == ["plne"]:  # regenerate only section 10
         plne_goldens()

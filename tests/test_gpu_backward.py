@@ -68,16 +68,31 @@ def test_skip_amplify_takes_d_merged(cuda):  # embed_backward alone (embedding.h
     assert_grads_close(b.download(), a.download(), ln)
 
 
-def test_out_of_range_token_leaves_gradients_untouched(cuda):  # hashing.cpp:49-54
+@pytest.mark.parametrize("mode", [{}, {"tf32": True}, {"pedantic": True}])
+def test_out_of_range_token_leaves_gradients_untouched(cuda, mode):  # hashing.cpp:49-54
+    """A bad call leaves EVERY gradient -- E0, sub-tables and the projection (W_cat) -- exactly as
+    it was, including after a good call filled the GEMM workspaces with that call's operands."""
     g, cfg, hb, db, args, ln = _setup("backward_tc_none.npz", cuda)
-    gb = G.GradBank(db)
+    gb = G.GradBank(db, **mode)
     bad = args["tokens"].clone()
     bad[77] = cfg["base_vocab"]
-    gb.backward(**dict(args, tokens=bad))
+    gb.backward(**dict(args, tokens=bad))  # first call: fresh (uninitialised) workspaces
     with pytest.raises(OutOfRange):
         db.sync_errors()
     got = gb.download()
     assert not got["base"].any() and not any(x.any() for x in got["sub"])
+    assert not any(x.any() for x in got["proj"])
+    gb.backward(**args)  # a good call, then a bad one: the gradients stay those of the good call
+    db.sync_errors()
+    good = gb.download()
+    gb.backward(**dict(args, tokens=bad))
+    with pytest.raises(OutOfRange):
+        db.sync_errors()
+    after = gb.download()
+    for k in ("base", "sub", "proj"):
+        for x, y in zip(good[k] if isinstance(good[k], list) else [good[k]],
+                        after[k] if isinstance(after[k], list) else [after[k]]):
+            assert np.array_equal(x, y), k
 
 
 def test_forward_then_backward_at_longcat_width(cuda):

@@ -40,3 +40,30 @@ def test_sharded_forward_bit_identical_to_single_gpu(cuda, P, amp):
             assert torch.equal(rows, ref_rows[rank_tok[r]:rank_tok[r + 1]]), (P, r, step)
             assert torch.equal(merged, ref_merged[rank_tok[r]:rank_tok[r + 1]])
         banks[0].sync_errors()
+
+
+@pytest.mark.parametrize("P,home", [(2, 96), (4, 80), (2, 40)])
+def test_sharded_small_batch_follows_the_gathered_batch_regime(cuda, P, home):
+    """A sharded projection of home_T rows runs the kernel regime of the GATHERED batch (the
+    T the 1-GPU call sees): global 192 -> split-K sub-regime 2 although home 96 <= 128; global
+    320 -> the pair GEMM although home 80 <= 256; global 80 -> sub-regime 1.  At D = 3072 the
+    regimes split K differently, so only this choice keeps the result bit-identical."""
+    cfg = O.make_default_config(1000, 3072, 4, 4)
+    full = G.DeviceBank(cfg).generate(5)
+    T = P * home
+    toks = np.random.default_rng(T).integers(0, 1000, size=T).astype(np.uint32)
+    prior = np.random.default_rng(8).integers(0, 1000, size=(T, 3)).astype(np.uint32)
+    off = np.arange(0, T + 1)  # one token per stream (a decode step of T streams)
+    t_all, off_all, pr_all = dev_u32(torch, toks, cuda), dev_i64(torch, off, cuda), dev_u32(torch, prior, cuda)
+    ref_rows, _ = G.embed_forward(full, t_all, off_all, prior=pr_all)
+    rank_tok = [r * home for r in range(P + 1)]
+    banks = [G.DeviceBank(cfg, shard_rank=r, shard_count=P).generate(5) for r in range(P)]
+    groups = [G.ShardGroup(b, home) for b in banks]
+    G.emulate_shards_single_process(groups)
+    for g in groups:
+        g.scatter(t_all, off_all, rank_tok, pr_all)
+    torch.cuda.synchronize()
+    for r, g in enumerate(groups):
+        rows, _ = g.project(t_all[rank_tok[r]:rank_tok[r + 1]])
+        assert torch.equal(rows, ref_rows[rank_tok[r]:rank_tok[r + 1]]), (P, home, r)
+    banks[0].sync_errors()

@@ -18,7 +18,7 @@ GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
 import helpers  # noqa: E402
-from helpers import gold  # noqa: E402
+from helpers import gold, gold_config  # noqa: E402
 
 
 # ---------------------------------------------------------------- hashing (test_hashing.cpp)
@@ -301,3 +301,20 @@ def test_analysis_reference_worked_examples():  # test_analysis.cpp:50-113
     assert coll([[1, 5], [3, 5], [5, 5]], 2, 10, 20) == 2 and coll([[1, 5], [3, 5], [5, 5]], 2, 10, 23) == 0
     assert coll([list(range(1, 10))], 2, 10, 1000000) == 0
     assert O.corpus_analyze(1 << 17, [8], [100], [[1]])[0] == -1  # V0^order beyond 128 bits
+
+
+def test_oracle_hash_matches_reference_at_barrett_edge():  # make_golden.py section 17
+    g = gold("barrett_edge_ids.npz")
+    cfg = gold_config(g)
+    off = g["seq_offsets"]
+    got = np.concatenate([O.hash_sequence(cfg, g["tokens"][off[i]:off[i + 1]]) for i in range(len(off) - 1)])
+    assert np.array_equal(got, g["ids"])
+
+
+def test_oracle_embed_matches_reference_d3072_regime2_rows():  # make_golden.py section 12 (first rows)
+    g = gold("regime2_d3072.npz")
+    cfg = gold_config(g)
+    hb = O.make_bank(cfg, int(g["seed"]), round_bf16=True)
+    assert O.bank_checksum(hb) == int(g["bank_checksum"])
+    rows, _ = O.embed_sequence(hb, g["tokens"][:12], double=True)
+    assert np.allclose(rows, g["rows_f64_f32"][:12], rtol=0, atol=1e-7 * np.abs(rows).max())
