@@ -321,11 +321,9 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        if one_dev:
-            dist.init_process_group("gloo", timeout=_PG_TIMEOUT)
-        else:
-            dist.init_process_group("nccl", device_id=dev, timeout=_PG_TIMEOUT)
+        init_dist(dev, one_dev)
     sharding = args.sharding if world > 1 else "single"
+    exchange = args.exchange
 
     cfg, nseq, seq_len, label = workload(args.workload)
     if nseq % world != 0:
@@ -355,20 +353,20 @@ def run_ours(args):
         # Set-up is agreed collectively: if any rank cannot map its peers (CUDA IPC), every
         # rank falls back to replicas and the JSON line says so.
         ok, why = 1, ""
-        try:
-            bank = G.DeviceBank(cfg, device=local, shard_rank=rank, shard_count=world)
-            bank.generate(1234)
-            group = G.ShardGroup(bank, T)
-            G.connect_shard_groups(group)
-        except Exception as e:  # noqa: BLE001 -- reported, then agreed across ranks
-            ok, why = 0, f"rank {rank}: {type(e).__name__}: {e}"
+        bank = G.DeviceBank(cfg, device=local, shard_rank=rank, shard_count=world)
+        bank.generate(1234)
+        group = G.ShardGroup(bank, T)
+        if exchange == "peer":
+            try:
+                G.connect_shard_groups(group)
+            except Exception as e:  # noqa: BLE001 -- reported, then agreed across ranks
+                ok, why = 0, f"rank {rank}: {type(e).__name__}: {e}"
         flag = torch.tensor([ok], dtype=torch.int32, device=dev)
         dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-        if int(flag.item()) == 0:
-            fallback = why or "a peer rank failed to set up the row-sharded exchange"
-            group = bank = None
+        if int(flag.item()) == 0:  # no peer mappings: the same rows move by NCCL all-to-all instead
+            fallback = (why or "a peer rank failed to map the peer buffers") + "; exchange falls back to NCCL a2a"
+            exchange = "a2a"
             torch.cuda.synchronize()
-            sharding = "replica"
     if sharding == "row":
         all_t = torch.empty(total_tokens, dtype=torch.int32, device=dev)
         all_off = torch.arange(0, total_tokens + 1, seq_len, dtype=torch.int64, device=dev)
@@ -376,16 +374,22 @@ def run_ours(args):
         one = torch.ones(1, dtype=torch.float32, device=dev)
         sev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
 
-        def step(record=False):
+        def step(record=False, xchg=None):
+            xchg = xchg or exchange
             if record:
                 sev[0].record(stream)
             dist.all_gather_into_tensor(all_t, toks)  # 4 B/token
             if record:
                 sev[1].record(stream)
-            group.scatter(all_t, all_off, rank_tok)   # K1 + fused gather / NVLink peer store
-            if record:
-                sev[2].record(stream)
-            dist.all_reduce(one)                      # every rank's rows have landed
+            if xchg == "peer":
+                group.scatter(all_t, all_off, rank_tok)   # K1 + fused gather / NVLink peer store
+                if record:
+                    sev[2].record(stream)
+                dist.all_reduce(one)                      # every rank's rows have landed
+            else:  # K1 + pack, the NCCL collective, unpack (a2a) -- the collective orders the stream
+                group.exchange(xchg, all_t, all_off, rank_tok)
+                if record:
+                    sev[2].record(stream)
             if record:
                 sev[3].record(stream)
             group.project(toks, out_dtype=out_dtype, out_rows=rows)  # K3 on the home X
@@ -444,6 +448,30 @@ def run_ours(args):
         stages = {"all_gather_tokens": st_ms[0], "k1_k2_scatter_nvlink": st_ms[1], "barrier": st_ms[2],
                   "k3_projection_epilogue": st_ms[3]}
         proj_ms = st_ms[3]
+        # every exchange variant on the same tables and tokens (pick by measured
+        # latency): whole-step ms, max over ranks, L2 flushed as above
+        exchange_ms = {}
+        reps = 1 if one_dev else max(3, args.steps)
+        for xv in ("peer", "a2a", "rs"):
+            if xv == "peer" and fallback:
+                continue
+            for _ in range(2):
+                step(xchg=xv)
+            torch.cuda.synchronize()
+            dist.barrier()
+            tt = []
+            for i in range(reps):
+                flush.fill_(i & 0xff)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                step(xchg=xv)
+                e1.record(stream)
+                e1.synchronize()
+                tt.append(e0.elapsed_time(e1))
+            t = torch.tensor([float(np.mean(tt))], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            exchange_ms[xv] = float(t.item())
+        bank.sync_errors()
     else:
         # K1 (hash) and K2 (gather) run fused in one kernel on the X path (stage 1 ~ 0 then)
         stages = {"k1_k2_hash_gather": st_ms[0] + st_ms[1], "k3_projection_epilogue": st_ms[2]}
@@ -462,7 +490,8 @@ def run_ours(args):
             step()
             host_out.copy_(rows, non_blocking=True)
             torch.cuda.current_stream().synchronize()
-        e2e_path = "pinned host tokens -> H2D -> all-gather -> scatter -> barrier -> K3 -> D2H pinned embeddings"
+        e2e_path = ("pinned host tokens -> H2D -> all-gather -> " +
+                    ("scatter -> barrier" if exchange == "peer" else f"NCCL {exchange}") + " -> K3 -> D2H pinned embeddings")
     else:
         def e2e_step():
             abi.check(abi.lib().ngram_embed_sequence_host(bank.handle, C.c_void_p(host_tok.data_ptr()),
@@ -538,6 +567,8 @@ def run_ours(args):
     if one_dev and world > 1:
         line["config"]["one_device_test"] = "all ranks on cuda:0 over gloo (functional only)"
     if sharding == "row":
+        line["config"]["exchange"] = exchange
+        line["exchange_ms"] = exchange_ms
         remote = T * world * B * d * 2 * (world - 1) / world / world  # rows this rank ships to peers
         line["nvlink"] = {"remote_bytes_per_rank": remote, "scatter_ms": st_ms[1],
                           "gbs": remote / (st_ms[1] * 1e-3) / 1e9, "peak_gbs": 770.0,
@@ -620,10 +651,7 @@ def run_decode_sharded(args):
         local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if one_dev:
-        dist.init_process_group("gloo", timeout=_PG_TIMEOUT)
-    else:
-        dist.init_process_group("nccl", device_id=dev, timeout=_PG_TIMEOUT)
+    init_dist(dev, one_dev)
     cfg, _, _, _ = workload("C" if not os.environ.get("NGRAM_BENCH_DECODE_CFG") else os.environ["NGRAM_BENCH_DECODE_CFG"])
     cfg = dict(cfg)
     cfg["amplification"] = "none"  # the cache path returns merged vectors (cache.hpp:122-124)
@@ -644,24 +672,29 @@ def run_decode_sharded(args):
         toks = torch.from_numpy(rng.integers(0, cfg["base_vocab"], size=(B, L)).astype(np.int32)).to(dev)
         acc = torch.from_numpy(rng.integers(0, L + 1, size=B).astype(np.int32)).to(dev)
 
-        def one():
-            G.sharded_verify_block(group, st, toks, out_dtype=torch.bfloat16, barrier=barrier)
+        def one(xv):
+            G.sharded_verify_block(group, st, toks, out_dtype=torch.bfloat16, barrier=barrier, exchange=xv)
             st.commit(toks, acc)
-        for _ in range(args.warmup):
-            one()
-        torch.cuda.synchronize()
-        dist.barrier()
-        n = args.steps * 10
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-        ev[0].record(stream)
-        for _ in range(n):
-            one()
-        ev[1].record(stream)
-        torch.cuda.synchronize()
-        t = torch.tensor([ev[0].elapsed_time(ev[1]) / n], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        res[B] = {"us_per_step": ms * 1e3, "tokens_per_s": world * B * L / (ms * 1e-3)}
+
+        per = {}
+        for xv in [args.exchange] + [v for v in ("peer", "rs", "a2a") if v != args.exchange]:
+            for _ in range(args.warmup):
+                one(xv)
+            torch.cuda.synchronize()
+            dist.barrier()
+            n = args.steps * (1 if one_dev else 10)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            ev[0].record(stream)
+            for _ in range(n):
+                one(xv)
+            ev[1].record(stream)
+            torch.cuda.synchronize()
+            t = torch.tensor([ev[0].elapsed_time(ev[1]) / n], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            per[xv] = float(t.item()) * 1e3
+        us = per[args.exchange]
+        res[B] = {"us_per_step": us, "tokens_per_s": world * B * L / (us * 1e-6), "exchange": args.exchange,
+                  "exchange_us": per}
         st.close()
     bank.sync_errors()
     if rank == 0:
@@ -826,6 +859,37 @@ def run_analysis(args):
     print(json.dumps(line))
 
 
+def spawn_ranks(n: int) -> int:
+    """Re-launch this command as n ranks (torch.distributed.run --nproc-per-node n) and return
+    the launcher's exit code; stdout / stderr stream through (rank 0 prints the JSON line)."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(n),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd, env=env).returncode
+
+
+def init_dist(dev, one_dev: bool):
+    """One process group per run: NCCL over NVLink (one GPU per rank), or gloo when every rank
+    shares cuda:0 (functional tests).  NCCL's communicator-init lines (NCCL_DEBUG=INFO, INIT
+    subsystem) are printed so the rank count of the communicator is visible in the log."""
+    import torch.distributed as dist
+    if one_dev:
+        dist.init_process_group("gloo", timeout=_PG_TIMEOUT)
+        return
+    import torch
+    if torch.cuda.device_count() < int(os.environ.get("WORLD_SIZE", "1")):
+        raise SystemExit(f"--gpus {os.environ.get('WORLD_SIZE')} needs that many GPUs, "
+                         f"this node has {torch.cuda.device_count()}")
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    dist.init_process_group("nccl", device_id=dev, timeout=_PG_TIMEOUT)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -842,9 +906,17 @@ def main():
     ap.add_argument("--draft", type=int, default=8, help="verify block length (workload E)")
     ap.add_argument("--sharding", choices=["row", "replica"], default="row",
                     help="N > 1: row-sharded tables (default) or full replicas")
+    ap.add_argument("--exchange", choices=["peer", "a2a", "rs"], default="peer",
+                    help="row-sharded exchange: NVLink peer stores (default), NCCL all-to-all of the owned rows, "
+                         "or NCCL reduce-scatter of the -0.0-padded X (all bit-identical); the other two are "
+                         "timed too and reported under exchange_ms")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        # `python bench.py --gpus N` with no launcher: start the N ranks here (one process per
+        # GPU, torch.distributed.run on 127.0.0.1) and pass rank 0's line through
+        sys.exit(spawn_ranks(args.gpus))
     if args.impl == "reference":
         run_reference(args)
     elif args.workload == "analysis":

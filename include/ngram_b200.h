@@ -246,6 +246,38 @@ int ngram_shard_scatter_rows(ngram_shard_group* g, const uint32_t* all_tokens, c
 int ngram_shard_project(ngram_shard_group* g, const uint32_t* home_tokens, int64_t home_T, void* rows_out,
                         void* merged_out, int out_dtype, void* stream);
 
+/* NCCL exchange variants of step 2 (SURVEY.md 8(e) "all-to-all of rows" for large
+ * batches, "reduce-scatter of the zero-padded X" for decode / verify).  The caller runs the
+ * collective (NCCL through torch.distributed, or grouped ncclSend/ncclRecv); rows move raw, so
+ * every variant leaves the same home X as the peer-store scatter, bit for bit.  Arguments of the
+ * gathered batch as ngram_shard_scatter_rows.
+ * All-to-all:
+ *   1. ngram_shard_xchg_prepare: K1 over the gathered batch + the exchange counts; synchronises
+ *      `stream`; send_rows[p] / recv_rows[p] (HOST, nranks) = d-wide bf16 rows this rank sends to /
+ *      receives from rank p;
+ *   2. ngram_shard_xchg_pack: the owned rows into `send` (dev, sum(send_rows) x d bf16), grouped
+ *      by destination rank, (token, branch) order within a group;
+ *   3. the all-to-all (send splits send_rows, receive splits recv_rows, rank order);
+ *   4. ngram_shard_xchg_unpack: the received rows (dev, sum(recv_rows) x d) into this rank's home X
+ *      (each row's slot follows from the ids this rank hashed: no index travels with the rows);
+ *   5. ngram_shard_project.
+ * Reduce-scatter:
+ *   1. ngram_shard_pack_padded: `send` (dev, nranks x max_home_tokens x D bf16) = every rank's
+ *      home X with only this rank's rows filled, -0.0 elsewhere (the additive identity, so the sum
+ *      is exact);
+ *   2. reduce-scatter (sum, bf16) of `send` into ngram_shard_home_x (max_home_tokens x D);
+ *   3. ngram_shard_project. */
+int ngram_shard_xchg_prepare(ngram_shard_group* g, const uint32_t* all_tokens, const int64_t* all_seq_offsets,
+                             int64_t all_nseq, int64_t all_tokens_n, const int64_t* rank_token_offsets,
+                             const uint32_t* all_prior, int64_t* send_rows, int64_t* recv_rows, void* stream);
+int ngram_shard_xchg_pack(ngram_shard_group* g, void* send, void* stream);
+int ngram_shard_xchg_unpack(ngram_shard_group* g, const void* recv, void* stream);
+int ngram_shard_pack_padded(ngram_shard_group* g, const uint32_t* all_tokens, const int64_t* all_seq_offsets,
+                            int64_t all_nseq, int64_t all_tokens_n, const int64_t* rank_token_offsets,
+                            const uint32_t* all_prior, void* send, void* stream);
+/* Device pointer of the home X the next ngram_shard_project reads (max_home_tokens x D bf16). */
+int ngram_shard_home_x(ngram_shard_group* g, void** x);
+
 /* amplify (embedding.hpp:239-287) of `rows` HOST rows of width D on the current device:
  * amp_mode 0 none, 1 scale_sqrt_d, 2 layer_norm (gain / bias of size D). Synchronous. */
 int ngram_amplify_host(int amp_mode, int D, int64_t rows, const float* gain, const float* bias, const float* in,

@@ -37,6 +37,8 @@ SYMBOLS = [
     "ngram_decode_get_state",
     "ngram_shard_rows", "ngram_shard_group_create", "ngram_shard_group_destroy", "ngram_shard_export", "ngram_shard_open",
     "ngram_shard_local_buffers", "ngram_shard_set_peer", "ngram_shard_scatter_rows", "ngram_shard_project",
+    "ngram_shard_xchg_prepare", "ngram_shard_xchg_pack", "ngram_shard_xchg_unpack", "ngram_shard_pack_padded",
+    "ngram_shard_home_x",
     "ngram_grad_create", "ngram_grad_destroy", "ngram_grad_zero", "ngram_embed_backward", "ngram_grad_tensor",
     "ngram_grad_download", "ngram_embed_backward_host",
     "ngram_plne_create", "ngram_plne_destroy", "ngram_plne_forward", "ngram_plne_backward",
@@ -152,6 +154,11 @@ def lib() -> C.CDLL:
         "ngram_shard_set_peer": ([vp, i32, vp, vp], i32),
         "ngram_shard_scatter_rows": ([vp, vp, vp, i64, i64, vp, vp, vp], i32),
         "ngram_shard_project": ([vp, vp, i64, vp, vp, i32, vp], i32),
+        "ngram_shard_xchg_prepare": ([vp, vp, vp, i64, i64, vp, vp, vp, vp, vp], i32),
+        "ngram_shard_xchg_pack": ([vp, vp, vp], i32),
+        "ngram_shard_xchg_unpack": ([vp, vp, vp], i32),
+        "ngram_shard_pack_padded": ([vp, vp, vp, i64, i64, vp, vp, vp, vp], i32),
+        "ngram_shard_home_x": ([vp, C.POINTER(vp)], i32),
         "ngram_grad_create": ([vp, C.POINTER(vp)], i32),
         "ngram_grad_destroy": ([vp], i32),
         "ngram_grad_zero": ([vp, vp], i32),

@@ -23,6 +23,13 @@ struct ngram_shard_group {
     DevBuf<int32_t> grow_all;
     int parity = 0;  // buffer the next scatter writes and the next project reads
     int64_t regime_T = 0;  // size of the gathered batch of the last scatter: the projection's kernel regime
+    // NCCL exchange variants (ngram_shard_xchg_*): the prepared step
+    DevBuf<uint64_t> ids_all;                 // [all_T][B] global bucket ids of the gathered batch
+    DevBuf<int64_t> xtot, xchunk, xcoltot;    // scan scratch
+    DevBuf<int64_t> xpref;                    // [1 + nranks][pref_stride] exclusive prefixes
+    DevBuf<int64_t> xbounds;                  // [2 * nranks + 1]
+    int64_t pref_stride = 0, xchg_T = -1;
+    std::vector<int64_t> rank_tok, send_rows, recv_rows;
     ~ngram_shard_group() {
         for (void* p : ipc_mapped) cudaIpcCloseMemHandle(p);
     }
@@ -130,6 +137,128 @@ int ngram_shard_scatter_rows(ngram_shard_group* g, const uint32_t* all_tokens, c
     ngk::launch_shard_scatter(b->shape, g->grow_all.p, Tpad, rank_token_offsets, g->nranks, b->sub.p,
                               g->peer[g->parity], all_T, b->err.p, st);
     NGH_CUDA(cudaGetLastError());
+    NGRAM_API_END
+}
+
+// Shared argument checks of the calls that consume the gathered batch.
+static void check_gathered(ngram_shard_group* g, const uint32_t* all_tokens, const int64_t* all_seq_offsets,
+                           int64_t all_nseq, int64_t all_T, const int64_t* rank_token_offsets, bool peers) {
+    if (!g || !all_tokens || !all_seq_offsets || !rank_token_offsets || all_nseq < 1 || all_T < 0)
+        throw Error(NGRAM_EINVAL, "sharded exchange: bad argument");
+    if (rank_token_offsets[0] != 0 || rank_token_offsets[g->nranks] != all_T)
+        throw Error(NGRAM_EINVAL, "rank_token_offsets must span the gathered batch");
+    for (int r = 0; r < g->nranks; ++r) {
+        if (rank_token_offsets[r + 1] < rank_token_offsets[r] ||
+            rank_token_offsets[r + 1] - rank_token_offsets[r] > g->max_home)
+            throw Error(NGRAM_EINVAL, "a rank's home tokens exceed max_home_tokens");
+        if (peers && !g->peer[g->parity][r]) throw Error(NGRAM_EINVAL, "peer " + std::to_string(r) + " not opened");
+    }
+}
+
+int ngram_shard_xchg_prepare(ngram_shard_group* g, const uint32_t* all_tokens, const int64_t* all_seq_offsets,
+                             int64_t all_nseq, int64_t all_T, const int64_t* rank_token_offsets,
+                             const uint32_t* all_prior, int64_t* send_rows, int64_t* recv_rows, void* stream) {
+    NGRAM_API_BEGIN
+    check_gathered(g, all_tokens, all_seq_offsets, all_nseq, all_T, rank_token_offsets, false);
+    if (!send_rows || !recv_rows) throw Error(NGRAM_EINVAL, "ngram_shard_xchg_prepare: null counts");
+    ngram_bank* b = g->bank;
+    DeviceGuard dg(b->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int P = g->nranks, B = b->shape.B;
+    const int64_t Tpad = round_up(std::max<int64_t>(all_T, 1), kRowPad);
+    g->grow_all.ensure(size_t(B) * size_t(Tpad));
+    g->ids_all.ensure(size_t(std::max<int64_t>(all_T, 1)) * size_t(B));
+    const int64_t nchunks = (all_T + ngk::kXchgChunkTokens - 1) / ngk::kXchgChunkTokens;
+    g->xtot.ensure(size_t(std::max<int64_t>(nchunks, 1)) * size_t(P + 1));
+    g->xchunk.ensure(size_t(std::max<int64_t>(nchunks, 1)) * size_t(P + 1));
+    g->xcoltot.ensure(size_t(P + 1));
+    g->pref_stride = std::max<int64_t>(all_T, 1);
+    g->xpref.ensure(size_t(g->pref_stride) * size_t(P + 1));
+    g->xbounds.ensure(size_t(2 * P + 1));
+    g->rank_tok.assign(rank_token_offsets, rank_token_offsets + P + 1);
+    g->send_rows.assign(size_t(P), 0);
+    g->recv_rows.assign(size_t(P), 0);
+    g->xchg_T = all_T;
+    reset_error_word(b, st);
+    g->regime_T = all_T;
+    if (all_T > 0) {
+        ngk::launch_hash_ids(b->shape, b->ht.p, all_tokens, all_seq_offsets, all_nseq, all_T, all_prior, g->ids_all.p,
+                             1, g->grow_all.p, Tpad, b->err.p, st);
+        ngk::launch_xchg_prepare(b->shape, b->cfg.sub_vocab.data(), g->rank, P, rank_token_offsets, all_T,
+                                 g->ids_all.p, g->xtot.p, g->xchunk.p, g->xcoltot.p, g->xpref.p, g->pref_stride,
+                                 g->xbounds.p, b->err.p, st);
+        std::vector<int64_t> bounds(size_t(2 * P + 1));
+        NGH_CUDA(cudaMemcpyAsync(bounds.data(), g->xbounds.p, bounds.size() * 8, cudaMemcpyDeviceToHost, st));
+        NGH_CUDA(cudaStreamSynchronize(st));
+        for (int p = 0; p < P; ++p) {
+            g->send_rows[size_t(p)] = bounds[size_t(p + 1)] - bounds[size_t(p)];
+            g->recv_rows[size_t(p)] = bounds[size_t(P + 1 + p)];
+        }
+    }
+    std::copy(g->send_rows.begin(), g->send_rows.end(), send_rows);
+    std::copy(g->recv_rows.begin(), g->recv_rows.end(), recv_rows);
+    NGH_CUDA(cudaGetLastError());
+    NGRAM_API_END
+}
+
+int ngram_shard_xchg_pack(ngram_shard_group* g, void* send, void* stream) {
+    NGRAM_API_BEGIN
+    if (!g || g->xchg_T < 0) throw Error(NGRAM_EINVAL, "ngram_shard_xchg_pack: no prepared exchange");
+    ngram_bank* b = g->bank;
+    int64_t total = 0;
+    for (const int64_t n : g->send_rows) total += n;
+    if (total > 0 && !send) throw Error(NGRAM_EINVAL, "ngram_shard_xchg_pack: null send buffer");
+    DeviceGuard dg(b->device);
+    const int64_t Tpad = round_up(std::max<int64_t>(g->xchg_T, 1), kRowPad);
+    ngk::launch_xchg_pack(b->shape, b->cfg.sub_vocab.data(), g->rank, g->nranks, g->xchg_T, g->ids_all.p,
+                          g->grow_all.p, Tpad, g->xpref.p, b->sub.p, static_cast<__nv_bfloat16*>(send), b->err.p,
+                          static_cast<cudaStream_t>(stream));
+    NGH_CUDA(cudaGetLastError());
+    NGRAM_API_END
+}
+
+int ngram_shard_xchg_unpack(ngram_shard_group* g, const void* recv, void* stream) {
+    NGRAM_API_BEGIN
+    if (!g || g->xchg_T < 0) throw Error(NGRAM_EINVAL, "ngram_shard_xchg_unpack: no prepared exchange");
+    int64_t total = 0;
+    for (const int64_t n : g->recv_rows) total += n;
+    if (total > 0 && !recv) throw Error(NGRAM_EINVAL, "ngram_shard_xchg_unpack: null receive buffer");
+    ngram_bank* b = g->bank;
+    DeviceGuard dg(b->device);
+    ngk::launch_xchg_unpack(b->shape, b->cfg.sub_vocab.data(), g->rank, g->nranks, g->rank_tok.data(), g->ids_all.p,
+                            g->xpref.p, g->pref_stride, g->recv_rows.data(),
+                            static_cast<const __nv_bfloat16*>(recv), g->x[g->parity].x.p, b->err.p,
+                            static_cast<cudaStream_t>(stream));
+    NGH_CUDA(cudaGetLastError());
+    NGRAM_API_END
+}
+
+int ngram_shard_pack_padded(ngram_shard_group* g, const uint32_t* all_tokens, const int64_t* all_seq_offsets,
+                            int64_t all_nseq, int64_t all_T, const int64_t* rank_token_offsets,
+                            const uint32_t* all_prior, void* send, void* stream) {
+    NGRAM_API_BEGIN
+    check_gathered(g, all_tokens, all_seq_offsets, all_nseq, all_T, rank_token_offsets, false);
+    if (!send) throw Error(NGRAM_EINVAL, "ngram_shard_pack_padded: null send buffer");
+    ngram_bank* b = g->bank;
+    DeviceGuard dg(b->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t Tpad = round_up(std::max<int64_t>(all_T, 1), kRowPad);
+    g->grow_all.ensure(size_t(b->shape.B) * size_t(Tpad));
+    reset_error_word(b, st);
+    g->regime_T = all_T;
+    if (all_T > 0)
+        ngk::launch_hash_ids(b->shape, b->ht.p, all_tokens, all_seq_offsets, all_nseq, all_T, all_prior, nullptr, 0,
+                             g->grow_all.p, Tpad, b->err.p, st);
+    ngk::launch_xchg_pack_padded(b->shape, g->grow_all.p, Tpad, rank_token_offsets, g->nranks, g->max_home, b->sub.p,
+                                 static_cast<__nv_bfloat16*>(send), all_T, b->err.p, st);
+    NGH_CUDA(cudaGetLastError());
+    NGRAM_API_END
+}
+
+int ngram_shard_home_x(ngram_shard_group* g, void** x) {
+    NGRAM_API_BEGIN
+    if (!g || !x) throw Error(NGRAM_EINVAL, "null argument");
+    *x = g->x[g->parity].x.p;
     NGRAM_API_END
 }
 

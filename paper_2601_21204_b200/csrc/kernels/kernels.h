@@ -194,6 +194,26 @@ void launch_decode_reset(const Shape& s, uint32_t* ring, uint64_t* length, uint3
 void launch_shard_scatter(const Shape& s, const int32_t* grow_all, int64_t Tpad_all, const int64_t* rank_token_offsets,
                           int nranks, const __nv_bfloat16* sub, __nv_bfloat16* const* peer_x, int64_t T_all,
                           const unsigned long long* err, cudaStream_t st);
+// NCCL exchange variants (shard.cu).  prepare: exclusive prefixes of the exchange counts
+// (column 0: this rank's owned pairs over the gathered batch; column 1+o: home-token pairs owned
+// by rank o) into pref [1+nranks][pref_stride]; bounds_out (dev, 2*nranks+1): column-0 prefix at
+// each rank's first home token (+ the total), then the rows received from each rank.
+void launch_xchg_prepare(const Shape& s, const uint64_t* sub_vocab, int rank, int nranks,
+                         const int64_t* rank_token_offsets, int64_t all_T, const uint64_t* ids_all,
+                         int64_t* tot, int64_t* chunk_off, int64_t* col_tot, int64_t* pref, int64_t pref_stride,
+                         int64_t* bounds_out, const unsigned long long* err, cudaStream_t st);
+void launch_xchg_pack(const Shape& s, const uint64_t* sub_vocab, int rank, int nranks, int64_t all_T,
+                      const uint64_t* ids_all, const int32_t* grow_all, int64_t Tpad, const int64_t* pref0,
+                      const __nv_bfloat16* sub, __nv_bfloat16* send, const unsigned long long* err, cudaStream_t st);
+void launch_xchg_unpack(const Shape& s, const uint64_t* sub_vocab, int rank, int nranks,
+                        const int64_t* rank_token_offsets, const uint64_t* ids_all, const int64_t* pref,
+                        int64_t pref_stride, const int64_t* recv_rows, const __nv_bfloat16* recv, __nv_bfloat16* X,
+                        const unsigned long long* err, cudaStream_t st);
+void launch_xchg_pack_padded(const Shape& s, const int32_t* grow_all, int64_t Tpad_all,
+                             const int64_t* rank_token_offsets, int nranks, int64_t max_home,
+                             const __nv_bfloat16* sub, __nv_bfloat16* send, int64_t T_all,
+                             const unsigned long long* err, cudaStream_t st);
+constexpr int kXchgChunkTokens = 1024;
 
 // ---- corpus analysis (analysis.cu; corpus_analyzer, analysis.cpp:93-121)
 // Open-addressing set of 128-bit keys (x = low word); all-ones = empty slot; mask = slots - 1.

@@ -620,6 +620,21 @@ class CorpusAnalyzer:
         return out
 
 
+class _CudaArray:
+    """__cuda_array_interface__ of library-owned device memory (so torch can alias it)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def _device_view(ptr: int, shape, dtype, device: int) -> torch.Tensor:
+    """A torch tensor aliasing `ptr` (no copy); bf16 goes through its int16 bit pattern."""
+    typestr = {torch.bfloat16: "<i2", torch.float32: "<f4", torch.int32: "<i4", torch.int64: "<i8"}[dtype]
+    t = torch.as_tensor(_CudaArray(ptr, shape, typestr), device=torch.device("cuda", device))
+    return t.view(dtype) if dtype == torch.bfloat16 else t
+
+
 # ----------------------------------------------------------------------------- row shards
 class ShardGroup:
     """Row-sharded exchange of one rank: double-buffered home X, peer buffers
@@ -631,6 +646,7 @@ class ShardGroup:
         h = C.c_void_p()
         check(abi.lib().ngram_shard_group_create(bank.handle, max_home_tokens, C.byref(h)))
         self.handle = h
+        self.max_home = max_home_tokens
 
     def close(self):
         if self.handle:
@@ -659,6 +675,73 @@ class ShardGroup:
     def set_peer(self, peer_rank: int, bufs) -> None:
         check(abi.lib().ngram_shard_set_peer(self.handle, peer_rank, C.c_void_p(bufs[0]), C.c_void_p(bufs[1])))
 
+    # ---- NCCL exchange variants (include/ngram_b200.h): the caller runs the collective
+    def xchg_prepare(self, all_tokens: torch.Tensor, all_seq_offsets: torch.Tensor, rank_token_offsets,
+                     all_prior: Optional[torch.Tensor] = None, stream=None):
+        """K1 over the gathered batch + the all-to-all counts -> (send_rows, recv_rows) per rank."""
+        rto = np.ascontiguousarray(rank_token_offsets, np.int64)
+        snd = np.zeros(self.nranks, np.int64)
+        rcv = np.zeros(self.nranks, np.int64)
+        check(abi.lib().ngram_shard_xchg_prepare(self.handle, _ptr(all_tokens), _ptr(all_seq_offsets),
+                                                 all_seq_offsets.numel() - 1, all_tokens.numel(), rto.ctypes.data,
+                                                 _ptr(all_prior), snd.ctypes.data, rcv.ctypes.data, _stream(stream)))
+        return snd, rcv
+
+    def xchg_pack(self, send: torch.Tensor, stream=None) -> None:
+        check(abi.lib().ngram_shard_xchg_pack(self.handle, _ptr(send), _stream(stream)))
+
+    def xchg_unpack(self, recv: torch.Tensor, stream=None) -> None:
+        check(abi.lib().ngram_shard_xchg_unpack(self.handle, _ptr(recv), _stream(stream)))
+
+    def pack_padded(self, all_tokens: torch.Tensor, all_seq_offsets: torch.Tensor, rank_token_offsets, send: torch.Tensor,
+                    all_prior: Optional[torch.Tensor] = None, stream=None) -> None:
+        rto = np.ascontiguousarray(rank_token_offsets, np.int64)
+        check(abi.lib().ngram_shard_pack_padded(self.handle, _ptr(all_tokens), _ptr(all_seq_offsets),
+                                                all_seq_offsets.numel() - 1, all_tokens.numel(), rto.ctypes.data,
+                                                _ptr(all_prior), _ptr(send), _stream(stream)))
+
+    def home_x(self) -> torch.Tensor:
+        """The home X the next project() reads, as a [max_home, D] bf16 tensor aliasing it."""
+        p = C.c_void_p()
+        check(abi.lib().ngram_shard_home_x(self.handle, C.byref(p)))
+        return _device_view(p.value, (self.max_home, self.bank.D), torch.bfloat16, self.bank.device)
+
+    def exchange(self, mode: str, all_tokens: torch.Tensor, all_seq_offsets: torch.Tensor, rank_token_offsets,
+                 all_prior: Optional[torch.Tensor] = None, pg=None) -> None:
+        """Step 2 of the row-sharded forward through an NCCL collective (torch.distributed):
+        mode "a2a" -- all-to-all of the owned rows (compact); "rs" -- reduce-scatter of the
+        -0.0-padded X.  Leaves this rank's home X as scatter() would (bit-identical)."""
+        import torch.distributed as dist
+        dev = all_tokens.device
+        D, d = self.bank.D, self.bank.D // max(self.bank.B, 1)
+        # gloo (functional runs with every rank on one device) moves host tensors only
+        host = dist.get_backend(pg) == "gloo"
+        if mode == "a2a":
+            snd, rcv = self.xchg_prepare(all_tokens, all_seq_offsets, rank_token_offsets, all_prior)
+            send = torch.empty((int(snd.sum()), d), dtype=torch.bfloat16, device=dev)
+            recv = torch.empty((int(rcv.sum()), d), dtype=torch.bfloat16, device=dev)
+            self.xchg_pack(send)
+            if host:  # fp32 staging (gloo has no 16-bit types; bf16 -> fp32 -> bf16 is exact)
+                r = torch.empty((int(rcv.sum()), d), dtype=torch.float32)
+                dist.all_to_all_single(r, send.float().cpu(), output_split_sizes=[int(x) for x in rcv],
+                                       input_split_sizes=[int(x) for x in snd], group=pg)
+                recv.copy_(r.to(torch.bfloat16))
+            else:
+                dist.all_to_all_single(recv, send, output_split_sizes=[int(x) for x in rcv],
+                                       input_split_sizes=[int(x) for x in snd], group=pg)
+            self.xchg_unpack(recv)
+        elif mode == "rs":
+            send = torch.empty((self.nranks * self.max_home, D), dtype=torch.bfloat16, device=dev)
+            self.pack_padded(all_tokens, all_seq_offsets, rank_token_offsets, send, all_prior)
+            if host:  # all-reduce of the padded batch, then this rank's slice (same sum)
+                h = send.float().cpu()
+                dist.all_reduce(h, op=dist.ReduceOp.SUM, group=pg)
+                self.home_x().copy_(h[self.rank * self.max_home:(self.rank + 1) * self.max_home].to(torch.bfloat16))
+            else:
+                dist.reduce_scatter_tensor(self.home_x(), send, op=dist.ReduceOp.SUM, group=pg)
+        else:
+            raise ValueError(f"unknown exchange {mode!r}")
+
     def scatter(self, all_tokens: torch.Tensor, all_seq_offsets: torch.Tensor, rank_token_offsets,
                 all_prior: Optional[torch.Tensor] = None, stream=None) -> None:
         rto = np.ascontiguousarray(rank_token_offsets, np.int64)
@@ -680,12 +763,14 @@ class ShardGroup:
 
 
 def sharded_verify_block(group: ShardGroup, state: DecodeState, draft: torch.Tensor, out_dtype=torch.bfloat16,
-                         pg=None, barrier=None) -> torch.Tensor:
+                         pg=None, barrier=None, exchange: str = "peer") -> torch.Tensor:
     """A verify block (L = 1: a decode step) of this rank's home streams on row-sharded tables
     (DESIGN.md 7): all-gather the drafts and the decode rings (the windows' prior), scatter the
     owned rows into every home X, barrier, project the home rows (merged, pre-amplification,
     cache.hpp:122-124).  `state` is this rank's DecodeState on its shard bank; commit with
-    state.commit(draft, accept) afterwards.  Every rank must hold the same number of streams."""
+    state.commit(draft, accept) afterwards.  Every rank must hold the same number of streams.
+    exchange: "peer" (NVLink peer stores + a barrier), or the NCCL forms "rs" (reduce-scatter of
+    the padded X) / "a2a" (all-to-all of the owned rows); all bit-identical."""
     import torch.distributed as dist
     world = dist.get_world_size(pg)
     Bh, L = draft.shape
@@ -697,12 +782,16 @@ def sharded_verify_block(group: ShardGroup, state: DecodeState, draft: torch.Ten
         all_ring = torch.empty((world * Bh, R), dtype=torch.int32, device=draft.device)
         dist.all_gather_into_tensor(all_ring, state.rings().contiguous(), group=pg)
     all_off = torch.arange(0, world * Bh * L + 1, L, dtype=torch.int64, device=draft.device)
-    group.scatter(all_draft.view(-1), all_off, [r * Bh * L for r in range(world + 1)], all_ring)
-    if barrier is not None:
-        barrier()
+    rank_tok = [r * Bh * L for r in range(world + 1)]
+    if exchange != "peer":
+        group.exchange(exchange, all_draft.view(-1), all_off, rank_tok, all_ring, pg=pg)
     else:
-        one = torch.ones(1, device=draft.device)
-        dist.all_reduce(one, group=pg)  # stream-ordered (NCCL): every rank's rows have landed
+        group.scatter(all_draft.view(-1), all_off, rank_tok, all_ring)
+        if barrier is not None:
+            barrier()
+        else:
+            one = torch.ones(1, device=draft.device)
+            dist.all_reduce(one, group=pg)  # stream-ordered (NCCL): every rank's rows have landed
     _, merged = group.project(draft.contiguous().view(-1).to(torch.int32), rows=False, merged=True,
                               out_dtype=out_dtype)
     return merged.view(Bh, L, -1)

@@ -58,6 +58,21 @@ def test_bench_two_ranks_one_device(cuda, sharding):
                                           "k3_projection_epilogue"}
 
 
+def test_bench_gpus_flag_launches_the_ranks_itself(cuda):
+    """`python bench.py --gpus 2` with no torchrun wrapper (the driver's command line) starts the
+    two ranks itself: the line reports n_gpus = 2 and the row-sharded stages."""
+    env = dict(os.environ, NGRAM_BENCH_ONE_DEVICE="1")
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "3", "--warmup",
+                          "3", "--workload", "B"], capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["config"]["sharding"] == "row"
+    assert set(line["stages_ms"]) == {"all_gather_tokens", "k1_k2_scatter_nvlink", "barrier", "k3_projection_epilogue"}
+
+
 def test_bench_sharded_verify_two_ranks_one_device(cuda):
     """bench.py --workload E at N = 2 (row-sharded verify + commit), functional, one device."""
     import socket

@@ -67,3 +67,55 @@ def test_sharded_small_batch_follows_the_gathered_batch_regime(cuda, P, home):
         rows, _ = g.project(t_all[rank_tok[r]:rank_tok[r + 1]])
         assert torch.equal(rows, ref_rows[rank_tok[r]:rank_tok[r + 1]]), (P, home, r)
     banks[0].sync_errors()
+
+
+@pytest.mark.parametrize("P", [2, 3, 8])
+@pytest.mark.parametrize("mode", ["a2a", "rs"])
+def test_nccl_exchange_variants_bit_identical_to_single_gpu(cuda, P, mode):
+    """The NCCL forms of the exchange (include/ngram_b200.h): all-to-all of the owned rows
+    (compact, slots derived from the receiver's own ids) and reduce-scatter of the -0.0-padded X.
+    The collective is emulated in-process (slices / an fp32 sum of the chunks, which is what NCCL's
+    bf16 sum computes for one real value plus -0.0 pads); ranks hold unequal numbers of tokens."""
+    cfg = O.make_default_config(4000, 768, 4, 4)
+    full = G.DeviceBank(cfg).generate(13)
+    rng = np.random.default_rng(P)
+    lens = [int(x) for x in rng.integers(1, 400, size=2 * P)]
+    toks = rng.integers(0, 4000, size=sum(lens)).astype(np.uint32)
+    off = np.concatenate([[0], np.cumsum(lens)])
+    prior = rng.integers(0, 4000, size=(len(lens), 3)).astype(np.uint32)
+    t_all, off_all, pr_all = dev_u32(torch, toks, cuda), dev_i64(torch, off, cuda), dev_u32(torch, prior, cuda)
+    ref_rows, _ = G.embed_forward(full, t_all, off_all, prior=pr_all)
+    rank_tok = [int(off[2 * r]) for r in range(P)] + [int(off[-1])]  # two sequences per rank
+    max_home = max(rank_tok[r + 1] - rank_tok[r] for r in range(P))
+    banks = [G.DeviceBank(cfg, shard_rank=r, shard_count=P).generate(13) for r in range(P)]
+    groups = [G.ShardGroup(b, max_home) for b in banks]
+    for step in range(2):  # both halves of the double-buffered X
+        if mode == "a2a":
+            counts = [g.xchg_prepare(t_all, off_all, rank_tok, pr_all) for g in groups]
+            sends = []
+            for g, (snd, rcv) in zip(groups, counts):
+                s = torch.empty((int(snd.sum()), 64), dtype=torch.bfloat16, device=cuda)
+                g.xchg_pack(s)
+                sends.append(s)
+            for p, g in enumerate(groups):
+                parts = []
+                for r in range(P):
+                    snd = counts[r][0]
+                    assert snd[p] == counts[p][1][r]  # what r sends p is what p expects from r
+                    a = int(snd[:p].sum())
+                    parts.append(sends[r][a:a + int(snd[p])])
+                g.xchg_unpack(torch.cat(parts).contiguous())
+        else:
+            sends = []
+            for g in groups:
+                s = torch.empty((P * max_home, 768), dtype=torch.bfloat16, device=cuda)
+                g.pack_padded(t_all, off_all, rank_tok, s, pr_all)
+                sends.append(s)
+            for p, g in enumerate(groups):
+                chunk = torch.stack([s[p * max_home:(p + 1) * max_home].float() for s in sends]).sum(0)
+                g.home_x().copy_(chunk.to(torch.bfloat16))
+        torch.cuda.synchronize()
+        for r, g in enumerate(groups):
+            rows, _ = g.project(t_all[rank_tok[r]:rank_tok[r + 1]])
+            assert torch.equal(rows, ref_rows[rank_tok[r]:rank_tok[r + 1]]), (mode, P, r, step)
+    banks[0].sync_errors()

@@ -119,7 +119,8 @@ def barrier():
 
 ok = True
 for step in range(2):  # both halves of the double-buffered X
-    merged = G.sharded_verify_block(group, st, draft[home], out_dtype=torch.float32, barrier=barrier)
+    merged = G.sharded_verify_block(group, st, draft[home], out_dtype=torch.float32, barrier=barrier,
+                                    exchange=sys.argv[4])
     torch.cuda.synchronize()
     dist.barrier()  # nobody scatters into a buffer a peer still projects from
     ok = ok and torch.equal(merged, ref[home])
@@ -131,18 +132,20 @@ dist.destroy_process_group()
 """
 
 
-@pytest.mark.parametrize("L", [1, 4])
-def test_two_process_sharded_verify_and_commit(cuda, L):
+@pytest.mark.parametrize("L,exchange", [(1, "peer"), (4, "peer"), (4, "rs"), (4, "a2a"), (1, "a2a")])
+def test_two_process_sharded_verify_and_commit(cuda, L, exchange):
     """Config E on row-sharded tables, two ranks: all-gathered drafts + rings, owned rows
-    scattered over CUDA IPC, split-K projection of the home block, local commit -- identical
-    to the single-GPU verify + commit of the same streams.  L = 1 is a sharded decode step."""
+    moved to their home rank -- scattered over CUDA IPC ("peer"), or by the collective forms
+    (reduce-scatter of the -0.0-padded X, all-to-all of the owned rows; gloo here, NCCL on a
+    multi-GPU node) -- split-K projection of the home block, local commit: identical to the
+    single-GPU verify + commit of the same streams.  L = 1 is a sharded decode step."""
     code = VERIFY_WORKER.format(root=ROOT, tests=HERE, port=_free_port())
     with tempfile.TemporaryDirectory() as td:
         procs, outs = [], []
         for r in range(2):
             out = os.path.join(td, f"r{r}.npy")
             outs.append(out)
-            procs.append(subprocess.Popen([sys.executable, "-c", code, str(r), out, str(L)]))
+            procs.append(subprocess.Popen([sys.executable, "-c", code, str(r), out, str(L), exchange]))
         for p in procs:
             assert p.wait(timeout=300) == 0
         assert all(int(np.load(o)[0]) == 1 for o in outs)
