@@ -161,6 +161,9 @@ def ref():
                                        _f32p, _u64p]
         L.ref_embed_positions_f64.argtypes = [C.c_void_p, _u32p, np.ctypeslib.ndpointer(np.int64), C.c_int64,
                                               np.ctypeslib.ndpointer(np.int64), C.c_int64, C.c_void_p, C.c_void_p]
+        L.ref_decode_mt.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, _u32p, C.c_int, _u32p, C.c_int, C.c_int,
+                                    C.c_void_p, C.c_int64, _f32p]
+        L.ref_hash_all_orders_mt.argtypes = [C.c_char_p, _u32p, C.c_int64, C.c_int, _u64p]
         _REF = L
     return _REF
 

@@ -495,4 +495,98 @@ int ref_draft_verify(void* cache, void* bank, const uint32_t* draft, int64_t len
     }
 }
 
+// --- CPU baselines for the decode / verify workloads and the index stage -------------
+// (bench.py cpu_baseline of configs D / E and of hash_all_orders alone; BASELINE.md "CPU
+// baseline plan").  Every stream owns a sequence_cache and an embedding_memo; streams are
+// independent, so they are spread over `nthreads` std::threads.  The reference calls are
+// the stock ones:
+//   mode 0 (decode step, config D):  ids = sequence_cache::append(t) (cache.cpp:37-57),
+//                                    e = embedding_memo::lookup(t, ids, bank) (cache.cpp:123-150)
+//   mode 1 (verify block, config E): draft_verify(state, memo, bank, draft[L], accept)
+//                                    (cache.cpp:152-195)
+// prior: [nstreams][prior_len] tokens appended first (the prefill hand-off); tokens:
+// [nstreams][steps * L]; accept: [nstreams][steps] (mode 1).  last_out: [nstreams][D], the
+// last merged vector each stream produced (so the work cannot be optimised away).
+int ref_decode_mt(void* bank, int mode, int nstreams, int nthreads, const uint32_t* prior, int prior_len,
+                  const uint32_t* tokens, int steps, int L, const int32_t* accept, int64_t memo_capacity,
+                  float* last_out) {
+    auto& bk = static_cast<ref_bank*>(bank)->bank;
+    const std::size_t D = std::size_t(bk.config.dim);
+    std::vector<int> rc(std::size_t(nstreams), 0);
+    std::atomic<int> next{0};
+    std::vector<std::thread> pool;
+    if (nthreads < 1) nthreads = 1;
+    const int per = mode == 0 ? steps : steps * L;
+    for (int w = 0; w < nthreads; ++w) {
+        pool.emplace_back([&]() {
+            for (;;) {
+                const int s = next.fetch_add(1);
+                if (s >= nstreams) return;
+                try {
+                    sequence_cache state(bk.config);
+                    embedding_memo memo{std::size_t(memo_capacity)};
+                    for (int i = 0; i < prior_len; ++i) state.append(prior[std::size_t(s) * prior_len + i]);
+                    const uint32_t* tk = tokens + std::size_t(s) * std::size_t(per);
+                    std::vector<float> last(D, 0.0f);
+                    if (mode == 0) {
+                        for (int i = 0; i < steps; ++i) {
+                            const auto ids = state.append(tk[i]);
+                            last = memo.lookup(tk[i], ids, bk);
+                        }
+                    } else {
+                        for (int r = 0; r < steps; ++r) {
+                            const auto res = draft_verify(state, memo, bk,
+                                                          std::span<const token_id>(tk + std::size_t(r) * L, std::size_t(L)),
+                                                          std::size_t(accept[std::size_t(s) * steps + r]));
+                            if (!res.accepted.empty()) last = res.accepted.back();
+                        }
+                    }
+                    std::memcpy(last_out + std::size_t(s) * D, last.data(), D * 4);
+                } catch (...) {
+                    rc[std::size_t(s)] = map_exc();
+                }
+            }
+        });
+    }
+    for (auto& t : pool) t.join();
+    for (int x : rc)
+        if (x) return x;
+    return 0;
+}
+
+// hashing.cpp:61-81 hash_all_orders over every position of `len` tokens (one zero-padded
+// sequence; windows via corpus.cpp:273-280 window_at), positions split over nthreads.
+// ids: len x branch_count.
+int ref_hash_all_orders_mt(const char* cfg_json, const uint32_t* tokens, int64_t len, int nthreads, uint64_t* ids) {
+    try {
+        const auto cfg = ngram_config_from_json(cfg_json);
+        const std::vector<token_id> seq(tokens, tokens + len);
+        const std::size_t nb = std::size_t(cfg.branch_count());
+        std::vector<std::thread> pool;
+        std::vector<int> rc(std::size_t(std::max(nthreads, 1)), 0);
+        if (nthreads < 1) nthreads = 1;
+        for (int w = 0; w < nthreads; ++w) {
+            pool.emplace_back([&, w]() {
+                try {
+                    std::vector<token_id> window;
+                    const int64_t a = len * w / nthreads, b = len * (w + 1) / nthreads;
+                    for (int64_t p = a; p < b; ++p) {
+                        window_at(seq, std::size_t(p), cfg.max_order, window);
+                        const auto v = hash_all_orders(window, cfg);
+                        std::memcpy(ids + std::size_t(p) * nb, v.data(), nb * 8);
+                    }
+                } catch (...) {
+                    rc[std::size_t(w)] = map_exc();
+                }
+            });
+        }
+        for (auto& t : pool) t.join();
+        for (int x : rc)
+            if (x) return x;
+        return 0;
+    } catch (...) {
+        return map_exc();
+    }
+}
+
 }  // extern "C"

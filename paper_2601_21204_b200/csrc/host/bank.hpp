@@ -70,6 +70,31 @@ struct DevBuf {
     }
 };
 
+// Page-locked host staging (cudaMallocHost), grown on demand.
+struct PinBuf {
+    unsigned char* p = nullptr;
+    size_t n = 0;
+    PinBuf() = default;
+    PinBuf(const PinBuf&) = delete;
+    PinBuf& operator=(const PinBuf&) = delete;
+    ~PinBuf() {
+        if (p) cudaFreeHost(p);
+    }
+    void ensure(size_t bytes) {
+        if (bytes <= n) return;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        n = 0;
+        cudaError_t e = cudaMallocHost(reinterpret_cast<void**>(&p), bytes);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            p = nullptr;
+            throw Error(NGRAM_ENOMEM, "cudaMallocHost of " + std::to_string(bytes) + " bytes failed");
+        }
+        n = bytes;
+    }
+};
+
 // A materialised X buffer (T x D bf16) with its TMA descriptor (box 64 x 128 rows).
 struct XBuf {
     DevBuf<__nv_bfloat16> x;
@@ -151,6 +176,18 @@ struct ngram_decode {
     ngh::DevBuf<int32_t> grow;              // [B][round_up(batch*max_draft, 128)]
     ngh::DevBuf<unsigned long long> derr;   // decode error word
     ngh::XBuf xbuf;                         // gathered block rows
+    // host-buffer entries (ngram_decode_step_host / ngram_verify_commit_host): persistent device
+    // buffers + one pinned staging block, so a call is H2D -> kernels -> D2H with one sync and
+    // no allocation after the first call
+    ngh::DevBuf<uint32_t> io_tok;           // [batch][max_draft]
+    ngh::DevBuf<int32_t> io_acc;            // [batch]
+    ngh::DevBuf<uint64_t> io_ids;           // [batch][B]
+    ngh::DevBuf<float> io_out;              // [batch][max_draft][D]
+    ngh::PinBuf io_pin;                     // error words | ids | out, then tokens | accept
+    cudaStream_t io_stream = nullptr;
+    ~ngram_decode() {
+        if (io_stream) cudaStreamDestroy(io_stream);
+    }
 };
 
 namespace ngh {

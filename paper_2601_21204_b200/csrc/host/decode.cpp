@@ -3,6 +3,8 @@
 // device-resident streams.  No host round trip on the hot calls.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstring>
 #include <memory>
 #include <vector>
 
@@ -211,6 +213,50 @@ int ngram_decode_reset_host(ngram_decode* d, const uint32_t* prior, const uint64
     NGRAM_API_END
 }
 
+// Host-buffer path: stage the inputs in pinned memory, enqueue H2D -> step -> D2H of the
+// error words and outputs on the state's own stream, one synchronisation, then copy out
+// (the caller's buffers are written only on success, as the reference returns by value).
+namespace {
+struct HostIo {
+    ngram_decode* d;
+    unsigned long long* words;  // [0] token error, [1] released (reported) error
+    unsigned char* ids;
+    unsigned char* out;
+    unsigned char* in;
+};
+
+HostIo host_io(ngram_decode* d, size_t ids_bytes, size_t out_bytes, size_t in_bytes) {
+    if (!d->io_stream) NGH_CUDA(cudaStreamCreateWithFlags(&d->io_stream, cudaStreamNonBlocking));
+    const size_t a = 16, b = a + round_up(int64_t(ids_bytes), 16), c = b + round_up(int64_t(out_bytes), 16);
+    d->io_pin.ensure(c + in_bytes);
+    return {d, reinterpret_cast<unsigned long long*>(d->io_pin.p), d->io_pin.p + a, d->io_pin.p + b,
+            d->io_pin.p + c};
+}
+
+// Enqueue the error-word read, synchronise, and raise a token error like ngram_sync_errors.
+void finish_host_io(const HostIo& io) {
+    ngram_bank* b = io.d->bank;
+    cudaStream_t st = io.d->io_stream;
+    NGH_CUDA(cudaStreamSynchronize(st));
+    const unsigned long long e = std::min(io.words[0], io.words[1]);
+    b->err_clean = true;
+    if (e != ~0ull) {
+        NGH_CUDA(cudaMemsetAsync(b->err.p, 0xff, 8, st));
+        NGH_CUDA(cudaMemsetAsync(b->err_rep.p, 0xff, 8, st));
+        NGH_CUDA(cudaStreamSynchronize(st));
+        throw Error(NGRAM_ERANGE, "embedding: token out of range for base vocabulary " +
+                                      std::to_string(b->cfg.base_vocab) + " (first bad window at position " +
+                                      std::to_string(e) + ")");
+    }
+}
+
+void read_words(const HostIo& io) {
+    ngram_bank* b = io.d->bank;
+    NGH_CUDA(cudaMemcpyAsync(&io.words[0], b->err.p, 8, cudaMemcpyDeviceToHost, io.d->io_stream));
+    NGH_CUDA(cudaMemcpyAsync(&io.words[1], b->err_rep.p, 8, cudaMemcpyDeviceToHost, io.d->io_stream));
+}
+}  // namespace
+
 int ngram_decode_step_host(ngram_decode* d, const uint32_t* tokens, uint64_t* ids_out, float* merged_out) {
     NGRAM_API_BEGIN
     if (!d || !tokens) throw Error(NGRAM_EINVAL, "ngram_decode_step_host: bad argument");
@@ -220,21 +266,26 @@ int ngram_decode_step_host(ngram_decode* d, const uint32_t* tokens, uint64_t* id
     for (int64_t s = 0; s < d->batch; ++s)  // the reference validates before mutating (cache.cpp:39-42)
         if (tokens[s] >= b->cfg.base_vocab)
             throw Error(NGRAM_ERANGE, "sequence_cache: token " + std::to_string(tokens[s]) + " out of range");
-    DevBuf<uint32_t> t;
-    DevBuf<uint64_t> ids;
-    DevBuf<float> out;
-    t.alloc(size_t(d->batch));
-    NGH_CUDA(cudaMemcpy(t.p, tokens, size_t(d->batch) * 4, cudaMemcpyHostToDevice));
-    if (ids_out) ids.alloc(size_t(d->batch) * size_t(std::max(b->shape.B, 1)));
-    if (merged_out) out.alloc(size_t(d->batch) * size_t(b->cfg.dim));
-    int rc = ngram_decode_step(d, t.p, ids.p, out.p, NGRAM_F32, nullptr);
+    const size_t nb = size_t(std::max(b->shape.B, 0));
+    const size_t tok_bytes = size_t(d->batch) * 4;
+    const size_t ids_bytes = ids_out ? size_t(d->batch) * nb * 8 : 0;
+    const size_t out_bytes = merged_out ? size_t(d->batch) * size_t(b->cfg.dim) * 4 : 0;
+    d->io_tok.ensure(size_t(d->batch) * size_t(d->max_draft));
+    if (ids_out) d->io_ids.ensure(std::max<size_t>(size_t(d->batch) * nb, 1));
+    if (merged_out) d->io_out.ensure(size_t(d->batch) * size_t(d->max_draft) * size_t(b->cfg.dim));
+    const HostIo io = host_io(d, ids_bytes, out_bytes, tok_bytes);
+    cudaStream_t st = d->io_stream;
+    std::memcpy(io.in, tokens, tok_bytes);
+    NGH_CUDA(cudaMemcpyAsync(d->io_tok.p, io.in, tok_bytes, cudaMemcpyHostToDevice, st));
+    int rc = ngram_decode_step(d, d->io_tok.p, ids_out ? d->io_ids.p : nullptr, merged_out ? d->io_out.p : nullptr,
+                               NGRAM_F32, st);
     if (rc) return rc;
-    rc = ngram_sync_errors(b, nullptr);
-    if (rc) return rc;
-    if (ids_out && b->shape.B > 0)
-        NGH_CUDA(cudaMemcpy(ids_out, ids.p, size_t(d->batch) * size_t(b->shape.B) * 8, cudaMemcpyDeviceToHost));
-    if (merged_out)
-        NGH_CUDA(cudaMemcpy(merged_out, out.p, size_t(d->batch) * size_t(b->cfg.dim) * 4, cudaMemcpyDeviceToHost));
+    read_words(io);
+    if (ids_bytes) NGH_CUDA(cudaMemcpyAsync(io.ids, d->io_ids.p, ids_bytes, cudaMemcpyDeviceToHost, st));
+    if (out_bytes) NGH_CUDA(cudaMemcpyAsync(io.out, d->io_out.p, out_bytes, cudaMemcpyDeviceToHost, st));
+    finish_host_io(io);
+    if (ids_bytes) std::memcpy(ids_out, io.ids, ids_bytes);
+    if (out_bytes) std::memcpy(merged_out, io.out, out_bytes);
     NGRAM_API_END
 }
 
@@ -252,23 +303,25 @@ int ngram_verify_commit_host(ngram_decode* d, const uint32_t* draft, int L, cons
                 throw Error(NGRAM_ERANGE, "sequence_cache: token " + std::to_string(draft[s * L + i]) + " out of range");
     }
     DeviceGuard g(b->device);
-    DevBuf<uint32_t> dr;
-    DevBuf<int32_t> ac;
-    DevBuf<float> out;
-    dr.alloc(size_t(d->batch) * size_t(L));
-    ac.alloc(size_t(d->batch));
-    out.alloc(size_t(d->batch) * size_t(L) * size_t(b->cfg.dim));
-    NGH_CUDA(cudaMemcpy(dr.p, draft, size_t(d->batch) * size_t(L) * 4, cudaMemcpyHostToDevice));
-    NGH_CUDA(cudaMemcpy(ac.p, accept, size_t(d->batch) * 4, cudaMemcpyHostToDevice));
-    int rc = ngram_verify_block(d, dr.p, L, out.p, NGRAM_F32, nullptr);
+    const size_t dr_bytes = size_t(d->batch) * size_t(L) * 4, ac_bytes = size_t(d->batch) * 4;
+    const size_t out_bytes = merged_out ? size_t(d->batch) * size_t(L) * size_t(b->cfg.dim) * 4 : 0;
+    d->io_tok.ensure(size_t(d->batch) * size_t(d->max_draft));
+    d->io_acc.ensure(size_t(d->batch));
+    d->io_out.ensure(size_t(d->batch) * size_t(d->max_draft) * size_t(b->cfg.dim));
+    const HostIo io = host_io(d, 0, out_bytes, dr_bytes + ac_bytes);
+    cudaStream_t st = d->io_stream;
+    std::memcpy(io.in, draft, dr_bytes);
+    std::memcpy(io.in + dr_bytes, accept, ac_bytes);
+    NGH_CUDA(cudaMemcpyAsync(d->io_tok.p, io.in, dr_bytes, cudaMemcpyHostToDevice, st));
+    NGH_CUDA(cudaMemcpyAsync(d->io_acc.p, io.in + dr_bytes, ac_bytes, cudaMemcpyHostToDevice, st));
+    int rc = ngram_verify_block(d, d->io_tok.p, L, d->io_out.p, NGRAM_F32, st);
     if (rc) return rc;
-    rc = ngram_commit(d, dr.p, L, ac.p, nullptr);
+    rc = ngram_commit(d, d->io_tok.p, L, d->io_acc.p, st);
     if (rc) return rc;
-    rc = ngram_sync_errors(b, nullptr);
-    if (rc) return rc;
-    if (merged_out)
-        NGH_CUDA(cudaMemcpy(merged_out, out.p, size_t(d->batch) * size_t(L) * size_t(b->cfg.dim) * 4,
-                            cudaMemcpyDeviceToHost));
+    read_words(io);
+    if (out_bytes) NGH_CUDA(cudaMemcpyAsync(io.out, d->io_out.p, out_bytes, cudaMemcpyDeviceToHost, st));
+    finish_host_io(io);
+    if (out_bytes) std::memcpy(merged_out, io.out, out_bytes);
     NGRAM_API_END
 }
 
