@@ -35,8 +35,12 @@ struct snapshot_handle {
     std::size_t slot = 0;
 };
 
+// Single-owner decode stream.  Constructed from a config (the reference's form,
+// cache.hpp:45) the state hashes on a shared hash-only device bank; the first draft_verify /
+// memo lookup against a bank with tables moves the state onto that bank's device copy.
 class sequence_cache {
   public:
+    explicit sequence_cache(const ngram_config& cfg);
     explicit sequence_cache(const device_bank& bank);
     std::vector<std::uint64_t> append(token_id token, cache_counters* counters = nullptr);
     snapshot_handle snapshot();
@@ -45,10 +49,14 @@ class sequence_cache {
     std::uint64_t length() const;
     std::size_t snapshot_depth() const { return snaps_.size(); }
     token_id last_token() const;
-    const ngram_config& config() const { return bank_->config(); }
-    std::vector<token_id> ring() const;
+    const ngram_config& config() const { return cfg_; }
+    // The trailing N-1 confirmed tokens, oldest first (a view valid until the next call on
+    // this state, as the reference's span into its ring).
+    std::span<const token_id> ring() const;
     ngram_decode* handle() const { return st_.get(); }
-    const device_bank& bank() const { return *bank_; }
+    // Move the state (ring, length, last) onto `bank`'s device copy if it lives elsewhere, so
+    // verify blocks gather from that bank's tables.
+    void bind(const device_bank& bank);
 
   private:
     struct snap {
@@ -58,8 +66,10 @@ class sequence_cache {
     };
     void check(const snapshot_handle& h) const;
     void restore(const snap& s);
-    const device_bank* bank_;
+    ngram_config cfg_;
+    std::shared_ptr<ngram_bank> bank_;  // the device bank the decode state runs on
     std::shared_ptr<ngram_decode> st_;
+    mutable std::vector<token_id> ring_view_;
     std::uint64_t uid_ = 0, next_serial_ = 1;
     std::vector<snap> snaps_;
 };
@@ -101,6 +111,11 @@ struct draft_result {
 draft_result draft_verify(sequence_cache& state, const device_bank& bank, std::span<const token_id> draft,
                           std::size_t accept_count, cache_counters* counters = nullptr, const draft_options& opts = {});
 draft_result draft_verify(sequence_cache& state, embedding_memo& memo, const device_bank& bank,
+                          std::span<const token_id> draft, std::size_t accept_count, cache_counters* counters = nullptr,
+                          const draft_options& opts = {});
+// The reference's signature (cache.hpp:131-136): the host bank's device copy is cached
+// (see device_bank_for), so repeated rounds against one bank upload it once.
+draft_result draft_verify(sequence_cache& state, embedding_memo& memo, const embedding_bank& bank,
                           std::span<const token_id> draft, std::size_t accept_count, cache_counters* counters = nullptr,
                           const draft_options& opts = {});
 

@@ -14,6 +14,7 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "ngram/config.hpp"
@@ -119,16 +120,32 @@ class device_bank {
     ngram_bank* handle() const { return h_.get(); }
     bool tensor_core_path() const;
 
+    const std::shared_ptr<ngram_bank>& shared_handle() const { return h_; }
+
   private:
     ngram_config cfg_;
     std::shared_ptr<ngram_bank> h_;
 };
+
+// The device copy of a host bank, cached across calls: keyed by the bank's address and a
+// 64-bit fingerprint of its contents, so a bank edited in place between calls is re-uploaded
+// and an unchanged one is not.  Every embedding_bank overload below goes through it.
+std::shared_ptr<const device_bank> device_bank_for(const embedding_bank& host);
 
 // embed_from_ids (embedding.hpp:163-201): merged, pre-amplification.
 void embed_from_ids(token_id token, std::span<const std::uint64_t> ids, const device_bank& bank, std::span<float> out,
                     embed_counters* counters = nullptr);
 void embed_from_ids(token_id token, std::span<const std::uint64_t> ids, const embedding_bank& bank,
                     std::span<float> out, embed_counters* counters = nullptr);
+// The reference's template form (embed_from_ids<float>(...), embedding.hpp:163): float banks
+// run on the device; the double instantiation of the reference is a CPU gradient-check tool
+// and has no device path here.
+template <typename T>
+void embed_from_ids(token_id token, std::span<const std::uint64_t> ids, const embedding_bank_t<T>& bank,
+                    std::span<T> out, embed_counters* counters = nullptr) {
+    static_assert(std::is_same_v<T, float>, "device embeddings are computed from float banks");
+    embed_from_ids(token, ids, static_cast<const embedding_bank&>(bank), out, counters);
+}
 
 // embed_window / embed_v1 / embed_v2 (embedding.hpp:205-237): merged embedding of one window.
 void embed_window(std::span<const token_id> context, const device_bank& bank, std::span<float> out,

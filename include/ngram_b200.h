@@ -200,6 +200,10 @@ int ngram_decode_reset_host(ngram_decode* st, const uint32_t* prior, const uint6
 int ngram_decode_step_host(ngram_decode* st, const uint32_t* tokens, uint64_t* ids_out, float* merged_out);
 int ngram_verify_commit_host(ngram_decode* st, const uint32_t* draft, int L, const int32_t* accept,
                              float* merged_out);
+/* Overwrite the state (host buffers): ring batch x (N-1) (NULL = zeros), length (NULL = 0)
+ * and last token (NULL = the ring's newest entry) -- an exact restore of ngram_decode_get_state
+ * (sequence_cache::rollback, cache.cpp:78-87). */
+int ngram_decode_set_state_host(ngram_decode* st, const uint32_t* ring, const uint64_t* length, const uint32_t* last);
 /* Read back the state (host buffers): ring batch x (N-1), length, last token. */
 int ngram_decode_get_state(ngram_decode* st, uint32_t* ring, uint64_t* length, uint32_t* last);
 /* Device pointer of the rings [batch][max_order-1] (oldest first): the `prior` of a decode

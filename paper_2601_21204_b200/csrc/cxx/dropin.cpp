@@ -3,7 +3,9 @@
 // order, exception mapping, JSON; every hash / embedding is computed by the
 // CUDA kernels behind libngram_b200.so.  Built as libngram.so (g++), linked to it.
 #include <atomic>
+#include <cstring>
 #include <fstream>
+#include <list>
 #include <map>
 #include <mutex>
 #include <sstream>
@@ -134,6 +136,56 @@ bool device_bank::tensor_core_path() const {
     return info.tensor_core_path != 0;
 }
 
+namespace {
+std::uint64_t fingerprint(std::uint64_t h, const std::vector<float>& v) {
+    const std::size_t n = v.size();
+    const float* p = v.data();
+    std::size_t i = 0;
+    for (; i + 2 <= n; i += 2) {
+        std::uint64_t w;
+        std::memcpy(&w, p + i, 8);
+        h = (h ^ w) * 0x100000001b3ULL + (h >> 29);
+    }
+    if (i < n) {
+        std::uint32_t w;
+        std::memcpy(&w, p + i, 4);
+        h = (h ^ w) * 0x100000001b3ULL + (h >> 29);
+    }
+    return (h ^ n) * 0x9e3779b97f4a7c15ULL;
+}
+
+std::uint64_t fingerprint(const embedding_bank& b) {
+    std::uint64_t h = std::hash<std::string>()(to_json_string(b.config));
+    h = fingerprint(h, b.base);
+    for (const auto& t : b.sub_tables) h = fingerprint(h, t);
+    for (const auto& w : b.projections) h = fingerprint(h, w);
+    h = fingerprint(h, b.ln_gain);
+    return fingerprint(h, b.ln_bias);
+}
+}  // namespace
+
+std::shared_ptr<const device_bank> device_bank_for(const embedding_bank& host) {
+    struct entry {
+        const embedding_bank* addr;
+        std::uint64_t fp;
+        std::shared_ptr<const device_bank> dev;
+    };
+    static std::mutex mu;
+    static std::list<entry> cache;  // most recently used first, at most kKeep banks
+    constexpr std::size_t kKeep = 4;
+    const std::uint64_t fp = fingerprint(host);
+    std::lock_guard<std::mutex> g(mu);
+    for (auto it = cache.begin(); it != cache.end(); ++it)
+        if (it->addr == &host && it->fp == fp) {
+            cache.splice(cache.begin(), cache, it);
+            return cache.front().dev;
+        }
+    auto dev = std::make_shared<const device_bank>(host);
+    cache.push_front({&host, fp, dev});
+    if (cache.size() > kKeep) cache.pop_back();
+    return dev;
+}
+
 // ------------------------------------------------------------------------ hashing
 void hash_spec::validate() const {
     if (order < 2) throw std::invalid_argument("hash_spec: order must be >= 2, got " + std::to_string(order));
@@ -221,7 +273,7 @@ void embed_from_ids(token_id token, std::span<const std::uint64_t> ids, const de
 
 void embed_from_ids(token_id token, std::span<const std::uint64_t> ids, const embedding_bank& bank,
                     std::span<float> out, embed_counters* counters) {
-    embed_from_ids(token, ids, device_bank(bank), out, counters);
+    embed_from_ids(token, ids, *device_bank_for(bank), out, counters);
 }
 
 sequence_embedding<float> embed_sequence_cached(std::span<const token_id> tokens, const device_bank& bank,
@@ -251,12 +303,12 @@ std::vector<float> embed_sequence(std::span<const token_id> tokens, const device
 
 sequence_embedding<float> embed_sequence_cached(std::span<const token_id> tokens, const embedding_bank& bank,
                                                 std::span<const token_id> prior_context, embed_counters* counters) {
-    return embed_sequence_cached(tokens, device_bank(bank), prior_context, counters);
+    return embed_sequence_cached(tokens, *device_bank_for(bank), prior_context, counters);
 }
 
 std::vector<float> embed_sequence(std::span<const token_id> tokens, const embedding_bank& bank,
                                   std::span<const token_id> prior_context) {
-    return embed_sequence_cached(tokens, device_bank(bank), prior_context).rows;
+    return embed_sequence_cached(tokens, *device_bank_for(bank), prior_context).rows;
 }
 
 namespace {
@@ -314,7 +366,7 @@ void amplify_backward(std::span<const float> pre, std::span<const float> upstrea
 
 void amplify_backward(std::span<const float> pre, std::span<const float> upstream, const embedding_bank& bank,
                       embedding_bank& grads, std::span<float> d_pre) {
-    amplify_backward(pre, upstream, device_bank(bank), grads, d_pre);
+    amplify_backward(pre, upstream, *device_bank_for(bank), grads, d_pre);
 }
 
 void embed_backward(std::span<const token_id> context, const device_bank& bank, std::span<const float> upstream,
@@ -330,7 +382,7 @@ void embed_backward(std::span<const token_id> context, const device_bank& bank, 
 
 void embed_backward(std::span<const token_id> context, const embedding_bank& bank, std::span<const float> upstream,
                     embedding_bank& grads) {
-    embed_backward(context, device_bank(bank), upstream, grads);
+    embed_backward(context, *device_bank_for(bank), upstream, grads);
 }
 
 void embed_sequence_backward(std::span<const token_id> tokens, const device_bank& bank, std::span<const float> merged,
@@ -346,7 +398,7 @@ void embed_sequence_backward(std::span<const token_id> tokens, const device_bank
 void embed_sequence_backward(std::span<const token_id> tokens, const embedding_bank& bank,
                              std::span<const float> merged, std::span<const float> upstream, embedding_bank& grads,
                              std::span<const token_id> prior_context) {
-    embed_sequence_backward(tokens, device_bank(bank), merged, upstream, grads, prior_context);
+    embed_sequence_backward(tokens, *device_bank_for(bank), merged, upstream, grads, prior_context);
 }
 
 void embed_window(std::span<const token_id> context, const device_bank& bank, std::span<float> out,
@@ -408,12 +460,36 @@ std::uint64_t next_uid() {
 constexpr int kMaxDraft = 64;
 }  // namespace
 
-sequence_cache::sequence_cache(const device_bank& bank) : bank_(&bank) {
-    bank.config().validate();
+sequence_cache::sequence_cache(const ngram_config& cfg) : cfg_(cfg) {
+    cfg_.validate();
+    bank_ = hasher_for(cfg_);  // ids need only the config; tables join at the first bind()
+    ngram_decode* d = nullptr;
+    throw_status(ngram_decode_create(bank_.get(), 1, kMaxDraft, &d));
+    st_.reset(d, [](ngram_decode* p) { ngram_decode_destroy(p); });
+    uid_ = next_uid();
+}
+
+sequence_cache::sequence_cache(const device_bank& bank) : cfg_(bank.config()), bank_(bank.shared_handle()) {
+    cfg_.validate();
+    ngram_decode* d = nullptr;
+    throw_status(ngram_decode_create(bank_.get(), 1, kMaxDraft, &d));
+    st_.reset(d, [](ngram_decode* p) { ngram_decode_destroy(p); });
+    uid_ = next_uid();
+}
+
+void sequence_cache::bind(const device_bank& bank) {
+    if (bank.handle() == bank_.get()) return;
+    if (to_json_string(bank.config()) != to_json_string(cfg_))
+        throw std::invalid_argument("sequence_cache: bank config does not match the state's config");
+    snap cur;
+    cur.ring.assign(std::size_t(std::max(cfg_.max_order - 1, 0)), 0);
+    throw_status(ngram_decode_get_state(st_.get(), cur.ring.empty() ? nullptr : cur.ring.data(), &cur.length,
+                                        &cur.last));
     ngram_decode* d = nullptr;
     throw_status(ngram_decode_create(bank.handle(), 1, kMaxDraft, &d));
     st_.reset(d, [](ngram_decode* p) { ngram_decode_destroy(p); });
-    uid_ = next_uid();
+    bank_ = bank.shared_handle();
+    restore(cur);
 }
 
 std::vector<std::uint64_t> sequence_cache::append(token_id token, cache_counters* counters) {
@@ -427,26 +503,24 @@ std::vector<std::uint64_t> sequence_cache::append(token_id token, cache_counters
 
 std::uint64_t sequence_cache::length() const {
     uint64_t len = 0;
-    std::vector<token_id> ring(std::size_t(std::max(config().max_order - 1, 1)));
     token_id last = 0;
-    throw_status(ngram_decode_get_state(st_.get(), ring.data(), &len, &last));
+    throw_status(ngram_decode_get_state(st_.get(), nullptr, &len, &last));
     return len;
 }
 
 token_id sequence_cache::last_token() const {
     uint64_t len = 0;
-    std::vector<token_id> ring(std::size_t(std::max(config().max_order - 1, 1)));
     token_id last = 0;
-    throw_status(ngram_decode_get_state(st_.get(), ring.data(), &len, &last));
+    throw_status(ngram_decode_get_state(st_.get(), nullptr, &len, &last));
     return last;
 }
 
-std::vector<token_id> sequence_cache::ring() const {
+std::span<const token_id> sequence_cache::ring() const {
     uint64_t len = 0;
-    std::vector<token_id> ring(std::size_t(std::max(config().max_order - 1, 0)));
     token_id last = 0;
-    throw_status(ngram_decode_get_state(st_.get(), ring.empty() ? nullptr : ring.data(), &len, &last));
-    return ring;
+    ring_view_.resize(std::size_t(std::max(config().max_order - 1, 0)));
+    throw_status(ngram_decode_get_state(st_.get(), ring_view_.empty() ? nullptr : ring_view_.data(), &len, &last));
+    return ring_view_;
 }
 
 snapshot_handle sequence_cache::snapshot() {
@@ -465,7 +539,7 @@ void sequence_cache::check(const snapshot_handle& h) const {
 }
 
 void sequence_cache::restore(const snap& s) {
-    throw_status(ngram_decode_reset_host(st_.get(), s.ring.empty() ? nullptr : s.ring.data(), &s.length));
+    throw_status(ngram_decode_set_state_host(st_.get(), s.ring.empty() ? nullptr : s.ring.data(), &s.length, &s.last));
 }
 
 void sequence_cache::rollback(const snapshot_handle& h, cache_counters* counters) {
@@ -511,13 +585,23 @@ std::vector<float> embedding_memo::lookup(token_id token, std::span<const std::u
 
 std::vector<float> embedding_memo::lookup(token_id token, std::span<const std::uint64_t> ids,
                                           const embedding_bank& bank, cache_counters* counters) {
-    return lookup(token, ids, device_bank(bank), counters);
+    key k;  // a hit touches no table (cache.cpp:123-133): look up before resolving the device bank
+    k.reserve(ids.size() + 1);
+    k.push_back(token);
+    k.insert(k.end(), ids.begin(), ids.end());
+    if (const auto it = where_.find(k); it != where_.end()) {
+        lru_.splice(lru_.begin(), lru_, it->second);
+        if (counters) counters->memo_hits++;
+        return it->second->second;
+    }
+    return lookup(token, ids, *device_bank_for(bank), counters);
 }
 
 draft_result draft_verify(sequence_cache& state, const device_bank& bank, std::span<const token_id> draft,
                           std::size_t accept_count, cache_counters* counters, const draft_options& opts) {
     if (accept_count > draft.size()) throw std::invalid_argument("draft_verify: accept count exceeds draft length");
     const auto& cfg = bank.config();
+    state.bind(bank);
     for (const token_id t : draft)
         if (std::uint64_t(t) >= cfg.base_vocab)
             throw std::out_of_range("sequence_cache: token " + std::to_string(t) + " out of range");
@@ -562,6 +646,13 @@ draft_result draft_verify(sequence_cache& state, embedding_memo&, const device_b
                           std::span<const token_id> draft, std::size_t accept_count, cache_counters* counters,
                           const draft_options& opts) {
     return draft_verify(state, bank, draft, accept_count, counters, opts);
+}
+
+draft_result draft_verify(sequence_cache& state, embedding_memo& memo, const embedding_bank& bank,
+                          std::span<const token_id> draft, std::size_t accept_count, cache_counters* counters,
+                          const draft_options& opts) {
+    if (accept_count > draft.size()) throw std::invalid_argument("draft_verify: accept count exceeds draft length");
+    return draft_verify(state, memo, *device_bank_for(bank), draft, accept_count, counters, opts);
 }
 
 void amplify(std::span<const float> e, amp_mode mode, std::span<const float> gain, std::span<const float> bias,

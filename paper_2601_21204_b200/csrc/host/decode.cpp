@@ -257,6 +257,17 @@ void read_words(const HostIo& io) {
 }
 }  // namespace
 
+int ngram_decode_set_state_host(ngram_decode* d, const uint32_t* ring, const uint64_t* length, const uint32_t* last) {
+    NGRAM_API_BEGIN
+    const int rc = ngram_decode_reset_host(d, ring, length);
+    if (rc) return rc;
+    if (last) {
+        DeviceGuard g(d->bank->device);
+        NGH_CUDA(cudaMemcpy(d->last.p, last, size_t(d->batch) * 4, cudaMemcpyHostToDevice));
+    }
+    NGRAM_API_END
+}
+
 int ngram_decode_step_host(ngram_decode* d, const uint32_t* tokens, uint64_t* ids_out, float* merged_out) {
     NGRAM_API_BEGIN
     if (!d || !tokens) throw Error(NGRAM_EINVAL, "ngram_decode_step_host: bad argument");

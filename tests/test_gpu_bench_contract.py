@@ -31,6 +31,37 @@ def test_bench_json_contract(cuda):
     assert line["gpu_launches"] > 0 and line["config"]["workload"]
 
 
+def _contract_keys(line):
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "clocks", "gpu_launches"):
+        assert k in line, k
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert k in line["roofline"], k
+    for k in ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"):
+        assert k in line["e2e"], k
+    assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["d2h_bytes_per_step"] > 0
+    assert line["gpu_launches"] > 0 and line["value"] > 0
+
+
+@pytest.mark.parametrize("wl,extra", [("D", ["--batches", "1,8"]), ("E", ["--batches", "4", "--draft", "4"])])
+def test_bench_decode_verify_contract(cuda, wl, extra):
+    """The decode (D) and verify (E) lines carry the same keys as the prefill line, plus the
+    reference CPU baseline (sequence_cache::append + memo / draft_verify, hash_all_orders)."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "3", "--warmup", "3",
+                          "--workload", wl, "--cpu-seconds", "0.5"] + extra,
+                         capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    _contract_keys(line)
+    assert line["roofline"]["bound"] == "hbm"
+    if "cpu_baseline" in line:  # oracle/_ref travels with the snapshot when it was built
+        cb = line["cpu_baseline"]
+        assert cb["kind"] == "reference" and cb["value"] > 0 and cb["cores"] >= 1
+        assert cb["hash_all_orders"]["tokens_per_s"] > 0
+    for r in line["results"].values():
+        assert r["us_per_step"] > 0 and r["e2e"]["us_per_step"] > 0
+
+
 @pytest.mark.parametrize("sharding", ["row", "replica"])
 def test_bench_two_ranks_one_device(cuda, sharding):
     """The N > 1 flow of bench.py (torchrun, row-sharded exchange over CUDA IPC or replicas,
