@@ -287,6 +287,17 @@ int ngram_shard_home_x(ngram_shard_group* g, void** x);
 int ngram_amplify_host(int amp_mode, int D, int64_t rows, const float* gain, const float* bias, const float* in,
                        float* out);
 
+/* Dense GEMM building block of the backward pass and PLNE (device buffers, stream-ordered):
+ *   C[M][N] (fp32, pitch ldc) (+)= sum_k A(m, k) B(n, k)
+ * A is logical [M][K], B logical [N][K]; each stored K-major (x_mn = 0: element (r, k) at
+ * x[r * ldx + k]) or MN-major (x_mn = 1: at x[k * ldx + r]).  a_terms / b_terms: 3 = split the
+ * fp32 operand into three bf16 terms (fp32-accurate tcgen05 products), 1 = one bf16 term (the
+ * operand must be bf16-exact for an fp32-accurate result); a_terms = 0 = the fp32 CUDA-core
+ * GEMM.  The embedding backward uses (3, 1), PLNE (3, 3) with NGRAM_PLNE_FAST and (0, -). */
+int ngram_gemm_f32(int device, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, int a_mn, const float* B,
+                   int64_t ldb, int b_mn, float* C, int64_t ldc, int accumulate, int a_terms, int b_terms,
+                   void* stream);
+
 /* ------------------------------------------------------------------ backward (training) */
 /* embed_sequence_backward (embedding.hpp:438-459) batched on the device: gradients of the
  * embedding rows w.r.t. every bank parameter, ACCUMULATED (+=) into an fp32 gradient bank

@@ -171,7 +171,9 @@ std::shared_ptr<const device_bank> device_bank_for(const embedding_bank& host) {
         std::shared_ptr<const device_bank> dev;
     };
     static std::mutex mu;
-    static std::list<entry> cache;  // most recently used first, at most kKeep banks
+    // most recently used first, at most kKeep banks; never destroyed (device banks must not be
+    // released after the CUDA driver has shut down at process exit)
+    static auto& cache = *new std::list<entry>();
     constexpr std::size_t kKeep = 4;
     const std::uint64_t fp = fingerprint(host);
     std::lock_guard<std::mutex> g(mu);
@@ -211,7 +213,7 @@ namespace {
 // Hash-only device banks keyed by config: hash_all_orders needs only the config.
 std::shared_ptr<ngram_bank> hasher_for(const ngram_config& cfg) {
     static std::mutex mu;
-    static std::map<std::string, std::shared_ptr<ngram_bank>> cache;
+    static auto& cache = *new std::map<std::string, std::shared_ptr<ngram_bank>>();  // never destroyed (see below)
     const std::string key = to_json_string(cfg);
     std::lock_guard<std::mutex> g(mu);
     auto it = cache.find(key);

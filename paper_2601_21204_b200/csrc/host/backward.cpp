@@ -5,11 +5,11 @@
 //   amp_bwd   U = fp32(1/denom) * amplify_backward(merged, upstream); g_E0[tok] += U;
 //             layer_norm: g_gain / g_bias                               (backward.cu)
 //   v2:  X    = gathered sub-table rows (f32)                           (backward.cu)
-//        g_W += U^T X            fp32 GEMM, D x D x T                   (cuBLAS)
-//        dX   = U W_cat          fp32 GEMM, T x D x D                   (cuBLAS)
+//        g_W += U^T X            D x D x T   tcgen05 (gemm_gen.cu), U in three bf16 terms
+//        dX   = U W_cat          T x D x D   tcgen05 (gemm_gen.cu), U in three bf16 terms
+//        (pedantic mode / CUDA-core-shaped banks: the fp32 CUDA-core GEMM of gemm_gen.cu)
 //        g_sub[row_b(t)] += dX[t, b]                                    (backward.cu)
 //   v1:  g_sub[row_b(t)] += U[t]                                        (backward.cu)
-#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -20,6 +20,7 @@
 
 #include "api_util.hpp"
 #include "bank.hpp"
+#include "gemm.hpp"
 
 using namespace ngh;
 
@@ -28,7 +29,7 @@ struct ngram_grad {
     DevBuf<float> e0, sub, w, gain, bias;  // gradients, device layout
     DevBuf<float> U, X, dX, wf;            // workspaces
     DevBuf<__nv_bfloat16> X16, Ub;         // bf16x3 mode: bf16 X and the three bf16 terms of U
-    int gemm_mode = 0;                     // 0 split-bf16 (default), 1 TF32, 2 pedantic fp32
+    int gemm_mode = 0;                     // 0 split-bf16 (default), 1 single-term bf16, 2 pedantic fp32
     DevBuf<int32_t> grow;
     int64_t cap = 0;
     bool sparse = false;                 // NGRAM_GRAD_SPARSE_ROWS
@@ -38,10 +39,6 @@ struct ngram_grad {
     DevBuf<uint32_t> h_tokens, h_prior;  // host-buffer entry staging
     DevBuf<int64_t> h_off;
     DevBuf<float> h_merged, h_up;
-    cublasHandle_t blas = nullptr;
-    ~ngram_grad() {
-        if (blas) cublasDestroy(blas);
-    }
 };
 
 namespace ngh {
@@ -49,11 +46,6 @@ ngram_bank* grad_bank(ngram_grad* g) { return g->bank; }
 }  // namespace ngh
 
 namespace {
-
-void check_blas(cublasStatus_t s, const char* what) {
-    if (s != CUBLAS_STATUS_SUCCESS)
-        throw Error(NGRAM_ECUDA, std::string(what) + " failed (cublas status " + std::to_string(int(s)) + ")");
-}
 
 void zero_all(ngram_grad* g, cudaStream_t st) {
     for (DevBuf<float>* b : {&g->e0, &g->sub, &g->w, &g->gain, &g->bias})
@@ -107,12 +99,10 @@ int ngram_grad_create_ex(ngram_bank* b, int flags, ngram_grad** out) {
         g->gain.alloc(size_t(s.D));
         g->bias.alloc(size_t(s.D));
     }
-    check_blas(cublasCreate(&g->blas), "cublasCreate");
-    // 0: split-bf16 tensor-core GEMMs (tensor-core banks: X and W_cat are bf16), 1: TF32,
-    // 2: pedantic fp32 (also the default on CUDA-core-shaped banks)
-    g->gemm_mode = (flags & NGRAM_GRAD_TF32) ? 1 : ((flags & NGRAM_GRAD_PEDANTIC) || !b->tc_path) ? 2 : 0;
-    check_blas(cublasSetMathMode(g->blas, g->gemm_mode == 2 ? CUBLAS_PEDANTIC_MATH : CUBLAS_TF32_TENSOR_OP_MATH),
-               "cublasSetMathMode");
+    // 0: U in three bf16 terms on the tensor cores (tensor-core banks: X and W_cat are bf16),
+    // 1 (NGRAM_GRAD_TF32): U rounded to one bf16 term (training precision, 3x fewer products),
+    // 2: the fp32 CUDA-core GEMM (pedantic; also every CUDA-core-shaped bank)
+    g->gemm_mode = ((flags & NGRAM_GRAD_PEDANTIC) || !b->tc_path) ? 2 : (flags & NGRAM_GRAD_TF32) ? 1 : 0;
     zero_all(g.get(), nullptr);
     NGH_CUDA(cudaDeviceSynchronize());
     *out = g.release();
@@ -156,7 +146,7 @@ int ngram_embed_backward(ngram_grad* g, const uint32_t* tokens, const int64_t* s
     if (T > g->cap) {
         g->U.alloc(size_t(Tpad) * size_t(D));
         if (s.variant == 1 && B > 0) {
-            if (g->gemm_mode != 0) g->X.alloc(size_t(Tpad) * size_t(D));  // fp32 X: TF32 / pedantic GEMMs only
+            if (g->gemm_mode == 2) g->X.alloc(size_t(Tpad) * size_t(D));  // fp32 X: pedantic GEMMs only
             g->dX.alloc(size_t(Tpad) * size_t(D));
         }
         g->grow.alloc(size_t(std::max(B, 1)) * size_t(Tpad));
@@ -166,31 +156,33 @@ int ngram_embed_backward(ngram_grad* g, const uint32_t* tokens, const int64_t* s
     ngk::launch_hash_ids(s, b->ht.p, tokens, seq_offsets, nseq, T, prior, nullptr, 0, g->grow.p, g->cap, b->err.p, st);
     ngk::launch_amp_backward(s, upstream, merged, tokens, T, amp, b->ln_gain.p, g->U.p, g->e0.p, g->gain.p,
                              g->bias.p, b->err.p, st);
-    // Default on tensor-core banks: X and W_cat are bf16 already, U = u1 + u2 + u3 in bf16 (24
-    // mantissa bits): six bf16 tensor-core GEMMs with fp32 accumulation give fp32-level products
-    // (a two-term TF32 split was measured 25x less accurate at K = 3072 and slower).
-    if (B > 0 && s.variant == 1 && g->gemm_mode == 0) {
+    // Tensor-core banks: X (gathered rows) and W_cat are exact in bf16, so only U is split
+    // (three bf16 terms = 24 mantissa bits, or one term in the single-term mode); the products
+    // accumulate in fp32 TMEM.  Row-major views in the GEMM convention C[M][N] += A(m,k) B(n,k):
+    //   g_W[i][k] += sum_t U[t][i] X[t][k]   A = U (MN-major), B = X (MN-major), K = T
+    //   dX[t][k]   = sum_i U[t][i] W[i][k]   A = U (K-major),  B = W_cat (MN-major), K = D
+    if (B > 0 && s.variant == 1 && g->gemm_mode != 2) {
         const size_t n = size_t(T) * size_t(D);
         const size_t had = g->X16.n;
         g->X16.ensure(n);
         // fresh workspace holds arbitrary bits: zero it once, so that after a bad token (U = 0,
         // the gather skipped) the products are exact zeros, never 0 * NaN
         if (g->X16.n != had) NGH_CUDA(cudaMemsetAsync(g->X16.p, 0, g->X16.n * sizeof(*g->X16.p), st));
-        g->Ub.ensure(3 * n);
+        const int terms = g->gemm_mode == 0 ? 3 : 1;
+        g->Ub.ensure(size_t(terms) * n);
         ngk::launch_gather_rows(s, g->grow.p, g->cap, T, b->sub.p, g->X16.p, b->err.p, st);
-        ngk::launch_split_bf16x3(g->U.p, g->Ub.p, g->Ub.p + n, g->Ub.p + 2 * n, int64_t(n), st);
-        check_blas(cublasSetStream(g->blas, st), "cublasSetStream");
-        const float one = 1.0f, zero = 0.0f;
-        for (int h = 0; h < 3; ++h)
-            check_blas(cublasGemmEx(g->blas, CUBLAS_OP_N, CUBLAS_OP_T, D, D, int(T), &one, g->X16.p, CUDA_R_16BF, D,
-                                    g->Ub.p + size_t(h) * n, CUDA_R_16BF, D, &one, g->w.p, CUDA_R_32F, D,
-                                    CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT),
-                       "cublasGemmEx(dW)");
-        for (int h = 0; h < 3; ++h)
-            check_blas(cublasGemmEx(g->blas, CUBLAS_OP_N, CUBLAS_OP_N, D, int(T), D, &one, b->wcat.p, CUDA_R_16BF, D,
-                                    g->Ub.p + size_t(h) * n, CUDA_R_16BF, D, h ? &one : &zero, g->dX.p, CUDA_R_32F,
-                                    D, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT),
-                       "cublasGemmEx(dX)");
+        ngk::launch_split3(g->U.p, T, D, D, g->Ub.p, terms > 1 ? g->Ub.p + n : nullptr,
+                           terms > 2 ? g->Ub.p + 2 * n : nullptr, D, st);
+        Bf16Op u{};
+        u.terms = terms;
+        u.ld = D;
+        for (int h = 0; h < terms; ++h) u.t[h] = g->Ub.p + size_t(h) * n;
+        const Bf16Op x{{g->X16.p, nullptr, nullptr}, 1, true, D};
+        const Bf16Op w{{b->wcat.p, nullptr, nullptr}, 1, true, D};
+        u.mn = true;
+        gemm_bf16_terms(u, x, D, D, T, g->w.p, D, true, b->num_sms, st);
+        u.mn = false;
+        gemm_bf16_terms(u, w, T, D, D, g->dX.p, D, false, b->num_sms, st);
         if (g->sparse) {
             sparse_reserve(g, T * B, d, st);
             NGH_CUDA(cudaMemcpyAsync(g->sp_vals.p + size_t(g->sp_count) * size_t(d), g->dX.p,
@@ -205,17 +197,9 @@ int ngram_embed_backward(ngram_grad* g, const uint32_t* tokens, const int64_t* s
         // fp32 W_cat (re-widened every call: the bank may have been re-uploaded)
         g->wf.ensure(size_t(D) * size_t(D));
         ngk::launch_bf16_to_f32(b->wcat.p, g->wf.p, int64_t(D) * D, st);
-        check_blas(cublasSetStream(g->blas, st), "cublasSetStream");
-        const float one = 1.0f, zero = 0.0f;
-        // row-major M (r x c) is column-major M^T with ld = c.
-        // g_W (D x D, row-major [i][k]) += U^T X  <=>  col-major g_W^T = X_cm * U_cm^T
-        check_blas(cublasSgemm(g->blas, CUBLAS_OP_N, CUBLAS_OP_T, D, D, int(T), &one, g->X.p, D, g->U.p, D, &one,
-                               g->w.p, D),
-                   "cublasSgemm(dW)");
-        // dX (T x D) = U W_cat  <=>  col-major dX^T = W_cm * U_cm
-        check_blas(cublasSgemm(g->blas, CUBLAS_OP_N, CUBLAS_OP_N, D, int(T), D, &one, g->wf.p, D, g->U.p, D, &zero,
-                               g->dX.p, D),
-                   "cublasSgemm(dX)");
+        ngk::launch_gemm_f32(g->U.p, D, true, g->X.p, D, true, D, D, T, g->w.p, D, true, st);     // g_W += U^T X
+        ngk::launch_gemm_f32(g->U.p, D, false, g->wf.p, D, true, T, D, D, g->dX.p, D, false, st);  // dX = U W_cat
+        NGH_CUDA(cudaGetLastError());
         if (g->sparse) {  // dX is [T][B][d]: exactly the appended values, rows transposed from grow
             sparse_reserve(g, T * B, d, st);
             NGH_CUDA(cudaMemcpyAsync(g->sp_vals.p + size_t(g->sp_count) * size_t(d), g->dX.p,

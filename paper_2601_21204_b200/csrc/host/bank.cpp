@@ -97,13 +97,17 @@ uint64_t ngram_bank::device_bytes() const {
 }
 
 ngram_bank::~ngram_bank() {
-    DeviceGuard g(device);
+    // no DeviceGuard (it throws): a bank may be released after the driver has shut down
+    int prev = -1;
+    if (cudaGetDevice(&prev) == cudaSuccess && prev != device) cudaSetDevice(device);
     for (auto& e : prof_ev)
         if (e) cudaEventDestroy(e);
     for (int i = 0; i < 2; ++i) {
         if (host_streams[i]) cudaStreamDestroy(host_streams[i]);
         if (pinned[i]) cudaFreeHost(pinned[i]);
     }
+    cudaGetLastError();
+    if (prev >= 0 && prev != device) cudaSetDevice(prev);
 }
 
 extern "C" {

@@ -1,10 +1,11 @@
 // plne.cpp -- C-ABI of the per-layer N-gram FFN (PLNE, ple.hpp:168-196):
 //   y = W_d (SiLU(W_g x) (.) g),   g = the layer bank's merged embedding (no amplification).
 // Batched over T positions: G from the N-gram forward (K1+K2 -> K3, amp none), U = X W_g^T and
-// Y = Hh W_d^T as fp32 GEMMs (cuBLAS, no TF32), SiLU gating elementwise (plne.cu).  The plain
+// Y = Hh W_d^T as fp32 GEMMs (gemm_gen.cu: the fp32 CUDA-core GEMM by default, or -- with
+// NGRAM_PLNE_FAST -- both operands split into three bf16 terms on the tensor cores), SiLU
+// gating elementwise (plne.cu).  The plain
 // per-layer form ffn_ple (a table row as the gate) is PLNE with a base-only layer bank
 // (max_order 1, E0 = the table), as the reference's own test states (test_ple.cpp:150-172).
-#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -13,13 +14,13 @@
 
 #include "api_util.hpp"
 #include "bank.hpp"
+#include "gemm.hpp"
 
 using namespace ngh;
 
 struct ngram_plne {
     ngram_bank* bank = nullptr;
     int d_model = 0, hidden = 0;
-    cublasHandle_t blas = nullptr;
     DevBuf<float> U, G, Hh, dHh, dG, dU;
     int64_t cap = 0;
     // host-buffer entry staging
@@ -27,44 +28,18 @@ struct ngram_plne {
     DevBuf<uint32_t> h_tok, h_prior;
     DevBuf<int64_t> h_off;
     bool three = false;                // NGRAM_PLNE_FAST: split-bf16 tensor-core GEMMs
-    DevBuf<__nv_bfloat16> as, bs;      // three bf16 terms of each GEMM operand
-    ~ngram_plne() {
-        if (blas) cublasDestroy(blas);
-    }
+    SplitWs ws;                        // three bf16 terms of each GEMM operand
 };
 
 namespace {
 
-void blas_ok(cublasStatus_t s, const char* what) {
-    if (s != CUBLAS_STATUS_SUCCESS)
-        throw Error(NGRAM_ECUDA, std::string(what) + " failed (cublas status " + std::to_string(int(s)) + ")");
-}
-
-// C = A op B (+ beta C).  Default: one pedantic fp32 GEMM (CUDA cores; relL2 6e-7 vs fp64 at
-// K = 3072).  NGRAM_PLNE_FAST: on the bf16 tensor cores -- A = a1 + a2 + a3 and B = b1 + b2 + b3
-// in bf16, the six products a_i b_j with i + j <= 4 accumulated in fp32: 2.9x faster, relL2 7e-6
-// vs fp64 at K = 3072 (a three-term TF32 split measured 1.5e-5; tests/test_gpu_plne.py).
-// nA / nB: element counts of the stored operands (split elementwise, whatever the op).
-void gemm(ngram_plne* p, cublasOperation_t ta, cublasOperation_t tb, int m, int n, int k, const float* A, size_t nA,
-          int lda, const float* B, size_t nB, int ldb, float beta, float* C, int ldc, cudaStream_t st,
-          const char* what) {
-    const float one = 1.0f;
-    if (!p->three) {
-        blas_ok(cublasSgemm(p->blas, ta, tb, m, n, k, &one, A, lda, B, ldb, &beta, C, ldc), what);
-        return;
-    }
-    p->as.ensure(3 * nA);
-    p->bs.ensure(3 * nB);
-    ngk::launch_split_bf16x3(A, p->as.p, p->as.p + nA, p->as.p + 2 * nA, int64_t(nA), st);
-    ngk::launch_split_bf16x3(B, p->bs.p, p->bs.p + nB, p->bs.p + 2 * nB, int64_t(nB), st);
-    static const int pairs[6][2] = {{2, 0}, {1, 1}, {0, 2}, {1, 0}, {0, 1}, {0, 0}};  // small terms first
-    for (int q = 0; q < 6; ++q) {
-        const float* bt = &beta;
-        blas_ok(cublasGemmEx(p->blas, ta, tb, m, n, k, &one, p->as.p + size_t(pairs[q][0]) * nA, CUDA_R_16BF, lda,
-                             p->bs.p + size_t(pairs[q][1]) * nB, CUDA_R_16BF, ldb, q ? &one : bt, C, CUDA_R_32F, ldc,
-                             CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT),
-                what);
-    }
+// C[M][N] (+)= sum_k A(m, k) B(n, k) (gemm.hpp convention).  Default: the fp32 CUDA-core GEMM
+// (pedantic).  NGRAM_PLNE_FAST: on the bf16 tensor cores -- A = a1 + a2 + a3 and B = b1 + b2 + b3
+// in bf16, the six products a_i b_j with i + j <= 4 accumulated in fp32 TMEM
+// (tests/test_gpu_plne.py: within 1e-5 relL2 of fp64 at d_model = hidden = 3072).
+void gemm(ngram_plne* p, const F32Op& A, const F32Op& B, int64_t M, int64_t N, int64_t K, float* C, int64_t ldc,
+          bool accumulate, cudaStream_t st) {
+    gemm_f32(A, B, M, N, K, C, ldc, accumulate, p->three, p->ws, p->bank->num_sms, st);
 }
 
 void status_ok(int rc) {
@@ -86,12 +61,9 @@ void ensure(ngram_plne* p, int64_t T, bool backward) {
 void forward_common(ngram_plne* p, const float* gate, const float* x, const uint32_t* tokens, const int64_t* off,
                     int64_t nseq, int64_t T, const uint32_t* prior, cudaStream_t st) {
     status_ok(ngram_embed_forward(p->bank, tokens, off, nseq, T, prior, nullptr, p->G.p, NGRAM_F32, st));
-    const float one = 1.0f, zero = 0.0f;
     const int H = p->hidden, Dm = p->d_model;
-    blas_ok(cublasSetStream(p->blas, st), "cublasSetStream");
-    (void)one;
-    gemm(p, CUBLAS_OP_T, CUBLAS_OP_N, H, int(T), Dm, gate, size_t(H) * Dm, Dm, x, size_t(T) * Dm, Dm, zero, p->U.p, H,
-         st, "cublasSgemm(U = X W_g^T)");
+    // U[t][h] = sum_dm X[t][dm] W_g[h][dm]
+    gemm(p, {x, false, Dm}, {gate, false, Dm}, T, H, Dm, p->U.p, H, false, st);
     ngk::launch_silu_gate(p->U.p, p->G.p, p->Hh.p, T * H, p->bank->err.p, st);
 }
 
@@ -114,9 +86,7 @@ int ngram_plne_create_ex(ngram_bank* b, int d_model, int flags, ngram_plne** out
     p->bank = b;
     p->d_model = d_model;
     p->hidden = b->shape.D;
-    blas_ok(cublasCreate(&p->blas), "cublasCreate");
     p->three = (flags & NGRAM_PLNE_FAST) != 0;
-    blas_ok(cublasSetMathMode(p->blas, p->three ? CUBLAS_DEFAULT_MATH : CUBLAS_PEDANTIC_MATH), "cublasSetMathMode");
     *out = p.release();
     NGRAM_API_END
 }
@@ -141,11 +111,9 @@ int ngram_plne_forward(ngram_plne* p, const float* gate, const float* down, cons
     if (T == 0) return NGRAM_OK;
     ensure(p, T, false);
     forward_common(p, gate, x, tokens, seq_offsets, nseq, T, prior, st);
-    const float one = 1.0f, zero = 0.0f;
     const int H = p->hidden, Dm = p->d_model;
-    (void)one;
-    gemm(p, CUBLAS_OP_T, CUBLAS_OP_N, Dm, int(T), H, down, size_t(H) * Dm, H, p->Hh.p, size_t(T) * H, H, zero, y, Dm,
-         st, "cublasSgemm(Y = Hh W_d^T)");
+    // Y[t][dm] = sum_h Hh[t][h] W_d[dm][h]
+    gemm(p, {p->Hh.p, false, H}, {down, false, H}, T, Dm, H, y, Dm, false, st);
     NGRAM_API_END
 }
 
@@ -164,25 +132,19 @@ int ngram_plne_backward(ngram_plne* p, ngram_grad* bank_grads, const float* gate
     if (T == 0) return NGRAM_OK;
     ensure(p, T, true);
     forward_common(p, gate, x, tokens, seq_offsets, nseq, T, prior, st);  // recompute, as the reference
-    const float one = 1.0f, zero = 0.0f;
     const int H = p->hidden, Dm = p->d_model;
-    const int n = int(T);
-    // g_down (Dm x H) += dY^T Hh  <=>  col-major g_down^T (H x Dm) += Hh_cm dY_cm^T
-    gemm(p, CUBLAS_OP_N, CUBLAS_OP_T, H, Dm, n, p->Hh.p, size_t(n) * H, H, upstream, size_t(n) * Dm, Dm, one, d_down,
-         H, st, "cublasSgemm(dW_d)");
-    // dHh (T x H) = dY W_d  <=>  col-major dHh^T = down_cm dY_cm
-    gemm(p, CUBLAS_OP_N, CUBLAS_OP_N, H, n, Dm, down, size_t(H) * Dm, H, upstream, size_t(n) * Dm, Dm, zero, p->dHh.p,
-         H, st, "cublasSgemm(dHh)");
+    // g_down[dm][h] += sum_t dY[t][dm] Hh[t][h]
+    gemm(p, {upstream, true, Dm}, {p->Hh.p, true, H}, Dm, H, T, d_down, H, true, st);
+    // dHh[t][h] = sum_dm dY[t][dm] W_d[dm][h]
+    gemm(p, {upstream, false, Dm}, {down, true, H}, T, H, Dm, p->dHh.p, H, false, st);
     ngk::launch_silu_gate_backward(p->dHh.p, p->U.p, p->G.p, p->dG.p, p->dU.p, T * H, p->bank->err.p, st);
     if (bank_grads)  // embed_backward of dL/dg (ple.hpp:195)
         status_ok(ngram_embed_backward(bank_grads, tokens, seq_offsets, nseq, T, prior, nullptr, p->dG.p,
                                        NGRAM_BWD_SKIP_AMPLIFY, st));
-    // g_gate (H x Dm) += dU^T X  <=>  col-major g_gate^T (Dm x H) += X_cm dU_cm^T
-    gemm(p, CUBLAS_OP_N, CUBLAS_OP_T, Dm, H, n, x, size_t(n) * Dm, Dm, p->dU.p, size_t(n) * H, H, one, d_gate, Dm, st,
-         "cublasSgemm(dW_g)");
-    // dx (T x Dm) += dU W_g  <=>  col-major dx^T += gate_cm dU_cm
-    gemm(p, CUBLAS_OP_N, CUBLAS_OP_N, Dm, n, H, gate, size_t(H) * Dm, Dm, p->dU.p, size_t(n) * H, H, one, dx, Dm, st,
-         "cublasSgemm(dx)");
+    // g_gate[h][dm] += sum_t dU[t][h] X[t][dm]
+    gemm(p, {p->dU.p, true, H}, {x, true, Dm}, H, Dm, T, d_gate, Dm, true, st);
+    // dx[t][dm] += sum_h dU[t][h] W_g[h][dm]
+    gemm(p, {p->dU.p, false, H}, {gate, true, Dm}, T, Dm, H, dx, Dm, true, st);
     NGRAM_API_END
 }
 

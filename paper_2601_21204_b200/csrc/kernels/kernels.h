@@ -84,6 +84,18 @@ void launch_bf16_to_f32(const __nv_bfloat16* src, float* dst, int64_t n, cudaStr
 void launch_split_tf32(float* u, float* lo, int64_t n, cudaStream_t st);
 void launch_split_tf32_copy(const float* a, float* hi, float* lo, int64_t n, cudaStream_t st);
 // u -> u1 + u2 + u3 in bf16 (three-term split for bf16 tensor-core GEMMs with fp32-level accuracy)
+// ---- dense GEMMs (gemm_gen.cu): C[M][N] (fp32) (+)= sum of term-pair products A_i . B_j^T.
+// Operands are logical [R][K] (R = M for A, N for B): K-major maps are (inner K, rows R, box
+// 64 x 128), MN-major maps (inner R, rows K, box 64 x 64); na / nb in {1, 3} terms.
+void launch_gemm_bf16_terms(const CUtensorMap* ma, int na, bool a_mn, const CUtensorMap* mb, int nb, bool b_mn,
+                            int64_t M, int64_t N, int64_t K, float* C, int64_t ldc, bool accumulate, int num_sms,
+                            cudaStream_t st);
+// fp32 CUDA-core GEMM, same convention (pedantic mode), two-level (per 16-k block) accumulation.
+void launch_gemm_f32(const float* A, int64_t lda, bool a_mn, const float* B, int64_t ldb, bool b_mn, int64_t M,
+                     int64_t N, int64_t K, float* C, int64_t ldc, bool accumulate, cudaStream_t st);
+// rows x cols fp32 (pitch ldx) -> up to three bf16 terms (pitch ldt; t1 / t2 may be null).
+void launch_split3(const float* x, int64_t rows, int64_t cols, int64_t ldx, __nv_bfloat16* t0, __nv_bfloat16* t1,
+                   __nv_bfloat16* t2, int64_t ldt, cudaStream_t st);
 void launch_split_bf16x3(const float* u, __nv_bfloat16* u1, __nv_bfloat16* u2, __nv_bfloat16* u3, int64_t n,
                          cudaStream_t st);
 void launch_rows_to_coo(const Shape& s, const int32_t* grow, int64_t Tpad, int64_t T, int32_t* rows,

@@ -18,3 +18,15 @@ def test_reference_cases_through_cpp_dropin(cuda):
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failures" in r.stdout
+
+
+@pytest.mark.parametrize("name", ["hashing", "cache"])
+def test_reference_test_files_unmodified(cuda, name):
+    """The reference's own proj/tests/test_{hashing,cache}.cpp, compiled unmodified against
+    include/ngram (tests/cxx/Makefile, doctest / cpp_int shims) and run on the B200."""
+    exe = os.path.join(ROOT, "tests", "cxx", "_ref_tests", f"test_{name}")
+    assert os.path.exists(exe), "build() compiles tests/cxx/_ref_tests from /root/reference (make -C tests/cxx)"
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(r.stdout[-4000:])
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert "| 0 failed |" in r.stdout
