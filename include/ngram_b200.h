@@ -316,14 +316,17 @@ int ngram_grad_create(ngram_bank* bank, ngram_grad** out); /* zero-initialised *
  * W_cat and LN gradients stay dense.  Needed at LongCat scale, where a dense fp32 copy of
  * the 31.5 B sub-table parameters (126 GB) does not fit beside the tables. */
 #define NGRAM_GRAD_SPARSE_ROWS 1
-/* NGRAM_GRAD_TF32: the two backward GEMMs as single-term TF32 (U rounded to TF32, fp32
- * accumulation) -- ~1.8x faster than the default at LongCat scale; gradients agree with the
- * reference to ~1e-3 relative (training precision), not the 1e-5 fp32 contract. */
+/* Backward GEMM precision on tensor-core banks (X and W_cat are exact bf16 values; only the
+ * fp32 U = d(merged) * 1/denom is split into bf16 terms, products accumulated in fp32):
+ *   default              U in two bf16 terms (17-bit operand, ~2-3e-6 relL2 of pedantic fp32 at
+ *                        D = 3072; the 1e-5 gradient contract holds)
+ *   NGRAM_GRAD_EXACT     three terms (24-bit operand: fp32-accurate, 1.5x the default's MMAs)
+ *   NGRAM_GRAD_TF32      one term (U rounded to bf16: ~1e-3 relative, training precision; the
+ *                        name is kept from the TF32 form it replaces)
+ *   NGRAM_GRAD_PEDANTIC  the fp32 CUDA-core GEMM (also every bank without a tensor-core shape) */
 #define NGRAM_GRAD_TF32 2
-/* NGRAM_GRAD_PEDANTIC: the two backward GEMMs as pedantic fp32 (CUDA cores).  The default
- * runs them fp32-accurate on the tensor cores: X and W_cat are bf16 values, U is split into
- * three bf16 terms (~3e-6 relL2 of pedantic at D = 3072), the default tolerance holds. */
 #define NGRAM_GRAD_PEDANTIC 4
+#define NGRAM_GRAD_EXACT 8
 int ngram_grad_create_ex(ngram_bank* bank, int flags, ngram_grad** out);
 /* Row-sparse gradient view: rows = dev int32 [count] storage rows (the device layout of
  * ngram_grad_tensor(1)), vals = dev f32 [count][branch_dim]; count resets on ngram_grad_zero. */

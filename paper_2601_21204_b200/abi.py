@@ -21,6 +21,7 @@ NGRAM_BWD_SKIP_AMPLIFY = 1
 NGRAM_GRAD_SPARSE_ROWS = 1
 NGRAM_GRAD_TF32 = 2
 NGRAM_GRAD_PEDANTIC = 4
+NGRAM_GRAD_EXACT = 8
 NGRAM_PLNE_FAST = 1
 NGRAM_SHARD_HANDLE_BYTES = 128
 

@@ -5,8 +5,8 @@
 //   amp_bwd   U = fp32(1/denom) * amplify_backward(merged, upstream); g_E0[tok] += U;
 //             layer_norm: g_gain / g_bias                               (backward.cu)
 //   v2:  X    = gathered sub-table rows (f32)                           (backward.cu)
-//        g_W += U^T X            D x D x T   tcgen05 (gemm_gen.cu), U in three bf16 terms
-//        dX   = U W_cat          T x D x D   tcgen05 (gemm_gen.cu), U in three bf16 terms
+//        g_W += U^T X            D x D x T   tcgen05 (gemm_gen.cu), U in bf16 split terms
+//        dX   = U W_cat          T x D x D   tcgen05 (gemm_gen.cu), U in bf16 split terms
 //        (pedantic mode / CUDA-core-shaped banks: the fp32 CUDA-core GEMM of gemm_gen.cu)
 //        g_sub[row_b(t)] += dX[t, b]                                    (backward.cu)
 //   v1:  g_sub[row_b(t)] += U[t]                                        (backward.cu)
@@ -30,6 +30,7 @@ struct ngram_grad {
     DevBuf<float> U, X, dX, wf;            // workspaces
     DevBuf<__nv_bfloat16> X16, Ub;         // bf16x3 mode: bf16 X and the three bf16 terms of U
     int gemm_mode = 0;                     // 0 split-bf16 (default), 1 single-term bf16, 2 pedantic fp32
+    int terms = 2;                         // bf16 terms of U in mode 0 (NGRAM_GRAD_EXACT: 3)
     DevBuf<int32_t> grow;
     int64_t cap = 0;
     bool sparse = false;                 // NGRAM_GRAD_SPARSE_ROWS
@@ -82,8 +83,9 @@ int ngram_grad_create(ngram_bank* b, ngram_grad** out) { return ngram_grad_creat
 
 int ngram_grad_create_ex(ngram_bank* b, int flags, ngram_grad** out) {
     NGRAM_API_BEGIN
-    if (!b || !out || (flags & ~(NGRAM_GRAD_SPARSE_ROWS | NGRAM_GRAD_TF32 | NGRAM_GRAD_PEDANTIC)) ||
-        ((flags & NGRAM_GRAD_TF32) && (flags & NGRAM_GRAD_PEDANTIC)))
+    if (!b || !out ||
+        (flags & ~(NGRAM_GRAD_SPARSE_ROWS | NGRAM_GRAD_TF32 | NGRAM_GRAD_PEDANTIC | NGRAM_GRAD_EXACT)) ||
+        __builtin_popcount(unsigned(flags & (NGRAM_GRAD_TF32 | NGRAM_GRAD_PEDANTIC | NGRAM_GRAD_EXACT))) > 1)
         throw Error(NGRAM_EINVAL, "ngram_grad_create: bad argument");
     if (b->hash_only) throw Error(NGRAM_EINVAL, "bank was created hash-only (NGRAM_BANK_HASH_ONLY)");
     if (b->shard_count != 1) throw Error(NGRAM_EINVAL, "ngram_grad_create: row-sharded banks are not supported");
@@ -99,10 +101,11 @@ int ngram_grad_create_ex(ngram_bank* b, int flags, ngram_grad** out) {
         g->gain.alloc(size_t(s.D));
         g->bias.alloc(size_t(s.D));
     }
-    // 0: U in three bf16 terms on the tensor cores (tensor-core banks: X and W_cat are bf16),
-    // 1 (NGRAM_GRAD_TF32): U rounded to one bf16 term (training precision, 3x fewer products),
+    // 0: U in bf16 split terms on the tensor cores (tensor-core banks: X and W_cat are bf16) --
+    //    two by default, three with NGRAM_GRAD_EXACT; 1 (NGRAM_GRAD_TF32): one bf16 term;
     // 2: the fp32 CUDA-core GEMM (pedantic; also every CUDA-core-shaped bank)
     g->gemm_mode = ((flags & NGRAM_GRAD_PEDANTIC) || !b->tc_path) ? 2 : (flags & NGRAM_GRAD_TF32) ? 1 : 0;
+    g->terms = g->gemm_mode == 1 ? 1 : (flags & NGRAM_GRAD_EXACT) ? 3 : 2;
     zero_all(g.get(), nullptr);
     NGH_CUDA(cudaDeviceSynchronize());
     *out = g.release();
@@ -143,53 +146,52 @@ int ngram_embed_backward(ngram_grad* g, const uint32_t* tokens, const int64_t* s
     if (T == 0) return NGRAM_OK;
     const int64_t Tpad = round_up(T, kRowPad);
     const int D = s.D, B = s.B, d = s.d;
+    const bool tc_terms = B > 0 && s.variant == 1 && g->gemm_mode != 2;  // u goes out as bf16 terms only
     if (T > g->cap) {
-        g->U.alloc(size_t(Tpad) * size_t(D));
+        if (!tc_terms) g->U.alloc(size_t(Tpad) * size_t(D));
         if (s.variant == 1 && B > 0) {
             if (g->gemm_mode == 2) g->X.alloc(size_t(Tpad) * size_t(D));  // fp32 X: pedantic GEMMs only
-            g->dX.alloc(size_t(Tpad) * size_t(D));
+            if (!(tc_terms && g->sparse)) g->dX.alloc(size_t(Tpad) * size_t(D));  // sparse: straight to COO
         }
         g->grow.alloc(size_t(std::max(B, 1)) * size_t(Tpad));
         g->cap = Tpad;
     }
     // K1: storage rows (and token validation: a bad token leaves every gradient untouched)
     ngk::launch_hash_ids(s, b->ht.p, tokens, seq_offsets, nseq, T, prior, nullptr, 0, g->grow.p, g->cap, b->err.p, st);
-    ngk::launch_amp_backward(s, upstream, merged, tokens, T, amp, b->ln_gain.p, g->U.p, g->e0.p, g->gain.p,
-                             g->bias.p, b->err.p, st);
+    const size_t n_td = size_t(T) * size_t(D);
+    if (tc_terms) g->Ub.ensure(size_t(g->terms) * n_td);
+    ngk::launch_amp_backward(s, upstream, merged, tokens, T, amp, b->ln_gain.p, tc_terms ? nullptr : g->U.p, g->e0.p,
+                             g->gain.p, g->bias.p, b->err.p, st, tc_terms ? g->Ub.p : nullptr, g->terms,
+                             int64_t(n_td));
     // Tensor-core banks: X (gathered rows) and W_cat are exact in bf16, so only U is split
     // (three bf16 terms = 24 mantissa bits, or one term in the single-term mode); the products
     // accumulate in fp32 TMEM.  Row-major views in the GEMM convention C[M][N] += A(m,k) B(n,k):
     //   g_W[i][k] += sum_t U[t][i] X[t][k]   A = U (MN-major), B = X (MN-major), K = T
     //   dX[t][k]   = sum_i U[t][i] W[i][k]   A = U (K-major),  B = W_cat (MN-major), K = D
-    if (B > 0 && s.variant == 1 && g->gemm_mode != 2) {
-        const size_t n = size_t(T) * size_t(D);
+    if (tc_terms) {
+        const size_t n = n_td;
         const size_t had = g->X16.n;
         g->X16.ensure(n);
-        // fresh workspace holds arbitrary bits: zero it once, so that after a bad token (U = 0,
+        // fresh workspace holds arbitrary bits: zero it once, so that after a bad token (u = 0,
         // the gather skipped) the products are exact zeros, never 0 * NaN
         if (g->X16.n != had) NGH_CUDA(cudaMemsetAsync(g->X16.p, 0, g->X16.n * sizeof(*g->X16.p), st));
-        const int terms = g->gemm_mode == 0 ? 3 : 1;
-        g->Ub.ensure(size_t(terms) * n);
         ngk::launch_gather_rows(s, g->grow.p, g->cap, T, b->sub.p, g->X16.p, b->err.p, st);
-        ngk::launch_split3(g->U.p, T, D, D, g->Ub.p, terms > 1 ? g->Ub.p + n : nullptr,
-                           terms > 2 ? g->Ub.p + 2 * n : nullptr, D, st);
         Bf16Op u{};
-        u.terms = terms;
+        u.terms = g->terms;
         u.ld = D;
-        for (int h = 0; h < terms; ++h) u.t[h] = g->Ub.p + size_t(h) * n;
+        for (int h = 0; h < g->terms; ++h) u.t[h] = g->Ub.p + size_t(h) * n;
         const Bf16Op x{{g->X16.p, nullptr, nullptr}, 1, true, D};
         const Bf16Op w{{b->wcat.p, nullptr, nullptr}, 1, true, D};
         u.mn = true;
         gemm_bf16_terms(u, x, D, D, T, g->w.p, D, true, b->num_sms, st);
         u.mn = false;
-        gemm_bf16_terms(u, w, T, D, D, g->dX.p, D, false, b->num_sms, st);
-        if (g->sparse) {
+        if (g->sparse) {  // dX [T][B][d] is exactly the appended COO values: the GEMM writes them there
             sparse_reserve(g, T * B, d, st);
-            NGH_CUDA(cudaMemcpyAsync(g->sp_vals.p + size_t(g->sp_count) * size_t(d), g->dX.p,
-                                     size_t(T) * size_t(D) * 4, cudaMemcpyDeviceToDevice, st));
+            gemm_bf16_terms(u, w, T, D, D, g->sp_vals.p + size_t(g->sp_count) * size_t(d), D, false, b->num_sms, st);
             ngk::launch_rows_to_coo(s, g->grow.p, g->cap, T, g->sp_rows.p + g->sp_count, b->err.p, st);
             g->sp_count += T * B;
         } else {
+            gemm_bf16_terms(u, w, T, D, D, g->dX.p, D, false, b->num_sms, st);
             ngk::launch_scatter_rows(s, g->grow.p, g->cap, T, d, D, d, g->dX.p, g->sub.p, b->err.p, st);
         }
     } else if (B > 0 && s.variant == 1) {

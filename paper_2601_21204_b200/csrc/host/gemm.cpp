@@ -27,8 +27,8 @@ void operand_maps(const Bf16Op& X, int64_t R, int64_t K, CUtensorMap (&maps)[3])
 void gemm_bf16_terms(const Bf16Op& A, const Bf16Op& B, int64_t M, int64_t N, int64_t K, float* C, int64_t ldc,
                      bool accumulate, int num_sms, cudaStream_t st) {
     if (M <= 0 || N <= 0) return;
-    if ((A.terms != 1 && A.terms != 3) || (B.terms != 1 && B.terms != 3))
-        throw Error(NGRAM_EINVAL, "gemm: operands have 1 or 3 terms");
+    if (!((A.terms == 1 || A.terms == 3) && (B.terms == 1 || B.terms == 3)) && !(A.terms == 2 && B.terms == 1))
+        throw Error(NGRAM_EINVAL, "gemm: operand terms (1 or 3 each, or 2 x 1)");
     if (K <= 0) {
         if (!accumulate) NGH_CUDA(cudaMemset2DAsync(C, size_t(ldc) * 4, 0, size_t(N) * 4, size_t(M), st));
         return;
@@ -83,8 +83,9 @@ extern "C" int ngram_gemm_f32(int device, int64_t M, int64_t N, int64_t K, const
     NGRAM_API_BEGIN
     if (M < 0 || N < 0 || K < 0 || (M && N && (!C || ldc < N)) || (M && N && K && (!A || !B)))
         throw Error(NGRAM_EINVAL, "ngram_gemm_f32: bad argument");
-    if (a_terms != 0 && ((a_terms != 1 && a_terms != 3) || (b_terms != 1 && b_terms != 3)))
-        throw Error(NGRAM_EINVAL, "ngram_gemm_f32: terms must be 1 or 3 (or a_terms = 0: fp32 CUDA cores)");
+    if (a_terms != 0 && !(((a_terms == 1 || a_terms == 3) && (b_terms == 1 || b_terms == 3)) ||
+                          (a_terms == 2 && b_terms == 1)))
+        throw Error(NGRAM_EINVAL, "ngram_gemm_f32: terms 1 or 3 each, or 2 x 1 (or a_terms = 0: fp32 CUDA cores)");
     if (lda < (a_mn ? M : K) || ldb < (b_mn ? N : K)) throw Error(NGRAM_EINVAL, "ngram_gemm_f32: bad pitch");
     DeviceGuard g(device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);

@@ -9,8 +9,8 @@
 //     (the right operand of dW_cat = U^T X).
 //   * scatter_rows_kernel: the sub-table gradients, g_sub[row_b(t)] += dX[t, b*d:(b+1)*d]
 //     (v2: dX = U W_cat) or += U[t] (v1: averaged rows, embedding.hpp:364-365).
-// The two dense products (dW_cat += U^T X, dX = U W_cat) are plain fp32 GEMMs (cuBLAS,
-// host side).  Accumulation order differs from the reference's sequential loops (atomics),
+// The two dense products (dW_cat += U^T X, dX = U W_cat) run in gemm_gen.cu; on tensor-core
+// banks amp_backward writes u straight as its bf16 split terms (the GEMM operand).  Accumulation order differs from the reference's sequential loops (atomics),
 // so parity is within a stated fp32 tolerance against the reference's double path.
 #include <cuda_bf16.h>
 
@@ -30,29 +30,76 @@ __device__ __forceinline__ float warp_sum(float v) {
 
 constexpr int kBwdWarps = 8;
 
+// u -> the GEMM operand: fp32 (U) and / or `nterms` bf16 split terms (u = t1 + t2 (+ t3), each
+// the bf16 rounding of the remainder; terms[h * tstride + i])
+__device__ __forceinline__ void put_u(float u, int64_t i, float* __restrict__ U, __nv_bfloat16* __restrict__ terms,
+                                      int nterms, int64_t tstride) {
+    if (U) U[i] = u;
+    if (terms) {
+        float r = u;
+        for (int h = 0; h < nterms; ++h) {
+            const __nv_bfloat16 b = __float2bfloat16_rn(r);
+            terms[h * tstride + i] = b;
+            r -= __bfloat162float(b);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kBwdWarps * 32) amp_backward_kernel(
     const float* __restrict__ up, const float* __restrict__ pre, const uint32_t* __restrict__ tokens, int64_t T,
     int D, int amp, float scale, float sqrt_d, const float* __restrict__ gain, float* __restrict__ U,
-    float* __restrict__ g_e0, float* __restrict__ g_gain, float* __restrict__ g_bias,
-    const unsigned long long* __restrict__ err) {
+    __nv_bfloat16* __restrict__ terms, int nterms, int64_t tstride, float* __restrict__ g_e0,
+    float* __restrict__ g_gain, float* __restrict__ g_bias, const unsigned long long* __restrict__ err) {
     extern __shared__ float s_ln[];  // [2][D] gain / bias partials (layer_norm only)
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     if (*err != ~0ull) {  // a bad token: no gradient is produced (hashing.cpp:49-54)
-        // U = 0, so the dense products that follow (library or own GEMMs, which may not read the
-        // error word) add exact zeros to the W_cat gradient instead of stale workspace contents
+        // u = 0, so the dense products that follow (which do not read the error word) add exact
+        // zeros to the W_cat gradient instead of stale workspace contents
         for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < T * D; i += (int64_t)gridDim.x * blockDim.x)
-            U[i] = 0.0f;
+            put_u(0.0f, i, U, terms, nterms, tstride);
         return;
     }
     if (amp == kAmpLN) {
         for (int i = threadIdx.x; i < 2 * D; i += blockDim.x) s_ln[i] = 0.0f;
         __syncthreads();
     }
+    const bool vec = amp != kAmpLN && (D % 4) == 0;
     for (int64_t t = (int64_t)blockIdx.x * kBwdWarps + warp; t < T; t += (int64_t)gridDim.x * kBwdWarps) {
         const float* ur = up + t * D;
-        float* Ur = U + t * D;
         float* g0 = g_e0 + (int64_t)tokens[t] * D;
-        if (amp == kAmpLN) {
+        if (vec) {
+            // 16-byte loads, stores and vector atomics (red.global.add.v4.f32): a quarter of the
+            // atomic operations of the scalar form
+            const bool two = amp == kAmpSqrt;  // reference order: (up * sqrt(D)) * (1/denom)
+            for (int i = 4 * lane; i < D; i += 128) {
+                const float4 x = *reinterpret_cast<const float4*>(ur + i);
+                float4 u;
+                if (two) {
+                    u = make_float4(scale * (x.x * sqrt_d), scale * (x.y * sqrt_d), scale * (x.z * sqrt_d),
+                                    scale * (x.w * sqrt_d));
+                } else {
+                    u = make_float4(scale * x.x, scale * x.y, scale * x.z, scale * x.w);
+                }
+                const int64_t o = t * D + i;
+                if (U) *reinterpret_cast<float4*>(U + o) = u;
+                if (terms) {
+                    float r[4] = {u.x, u.y, u.z, u.w};
+                    for (int h = 0; h < nterms; ++h) {
+                        __nv_bfloat162 lo = __floats2bfloat162_rn(r[0], r[1]);
+                        __nv_bfloat162 hi = __floats2bfloat162_rn(r[2], r[3]);
+                        uint2 pk;
+                        pk.x = *reinterpret_cast<uint32_t*>(&lo);
+                        pk.y = *reinterpret_cast<uint32_t*>(&hi);
+                        *reinterpret_cast<uint2*>(terms + h * tstride + o) = pk;
+                        r[0] -= __low2float(lo);
+                        r[1] -= __high2float(lo);
+                        r[2] -= __low2float(hi);
+                        r[3] -= __high2float(hi);
+                    }
+                }
+                atomicAdd(reinterpret_cast<float4*>(g0 + i), u);
+            }
+        } else if (amp == kAmpLN) {
             const float* pr = pre + t * D;
             float sum = 0.0f;
             for (int i = lane; i < D; i += 32) sum += pr[i];
@@ -79,14 +126,13 @@ __global__ void __launch_bounds__(kBwdWarps * 32) amp_backward_kernel(
                 const float xhat = (pr[i] - mean) * inv_std;
                 const float s = ur[i] * gain[i];
                 const float u = scale * ((s - mean_s - xhat * mean_sx) * inv_std);
-                Ur[i] = u;
+                put_u(u, t * D + i, U, terms, nterms, tstride);
                 atomicAdd(&g0[i], u);
             }
         } else {
-            const float m = amp == kAmpSqrt ? sqrt_d : 1.0f;
             for (int i = lane; i < D; i += 32) {
-                const float u = scale * (amp == kAmpSqrt ? ur[i] * m : ur[i]);
-                Ur[i] = u;
+                const float u = scale * (amp == kAmpSqrt ? ur[i] * sqrt_d : ur[i]);
+                put_u(u, t * D + i, U, terms, nterms, tstride);
                 atomicAdd(&g0[i], u);
             }
         }
@@ -230,7 +276,8 @@ int grid_for(int64_t n, int threads) {
 
 void launch_amp_backward(const Shape& s, const float* up, const float* pre, const uint32_t* tokens, int64_t T,
                          int amp, const float* gain, float* U, float* g_e0, float* g_gain, float* g_bias,
-                         const unsigned long long* err, cudaStream_t st) {
+                         const unsigned long long* err, cudaStream_t st, __nv_bfloat16* terms, int nterms,
+                         int64_t tstride) {
     if (T <= 0) return;
     const float scale = 1.0f / (float)s.denom;  // T(1) / T(denom), embedding.hpp:350
     const float sqrt_d = (float)__builtin_sqrt((double)s.D);
@@ -240,7 +287,8 @@ void launch_amp_backward(const Shape& s, const float* up, const float* pre, cons
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(amp_backward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     amp_backward_kernel<<<(unsigned)blocks, kBwdWarps * 32, smem, st>>>(up, pre, tokens, T, s.D, amp, scale, sqrt_d,
-                                                                        gain, U, g_e0, g_gain, g_bias, err);
+                                                                        gain, U, terms, nterms, tstride, g_e0, g_gain,
+                                                                        g_bias, err);
     count_launch();
 }
 

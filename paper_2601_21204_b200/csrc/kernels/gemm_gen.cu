@@ -49,8 +49,8 @@ constexpr int kGemmThreads = (2 + kEpiWarpsG) * 32;
 constexpr int kMmaWarpG = 1 + kEpiWarpsG;
 // k-blocks per TMEM accumulation chunk: one k-block when there are six products (the five
 // small ones are issued first, into a still-tiny accumulator, then the big a1 b1 -- so only its
-// four MMAs meet a large accumulator), two with three, eight for a single product.
-constexpr int chunk_kb(int pairs) { return pairs >= 6 ? 1 : pairs >= 3 ? 2 : 8; }
+// four MMAs meet a large accumulator), four with two or three, eight for a single product.
+constexpr int chunk_kb(int pairs) { return pairs >= 6 ? 1 : pairs >= 2 ? 4 : 8; }
 constexpr int kSmemBudget = 200 * 1024;
 
 constexpr int gstages(int na, int nb) {
@@ -247,14 +247,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                 mbar_wait(&tfull[acc], acc_phase);
                 tc_fence_after();
 #pragma unroll
-                for (int c = 0; c < GBN / 2 / 32; ++c) {
-                    uint32_t v[32];
-                    tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) +
-                                           (uint32_t)(acc * GBN + half * (GBN / 2) + c * 32),
-                                       v);
+                for (int c = 0; c < GBN / 2 / 32; c += 2) {  // two loads in flight per wait
+                    uint32_t v[2][32];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+                        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) +
+                                               (uint32_t)(acc * GBN + half * (GBN / 2) + (c + h) * 32),
+                                           v[h]);
                     tmem_ld_wait();
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) sum[c * 32 + j] += __uint_as_float(v[j]);
+                    for (int h = 0; h < 2; ++h)
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) sum[(c + h) * 32 + j] += __uint_as_float(v[h][j]);
                 }
                 tc_fence_before();
                 __syncwarp();
@@ -407,6 +411,7 @@ void launch_gemm_bf16_terms(const CUtensorMap* ma, int na, bool a_mn, const CUte
     const GemmParams p{M, N, K, C, ldc, accumulate ? 1 : 0};
     if (na == 1 && nb == 1) dispatch_major<1, 1>(ma, mb, a_mn, b_mn, p, num_sms, st);
     else if (na == 3 && nb == 1) dispatch_major<3, 1>(ma, mb, a_mn, b_mn, p, num_sms, st);
+    else if (na == 2 && nb == 1) dispatch_major<2, 1>(ma, mb, a_mn, b_mn, p, num_sms, st);
     else if (na == 1 && nb == 3) dispatch_major<1, 3>(ma, mb, a_mn, b_mn, p, num_sms, st);
     else dispatch_major<3, 3>(ma, mb, a_mn, b_mn, p, num_sms, st);
 }

@@ -71,9 +71,11 @@ void launch_fill_f32(float* dst, float v, int64_t n, cudaStream_t st);
 
 // ---- forward
 // ---- backward (backward.cu): embed_sequence_backward's scatter / elementwise parts
+// U (fp32, may be null) and / or `nterms` bf16 split terms of u (terms + h * tstride, may be null).
 void launch_amp_backward(const Shape& s, const float* up, const float* pre, const uint32_t* tokens, int64_t T,
                          int amp, const float* gain, float* U, float* g_e0, float* g_gain, float* g_bias,
-                         const unsigned long long* err, cudaStream_t st);
+                         const unsigned long long* err, cudaStream_t st, __nv_bfloat16* terms = nullptr,
+                         int nterms = 0, int64_t tstride = 0);
 void launch_gather_rows_f32(const Shape& s, const int32_t* grow, int64_t Tpad, int64_t T, const __nv_bfloat16* sub,
                             float* X, const unsigned long long* err, cudaStream_t st);
 void launch_scatter_rows(const Shape& s, const int32_t* grow, int64_t Tpad, int64_t T, int width, int src_stride,

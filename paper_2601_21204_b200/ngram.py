@@ -413,12 +413,13 @@ class GradBank:
     """fp32 gradient accumulator of a DeviceBank (embedding_bank_t<T>& grads of
     embed_sequence_backward, embedding.hpp:438-459), zero-initialised, device layout."""
 
-    def __init__(self, bank: DeviceBank, sparse_rows: bool = False, tf32: bool = False, pedantic: bool = False):
+    def __init__(self, bank: DeviceBank, sparse_rows: bool = False, tf32: bool = False, pedantic: bool = False,
+                 exact: bool = False):
         self.bank = bank
         self.sparse_rows = sparse_rows
         h = C.c_void_p()
         flags = ((abi.NGRAM_GRAD_SPARSE_ROWS if sparse_rows else 0) | (abi.NGRAM_GRAD_TF32 if tf32 else 0) |
-                 (abi.NGRAM_GRAD_PEDANTIC if pedantic else 0))
+                 (abi.NGRAM_GRAD_PEDANTIC if pedantic else 0) | (abi.NGRAM_GRAD_EXACT if exact else 0))
         check(abi.lib().ngram_grad_create_ex(bank.handle, flags, C.byref(h)))
         self.handle = h
 

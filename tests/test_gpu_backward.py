@@ -68,7 +68,7 @@ def test_skip_amplify_takes_d_merged(cuda):  # embed_backward alone (embedding.h
     assert_grads_close(b.download(), a.download(), ln)
 
 
-@pytest.mark.parametrize("mode", [{}, {"tf32": True}, {"pedantic": True}])
+@pytest.mark.parametrize("mode", [{}, {"exact": True}, {"tf32": True}, {"pedantic": True}])
 def test_out_of_range_token_leaves_gradients_untouched(cuda, mode):  # hashing.cpp:49-54
     """A bad call leaves EVERY gradient -- E0, sub-tables and the projection (W_cat) -- exactly as
     it was, including after a good call filled the GEMM workspaces with that call's operands."""
@@ -206,9 +206,9 @@ def test_longcat_scale_sparse_backward_sampled(cuda):
 
 
 def test_default_gemms_match_pedantic_at_width(cuda):
-    """At D = 3072 (K = 3072 / T = 1024 accumulations) the default split-bf16 tensor-core GEMMs
-    give the pedantic fp32 gradients to within 1e-5 relL2 (measured ~1e-6 for W_cat, ~3e-6 for
-    the sub-table rows); single-term TF32 is ~2e-4 (why it is opt-in)."""
+    """At D = 3072 (K = 3072 / T = 1024 accumulations) the default tensor-core GEMMs (U in two
+    bf16 terms) give the pedantic fp32 gradients to within 1e-5 relL2, and NGRAM_GRAD_EXACT
+    (three terms) to within 2e-6; the single-term mode is ~1e-3 (why it is opt-in)."""
     cfg = O.make_default_config(2000, 3072, 4, 4)
     db = G.DeviceBank(cfg).generate(3)
     T = 1024
@@ -217,12 +217,14 @@ def test_default_gemms_match_pedantic_at_width(cuda):
     off = torch.tensor([0, 512, T], dtype=torch.int64, device=cuda)
     up = torch.randn((T, 3072), device=cuda, generator=gen)
     res = {}
-    for name, kw in (("default", {}), ("pedantic", {"pedantic": True})):
+    for name, kw in (("default", {}), ("exact", {"exact": True}), ("pedantic", {"pedantic": True})):
         gb = G.GradBank(db, **kw)
         gb.backward(toks, off, up)
         db.sync_errors()
         d = gb.download()
         res[name] = (np.stack(d["proj"]).astype(np.float64), np.concatenate(d["sub"]).astype(np.float64))
         gb.close()
-    for a, b in zip(res["default"], res["pedantic"]):
-        assert np.linalg.norm(a - b) / np.linalg.norm(b) < 1e-5
+    errs = {k: [np.linalg.norm(a - b) / np.linalg.norm(b) for a, b in zip(res[k], res["pedantic"])]
+            for k in ("default", "exact")}
+    print("relL2 vs pedantic (W_cat, sub rows):", errs)
+    assert max(errs["default"]) < 1e-5 and max(errs["exact"]) < 2e-6, errs

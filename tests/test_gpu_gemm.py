@@ -30,7 +30,7 @@ def _operand(R, K, mn, gen, bf16_exact=False):
 
 @pytest.mark.parametrize("a_mn", [False, True])
 @pytest.mark.parametrize("b_mn", [False, True])
-@pytest.mark.parametrize("terms", [(3, 1), (3, 3), (1, 3), (1, 1), (0, 0)])
+@pytest.mark.parametrize("terms", [(3, 1), (2, 1), (3, 3), (1, 3), (1, 1), (0, 0)])
 def test_gemm_layouts_and_terms(cuda, a_mn, b_mn, terms):
     gen = torch.Generator(device="cuda").manual_seed(7)
     M, N, K = 520, 264, 392  # ragged in every dimension (tiles 256 x 256 x 64)
@@ -43,7 +43,7 @@ def test_gemm_layouts_and_terms(cuda, a_mn, b_mn, terms):
     torch.cuda.synchronize()
     ref = C0[:, :N].double() + Ad @ Bd.t()
     err = float((Cm[:, :N].double() - ref).norm() / ref.norm())
-    assert err < 1e-6, err
+    assert err < (5e-6 if at == 2 else 1e-6), err  # two terms: a 17-bit operand
     assert torch.equal(Cm[:, N:], C0[:, N:]), "wrote past N"
 
 
