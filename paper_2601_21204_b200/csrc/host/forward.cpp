@@ -43,6 +43,25 @@ static bool fused_gather(int D) {
     return env != 0;
 }
 
+// Prefill path for the pair kernel (D % 256 == 0, T beyond the split-K regime):
+//   "x"   (default) fused K1+K2 kernel writes X, K3 reads it (two launches, X round trip)
+//   "lsu" token validation, then K3 alone with K1+K2 in its producers (hash + cp.async rows
+//         into shared memory; the peer CTA's stages relayed to the leader): no X, no
+//         storage-row array.  Bit-identical, but measured slower (profiles/README.md):
+//         config B 205 vs 150 us, C 1.30 vs 1.02 ms -- every n-tile pair re-gathers its
+//         m-block's rows as 128-byte L2 requests (12x at D = 3072) where the X path moves the
+//         same bytes as 16 KB TMA tiles; tensor pipe 33 % active vs 66 % (ncu).
+// NGRAM_PREFILL_PATH selects.
+static bool lsu_prefill(const ngram_bank* b) {
+    static const int env = [] {
+        const char* e = getenv("NGRAM_PREFILL_PATH");
+        return e ? (std::string(e) == "lsu" ? 1 : std::string(e) == "x" ? 0 : -1) : -1;
+    }();
+    const auto& s = b->shape;
+    if (!b->tc_path || s.D % 256 != 0 || s.N > 8 || s.variant != 1 || s.B < 1) return false;
+    return env == 1;
+}
+
 // Entry points that gather rows themselves need every row on this device: a row-sharded bank
 // (shard_count > 1) holds only its row block, its forward runs through the shard group.
 static void require_unsharded(const ngram_bank* b, const char* what) {
@@ -173,6 +192,15 @@ bool forward_tokens(ngram_bank* b, const uint32_t* tokens, const int64_t* seq_of
         const HashCtx hc{seq_off, nseq, prior};
         run_projection(b, tokens, nullptr, Tpad, T, rows, merged, out_bf16, b->ws.merged_f32.p, nullptr, st, amp,
                        nullptr, true, fused_commit ? commit : nullptr, &hc);
+    } else if (!(allow_splitk && small_t(b, T)) && lsu_prefill(b) && !fused_gather(b->shape.D)) {
+        // K1+K2 fused into the projection's producers; a bad token must still abort the call
+        // before any output, so the range check runs first (the kernel returns on the error word)
+        ngk::launch_validate_tokens(b->shape, tokens, T, seq_off, nseq, prior, b->err.p, st);
+        b->prof_record(1, st);
+        const HashCtx hc{seq_off, nseq, prior};
+        fused_commit = commit != nullptr;
+        run_projection(b, tokens, nullptr, Tpad, T, rows, merged, out_bf16, b->ws.merged_f32.p, nullptr, st, amp,
+                       nullptr, allow_splitk, fused_commit ? commit : nullptr, &hc);
     } else if (b->tc_path && ((allow_splitk && small_t(b, T)) || !fused_gather(b->shape.D))) {
         if (!xb) xb = &b->ws.xbuf;
         xb->ensure(Tpad, b->shape.D);

@@ -69,6 +69,7 @@ struct TcParams {
     float scale, amp;
     const unsigned long long* err;
     int use_x;  // A operand from materialised X (tmap_a is X) instead of gathered sub-table rows
+    int hash_lsu;  // pair kernel: producers hash the windows and cp.async the rows (K1+K2+K3 in one)
     int epi_skip;  // diagnostics only (NGRAM_DEBUG_EPI_SKIP): 1 drain TMEM without loads/stores,
                    // 2 (pair kernel) skip the E0 loads, 3 (pair kernel) skip the output stores
     int diag_skip_a;  // diagnostics only (NGRAM_DEBUG_SKIP_A): X-path pair kernel loads W tiles only
@@ -536,7 +537,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::kThreads, 1)
     uint64_t* tfull = empty + kStages2;
     uint64_t* tempty = tfull + 2;
     uint64_t* e0bar = tempty + 2;  // [kEpiWarps2][ring] E0 ring slots (mode 1)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(e0bar + epi_ring(EPI) * kEpiWarps2);
+    uint64_t* lfull = e0bar + epi_ring(EPI) * kEpiWarps2;  // hash_lsu: the peer's own stage barriers
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lfull + kStages2);
 
     if (*p.err != ~0ull) return;  // uniform across the grid
 
@@ -555,7 +557,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::kThreads, 1)
 
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < kStages2; ++i) {
-            mbar_init(&full[i], p.use_x ? 1 : NP2);  // leader's: one arrive per leader producer warp
+            // leader's: X path one (expect_tx); gather4 path one per leader producer warp; hash_lsu
+            // one cp.async arrival per leader producer thread + the peer's relay + the W expect_tx
+            mbar_init(&full[i], p.use_x ? 1 : p.hash_lsu ? NP2 * 32 + 2 : NP2);
+            mbar_init(&lfull[i], NP2 * 32);  // hash_lsu, peer CTA: its producer threads' cp.async
             mbar_init(&empty[i], 1);                 // leader's multicast commit
         }
         for (int i = 0; i < 2; ++i) {
@@ -580,12 +585,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::kThreads, 1)
         uint32_t phase = 0;
         const uint64_t pol_w = policy_evict_last();
         const int r0 = warp * C::kRowsPerWarp;
-        for (int64_t tile = pair; tile < tiles; tile += npairs) {
+        for (int64_t tile = pair; p.use_x && tile < tiles; tile += npairs) {
             const int64_t m = tile / nN;
             const int n = (int)(tile - m * nN);
             const int64_t t0 = m * BM2 + (int64_t)rank * 128;  // this CTA's first token row
             const int wrow = n * BN2 + (int)rank * (BN2 / 2);  // this CTA's first W row
-            if (p.use_x) {
+            {
                 for (int kb = 0; kb < KB; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (warp == 0 && lane == 0) {
@@ -603,34 +608,162 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::kThreads, 1)
                         phase ^= 1;
                     }
                 }
-                continue;
             }
-            for (int b = 0; b < p.s.B; ++b) {
-                int4 rows4 = make_int4(0, 0, 0, 0);
-                if (lane < C::kRowsPerWarp / 4)
-                    rows4 = *reinterpret_cast<const int4*>(p.grow + (int64_t)b * p.Tpad + t0 + r0 + 4 * lane);
-                for (int c = 0; c < KPB; ++c) {
-                    mbar_wait(&empty[stage], phase ^ 1);
-                    uint8_t* a_dst = smem + stage * C::kStageBytes;
-                    if (leader && lane == 0)  // expect this warp's rows of BOTH CTAs (+ both W halves)
-                        mbar_arrive_expect_tx(&full[stage], 2 * (C::kRowsPerWarp * BK * 2) +
-                                                                (warp == 0 ? 2 * C::kBBytes : 0));
-                    __syncwarp();
-                    if (lane < C::kRowsPerWarp / 4)
-                        tma_gather4_2cta(a_dst + (r0 + 4 * lane) * (BK * 2), &tmap_a, leader_bar(&full[stage]),
-                                         c * BK, rows4.x, rows4.y, rows4.z, rows4.w);
-                    if (warp == 0 && lane == 0)
-                        tma_load_2d_2cta(a_dst + C::kABytes, &tmap_w, leader_bar(&full[stage]), (b * KPB + c) * BK,
-                                         wrow, pol_w);
-                    if (++stage == kStages2) {
-                        stage = 0;
-                        phase ^= 1;
+        }
+        if (p.hash_lsu) {
+            // K1 + K2 in the producers (no X, no grow): lane l of producer warp w owns tile row
+            // r = 32 w + l -- it loads its window once per tile, hashes one branch per d-wide
+            // slab, and the warp copies its 32 rows of each 64-column K-block with cp.async
+            // (4 rows x 8 16-byte chunks per instruction: every 128-byte row segment is one
+            // coalesced request) into the SWIZZLE_128B A slab.  Completion is signalled by the
+            // copies themselves (cp.async.mbarrier.arrive.noinc): the producer never waits on its
+            // own loads, so as many K-blocks are in flight as there are free stages.  The leader's
+            // threads arrive on its full barrier directly; the peer's arrive on a local barrier
+            // that the peer's (otherwise idle) MMA warp relays to the leader -- a remote arrive
+            // from a thread with cp.async in flight would fence on all of them (measured: the
+            // release-cluster arrive serialised every stage).  Tokens were range-checked by the
+            // validation kernel before this launch (a bad call produces no output).
+            const int rw = warp * 32;
+            const int q = lane & 7;
+            uint64_t* arrive_bar = leader ? full : lfull;  // the peer's rows are relayed (MMA warp)
+            // L2 prefetch of the rows PB branches ahead (crossing into the next tile): the
+            // random-row DRAM latency is paid by the prefetch, the cp.async of a stage hits L2 --
+            // four smem stages alone cover ~1 us of load latency, the random rows take longer
+            const int PB = (4 + KPB - 1) / KPB;
+            const int rowbytes = p.s.d * 2;
+            auto window_of = [&](int64_t tile, uint32_t (&w)[kMaxDecodeN]) {
+                if (tile >= tiles) return false;
+                const int64_t t = (tile / nN) * BM2 + (int64_t)rank * 128 + rw + lane;
+                return t < p.T && load_window<kMaxDecodeN>(p.s, p.tokens, p.seq_off, p.nseq, p.prior, t, w);
+            };
+            auto prefetch_row = [&](bool okw, const uint32_t (&w)[kMaxDecodeN], int b) {
+                if (!okw) return;
+                const int32_t r = storage_row(p.ht, b, branch_hash<kMaxDecodeN>(p.s, p.ht, w, b), nullptr);
+                const char* base = reinterpret_cast<const char*>(p.sub + (int64_t)r * p.s.d);
+                for (int o = 0; o < rowbytes; o += 128) prefetch_l2(base + o);
+            };
+            uint32_t win[kMaxDecodeN], nwin[kMaxDecodeN];
+            bool ok = window_of(pair, win);
+            constexpr bool kPrefetchL2 = false;  // measured slower (B 205 -> 339 us, C 1.95 -> 2.38 ms)
+            for (int b = 0; kPrefetchL2 && b < PB && b < p.s.B; ++b) prefetch_row(ok, win, b);
+            for (int64_t tile = pair; tile < tiles; tile += npairs) {
+                const int64_t m = tile / nN;
+                const int n = (int)(tile - m * nN);
+                const int wrow = n * BN2 + (int)rank * (BN2 / 2);
+                const bool nok = window_of(tile + npairs, nwin);
+                for (int b = 0; b < p.s.B; ++b) {
+                    const int32_t row1 = ok ? storage_row(p.ht, b, branch_hash<kMaxDecodeN>(p.s, p.ht, win, b), nullptr)
+                                            : 0;  // rows past T: any valid row (never stored)
+                    if (kPrefetchL2) {
+                        if (b + PB < p.s.B) prefetch_row(ok, win, b + PB);
+                        else prefetch_row(nok, nwin, b + PB - p.s.B);
+                    }
+                    for (int c = 0; c < KPB; ++c) {
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        uint8_t* a_dst = smem + stage * C::kStageBytes;
+                        if (warp == 0 && lane == 0) {
+                            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * C::kBBytes);
+                            tma_load_2d_2cta(a_dst + C::kABytes, &tmap_w, leader_bar(&full[stage]),
+                                             (b * KPB + c) * BK, wrow, pol_w);
+                        }
+                        const uint32_t a_base = smem_u32(a_dst);
+                        const __nv_bfloat16* col = p.sub + c * BK + q * 8;
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const int rl = 4 * j + (lane >> 3);
+                            const int r = rw + rl;
+                            const int32_t src = __shfl_sync(0xffffffffu, row1, rl);
+                            cp_async_16(a_base + r * 128 + ((q ^ (r & 7)) << 4), col + (int64_t)src * p.s.d);
+                        }
+                        cp_async_mbar_arrive_noinc(&arrive_bar[stage]);
+                        if (++stage == kStages2) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                    }
+                }
+                ok = nok;
+#pragma unroll
+                for (int j = 0; j < kMaxDecodeN; ++j) win[j] = nwin[j];
+            }
+            cp_async_wait<0>();
+        } else if (!p.use_x) {
+            // Gather producers: the storage rows of (tile, branch) unit u are loaded kAhead units
+            // ahead (across tile boundaries), so a stage only issues gathers -- a row-index load
+            // per stage put a global-memory latency (~0.7 us) on every K-block, against 0.26 us
+            // of MMA per stage at D = 768 (the fused path ran at 43 % of the X path's speed).
+            constexpr int kAhead = 4;
+            const int B = p.s.B;
+            const int64_t my_tiles = pair < tiles ? (tiles - pair + npairs - 1) / npairs : 0;
+            const int64_t units = my_tiles * B;
+            auto load_unit = [&](int64_t u) {
+                int4 r = make_int4(0, 0, 0, 0);
+                if (u < units && lane < C::kRowsPerWarp / 4) {
+                    const int64_t tile = pair + (u / B) * npairs;
+                    const int64_t t0 = (tile / nN) * BM2 + (int64_t)rank * 128;
+                    r = *reinterpret_cast<const int4*>(p.grow + (int64_t)(u % B) * p.Tpad + t0 + r0 + 4 * lane);
+                }
+                return r;
+            };
+            int4 rq[kAhead];
+#pragma unroll
+            for (int j = 0; j < kAhead; ++j) rq[j] = load_unit(j);
+            for (int64_t u0 = 0; u0 < units; u0 += kAhead) {
+#pragma unroll
+                for (int j = 0; j < kAhead; ++j) {
+                    const int64_t u = u0 + j;
+                    if (u >= units) break;
+                    const int4 rows4 = rq[j];
+                    rq[j] = load_unit(u + kAhead);
+                    const int64_t tile = pair + (u / B) * npairs;
+                    const int b = (int)(u % B);
+                    const int n = (int)(tile % nN);
+                    const int wrow = n * BN2 + (int)rank * (BN2 / 2);
+                    for (int c = 0; c < KPB; ++c) {
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        uint8_t* a_dst = smem + stage * C::kStageBytes;
+                        if (leader && lane == 0)  // expect this warp's rows of BOTH CTAs (+ both W halves)
+                            mbar_arrive_expect_tx(&full[stage], 2 * (C::kRowsPerWarp * BK * 2) +
+                                                                    (warp == 0 ? 2 * C::kBBytes : 0));
+                        __syncwarp();
+                        if (lane < C::kRowsPerWarp / 4)
+                            tma_gather4_2cta(a_dst + (r0 + 4 * lane) * (BK * 2), &tmap_a, leader_bar(&full[stage]),
+                                             c * BK, rows4.x, rows4.y, rows4.z, rows4.w);
+                        if (warp == 0 && lane == 0)
+                            tma_load_2d_2cta(a_dst + C::kABytes, &tmap_w, leader_bar(&full[stage]),
+                                             (b * KPB + c) * BK, wrow, pol_w);
+                        if (++stage == kStages2) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
                     }
                 }
             }
         }
     } else if (warp == kMmaWarp) {
         // ------------------------------------------------------------ MMA issuer (leader only)
+        if (!leader && p.hash_lsu) {
+            // relay: each stage's rows of this CTA landed (its producers' cp.async arrivals) ->
+            // ordered for the async proxy -> one arrive on the leader's full barrier
+            if (lane == 0) {
+                int stage = 0;
+                uint32_t phase = 0;
+                const int64_t steps = (pair < tiles ? (tiles - pair + npairs - 1) / npairs : 0) * KB;
+                for (int64_t i = 0; i < steps; ++i) {
+                    mbar_wait(&lfull[stage], phase);
+                    fence_proxy_async_smem();
+                    // the rows are complete and fenced for this SM's tensor core (which reads them
+                    // for the pair MMA): a relaxed arrive suffices and avoids a GPU-scope MEMBAR
+                    // per stage (measured: the release arrive serialised the peer's stages)
+                    mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(&full[stage]), 0));
+                    if (++stage == kStages2) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+            __syncwarp();
+        }
         if (leader) {
             constexpr uint32_t idesc = idesc_bf16_f32(BM2, BN2);
             int stage = 0;
@@ -644,6 +777,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::kThreads, 1)
                 for (int kb = 0; kb < KB; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
+                    if (p.hash_lsu) fence_proxy_async_smem();  // the producers' cp.async rows -> async proxy
                     if (lane == 0) {
                         const uint32_t a_addr = smem_u32(smem + stage * C::kStageBytes);
                         const uint64_t adesc = smem_desc_sw128(a_addr);
@@ -952,6 +1086,11 @@ void launch_tc2(const FwdArgs& a, int num_sms, cudaStream_t st) {
     p.amp = a.s.amp == kAmpSqrt ? (float)__builtin_sqrt((double)a.s.D) : 1.0f;
     p.err = a.err;
     p.use_x = a.tmap_x != nullptr;
+    p.hash_lsu = !p.use_x && a.seq_off != nullptr;
+    p.ht = a.ht;
+    p.seq_off = a.seq_off;
+    p.nseq = a.nseq;
+    p.prior = a.prior;
     p.epi_skip = debug_epi_skip();
     p.diag_skip_a = debug_skip_a();
     const int64_t tiles = ((a.T + BM2 - 1) / BM2) * (a.s.D / BN2);

@@ -378,10 +378,14 @@ def test_verify_sized_regime_at_longcat_width(cuda):
     assert torch.equal(a01, rows[:500])  # T = 500 and T = 600: same regime, same bits
 
 
-def test_fused_gather_variant_is_bit_identical(cuda):
-    """The opt-in fused-gather GEMM (A rows gathered by tile::gather4 straight into shared
-    memory, NGRAM_FUSED_GATHER=1, selected once per process) feeds the tensor cores the same
-    bf16 rows in the same K order as the default X path: identical bits (D = 768, T = 900)."""
+@pytest.mark.parametrize("env", [{"NGRAM_FUSED_GATHER": "1"}, {"NGRAM_PREFILL_PATH": "lsu"},
+                                 {"NGRAM_PREFILL_PATH": "x"}])
+def test_fused_gather_variant_is_bit_identical(cuda, env):
+    """Every prefill producer variant -- A rows gathered by tile::gather4 straight into shared
+    memory (NGRAM_FUSED_GATHER=1), hashed and cp.async-copied by the projection's own producers
+    (NGRAM_PREFILL_PATH=lsu), or materialised as X by the K1+K2 kernel (x) -- feeds the tensor
+    cores the same bf16 rows in the same K order: identical bits (D = 768, T = 900, with a
+    carried prior context).  Selected once per process, hence the subprocesses."""
     import os, subprocess, sys, tempfile
     code = f"""
 import sys, numpy as np, torch
@@ -394,15 +398,16 @@ cfg = O.make_default_config(3000, 768, 4, 4)
 hb = O.make_bank(cfg, 29, round_bf16=True)
 db = G.DeviceBank(cfg).upload(hb.base, hb.sub, hb.proj)
 toks = O.uniform_tokens(83, 3000, 900)
-r, m = G.embed_forward(db, dev_u32(torch, toks, "cuda:0"), dev_i64(torch, [0, 400, 900], "cuda:0"), merged=True)
+prior = dev_u32(torch, np.array([[5, 6, 7], [2900, 1, 17]], np.uint32), "cuda:0")
+r, m = G.embed_forward(db, dev_u32(torch, toks, "cuda:0"), dev_i64(torch, [0, 400, 900], "cuda:0"), merged=True,
+                       prior=prior)
 db.sync_errors()
 np.save(sys.argv[1], torch.stack([r, m]).view(torch.int32).cpu().numpy())
 """
     outs = []
     with tempfile.TemporaryDirectory() as td:
-        for v in ("0", "1"):
-            path = os.path.join(td, f"o{v}.npy")
-            subprocess.run([sys.executable, "-c", code, path], check=True, timeout=300,
-                           env={**os.environ, "NGRAM_FUSED_GATHER": v})
+        for i, e in enumerate(({"NGRAM_FUSED_GATHER": "0", "NGRAM_PREFILL_PATH": "x"}, env)):
+            path = os.path.join(td, f"o{i}.npy")
+            subprocess.run([sys.executable, "-c", code, path], check=True, timeout=300, env={**os.environ, **e})
             outs.append(np.load(path))
     assert np.array_equal(outs[0], outs[1])
