@@ -1158,29 +1158,60 @@ int producer_mode() {
 }  // namespace
 
 // Split-K reduction + epilogue: out = amp((E0[tok] + sum_s partial[s]) * 1/denom); the
-// partials are summed in split order (deterministic).
-__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ partial, int S, int64_t T, int D,
+// partials are summed in split order (deterministic).  Latency shape (decode / verify): the
+// E0 row is gathered BEFORE the programmatic-launch wait (tokens and E0 do not depend on the
+// GEMM; a token >= V0 reads row 0, its output is never written), and the S partial loads are
+// issued back to back (independent, one L2 round trip instead of S); 128-thread blocks spread
+// a small batch over more SMs.
+constexpr int kReduceThreads = 128;
+constexpr int kReduceMaxS = 8;
+__global__ void __launch_bounds__(kReduceThreads) splitk_reduce_kernel(const float* __restrict__ partial, int S,
+                                                                       int64_t T, int D,
                                                             const uint32_t* __restrict__ tokens,
-                                                            const __nv_bfloat16* __restrict__ e0, float scale,
-                                                            float amp, int write_rows, void* rows, void* merged,
-                                                            int out_bf16, const unsigned long long* err,
-                                                            DecodeCommit commit) {
+                                                            const __nv_bfloat16* __restrict__ e0, uint32_t V0,
+                                                            float scale, float amp, int write_rows, void* rows,
+                                                            void* merged, int out_bf16,
+                                                            const unsigned long long* err, DecodeCommit commit) {
+    const int64_t n4 = T * D / 4;
+    const int64_t v0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint2 eb0 = make_uint2(0, 0);
+    if (v0 < n4) {  // first element's E0 chunk, ahead of the GEMM's completion
+        const int64_t t = v0 * 4 / D;
+        const uint32_t tok = __ldg(tokens + t);
+        eb0 = __ldg(reinterpret_cast<const uint2*>(e0 + (int64_t)(tok < V0 ? tok : 0u) * D + (v0 * 4 - t * D)));
+    }
     griddep_wait();  // PDL launch: the split-K GEMM has completed (no-op for a normal launch)
     if (commit.ring && blockIdx.x == 0) decode_commit_block(commit, err);  // fused decode-state commit
     const bool bad = *err != ~0ull;  // a token was out of range: no output (uniform)
-    const int64_t n4 = bad ? 0 : T * D / 4;
-    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n4; v += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t v = v0; !bad && v < n4; v += (int64_t)gridDim.x * blockDim.x) {
         const int64_t t = v * 4 / D;
         const int i = (int)(v * 4 - t * D);
-        float4 acc = reinterpret_cast<const float4*>(partial)[v];
-        for (int s = 1; s < S; ++s) {
-            const float4 q = reinterpret_cast<const float4*>(partial + (int64_t)s * T * D)[v];
-            acc.x += q.x;
-            acc.y += q.y;
-            acc.z += q.z;
-            acc.w += q.w;
+        float4 acc;
+        if (S <= kReduceMaxS) {
+            float4 q[kReduceMaxS];
+#pragma unroll
+            for (int s = 0; s < kReduceMaxS; ++s)
+                if (s < S) q[s] = __ldcg(reinterpret_cast<const float4*>(partial + (int64_t)s * T * D) + v);
+            acc = q[0];
+#pragma unroll
+            for (int s = 1; s < kReduceMaxS; ++s)
+                if (s < S) {
+                    acc.x += q[s].x;
+                    acc.y += q[s].y;
+                    acc.z += q[s].z;
+                    acc.w += q[s].w;
+                }
+        } else {
+            acc = reinterpret_cast<const float4*>(partial)[v];
+            for (int s = 1; s < S; ++s) {
+                const float4 q = reinterpret_cast<const float4*>(partial + (int64_t)s * T * D)[v];
+                acc.x += q.x;
+                acc.y += q.y;
+                acc.z += q.z;
+                acc.w += q.w;
+            }
         }
-        const uint2 eb = *reinterpret_cast<const uint2*>(e0 + (int64_t)__ldg(tokens + t) * D + i);
+        const uint2 eb = v == v0 ? eb0 : *reinterpret_cast<const uint2*>(e0 + (int64_t)__ldg(tokens + t) * D + i);
         float m[4] = {__fmul_rn(__fadd_rn(bf16_bits_to_f32(eb.x & 0xffffu), acc.x), scale),
                       __fmul_rn(__fadd_rn(bf16_bits_to_f32(eb.x >> 16), acc.y), scale),
                       __fmul_rn(__fadd_rn(bf16_bits_to_f32(eb.y & 0xffffu), acc.z), scale),
@@ -1274,13 +1305,13 @@ void launch_forward_tc(const FwdArgs& a, int num_sms, cudaStream_t st, float* sp
             const int64_t n4 = a.T * a.s.D / 4;
             DecodeCommit c{};
             if (a.commit) c = *a.commit;
-            int64_t blocks = (n4 + 255) / 256;
-            if (blocks > num_sms * 8) blocks = num_sms * 8;
+            int64_t blocks = (n4 + kReduceThreads - 1) / kReduceThreads;
+            if (blocks > num_sms * 16) blocks = num_sms * 16;
             const int wr = (a.rows_out != nullptr && a.s.amp != kAmpLN) ? 1 : 0;
             if (pdl) {
                 cudaLaunchConfig_t cfg{};
                 cfg.gridDim = dim3((unsigned)blocks);
-                cfg.blockDim = dim3(256);
+                cfg.blockDim = dim3(kReduceThreads);
                 cfg.stream = st;
                 cudaLaunchAttribute attr[1];
                 attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1288,11 +1319,11 @@ void launch_forward_tc(const FwdArgs& a, int num_sms, cudaStream_t st, float* sp
                 cfg.attrs = attr;
                 cfg.numAttrs = 1;
                 cudaLaunchKernelEx(&cfg, splitk_reduce_kernel, (const float*)splitk_ws, S, a.T, a.s.D, a.tokens, a.e0,
-                                   scale, amp, wr, a.rows_out, a.merged_out, a.out_bf16, a.err, c);
+                                   a.s.V0, scale, amp, wr, a.rows_out, a.merged_out, a.out_bf16, a.err, c);
             } else {
-                splitk_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(splitk_ws, S, a.T, a.s.D, a.tokens, a.e0, scale,
-                                                                       amp, wr, a.rows_out, a.merged_out, a.out_bf16,
-                                                                       a.err, c);
+                splitk_reduce_kernel<<<(unsigned)blocks, kReduceThreads, 0, st>>>(
+                    splitk_ws, S, a.T, a.s.D, a.tokens, a.e0, a.s.V0, scale, amp, wr, a.rows_out, a.merged_out,
+                    a.out_bf16, a.err, c);
             }
             count_launch();
             return;
