@@ -6,7 +6,8 @@
 
 Secondary lines (not the driver's headline): --workload D | E (decode steps / verify blocks,
 CUDA-graph replay; sharded under torchrun), --workload backward (config C gradients),
---workload analysis (corpus collision analysis), --workload plne (per-layer N-gram FFN);
+--workload analysis (corpus collision analysis), --workload plne (per-layer N-gram FFN),
+--workload dropin (per-call latency of the C++ drop-in's one-token entries vs the reference);
 --tokens zipf (the reference's text model).
 
 A "step" is one pass of the hot path -- hash-index (K1) + gather/projection/epilogue
@@ -1112,6 +1113,37 @@ def run_analysis(args):
     print(json.dumps(line))
 
 
+def run_dropin(args):
+    """Per-call latency of the C++ drop-in's one-token entries (tests/cxx/bench_dropin: host ->
+    device -> host round trips through the C-ABI) beside the reference's own per-call cost on
+    one host thread (oracle/_ref, ref_time_calls), LongCat shape (N = 4, K = 4, D = 3072,
+    reduced vocabulary).  Not a throughput line: the batched entries are the fast path."""
+    import ctypes as C
+    exe = os.path.join(ROOT, "tests", "cxx", "bench_dropin")
+    r = subprocess.run([exe, "3072", "100"], capture_output=True, text=True, timeout=900)
+    if r.returncode != 0:
+        raise SystemExit(f"bench_dropin failed: {r.stderr[-2000:]}")
+    ours = json.loads(r.stdout.strip().splitlines()[-1])
+    line = {"metric": "dropin_us_per_call", "unit": "us", "higher_is_better": False, "n_gpus": 1,
+            "config": {"workload": "dropin_per_call_latency", "V0": 1000, "N": 4, "K": 4, "D": 3072},
+            "ours": ours["us_per_call"]}
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O  # noqa: E402  (reference timing only)
+    if O.ref_available():
+        R = O.ref()
+        buf = C.create_string_buffer(1 << 16)
+        R.ref_make_default_config_json(1000, 3072, 4, 4, buf, len(buf))
+        h = R.ref_bank_create(buf.value, 3, 1)
+        out = (C.c_double * 5)()
+        if R.ref_time_calls(h, 3, out) == 0:
+            line["reference_1thread"] = {"rolling_hash": out[0] / 1e3, "hash_all_orders": out[1] / 1e3,
+                                         "sequence_cache_append": out[2] / 1e3,
+                                         "append_plus_memo_lookup_miss": out[3] / 1e3,
+                                         "draft_verify_4_accept_2": out[4] / 1e3}
+        R.ref_bank_destroy(h)
+    print(json.dumps(line))
+
+
 def spawn_ranks(n: int) -> int:
     """Re-launch this command as n ranks (torch.distributed.run --nproc-per-node n) and return
     the launcher's exit code; stdout / stderr stream through (rank 0 prints the JSON line)."""
@@ -1179,6 +1211,8 @@ def main():
         run_backward(args)
     elif args.workload == "plne":
         run_plne(args)
+    elif args.workload == "dropin":
+        run_dropin(args)
     elif args.workload in ("D", "E") and int(os.environ.get("WORLD_SIZE", "1")) > 1:
         run_decode_sharded(args)
     elif args.workload in ("D", "E"):

@@ -164,6 +164,7 @@ def ref():
         L.ref_decode_mt.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, _u32p, C.c_int, _u32p, C.c_int, C.c_int,
                                     C.c_void_p, C.c_int64, _f32p]
         L.ref_hash_all_orders_mt.argtypes = [C.c_char_p, _u32p, C.c_int64, C.c_int, _u64p]
+        L.ref_time_calls.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_double)]
         _REF = L
     return _REF
 

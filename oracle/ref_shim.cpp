@@ -9,6 +9,8 @@
 //   * time the reference CPU path for bench.py --impl reference / cpu_baseline.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <functional>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -583,6 +585,47 @@ int ref_hash_all_orders_mt(const char* cfg_json, const uint32_t* tokens, int64_t
         for (auto& t : pool) t.join();
         for (int x : rc)
             if (x) return x;
+        return 0;
+    } catch (...) {
+        return map_exc();
+    }
+}
+
+// Per-call latency of the reference's one-token entries on one host thread (ns per call, median
+// of `reps` timed batches of 16 calls): rolling_hash (order 3), hash_all_orders,
+// sequence_cache::append, embedding_memo::lookup (a miss: embed_from_ids), draft_verify (4 drafts,
+// accept 2).  out: 5 doubles.  bench.py --workload dropin (the drop-in's per-call latency beside it).
+int ref_time_calls(void* bank, int reps, double* out) {
+    try {
+        auto& bk = static_cast<ref_bank*>(bank)->bank;
+        const auto& cfg = bk.config;
+        auto med = [&](const std::function<void()>& f) {
+            for (int i = 0; i < 3; ++i) f();
+            std::vector<double> t;
+            for (int r = 0; r < reps; ++r) {
+                const auto a = std::chrono::steady_clock::now();
+                for (int i = 0; i < 16; ++i) f();
+                t.push_back(std::chrono::duration<double, std::nano>(std::chrono::steady_clock::now() - a).count() / 16);
+            }
+            std::sort(t.begin(), t.end());
+            return t[t.size() / 2];
+        };
+        std::vector<token_id> ctx{5, 6, 7, 8};
+        ctx.resize(std::size_t(cfg.max_order), 1);
+        volatile uint64_t sink = 0;
+        sequence_cache st(cfg);
+        embedding_memo memo(1);  // capacity 1: every lookup of a new key is a miss (embed_from_ids)
+        token_id tk = 1;
+        out[0] = med([&] { sink = sink + rolling_hash(std::span<const token_id>(ctx).last(2), {2, cfg.base_vocab, 997}); });
+        out[1] = med([&] { sink = sink + hash_all_orders(ctx, cfg)[0]; });
+        out[2] = med([&] { sink = sink + st.append(tk = (tk * 7 + 3) % cfg.base_vocab)[0]; });
+        out[3] = med([&] {
+            tk = (tk * 7 + 3) % cfg.base_vocab;
+            const auto ids = st.append(tk);
+            sink = sink + uint64_t(memo.lookup(tk, ids, bk)[0] != 0.0f);
+        });
+        std::vector<token_id> draft{3, 1, 4, 1};
+        out[4] = med([&] { sink = sink + draft_verify(st, memo, bk, draft, 2).accepted.size(); });
         return 0;
     } catch (...) {
         return map_exc();

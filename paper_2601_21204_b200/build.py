@@ -109,15 +109,17 @@ def build_cxx() -> None:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"g++ failed for libngram.so:\n{r.stderr}")
-    test_src = os.path.join(ROOT, "tests", "cxx", "test_dropin.cpp")
-    if os.path.exists(test_src) and (not os.path.exists(CXX_TEST) or os.path.getmtime(CXX_TEST) <
-                                     max(newest, os.path.getmtime(test_src), os.path.getmtime(CXX_LIB))):
-        os.makedirs(os.path.dirname(CXX_TEST), exist_ok=True)
-        cmd = ["g++"] + flags + ["-o", CXX_TEST, test_src, "-L" + PKG, "-lngram", "-lngram_b200",
-                                 "-Wl,-rpath,$ORIGIN/../../paper_2601_21204_b200"]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
-            raise RuntimeError(f"g++ failed for test_dropin:\n{r.stderr}")
+    for name in ("test_dropin", "bench_dropin"):  # C++ parity test program, per-call latency bench
+        src = os.path.join(ROOT, "tests", "cxx", name + ".cpp")
+        exe = os.path.join(ROOT, "tests", "cxx", name)
+        if os.path.exists(src) and (not os.path.exists(exe) or os.path.getmtime(exe) <
+                                    max(newest, os.path.getmtime(src), os.path.getmtime(CXX_LIB))):
+            os.makedirs(os.path.dirname(exe), exist_ok=True)
+            cmd = ["g++"] + flags + ["-o", exe, src, "-L" + PKG, "-lngram", "-lngram_b200",
+                                     "-Wl,-rpath,$ORIGIN/../../paper_2601_21204_b200"]
+            r = subprocess.run(cmd, capture_output=True, text=True)
+            if r.returncode != 0:
+                raise RuntimeError(f"g++ failed for {name}:\n{r.stderr}")
 
 
 if __name__ == "__main__":
