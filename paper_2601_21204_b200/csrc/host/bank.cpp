@@ -106,6 +106,7 @@ ngram_bank::~ngram_bank() {
         if (host_streams[i]) cudaStreamDestroy(host_streams[i]);
         if (pinned[i]) cudaFreeHost(pinned[i]);
     }
+    if (io_stream) cudaStreamDestroy(io_stream);
     cudaGetLastError();
     if (prev >= 0 && prev != device) cudaSetDevice(prev);
 }

@@ -153,6 +153,12 @@ struct ngram_bank {
     ngh::XBuf host_x[2];
     void* pinned[2] = {nullptr, nullptr};
     size_t pinned_bytes = 0;
+    // small host calls (ngram_hash_ids_host, ngram_embed_from_ids_host): one pinned staging block
+    // and one device block, reused -- inputs in one H2D copy, outputs + error words in one D2H
+    // copy, one synchronisation, no allocation after the first call
+    ngh::PinBuf io_pin;
+    ngh::DevBuf<uint8_t> io_dev;
+    cudaStream_t io_stream = nullptr;
 
     // stage profiling (ngram_profile_enable)
     bool prof = false;

@@ -496,6 +496,59 @@ int ngram_embed_sequence_host(ngram_bank* b, const uint32_t* tokens, const int64
 
 // ---------------------------------------------------------------- host-buffer variants
 namespace {
+// One small host call on the bank's I/O arena (bank.hpp): inputs packed into the pinned block
+// and copied in ONE H2D transfer, outputs and the two error words copied back in ONE D2H
+// transfer, ONE stream synchronisation; a token error raises as ngram_sync_errors does.
+class Staged {
+  public:
+    explicit Staged(ngram_bank* b) : b_(b) {}
+    size_t in(size_t bytes) { return take(in_, bytes); }
+    size_t out(size_t bytes) { return take(out_, bytes) | kOut; }
+    void ready() {
+        words_ = al(in_ + out_);
+        total_ = words_ + 16;
+        b_->io_pin.ensure(total_);
+        b_->io_dev.ensure(total_);
+        if (!b_->io_stream) NGH_CUDA(cudaStreamCreateWithFlags(&b_->io_stream, cudaStreamNonBlocking));
+    }
+    void put(size_t off, const void* src, size_t bytes) { std::memcpy(b_->io_pin.p + at(off), src, bytes); }
+    void upload() { NGH_CUDA(cudaMemcpyAsync(b_->io_dev.p, b_->io_pin.p, in_, cudaMemcpyHostToDevice, stream())); }
+    template <typename T>
+    T* dev(size_t off) { return reinterpret_cast<T*>(b_->io_dev.p + at(off)); }
+    const uint8_t* host(size_t off) const { return b_->io_pin.p + at(off); }
+    cudaStream_t stream() const { return b_->io_stream; }
+    void finish() {
+        cudaStream_t st = stream();
+        if (out_) NGH_CUDA(cudaMemcpyAsync(b_->io_pin.p + in_, b_->io_dev.p + in_, out_, cudaMemcpyDeviceToHost, st));
+        auto* w = reinterpret_cast<unsigned long long*>(b_->io_pin.p + words_);
+        NGH_CUDA(cudaMemcpyAsync(&w[0], b_->err.p, 8, cudaMemcpyDeviceToHost, st));
+        NGH_CUDA(cudaMemcpyAsync(&w[1], b_->err_rep.p, 8, cudaMemcpyDeviceToHost, st));
+        NGH_CUDA(cudaStreamSynchronize(st));
+        const unsigned long long e = std::min(w[0], w[1]);
+        b_->err_clean = true;
+        if (e != ~0ull) {
+            NGH_CUDA(cudaMemsetAsync(b_->err.p, 0xff, 8, st));
+            NGH_CUDA(cudaMemsetAsync(b_->err_rep.p, 0xff, 8, st));
+            NGH_CUDA(cudaStreamSynchronize(st));
+            throw Error(NGRAM_ERANGE, "embedding: token out of range for base vocabulary " +
+                                          std::to_string(b_->cfg.base_vocab) + " (first bad window at position " +
+                                          std::to_string(e) + ")");
+        }
+    }
+
+  private:
+    static constexpr size_t kOut = size_t(1) << 62;  // tag: offset in the output region
+    static size_t al(size_t x) { return (x + 15) & ~size_t(15); }
+    static size_t take(size_t& region, size_t bytes) {
+        const size_t off = region;
+        region = al(region + bytes);
+        return off;
+    }
+    size_t at(size_t off) const { return (off & kOut) ? in_ + (off & ~kOut) : off; }
+    ngram_bank* b_;
+    size_t in_ = 0, out_ = 0, words_ = 0, total_ = 0;
+};
+
 template <typename T>
 struct HostStage {  // device copy of a host array, freed on scope exit
     DevBuf<T> d;
@@ -519,18 +572,23 @@ int ngram_hash_ids_host(ngram_bank* b, const uint32_t* tokens, const int64_t* se
     std::lock_guard<std::mutex> host_lock(b->host_mu);
     if (T == 0) NGRAM_API_RETURN_OK;
     DeviceGuard g(b->device);
-    HostStage<uint32_t> t, p;
-    HostStage<int64_t> o;
-    DevBuf<uint64_t> ids;
-    ids.alloc(size_t(T) * size_t(std::max(b->shape.B, 1)));
     const int N1 = std::max(b->cfg.max_order - 1, 0);
-    int rc = ngram_hash_ids(b, t.put(tokens, size_t(T)), o.put(seq_offsets, size_t(nseq + 1)), nseq, T,
-                            N1 > 0 ? p.put(prior, size_t(nseq) * size_t(N1)) : nullptr, ids.p, 1, nullptr);
+    const size_t nb = size_t(std::max(b->shape.B, 1));
+    Staged io(b);
+    const size_t o_tok = io.in(size_t(T) * 4), o_off = io.in(size_t(nseq + 1) * 8);
+    const size_t o_pri = (prior && N1 > 0) ? io.in(size_t(nseq) * size_t(N1) * 4) : 0;
+    const size_t o_ids = io.out(size_t(T) * nb * 8);
+    io.ready();
+    io.put(o_tok, tokens, size_t(T) * 4);
+    io.put(o_off, seq_offsets, size_t(nseq + 1) * 8);
+    if (prior && N1 > 0) io.put(o_pri, prior, size_t(nseq) * size_t(N1) * 4);
+    io.upload();
+    int rc = ngram_hash_ids(b, io.dev<uint32_t>(o_tok), io.dev<int64_t>(o_off), nseq, T,
+                            (prior && N1 > 0) ? io.dev<uint32_t>(o_pri) : nullptr, io.dev<uint64_t>(o_ids), 1,
+                            io.stream());
     if (rc) return rc;
-    rc = ngram_sync_errors(b, nullptr);
-    if (rc) return rc;
-    if (b->shape.B > 0)
-        NGH_CUDA(cudaMemcpy(ids_out, ids.p, size_t(T) * size_t(b->shape.B) * 8, cudaMemcpyDeviceToHost));
+    io.finish();  // one D2H of outputs + error words, one sync; raises a token error
+    if (b->shape.B > 0) std::memcpy(ids_out, io.host(o_ids), size_t(T) * size_t(b->shape.B) * 8);
     NGRAM_API_END
 }
 
@@ -539,20 +597,42 @@ int ngram_rolling_hash_host(const uint32_t* windows, int64_t stride, const int32
                             int32_t* status) {
     NGRAM_API_BEGIN
     if (count <= 0) NGRAM_API_RETURN_OK;
-    HostStage<uint32_t> w;
-    HostStage<int32_t> l, o;
-    HostStage<uint64_t> ba, mo;
-    DevBuf<uint64_t> dout;
-    DevBuf<int32_t> dst;
-    dout.alloc(size_t(count));
-    dst.alloc(size_t(count));
-    int rc = ngram_rolling_hash_batch(w.put(windows, size_t(count) * size_t(stride)), stride,
-                                      lengths ? l.put(lengths, size_t(count)) : nullptr, o.put(orders, size_t(count)),
-                                      ba.put(bases, size_t(count)), mo.put(moduli, size_t(count)), count, dout.p,
-                                      dst.p, nullptr);
+    // a bank-free entry: a per-thread staging arena on the current device
+    thread_local PinBuf pin;
+    thread_local DevBuf<uint8_t> dev;
+    thread_local cudaStream_t st = nullptr;
+    thread_local int st_dev = -1;
+    int cur = 0;
+    NGH_CUDA(cudaGetDevice(&cur));
+    if (!st || st_dev != cur) {
+        NGH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        dev.release();
+        st_dev = cur;
+    }
+    auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
+    const size_t s_w = size_t(count) * size_t(stride) * 4, s_c = size_t(count) * 4, s_8 = size_t(count) * 8;
+    const size_t o_w = 0, o_l = al(o_w + s_w), o_o = al(o_l + s_c), o_b = al(o_o + s_c), o_m = al(o_b + s_8);
+    const size_t o_out = al(o_m + s_8), o_st = al(o_out + s_8), total = al(o_st + s_c);
+    pin.ensure(total);
+    dev.ensure(total);
+    std::memcpy(pin.p + o_w, windows, s_w);
+    if (lengths) std::memcpy(pin.p + o_l, lengths, s_c);
+    std::memcpy(pin.p + o_o, orders, s_c);
+    std::memcpy(pin.p + o_b, bases, s_8);
+    std::memcpy(pin.p + o_m, moduli, s_8);
+    NGH_CUDA(cudaMemcpyAsync(dev.p, pin.p, o_out, cudaMemcpyHostToDevice, st));
+    int rc = ngram_rolling_hash_batch(reinterpret_cast<const uint32_t*>(dev.p + o_w), stride,
+                                      lengths ? reinterpret_cast<const int32_t*>(dev.p + o_l) : nullptr,
+                                      reinterpret_cast<const int32_t*>(dev.p + o_o),
+                                      reinterpret_cast<const uint64_t*>(dev.p + o_b),
+                                      reinterpret_cast<const uint64_t*>(dev.p + o_m), count,
+                                      reinterpret_cast<uint64_t*>(dev.p + o_out),
+                                      reinterpret_cast<int32_t*>(dev.p + o_st), st);
     if (rc) return rc;
-    NGH_CUDA(cudaMemcpy(out, dout.p, size_t(count) * 8, cudaMemcpyDeviceToHost));
-    NGH_CUDA(cudaMemcpy(status, dst.p, size_t(count) * 4, cudaMemcpyDeviceToHost));
+    NGH_CUDA(cudaMemcpyAsync(pin.p + o_out, dev.p + o_out, total - o_out, cudaMemcpyDeviceToHost, st));
+    NGH_CUDA(cudaStreamSynchronize(st));
+    std::memcpy(out, pin.p + o_out, s_8);
+    std::memcpy(status, pin.p + o_st, s_c);
     NGRAM_API_END
 }
 
@@ -564,16 +644,19 @@ int ngram_embed_from_ids_host(ngram_bank* b, const uint32_t* tokens, const uint6
     std::lock_guard<std::mutex> host_lock(b->host_mu);
     if (T == 0) NGRAM_API_RETURN_OK;
     DeviceGuard g(b->device);
-    HostStage<uint32_t> t;
-    HostStage<uint64_t> i;
-    DevBuf<float> out;
-    out.alloc(size_t(T) * size_t(b->cfg.dim));
-    int rc = ngram_embed_from_ids(b, t.put(tokens, size_t(T)), i.put(ids, size_t(T) * size_t(std::max(b->shape.B, 1))),
-                                  T, out.p, NGRAM_F32, nullptr);
+    const size_t nb = size_t(std::max(b->shape.B, 1)), D = size_t(b->cfg.dim);
+    Staged io(b);
+    const size_t o_tok = io.in(size_t(T) * 4), o_ids = io.in(size_t(T) * nb * 8);
+    const size_t o_out = io.out(size_t(T) * D * 4);
+    io.ready();
+    io.put(o_tok, tokens, size_t(T) * 4);
+    io.put(o_ids, ids, size_t(T) * nb * 8);
+    io.upload();
+    int rc = ngram_embed_from_ids(b, io.dev<uint32_t>(o_tok), io.dev<uint64_t>(o_ids), T, io.dev<float>(o_out),
+                                  NGRAM_F32, io.stream());
     if (rc) return rc;
-    rc = ngram_sync_errors(b, nullptr);
-    if (rc) return rc;
-    NGH_CUDA(cudaMemcpy(merged_out, out.p, size_t(T) * size_t(b->cfg.dim) * 4, cudaMemcpyDeviceToHost));
+    io.finish();
+    std::memcpy(merged_out, io.host(o_out), size_t(T) * D * 4);
     NGRAM_API_END
 }
 
