@@ -32,6 +32,7 @@
 // behind the next chunk's MMAs (>= 12 MMAs of 256 x 256 x 16 per chunk).
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.h"
 #include "ptx.cuh"
@@ -51,7 +52,9 @@ constexpr int kMmaWarpG = 1 + kEpiWarpsG;
 // small ones are issued first, into a still-tiny accumulator, then the big a1 b1 -- so only its
 // four MMAs meet a large accumulator), four with two or three, eight for a single product.
 constexpr int chunk_kb(int pairs) { return pairs >= 6 ? 1 : pairs >= 2 ? 4 : 8; }
-constexpr int kSmemBudget = 200 * 1024;
+constexpr int kStageRowFloats = 33;  // epilogue transpose tile: 32 rows x 32 floats, padded (no bank conflicts)
+constexpr int kEpiStageBytes = kEpiWarpsG * 32 * kStageRowFloats * 4;  // 33.8 KB
+constexpr int kSmemBudget = 227 * 1024 - kEpiStageBytes - 2048;
 
 constexpr int gstages(int na, int nb) {
     const int s = kSmemBudget / ((na + nb) * kTileBytes);
@@ -76,7 +79,14 @@ struct GemmParams {
     float* C;
     int64_t ldc;
     int accumulate;
+    int staged_store;  // overwrite mode: coalesced stores through the smem transpose tile
 };
+
+// NGRAM_GEMM_STAGED_STORE=0 selects per-thread row stores in overwrite mode too (A/B switch)
+int staged_store() {
+    static const int v = getenv("NGRAM_GEMM_STAGED_STORE") ? atoi(getenv("NGRAM_GEMM_STAGED_STORE")) : 1;
+    return v;
+}
 
 template <int NA, int NB, bool A_MN, bool B_MN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
@@ -94,6 +104,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     uint64_t* tfull = empty + kStages;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    float* epi_stage = reinterpret_cast<float*>(smem + kStages * kStageBytes + 256);  // [8 warps][32][33]
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
@@ -269,7 +280,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                 }
             }
             const int64_t col0 = n * GBN + half * (GBN / 2);
-            if (row < p.M && col0 < p.N) {
+            if (!p.accumulate && p.staged_store) {
+                // overwrite: each 32 x 32 block goes through this warp's padded smem tile so every
+                // store instruction writes one row's 32 consecutive floats (a 128-byte segment)
+                // instead of 32 rows x 16 bytes (dX of the backward: 805 MB at config C)
+                const int64_t row0 = row - lane;
+                const int nr = p.M - row0 < 32 ? (p.M - row0 > 0 ? (int)(p.M - row0) : 0) : 32;
+                float* stg = epi_stage + (warp - 1) * 32 * kStageRowFloats;
+#pragma unroll
+                for (int c = 0; c < GBN / 2 / 32; ++c) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) stg[lane * kStageRowFloats + j] = sum[c * 32 + j];
+                    __syncwarp();
+                    const int64_t col = col0 + c * 32 + lane;
+                    if (col < p.N) {
+                        float* dst = p.C + row0 * p.ldc + col;
+#pragma unroll 4
+                        for (int r = 0; r < nr; ++r) dst[r * p.ldc] = stg[r * kStageRowFloats + lane];
+                    }
+                    __syncwarp();
+                }
+            } else if (row < p.M && col0 < p.N) {
                 float* dst = p.C + row * p.ldc + col0;
                 if (vec && col0 + GBN / 2 <= p.N) {
 #pragma unroll
@@ -304,7 +335,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 template <int NA, int NB, bool A_MN, bool B_MN>
 void launch_g2(const CUtensorMap* ma, const CUtensorMap* mb, const GemmParams& p, int num_sms, cudaStream_t st) {
     constexpr int kStages = gstages(NA, NB);
-    constexpr int smem = kStages * (NA + NB) * kTileBytes + 1024 + 256;
+    constexpr int smem = kStages * (NA + NB) * kTileBytes + 1024 + 256 + kEpiStageBytes;
     const int64_t tiles = ((p.M + GBM - 1) / GBM) * ((p.N + GBN - 1) / GBN);
     int64_t pairs = num_sms / 2;
     if (tiles < pairs) pairs = tiles;
@@ -408,7 +439,7 @@ __global__ void split3_kernel(const float* __restrict__ x, int64_t rows, int64_t
 void launch_gemm_bf16_terms(const CUtensorMap* ma, int na, bool a_mn, const CUtensorMap* mb, int nb, bool b_mn,
                             int64_t M, int64_t N, int64_t K, float* C, int64_t ldc, bool accumulate, int num_sms,
                             cudaStream_t st) {
-    const GemmParams p{M, N, K, C, ldc, accumulate ? 1 : 0};
+    const GemmParams p{M, N, K, C, ldc, accumulate ? 1 : 0, staged_store()};
     if (na == 1 && nb == 1) dispatch_major<1, 1>(ma, mb, a_mn, b_mn, p, num_sms, st);
     else if (na == 3 && nb == 1) dispatch_major<3, 1>(ma, mb, a_mn, b_mn, p, num_sms, st);
     else if (na == 2 && nb == 1) dispatch_major<2, 1>(ma, mb, a_mn, b_mn, p, num_sms, st);
@@ -419,7 +450,7 @@ void launch_gemm_bf16_terms(const CUtensorMap* ma, int na, bool a_mn, const CUte
 void launch_gemm_f32(const float* A, int64_t lda, bool a_mn, const float* B, int64_t ldb, bool b_mn, int64_t M,
                      int64_t N, int64_t K, float* C, int64_t ldc, bool accumulate, cudaStream_t st) {
     if (M <= 0 || N <= 0) return;
-    const GemmParams p{M, N, K, C, ldc, accumulate ? 1 : 0};
+    const GemmParams p{M, N, K, C, ldc, accumulate ? 1 : 0, 0};
     const dim3 grid((unsigned)((N + FB - 1) / FB), (unsigned)((M + FB - 1) / FB));
     gemm_f32_kernel<<<grid, 256, 0, st>>>(A, lda, a_mn ? 1 : 0, B, ldb, b_mn ? 1 : 0, p);
     count_launch();
