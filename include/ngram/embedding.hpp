@@ -174,6 +174,44 @@ std::vector<float> embed_sequence(std::span<const token_id> tokens, const embedd
 // Batched extension: many sequences in one launch (rows concatenated, len_total x D).
 std::vector<float> embed_batch(const std::vector<std::vector<token_id>>& sequences, const device_bank& bank);
 
+// ---- the reference's template entry points over host banks (embedding.hpp:205-459) ----------
+// T = float runs the device float path on the bank's cached device copy (device_bank_for);
+// T = double runs the device fp64 instantiation (ngram_f64_*, include/ngram_b200.h) -- the
+// precision the reference's own gradient checks use.  Explicitly instantiated for float and
+// double in libngram.so.
+template <typename T>
+std::vector<T> embed_v1(std::span<const token_id> context, const embedding_bank_t<T>& bank);
+template <typename T>
+std::vector<T> embed_v2(std::span<const token_id> context, const embedding_bank_t<T>& bank);
+template <typename T>
+void embed_window(std::span<const token_id> context, const embedding_bank_t<T>& bank, std::span<T> out,
+                  embed_counters* counters = nullptr);
+template <typename T>
+sequence_embedding<T> embed_sequence_cached(std::span<const token_id> tokens, const embedding_bank_t<T>& bank,
+                                            std::span<const token_id> prior_context = {},
+                                            embed_counters* counters = nullptr);
+template <typename T>
+std::vector<T> embed_sequence(std::span<const token_id> tokens, const embedding_bank_t<T>& bank,
+                              std::span<const token_id> prior_context = {});
+template <typename T>
+void amplify(std::span<const T> e, amp_mode mode, std::span<const T> gain, std::span<const T> bias, std::span<T> out);
+template <typename T>
+std::vector<T> amplify(std::span<const T> e, const embedding_bank_t<T>& bank) {
+    std::vector<T> out(e.size());
+    amplify<T>(e, bank.config.amplification, bank.ln_gain, bank.ln_bias, std::span<T>(out));
+    return out;
+}
+template <typename T>
+void amplify_backward(std::span<const T> pre, std::span<const T> upstream, const embedding_bank_t<T>& bank,
+                      embedding_bank_t<T>& grads, std::span<T> d_pre);
+template <typename T>
+void embed_backward(std::span<const token_id> context, const embedding_bank_t<T>& bank,
+                    std::span<const T> upstream, embedding_bank_t<T>& grads);
+template <typename T>
+void embed_sequence_backward(std::span<const token_id> tokens, const embedding_bank_t<T>& bank,
+                             std::span<const T> merged, std::span<const T> upstream, embedding_bank_t<T>& grads,
+                             std::span<const token_id> prior_context = {});
+
 // ---- parameter accounting (embedding.hpp:461-484, embedding.cpp:13-56): host arithmetic
 struct param_count_report {
     std::uint64_t base = 0;

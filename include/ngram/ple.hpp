@@ -80,4 +80,19 @@ void ffn_plne_backward(std::span<const float> x, std::span<const token_id> conte
                        const ple_params& p, std::span<const float> upstream, ple_params& grads,
                        embedding_bank& bank_grads, std::span<float> dx);
 
+// The reference's templates (ple.hpp:148-198): T = float -> the device float path above,
+// T = double -> the device fp64 instantiation (ngram_f64_gated_ffn*, embed via ngram_f64_*).
+template <typename T>
+std::vector<T> ffn_ple(std::span<const T> x, token_id token, const ple_params_t<T>& p);
+template <typename T>
+void ffn_ple_backward(std::span<const T> x, token_id token, const ple_params_t<T>& p, std::span<const T> upstream,
+                      ple_params_t<T>& grads, std::span<T> dx);
+template <typename T>
+std::vector<T> ffn_plne(std::span<const T> x, std::span<const token_id> context, const embedding_bank_t<T>& layer_bank,
+                        const ple_params_t<T>& p);
+template <typename T>
+void ffn_plne_backward(std::span<const T> x, std::span<const token_id> context, const embedding_bank_t<T>& layer_bank,
+                       const ple_params_t<T>& p, std::span<const T> upstream, ple_params_t<T>& grads,
+                       embedding_bank_t<T>& bank_grads, std::span<T> dx);
+
 }  // namespace ngram

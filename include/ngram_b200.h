@@ -298,6 +298,34 @@ int ngram_gemm_f32(int device, int64_t M, int64_t N, int64_t K, const float* A, 
                    int64_t ldb, int b_mn, float* C, int64_t ldc, int accumulate, int a_terms, int b_terms,
                    void* stream);
 
+/* ------------------------------------------------------------------ fp64 instantiations */
+/* The reference's double-precision templates (embedding_bank_t<double>, ple_params_t<double>)
+ * evaluated on the device in double, in the reference's operation order -- the instantiations
+ * its gradient checks use (proj/tests/gradcases.hpp).  Host buffers, synchronous, small
+ * problems (tables uploaded per call).  Tables in the reference layout: base V0 x D,
+ * sub[b] V_b x d, proj[b] D x d (branch order b = (n-2)K + (k-1)).  One sequence of T tokens
+ * (+ prior context, right-aligned).  rows (amplified) may be NULL. */
+int ngram_f64_forward(const char* config_json, const double* base, const double* const* sub,
+                      const double* const* proj, const double* ln_gain, const double* ln_bias, const uint32_t* tokens,
+                      int64_t T, const uint32_t* prior, int64_t prior_len, double* merged, double* rows);
+/* embed_sequence_backward (merged != NULL: through amplify) / embed_backward (merged == NULL:
+ * upstream is d(merged)); gradients ACCUMULATED into the host tables g_*. */
+int ngram_f64_backward(const char* config_json, const double* base, const double* const* sub,
+                       const double* const* proj, const double* ln_gain, const double* ln_bias, const uint32_t* tokens,
+                       int64_t T, const uint32_t* prior, int64_t prior_len, const double* merged,
+                       const double* upstream, double* g_base, double* const* g_sub, double* const* g_proj,
+                       double* g_gain, double* g_bias);
+int ngram_f64_amplify(int amp_mode, int64_t D, const double* gain, const double* bias, const double* in, double* out);
+int ngram_f64_amplify_backward(int amp_mode, int64_t D, const double* pre, const double* upstream, const double* gain,
+                               double* d_pre, double* g_gain, double* g_bias);
+/* gated FFN body of ffn_ple / ffn_plne (ple.hpp:77-146): y = W_d (SiLU(W_g x) (.) g); the
+ * backward accumulates g_gate, g_down, dx and dg (+= dL/dg). */
+int ngram_f64_gated_ffn(int d_model, int hidden, const double* gate, const double* down, const double* x,
+                        const double* g, double* y);
+int ngram_f64_gated_ffn_backward(int d_model, int hidden, const double* gate, const double* down, const double* x,
+                                 const double* g, const double* upstream, double* g_gate, double* g_down, double* dx,
+                                 double* dg);
+
 /* ------------------------------------------------------------------ backward (training) */
 /* embed_sequence_backward (embedding.hpp:438-459) batched on the device: gradients of the
  * embedding rows w.r.t. every bank parameter, ACCUMULATED (+=) into an fp32 gradient bank

@@ -35,7 +35,9 @@ SYMBOLS = [
     "ngram_profile_enable", "ngram_profile_read", "ngram_decode_create", "ngram_decode_destroy", "ngram_decode_reset",
     "ngram_decode_step", "ngram_verify_block", "ngram_commit", "ngram_decode_reset_host", "ngram_decode_step_host",
     "ngram_verify_commit_host",
-    "ngram_decode_get_state", "ngram_decode_set_state_host", "ngram_gemm_f32",
+    "ngram_decode_get_state", "ngram_decode_set_state_host", "ngram_gemm_f32", "ngram_f64_forward",
+    "ngram_f64_backward", "ngram_f64_amplify", "ngram_f64_amplify_backward", "ngram_f64_gated_ffn",
+    "ngram_f64_gated_ffn_backward",
     "ngram_shard_rows", "ngram_shard_group_create", "ngram_shard_group_destroy", "ngram_shard_export", "ngram_shard_open",
     "ngram_shard_local_buffers", "ngram_shard_set_peer", "ngram_shard_scatter_rows", "ngram_shard_project",
     "ngram_shard_xchg_prepare", "ngram_shard_xchg_pack", "ngram_shard_xchg_unpack", "ngram_shard_pack_padded",
@@ -148,6 +150,12 @@ def lib() -> C.CDLL:
         "ngram_decode_get_state": ([vp, vp, vp, vp], i32),
         "ngram_decode_set_state_host": ([vp, vp, vp, vp], i32),
         "ngram_gemm_f32": ([i32, i64, i64, i64, vp, i64, i32, vp, i64, i32, vp, i64, i32, i32, i32, vp], i32),
+        "ngram_f64_forward": ([C.c_char_p, vp, vp, vp, vp, vp, vp, i64, vp, i64, vp, vp], i32),
+        "ngram_f64_backward": ([C.c_char_p, vp, vp, vp, vp, vp, vp, i64, vp, i64, vp, vp, vp, vp, vp, vp, vp], i32),
+        "ngram_f64_amplify": ([i32, i64, vp, vp, vp, vp], i32),
+        "ngram_f64_amplify_backward": ([i32, i64, vp, vp, vp, vp, vp, vp], i32),
+        "ngram_f64_gated_ffn": ([i32, i32, vp, vp, vp, vp, vp], i32),
+        "ngram_f64_gated_ffn_backward": ([i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp], i32),
         "ngram_shard_rows": ([u64, i32, i32, C.POINTER(i64), C.POINTER(i64)], i32),
         "ngram_shard_group_create": ([vp, i64, C.POINTER(vp)], i32),
         "ngram_shard_group_destroy": ([vp], i32),

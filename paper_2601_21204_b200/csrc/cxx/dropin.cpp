@@ -10,6 +10,7 @@
 #include <mutex>
 #include <sstream>
 #include <thread>
+#include <type_traits>
 
 #include <json.hpp>
 
@@ -847,7 +848,7 @@ std::vector<float> ffn_plne(std::span<const float> x, std::span<const token_id> 
 
 std::vector<float> ffn_plne(std::span<const float> x, std::span<const token_id> context,
                             const embedding_bank& layer_bank, const ple_params& p) {
-    return ffn_plne(x, context, device_bank(layer_bank), p);
+    return ffn_plne(x, context, *device_bank_for(layer_bank), p);
 }
 
 void ffn_plne_backward(std::span<const float> x, std::span<const token_id> context, const device_bank& layer_bank,
@@ -871,7 +872,7 @@ void ffn_plne_backward(std::span<const float> x, std::span<const token_id> conte
 void ffn_plne_backward(std::span<const float> x, std::span<const token_id> context, const embedding_bank& layer_bank,
                        const ple_params& p, std::span<const float> upstream, ple_params& grads,
                        embedding_bank& bank_grads, std::span<float> dx) {
-    ffn_plne_backward(x, context, device_bank(layer_bank), p, upstream, grads, bank_grads, dx);
+    ffn_plne_backward(x, context, *device_bank_for(layer_bank), p, upstream, grads, bank_grads, dx);
 }
 
 std::vector<float> ffn_ple(std::span<const float> x, token_id token, const ple_params& p) {
@@ -891,5 +892,276 @@ void ffn_ple_backward(std::span<const float> x, token_id token, const ple_params
     ffn_plne_backward(x, ctx, bank, p, upstream, grads, bg, dx);
     for (std::size_t i = 0; i < grads.table.size(); ++i) grads.table[i] += bg.base[i];
 }
+
+// ============================================================== the reference's templates
+// (embedding.hpp:205-459, ple.hpp:148-198) over host banks: float -> the device float path,
+// double -> the device fp64 instantiation (include/ngram_b200.h, ngram_f64_*).
+namespace {
+struct F64View {  // C-ABI view of a host embedding_bank_t<double>
+    std::string cfg;
+    std::vector<const double*> sub, proj;
+    explicit F64View(const embedding_bank_t<double>& b) : cfg(to_json_string(b.config)) {
+        for (const auto& t : b.sub_tables) sub.push_back(t.data());
+        for (const auto& w : b.projections) proj.push_back(w.data());
+    }
+};
+
+void check_window(std::span<const token_id> context, const ngram_config& cfg) {
+    if (context.size() != std::size_t(cfg.max_order))
+        throw std::invalid_argument("hash_all_orders: context length " + std::to_string(context.size()) +
+                                    " does not match max order " + std::to_string(cfg.max_order));
+}
+
+// merged (and amplified) rows of one sequence in fp64 on the device
+void f64_sequence(std::span<const token_id> tokens, const embedding_bank_t<double>& bank,
+                  std::span<const token_id> prior, double* merged, double* rows) {
+    if (tokens.empty()) return;
+    const F64View v(bank);
+    throw_status(ngram_f64_forward(v.cfg.c_str(), bank.base.data(), v.sub.data(), v.proj.empty() ? nullptr : v.proj.data(),
+                                   bank.ln_gain.empty() ? nullptr : bank.ln_gain.data(),
+                                   bank.ln_bias.empty() ? nullptr : bank.ln_bias.data(), tokens.data(),
+                                   int64_t(tokens.size()), prior.empty() ? nullptr : prior.data(), int64_t(prior.size()),
+                                   merged, rows));
+}
+
+void f64_backward(std::span<const token_id> tokens, const embedding_bank_t<double>& bank,
+                  std::span<const token_id> prior, const double* merged, const double* upstream,
+                  embedding_bank_t<double>& grads) {
+    if (tokens.empty()) return;
+    const auto& cfg = bank.config;
+    if (grads.base.size() != bank.base.size() || grads.sub_tables.size() != bank.sub_tables.size())
+        throw std::invalid_argument("embed_backward: gradient bank shape does not match the bank");
+    const F64View v(bank);
+    std::vector<double*> gs, gp;
+    for (auto& t : grads.sub_tables) gs.push_back(t.data());
+    for (auto& w : grads.projections) gp.push_back(w.data());
+    const bool ln = cfg.amplification == amp_mode::layer_norm && merged;
+    throw_status(ngram_f64_backward(v.cfg.c_str(), bank.base.data(), v.sub.data(),
+                                    v.proj.empty() ? nullptr : v.proj.data(),
+                                    bank.ln_gain.empty() ? nullptr : bank.ln_gain.data(),
+                                    bank.ln_bias.empty() ? nullptr : bank.ln_bias.data(), tokens.data(),
+                                    int64_t(tokens.size()), prior.empty() ? nullptr : prior.data(),
+                                    int64_t(prior.size()), merged, upstream, grads.base.data(), gs.data(),
+                                    gp.empty() ? nullptr : gp.data(), ln ? grads.ln_gain.data() : nullptr,
+                                    ln ? grads.ln_bias.data() : nullptr));
+}
+
+int amp_code(amp_mode m) { return m == amp_mode::none ? 0 : m == amp_mode::scale_sqrt_d ? 1 : 2; }
+}  // namespace
+
+template <typename T>
+void embed_window(std::span<const token_id> context, const embedding_bank_t<T>& bank, std::span<T> out,
+                  embed_counters* counters) {
+    if constexpr (std::is_same_v<T, float>) {
+        embed_window(context, *device_bank_for(bank), out, counters);
+    } else {
+        const auto& cfg = bank.config;
+        check_window(context, cfg);
+        if (out.size() != std::size_t(cfg.dim)) throw std::invalid_argument("embed_from_ids: output size mismatch");
+        f64_sequence(context.last(1), bank, context.first(context.size() - 1), out.data(), nullptr);
+        if (counters) {
+            counters->table_gathers += 1 + std::uint64_t(cfg.branch_count());
+            if (cfg.variant == ne_variant::subtable_v2)
+                counters->projection_madds += std::uint64_t(cfg.dim) * std::uint64_t(cfg.branch_dim()) * cfg.branch_count();
+        }
+    }
+}
+
+template <typename T>
+std::vector<T> embed_v1(std::span<const token_id> context, const embedding_bank_t<T>& bank) {
+    if (bank.config.variant != ne_variant::averaged_v1) throw std::invalid_argument("embed_v1 requires the averaged variant");
+    std::vector<T> out(std::size_t(bank.config.dim));
+    embed_window<T>(context, bank, std::span<T>(out));
+    return out;
+}
+
+template <typename T>
+std::vector<T> embed_v2(std::span<const token_id> context, const embedding_bank_t<T>& bank) {
+    if (bank.config.variant != ne_variant::subtable_v2) throw std::invalid_argument("embed_v2 requires the sub-table variant");
+    std::vector<T> out(std::size_t(bank.config.dim));
+    embed_window<T>(context, bank, std::span<T>(out));
+    return out;
+}
+
+template <typename T>
+sequence_embedding<T> embed_sequence_cached(std::span<const token_id> tokens, const embedding_bank_t<T>& bank,
+                                            std::span<const token_id> prior_context, embed_counters* counters) {
+    if constexpr (std::is_same_v<T, float>) {
+        return embed_sequence_cached(tokens, *device_bank_for(bank), prior_context, counters);
+    } else {
+        const auto& cfg = bank.config;
+        sequence_embedding<double> r;
+        r.rows.resize(tokens.size() * std::size_t(cfg.dim));
+        r.merged.resize(r.rows.size());
+        f64_sequence(tokens, bank, prior_context, r.merged.data(), r.rows.data());
+        if (counters) {
+            counters->table_gathers += tokens.size() * (1 + std::uint64_t(cfg.branch_count()));
+            if (cfg.variant == ne_variant::subtable_v2)
+                counters->projection_madds +=
+                    tokens.size() * std::uint64_t(cfg.dim) * std::uint64_t(cfg.branch_dim()) * cfg.branch_count();
+        }
+        return r;
+    }
+}
+
+template <typename T>
+std::vector<T> embed_sequence(std::span<const token_id> tokens, const embedding_bank_t<T>& bank,
+                              std::span<const token_id> prior_context) {
+    return embed_sequence_cached<T>(tokens, bank, prior_context).rows;
+}
+
+template <typename T>
+void amplify(std::span<const T> e, amp_mode mode, std::span<const T> gain, std::span<const T> bias, std::span<T> out) {
+    if constexpr (std::is_same_v<T, float>) {
+        amplify(e, mode, gain, bias, out);  // the non-template float entry
+    } else {
+        const std::size_t D = e.size();
+        if (out.size() != D) throw std::invalid_argument("amplify: output size mismatch");
+        if (mode == amp_mode::layer_norm && (gain.size() != D || bias.size() != D))
+            throw std::invalid_argument("amplify: layer_norm needs gain/bias of size D");
+        const bool ln = mode == amp_mode::layer_norm;
+        throw_status(ngram_f64_amplify(amp_code(mode), int64_t(D), ln ? gain.data() : nullptr,
+                                       ln ? bias.data() : nullptr, e.data(), out.data()));
+    }
+}
+
+template <typename T>
+void amplify_backward(std::span<const T> pre, std::span<const T> upstream, const embedding_bank_t<T>& bank,
+                      embedding_bank_t<T>& grads, std::span<T> d_pre) {
+    if constexpr (std::is_same_v<T, float>) {
+        amplify_backward(pre, upstream, *device_bank_for(bank), grads, d_pre);
+    } else {
+        const std::size_t D = std::size_t(bank.config.dim);
+        if (pre.size() != D || upstream.size() != D || d_pre.size() != D)
+            throw std::invalid_argument("amplify_backward: size mismatch");
+        const bool ln = bank.config.amplification == amp_mode::layer_norm;
+        if (ln && (grads.ln_gain.size() != D || grads.ln_bias.size() != D))
+            throw std::invalid_argument("amplify_backward: gradient bank has no layer-norm parameters");
+        throw_status(ngram_f64_amplify_backward(amp_code(bank.config.amplification), int64_t(D), pre.data(),
+                                                upstream.data(), ln ? bank.ln_gain.data() : nullptr, d_pre.data(),
+                                                ln ? grads.ln_gain.data() : nullptr, ln ? grads.ln_bias.data() : nullptr));
+    }
+}
+
+template <typename T>
+void embed_backward(std::span<const token_id> context, const embedding_bank_t<T>& bank, std::span<const T> upstream,
+                    embedding_bank_t<T>& grads) {
+    if constexpr (std::is_same_v<T, float>) {
+        embed_backward(context, *device_bank_for(bank), upstream, grads);
+    } else {
+        if (upstream.size() != std::size_t(bank.config.dim))
+            throw std::invalid_argument("embed_backward: upstream size mismatch");
+        check_window(context, bank.config);
+        f64_backward(context.last(1), bank, context.first(context.size() - 1), nullptr, upstream.data(), grads);
+    }
+}
+
+template <typename T>
+void embed_sequence_backward(std::span<const token_id> tokens, const embedding_bank_t<T>& bank,
+                             std::span<const T> merged, std::span<const T> upstream, embedding_bank_t<T>& grads,
+                             std::span<const token_id> prior_context) {
+    if constexpr (std::is_same_v<T, float>) {
+        embed_sequence_backward(tokens, *device_bank_for(bank), merged, upstream, grads, prior_context);
+    } else {
+        const std::size_t n = tokens.size() * std::size_t(bank.config.dim);
+        if (upstream.size() != n || merged.size() != n)
+            throw std::invalid_argument("embed_sequence_backward: merged / upstream size mismatch");
+        f64_backward(tokens, bank, prior_context, merged.data(), upstream.data(), grads);
+    }
+}
+
+template <typename T>
+std::vector<T> ffn_ple(std::span<const T> x, token_id token, const ple_params_t<T>& p) {
+    if constexpr (std::is_same_v<T, float>) {
+        return ffn_ple(x, token, static_cast<const ple_params&>(p));
+    } else {
+        if (std::uint64_t(token) >= p.base_vocab) throw std::out_of_range("ffn_ple: token out of range");
+        if (x.size() != std::size_t(p.d_model)) throw std::invalid_argument("ple: input/gate width mismatch");
+        std::vector<double> y(std::size_t(p.d_model));
+        throw_status(ngram_f64_gated_ffn(p.d_model, p.hidden, p.gate.data(), p.down.data(), x.data(),
+                                         p.table.data() + std::size_t(token) * std::size_t(p.hidden), y.data()));
+        return y;
+    }
+}
+
+template <typename T>
+void ffn_ple_backward(std::span<const T> x, token_id token, const ple_params_t<T>& p, std::span<const T> upstream,
+                      ple_params_t<T>& grads, std::span<T> dx) {
+    if constexpr (std::is_same_v<T, float>) {
+        ffn_ple_backward(x, token, static_cast<const ple_params&>(p), upstream, static_cast<ple_params&>(grads), dx);
+    } else {
+        if (std::uint64_t(token) >= p.base_vocab) throw std::out_of_range("ffn_ple: token out of range");
+        const std::size_t row = std::size_t(token) * std::size_t(p.hidden);
+        // dL/dg accumulates straight into the table row's gradient (ple.hpp:163-165)
+        throw_status(ngram_f64_gated_ffn_backward(p.d_model, p.hidden, p.gate.data(), p.down.data(), x.data(),
+                                                  p.table.data() + row, upstream.data(), grads.gate.data(),
+                                                  grads.down.data(), dx.data(), grads.table.data() + row));
+    }
+}
+
+template <typename T>
+std::vector<T> ffn_plne(std::span<const T> x, std::span<const token_id> context, const embedding_bank_t<T>& layer_bank,
+                        const ple_params_t<T>& p) {
+    if constexpr (std::is_same_v<T, float>) {
+        return ffn_plne(x, context, static_cast<const embedding_bank&>(layer_bank), static_cast<const ple_params&>(p));
+    } else {
+        if (layer_bank.config.dim != p.hidden)
+            throw std::invalid_argument("ffn_plne: layer bank width must equal gate width");
+        if (layer_bank.config.amplification != amp_mode::none)
+            throw std::invalid_argument("ffn_plne: layer banks use no amplification");
+        std::vector<double> g(std::size_t(p.hidden)), y(std::size_t(p.d_model));
+        embed_window<double>(context, layer_bank, std::span<double>(g));
+        if (x.size() != std::size_t(p.d_model)) throw std::invalid_argument("ple: input/gate width mismatch");
+        throw_status(ngram_f64_gated_ffn(p.d_model, p.hidden, p.gate.data(), p.down.data(), x.data(), g.data(),
+                                         y.data()));
+        return y;
+    }
+}
+
+template <typename T>
+void ffn_plne_backward(std::span<const T> x, std::span<const token_id> context, const embedding_bank_t<T>& layer_bank,
+                       const ple_params_t<T>& p, std::span<const T> upstream, ple_params_t<T>& grads,
+                       embedding_bank_t<T>& bank_grads, std::span<T> dx) {
+    if constexpr (std::is_same_v<T, float>) {
+        ffn_plne_backward(x, context, static_cast<const embedding_bank&>(layer_bank), static_cast<const ple_params&>(p),
+                          upstream, static_cast<ple_params&>(grads), static_cast<embedding_bank&>(bank_grads), dx);
+    } else {
+        std::vector<double> g(std::size_t(p.hidden)), dg(std::size_t(p.hidden), 0.0);
+        embed_window<double>(context, layer_bank, std::span<double>(g));
+        throw_status(ngram_f64_gated_ffn_backward(p.d_model, p.hidden, p.gate.data(), p.down.data(), x.data(), g.data(),
+                                                  upstream.data(), grads.gate.data(), grads.down.data(), dx.data(),
+                                                  dg.data()));
+        embed_backward<double>(context, layer_bank, dg, bank_grads);  // ple.hpp:196-197
+    }
+}
+
+#define NGRAM_INSTANTIATE(T)                                                                                        \
+    template void embed_window<T>(std::span<const token_id>, const embedding_bank_t<T>&, std::span<T>,              \
+                                  embed_counters*);                                                                 \
+    template std::vector<T> embed_v1<T>(std::span<const token_id>, const embedding_bank_t<T>&);                    \
+    template std::vector<T> embed_v2<T>(std::span<const token_id>, const embedding_bank_t<T>&);                    \
+    template sequence_embedding<T> embed_sequence_cached<T>(std::span<const token_id>, const embedding_bank_t<T>&, \
+                                                            std::span<const token_id>, embed_counters*);           \
+    template std::vector<T> embed_sequence<T>(std::span<const token_id>, const embedding_bank_t<T>&,               \
+                                              std::span<const token_id>);                                          \
+    template void amplify<T>(std::span<const T>, amp_mode, std::span<const T>, std::span<const T>, std::span<T>);   \
+    template void amplify_backward<T>(std::span<const T>, std::span<const T>, const embedding_bank_t<T>&,         \
+                                      embedding_bank_t<T>&, std::span<T>);                                          \
+    template void embed_backward<T>(std::span<const token_id>, const embedding_bank_t<T>&, std::span<const T>,     \
+                                    embedding_bank_t<T>&);                                                          \
+    template void embed_sequence_backward<T>(std::span<const token_id>, const embedding_bank_t<T>&,                \
+                                             std::span<const T>, std::span<const T>, embedding_bank_t<T>&,          \
+                                             std::span<const token_id>);                                            \
+    template std::vector<T> ffn_ple<T>(std::span<const T>, token_id, const ple_params_t<T>&);                      \
+    template void ffn_ple_backward<T>(std::span<const T>, token_id, const ple_params_t<T>&, std::span<const T>,   \
+                                      ple_params_t<T>&, std::span<T>);                                              \
+    template std::vector<T> ffn_plne<T>(std::span<const T>, std::span<const token_id>, const embedding_bank_t<T>&, \
+                                        const ple_params_t<T>&);                                                    \
+    template void ffn_plne_backward<T>(std::span<const T>, std::span<const token_id>, const embedding_bank_t<T>&, \
+                                       const ple_params_t<T>&, std::span<const T>, ple_params_t<T>&,               \
+                                       embedding_bank_t<T>&, std::span<T>);
+NGRAM_INSTANTIATE(float)
+NGRAM_INSTANTIATE(double)
+#undef NGRAM_INSTANTIATE
 
 }  // namespace ngram

@@ -86,6 +86,26 @@ void launch_bf16_to_f32(const __nv_bfloat16* src, float* dst, int64_t n, cudaStr
 void launch_split_tf32(float* u, float* lo, int64_t n, cudaStream_t st);
 void launch_split_tf32_copy(const float* a, float* hi, float* lo, int64_t n, cudaStream_t st);
 // u -> u1 + u2 + u3 in bf16 (three-term split for bf16 tensor-core GEMMs with fp32-level accuracy)
+// ---- fp64 instantiations of the reference templates (f64.cu): one sequence, small banks
+void launch_f64_forward(const Shape& s, const HashTables* ht, const uint32_t* tokens, const int64_t* off, int64_t T,
+                        const uint32_t* prior, const double* base, const double* sub, const double* proj,
+                        const double* gain, const double* bias, int amp, double* merged, double* rows,
+                        cudaStream_t st);
+// ws: [T][D] d_pre + [T][2][D] zeroed LN scratch
+void launch_f64_backward(const Shape& s, const HashTables* ht, const uint32_t* tokens, const int64_t* off, int64_t T,
+                         const uint32_t* prior, const double* sub, const double* proj, const double* gain, int amp,
+                         const double* merged, const double* upstream, double* ws, double* g_base, double* g_sub,
+                         double* g_proj, double* g_gain, double* g_bias, cudaStream_t st);
+void launch_f64_amplify(int amp, int D, const double* gain, const double* bias, const double* in, double* out,
+                        cudaStream_t st);
+void launch_f64_amplify_backward(int amp, int D, const double* pre, const double* up, const double* gain,
+                                 double* d_pre, double* g_gain, double* g_bias, cudaStream_t st);
+void launch_f64_gated_ffn(int Dm, int H, const double* gate, const double* down, const double* x, const double* g,
+                          double* h_ws, double* y, cudaStream_t st);
+void launch_f64_gated_ffn_backward(int Dm, int H, const double* gate, const double* down, const double* x,
+                                   const double* g, const double* up, double* ws, double* g_gate, double* g_down,
+                                   double* dx, double* dg, cudaStream_t st);
+
 // ---- dense GEMMs (gemm_gen.cu): C[M][N] (fp32) (+)= sum of term-pair products A_i . B_j^T.
 // Operands are logical [R][K] (R = M for A, N for B): K-major maps are (inner K, rows R, box
 // 64 x 128), MN-major maps (inner R, rows K, box 64 x 64); na / nb in {1, 3} terms.

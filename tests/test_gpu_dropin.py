@@ -20,10 +20,11 @@ def test_reference_cases_through_cpp_dropin(cuda):
     assert "0 failures" in r.stdout
 
 
-@pytest.mark.parametrize("name", ["hashing", "cache"])
+@pytest.mark.parametrize("name", ["hashing", "cache", "embedding", "ple"])
 def test_reference_test_files_unmodified(cuda, name):
-    """The reference's own proj/tests/test_{hashing,cache}.cpp, compiled unmodified against
-    include/ngram (tests/cxx/Makefile, doctest / cpp_int shims) and run on the B200."""
+    """The reference's own proj/tests/test_{hashing,cache,embedding,ple}.cpp, compiled unmodified
+    against include/ngram (tests/cxx/Makefile, doctest / cpp_int shims) and run on the B200: the
+    float cases on the device float path, the double gradient checks on the device fp64 path."""
     exe = os.path.join(ROOT, "tests", "cxx", "_ref_tests", f"test_{name}")
     assert os.path.exists(exe), "build() compiles tests/cxx/_ref_tests from /root/reference (make -C tests/cxx)"
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
