@@ -977,8 +977,8 @@ def run_backward(args):
     off = torch.arange(0, T + 1, seq_len, dtype=torch.int64, device=dev)
     up = torch.randn((T, cfg["dim"]), dtype=torch.float32, device=dev, generator=gen)
     res = {}
-    modes = (("default_2term", {}), ("exact_3term", {"exact": True}), ("tf32_1term", {"tf32": True}),
-             ("pedantic_fp32", {"pedantic": True}))
+    modes = (("default_2term", {}), ("sparsebase_2term", {"sparse_base": True}), ("exact_3term", {"exact": True}),
+             ("tf32_1term", {"tf32": True}), ("pedantic_fp32", {"pedantic": True}))
     for name, kw in [m for m in modes if m[0].split("_")[0] in args.bwd_modes.split(",")]:
         gb = G.GradBank(bank, sparse_rows=True, **kw)
         for _ in range(args.warmup):
@@ -1189,7 +1189,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--batches", default="", help="decode / verify batch sizes (workloads D, E; default D 1,8,64,256 and E 64; the last is the headline)")
     ap.add_argument("--draft", type=int, default=8, help="verify block length (workload E)")
-    ap.add_argument("--bwd-modes", default="default,exact,tf32,pedantic", help="backward workload: GEMM modes to time")
+    ap.add_argument("--bwd-modes", default="default,sparsebase,exact,tf32,pedantic",
+                    help="backward workload: modes to time (sparsebase: E0 gradient as (token, u) pairs too)")
     ap.add_argument("--sharding", choices=["row", "replica"], default="row",
                     help="N > 1: row-sharded tables (default) or full replicas")
     ap.add_argument("--exchange", choices=["peer", "a2a", "rs"], default="peer",

@@ -355,6 +355,12 @@ int ngram_grad_create(ngram_bank* bank, ngram_grad** out); /* zero-initialised *
 #define NGRAM_GRAD_TF32 2
 #define NGRAM_GRAD_PEDANTIC 4
 #define NGRAM_GRAD_EXACT 8
+/* NGRAM_GRAD_SPARSE_BASE: the E0 (base-table) gradient is kept as COO pairs too -- each call
+ * appends (token, u) per position (u = the D-wide merged-row gradient, duplicates unmerged) --
+ * instead of scatter-adding into a dense V0 x D table: no per-step zeroing of that table and no
+ * read-modify-write of its rows.  ngram_grad_sparse_base reads the pairs; ngram_grad_tensor(0) /
+ * ngram_grad_download densify on request. */
+#define NGRAM_GRAD_SPARSE_BASE 16
 int ngram_grad_create_ex(ngram_bank* bank, int flags, ngram_grad** out);
 /* Row-sparse gradient view: rows = dev int32 [count] storage rows (the device layout of
  * ngram_grad_tensor(1)), vals = dev f32 [count][branch_dim]; count resets on ngram_grad_zero. */
@@ -362,6 +368,9 @@ int ngram_grad_sparse_rows(ngram_grad* g, int32_t** rows, float** vals, int64_t*
 /* Copy pairs [first, first + count) to caller buffers (host or device; stream-ordered).
  * Pairs appended by a call whose tokens were out of range carry row -1 (no gradient). */
 int ngram_grad_sparse_read(ngram_grad* g, int64_t first, int64_t count, int32_t* rows, float* vals, void* stream);
+/* NGRAM_GRAD_SPARSE_BASE: the base-table gradient pairs, tokens = dev int32 [count], vals = dev
+ * f32 [count][D]; count resets on ngram_grad_zero. */
+int ngram_grad_sparse_base(ngram_grad* g, int32_t** tokens, float** vals, int64_t* count);
 int ngram_grad_destroy(ngram_grad* g);
 int ngram_grad_zero(ngram_grad* g, void* stream);
 #define NGRAM_BWD_SKIP_AMPLIFY 1 /* upstream is d(merged) already: embed_backward only */

@@ -22,6 +22,7 @@ NGRAM_GRAD_SPARSE_ROWS = 1
 NGRAM_GRAD_TF32 = 2
 NGRAM_GRAD_PEDANTIC = 4
 NGRAM_GRAD_EXACT = 8
+NGRAM_GRAD_SPARSE_BASE = 16
 NGRAM_PLNE_FAST = 1
 NGRAM_SHARD_HANDLE_BYTES = 128
 
@@ -35,7 +36,7 @@ SYMBOLS = [
     "ngram_profile_enable", "ngram_profile_read", "ngram_decode_create", "ngram_decode_destroy", "ngram_decode_reset",
     "ngram_decode_step", "ngram_verify_block", "ngram_commit", "ngram_decode_reset_host", "ngram_decode_step_host",
     "ngram_verify_commit_host",
-    "ngram_decode_get_state", "ngram_decode_set_state_host", "ngram_gemm_f32", "ngram_f64_forward",
+    "ngram_decode_get_state", "ngram_decode_set_state_host", "ngram_gemm_f32", "ngram_grad_sparse_base", "ngram_f64_forward",
     "ngram_f64_backward", "ngram_f64_amplify", "ngram_f64_amplify_backward", "ngram_f64_gated_ffn",
     "ngram_f64_gated_ffn_backward",
     "ngram_shard_rows", "ngram_shard_group_create", "ngram_shard_group_destroy", "ngram_shard_export", "ngram_shard_open",
@@ -149,6 +150,7 @@ def lib() -> C.CDLL:
         "ngram_verify_commit_host": ([vp, vp, i32, vp, vp], i32),
         "ngram_decode_get_state": ([vp, vp, vp, vp], i32),
         "ngram_decode_set_state_host": ([vp, vp, vp, vp], i32),
+        "ngram_grad_sparse_base": ([vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(i64)], i32),
         "ngram_gemm_f32": ([i32, i64, i64, i64, vp, i64, i32, vp, i64, i32, vp, i64, i32, i32, i32, vp], i32),
         "ngram_f64_forward": ([C.c_char_p, vp, vp, vp, vp, vp, vp, i64, vp, i64, vp, vp], i32),
         "ngram_f64_backward": ([C.c_char_p, vp, vp, vp, vp, vp, vp, i64, vp, i64, vp, vp, vp, vp, vp, vp, vp], i32),

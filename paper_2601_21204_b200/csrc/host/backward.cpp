@@ -37,6 +37,11 @@ struct ngram_grad {
     DevBuf<int32_t> sp_rows;             // [sp_cap] storage rows
     DevBuf<float> sp_vals;               // [sp_cap][d]
     int64_t sp_count = 0, sp_cap = 0;
+    bool sparse_base = false;            // NGRAM_GRAD_SPARSE_BASE
+    DevBuf<int32_t> sb_tok;              // [sb_cap] tokens
+    DevBuf<float> sb_vals;               // [sb_cap][D] merged-row gradients u
+    int64_t sb_count = 0, sb_cap = 0;
+    bool e0_dense_stale = false;         // sparse base: g->e0 must be rebuilt from the pairs
     DevBuf<uint32_t> h_tokens, h_prior;  // host-buffer entry staging
     DevBuf<int64_t> h_off;
     DevBuf<float> h_merged, h_up;
@@ -50,8 +55,43 @@ namespace {
 
 void zero_all(ngram_grad* g, cudaStream_t st) {
     for (DevBuf<float>* b : {&g->e0, &g->sub, &g->w, &g->gain, &g->bias})
-        if (b->n) NGH_CUDA(cudaMemsetAsync(b->p, 0, b->n * sizeof(float), st));
+        if (b->n && !(b == &g->e0 && g->sparse_base))  // a sparse base is rebuilt from its pairs on request
+            NGH_CUDA(cudaMemsetAsync(b->p, 0, b->n * sizeof(float), st));
     g->sp_count = 0;
+    g->sb_count = 0;
+    g->e0_dense_stale = g->sparse_base;
+}
+
+// sparse base-table gradient: room for `more` (token, D-wide row) pairs, keeping the held ones
+void base_reserve(ngram_grad* g, int64_t more, int D, cudaStream_t st) {
+    const int64_t need = g->sb_count + more;
+    if (need <= g->sb_cap) return;
+    const int64_t cap = std::max<int64_t>(need, g->sb_cap * 2);
+    DevBuf<int32_t> r;
+    DevBuf<float> v;
+    r.alloc(size_t(cap));
+    v.alloc(size_t(cap) * size_t(D));
+    if (g->sb_count) {
+        NGH_CUDA(cudaMemcpyAsync(r.p, g->sb_tok.p, size_t(g->sb_count) * 4, cudaMemcpyDeviceToDevice, st));
+        NGH_CUDA(cudaMemcpyAsync(v.p, g->sb_vals.p, size_t(g->sb_count) * size_t(D) * 4, cudaMemcpyDeviceToDevice, st));
+        NGH_CUDA(cudaStreamSynchronize(st));
+    }
+    std::swap(g->sb_tok.p, r.p);
+    std::swap(g->sb_tok.n, r.n);
+    std::swap(g->sb_vals.p, v.p);
+    std::swap(g->sb_vals.n, v.n);
+    g->sb_cap = cap;
+}
+
+// sparse base: rebuild the dense E0 gradient from the pairs (ngram_grad_tensor(0) / download)
+void densify_base(ngram_grad* g, cudaStream_t st) {
+    if (!g->sparse_base || !g->e0_dense_stale) return;
+    const size_t n = size_t(g->bank->cfg.base_vocab) * size_t(g->bank->shape.D);
+    if (g->e0.n != n) g->e0.alloc(n);
+    NGH_CUDA(cudaMemsetAsync(g->e0.p, 0, n * sizeof(float), st));
+    ngk::launch_coo_densify(g->sb_tok.p, g->sb_vals.p, g->sb_count, g->bank->shape.D, g->e0.p, st);
+    NGH_CUDA(cudaGetLastError());
+    g->e0_dense_stale = false;
 }
 
 // Make room for `more` sparse (row, gradient row) pairs, preserving the ones already held.
@@ -84,7 +124,8 @@ int ngram_grad_create(ngram_bank* b, ngram_grad** out) { return ngram_grad_creat
 int ngram_grad_create_ex(ngram_bank* b, int flags, ngram_grad** out) {
     NGRAM_API_BEGIN
     if (!b || !out ||
-        (flags & ~(NGRAM_GRAD_SPARSE_ROWS | NGRAM_GRAD_TF32 | NGRAM_GRAD_PEDANTIC | NGRAM_GRAD_EXACT)) ||
+        (flags & ~(NGRAM_GRAD_SPARSE_ROWS | NGRAM_GRAD_TF32 | NGRAM_GRAD_PEDANTIC | NGRAM_GRAD_EXACT |
+                   NGRAM_GRAD_SPARSE_BASE)) ||
         __builtin_popcount(unsigned(flags & (NGRAM_GRAD_TF32 | NGRAM_GRAD_PEDANTIC | NGRAM_GRAD_EXACT))) > 1)
         throw Error(NGRAM_EINVAL, "ngram_grad_create: bad argument");
     if (b->hash_only) throw Error(NGRAM_EINVAL, "bank was created hash-only (NGRAM_BANK_HASH_ONLY)");
@@ -94,7 +135,8 @@ int ngram_grad_create_ex(ngram_bank* b, int flags, ngram_grad** out) {
     g->bank = b;
     const auto& s = b->shape;
     g->sparse = (flags & NGRAM_GRAD_SPARSE_ROWS) != 0;
-    g->e0.alloc(size_t(b->cfg.base_vocab) * size_t(s.D));
+    g->sparse_base = (flags & NGRAM_GRAD_SPARSE_BASE) != 0;
+    if (!g->sparse_base) g->e0.alloc(size_t(b->cfg.base_vocab) * size_t(s.D));  // else densified on request
     if (!g->sparse) g->sub.alloc(size_t(b->local_rows) * size_t(s.d));
     if (s.variant == 1 && s.B > 0) g->w.alloc(size_t(s.D) * size_t(s.D));
     if (s.amp == ngk::kAmpLN) {
@@ -160,9 +202,25 @@ int ngram_embed_backward(ngram_grad* g, const uint32_t* tokens, const int64_t* s
     ngk::launch_hash_ids(s, b->ht.p, tokens, seq_offsets, nseq, T, prior, nullptr, 0, g->grow.p, g->cap, b->err.p, st);
     const size_t n_td = size_t(T) * size_t(D);
     if (tc_terms) g->Ub.ensure(size_t(g->terms) * n_td);
-    ngk::launch_amp_backward(s, upstream, merged, tokens, T, amp, b->ln_gain.p, tc_terms ? nullptr : g->U.p, g->e0.p,
-                             g->gain.p, g->bias.p, b->err.p, st, tc_terms ? g->Ub.p : nullptr, g->terms,
-                             int64_t(n_td));
+    float* u_rows = tc_terms ? nullptr : g->U.p;
+    if (g->sparse_base) {  // the E0 gradient is the (token, u) pairs: u lands in the COO values directly
+        base_reserve(g, T, D, st);
+        float* vals = g->sb_vals.p + size_t(g->sb_count) * size_t(D);
+        if (u_rows) {  // v1 / pedantic paths read U later: keep writing it, then copy to the pairs
+        } else {
+            u_rows = vals;
+        }
+        NGH_CUDA(cudaMemcpyAsync(g->sb_tok.p + g->sb_count, tokens, size_t(T) * 4, cudaMemcpyDeviceToDevice, st));
+    }
+    ngk::launch_amp_backward(s, upstream, merged, tokens, T, amp, b->ln_gain.p, u_rows,
+                             g->sparse_base ? nullptr : g->e0.p, g->gain.p, g->bias.p, b->err.p, st,
+                             tc_terms ? g->Ub.p : nullptr, g->terms, int64_t(n_td));
+    if (g->sparse_base) {
+        float* vals = g->sb_vals.p + size_t(g->sb_count) * size_t(D);
+        if (u_rows != vals) NGH_CUDA(cudaMemcpyAsync(vals, u_rows, n_td * 4, cudaMemcpyDeviceToDevice, st));
+        g->sb_count += T;
+        g->e0_dense_stale = true;
+    }
     // Tensor-core banks: X (gathered rows) and W_cat are exact in bf16, so only U is split
     // (three bf16 terms = 24 mantissa bits, or one term in the single-term mode); the products
     // accumulate in fp32 TMEM.  Row-major views in the GEMM convention C[M][N] += A(m,k) B(n,k):
@@ -333,10 +391,21 @@ int ngram_grad_sparse_read(ngram_grad* g, int64_t first, int64_t count, int32_t*
     NGRAM_API_END
 }
 
+int ngram_grad_sparse_base(ngram_grad* g, int32_t** tokens, float** vals, int64_t* count) {
+    NGRAM_API_BEGIN
+    if (!g || !tokens || !vals || !count) throw Error(NGRAM_EINVAL, "ngram_grad_sparse_base: bad argument");
+    if (!g->sparse_base) throw Error(NGRAM_EINVAL, "gradient bank was not created with NGRAM_GRAD_SPARSE_BASE");
+    *tokens = g->sb_tok.p;
+    *vals = g->sb_vals.p;
+    *count = g->sb_count;
+    NGRAM_API_END
+}
+
 int ngram_grad_tensor(ngram_grad* g, int which, float** dev_ptr, int64_t* numel) {
     NGRAM_API_BEGIN
     if (!g || !dev_ptr || !numel) throw Error(NGRAM_EINVAL, "ngram_grad_tensor: bad argument");
     DevBuf<float>* t = nullptr;
+    if (which == 0) densify_base(g, nullptr);
     switch (which) {
         case 0: t = &g->e0; break;
         case 1: t = &g->sub; break;
@@ -355,6 +424,7 @@ int ngram_grad_download(ngram_grad* g, float* base, float* const* sub, float* co
     if (!g) throw Error(NGRAM_EINVAL, "null gradient bank");
     ngram_bank* b = g->bank;
     DeviceGuard dg(b->device);
+    if (base) densify_base(g, nullptr);
     NGH_CUDA(cudaDeviceSynchronize());
     const auto& s = b->shape;
     if (base) NGH_CUDA(cudaMemcpy(base, g->e0.p, g->e0.n * sizeof(float), cudaMemcpyDeviceToHost));

@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32) amp_backward_kernel(
     const bool vec = amp != kAmpLN && (D % 4) == 0;
     for (int64_t t = (int64_t)blockIdx.x * kBwdWarps + warp; t < T; t += (int64_t)gridDim.x * kBwdWarps) {
         const float* ur = up + t * D;
-        float* g0 = g_e0 + (int64_t)tokens[t] * D;
+        float* g0 = g_e0 ? g_e0 + (int64_t)tokens[t] * D : nullptr;  // null: sparse E0 (U holds the pairs)
         if (vec) {
             // 16-byte loads, stores and vector atomics (red.global.add.v4.f32): a quarter of the
             // atomic operations of the scalar form
@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32) amp_backward_kernel(
                         r[3] -= __high2float(hi);
                     }
                 }
-                atomicAdd(reinterpret_cast<float4*>(g0 + i), u);
+                if (g_e0) atomicAdd(reinterpret_cast<float4*>(g0 + i), u);
             }
         } else if (amp == kAmpLN) {
             const float* pr = pre + t * D;
@@ -127,13 +127,13 @@ __global__ void __launch_bounds__(kBwdWarps * 32) amp_backward_kernel(
                 const float s = ur[i] * gain[i];
                 const float u = scale * ((s - mean_s - xhat * mean_sx) * inv_std);
                 put_u(u, t * D + i, U, terms, nterms, tstride);
-                atomicAdd(&g0[i], u);
+                if (g_e0) atomicAdd(&g0[i], u);
             }
         } else {
             for (int i = lane; i < D; i += 32) {
                 const float u = scale * (amp == kAmpSqrt ? ur[i] * sqrt_d : ur[i]);
                 put_u(u, t * D + i, U, terms, nterms, tstride);
-                atomicAdd(&g0[i], u);
+                if (g_e0) atomicAdd(&g0[i], u);
             }
         }
     }
@@ -143,6 +143,16 @@ __global__ void __launch_bounds__(kBwdWarps * 32) amp_backward_kernel(
             atomicAdd(&g_gain[i], s_ln[i]);
             atomicAdd(&g_bias[i], s_ln[D + i]);
         }
+    }
+}
+
+// dense[tok[i]][:] += vals[i][:] (the sparse base-table gradient, densified on request)
+__global__ void coo_densify_kernel(const int32_t* __restrict__ tok, const float* __restrict__ vals, int64_t n, int D,
+                                   float* __restrict__ dense) {
+    const int64_t total = n * D;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / D;
+        atomicAdd(&dense[(int64_t)tok[i] * D + (e - i * D)], vals[e]);
     }
 }
 
@@ -341,6 +351,12 @@ void launch_split_tf32(float* u, float* lo, int64_t n, cudaStream_t st) {
 void launch_bf16_to_f32(const __nv_bfloat16* src, float* dst, int64_t n, cudaStream_t st) {
     if (n <= 0) return;
     bf16_to_f32_kernel<<<grid_for(n, 256), 256, 0, st>>>(src, dst, n);
+    count_launch();
+}
+
+void launch_coo_densify(const int32_t* tok, const float* vals, int64_t n, int D, float* dense, cudaStream_t st) {
+    if (n <= 0) return;
+    coo_densify_kernel<<<grid_for(n * D, 256), 256, 0, st>>>(tok, vals, n, D, dense);
     count_launch();
 }
 

@@ -71,7 +71,10 @@ void launch_fill_f32(float* dst, float v, int64_t n, cudaStream_t st);
 
 // ---- forward
 // ---- backward (backward.cu): embed_sequence_backward's scatter / elementwise parts
-// U (fp32, may be null) and / or `nterms` bf16 split terms of u (terms + h * tstride, may be null).
+// dense[tok[i]][:] += vals[i][:] over n D-wide rows
+void launch_coo_densify(const int32_t* tok, const float* vals, int64_t n, int D, float* dense, cudaStream_t st);
+// U (fp32, may be null) and / or `nterms` bf16 split terms of u (terms + h * tstride, may be null);
+// g_e0 null: no E0 scatter-add (the sparse base-table gradient keeps U as its values).
 void launch_amp_backward(const Shape& s, const float* up, const float* pre, const uint32_t* tokens, int64_t T,
                          int amp, const float* gain, float* U, float* g_e0, float* g_gain, float* g_bias,
                          const unsigned long long* err, cudaStream_t st, __nv_bfloat16* terms = nullptr,

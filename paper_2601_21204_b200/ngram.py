@@ -414,12 +414,13 @@ class GradBank:
     embed_sequence_backward, embedding.hpp:438-459), zero-initialised, device layout."""
 
     def __init__(self, bank: DeviceBank, sparse_rows: bool = False, tf32: bool = False, pedantic: bool = False,
-                 exact: bool = False):
+                 exact: bool = False, sparse_base: bool = False):
         self.bank = bank
         self.sparse_rows = sparse_rows
         h = C.c_void_p()
         flags = ((abi.NGRAM_GRAD_SPARSE_ROWS if sparse_rows else 0) | (abi.NGRAM_GRAD_TF32 if tf32 else 0) |
-                 (abi.NGRAM_GRAD_PEDANTIC if pedantic else 0) | (abi.NGRAM_GRAD_EXACT if exact else 0))
+                 (abi.NGRAM_GRAD_PEDANTIC if pedantic else 0) | (abi.NGRAM_GRAD_EXACT if exact else 0) |
+                 (abi.NGRAM_GRAD_SPARSE_BASE if sparse_base else 0))
         check(abi.lib().ngram_grad_create_ex(bank.handle, flags, C.byref(h)))
         self.handle = h
 
@@ -459,6 +460,18 @@ class GradBank:
         vals = torch.empty((n.value, d), dtype=torch.float32, device=dev)
         check(abi.lib().ngram_grad_sparse_read(self.handle, 0, n.value, _ptr(rows), _ptr(vals), _stream()))
         return rows, vals
+
+    def sparse_base(self, device=None):
+        """Base-table gradient pairs (sparse_base=True): (tokens int32 [n], vals f32 [n, D]) on the
+        device, a view of the bank's buffers (valid until the next backward / zero)."""
+        p_t, p_v, n = C.c_void_p(), C.c_void_p(), C.c_int64()
+        check(abi.lib().ngram_grad_sparse_base(self.handle, C.byref(p_t), C.byref(p_v), C.byref(n)))
+        if n.value == 0:
+            dev = device or torch.device("cuda", self.bank.device)
+            return (torch.empty(0, dtype=torch.int32, device=dev),
+                    torch.empty((0, self.bank.D), dtype=torch.float32, device=dev))
+        return (_device_view(p_t.value, (n.value,), torch.int32, self.bank.device),
+                _device_view(p_v.value, (n.value, self.bank.D), torch.float32, self.bank.device))
 
     def tensor(self, which: int) -> tuple:
         """(device pointer, numel) of 0 E0, 1 sub-tables, 2 W_cat, 3 ln_gain, 4 ln_bias."""

@@ -228,3 +228,25 @@ def test_default_gemms_match_pedantic_at_width(cuda):
             for k in ("default", "exact")}
     print("relL2 vs pedantic (W_cat, sub rows):", errs)
     assert max(errs["default"]) < 1e-5 and max(errs["exact"]) < 2e-6, errs
+
+
+@pytest.mark.parametrize("name", ["backward_tc_scale_sqrt_d.npz", "backward_tc_layer_norm.npz", "backward_simt_v2.npz"])
+def test_sparse_base_equals_dense(cuda, name):
+    """NGRAM_GRAD_SPARSE_BASE keeps the E0 gradient as (token, u) pairs: the pairs sum to the dense
+    gradient (densified on request), two accumulating calls append, zero() clears."""
+    g, cfg, hb, db, args, ln = _setup(name, cuda)
+    dense = G.GradBank(db)
+    sparse = G.GradBank(db, sparse_base=True)
+    for gb in (dense, sparse):
+        gb.backward(**args)
+        gb.backward(**args)
+    db.sync_errors()
+    toks, vals = sparse.sparse_base()
+    assert toks.numel() == 2 * args["tokens"].numel() and vals.shape[1] == db.D
+    a, b = dense.download(), sparse.download()
+    # both sums are fp32 atomics in no fixed order: equal to fp32 rounding of the largest terms
+    for x, y in zip([a["base"]] + a["sub"] + a["proj"], [b["base"]] + b["sub"] + b["proj"]):
+        assert np.abs(x - y).max() <= 1e-5 * max(float(np.abs(x).max()), 1e-30)
+    sparse.zero()
+    t2, _ = sparse.sparse_base()
+    assert t2.numel() == 0 and float(np.abs(sparse.download()["base"]).max()) == 0.0
