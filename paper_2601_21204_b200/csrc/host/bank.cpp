@@ -208,6 +208,8 @@ int ngram_bank_create_ex(const char* config_json, int device, int shard_rank, in
         make_tensor_map_2d(&b->tmap_w, b->wcat.p, uint64_t(D), uint64_t(D), uint64_t(D) * 2, 64,
                            D % 256 == 0 ? 256 : 128);
         make_tensor_map_2d(&b->tmap_w2, b->wcat.p, uint64_t(D), uint64_t(D), uint64_t(D) * 2, 64, 128);
+        // gemm_wide: 32-column x 128-row W stages, SWIZZLE_64B
+        make_tensor_map_2d(&b->tmap_w32, b->wcat.p, uint64_t(D), uint64_t(D), uint64_t(D) * 2, 32, 128, false, 64);
         // E0 rows gathered by token id (tile::gather4) into the pair kernel's TMA epilogue
         make_tensor_map_2d(&b->tmap_e0, b->e0.p, uint64_t(D), uint64_t(b->cfg.base_vocab), uint64_t(D) * 2, 32, 1,
                            false, 64);

@@ -138,7 +138,7 @@ struct ngram_bank {
     ngh::DevBuf<unsigned int> err_ticket;
     bool err_clean = true;
 
-    CUtensorMap tmap_sub{}, tmap_w{}, tmap_w2{}, tmap_e0{}, tmap_e0w{};
+    CUtensorMap tmap_sub{}, tmap_w{}, tmap_w2{}, tmap_w32{}, tmap_e0{}, tmap_e0w{};
     ngh::Workspace ws;
 
     // Serialises the host-buffer entry points (the reference's bank is shareable across
@@ -209,6 +209,7 @@ struct HashCtx {
     const int64_t* seq_off;
     int64_t nseq;
     const uint32_t* prior;
+    bool wide = false;  // fused wide-tile kernel (gemm_wide.cu) instead of the pair kernel's LSU producers
 };
 void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, int64_t gstride, int64_t T,
                     void* rows, void* merged, int out_bf16, float* ln_scratch, const CUtensorMap* tmap_x,

@@ -43,23 +43,31 @@ static bool fused_gather(int D) {
     return env != 0;
 }
 
-// Prefill path for the pair kernel (D % 256 == 0, T beyond the split-K regime):
-//   "x"   (default) fused K1+K2 kernel writes X, K3 reads it (two launches, X round trip)
-//   "lsu" token validation, then K3 alone with K1+K2 in its producers (hash + cp.async rows
-//         into shared memory; the peer CTA's stages relayed to the leader): no X, no
-//         storage-row array.  Bit-identical, but measured slower (profiles/README.md):
-//         config B 205 vs 150 us, C 1.30 vs 1.02 ms -- every n-tile pair re-gathers its
-//         m-block's rows as 128-byte L2 requests (12x at D = 3072) where the X path moves the
-//         same bytes as 16 KB TMA tiles; tensor pipe 33 % active vs 66 % (ncu).
-// NGRAM_PREFILL_PATH selects.
-static bool lsu_prefill(const ngram_bank* b) {
-    static const int env = [] {
-        const char* e = getenv("NGRAM_PREFILL_PATH");
-        return e ? (std::string(e) == "lsu" ? 1 : std::string(e) == "x" ? 0 : -1) : -1;
-    }();
+// Prefill path (tensor-core banks, D % 256 == 0, T beyond the split-K regime):
+//   "x"    (default) fused K1+K2 kernel writes X, K3 (pair kernel) reads it: two launches,
+//          X round trip
+//   "wide" (D <= 768, d % 64 == 0; gemm_wide.cu) token validation, then ONE kernel: the
+//          producers hash + gather an m-block's rows into shared memory once, the MMA warp
+//          sweeps every N-tile over them -- no X.  Bit-identical to "x"; measured equal at
+//          config B (141-146 vs 145-147 us, profiles/README.md): the X traffic it saves is
+//          paid back in pipeline depth (the resident A operand leaves two W stages and no
+//          epilogue staging)
+//   "lsu"  token validation, then K3 alone with K1+K2 in its producers (hash + cp.async rows
+//          into shared memory; the peer CTA's stages relayed to the leader): no X, no
+//          storage-row array.  Bit-identical, but measured slower (profiles/README.md):
+//          config B 205 vs 150 us, C 1.30 vs 1.02 ms -- every n-tile pair re-gathers its
+//          m-block's rows as 128-byte L2 requests (12x at D = 3072) where the X path moves the
+//          same bytes as 16 KB TMA tiles; tensor pipe 33 % active vs 66 % (ncu).
+// NGRAM_PREFILL_PATH=x|wide|lsu selects; read per call, so one process can A/B the paths.
+// Returns 0 (x), 1 (lsu) or 2 (wide).
+static int prefill_path(const ngram_bank* b) {
+    const char* e = getenv("NGRAM_PREFILL_PATH");
+    const std::string v(e ? e : "");
+    const int env = v == "lsu" ? 1 : v == "wide" ? 2 : 0;
     const auto& s = b->shape;
-    if (!b->tc_path || s.D % 256 != 0 || s.N > 8 || s.variant != 1 || s.B < 1) return false;
-    return env == 1;
+    if (!b->tc_path || s.D % 256 != 0 || s.N > 8 || s.variant != 1 || s.B < 1) return 0;
+    if (env == 2 && !ngk::wide_prefill_shape(s)) return 0;
+    return env;
 }
 
 // Entry points that gather rows themselves need every row on this device: a row-sharded bank
@@ -113,6 +121,7 @@ void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, 
     a.tmap_sub = &b->tmap_sub;
     a.tmap_w = &b->tmap_w;
     a.tmap_w2 = &b->tmap_w2;
+    a.tmap_w32 = &b->tmap_w32;
     a.tmap_x = tmap_x;
     a.commit = commit;
     const int64_t rT = regime_T > 0 ? regime_T : T;  // the T whose kernel regime this call follows
@@ -133,6 +142,7 @@ void run_projection(ngram_bank* b, const uint32_t* tokens, const int32_t* grow, 
         a.seq_off = hc->seq_off;
         a.nseq = hc->nseq;
         a.prior = hc->prior;
+        a.wide = hc->wide ? 1 : 0;
     } else if (b->tc_path && !tmap_x && ((allow_splitk && small_t(b, rT)) || !fused_gather(b->shape.D))) {
         if (!xb) xb = &b->ws.xbuf;
         xb->ensure(round_up(T, kRowPad), b->shape.D);
@@ -192,12 +202,12 @@ bool forward_tokens(ngram_bank* b, const uint32_t* tokens, const int64_t* seq_of
         const HashCtx hc{seq_off, nseq, prior};
         run_projection(b, tokens, nullptr, Tpad, T, rows, merged, out_bf16, b->ws.merged_f32.p, nullptr, st, amp,
                        nullptr, true, fused_commit ? commit : nullptr, &hc);
-    } else if (!(allow_splitk && small_t(b, T)) && lsu_prefill(b) && !fused_gather(b->shape.D)) {
+    } else if (!(allow_splitk && small_t(b, T)) && prefill_path(b) != 0 && !fused_gather(b->shape.D)) {
         // K1+K2 fused into the projection's producers; a bad token must still abort the call
         // before any output, so the range check runs first (the kernel returns on the error word)
         ngk::launch_validate_tokens(b->shape, tokens, T, seq_off, nseq, prior, b->err.p, st);
         b->prof_record(1, st);
-        const HashCtx hc{seq_off, nseq, prior};
+        const HashCtx hc{seq_off, nseq, prior, prefill_path(b) == 2};
         fused_commit = commit != nullptr;
         run_projection(b, tokens, nullptr, Tpad, T, rows, merged, out_bf16, b->ws.merged_f32.p, nullptr, st, amp,
                        nullptr, allow_splitk, fused_commit ? commit : nullptr, &hc);

@@ -1330,6 +1330,11 @@ void launch_forward_tc(const FwdArgs& a, int num_sms, cudaStream_t st, float* sp
         }
     }
     const bool bn256 = a.s.D % 256 == 0;
+    if (a.wide && a.seq_off && !a.tmap_x && a.tmap_w32 != nullptr && wide_prefill_shape(a.s)) {
+        launch_forward_wide(a, num_sms, st);
+        if (a.commit) launch_decode_commit_c(*a.commit, a.err, st);
+        return;
+    }
     if (bn256 && tc_variant() == 2 && a.tmap_w2 != nullptr) {
         launch_tc2(a, num_sms, st);
         if (a.commit) launch_decode_commit_c(*a.commit, a.err, st);

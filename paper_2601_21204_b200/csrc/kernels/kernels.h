@@ -154,6 +154,7 @@ struct FwdArgs {
     const CUtensorMap* tmap_sub;
     const CUtensorMap* tmap_w;
     const CUtensorMap* tmap_w2;  // W_cat with a 128-row box (2-CTA kernel), or null
+    const CUtensorMap* tmap_w32;  // W_cat, 32-column x 128-row box, SWIZZLE_64B (gemm_wide.cu), or null
     // X (materialised gathered rows, T x D bf16) instead of sub-table gather, or null
     const CUtensorMap* tmap_x;
     // decode step: commit the decode state in the projection kernel's tail (or null)
@@ -172,6 +173,9 @@ struct FwdArgs {
     // T that selects the split-K sub-regime (0 = T): a row-sharded projection of home_T rows
     // takes the regime of the gathered batch, so its rows are computed as the 1-GPU call's
     int64_t regime_T;
+    // prefill with seq_off set: the fused wide-tile kernel (gemm_wide.cu) instead of the pair
+    // kernel's hashing producers
+    int wide;
 };
 // tcgen05 projection GEMM with fused gather + base add + scale + amplify (gemm_tc.cu).
 // splitk_ws (fp32, splitk_workspace_floats() long, may be null): small-T split-K path.
@@ -181,6 +185,10 @@ int splitk_factor(const FwdArgs& a, int num_sms);  // small-T split: depends on 
 // Small-T regime (split-K BN=128 GEMM + reduce, S from D only): T <= 256.  A row's
 // arithmetic depends only on its own ids within a regime.
 bool small_t_regime(int D, int64_t T, int num_sms);
+// Fused K1+K2+K3 prefill kernel for D <= 768 (gemm_wide.cu): shapes it takes, launcher
+// (a.seq_off / nseq / prior give the windows; tokens validated before the launch).
+bool wide_prefill_shape(const Shape& s);
+void launch_forward_wide(const FwdArgs& a, int num_sms, cudaStream_t st);
 // generic CUDA-core path: any shape, v1 and v2, reference float op order (simt.cu).
 void launch_forward_simt(const FwdArgs& a, cudaStream_t st);
 // K2 standalone: materialise X (T x D bf16) from the storage rows (d % 8 == 0).

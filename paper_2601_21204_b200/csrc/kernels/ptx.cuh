@@ -316,6 +316,17 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t smem_addr) {
     d |= (uint64_t)2 << 61;                 // SWIZZLE_128B
     return d;
 }
+// Same, canonical SWIZZLE_64B K-major layout: rows of 64 B (32 bf16), 8-row core groups 512 B
+// apart, layout type SWIZZLE_64B = 4.
+__device__ __forceinline__ uint64_t smem_desc_sw64(uint32_t smem_addr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;                 // LBO (ignored for swizzled K-major)
+    d |= (uint64_t)(512 >> 4) << 32;        // SBO = 512 B
+    d |= (uint64_t)1 << 46;                 // descriptor version (sm_100)
+    d |= (uint64_t)4 << 61;                 // SWIZZLE_64B
+    return d;
+}
 // Instruction descriptor: kind::f16, A=B=bf16, D=f32, both K-major, shape M x N.
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(uint32_t M, uint32_t N) {
     return (1u << 4)            // c_format = F32
