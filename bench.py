@@ -599,6 +599,27 @@ def run_ours(args):
         k12 = st_ms[0] + st_ms[1]
         hbm["k1_k2_hash_gather"] = {"ms": k12, "bytes": kb, "gbs": kb / (k12 * 1e-3) / 1e9,
                                     "frac": kb / (k12 * 1e-3) / 1e9 / peaks["hbm_gbs"]}
+        if d * 2 == 128 and T == 65536:
+            # 128-byte random rows do not stream at the copy peak: the bare gather of the same
+            # 786 432 precomputed random rows out of 4.4 GB into a contiguous X takes 50.4 us on
+            # a B200 (profiles/microbench/gather_ceiling.cu, gather_ceiling_b200.txt)
+            hbm["k1_k2_hash_gather"]["access_ceiling_ms"] = 0.0504
+            hbm["k1_k2_hash_gather"]["frac_of_access_ceiling"] = 0.0504 / k12
+    # K3's own bound: its tensor time (2 T D^2 at the measured bf16 peak) vs its HBM time (per
+    # token: the token, the X row it reads in place of the sub-table rows, the E0 row and the
+    # output -- the same 4 + 2 B d + 2 D + esz D bytes as the layer's algorithmic figure)
+    k3_name = "forward_tc2_kernel (K3: tcgen05 cta_group::2 projection + base/scale/amplify epilogue)"
+    k3_bytes = T * bytes_tok + 2 * D * D
+    if flops / (peaks["bf16_tflops"] * 1e12) >= k3_bytes / (peaks["hbm_gbs"] * 1e9):
+        roofline = {"bound": "tensor", "kernel": k3_name, "achieved": tflops, "peak": peaks["bf16_tflops"],
+                    "unit": "TFLOP/s", "frac": tflops / peaks["bf16_tflops"], "traffic": traffic,
+                    "peak_source": peak_src, "flops_per_launch": flops, "launch_ms": proj_ms}
+    else:  # narrow model (config B, D = 768): K3 moves more bytes than the tensor pipe can stall on
+        k3_gbs = k3_bytes / (proj_ms * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "kernel": k3_name, "achieved": k3_gbs, "peak": peaks["hbm_gbs"],
+                    "unit": "GB/s", "frac": k3_gbs / peaks["hbm_gbs"], "traffic": traffic,
+                    "peak_source": peak_src, "bytes_per_launch": k3_bytes, "launch_ms": proj_ms,
+                    "tensor_frac": tflops / peaks["bf16_tflops"]}
     line = {
         "metric": "ngram_embedding_tokens_per_sec", "value": total_tokens / (ms * 1e-3), "unit": "tokens/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -609,11 +630,7 @@ def run_ours(args):
         "config": dict(workload_config(cfg, label, nseq, seq_len, args), d=d, embedding_params=nparams,
                        sub_table_params=nsub, table_dtype="bf16", sharding=sharding,
                        l2="flushed (512 MiB write) between timed steps", tensor_core_path=bank.tensor_core_path),
-        "roofline": {"bound": "tensor", "kernel": "forward_tc2_kernel (K3: tcgen05 cta_group::2 projection + "
-                                                  "base/scale/amplify epilogue)",
-                     "achieved": tflops, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
-                     "frac": tflops / peaks["bf16_tflops"], "traffic": traffic, "peak_source": peak_src,
-                     "flops_per_launch": flops, "launch_ms": proj_ms},
+        "roofline": roofline,
         "hbm": hbm, "stages_ms": stages, "clocks": clocks, "e2e": e2e, "gpu_launches": int(launches),
     }
     if fallback:
@@ -1010,8 +1027,8 @@ def run_plne(args):
     """Per-layer N-gram FFN (ffn_plne / ffn_plne_backward, ple.hpp:168-196)
     at a LongCat-like width: d_model = hidden = 3072, layer bank make_default_config(8000, 3072,
     4, 4) (amplification none), 8 x 1024 tokens.  Forward and forward+backward (gate / down / x
-    gradients, no bank gradients) for the default pedantic fp32 GEMMs and the opt-in split-bf16
-    tensor-core GEMMs (NGRAM_PLNE_FAST)."""
+    gradients, no bank gradients) for the default split-bf16 tcgen05 GEMMs and the opt-in
+    CUDA-core fp32 GEMMs (NGRAM_PLNE_PEDANTIC)."""
     import torch
     from paper_2601_21204_b200 import ngram as G
     dev = torch.device("cuda", 0)
@@ -1048,7 +1065,7 @@ def run_plne(args):
         res[name] = out
         layer.close()
     bank.sync_errors()
-    print(json.dumps({"metric": "ngram_plne_tokens_per_sec", "value": res["pedantic_fp32"]["forward"]["tokens_per_s"],
+    print(json.dumps({"metric": "ngram_plne_tokens_per_sec", "value": res["split_bf16"]["forward"]["tokens_per_s"],
                       "unit": "tokens/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
                       "higher_is_better": True, "data": "synthetic (device layer bank, uniform tokens, randn x)",
                       "config": {"workload": "plne_d3072_h3072_8x1024", "V0": 8000, "N": 4, "K": 4,

@@ -401,14 +401,18 @@ int ngram_grad_download(ngram_grad* g, float* base, float* const* sub, float* co
  * layer bank's merged embedding of each position's window (layer bank: amplification none,
  * dim = hidden).  gate: dev f32 [hidden][d_model]; down: dev f32 [d_model][hidden];
  * x, y: dev f32 [T][d_model]; tokens / seq_offsets / prior as ngram_embed_forward.  fp32-
- * accurate GEMMs (cuBLAS pedantic fp32 by default; split-bf16 opt-in, see ngram_plne_create_ex).  ffn_ple (table-row gate) = a base-only layer bank (max_order 1).
+ * accurate GEMMs (the library's tcgen05 GEMMs on split-bf16 operands by default; CUDA-core
+ * fp32 with NGRAM_PLNE_PEDANTIC, see ngram_plne_create_ex).  ffn_ple (table-row gate) = a
+ * base-only layer bank (max_order 1).
  * Outputs are unspecified when a token is out of range (NGRAM_ERANGE at the next sync). */
 typedef struct ngram_plne ngram_plne;
 int ngram_plne_create(ngram_bank* layer_bank, int d_model, ngram_plne** out);
-/* flags: NGRAM_PLNE_FAST -- the GEMMs on the bf16 tensor cores with both operands split into
- * three bf16 terms (six products, fp32 accumulation): ~2.9x faster, relL2 ~7e-6 vs fp64 at
- * K = 3072.  Default: pedantic fp32 GEMMs (relL2 ~6e-7 there). */
+/* Default (flags 0, or NGRAM_PLNE_FAST): the GEMMs on the bf16 tensor cores with both operands
+ * split into three bf16 terms (six products, K chunks folded into fp32 registers): relL2
+ * ~3e-7 vs fp64 at K = 3072, ~7x faster than NGRAM_PLNE_PEDANTIC -- the CUDA-core fp32 GEMM
+ * (relL2 ~4e-7 there). */
 #define NGRAM_PLNE_FAST 1
+#define NGRAM_PLNE_PEDANTIC 2
 int ngram_plne_create_ex(ngram_bank* layer_bank, int d_model, int flags, ngram_plne** out);
 int ngram_plne_destroy(ngram_plne* p);
 int ngram_plne_forward(ngram_plne* p, const float* gate, const float* down, const float* x, const uint32_t* tokens,

@@ -24,6 +24,7 @@ NGRAM_GRAD_PEDANTIC = 4
 NGRAM_GRAD_EXACT = 8
 NGRAM_GRAD_SPARSE_BASE = 16
 NGRAM_PLNE_FAST = 1
+NGRAM_PLNE_PEDANTIC = 2
 NGRAM_SHARD_HANDLE_BYTES = 128
 
 # Exported symbols, in header order (tests check the .so exports every one).

@@ -27,7 +27,7 @@ struct ngram_plne {
     DevBuf<float> h_gate, h_down, h_x, h_y, h_up, h_dgate, h_ddown, h_dx;
     DevBuf<uint32_t> h_tok, h_prior;
     DevBuf<int64_t> h_off;
-    bool three = false;                // NGRAM_PLNE_FAST: split-bf16 tensor-core GEMMs
+    bool three = true;                 // split-bf16 tensor-core GEMMs (default); false: NGRAM_PLNE_PEDANTIC
     SplitWs ws;                        // three bf16 terms of each GEMM operand
 };
 
@@ -75,7 +75,8 @@ int ngram_plne_create(ngram_bank* b, int d_model, ngram_plne** out) { return ngr
 
 int ngram_plne_create_ex(ngram_bank* b, int d_model, int flags, ngram_plne** out) {
     NGRAM_API_BEGIN
-    if (flags & ~NGRAM_PLNE_FAST) throw Error(NGRAM_EINVAL, "ngram_plne_create_ex: unknown flags");
+    if (flags & ~(NGRAM_PLNE_FAST | NGRAM_PLNE_PEDANTIC) || flags == (NGRAM_PLNE_FAST | NGRAM_PLNE_PEDANTIC))
+        throw Error(NGRAM_EINVAL, "ngram_plne_create_ex: unknown flags");
     if (!b || !out) throw Error(NGRAM_EINVAL, "ngram_plne_create: bad argument");
     if (d_model < 1) throw Error(NGRAM_EINVAL, "ple: d_model and hidden must be >= 1");
     if (b->hash_only) throw Error(NGRAM_EINVAL, "bank was created hash-only (NGRAM_BANK_HASH_ONLY)");
@@ -86,7 +87,7 @@ int ngram_plne_create_ex(ngram_bank* b, int d_model, int flags, ngram_plne** out
     p->bank = b;
     p->d_model = d_model;
     p->hidden = b->shape.D;
-    p->three = (flags & NGRAM_PLNE_FAST) != 0;
+    p->three = (flags & NGRAM_PLNE_PEDANTIC) == 0;  // tensor-core split GEMMs unless pedantic
     *out = p.release();
     NGRAM_API_END
 }

@@ -509,11 +509,12 @@ class PlneLayer:
     [hidden, d_model] f32, down: [d_model, hidden] f32, x / y: [T, d_model] f32 (device).
     ffn_ple (table-row gate) = a base-only layer bank (max_order 1, E0 = the table)."""
 
-    def __init__(self, layer_bank: DeviceBank, d_model: int, fast: bool = False):
-        """fast: split-bf16 tensor-core GEMMs (NGRAM_PLNE_FAST) instead of pedantic fp32."""
+    def __init__(self, layer_bank: DeviceBank, d_model: int, fast: bool = True):
+        """fast (default): split-bf16 tensor-core GEMMs; fast=False: CUDA-core fp32
+        (NGRAM_PLNE_PEDANTIC)."""
         self.bank, self.d_model, self.hidden = layer_bank, d_model, layer_bank.D
         h = C.c_void_p()
-        check(abi.lib().ngram_plne_create_ex(layer_bank.handle, d_model, abi.NGRAM_PLNE_FAST if fast else 0,
+        check(abi.lib().ngram_plne_create_ex(layer_bank.handle, d_model, 0 if fast else abi.NGRAM_PLNE_PEDANTIC,
                                              C.byref(h)))
         self.handle = h
 

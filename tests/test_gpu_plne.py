@@ -34,7 +34,7 @@ def _setup(name, cuda):
     return g, cfg, hb, db, a
 
 
-@pytest.mark.parametrize("fast", [False, True])  # pedantic fp32 (default) / split-bf16 tensor cores
+@pytest.mark.parametrize("fast", [False, True])  # pedantic fp32 / split-bf16 tensor cores (default)
 @pytest.mark.parametrize("name", ["plne_tc.npz", "plne_small.npz"])
 def test_plne_forward_matches_reference(cuda, name, fast):
     g, cfg, hb, db, a = _setup(name, cuda)
@@ -92,8 +92,9 @@ def test_plne_validates_the_layer_bank_and_tokens(cuda):  # test_ple.cpp:174-181
 
 def test_split_bf16_gemms_match_fp64_at_width(cuda):
     """At a LongCat-like width (d_model = hidden = 3072, K = 3072 accumulations), vs an fp64
-    evaluation: the default pedantic fp32 GEMMs within 1e-6 relL2, the opt-in split-bf16 ones
-    (NGRAM_PLNE_FAST) within 1e-5 (forward and the gate / down / x gradients).  (A three-term
+    evaluation: the default split-bf16 tensor-core GEMMs within 2e-6 relL2 and the pedantic
+    CUDA-core fp32 ones (NGRAM_PLNE_PEDANTIC) within 1e-6 (forward and the gate / down / x
+    gradients).  (A three-term
     TF32 split measured 1.5e-5 here and was dropped.)"""
     cfg = O.make_default_config(500, 3072, 3, 2)
     cfg["amplification"] = "none"
@@ -129,4 +130,4 @@ def test_split_bf16_gemms_match_fp64_at_width(cuda):
         errs[fast] = [float((a.double() - r).norm() / r.norm()) for a, r in zip((y, dg, dd, dx), refs)]
     print("relL2 vs fp64 (split-bf16, pedantic):", errs[True], errs[False])
     for ef, ep in zip(errs[True], errs[False]):
-        assert ef < 1e-5 and ep < 1e-6, errs
+        assert ef < 2e-6 and ep < 1e-6, errs
