@@ -9,6 +9,7 @@ but the GPU pool refuses compute-sanitizer (profiles/r02_sanitizer.txt), so the 
 per-step invariants are the evidence.  Not a pytest module (no test_ prefix); run as one
 process.  Each step checks its result against a cheap invariant.
 Paths: fused K1+K2 + the pair tcgen05 projection (every amplification, fp32 / bf16 out), the
+fused wide-tile prefill kernel (D <= 768), the
 1-CTA tile and the split-K small-T GEMM + reduce, the CUDA-core kernels, decode step / verify /
 commit (fused error-word release), the backward (gather, amp_backward, both tcgen05 GEMM
 layouts, COO append), the generic GEMM in every layout / term count, PLNE (both modes), the
@@ -86,6 +87,34 @@ def forward_paths():
     rows, _ = G.embed_forward(bank, u32(np.arange(20) % 50), i64([0, 20]))
     bank.sync_errors()
     assert torch.isfinite(rows).all()
+
+
+def wide_paths():
+    # the fused wide-tile prefill kernel (gemm_wide.cu; NGRAM_PREFILL_PATH is read per call):
+    # canary-guarded rows-only fp32 (the OUT = 1 instance) and rows + merged bf16, ragged T,
+    # every width it takes; bits equal to the X path
+    for D in (256, 512, 768):
+        cfg = O.make_default_config(1000, D, 4 if D == 768 else 3, 4 if D == 768 else 2)
+        bank = G.DeviceBank(cfg).generate(9)
+        for T in (300, 1029):
+            step(f"wide prefill D={D} T={T}")
+            toks = u32(np.random.default_rng(T + D).integers(0, 1000, size=T))
+            off = i64([0, T // 2, T])
+            os.environ["NGRAM_PREFILL_PATH"] = "x"
+            ref, refm = G.embed_forward(bank, toks, off, merged=True, out_dtype=torch.bfloat16)
+            os.environ["NGRAM_PREFILL_PATH"] = "wide"
+            rv, chk = guarded((T, D))
+            G.embed_forward(bank, toks, off, out_rows=rv)
+            mv, chkm = guarded((T, D), torch.bfloat16)
+            rbv, chkr = guarded((T, D), torch.bfloat16)
+            G.embed_forward(bank, toks, off, merged=True, out_dtype=torch.bfloat16, out_rows=rbv, out_merged=mv)
+            bank.sync_errors()
+            chk(f"wide fp32 D={D} T={T}")
+            chkm(f"wide merged D={D} T={T}")
+            chkr(f"wide bf16 D={D} T={T}")
+            assert torch.equal(rbv, ref) and torch.equal(mv, refm)
+            os.environ.pop("NGRAM_PREFILL_PATH")
+            assert torch.isfinite(rv).all()
 
 
 def decode_paths():
@@ -199,7 +228,7 @@ def shard_paths():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["forward", "decode", "backward", "gemm", "plne", "analysis", "shard"]
+    which = sys.argv[1:] or ["forward", "wide", "decode", "backward", "gemm", "plne", "analysis", "shard"]
     for w in which:
         globals()[w + "_paths"]()
     torch.cuda.synchronize()
