@@ -1330,6 +1330,20 @@ void launch_forward_tc(const FwdArgs& a, int num_sms, cudaStream_t st, float* sp
         }
     }
     const bool bn256 = a.s.D % 256 == 0;
+    // Verify-sized T (past the split-K regime) whose 128 x 128 single-CTA tiles still fit one wave:
+    // more SMs busy than the pair kernel's few 256 x 256 tiles (D = 3072, 64 streams x 8 drafts:
+    // 96 CTAs vs 24 pairs), bit-identical results (same K order per element; tested).  Measured
+    // at D = 3072, L2 flushed, verify + commit: T = 320..768 2.0-3.5 us faster; T = 1024 (two
+    // waves) 10 us slower.  NGRAM_VERIFY_TILE=0 keeps the pair kernel (read per call: tests pin
+    // the pair kernel's epilogue on small ragged batches with it).
+    const char* vte = getenv("NGRAM_VERIFY_TILE");
+    const bool vt = !(vte && atoi(vte) == 0);
+    if (vt && a.tmap_x && a.s.D % 128 == 0 && !small_t_regime(a.s.D, a.T, num_sms) &&
+        ((a.T + 127) / 128) * (a.s.D / 128) <= num_sms && !a.wide) {
+        launch_cfg<128, 4, 1>(a, num_sms, st);
+        if (a.commit) launch_decode_commit_c(*a.commit, a.err, st);
+        return;
+    }
     if (a.wide && a.seq_off && !a.tmap_x && a.tmap_w32 != nullptr && wide_prefill_shape(a.s)) {
         launch_forward_wide(a, num_sms, st);
         if (a.commit) launch_decode_commit_c(*a.commit, a.err, st);

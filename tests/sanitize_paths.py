@@ -67,7 +67,7 @@ def forward_paths():
         cfg = O.make_default_config(1000, D, 3, 2)
         cfg["amplification"] = amp
         bank = G.DeviceBank(cfg).generate(3)
-        for T in (40, 300, 700):  # split-K small T, pair / 1-CTA tile, ragged
+        for T in (40, 300, 700, 20000 if D == 256 else 900):  # split-K, one-wave 1-CTA tiles, pair tiles, ragged
             step(f"forward D={D} amp={amp} T={T}")
             toks = np.random.default_rng(T).integers(0, 1000, size=T)
             off = [0, T // 3, T]

@@ -276,11 +276,12 @@ def test_fused_k1_k2_k3_kernel_matches_oracle(cuda):
 
 
 @pytest.mark.parametrize("out_dtype", [torch.float32, torch.bfloat16])
-def test_pair_kernel_tma_epilogue_edges(cuda, out_dtype):
+def test_pair_kernel_tma_epilogue_edges(cuda, out_dtype, monkeypatch):
     """The 2-CTA projection's TMA epilogue (E0 rows by tile::gather4, outputs by bulk tensor
     stores clipped at T): ragged T (not a multiple of 32 / 128 / 256), rows + merged; the
     direct-store epilogue and the 32-column E0 gather variant (NGRAM_TMA_EPI=0 / 1 in a
     subprocess are the A/B switches) compute the same bits.  Output buffers that are not 16-byte aligned are rejected up front."""
+    monkeypatch.setenv("NGRAM_VERIFY_TILE", "0")  # T = 1298 would take the one-wave 128 x 128 tiles
     cfg = O.make_default_config(3000, 512, 3, 2)
     hb = O.make_bank(cfg, 17, round_bf16=True)
     db = G.DeviceBank(cfg).upload(hb.base, hb.sub, hb.proj)
@@ -290,6 +291,12 @@ def test_pair_kernel_tma_epilogue_edges(cuda, out_dtype):
     T = len(allt)
     t, o = dev_u32(torch, allt, cuda), dev_i64(torch, off, cuda)
     rows, merged = G.embed_forward(db, t, o, merged=True, out_dtype=out_dtype)
+    # the one-wave 128 x 128 single-CTA tiles compute the same bits
+    monkeypatch.setenv("NGRAM_VERIFY_TILE", "1")
+    r1, m1 = G.embed_forward(db, t, o, merged=True, out_dtype=out_dtype)
+    monkeypatch.setenv("NGRAM_VERIFY_TILE", "0")
+    db.sync_errors()
+    assert torch.equal(r1, rows) and torch.equal(m1, merged)
     db.sync_errors()
     ref_r, ref_m = zip(*[O.embed_sequence(hb, s, double=True) for s in seqs])
     bf = out_dtype == torch.bfloat16
@@ -323,7 +330,7 @@ np.save(sys.argv[1], torch.stack([r, m]).view(torch.int16 if r.dtype == torch.bf
         with tempfile.TemporaryDirectory() as td:
             path = os.path.join(td, "other.npy")
             subprocess.run([sys.executable, "-c", code, path], check=True, timeout=300,
-                           env={**os.environ, "NGRAM_TMA_EPI": mode})
+                           env={**os.environ, "NGRAM_TMA_EPI": mode, "NGRAM_VERIFY_TILE": "0"})
             other = np.load(path)
         assert np.array_equal(ours, other), mode
 
