@@ -317,7 +317,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWThreads, 1)
         if (!p.a_tma) cp_async_wait<0>();
     } else if (warp == kWWWarp) {
         // ------------------------------------------------ W_cat producer (both CTAs)
-        if (lane == 0 && !(p.dbg & 16)) {
+        if (lane == 0) {
             const uint64_t pol = policy_evict_last();  // W_cat stays L2-resident
             int s = 0;
             uint32_t ph = 0;
@@ -371,12 +371,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWThreads, 1)
                     const uint32_t d_tmem = tmem_base + (uint32_t)(acc * kWBN);
 #pragma unroll 1
                     for (int kb = 0; kb < KB; ++kb) {
-                        if (!(p.dbg & 32)) mbar_wait(&afull[kb], par);  // once per m-block; later N-tiles pass
+                        mbar_wait(&afull[kb], par);  // completes once per m-block; later N-tiles pass through
                         if (!p.a_tma && n == 0) fence_proxy_async_smem();  // the producers' cp.async rows
                         const uint64_t adesc = smem_desc_sw128(smem_u32(aslot + kb * kWSlot));
 #pragma unroll
                         for (int hf = 0; hf < 64 / kWBK; ++hf) {  // the K-block's W stages
-                            if (!(p.dbg & 16)) mbar_wait(&bfull[s], ph);
+                            mbar_wait(&bfull[s], ph);
                             tc_fence_after();
                             if (lane == 0) {
                                 const uint32_t baddr = smem_u32(bstage + s * kWStage);
