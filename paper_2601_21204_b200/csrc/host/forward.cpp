@@ -411,9 +411,17 @@ int ngram_embed_sequence_host(ngram_bank* b, const uint32_t* tokens, const int64
         NGH_CUDA(cudaStreamSynchronize(s0));
         return NGRAM_OK;
     }
-    // K1 over the whole batch first: the reference raises before producing any output.
-    ngk::launch_hash_ids(b->shape, b->ht.p, b->ws.tokens.p, b->ws.offsets.p, nseq, T,
-                         (prior && N1 > 0) ? b->ws.prior.p : nullptr, nullptr, 0, b->ws.grow.p, Tpad, b->err.p, s0);
+    // The reference raises before producing any output: every token is checked first.  Tensor-
+    // core banks past the small-T regime then run the device entry's kernels chunk by chunk
+    // (the fused K1+K2 block kernel -> X -> projection); the other shapes hash the whole batch
+    // into storage rows here and gather per chunk.
+    const uint32_t* dprior = (prior && N1 > 0) ? b->ws.prior.p : nullptr;
+    const bool xpath = b->tc_path && !small_t(b, T) && !fused_gather(b->shape.D);
+    if (xpath)
+        ngk::launch_validate_tokens(b->shape, b->ws.tokens.p, T, b->ws.offsets.p, nseq, dprior, b->err.p, s0);
+    else
+        ngk::launch_hash_ids(b->shape, b->ht.p, b->ws.tokens.p, b->ws.offsets.p, nseq, T, dprior, nullptr, 0,
+                             b->ws.grow.p, Tpad, b->err.p, s0);
     unsigned long long e = 0;
     NGH_CUDA(cudaMemcpyAsync(&e, b->err.p, sizeof(e), cudaMemcpyDeviceToHost, s0));
     NGH_CUDA(cudaStreamSynchronize(s0));
@@ -473,9 +481,19 @@ int ngram_embed_sequence_host(ngram_bank* b, const uint32_t* tokens, const int64
         if (!direct) drain(slot);
         void* drows = rows_out ? b->host_out[slot].p : nullptr;
         void* dmerged = merged_out ? b->host_merged[slot].p : nullptr;
-        run_projection(b, b->ws.tokens.p + c0, b->ws.grow.p + c0, Tpad, n, drows, dmerged, out_dtype == NGRAM_BF16,
-                       b->ws.merged_f32.p ? b->ws.merged_f32.p + size_t(c0) * size_t(D) : nullptr, nullptr, st, -1,
-                       &b->host_x[slot], small_t(b, T), nullptr);  // chunks keep the batch's regime
+        float* ln = b->ws.merged_f32.p ? b->ws.merged_f32.p + size_t(c0) * size_t(D) : nullptr;
+        if (xpath) {
+            XBuf& xc = b->host_x[slot];
+            xc.ensure(round_up(chunk, kRowPad), int(D));
+            // the kernel writes X row t - c0 for position t: the slot's base shifted by c0 rows
+            ngk::launch_hash_gather(b->shape, b->ht.p, b->ws.tokens.p, b->ws.offsets.p, nseq, T, dprior, b->sub.p,
+                                    xc.x.p - c0 * D, nullptr, Tpad, b->err.p, st, c0, c0 + n);
+            run_projection(b, b->ws.tokens.p + c0, nullptr, Tpad, n, drows, dmerged, out_dtype == NGRAM_BF16, ln,
+                           &xc.map, st, -1, nullptr, false, nullptr);
+        } else {
+            run_projection(b, b->ws.tokens.p + c0, b->ws.grow.p + c0, Tpad, n, drows, dmerged, out_dtype == NGRAM_BF16,
+                           ln, nullptr, st, -1, &b->host_x[slot], small_t(b, T), nullptr);  // chunks keep the batch's regime
+        }
         const size_t bytes = size_t(n) * size_t(D) * esz;
         if (direct) {
             if (rows_out)
