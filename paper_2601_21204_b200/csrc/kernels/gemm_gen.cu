@@ -273,7 +273,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                 }
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive_cluster(acc == 0 ? tempty_leader0 : tempty_leader1);
+                // relaxed: the chunk's TMEM loads completed (tcgen05.wait::ld); a release arrive
+                // would put a GPU-scope MEMBAR behind the warp's outstanding epilogue stores
+                if (lane == 0) mbar_arrive_cluster_relaxed(acc == 0 ? tempty_leader0 : tempty_leader1);
                 if (++acc == 2) {
                     acc = 0;
                     acc_phase ^= 1;
