@@ -586,28 +586,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2::kThreads, 1)
         uint32_t phase = 0;
         const uint64_t pol_w = policy_evict_last();
         const int r0 = warp * C::kRowsPerWarp;
-        for (int64_t tile = pair; p.use_x && tile < tiles; tile += npairs) {
+        // X path: one thread issues both TMA loads per stage; producer warps 1..3 (needed by the
+        // gathering modes) leave at once instead of spinning on the same barriers
+        for (int64_t tile = pair; p.use_x && warp == 0 && lane == 0 && tile < tiles; tile += npairs) {
             const int64_t m = tile / nN;
             const int n = (int)(tile - m * nN);
             const int64_t t0 = m * BM2 + (int64_t)rank * 128;  // this CTA's first token row
             const int wrow = n * BN2 + (int)rank * (BN2 / 2);  // this CTA's first W row
-            {
-                for (int kb = 0; kb < KB; ++kb) {
-                    mbar_wait(&empty[stage], phase ^ 1);
-                    if (warp == 0 && lane == 0) {
-                        uint8_t* a_dst = smem + stage * C::kStageBytes;
-                        if (leader)
-                            mbar_arrive_expect_tx(&full[stage], p.diag_skip_a ? 2 * C::kBBytes : 2 * C::kStageBytes);
-                        if (!p.diag_skip_a)
-                            tma_load_2d_2cta(a_dst, &tmap_a, leader_bar(&full[stage]), kb * BK,
-                                             (int32_t)t0, 0);
-                        tma_load_2d_2cta(a_dst + C::kABytes, &tmap_w, leader_bar(&full[stage]), kb * BK, wrow, pol_w);
-                    }
-                    __syncwarp();
-                    if (++stage == kStages2) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
+            for (int kb = 0; kb < KB; ++kb) {
+                mbar_wait(&empty[stage], phase ^ 1);
+                uint8_t* a_dst = smem + stage * C::kStageBytes;
+                if (leader) mbar_arrive_expect_tx(&full[stage], p.diag_skip_a ? 2 * C::kBBytes : 2 * C::kStageBytes);
+                if (!p.diag_skip_a)
+                    tma_load_2d_2cta(a_dst, &tmap_a, leader_bar(&full[stage]), kb * BK, (int32_t)t0, 0);
+                tma_load_2d_2cta(a_dst + C::kABytes, &tmap_w, leader_bar(&full[stage]), kb * BK, wrow, pol_w);
+                if (++stage == kStages2) {
+                    stage = 0;
+                    phase ^= 1;
                 }
             }
         }
