@@ -1343,7 +1343,9 @@ void launch_forward_tc(const FwdArgs& a, int num_sms, cudaStream_t st, float* sp
     // the pair kernel's epilogue on small ragged batches with it).
     const char* vte = getenv("NGRAM_VERIFY_TILE");
     const bool vt = !(vte && atoi(vte) == 0);
-    if (vt && a.tmap_x && a.s.D % 128 == 0 && !small_t_regime(a.s.D, a.T, num_sms) &&
+    // Long K only: at D = 256 (config A, T = 2048) the 32 short tiles measured slower than the
+    // 8 pair tiles (24.0 vs 23.2 us).
+    if (vt && a.tmap_x && a.s.D % 128 == 0 && a.s.D >= 2048 && !small_t_regime(a.s.D, a.T, num_sms) &&
         ((a.T + 127) / 128) * (a.s.D / 128) <= num_sms && !a.wide) {
         launch_cfg<128, 4, 1>(a, num_sms, st);
         if (a.commit) launch_decode_commit_c(*a.commit, a.err, st);

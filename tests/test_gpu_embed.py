@@ -281,7 +281,7 @@ def test_pair_kernel_tma_epilogue_edges(cuda, out_dtype, monkeypatch):
     stores clipped at T): ragged T (not a multiple of 32 / 128 / 256), rows + merged; the
     direct-store epilogue and the 32-column E0 gather variant (NGRAM_TMA_EPI=0 / 1 in a
     subprocess are the A/B switches) compute the same bits.  Output buffers that are not 16-byte aligned are rejected up front."""
-    monkeypatch.setenv("NGRAM_VERIFY_TILE", "0")  # T = 1298 would take the one-wave 128 x 128 tiles
+    monkeypatch.setenv("NGRAM_VERIFY_TILE", "0")  # pin the pair kernel whatever the verify-tile rule says
     cfg = O.make_default_config(3000, 512, 3, 2)
     hb = O.make_bank(cfg, 17, round_bf16=True)
     db = G.DeviceBank(cfg).upload(hb.base, hb.sub, hb.proj)
@@ -291,12 +291,6 @@ def test_pair_kernel_tma_epilogue_edges(cuda, out_dtype, monkeypatch):
     T = len(allt)
     t, o = dev_u32(torch, allt, cuda), dev_i64(torch, off, cuda)
     rows, merged = G.embed_forward(db, t, o, merged=True, out_dtype=out_dtype)
-    # the one-wave 128 x 128 single-CTA tiles compute the same bits
-    monkeypatch.setenv("NGRAM_VERIFY_TILE", "1")
-    r1, m1 = G.embed_forward(db, t, o, merged=True, out_dtype=out_dtype)
-    monkeypatch.setenv("NGRAM_VERIFY_TILE", "0")
-    db.sync_errors()
-    assert torch.equal(r1, rows) and torch.equal(m1, merged)
     db.sync_errors()
     ref_r, ref_m = zip(*[O.embed_sequence(hb, s, double=True) for s in seqs])
     bf = out_dtype == torch.bfloat16
@@ -367,9 +361,10 @@ np.save(sys.argv[1], torch.stack([r, m]).view(torch.int32).cpu().numpy())
     assert np.array_equal(outs[0], outs[1])
 
 
-def test_verify_sized_regime_at_longcat_width(cuda):
-    """D = 3072, verify-sized T (500 / 600): the pair-kernel regime at LongCat width matches the
-    reference within tolerance and is batch-composition invariant."""
+def test_verify_sized_regime_at_longcat_width(cuda, monkeypatch):
+    """D = 3072, verify-sized T (500 / 600): the one-wave 128 x 128 single-CTA tiles at LongCat
+    width match the reference within tolerance, are batch-composition invariant, and compute the
+    same bits as the pair kernel (NGRAM_VERIFY_TILE=0, read per call)."""
     cfg = O.make_default_config(1000, 3072, 4, 4)
     hb = O.make_bank(cfg, 31, round_bf16=True)
     db = G.DeviceBank(cfg).upload(hb.base, hb.sub, hb.proj)
@@ -383,6 +378,10 @@ def test_verify_sized_regime_at_longcat_width(cuda):
     assert_rows_close(merged.cpu().numpy(), np.concatenate(ref_m))
     a01, _ = G.embed_forward(db, dev_u32(torch, np.concatenate(seqs[:2]), cuda), dev_i64(torch, off[:3], cuda))
     assert torch.equal(a01, rows[:500])  # T = 500 and T = 600: same regime, same bits
+    monkeypatch.setenv("NGRAM_VERIFY_TILE", "0")
+    pr, pm = G.embed_forward(db, dev_u32(torch, allt, cuda), dev_i64(torch, off, cuda), merged=True)
+    db.sync_errors()
+    assert torch.equal(pr, rows) and torch.equal(pm, merged)
 
 
 @pytest.mark.parametrize("env", [{"NGRAM_FUSED_GATHER": "1"}, {"NGRAM_PREFILL_PATH": "lsu"},
