@@ -383,7 +383,7 @@ def run_ours(args):
         bank = G.DeviceBank(cfg, device=local, shard_rank=rank, shard_count=world)
         bank.generate(1234)
         group = G.ShardGroup(bank, T)
-        if exchange == "peer":
+        if exchange in ("peer", "auto"):
             try:
                 G.connect_shard_groups(group)
             except Exception as e:  # noqa: BLE001 -- reported, then agreed across ranks
@@ -392,7 +392,7 @@ def run_ours(args):
         dist.all_reduce(flag, op=dist.ReduceOp.MIN)
         if int(flag.item()) == 0:  # no peer mappings: the same rows move by NCCL all-to-all instead
             fallback = (why or "a peer rank failed to map the peer buffers") + "; exchange falls back to NCCL a2a"
-            exchange = "a2a"
+            exchange = "a2a" if exchange == "peer" else exchange
             torch.cuda.synchronize()
     if sharding == "row":
         all_t = torch.empty(total_tokens, dtype=torch.int32, device=dev)
@@ -431,6 +431,32 @@ def run_ours(args):
         def step(record=False):
             G.embed_forward(bank, toks, off, rows=True, merged=False, out_dtype=out_dtype, out_rows=rows)
 
+    def time_exchange(xv, reps):
+        """whole-step ms of the row-sharded flow with exchange xv (max over ranks, L2 flushed)"""
+        for _ in range(2):
+            step(xchg=xv)
+        torch.cuda.synchronize()
+        dist.barrier()
+        tt = []
+        for i in range(reps):
+            flush.fill_(i & 0xff)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step(xchg=xv)
+            e1.record(stream)
+            e1.synchronize()
+            tt.append(e0.elapsed_time(e1))
+        t = torch.tensor([float(np.mean(tt))], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    exchange_pick = None
+    if sharding == "row" and exchange == "auto":
+        # SURVEY 8(e): pick the exchange by measured latency at this batch size (every rank
+        # agrees: the times are maxima over ranks)
+        variants = [v for v in ("peer", "a2a", "rs") if not (v == "peer" and fallback)]
+        exchange_pick = {v: time_exchange(v, 3) for v in variants}
+        exchange = min(exchange_pick, key=exchange_pick.get)
     for _ in range(args.warmup):
         step()
     bank.sync_errors()
@@ -491,22 +517,7 @@ def run_ours(args):
         for xv in ("peer", "a2a", "rs"):
             if xv == "peer" and fallback:
                 continue
-            for _ in range(2):
-                step(xchg=xv)
-            torch.cuda.synchronize()
-            dist.barrier()
-            tt = []
-            for i in range(reps):
-                flush.fill_(i & 0xff)
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                step(xchg=xv)
-                e1.record(stream)
-                e1.synchronize()
-                tt.append(e0.elapsed_time(e1))
-            t = torch.tensor([float(np.mean(tt))], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            exchange_ms[xv] = float(t.item())
+            exchange_ms[xv] = time_exchange(xv, reps)
         bank.sync_errors()
     else:
         # K1 (hash) and K2 (gather) run fused in one kernel on the X path (stage 1 ~ 0 then)
@@ -648,6 +659,8 @@ def run_ours(args):
         line["config"]["one_device_test"] = "all ranks on cuda:0 over gloo (functional only)"
     if sharding == "row":
         line["config"]["exchange"] = exchange
+        if exchange_pick is not None:
+            line["config"]["exchange_pick_ms"] = exchange_pick  # the pre-pass that chose it
         line["exchange_ms"] = exchange_ms
         remote = T * world * B * d * 2 * (world - 1) / world / world  # rows this rank ships to peers
         line["nvlink"] = {"remote_bytes_per_rank": remote, "scatter_ms": st_ms[1],
@@ -954,7 +967,8 @@ def run_decode_sharded(args):
             st.commit(toks, acc)
 
         per = {}
-        for xv in [args.exchange] + [v for v in ("peer", "rs", "a2a") if v != args.exchange]:
+        first = "peer" if args.exchange == "auto" else args.exchange
+        for xv in [first] + [v for v in ("peer", "rs", "a2a") if v != first]:
             for _ in range(args.warmup):
                 one(xv)
             torch.cuda.synchronize()
@@ -969,8 +983,9 @@ def run_decode_sharded(args):
             t = torch.tensor([ev[0].elapsed_time(ev[1]) / n], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             per[xv] = float(t.item()) * 1e3
-        us = per[args.exchange]
-        res[B] = {"us_per_step": us, "tokens_per_s": world * B * L / (us * 1e-6), "exchange": args.exchange,
+        xbest = min(per, key=per.get) if args.exchange == "auto" else args.exchange  # picked by measured latency
+        us = per[xbest]
+        res[B] = {"us_per_step": us, "tokens_per_s": world * B * L / (us * 1e-6), "exchange": xbest,
                   "exchange_us": per}
         st.close()
     bank.sync_errors()
@@ -1219,10 +1234,11 @@ def main():
                     help="backward workload: modes to time (sparsebase: E0 gradient as (token, u) pairs too)")
     ap.add_argument("--sharding", choices=["row", "replica"], default="row",
                     help="N > 1: row-sharded tables (default) or full replicas")
-    ap.add_argument("--exchange", choices=["peer", "a2a", "rs"], default="peer",
-                    help="row-sharded exchange: NVLink peer stores (default), NCCL all-to-all of the owned rows, "
-                         "or NCCL reduce-scatter of the -0.0-padded X (all bit-identical); the other two are "
-                         "timed too and reported under exchange_ms")
+    ap.add_argument("--exchange", choices=["auto", "peer", "a2a", "rs"], default="auto",
+                    help="row-sharded exchange: auto (default: the fastest of the three, measured before the "
+                         "timed steps), NVLink peer stores, NCCL all-to-all of the owned rows, or NCCL "
+                         "reduce-scatter of the -0.0-padded X (all bit-identical); every variant is timed and "
+                         "reported under exchange_ms")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -87,6 +87,10 @@ def test_bench_two_ranks_one_device(cuda, sharding):
     if sharding == "row":
         assert set(line["stages_ms"]) == {"all_gather_tokens", "k1_k2_scatter_nvlink", "barrier",
                                           "k3_projection_epilogue"}
+        # --exchange auto (default): the variant with the lowest pre-measured step time is timed
+        pick = line["config"]["exchange_pick_ms"]
+        assert line["config"]["exchange"] == min(pick, key=pick.get)
+        assert set(line["exchange_ms"]) == set(pick)
 
 
 def test_bench_gpus_flag_launches_the_ranks_itself(cuda):
