@@ -847,9 +847,11 @@ def run_decode(args):
         launches_total = per_step_launches * args.steps
         # e2e through the host-buffer C-ABI entry (host tokens in, host fp32 merged out)
         T = B * L
-        h_tok = np.ascontiguousarray(toks.cpu().numpy().astype(np.uint32))
-        h_acc = np.ascontiguousarray(acc.cpu().numpy().astype(np.int32))
-        h_out = np.zeros((B, L, D), np.float32)
+        # pinned host buffers (the e2e contract: inputs from and results to pinned host memory)
+        h_tok_t = torch.from_numpy(toks.cpu().numpy().astype(np.int32)).pin_memory()
+        h_acc_t = torch.from_numpy(acc.cpu().numpy().astype(np.int32)).pin_memory()
+        h_out_t = torch.zeros((B, L, D), dtype=torch.float32).pin_memory()
+        h_tok, h_acc, h_out = h_tok_t.numpy(), h_acc_t.numpy(), h_out_t.numpy()
         if args.workload == "D":
             def e2e_call():
                 abi.check(abi.lib().ngram_decode_step_host(st.handle, h_tok.ctypes.data, None, h_out.ctypes.data))

@@ -191,7 +191,15 @@ struct ngram_decode {
     ngh::DevBuf<float> io_out;              // [batch][max_draft][D]
     ngh::PinBuf io_pin;                     // error words | ids | out, then tokens | accept
     cudaStream_t io_stream = nullptr;
+    // ngram_decode_step_host in steady state (merged out, no ids, released error word): the
+    // whole H2D -> 3 kernels -> D2H sequence captured once and replayed (one launch per step);
+    // keyed by the staging block it was captured on
+    cudaGraphExec_t step_exec = nullptr;
+    const void* step_key[6] = {};  // staging in / out, device token / output buffers, X, split-K workspace
+    uint64_t step_launches = 0;
+    int64_t host_steps = 0;        // eager host steps so far (the first sizes every workspace)
     ~ngram_decode() {
+        if (step_exec) cudaGraphExecDestroy(step_exec);
         if (io_stream) cudaStreamDestroy(io_stream);
     }
 };

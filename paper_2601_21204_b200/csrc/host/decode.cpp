@@ -250,6 +250,16 @@ void finish_host_io(const HostIo& io) {
     }
 }
 
+// Page-locked host memory: the device-to-host copy can land in the caller's buffer directly.
+bool host_pinned(const void* p) {
+    cudaPointerAttributes pa{};
+    if (!p || cudaPointerGetAttributes(&pa, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return pa.type == cudaMemoryTypeHost;
+}
+
 void read_words(const HostIo& io) {
     ngram_bank* b = io.d->bank;
     NGH_CUDA(cudaMemcpyAsync(&io.words[0], b->err.p, 8, cudaMemcpyDeviceToHost, io.d->io_stream));
@@ -287,16 +297,60 @@ int ngram_decode_step_host(ngram_decode* d, const uint32_t* tokens, uint64_t* id
     const HostIo io = host_io(d, ids_bytes, out_bytes, tok_bytes);
     cudaStream_t st = d->io_stream;
     std::memcpy(io.in, tokens, tok_bytes);
-    NGH_CUDA(cudaMemcpyAsync(d->io_tok.p, io.in, tok_bytes, cudaMemcpyHostToDevice, st));
-    int rc = ngram_decode_step(d, d->io_tok.p, ids_out ? d->io_ids.p : nullptr, merged_out ? d->io_out.p : nullptr,
-                               NGRAM_F32, st);
-    if (rc) return rc;
-    read_words(io);
-    if (ids_bytes) NGH_CUDA(cudaMemcpyAsync(io.ids, d->io_ids.p, ids_bytes, cudaMemcpyDeviceToHost, st));
-    if (out_bytes) NGH_CUDA(cudaMemcpyAsync(io.out, d->io_out.p, out_bytes, cudaMemcpyDeviceToHost, st));
+    // a pinned output buffer receives the copy directly (no staging memcpy of batch x D floats)
+    unsigned char* out_dst = (out_bytes && host_pinned(merged_out)) ? reinterpret_cast<unsigned char*>(merged_out)
+                                                                       : io.out;
+    auto enqueue = [&]() {
+        NGH_CUDA(cudaMemcpyAsync(d->io_tok.p, io.in, tok_bytes, cudaMemcpyHostToDevice, st));
+        int rc = ngram_decode_step(d, d->io_tok.p, ids_out ? d->io_ids.p : nullptr,
+                                   merged_out ? d->io_out.p : nullptr, NGRAM_F32, st);
+        if (rc) return rc;
+        read_words(io);
+        if (ids_bytes) NGH_CUDA(cudaMemcpyAsync(io.ids, d->io_ids.p, ids_bytes, cudaMemcpyDeviceToHost, st));
+        if (out_bytes) NGH_CUDA(cudaMemcpyAsync(out_dst, d->io_out.p, out_bytes, cudaMemcpyDeviceToHost, st));
+        return 0;
+    };
+    // Steady state (merged out, no ids, the error word released by the previous step): replay
+    // the captured sequence -- the same copies and kernels, one graph launch instead of ~8 API
+    // calls.  Any other call, or a staging block moved by a larger request, runs eagerly.
+    // The graph holds raw pointers: it is re-captured whenever a buffer it uses was reallocated
+    // (a workspace grown by another call), and only after one eager step has sized them all.
+    const bool graphable = merged_out && !ids_out && b->tc_path && d->batch <= 256 && b->err_clean &&
+                           d->host_steps > 0 &&
+                           !(getenv("NGRAM_HOST_STEP_GRAPH") && atoi(getenv("NGRAM_HOST_STEP_GRAPH")) == 0);
+    const void* key[6] = {io.in, out_dst, d->io_tok.p, d->io_out.p, d->xbuf.x.p, b->ws.splitk.p};
+    if (graphable && d->step_exec && !std::equal(key, key + 6, d->step_key)) {
+        cudaGraphExecDestroy(d->step_exec);
+        d->step_exec = nullptr;
+    }
+    if (graphable && !d->step_exec) {
+        const uint64_t l0 = ngk::launches();
+        cudaGraph_t graph = nullptr;
+        NGH_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        const int rc = enqueue();
+        const cudaError_t ce = cudaStreamEndCapture(st, &graph);
+        if (rc) {
+            if (graph) cudaGraphDestroy(graph);
+            return rc;
+        }
+        NGH_CUDA(ce);
+        const cudaError_t ie = cudaGraphInstantiate(&d->step_exec, graph, 0);
+        cudaGraphDestroy(graph);
+        NGH_CUDA(ie);
+        std::copy(key, key + 6, d->step_key);
+        d->step_launches = ngk::launches() - l0;
+    }
+    if (graphable) {
+        NGH_CUDA(cudaGraphLaunch(d->step_exec, st));
+        ngk::count_launch(int(d->step_launches));
+    } else {
+        const int rc = enqueue();
+        if (rc) return rc;
+        ++d->host_steps;
+    }
     finish_host_io(io);
     if (ids_bytes) std::memcpy(ids_out, io.ids, ids_bytes);
-    if (out_bytes) std::memcpy(merged_out, io.out, out_bytes);
+    if (out_bytes && out_dst == io.out) std::memcpy(merged_out, io.out, out_bytes);
     NGRAM_API_END
 }
 
@@ -330,9 +384,11 @@ int ngram_verify_commit_host(ngram_decode* d, const uint32_t* draft, int L, cons
     rc = ngram_commit(d, d->io_tok.p, L, d->io_acc.p, st);
     if (rc) return rc;
     read_words(io);
-    if (out_bytes) NGH_CUDA(cudaMemcpyAsync(io.out, d->io_out.p, out_bytes, cudaMemcpyDeviceToHost, st));
+    unsigned char* out_dst = (out_bytes && host_pinned(merged_out)) ? reinterpret_cast<unsigned char*>(merged_out)
+                                                                       : io.out;
+    if (out_bytes) NGH_CUDA(cudaMemcpyAsync(out_dst, d->io_out.p, out_bytes, cudaMemcpyDeviceToHost, st));
     finish_host_io(io);
-    if (out_bytes) std::memcpy(merged_out, io.out, out_bytes);
+    if (out_bytes && out_dst == io.out) std::memcpy(merged_out, io.out, out_bytes);
     NGRAM_API_END
 }
 

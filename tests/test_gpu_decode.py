@@ -327,3 +327,61 @@ def test_bad_token_verify_then_commit_is_refused_and_reported(bank, cuda):
     st.commit(good, acc)
     db.sync_errors()
     assert (st.state()[1] == 2 * L).all()
+
+
+def test_host_decode_step_graph_replay_equals_device_steps(cuda, monkeypatch):
+    """ngram_decode_step_host in steady state replays a captured H2D -> kernels -> D2H graph:
+    over several steps it returns the device entry's bits (a twin state stepped on the device),
+    a bad token raises and leaves the state untouched, a verify block in between (which grows the
+    X workspace, forcing a re-capture) keeps both in step, and the eager form
+    (NGRAM_HOST_STEP_GRAPH=0) agrees."""
+    import ctypes as C
+    from paper_2601_21204_b200 import abi
+    cfg = O.make_default_config(1000, 768, 4, 2)
+    hb = O.make_bank(cfg, 13, round_bf16=True)
+    db = G.DeviceBank(cfg).upload(hb.base, hb.sub, hb.proj)
+    B = 6
+    host, dev = G.DecodeState(db, B, max_draft=3), G.DecodeState(db, B, max_draft=3)
+    rng = np.random.default_rng(3)
+    out = np.zeros((B, 768), np.float32)
+
+    def host_step(tok):
+        t = np.ascontiguousarray(tok, np.uint32)
+        abi.check(abi.lib().ngram_decode_step_host(host.handle, t.ctypes.data, None, out.ctypes.data))
+        return out.copy()
+
+    for i in range(8):
+        if i == 5:  # a verify block + commit on both: grows the workspace, the graph is re-captured
+            draft = dev_u32(torch, rng.integers(0, 1000, size=(B, 3)), cuda)
+            acc = torch.tensor(rng.integers(0, 4, size=B).astype(np.int32), device=cuda)
+            for s in (host, dev):
+                s.verify(draft)
+                s.commit(draft, acc)
+            db.sync_errors()
+        if i == 3:  # a bad token: raises, nothing changes
+            bad = rng.integers(0, 1000, size=B).astype(np.uint32)
+            bad[2] = 1000
+            with pytest.raises(OutOfRange):
+                host_step(bad)
+        tok = rng.integers(0, 1000, size=B).astype(np.uint32)
+        got = host_step(tok)
+        _, want = dev.step(dev_u32(torch, tok, cuda), want_ids=False)
+        db.sync_errors()
+        assert np.array_equal(got, want.cpu().numpy()), i
+    # a page-locked output buffer receives the device-to-host copy directly (graph re-captured)
+    pinned = torch.zeros((B, 768), dtype=torch.float32).pin_memory().numpy()
+    for _ in range(2):
+        tok = np.ascontiguousarray(rng.integers(0, 1000, size=B).astype(np.uint32))
+        abi.check(abi.lib().ngram_decode_step_host(host.handle, tok.ctypes.data, None, pinned.ctypes.data))
+        _, want = dev.step(dev_u32(torch, tok, cuda), want_ids=False)
+        db.sync_errors()
+        assert np.array_equal(pinned, want.cpu().numpy())
+    monkeypatch.setenv("NGRAM_HOST_STEP_GRAPH", "0")
+    tok = rng.integers(0, 1000, size=B).astype(np.uint32)
+    got = host_step(tok)
+    _, want = dev.step(dev_u32(torch, tok, cuda), want_ids=False)
+    db.sync_errors()
+    assert np.array_equal(got, want.cpu().numpy())
+    host.close()
+    dev.close()
+    db.close()
