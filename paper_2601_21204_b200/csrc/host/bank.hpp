@@ -195,7 +195,8 @@ struct ngram_decode {
     // whole H2D -> 3 kernels -> D2H sequence captured once and replayed (one launch per step);
     // keyed by the staging block it was captured on
     cudaGraphExec_t step_exec = nullptr;
-    const void* step_key[6] = {};  // staging in / out, device token / output buffers, X, split-K workspace
+    // staging in / out / ids, device token / output / ids buffers, X, split-K workspace, variant
+    const void* step_key[9] = {};
     uint64_t step_launches = 0;
     int64_t host_steps = 0;        // eager host steps so far (the first sizes every workspace)
     ~ngram_decode() {

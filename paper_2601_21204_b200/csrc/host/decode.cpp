@@ -310,16 +310,17 @@ int ngram_decode_step_host(ngram_decode* d, const uint32_t* tokens, uint64_t* id
         if (out_bytes) NGH_CUDA(cudaMemcpyAsync(out_dst, d->io_out.p, out_bytes, cudaMemcpyDeviceToHost, st));
         return 0;
     };
-    // Steady state (merged out, no ids, the error word released by the previous step): replay
-    // the captured sequence -- the same copies and kernels, one graph launch instead of ~8 API
-    // calls.  Any other call, or a staging block moved by a larger request, runs eagerly.
+    // Steady state (the error word clean after the previous step): replay the captured sequence
+    // -- the same copies and kernels, one graph launch instead of ~8 API calls.  The first call,
+    // a different output variant or a moved buffer re-captures; a larger batch runs eagerly.
     // The graph holds raw pointers: it is re-captured whenever a buffer it uses was reallocated
     // (a workspace grown by another call), and only after one eager step has sized them all.
-    const bool graphable = merged_out && !ids_out && b->tc_path && d->batch <= 256 && b->err_clean &&
-                           d->host_steps > 0 &&
+    const bool graphable = (merged_out || ids_out) && d->batch <= 256 && b->err_clean && d->host_steps > 0 &&
                            !(getenv("NGRAM_HOST_STEP_GRAPH") && atoi(getenv("NGRAM_HOST_STEP_GRAPH")) == 0);
-    const void* key[6] = {io.in, out_dst, d->io_tok.p, d->io_out.p, d->xbuf.x.p, b->ws.splitk.p};
-    if (graphable && d->step_exec && !std::equal(key, key + 6, d->step_key)) {
+    const void* key[9] = {io.in, out_dst, io.ids, d->io_tok.p, d->io_out.p, d->io_ids.p, d->xbuf.x.p,
+                          b->ws.splitk.p,
+                          reinterpret_cast<const void*>(uintptr_t((ids_out ? 1 : 0) | (merged_out ? 2 : 0)))};
+    if (graphable && d->step_exec && !std::equal(key, key + 9, d->step_key)) {
         cudaGraphExecDestroy(d->step_exec);
         d->step_exec = nullptr;
     }
@@ -337,7 +338,7 @@ int ngram_decode_step_host(ngram_decode* d, const uint32_t* tokens, uint64_t* id
         const cudaError_t ie = cudaGraphInstantiate(&d->step_exec, graph, 0);
         cudaGraphDestroy(graph);
         NGH_CUDA(ie);
-        std::copy(key, key + 6, d->step_key);
+        std::copy(key, key + 9, d->step_key);
         d->step_launches = ngk::launches() - l0;
     }
     if (graphable) {

@@ -376,6 +376,15 @@ def test_host_decode_step_graph_replay_equals_device_steps(cuda, monkeypatch):
         _, want = dev.step(dev_u32(torch, tok, cuda), want_ids=False)
         db.sync_errors()
         assert np.array_equal(pinned, want.cpu().numpy())
+    # the ids-only variant (the drop-in's sequence_cache::append) is captured too: ids equal the
+    # device entry's
+    ids_h = np.zeros((B, db.B), np.uint64)
+    for _ in range(3):
+        tok = np.ascontiguousarray(rng.integers(0, 1000, size=B).astype(np.uint32))
+        abi.check(abi.lib().ngram_decode_step_host(host.handle, tok.ctypes.data, ids_h.ctypes.data, None))
+        ids_d, _ = dev.step(dev_u32(torch, tok, cuda), want_ids=True, want_merged=False)
+        db.sync_errors()
+        assert np.array_equal(ids_h, ids_d.cpu().numpy().view(np.uint64).reshape(B, -1))
     monkeypatch.setenv("NGRAM_HOST_STEP_GRAPH", "0")
     tok = rng.integers(0, 1000, size=B).astype(np.uint32)
     got = host_step(tok)
