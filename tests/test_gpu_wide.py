@@ -23,6 +23,8 @@ CASES = {
     "d768_sqrt": (3000, 768, 4, 4, "scale_sqrt_d", [1001, 2900, 7, 513], 3),
     "d512_d128_none": (2000, 512, 3, 2, "none", [600, 1700], 5),
     "d256_ln": (1500, 256, 3, 2, "layer_norm", [300, 1029], 7),
+    "d768_n5_k3": (2500, 768, 5, 3, "scale_sqrt_d", [700, 333], 9),   # order-5 windows, 12 branches
+    "d512_n2_k8": (1200, 512, 2, 8, "none", [900, 41], 11),           # bigrams only, 8 sub-tables
 }
 
 
@@ -64,7 +66,8 @@ def test_wide_kernel_matches_oracle(cuda, path, case):
 
 
 @pytest.mark.parametrize("case,dtype", [("d768_sqrt", torch.float32), ("d768_sqrt", torch.bfloat16),
-                                        ("d512_d128_none", torch.float32), ("d256_ln", torch.float32)])
+                                        ("d512_d128_none", torch.float32), ("d256_ln", torch.float32),
+                                        ("d768_n5_k3", torch.float32), ("d512_n2_k8", torch.bfloat16)])
 def test_wide_kernel_bit_identical_to_x_path(cuda, path, case, dtype):
     _, db, _, prior, (t, o) = _case(case, cuda)
     pr = dev_u32(torch, prior, cuda)
