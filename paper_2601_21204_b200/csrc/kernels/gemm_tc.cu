@@ -1347,7 +1347,8 @@ void launch_forward_tc(const FwdArgs& a, int num_sms, cudaStream_t st, float* sp
     // 8 pair tiles (24.0 vs 23.2 us).
     if (vt && a.tmap_x && a.s.D % 128 == 0 && a.s.D >= 2048 && !small_t_regime(a.s.D, a.T, num_sms) &&
         ((a.T + 127) / 128) * (a.s.D / 128) <= num_sms && !a.wide) {
-        launch_cfg<128, 4, 1>(a, num_sms, st);
+        // programmatic dependent launch: set-up overlaps the gather kernel's tail (it waits for X)
+        launch_cfg<128, 4, 1>(a, num_sms, st, 1, nullptr, pdl_enabled());
         if (a.commit) launch_decode_commit_c(*a.commit, a.err, st);
         return;
     }
