@@ -10,14 +10,18 @@
 //   * reset: seed every ring from a prior context (prefill hand-off) or zeros.
 #include <cstdint>
 
+#include <cstdlib>
+
 #include "decodedev.cuh"
 #include "kernels.h"
+#include "ptx.cuh"
 
 namespace ngk {
 
 namespace {
 
 __global__ void __launch_bounds__(1024) commit_kernel(DecodeCommit c, const unsigned long long* err) {
+    griddep_wait();  // PDL launch: the preceding kernel (projection / gather) has completed
     decode_commit_block(c, err);
     if (c.err_reported) {
         __syncthreads();  // every thread's reads of the error word are done
@@ -35,6 +39,28 @@ __global__ void reset_kernel(int R, uint32_t* __restrict__ ring, uint64_t* __res
     last[s] = (prior && R > 0) ? prior[s * R + R - 1] : 0u;
 }
 
+// Commit kernels launch with programmatic stream serialization: the launch overlaps the tail
+// of the projection before them, griddepcontrol.wait then waits for its completion (so the
+// ring is updated only after every kernel that reads it).  NGRAM_PDL=0 launches plainly.
+void launch_commit(const DecodeCommit& c, const unsigned long long* err, cudaStream_t st) {
+    static const bool pdl = !(getenv("NGRAM_PDL") && atoi(getenv("NGRAM_PDL")) == 0);
+    const int threads = c.batch >= 1024 ? 1024 : (int)((c.batch + 31) / 32 * 32);
+    if (!pdl) {
+        commit_kernel<<<1, threads, 0, st>>>(c, err);
+        return;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3((unsigned)threads);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, commit_kernel, c, err);
+}
+
 }  // namespace
 
 void launch_decode_commit(const Shape& s, uint32_t* ring, uint64_t* length, uint32_t* last, const uint32_t* draft,
@@ -42,15 +68,13 @@ void launch_decode_commit(const Shape& s, uint32_t* ring, uint64_t* length, uint
                           unsigned long long* derr, cudaStream_t st, unsigned long long* err_reported) {
     if (batch <= 0) return;
     DecodeCommit c{s.N > 1 ? s.N - 1 : 0, ring, length, last, draft, L, accept, batch, derr, err_reported, nullptr};
-    const int threads = batch >= 1024 ? 1024 : (int)((batch + 31) / 32 * 32);
-    commit_kernel<<<1, threads, 0, st>>>(c, err);
+    launch_commit(c, err, st);
     count_launch();
 }
 
 void launch_decode_commit_c(const DecodeCommit& c, const unsigned long long* err, cudaStream_t st) {
     if (c.batch <= 0) return;
-    const int threads = c.batch >= 1024 ? 1024 : (int)((c.batch + 31) / 32 * 32);
-    commit_kernel<<<1, threads, 0, st>>>(c, err);
+    launch_commit(c, err, st);
     count_launch();
 }
 
