@@ -485,9 +485,9 @@ int ngram_embed_sequence_host(ngram_bank* b, const uint32_t* tokens, const int64
         if (xpath) {
             XBuf& xc = b->host_x[slot];
             xc.ensure(round_up(chunk, kRowPad), int(D));
-            // the kernel writes X row t - c0 for position t: the slot's base shifted by c0 rows
+            // positions [c0, c0 + n) into rows [0, n) of the chunk's X
             ngk::launch_hash_gather(b->shape, b->ht.p, b->ws.tokens.p, b->ws.offsets.p, nseq, T, dprior, b->sub.p,
-                                    xc.x.p - c0 * D, nullptr, Tpad, b->err.p, st, c0, c0 + n);
+                                    xc.x.p, nullptr, Tpad, b->err.p, st, c0, c0 + n, c0);
             run_projection(b, b->ws.tokens.p + c0, nullptr, Tpad, n, drows, dmerged, out_dtype == NGRAM_BF16, ln,
                            &xc.map, st, -1, nullptr, false, nullptr);
         } else {

@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(256) hash_gather_kernel(Shape s, const HashTab
                                                           const __nv_bfloat16* __restrict__ sub,
                                                           __nv_bfloat16* __restrict__ X, int32_t* __restrict__ grow,
                                                           int64_t Tpad, unsigned long long* err, int64_t t_begin,
-                                                          int64_t t_end) {
+                                                          int64_t t_end, int64_t x_row0) {
     const int lane = threadIdx.x & 31;
     const int64_t t = t_begin + (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     if (t >= t_end) return;
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(256) hash_gather_kernel(Shape s, const HashTab
         if (lane == 0) atomicMin(err, (unsigned long long)t);
         return;
     }
-    gather_position<MAXN, 4>(s, ht, w, sub, X + t * (int64_t)s.D, grow, Tpad, t, lane);
+    gather_position<MAXN, 4>(s, ht, w, sub, X + (t - x_row0) * (int64_t)s.D, grow, Tpad, t, lane);
 }
 
 // K1+K2, block-decoupled form (default when D == B*d, B <= 32 and d/8 is a power of two):
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(256) hash_gather_block_kernel(Shape s, const H
                                                                 __nv_bfloat16* __restrict__ X,
                                                                 int32_t* __restrict__ grow, int64_t Tpad,
                                                                 unsigned long long* err, int64_t t_begin,
-                                                                int64_t t_end) {
+                                                                int64_t t_end, int64_t x_row0) {
     __shared__ int32_t srow[kGatherP * 32];
     const int B = s.B;
     constexpr int VPR = 1 << LOG_VPR;  // 16-byte vectors per sub-table row
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(256) hash_gather_block_kernel(Shape s, const H
         }
         __syncthreads();
         const int n = np * B * VPR;
-        uint4* dst = X4 + t0 * vpos;
+        uint4* dst = X4 + (t0 - x_row0) * vpos;  // X row 0 holds position x_row0
         for (int v0 = threadIdx.x; v0 < n; v0 += blockDim.x * U) {
             uint4 val[U];
 #pragma unroll
@@ -299,7 +299,7 @@ void launch_validate_tokens(const Shape& s, const uint32_t* tokens, int64_t T, c
 void launch_hash_gather(const Shape& s, const HashTables* ht, const uint32_t* tokens, const int64_t* seq_off,
                         int64_t nseq, int64_t T, const uint32_t* prior, const __nv_bfloat16* sub, __nv_bfloat16* X,
                         int32_t* grow, int64_t Tpad, unsigned long long* err, cudaStream_t st, int64_t t_begin,
-                        int64_t t_end) {
+                        int64_t t_end, int64_t x_row0) {
     if (t_end < 0) t_end = T;
     if (t_end <= t_begin) return;
     static const bool warp_form = getenv("NGRAM_GATHER_WARP") != nullptr;  // A/B switch
@@ -313,7 +313,7 @@ void launch_hash_gather(const Shape& s, const HashTables* ht, const uint32_t* to
         const int64_t blocks = (t_end - t_begin + P - 1) / P;
         auto go = [&](auto kern) {
             kern<<<(unsigned)blocks, 256, 0, st>>>(s, ht, tokens, seq_off, nseq, T, prior, sub, X, grow, Tpad, err,
-                                                    t_begin, t_end);
+                                                    t_begin, t_end, x_row0);
         };
         const int lv = __builtin_ctz((unsigned)vpr);
         if (s.N <= 4) {
@@ -343,13 +343,13 @@ void launch_hash_gather(const Shape& s, const HashTables* ht, const uint32_t* to
     const unsigned blocks = (unsigned)((t_end - t_begin + 7) / 8);  // 8 warps (positions) per block
     if (s.N <= 4)
         hash_gather_kernel<4><<<blocks, 256, 0, st>>>(s, ht, tokens, seq_off, nseq, T, prior, sub, X, grow, Tpad, err,
-                                                      t_begin, t_end);
+                                                      t_begin, t_end, x_row0);
     else if (s.N <= 8)
         hash_gather_kernel<8><<<blocks, 256, 0, st>>>(s, ht, tokens, seq_off, nseq, T, prior, sub, X, grow, Tpad, err,
-                                                      t_begin, t_end);
+                                                      t_begin, t_end, x_row0);
     else
         hash_gather_kernel<16><<<blocks, 256, 0, st>>>(s, ht, tokens, seq_off, nseq, T, prior, sub, X, grow, Tpad,
-                                                       err, t_begin, t_end);
+                                                       err, t_begin, t_end, x_row0);
     count_launch();
 }
 

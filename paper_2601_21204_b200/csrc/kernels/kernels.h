@@ -43,7 +43,7 @@ void launch_hash_ids(const Shape& s, const HashTables* ht, const uint32_t* token
 void launch_hash_gather(const Shape& s, const HashTables* ht, const uint32_t* tokens, const int64_t* seq_off,
                         int64_t nseq, int64_t T, const uint32_t* prior, const __nv_bfloat16* sub, __nv_bfloat16* X,
                         int32_t* grow, int64_t Tpad, unsigned long long* err, cudaStream_t st, int64_t t_begin = 0,
-                        int64_t t_end = -1);
+                        int64_t t_end = -1, int64_t x_row0 = 0);  // X row 0 holds position x_row0
 // Same, one warp per (position, branch): the small-T (decode / verify) latency variant.
 void launch_hash_gather_rows(const Shape& s, const HashTables* ht, const uint32_t* tokens, const int64_t* seq_off,
                              int64_t nseq, int64_t T, const uint32_t* prior, const __nv_bfloat16* sub,
