@@ -39,7 +39,13 @@ __device__ __forceinline__ int64_t find_seq(const int64_t* __restrict__ off, int
     return lo;
 }
 
-// Bucket of branch b for the window w (oldest first, N tokens).
+// Bucket of branch b for the window w (oldest first, N tokens):
+//   h = sum_{j < n} (w[N-1-j] mod V_b) * (V0^j mod V_b)  mod V_b        (hashing.cpp:33-59)
+// The loop runs over the window slot k = N-1-j (a compile-time register index; indexing w by
+// the runtime N-1-j would put the window in local memory).  The terms are summed in another
+// order than the reference's, which leaves the residue unchanged.  Common case (every token
+// < V0 <= V_b <= 2^30): w mod V_b = w and each term < V_b^2 <= 2^60, so n <= 16 terms sum
+// below 2^64 and ONE Barrett reduction of the plain sum gives the same residue.
 template <int MAXN>
 __device__ __forceinline__ uint64_t branch_hash(const Shape& s, const HashTables* __restrict__ ht,
                                                 const uint32_t (&w)[MAXN], int b) {
@@ -47,21 +53,26 @@ __device__ __forceinline__ uint64_t branch_hash(const Shape& s, const HashTables
     const int n = 2 + b / s.K;
     const uint64_t m = __ldg(&ht->modulus[b]);
     if (m <= 1) return 0;
+    uint64_t acc = 0;
     if (s.fast_hash) {
         const uint64_t mu = __ldg(&ht->barrett[b]);
-        uint64_t acc = 0;
+        if (m <= (1ull << 30) && (uint64_t)s.V0 <= m) {
 #pragma unroll
-        for (int j = 0; j < MAXN; ++j)
-            if (j < n) {
-                const uint64_t tm = barrett_mod((uint64_t)w[N - 1 - j], m, mu);
-                acc += barrett_mod(tm * __ldg(&ht->pow[b][j]), m, mu);
+            for (int k = 0; k < MAXN; ++k)
+                if (k < N && k >= N - n) acc += (uint64_t)w[k] * (uint32_t)__ldg(&ht->pow[b][N - 1 - k]);
+            return barrett_mod(acc, m, mu);
+        }
+#pragma unroll
+        for (int k = 0; k < MAXN; ++k)
+            if (k < N && k >= N - n) {
+                const uint64_t tm = barrett_mod((uint64_t)w[k], m, mu);
+                acc += barrett_mod(tm * __ldg(&ht->pow[b][N - 1 - k]), m, mu);
             }
         return barrett_mod(acc, m, mu);  // acc < n * 2^32
     }
-    uint64_t acc = 0;
 #pragma unroll
-    for (int j = 0; j < MAXN; ++j)
-        if (j < n) acc = (acc + mulmod128((uint64_t)w[N - 1 - j] % m, __ldg(&ht->pow[b][j]), m)) % m;
+    for (int k = 0; k < MAXN; ++k)
+        if (k < N && k >= N - n) acc = (acc + mulmod128((uint64_t)w[k] % m, __ldg(&ht->pow[b][N - 1 - k]), m)) % m;
     return acc;
 }
 
