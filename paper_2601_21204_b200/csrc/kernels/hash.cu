@@ -36,9 +36,25 @@ __global__ void __launch_bounds__(256) hash_ids_kernel(Shape s, const HashTables
                                                         const uint32_t* __restrict__ prior, void* __restrict__ ids_tok,
                                                         int ids_u64, int32_t* __restrict__ grow, int64_t Tpad,
                                                         unsigned long long* err) {
+    const int N = s.N, K = s.K, B = s.B;
+    // the block's copy of the hash constants it uses (moduli, Barrett factors, V0^j, row
+    // ranges of B branches): one cooperative load instead of a global-latency chain per hash
+    __shared__ uint64_t sm_m[kMaxBranches], sm_mu[kMaxBranches], sm_pow[kMaxBranches][MAXN];
+    __shared__ int64_t sm_lo[kMaxBranches], sm_hi[kMaxBranches], sm_base[kMaxBranches];
+    for (int i = threadIdx.x; i < B * MAXN; i += blockDim.x) {
+        const int bb = i / MAXN, j = i % MAXN;
+        sm_pow[bb][j] = j < kMaxOrder ? __ldg(&ht->pow[bb][j]) : 0ull;
+        if (j == 0) {
+            sm_m[bb] = __ldg(&ht->modulus[bb]);
+            sm_mu[bb] = __ldg(&ht->barrett[bb]);
+            sm_lo[bb] = __ldg(&ht->row_lo[bb]);
+            sm_hi[bb] = __ldg(&ht->row_hi[bb]);
+            sm_base[bb] = __ldg(&ht->row_base[bb]);
+        }
+    }
+    __syncthreads();
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= Tpad) return;
-    const int N = s.N, K = s.K, B = s.B;
     if (t >= T) {  // padding rows of the GEMM's last m-tile: a valid (row 0) address, never stored
         if (grow)
             for (int b = 0; b < B; ++b) grow[(int64_t)b * Tpad + t] = 0;
@@ -66,30 +82,30 @@ __global__ void __launch_bounds__(256) hash_ids_kernel(Shape s, const HashTables
         return;
     }
     for (int b = 0; b < B; ++b) {
+        // hashing.cpp:33-59 term for term (see branch_hash, hashdev.cuh): window slot k holds
+        // the token of power N-1-k; one Barrett reduction when V0 <= V_b <= 2^30
         const int n = 2 + b / K;
-        const uint64_t m = __ldg(&ht->modulus[b]);
+        const uint64_t m = sm_m[b];
         uint64_t h = 0;
         if (m > 1) {
+            uint64_t acc = 0;
             if (s.fast_hash) {
-                const uint64_t mu = __ldg(&ht->barrett[b]);
-                uint64_t acc = 0;
+                const uint64_t mu = sm_mu[b];
+                if (m <= (1ull << 30) && (uint64_t)s.V0 <= m) {
 #pragma unroll
-                for (int j = 0; j < MAXN; ++j) {
-                    if (j < n) {
-                        const uint64_t tm = barrett_mod((uint64_t)w[N - 1 - j], m, mu);
-                        acc += barrett_mod(tm * __ldg(&ht->pow[b][j]), m, mu);
-                    }
+                    for (int k = 0; k < MAXN; ++k)
+                        if (k < N && k >= N - n) acc += (uint64_t)w[k] * (uint32_t)sm_pow[b][N - 1 - k];
+                } else {
+#pragma unroll
+                    for (int k = 0; k < MAXN; ++k)
+                        if (k < N && k >= N - n)
+                            acc += barrett_mod(barrett_mod((uint64_t)w[k], m, mu) * sm_pow[b][N - 1 - k], m, mu);
                 }
-                h = barrett_mod(acc, m, mu);  // acc < n * 2^32
+                h = barrett_mod(acc, m, mu);
             } else {
-                uint64_t acc = 0;
 #pragma unroll
-                for (int j = 0; j < MAXN; ++j) {
-                    if (j < n) {
-                        const uint64_t tm = (uint64_t)w[N - 1 - j] % m;
-                        acc = (acc + mulmod128(tm, __ldg(&ht->pow[b][j]), m)) % m;
-                    }
-                }
+                for (int k = 0; k < MAXN; ++k)
+                    if (k < N && k >= N - n) acc = (acc + mulmod128((uint64_t)w[k] % m, sm_pow[b][N - 1 - k], m)) % m;
                 h = acc;
             }
         }
@@ -98,9 +114,9 @@ __global__ void __launch_bounds__(256) hash_ids_kernel(Shape s, const HashTables
             else static_cast<uint32_t*>(ids_tok)[t * B + b] = (uint32_t)h;
         }
         if (grow) {
-            const int64_t lo = __ldg(&ht->row_lo[b]), hi = __ldg(&ht->row_hi[b]);
+            const int64_t lo = sm_lo[b], hi = sm_hi[b];
             const int64_t hh = (int64_t)h;
-            grow[(int64_t)b * Tpad + t] = (hh >= lo && hh < hi) ? (int32_t)(__ldg(&ht->row_base[b]) + (hh - lo)) : -1;
+            grow[(int64_t)b * Tpad + t] = (hh >= lo && hh < hi) ? (int32_t)(sm_base[b] + (hh - lo)) : -1;
         }
     }
 }
