@@ -37,22 +37,8 @@ __global__ void __launch_bounds__(256) hash_ids_kernel(Shape s, const HashTables
                                                         int ids_u64, int32_t* __restrict__ grow, int64_t Tpad,
                                                         unsigned long long* err) {
     const int N = s.N, K = s.K, B = s.B;
-    // the block's copy of the hash constants it uses (moduli, Barrett factors, V0^j, row
-    // ranges of B branches): one cooperative load instead of a global-latency chain per hash
-    __shared__ uint64_t sm_m[kMaxBranches], sm_mu[kMaxBranches], sm_pow[kMaxBranches][MAXN];
-    __shared__ int64_t sm_lo[kMaxBranches], sm_hi[kMaxBranches], sm_base[kMaxBranches];
-    for (int i = threadIdx.x; i < B * MAXN; i += blockDim.x) {
-        const int bb = i / MAXN, j = i % MAXN;
-        sm_pow[bb][j] = j < kMaxOrder ? __ldg(&ht->pow[bb][j]) : 0ull;
-        if (j == 0) {
-            sm_m[bb] = __ldg(&ht->modulus[bb]);
-            sm_mu[bb] = __ldg(&ht->barrett[bb]);
-            sm_lo[bb] = __ldg(&ht->row_lo[bb]);
-            sm_hi[bb] = __ldg(&ht->row_hi[bb]);
-            sm_base[bb] = __ldg(&ht->row_base[bb]);
-        }
-    }
-    __syncthreads();
+    __shared__ HashSmem<MAXN> hs;  // the block's hash constants (hashdev.cuh)
+    hs.load(ht, B);
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= Tpad) return;
     if (t >= T) {  // padding rows of the GEMM's last m-tile: a valid (row 0) address, never stored
@@ -82,42 +68,12 @@ __global__ void __launch_bounds__(256) hash_ids_kernel(Shape s, const HashTables
         return;
     }
     for (int b = 0; b < B; ++b) {
-        // hashing.cpp:33-59 term for term (see branch_hash, hashdev.cuh): window slot k holds
-        // the token of power N-1-k; one Barrett reduction when V0 <= V_b <= 2^30
-        const int n = 2 + b / K;
-        const uint64_t m = sm_m[b];
-        uint64_t h = 0;
-        if (m > 1) {
-            uint64_t acc = 0;
-            if (s.fast_hash) {
-                const uint64_t mu = sm_mu[b];
-                if (m <= (1ull << 30) && (uint64_t)s.V0 <= m) {
-#pragma unroll
-                    for (int k = 0; k < MAXN; ++k)
-                        if (k < N && k >= N - n) acc += (uint64_t)w[k] * (uint32_t)sm_pow[b][N - 1 - k];
-                } else {
-#pragma unroll
-                    for (int k = 0; k < MAXN; ++k)
-                        if (k < N && k >= N - n)
-                            acc += barrett_mod(barrett_mod((uint64_t)w[k], m, mu) * sm_pow[b][N - 1 - k], m, mu);
-                }
-                h = barrett_mod(acc, m, mu);
-            } else {
-#pragma unroll
-                for (int k = 0; k < MAXN; ++k)
-                    if (k < N && k >= N - n) acc = (acc + mulmod128((uint64_t)w[k] % m, sm_pow[b][N - 1 - k], m)) % m;
-                h = acc;
-            }
-        }
+        const uint64_t h = hs.hash(s, w, b);  // hashing.cpp:33-59 (branch_hash, hashdev.cuh)
         if (ids_tok) {
             if (ids_u64) static_cast<uint64_t*>(ids_tok)[t * B + b] = h;
             else static_cast<uint32_t*>(ids_tok)[t * B + b] = (uint32_t)h;
         }
-        if (grow) {
-            const int64_t lo = sm_lo[b], hi = sm_hi[b];
-            const int64_t hh = (int64_t)h;
-            grow[(int64_t)b * Tpad + t] = (hh >= lo && hh < hi) ? (int32_t)(sm_base[b] + (hh - lo)) : -1;
-        }
+        if (grow) grow[(int64_t)b * Tpad + t] = hs.row(b, h);
     }
 }
 
@@ -218,7 +174,9 @@ __global__ void __launch_bounds__(256) hash_gather_block_kernel(Shape s, const H
                                                                 unsigned long long* err, int64_t t_begin,
                                                                 int64_t t_end, int64_t x_row0) {
     __shared__ int32_t srow[kGatherP * 32];
+    __shared__ HashSmem<MAXN> hs;  // the block's hash constants (hashdev.cuh)
     const int B = s.B;
+    hs.load(ht, B);
     constexpr int VPR = 1 << LOG_VPR;  // 16-byte vectors per sub-table row
     const uint4* sub4 = reinterpret_cast<const uint4*>(sub);
     uint4* X4 = reinterpret_cast<uint4*>(X);
@@ -231,7 +189,8 @@ __global__ void __launch_bounds__(256) hash_gather_block_kernel(Shape s, const H
             uint32_t w[MAXN];
             int32_t row = -1;
             if (load_window<MAXN>(s, tokens, seq_off, nseq, prior, t, w)) {
-                row = storage_row(ht, b, branch_hash<MAXN>(s, ht, w, b), nullptr);
+                row = hs.row(b, hs.hash(s, w, b));
+                if (row < 0) row = 0;  // not on this shard: storage_row's fallback row
                 if (grow) grow[(int64_t)b * Tpad + t] = row;
             } else if (b == 0) {
                 atomicMin(err, (unsigned long long)t);
