@@ -231,17 +231,24 @@ __global__ void __launch_bounds__(256) hash_gather_rows_kernel(Shape s, const Ha
                                                                __nv_bfloat16* __restrict__ X,
                                                                unsigned long long* err, int64_t uniform_len) {
     griddep_launch_dependents();  // the decode GEMM may start its set-up (it waits for us)
+    __shared__ HashSmem<MAXN> hs;  // the block's hash constants (hashdev.cuh)
     const int lane = threadIdx.x & 31;
     const int64_t w = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-    if (w >= T * s.B) return;
-    const int64_t t = w / s.B;
-    const int b = (int)(w - t * s.B);
+    const bool active = w < T * s.B;
+    const int64_t t = active ? w / s.B : 0;
+    const int b = active ? (int)(w - t * s.B) : 0;
     uint32_t win[MAXN];
-    if (!load_window<MAXN>(s, tokens, seq_off, nseq, prior, t, win, uniform_len)) {
+    // the window loads are issued before the constants' cooperative load, so the two global
+    // round trips overlap instead of running back to back
+    const bool ok = active && load_window<MAXN>(s, tokens, seq_off, nseq, prior, t, win, uniform_len);
+    hs.load(ht, s.B);
+    if (!active) return;
+    if (!ok) {
         if (lane == 0 && b == 0) atomicMin(err, (unsigned long long)t);
         return;
     }
-    const int32_t row = storage_row(ht, b, branch_hash<MAXN>(s, ht, win, b), nullptr);
+    int32_t row = hs.row(b, hs.hash(s, win, b));
+    if (row < 0) row = 0;  // not on this shard: storage_row's fallback row
     const uint4* src = reinterpret_cast<const uint4*>(sub + (int64_t)row * s.d);
     uint4* dst = reinterpret_cast<uint4*>(X + t * (int64_t)s.D + (int64_t)b * s.d);
     for (int c = lane; c < s.d / 8; c += 32) dst[c] = __ldg(src + c);
