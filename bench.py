@@ -374,6 +374,7 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
 
     fallback = None
+    prefill_path = "x"  # row-sharded flow: scatter into X, then the pair projection
     if sharding == "row":
         # row-sharded tables: this rank keeps 1/world of every sub-table; rows travel over
         # NVLink by the fused gather + peer-store kernel; one NCCL all-reduce = barrier.
@@ -427,6 +428,9 @@ def run_ours(args):
         bank.generate(1234)
         bank.reserve(T)
         sbuf = (C.c_float * 3)()  # stage times: a separate profiled pass after the timed region
+        pp = C.c_int(0)
+        abi.check(abi.lib().ngram_prefill_path(bank.handle, T, C.byref(pp)))
+        prefill_path = {0: "x", 1: "lsu", 2: "wide"}[pp.value]
 
         def step(record=False):
             G.embed_forward(bank, toks, off, rows=True, merged=False, out_dtype=out_dtype, out_rows=rows)
@@ -520,8 +524,10 @@ def run_ours(args):
             exchange_ms[xv] = time_exchange(xv, reps)
         bank.sync_errors()
     else:
-        # K1 (hash) and K2 (gather) run fused in one kernel on the X path (stage 1 ~ 0 then)
-        stages = {"k1_k2_hash_gather": st_ms[0] + st_ms[1], "k3_projection_epilogue": st_ms[2]}
+        if prefill_path == "wide":  # token check, then the one fused kernel (no X)
+            stages = {"validate_tokens": st_ms[0] + st_ms[1], "fused_wide_kernel": st_ms[2]}
+        else:  # K1 (hash) and K2 (gather) run fused in one kernel on the X path (stage 1 ~ 0 then)
+            stages = {"k1_k2_hash_gather": st_ms[0] + st_ms[1], "k3_projection_epilogue": st_ms[2]}
         proj_ms = st_ms[2]
 
     # ---------------------------------------------------------------- index stage alone
@@ -614,7 +620,7 @@ def run_ours(args):
             traffic = None
     hbm = {"achieved_gbs": hbm_gbs, "peak_gbs": peaks["hbm_gbs"], "frac": hbm_gbs / peaks["hbm_gbs"],
            "algorithmic_bytes_per_token": bytes_tok}
-    if sharding != "row":
+    if sharding != "row" and prefill_path != "wide":
         kb = T * (4 + 2 * B * d + 2 * D)  # tokens in, B sub-table rows in, X out
         k12 = st_ms[0] + st_ms[1]
         hbm["k1_k2_hash_gather"] = {"ms": k12, "bytes": kb, "gbs": kb / (k12 * 1e-3) / 1e9,
@@ -629,6 +635,9 @@ def run_ours(args):
     # token: the token, the X row it reads in place of the sub-table rows, the E0 row and the
     # output -- the same 4 + 2 B d + 2 D + esz D bytes as the layer's algorithmic figure)
     k3_name = "forward_tc2_kernel (K3: tcgen05 cta_group::2 projection + base/scale/amplify epilogue)"
+    if prefill_path == "wide":  # the fused kernel moves the layer's own bytes (no X)
+        k3_name = ("forward_wide_kernel (hash + row gather into resident shared-memory K-blocks + tcgen05 "
+                   "cta_group::2 projection over every N-tile + base/scale/amplify epilogue; no X)")
     k3_bytes = T * bytes_tok + 2 * D * D
     if flops / (peaks["bf16_tflops"] * 1e12) >= k3_bytes / (peaks["hbm_gbs"] * 1e9):
         roofline = {"bound": "tensor", "kernel": k3_name, "achieved": tflops, "peak": peaks["bf16_tflops"],
@@ -653,6 +662,7 @@ def run_ours(args):
         "roofline": roofline,
         "hbm": hbm, "stages_ms": stages, "clocks": clocks, "e2e": e2e, "gpu_launches": int(launches),
     }
+    line["config"]["prefill_path"] = prefill_path
     if fallback:
         line["config"]["sharding_fallback"] = fallback
     if one_dev and world > 1:

@@ -139,6 +139,10 @@ int ngram_hash_ids(ngram_bank* bank, const uint32_t* tokens, const int64_t* seq_
 int ngram_embed_forward(ngram_bank* bank, const uint32_t* tokens, const int64_t* seq_offsets, int64_t nseq,
                         int64_t total_tokens, const uint32_t* prior, void* rows_out, void* merged_out,
                         int out_dtype, void* stream);
+/* Which prefill kernel sequence ngram_embed_forward runs for a batch of total_tokens (for
+ * benchmarks and logs): 0 fused K1+K2 -> X -> tcgen05 projection (or the small-T / CUDA-core
+ * paths), 1 K1+K2 in the projection's producers, 2 the fused wide-tile kernel (D <= 768). */
+int ngram_prefill_path(ngram_bank* bank, int64_t total_tokens, int* path);
 /* embed_from_ids (embedding.hpp:163-201) for T tokens: ids dev u64 T x branch_count
  * (global bucket ids), merged_out dev T x D (pre-amplification, as the reference). */
 int ngram_embed_from_ids(ngram_bank* bank, const uint32_t* tokens, const uint64_t* ids, int64_t T, void* merged_out,

@@ -32,7 +32,8 @@ SYMBOLS = [
     "ngram_last_error", "ngram_version", "ngram_kernel_launches", "ngram_config_validate",
     "ngram_make_default_config", "ngram_bank_create", "ngram_bank_create_ex", "ngram_bank_destroy", "ngram_bank_upload_f32",
     "ngram_bank_generate", "ngram_bank_load_file", "ngram_bank_reserve", "ngram_bank_get_info",
-    "ngram_rolling_hash_batch", "ngram_hash_ids", "ngram_embed_forward", "ngram_embed_from_ids", "ngram_sync_errors",
+    "ngram_rolling_hash_batch", "ngram_hash_ids", "ngram_embed_forward", "ngram_prefill_path", "ngram_embed_from_ids",
+    "ngram_sync_errors",
     "ngram_embed_sequence_host", "ngram_hash_ids_host", "ngram_rolling_hash_host", "ngram_embed_from_ids_host",
     "ngram_profile_enable", "ngram_profile_read", "ngram_decode_create", "ngram_decode_destroy", "ngram_decode_reset",
     "ngram_decode_step", "ngram_verify_block", "ngram_commit", "ngram_decode_reset_host", "ngram_decode_step_host",
@@ -132,6 +133,7 @@ def lib() -> C.CDLL:
         "ngram_rolling_hash_batch": ([vp, i64, vp, vp, vp, vp, i64, vp, vp, vp], i32),
         "ngram_hash_ids": ([vp, vp, vp, i64, i64, vp, vp, i32, vp], i32),
         "ngram_embed_forward": ([vp, vp, vp, i64, i64, vp, vp, vp, i32, vp], i32),
+        "ngram_prefill_path": ([vp, i64, vp], i32),
         "ngram_embed_from_ids": ([vp, vp, vp, i64, vp, i32, vp], i32),
         "ngram_sync_errors": ([vp, vp], i32),
         "ngram_embed_sequence_host": ([vp, vp, vp, i64, vp, vp, vp, i32], i32),

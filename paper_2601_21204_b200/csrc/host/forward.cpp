@@ -44,30 +44,31 @@ static bool fused_gather(int D) {
 }
 
 // Prefill path (tensor-core banks, D % 256 == 0, T beyond the split-K regime):
-//   "x"    (default) fused K1+K2 kernel writes X, K3 (pair kernel) reads it: two launches,
-//          X round trip
-//   "wide" (D <= 768, d % 64 == 0; gemm_wide.cu) token validation, then ONE kernel: the
+//   "x"    fused K1+K2 kernel writes X, K3 (pair kernel) reads it: two launches, X round trip
+//   "wide" (gemm_wide.cu; D <= 768, d % 64 == 0) token validation, then ONE kernel: the
 //          producers hash + gather an m-block's rows into shared memory once, the MMA warp
-//          sweeps every N-tile over them -- no X.  Bit-identical to "x"; measured equal at
-//          config B (141-146 vs 145-147 us, profiles/README.md): the X traffic it saves is
-//          paid back in pipeline depth (the resident A operand leaves two W stages and no
-//          epilogue staging)
+//          sweeps every N-tile over them -- no X.  Bit-identical to "x".  DEFAULT for its
+//          shapes once the batch fills a wave of CTA pairs (T >= 256 x num_sms / 2): config B
+//          129-131 vs 140-142 us; at T = 2048 (config A) the X path stays (23.1-24.2 vs
+//          24.1-24.8 us) -- profiles/README.md
 //   "lsu"  token validation, then K3 alone with K1+K2 in its producers (hash + cp.async rows
 //          into shared memory; the peer CTA's stages relayed to the leader): no X, no
 //          storage-row array.  Bit-identical, but measured slower (profiles/README.md):
 //          config B 205 vs 150 us, C 1.30 vs 1.02 ms -- every n-tile pair re-gathers its
 //          m-block's rows as 128-byte L2 requests (12x at D = 3072) where the X path moves the
 //          same bytes as 16 KB TMA tiles; tensor pipe 33 % active vs 66 % (ncu).
-// NGRAM_PREFILL_PATH=x|wide|lsu selects; read per call, so one process can A/B the paths.
+// NGRAM_PREFILL_PATH=x|wide|lsu forces one; read per call, so one process can A/B the paths.
 // Returns 0 (x), 1 (lsu) or 2 (wide).
-static int prefill_path(const ngram_bank* b) {
+static int prefill_path(const ngram_bank* b, int64_t T) {
     const char* e = getenv("NGRAM_PREFILL_PATH");
     const std::string v(e ? e : "");
-    const int env = v == "lsu" ? 1 : v == "wide" ? 2 : 0;
+    const int env = v == "lsu" ? 1 : v == "wide" ? 2 : v == "x" ? 0 : -1;
     const auto& s = b->shape;
     if (!b->tc_path || s.D % 256 != 0 || s.N > 8 || s.variant != 1 || s.B < 1) return 0;
-    if (env == 2 && !ngk::wide_prefill_shape(s)) return 0;
-    return env;
+    const bool wide_ok = ngk::wide_prefill_shape(s);
+    if (env == 2) return wide_ok ? 2 : 0;
+    if (env >= 0) return env;
+    return (wide_ok && T >= 256 * int64_t(b->num_sms / 2)) ? 2 : 0;
 }
 
 // Entry points that gather rows themselves need every row on this device: a row-sharded bank
@@ -202,12 +203,12 @@ bool forward_tokens(ngram_bank* b, const uint32_t* tokens, const int64_t* seq_of
         const HashCtx hc{seq_off, nseq, prior};
         run_projection(b, tokens, nullptr, Tpad, T, rows, merged, out_bf16, b->ws.merged_f32.p, nullptr, st, amp,
                        nullptr, true, fused_commit ? commit : nullptr, &hc);
-    } else if (!(allow_splitk && small_t(b, T)) && prefill_path(b) != 0 && !fused_gather(b->shape.D)) {
+    } else if (!(allow_splitk && small_t(b, T)) && prefill_path(b, T) != 0 && !fused_gather(b->shape.D)) {
         // K1+K2 fused into the projection's producers; a bad token must still abort the call
         // before any output, so the range check runs first (the kernel returns on the error word)
         ngk::launch_validate_tokens(b->shape, tokens, T, seq_off, nseq, prior, b->err.p, st);
         b->prof_record(1, st);
-        const HashCtx hc{seq_off, nseq, prior, prefill_path(b) == 2};
+        const HashCtx hc{seq_off, nseq, prior, prefill_path(b, T) == 2};
         fused_commit = commit != nullptr;
         run_projection(b, tokens, nullptr, Tpad, T, rows, merged, out_bf16, b->ws.merged_f32.p, nullptr, st, amp,
                        nullptr, allow_splitk, fused_commit ? commit : nullptr, &hc);
@@ -277,6 +278,13 @@ int ngram_amplify_host(int amp_mode, int D, int64_t rows, const float* gain, con
         ngk::launch_scale(din.p, dout.p, int64_t(n), amp_mode == 1 ? float(std::sqrt(double(D))) : 1.0f, nullptr);
     }
     NGH_CUDA(cudaMemcpy(out, dout.p, n * 4, cudaMemcpyDeviceToHost));
+    NGRAM_API_END
+}
+
+int ngram_prefill_path(ngram_bank* b, int64_t total_tokens, int* path) {
+    NGRAM_API_BEGIN
+    if (!b || !path || total_tokens < 0) throw Error(NGRAM_EINVAL, "ngram_prefill_path: bad argument");
+    *path = (b->tc_path && !small_t(b, total_tokens)) ? prefill_path(b, total_tokens) : 0;
     NGRAM_API_END
 }
 

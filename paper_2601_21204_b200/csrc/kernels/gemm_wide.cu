@@ -56,7 +56,13 @@ constexpr int kWEpiWarps = 8;
 constexpr int kWMmaWarp = 13;
 constexpr int kWThreads = 14 * 32;
 constexpr int kWSmemMax = 232448;     // sm_100 dynamic shared memory per block
-constexpr int kWSmemExtra = 1024 /*align*/ + 512 /*barriers*/;
+// the kernel's hash constants (B <= 12 branches, windows <= 8): moduli, Barrett factors, V0^j,
+// shard row ranges, copied to shared memory once (the K1 kernels gained 10-40 % from it)
+struct WideHash {
+    uint64_t m[kWMaxB], mu[kWMaxB], pw[kWMaxB][kWMaxN];
+    int64_t lo[kWMaxB], hi[kWMaxB], base[kWMaxB];
+};
+constexpr int kWSmemExtra = 1024 /*align*/ + 512 /*barriers*/ + (int)sizeof(WideHash);
 
 __host__ __device__ constexpr int wide_stages(int KB) {
     return (kWSmemMax - kWSmemExtra - KB * kWSlot) / kWStage > 8 ? 8
@@ -176,6 +182,26 @@ __device__ __forceinline__ uint64_t hash_rev(const Shape& s, const HashTables* _
 }
 
 // OUT: 1 = amplified rows in fp32 only (the prefill call), 0 = any combination (runtime)
+// hash_rev from the shared constants (the general forms fall back to the global tables)
+__device__ __forceinline__ uint64_t hash_rev_s(const Shape& s, const HashTables* __restrict__ ht, const WideHash& h,
+                                               const uint32_t (&wr)[kWMaxN], int b) {
+    const int n = 2 + b / s.K;
+    const uint64_t m = h.m[b];
+    if (m <= 1) return 0;
+    if (s.fast_hash && m <= (1ull << 30) && (uint64_t)s.V0 <= m) {
+        uint64_t acc = 0;
+#pragma unroll
+        for (int j = 0; j < kWMaxN; ++j)
+            if (j < n) acc += (uint64_t)wr[j] * (uint32_t)h.pw[b][j];
+        return barrett_mod(acc, m, h.mu[b]);
+    }
+    return hash_rev(s, ht, wr, b);
+}
+__device__ __forceinline__ int32_t wide_row(const WideHash& h, int b, uint64_t v) {
+    const int64_t hh = (int64_t)v;
+    return (hh >= h.lo[b] && hh < h.hi[b]) ? (int32_t)(h.base[b] + (hh - h.lo[b])) : 0;
+}
+
 template <int KB, int OUT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWThreads, 1)
     forward_wide_kernel(const __grid_constant__ CUtensorMap tmap_sub, const __grid_constant__ CUtensorMap tmap_w,
@@ -194,6 +220,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWThreads, 1)
     uint64_t* tempty = tfull + kWAcc;
     uint64_t* lfull = tempty + kWAcc;  // cp.async producers of the peer CTA: its own slot arrivals (relayed)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lfull + KB);
+    WideHash* wh = reinterpret_cast<WideHash*>(smem + KB * kWSlot + SB * kWStage + 512);
 
     if (*p.err != ~0ull) return;  // a token was out of range (validation kernel): no output
 
@@ -226,6 +253,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWThreads, 1)
         tma_prefetch_desc(&tmap_sub);
         tma_prefetch_desc(&tmap_w);
     }
+    if (warp < kWProd)  // the producers' hash constants (read only by this CTA's producer warps)
+        for (int i = threadIdx.x; i < p.s.B * kWMaxN; i += kWProd * 32) {
+            const int b = i / kWMaxN, j = i % kWMaxN;
+            wh->pw[b][j] = __ldg(&p.ht->pow[b][j]);
+            if (j == 0) {
+                wh->m[b] = __ldg(&p.ht->modulus[b]);
+                wh->mu[b] = __ldg(&p.ht->barrett[b]);
+                wh->lo[b] = __ldg(&p.ht->row_lo[b]);
+                wh->hi[b] = __ldg(&p.ht->row_hi[b]);
+                wh->base[b] = __ldg(&p.ht->row_base[b]);
+            }
+        }
     if (warp == kWMmaWarp) tmem_alloc_2cta<512>(tmem_slot);
     tc_fence_before();
     cluster_sync();
@@ -255,7 +294,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWThreads, 1)
             const bool ok = !(p.dbg & 1) && t < p.T && window_rev(p.s, p.tokens, p.seq_off, p.nseq, p.prior, t, w);
 #pragma unroll 1
             for (int b = 0; b < p.s.B; ++b) {  // (four chains per trip measured no faster)
-                const int32_t v = ok ? storage_row(p.ht, b, hash_rev(p.s, p.ht, w, b), nullptr)
+                const int32_t v = ok ? wide_row(*wh, b, hash_rev_s(p.s, p.ht, *wh, w, b))
                                      : (p.dbg & 1) ? (int32_t)((t * 7919 + b * 104729) % 1000000) : 0;
 #pragma unroll
                 for (int k = 0; k < kWMaxB; ++k) rr[k] = b == k ? v : rr[k];
