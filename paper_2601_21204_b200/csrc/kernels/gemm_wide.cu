@@ -89,6 +89,7 @@ struct WideParams {
     int dbg;    // diagnostics only (NGRAM_DEBUG_WIDE bits): 1 no hashing (synthetic rows), 2 no epilogue memory
                 // traffic, 4 no A copies (cp.async mode), 8 no W loads
     int a_tma;  // A producer: 0 = cp.async (default), 1 = TMA tile::gather4 (NGRAM_WIDE_GATHER4=1)
+    int pdl;    // launched as a programmatic dependent of the token check: only the epilogue waits
 };
 
 // 16 TMEM lanes x 32 columns: thread i gets lane (base + i/4) in r[4j], r[4j+1] and lane
@@ -222,7 +223,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWThreads, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lfull + KB);
     WideHash* wh = reinterpret_cast<WideHash*>(smem + KB * kWSlot + SB * kWStage + 512);
 
-    if (*p.err != ~0ull) return;  // a token was out of range (validation kernel): no output
+    // a token was out of range (the validation kernel before this one): no output.  Launched as
+    // its programmatic dependent, the kernel starts while the check still runs -- hashing,
+    // gathers and MMAs only read -- and the epilogue waits for the verdict before any store.
+    if (!p.pdl && *p.err != ~0ull) return;
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
@@ -446,6 +450,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWThreads, 1)
         }
     } else {
         // ------------------------------------------------ epilogue (both CTAs)
+        bool no_out = false;
+        if (p.pdl) {
+            griddep_wait();  // the token check has completed
+            no_out = *p.err != ~0ull;
+        }
         // Warp (quadrant q, half h) drains rows 32 q .. 32 q + 31 x columns h kWBN/2 .. + kWBN/2
         // of each tile in kWSteps steps: row half hh (16 TMEM lanes) x 32-column chunk ch.  E0
         // words come through a 4-slot register ring loaded 4 steps ahead (across tiles); the
@@ -528,7 +537,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWThreads, 1)
 #pragma unroll
                 for (int i2 = 0; i2 < 2; ++i2) {
                     const int64_t tr = r0 + 16 * hh + 8 * i2;
-                    if (tr >= p.T || (p.dbg & 2)) continue;
+                    if (tr >= p.T || no_out || (p.dbg & 2)) continue;
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
                         const uint32_t ew2 = E[s & 3][4 * i2 + j];
@@ -588,7 +597,22 @@ void launch_wide_out(const FwdArgs& a, const WideParams& p, int num_sms, cudaStr
     int64_t pairs = std::min<int64_t>(num_sms / 2, nM);
     if (pairs < 1) pairs = 1;
     cudaFuncSetAttribute(forward_wide_kernel<KB, OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, wide_smem(KB));
-    forward_wide_kernel<KB, OUT><<<(unsigned)(2 * pairs), kWThreads, wide_smem(KB), st>>>(*a.tmap_sub, kWBK == 64 ? *a.tmap_w2 : *a.tmap_w32, p);
+    const CUtensorMap& mw = kWBK == 64 ? *a.tmap_w2 : *a.tmap_w32;
+    if (!p.pdl) {
+        forward_wide_kernel<KB, OUT><<<(unsigned)(2 * pairs), kWThreads, wide_smem(KB), st>>>(*a.tmap_sub, mw, p);
+        return;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(2 * pairs));
+    cfg.blockDim = dim3(kWThreads);
+    cfg.dynamicSmemBytes = wide_smem(KB);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, forward_wide_kernel<KB, OUT>, *a.tmap_sub, mw, p);
 }
 template <int KB>
 void launch_wide(const FwdArgs& a, const WideParams& p, int num_sms, cudaStream_t st) {
@@ -628,6 +652,8 @@ void launch_forward_wide(const FwdArgs& a, int num_sms, cudaStream_t st) {
     p.a_tma = a_tma;
     static const int dbg = getenv("NGRAM_DEBUG_WIDE") ? atoi(getenv("NGRAM_DEBUG_WIDE")) : 0;
     p.dbg = dbg;
+    static const bool pdl = !(getenv("NGRAM_PDL") && atoi(getenv("NGRAM_PDL")) == 0);
+    p.pdl = pdl ? 1 : 0;  // the caller launched the token check right before (forward.cpp)
     switch (a.s.D / 64) {
         case 4: launch_wide<4>(a, p, num_sms, st); break;
         case 8: launch_wide<8>(a, p, num_sms, st); break;

@@ -257,6 +257,7 @@ __global__ void __launch_bounds__(256) hash_gather_rows_kernel(Shape s, const Ha
 __global__ void validate_tokens_kernel(uint32_t V0, const uint32_t* __restrict__ tokens, int64_t T,
                                        const int64_t* __restrict__ seq_off, int64_t nseq, const uint32_t* prior,
                                        int R, unsigned long long* err) {
+    griddep_launch_dependents();  // the fused prefill kernel may start (it waits before any output)
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < T) {
         if (__ldg(tokens + i) >= V0) atomicMin(err, (unsigned long long)i);
