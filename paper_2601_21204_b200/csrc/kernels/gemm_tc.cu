@@ -1176,9 +1176,15 @@ __global__ void __launch_bounds__(kReduceThreads) splitk_reduce_kernel(const flo
                                                             const __nv_bfloat16* __restrict__ e0, uint32_t V0,
                                                             float scale, float amp, int write_rows, void* rows,
                                                             void* merged, int out_bf16,
-                                                            const unsigned long long* err, DecodeCommit commit) {
+                                                            const unsigned long long* err, DecodeCommit commit,
+                                                            int commit_sep) {
     const int64_t n4 = T * D / 4;
-    const int64_t v0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // commit_sep: the decode-state commit runs in a block of its own (block 0, dispatched
+    // first), beside the reduction blocks instead of ahead of block 0's share of the reduction
+    const bool commit_here = commit.ring && blockIdx.x == 0;
+    const unsigned sep = commit.ring && commit_sep ? 1u : 0u;
+    const unsigned nred = gridDim.x - sep;
+    const int64_t v0 = (sep && blockIdx.x == 0) ? n4 : (int64_t)(blockIdx.x - sep) * blockDim.x + threadIdx.x;
     uint2 eb0 = make_uint2(0, 0);
     if (v0 < n4) {  // first element's E0 chunk, ahead of the GEMM's completion
         const int64_t t = v0 * 4 / D;
@@ -1186,9 +1192,9 @@ __global__ void __launch_bounds__(kReduceThreads) splitk_reduce_kernel(const flo
         eb0 = __ldg(reinterpret_cast<const uint2*>(e0 + (int64_t)(tok < V0 ? tok : 0u) * D + (v0 * 4 - t * D)));
     }
     griddep_wait();  // PDL launch: the split-K GEMM has completed (no-op for a normal launch)
-    if (commit.ring && blockIdx.x == 0) decode_commit_block(commit, err);  // fused decode-state commit
+    if (commit_here) decode_commit_block(commit, err);  // fused decode-state commit
     const bool bad = *err != ~0ull;  // a token was out of range: no output (uniform)
-    for (int64_t v = v0; !bad && v < n4; v += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t v = v0; !bad && v < n4; v += (int64_t)nred * blockDim.x) {
         const int64_t t = v * 4 / D;
         const int i = (int)(v * 4 - t * D);
         float4 acc;
@@ -1312,6 +1318,8 @@ void launch_forward_tc(const FwdArgs& a, int num_sms, cudaStream_t st, float* sp
             if (a.commit) c = *a.commit;
             int64_t blocks = (n4 + kReduceThreads - 1) / kReduceThreads;
             if (blocks > num_sms * 16) blocks = num_sms * 16;
+            static const int commit_sep = !(getenv("NGRAM_COMMIT_BLOCK") && atoi(getenv("NGRAM_COMMIT_BLOCK")) == 0);
+            if (c.ring && commit_sep) ++blocks;
             const int wr = (a.rows_out != nullptr && a.s.amp != kAmpLN) ? 1 : 0;
             if (pdl) {
                 cudaLaunchConfig_t cfg{};
@@ -1324,11 +1332,11 @@ void launch_forward_tc(const FwdArgs& a, int num_sms, cudaStream_t st, float* sp
                 cfg.attrs = attr;
                 cfg.numAttrs = 1;
                 cudaLaunchKernelEx(&cfg, splitk_reduce_kernel, (const float*)splitk_ws, S, a.T, a.s.D, a.tokens, a.e0,
-                                   a.s.V0, scale, amp, wr, a.rows_out, a.merged_out, a.out_bf16, a.err, c);
+                                   a.s.V0, scale, amp, wr, a.rows_out, a.merged_out, a.out_bf16, a.err, c, commit_sep);
             } else {
                 splitk_reduce_kernel<<<(unsigned)blocks, kReduceThreads, 0, st>>>(
                     splitk_ws, S, a.T, a.s.D, a.tokens, a.e0, a.s.V0, scale, amp, wr, a.rows_out, a.merged_out,
-                    a.out_bf16, a.err, c);
+                    a.out_bf16, a.err, c, commit_sep);
             }
             count_launch();
             return;
