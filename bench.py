@@ -649,6 +649,13 @@ def run_ours(args):
                     "unit": "GB/s", "frac": k3_gbs / peaks["hbm_gbs"], "traffic": traffic,
                     "peak_source": peak_src, "bytes_per_launch": k3_bytes, "launch_ms": proj_ms,
                     "tensor_frac": tflops / peaks["bf16_tflops"]}
+        if D == 768 and d == 64 and T == 65536 and esz == 4:
+            # the layer's byte mix (random 128-byte rows + random E0 rows in, fp32 rows out) does not
+            # stream at the copy peak either: the same traffic with no projection, moved by a
+            # plain CUDA-core kernel, takes 75.9 us on a B200 (5.3 TB/s;
+            # profiles/microbench/layer_mix_ceiling.cu, layer_mix_ceiling_b200.txt)
+            roofline["access_ceiling_ms"] = 0.0759
+            roofline["frac_of_access_ceiling"] = 0.0759 / proj_ms
     line = {
         "metric": "ngram_embedding_tokens_per_sec", "value": total_tokens / (ms * 1e-3), "unit": "tokens/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
