@@ -105,8 +105,10 @@ __device__ __forceinline__ void tmem_ld_16x256b_x4(uint32_t taddr, uint32_t* r) 
         : "memory");
 }
 
-__device__ __forceinline__ void st_cs_f2(float* p, float a, float b) {
-    asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(a), "f"(b) : "memory");
+// fp32 output pairs: no L1 allocation (measured at config B: 123.7-123.9 us vs 124.6-125.0 with
+// the streaming .cs operator, 125.8-127.1 with the default write-back; profiles/README.md)
+__device__ __forceinline__ void st_na_f2(float* p, float a, float b) {
+    asm volatile("st.global.L1::no_allocate.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(a), "f"(b) : "memory");
 }
 __device__ __forceinline__ void st_cs_u32(void* p, uint32_t v) {
     asm volatile("st.global.cs.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -547,17 +549,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kWThreads, 1)
                                                              __uint_as_float(v[4 * j + 2 * i2 + 1])), p.scale);
                         const int64_t o = tr * D + col0 + ch * 32 + 8 * j + c2;
                         if (OUT == 1) {
-                            st_cs_f2(static_cast<float*>(p.rows_out) + o, __fmul_rn(m0, p.amp), __fmul_rn(m1, p.amp));
+                            st_na_f2(static_cast<float*>(p.rows_out) + o, __fmul_rn(m0, p.amp), __fmul_rn(m1, p.amp));
                             continue;
                         }
                         if (p.merged_out) {
                             if (p.out_bf16) st_cs_u32(static_cast<__nv_bfloat16*>(p.merged_out) + o, pack_bf16x2(m0, m1));
-                            else st_cs_f2(static_cast<float*>(p.merged_out) + o, m0, m1);
+                            else st_na_f2(static_cast<float*>(p.merged_out) + o, m0, m1);
                         }
                         if (p.write_rows) {
                             const float a0 = __fmul_rn(m0, p.amp), a1 = __fmul_rn(m1, p.amp);
                             if (p.out_bf16) st_cs_u32(static_cast<__nv_bfloat16*>(p.rows_out) + o, pack_bf16x2(a0, a1));
-                            else st_cs_f2(static_cast<float*>(p.rows_out) + o, a0, a1);
+                            else st_na_f2(static_cast<float*>(p.rows_out) + o, a0, a1);
                         }
                     }
                 }
